@@ -1,0 +1,171 @@
+/* include/hfmm_cuda.h — C ABI of the B200-native FMM Helmholtz matvec (libhfmm_b200.so).
+ *
+ * This is the drop-in boundary for the ONE hot path of the reference: the FMM
+ * matrix-vector product used inside GMRES.  The reference is a C++20 static library without an
+ * FFI layer; its seams are ordinary functions.  Each entry point below names the reference
+ * interface it stands in for (paths relative to /root/reference/proj/core).  The C++ mirror of
+ * those interfaces (same names, argument meaning and exceptions) over this ABI is
+ * include/hfmm_b200.hpp; INTEGRATION.md shows the binding a reference maintainer would add.
+ *
+ * Conventions: plain pointers and sizes only; complex arrays are interleaved (re, im) doubles —
+ * bit-compatible with std::complex<double> / `cplx` (include/hfmm/common.hpp:14).  The caller owns
+ * every host buffer; the handle owns all device memory, streams and communicators.  One call in
+ * flight per handle (as "one apply at a time per system", include/hfmm/solver.hpp:92-94).
+ * Every function returns an hfmm_status; no exception crosses this boundary.  There is NO CPU
+ * fallback: without a CUDA device every compute call fails with HFMM_ERR_DEVICE.
+ */
+#ifndef HFMM_CUDA_H
+#define HFMM_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes map 1:1 onto the reference's error taxonomy (include/hfmm/common.hpp:43-55);
+ * the C++ mirror rethrows the matching exception type. */
+typedef enum {
+  HFMM_OK = 0,
+  HFMM_ERR_CONFIG = 1,     /* hfmm::config_error      */
+  HFMM_ERR_SINGULAR = 2,   /* hfmm::singular_error    */
+  HFMM_ERR_STRUCTURAL = 3, /* hfmm::structural_error  */
+  HFMM_ERR_ACCURACY = 4,   /* hfmm::accuracy_error    */
+  HFMM_ERR_DOMAIN = 5,     /* std::domain_error (point outside the box, octree.cpp:30-31) */
+  HFMM_ERR_DEVICE = 6,     /* CUDA / NCCL failure, or no device: never falls back to the CPU */
+  HFMM_ERR_INTERNAL = 9
+} hfmm_status;
+
+enum {
+  /* build tree + interaction lists with the host C++ builder instead of the device builder
+   * (debug toggle kept until list statistics match the reference exactly) */
+  HFMM_FLAG_HOST_TREE = 1 << 0,
+  /* time each phase with CUDA events (fills hfmm_cuda_stats seconds); costs a few syncs */
+  HFMM_FLAG_PHASE_TIMERS = 1 << 1
+};
+
+/* POD mirror of WaveNumber (common.hpp:37-40), TraversalConfig (traversal.hpp:11-18) and the
+ * build_tree arguments (octree.hpp:84-90).  wave_i must be 0 in this release. */
+typedef struct {
+  double wave_r, wave_i;
+  int order;       /* expansion order P (execute_plan `order`, traversal.hpp:59-62)           */
+  int ncrit;       /* leaf capacity c                                                          */
+  int grain;       /* task grain s; validated s >= c >= 1 (traversal.cpp:16-21), else unused   */
+  double theta;    /* opening angle, 0 < theta <= 1                                            */
+  double kd_max;   /* wavenumber gate; 0 disables (traversal.cpp:45-48)                        */
+  double leaf_cap; /* max leaf diameter; 0 none; < 0: kd_max/|k| as solver.cpp:238-242         */
+  int device;      /* CUDA device ordinal                                                      */
+  int flags;       /* HFMM_FLAG_*                                                              */
+} hfmm_cuda_config;
+
+/* Mirror of FmmStats (traversal.hpp:44-52) plus tree/list statistics and per-kernel device times */
+typedef struct {
+  uint64_t n_bodies, n_cells, n_leaves, max_level;
+  uint64_t m2l_pairs, p2p_pairs, p2p_body_pairs; /* cell pairs, leaf pairs, body pairs */
+  uint64_t m2l_shift_classes, rotation_tables, coaxial_tables;
+  uint64_t starved_cells;
+  double setup_seconds;        /* tree + lists + tables + upload (once per point set)       */
+  double upward_seconds;       /* P2M + M2M          (last matvec, CUDA events)              */
+  double interaction_seconds;  /* M2L + P2P                                                  */
+  double downward_seconds;     /* L2L + L2P                                                  */
+  double p2p_seconds, m2l_seconds, p2m_seconds, m2m_seconds, l2l_seconds, l2p_seconds;
+  double matvec_seconds;       /* whole device-side matvec                                   */
+  uint64_t kernel_launches;    /* kernels launched by the last matvec                        */
+  uint64_t device_bytes;       /* HBM held by the handle                                     */
+} hfmm_cuda_stats;
+
+typedef struct hfmm_cuda hfmm_cuda_t;
+
+/* Validates the configuration (config_error rules of traversal.cpp:16-21,212-213), selects the
+ * device, creates streams.  Stands in for constructing TraversalConfig/KernelConfig. */
+int hfmm_cuda_create(hfmm_cuda_t** out, const hfmm_cuda_config* cfg);
+void hfmm_cuda_destroy(hfmm_cuda_t* h);
+/* message of the last failure on this handle (or of the last failed create when h is NULL) */
+const char* hfmm_cuda_last_error(const hfmm_cuda_t* h);
+
+/* build_tree (octree.cpp:142-182) + dual_tree_traversal (traversal.cpp:82-97) on the same point
+ * set as sources and targets: Morton order, octree, M2L/P2P lists, translation tables, all
+ * device-resident afterwards.  xyz: n x 3 doubles, caller order. */
+int hfmm_cuda_set_points(hfmm_cuda_t* h, const double* xyz, size_t n);
+
+/* execute_plan (traversal.cpp:208-279): out[i] = sum_j G(x_i, x_j) q[j], j != coincident.
+ * q, out: n interleaved complex doubles in CALLER order (Body::index mapping, solver.cpp:327-331).
+ * Host buffers; host<->device copies happen inside the call. */
+int hfmm_cuda_matvec(hfmm_cuda_t* h, const double* q, double* out);
+
+/* Same product with operands already resident in HBM: q_dev / out_dev are device pointers to n
+ * float2 (complex FP32) in caller order.  No host traffic, asynchronous on the handle's stream
+ * until hfmm_cuda_sync. */
+int hfmm_cuda_matvec_device(hfmm_cuda_t* h, const void* q_dev, void* out_dev);
+int hfmm_cuda_sync(hfmm_cuda_t* h);
+
+/* apply_operator tail (solver.cpp:327-328,340-357) and gmres_solve's block-Jacobi right
+ * preconditioner (solver.cpp:376-382).  Any pointer group may be NULL to leave it unset.
+ *   far_weight[n]                      x is scaled by it before the FMM (solver.cpp:327-328)
+ *   patch_block[n/ni * ni * ni]        row-major complex blocks    (DiscreteSystem::patch_block)
+ *   near_offset[n+1], near_source[nnz], near_delta[nnz]   CSR      (DiscreteSystem::near_*)
+ *   block_lu[n/ni * ni * ni], block_piv[n]  LU factors + pivots    (DiscreteSystem::block_lu/piv)
+ * After this call hfmm_cuda_matvec computes the full apply_operator. */
+int hfmm_cuda_set_corrections(hfmm_cuda_t* h, int ni, const double* far_weight,
+                              const double* patch_block, const uint32_t* near_offset,
+                              const uint32_t* near_source, const double* near_delta,
+                              const double* block_lu, const int32_t* block_piv);
+
+/* GmresConfig / SolveReport (solver.hpp:97-116) */
+typedef struct {
+  double rtol;
+  int restart;
+  int max_iterations;
+  int precondition; /* use block_lu as right preconditioner when set */
+} hfmm_gmres_config;
+typedef struct {
+  int iterations;
+  int converged;
+  int breakdown;
+  double rhs_norm;
+  double final_residual;
+  double seconds;
+  double matvec_seconds;
+} hfmm_gmres_report;
+
+/* gmres / gmres_solve (gmres.cpp:35-174, solver.cpp:361-391) with device-resident Krylov vectors.
+ * rhs, x: n interleaved complex doubles (host).  residuals (optional) receives up to
+ * residual_cap per-iteration relative residual estimates. */
+int hfmm_cuda_gmres(hfmm_cuda_t* h, const double* rhs, double* x, const hfmm_gmres_config* cfg,
+                    hfmm_gmres_report* report, double* residuals, int residual_cap);
+
+/* evaluate_scattered_field (solver.cpp:393-419): plain single-layer sum at exterior points.
+ * coeff: n complex (caller order, multiplied by far_weight inside); obs: nobs x 3; out: nobs complex */
+int hfmm_cuda_evaluate_field(hfmm_cuda_t* h, const double* coeff, const double* obs, size_t nobs,
+                             double* out);
+
+int hfmm_cuda_get_stats(hfmm_cuda_t* h, hfmm_cuda_stats* out);
+
+/* ---- introspection used by the parity tests (tree / list / expansion level checks) -------- */
+/* cells in the library's level order: 8 x u32 per cell = level, ix, iy, iz, body_first,
+ * body_count, child_first, child_count (same record as the checkers' *_fmm_cells) */
+int hfmm_cuda_get_cells(hfmm_cuda_t* h, uint32_t* out, size_t capacity_cells);
+/* Morton order: out[slot] = caller index (Body::index) */
+int hfmm_cuda_get_body_order(hfmm_cuda_t* h, uint32_t* out);
+/* which: 0 M2L cell pairs, 1 P2P leaf pairs; (target, source) u32 pairs, unspecified order.
+ * Pass out == NULL to query the count only. */
+int hfmm_cuda_get_pairs(hfmm_cuda_t* h, int which, uint32_t* out, uint64_t* count);
+/* which: 0 multipole, 1 local, of the last matvec, UNSCALED back to the reference's convention
+ * (M_n^m / L_n^m at index n(n+1)+m); out: n_cells x (P+1)^2 interleaved complex doubles */
+int hfmm_cuda_get_expansions(hfmm_cuda_t* h, int which, double* out);
+
+/* ---- multi-GPU (one process per GPU) ---------------------------------------- */
+/* 128-byte NCCL unique id, created on rank 0 and distributed by the caller's own plumbing */
+int hfmm_cuda_comm_unique_id(uint8_t id[128]);
+/* joins the communicator; must precede set_points.  With nranks > 1, set_points takes the GLOBAL
+ * point set on every rank, the Morton order is cut into nranks contiguous ranges by estimated
+ * work, and matvec exchanges the locally essential tree over NCCL. */
+int hfmm_cuda_comm_init(hfmm_cuda_t* h, const uint8_t id[128], int rank, int nranks);
+
+const char* hfmm_cuda_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HFMM_CUDA_H */

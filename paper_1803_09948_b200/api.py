@@ -1,0 +1,262 @@
+"""ctypes binding of include/hfmm_cuda.h.  No arithmetic lives here; there is no CPU fallback —
+if the shared library or a CUDA device is missing every compute call raises."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libhfmm_b200.so")
+
+HFMM_FLAG_HOST_TREE = 1 << 0
+HFMM_FLAG_PHASE_TIMERS = 1 << 1
+
+_STATUS = {1: "config_error", 2: "singular_error", 3: "structural_error", 4: "accuracy_error",
+           5: "domain_error", 6: "device_error", 9: "internal_error"}
+
+
+class HfmmError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {message}")
+        self.status = status
+        self.kind = _STATUS.get(status, str(status))
+
+
+class _Config(C.Structure):
+    _fields_ = [("wave_r", C.c_double), ("wave_i", C.c_double), ("order", C.c_int),
+                ("ncrit", C.c_int), ("grain", C.c_int), ("theta", C.c_double),
+                ("kd_max", C.c_double), ("leaf_cap", C.c_double), ("device", C.c_int),
+                ("flags", C.c_int)]
+
+
+class Stats(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in
+                ("n_bodies", "n_cells", "n_leaves", "max_level", "m2l_pairs", "p2p_pairs",
+                 "p2p_body_pairs", "m2l_shift_classes", "rotation_tables", "coaxial_tables",
+                 "starved_cells")] + \
+               [(n, C.c_double) for n in
+                ("setup_seconds", "upward_seconds", "interaction_seconds", "downward_seconds",
+                 "p2p_seconds", "m2l_seconds", "p2m_seconds", "m2m_seconds", "l2l_seconds",
+                 "l2p_seconds", "matvec_seconds")] + \
+               [("kernel_launches", C.c_uint64), ("device_bytes", C.c_uint64)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+class _GmresConfig(C.Structure):
+    _fields_ = [("rtol", C.c_double), ("restart", C.c_int), ("max_iterations", C.c_int),
+                ("precondition", C.c_int)]
+
+
+class _GmresReport(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("breakdown", C.c_int),
+                ("rhs_norm", C.c_double), ("final_residual", C.c_double), ("seconds", C.c_double),
+                ("matvec_seconds", C.c_double)]
+
+
+def library_path() -> str:
+    return _SO
+
+
+def build_library(force: bool = False) -> str:
+    """compile csrc/ for sm_100a in-tree (nvcc cross-compiles without a GPU)"""
+    if force or not os.path.exists(_SO):
+        subprocess.check_call(["make", "-C", os.path.join(_HERE, "csrc"), "-j8"],
+                              stdout=subprocess.DEVNULL)
+    return _SO
+
+
+_lib = None
+
+
+def load_library():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_SO):
+            raise FileNotFoundError(
+                f"{_SO} is missing: build it with `make -C paper_1803_09948_b200/csrc` "
+                "(there is no CPU fallback)")
+        lib = C.CDLL(_SO)
+        lib.hfmm_cuda_last_error.restype = C.c_char_p
+        lib.hfmm_cuda_version.restype = C.c_char_p
+        _lib = lib
+    return _lib
+
+
+_dp = C.POINTER(C.c_double)
+
+
+def _c128(a):
+    return np.ascontiguousarray(a, dtype=np.complex128)
+
+
+class HfmmCuda:
+    """One FMM operator on one GPU (mirror of build_tree + dual_tree_traversal + execute_plan)."""
+
+    def __init__(self, k: float, order: int, ncrit: int = 64, theta: float = 0.4,
+                 kd_max: float = 1.0, leaf_cap: float = -1.0, grain: int | None = None,
+                 device: int = 0, flags: int = 0, wave_i: float = 0.0):
+        self.lib = load_library()
+        cfg = _Config(float(k), float(wave_i), int(order), int(ncrit),
+                      int(grain if grain is not None else ncrit), float(theta), float(kd_max),
+                      float(leaf_cap), int(device), int(flags))
+        self.h = C.c_void_p()
+        rc = self.lib.hfmm_cuda_create(C.byref(self.h), C.byref(cfg))
+        if rc:
+            raise HfmmError(rc, self.lib.hfmm_cuda_last_error(None).decode())
+        self.order = order
+        self.n = 0
+
+    def _check(self, rc):
+        if rc:
+            raise HfmmError(rc, self.lib.hfmm_cuda_last_error(self.h).decode())
+
+    def set_points(self, xyz):
+        xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+        if xyz.ndim != 2 or xyz.shape[1] != 3:
+            raise ValueError("xyz must be (n, 3)")
+        self._check(self.lib.hfmm_cuda_set_points(self.h, xyz.ctypes.data_as(_dp),
+                                                  C.c_size_t(xyz.shape[0])))
+        self.n = xyz.shape[0]
+
+    def matvec(self, q):
+        q = _c128(q)
+        if q.shape != (self.n,):
+            raise ValueError("charge vector length mismatch")
+        out = np.empty(self.n, dtype=np.complex128)
+        self._check(self.lib.hfmm_cuda_matvec(self.h, q.ctypes.data_as(_dp), out.ctypes.data_as(_dp)))
+        return out
+
+    def matvec_into(self, q_ptr: int, out_ptr: int):
+        """host buffers by address (pinned memory from the caller), no numpy allocation"""
+        self._check(self.lib.hfmm_cuda_matvec(self.h, C.c_void_p(q_ptr), C.c_void_p(out_ptr)))
+
+    def matvec_device(self, q_dev_ptr: int, out_dev_ptr: int):
+        self._check(self.lib.hfmm_cuda_matvec_device(self.h, C.c_void_p(q_dev_ptr),
+                                                     C.c_void_p(out_dev_ptr)))
+
+    def sync(self):
+        self._check(self.lib.hfmm_cuda_sync(self.h))
+
+    def stats(self) -> dict:
+        s = Stats()
+        self._check(self.lib.hfmm_cuda_get_stats(self.h, C.byref(s)))
+        return s.as_dict()
+
+    def cells(self):
+        nc = self.stats()["n_cells"]
+        out = np.zeros((nc, 8), dtype=np.uint32)
+        self._check(self.lib.hfmm_cuda_get_cells(self.h, out.ctypes.data_as(C.c_void_p), C.c_size_t(nc)))
+        return out
+
+    def body_order(self):
+        out = np.zeros(self.n, dtype=np.uint32)
+        self._check(self.lib.hfmm_cuda_get_body_order(self.h, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def pairs(self, which: int):
+        cnt = C.c_uint64()
+        self._check(self.lib.hfmm_cuda_get_pairs(self.h, which, None, C.byref(cnt)))
+        out = np.zeros((cnt.value, 2), dtype=np.uint32)
+        if cnt.value:
+            self._check(self.lib.hfmm_cuda_get_pairs(self.h, which, out.ctypes.data_as(C.c_void_p),
+                                                     C.byref(cnt)))
+        return out
+
+    def expansions(self, which: int):
+        nc = self.stats()["n_cells"]
+        out = np.zeros((nc, (self.order + 1) ** 2), dtype=np.complex128)
+        self._check(self.lib.hfmm_cuda_get_expansions(self.h, which, out.ctypes.data_as(_dp)))
+        return out
+
+    def set_corrections(self, ni, far_weight=None, patch_block=None, near_offset=None,
+                        near_source=None, near_delta=None, block_lu=None, block_piv=None):
+        keep = []
+
+        def ptr(a, dt):
+            if a is None or len(a) == 0:
+                return None
+            a = np.ascontiguousarray(a, dtype=dt)
+            keep.append(a)
+            return a.ctypes.data_as(C.c_void_p)
+
+        self._check(self.lib.hfmm_cuda_set_corrections(
+            self.h, int(ni), ptr(far_weight, np.float64), ptr(patch_block, np.complex128),
+            ptr(near_offset, np.uint32), ptr(near_source, np.uint32), ptr(near_delta, np.complex128),
+            ptr(block_lu, np.complex128), ptr(block_piv, np.int32)))
+
+    def gmres(self, rhs, rtol=1e-4, restart=30, max_iterations=500, precondition=True):
+        rhs = _c128(rhs)
+        x = np.zeros(self.n, dtype=np.complex128)
+        cfg = _GmresConfig(rtol, restart, max_iterations, int(precondition))
+        rep = _GmresReport()
+        res = np.zeros(max_iterations + 1)
+        self._check(self.lib.hfmm_cuda_gmres(self.h, rhs.ctypes.data_as(_dp), x.ctypes.data_as(_dp),
+                                             C.byref(cfg), C.byref(rep), res.ctypes.data_as(_dp),
+                                             len(res)))
+        return x, dict(iterations=rep.iterations, converged=bool(rep.converged),
+                       breakdown=bool(rep.breakdown), rhs_norm=rep.rhs_norm,
+                       final_residual=rep.final_residual, seconds=rep.seconds,
+                       matvec_seconds=rep.matvec_seconds, residuals=res[:rep.iterations].copy())
+
+    def evaluate_field(self, coeff, obs):
+        coeff = _c128(coeff)
+        obs = np.ascontiguousarray(obs, dtype=np.float64)
+        out = np.zeros(obs.shape[0], dtype=np.complex128)
+        self._check(self.lib.hfmm_cuda_evaluate_field(self.h, coeff.ctypes.data_as(_dp),
+                                                      obs.ctypes.data_as(_dp),
+                                                      C.c_size_t(obs.shape[0]), out.ctypes.data_as(_dp)))
+        return out
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            self.lib.hfmm_cuda_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---- host-only debug helpers (no device needed) used by the CPU-side tests -------------------
+def debug_compose_translation(order, k, t, kind, s_src=1.0, s_dst=1.0):
+    lib = load_library()
+    dim = (order + 1) ** 2
+    out = np.zeros((dim, dim), dtype=np.complex128)
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    rc = lib.hfmm_debug_compose_translation(int(order), C.c_double(k), t.ctypes.data_as(_dp),
+                                            int(kind), C.c_double(s_src), C.c_double(s_dst),
+                                            out.ctypes.data_as(_dp))
+    if rc:
+        raise HfmmError(rc, lib.hfmm_cuda_last_error(None).decode())
+    return out
+
+
+def debug_host_tree(xyz, ncrit, leaf_cap, k, theta, kd_max):
+    lib = load_library()
+    xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+    n = xyz.shape[0]
+    counts = (C.c_uint64 * 5)()
+    args = lambda *extra: lib.hfmm_debug_host_tree(
+        xyz.ctypes.data_as(_dp), C.c_size_t(n), int(ncrit), C.c_double(leaf_cap), C.c_double(k),
+        C.c_double(theta), C.c_double(kd_max), counts, *extra)
+    rc = args(None, C.c_size_t(0), None, None, None, C.c_size_t(0))
+    if rc:
+        raise HfmmError(rc, lib.hfmm_cuda_last_error(None).decode())
+    nc, nl, nm2l, np2p, maxl = [int(v) for v in counts]
+    cells = np.zeros((nc, 8), dtype=np.uint32)
+    order = np.zeros(n, dtype=np.uint32)
+    cap = max(nm2l, np2p, 1)
+    m2l = np.zeros((cap, 2), dtype=np.uint32)
+    p2p = np.zeros((cap, 2), dtype=np.uint32)
+    vp = lambda a: a.ctypes.data_as(C.c_void_p)
+    rc = args(vp(cells), C.c_size_t(nc), vp(order), vp(m2l), vp(p2p), C.c_size_t(cap))
+    if rc:
+        raise HfmmError(rc, lib.hfmm_cuda_last_error(None).decode())
+    return dict(cells=cells, order=order, m2l=m2l[:nm2l], p2p=p2p[:np2p], n_leaves=nl, max_level=maxl)

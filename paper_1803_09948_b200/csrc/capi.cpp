@@ -1,0 +1,205 @@
+// capi.cpp — the extern "C" surface declared in include/hfmm_cuda.h.  Converts exceptions to
+// status codes; nothing else lives here.
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "engine.hpp"
+#include "hfmm_cuda.h"
+
+using hfmm_b200::Engine;
+using hfmm_b200::Error;
+
+struct hfmm_cuda {
+  Engine* engine = nullptr;
+};
+
+namespace {
+thread_local std::string g_create_error;
+
+template <typename Fn>
+int guarded(hfmm_cuda* h, Fn&& fn) {
+  std::string* sink = (h && h->engine) ? &h->engine->last_error : &g_create_error;
+  try {
+    fn();
+    return HFMM_OK;
+  } catch (const Error& e) {
+    *sink = e.what();
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    *sink = "host allocation failed";
+    return HFMM_ERR_INTERNAL;
+  } catch (const std::exception& e) {
+    *sink = e.what();
+    return HFMM_ERR_INTERNAL;
+  }
+}
+
+int need(hfmm_cuda* h) {
+  if (h && h->engine) return HFMM_OK;
+  g_create_error = "null handle";
+  return HFMM_ERR_CONFIG;
+}
+}  // namespace
+
+extern "C" {
+
+int hfmm_cuda_create(hfmm_cuda_t** out, const hfmm_cuda_config* cfg) {
+  if (!out || !cfg) {
+    g_create_error = "null argument";
+    return HFMM_ERR_CONFIG;
+  }
+  *out = nullptr;
+  return guarded(nullptr, [&] {
+    auto* h = new hfmm_cuda;
+    try {
+      h->engine = new Engine(*cfg);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void hfmm_cuda_destroy(hfmm_cuda_t* h) {
+  if (!h) return;
+  delete h->engine;
+  delete h;
+}
+
+const char* hfmm_cuda_last_error(const hfmm_cuda_t* h) {
+  return (h && h->engine) ? h->engine->last_error.c_str() : g_create_error.c_str();
+}
+
+int hfmm_cuda_set_points(hfmm_cuda_t* h, const double* xyz, size_t n) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] {
+    if (!xyz && n) throw Error(HFMM_ERR_CONFIG, "null point array");
+    h->engine->set_points(xyz, n);
+  });
+}
+
+int hfmm_cuda_matvec(hfmm_cuda_t* h, const double* q, double* out) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] {
+    if (!q || !out) throw Error(HFMM_ERR_CONFIG, "null vector");
+    h->engine->matvec_host(q, out);
+  });
+}
+
+int hfmm_cuda_matvec_device(hfmm_cuda_t* h, const void* q_dev, void* out_dev) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] {
+    if (!q_dev || !out_dev) throw Error(HFMM_ERR_CONFIG, "null vector");
+    h->engine->matvec_device(q_dev, out_dev);
+  });
+}
+
+int hfmm_cuda_sync(hfmm_cuda_t* h) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] { h->engine->sync(); });
+}
+
+int hfmm_cuda_get_stats(hfmm_cuda_t* h, hfmm_cuda_stats* out) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] { h->engine->get_stats(out); });
+}
+
+int hfmm_cuda_get_cells(hfmm_cuda_t* h, uint32_t* out, size_t capacity_cells) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] { h->engine->get_cells(out, capacity_cells); });
+}
+
+int hfmm_cuda_get_body_order(hfmm_cuda_t* h, uint32_t* out) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] { h->engine->get_body_order(out); });
+}
+
+int hfmm_cuda_get_pairs(hfmm_cuda_t* h, int which, uint32_t* out, uint64_t* count) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] { h->engine->get_pairs(which, out, count); });
+}
+
+int hfmm_cuda_get_expansions(hfmm_cuda_t* h, int which, double* out) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] { h->engine->get_expansions(which, out); });
+}
+
+int hfmm_cuda_set_corrections(hfmm_cuda_t* h, int, const double*, const double*, const uint32_t*,
+                              const uint32_t*, const double*, const double*, const int32_t*) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] { throw Error(HFMM_ERR_INTERNAL, "set_corrections: not built yet"); });
+}
+
+int hfmm_cuda_gmres(hfmm_cuda_t* h, const double*, double*, const hfmm_gmres_config*,
+                    hfmm_gmres_report*, double*, int) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] { throw Error(HFMM_ERR_INTERNAL, "gmres: not built yet"); });
+}
+
+int hfmm_cuda_evaluate_field(hfmm_cuda_t* h, const double*, const double*, size_t, double*) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] { throw Error(HFMM_ERR_INTERNAL, "evaluate_field: not built yet"); });
+}
+
+int hfmm_cuda_comm_unique_id(uint8_t*) {
+  g_create_error = "multi-GPU mode not built yet";
+  return HFMM_ERR_INTERNAL;
+}
+int hfmm_cuda_comm_init(hfmm_cuda_t* h, const uint8_t*, int, int) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] { throw Error(HFMM_ERR_INTERNAL, "multi-GPU mode not built yet"); });
+}
+
+const char* hfmm_cuda_version(void) { return "hfmm-b200 0.1 (sm_100a)"; }
+
+// ---- host-only debug entry points for the CPU-side table tests (no device needed) ------------
+// dense (P+1)^2 x (P+1)^2 matrix composed in FP64 from the FP32 device tables, unscaled.
+// kind: 0 M2L, 1 regular (M2M/L2L).  Returns HFMM_OK.
+int hfmm_debug_compose_translation(int order, double k, const double* t, int kind, double s_src,
+                                   double s_dst, double* out) {
+  return guarded(nullptr, [&] {
+    if (order < 0 || order > hfmm_b200::kMaxOrder) throw Error(HFMM_ERR_CONFIG, "order out of range");
+    hfmm_b200::compose_dense_from_tables(order, k, t, kind, s_src, s_dst, out);
+  });
+}
+
+// tree + lists of the host builder without touching a device: counts[0..4] = cells, leaves,
+// m2l pairs, p2p leaf pairs, max level
+int hfmm_debug_host_tree(const double* xyz, size_t n, int ncrit, double leaf_cap, double k,
+                         double theta, double kd_max, uint64_t* counts, uint32_t* cells_out,
+                         size_t cells_capacity, uint32_t* order_out, uint32_t* m2l_out,
+                         uint32_t* p2p_out, size_t pair_capacity) {
+  return guarded(nullptr, [&] {
+    hfmm_b200::TreeArrays t;
+    hfmm_b200::PairLists p;
+    hfmm_b200::build_tree_host(t, xyz, n, ncrit, leaf_cap, 4);
+    hfmm_b200::dual_tree_traversal_host(t, k, theta, kd_max, p, 4);
+    counts[0] = t.n_cells();
+    counts[1] = t.leaves.size();
+    counts[2] = p.m2l_t.size();
+    counts[3] = p.p2p_t.size();
+    counts[4] = uint64_t(t.max_level);
+    if (cells_out && cells_capacity >= t.n_cells())
+      for (size_t c = 0; c < t.n_cells(); ++c) {
+        uint32_t* o = cells_out + 8 * c;
+        o[0] = t.level[c]; o[1] = t.ix[c]; o[2] = t.iy[c]; o[3] = t.iz[c];
+        o[4] = t.body_first[c]; o[5] = t.body_count[c];
+        o[6] = t.child_first[c]; o[7] = t.child_count[c];
+      }
+    if (order_out) std::memcpy(order_out, t.index.data(), sizeof(uint32_t) * n);
+    if (m2l_out && pair_capacity >= p.m2l_t.size())
+      for (size_t i = 0; i < p.m2l_t.size(); ++i) {
+        m2l_out[2 * i] = p.m2l_t[i];
+        m2l_out[2 * i + 1] = p.m2l_s[i];
+      }
+    if (p2p_out && pair_capacity >= p.p2p_t.size())
+      for (size_t i = 0; i < p.p2p_t.size(); ++i) {
+        p2p_out[2 * i] = p.p2p_t[i];
+        p2p_out[2 * i + 1] = p.p2p_s[i];
+      }
+  });
+}
+
+}  // extern "C"

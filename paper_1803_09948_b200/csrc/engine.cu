@@ -1,0 +1,659 @@
+// engine.cu — see engine.hpp
+#include "engine.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <complex>
+#include <map>
+#include <numeric>
+#include <thread>
+#include <unordered_map>
+
+#include "tables.hpp"
+
+namespace hfmm_b200 {
+
+size_t& device_bytes_counter() {
+  static size_t bytes = 0;
+  return bytes;
+}
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846264338327950288;
+
+template <typename Fn>
+void parallel_for(size_t n, int threads, Fn&& fn) {
+  const size_t parts = std::max<size_t>(1, std::min<size_t>(size_t(std::max(threads, 1)), n));
+  if (parts <= 1) {
+    for (size_t i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (size_t p = 0; p < parts; ++p)
+    pool.emplace_back([&fn, n, p, parts] {
+      for (size_t i = p; i < n; i += parts) fn(i);
+    });
+  for (auto& t : pool) t.join();
+}
+
+int64_t gcd64(int64_t a, int64_t b) {
+  while (b) {
+    const int64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a < 0 ? -a : a;
+}
+
+// de-duplicates rotation (by polar angle) and coaxial (by kind, levels, distance) tables
+struct TableRegistry {
+  struct CoaxSpec {
+    CoaxKind kind;
+    double dist, s_src, s_dst;
+  };
+  std::map<std::pair<int64_t, int64_t>, uint32_t> rot_ids;
+  std::vector<double> rot_cos;
+  std::map<std::tuple<int, int, int, int, int64_t>, uint32_t> coax_ids;
+  std::vector<CoaxSpec> coax_specs;
+
+  // direction (dx,dy,dz) on any lattice: key is the reduced fraction dz^2 / |d|^2 with dz's sign
+  uint32_t rot(int64_t dx, int64_t dy, int64_t dz) {
+    const int64_t r2 = dx * dx + dy * dy + dz * dz, z2 = dz * dz;
+    const int64_t g = gcd64(z2, r2);
+    const std::pair<int64_t, int64_t> key{(dz < 0 ? -1 : 1) * (z2 / g), r2 / g};
+    auto [it, fresh] = rot_ids.try_emplace(key, uint32_t(rot_cos.size()));
+    if (fresh) rot_cos.push_back(double(dz) / std::sqrt(double(r2)));
+    return it->second;
+  }
+  uint32_t coax(CoaxKind kind, int lsrc, int ldst, int lunit, int64_t r2, double unit,
+                double s_src, double s_dst) {
+    const auto key = std::make_tuple(int(kind), lsrc, ldst, lunit, r2);
+    auto [it, fresh] = coax_ids.try_emplace(key, uint32_t(coax_specs.size()));
+    if (fresh) coax_specs.push_back({kind, unit * std::sqrt(double(r2)), s_src, s_dst});
+    return it->second;
+  }
+};
+
+TranslateClass make_class(TableRegistry& reg, CoaxKind kind, int64_t dx, int64_t dy, int64_t dz,
+                          int lsrc, int ldst, int lunit, double unit, double s_src, double s_dst) {
+  TranslateClass c;
+  c.rot = reg.rot(dx, dy, dz);
+  c.coax = reg.coax(kind, lsrc, ldst, lunit, dx * dx + dy * dy + dz * dz, unit, s_src, s_dst);
+  const double rxy = std::sqrt(double(dx * dx + dy * dy));
+  c.cphi = rxy > 0 ? float(double(dx) / rxy) : 1.0f;
+  c.sphi = rxy > 0 ? float(double(dy) / rxy) : 0.0f;
+  return c;
+}
+
+struct ShiftKey {
+  int32_t dx, dy, dz;
+  int16_t lt, ls;
+  bool operator==(const ShiftKey& o) const {
+    return dx == o.dx && dy == o.dy && dz == o.dz && lt == o.lt && ls == o.ls;
+  }
+};
+struct ShiftKeyHash {
+  size_t operator()(const ShiftKey& k) const {
+    uint64_t h = 0x9e3779b97f4a7c15ull;
+    for (uint64_t v : {uint64_t(uint32_t(k.dx)), uint64_t(uint32_t(k.dy)), uint64_t(uint32_t(k.dz)),
+                       uint64_t(uint16_t(k.lt)) << 16 | uint16_t(k.ls)})
+      h = (h ^ v) * 0xff51afd7ed558ccdull + (h >> 29);
+    return size_t(h);
+  }
+};
+
+}  // namespace
+
+Engine::Engine(const hfmm_cuda_config& cfg) : cfg_(cfg) {
+  // config_error rules of the reference (traversal.cpp:16-21, 212-213; octree.cpp:144)
+  if (cfg.ncrit < 1 || cfg.grain < cfg.ncrit)
+    throw Error(HFMM_ERR_CONFIG, "traversal grain needs s >= c >= 1");
+  if (!(cfg.theta > 0) || cfg.theta > 1)
+    throw Error(HFMM_ERR_CONFIG, "opening angle must satisfy 0 < theta <= 1");
+  if (cfg.order < 0) throw Error(HFMM_ERR_CONFIG, "expansion order must be non-negative");
+  if (cfg.order > kMaxOrder)
+    throw Error(HFMM_ERR_CONFIG, "expansion order above the supported maximum (16)");
+  if (cfg.wave_i != 0) throw Error(HFMM_ERR_CONFIG, "complex wavenumbers (wave_i != 0) unsupported");
+  if (!(cfg.wave_r > 0)) throw Error(HFMM_ERR_CONFIG, "wavenumber must be positive");
+  if (cfg.kd_max < 0) throw Error(HFMM_ERR_CONFIG, "kd_max must be non-negative");
+  leaf_cap_ = cfg.leaf_cap;
+  if (leaf_cap_ < 0) leaf_cap_ = cfg.kd_max > 0 ? cfg.kd_max / std::abs(cfg.wave_r) : 0.0;
+  threads_ = int(std::max(1u, std::thread::hardware_concurrency()));
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw Error(HFMM_ERR_DEVICE, "no CUDA device available (this library has no CPU fallback)");
+  if (cfg.device < 0 || cfg.device >= ndev) throw Error(HFMM_ERR_CONFIG, "device ordinal out of range");
+  HFMM_CUDA_CHECK(cudaSetDevice(cfg.device));
+  HFMM_CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  HFMM_CUDA_CHECK(cudaStreamCreateWithFlags(&stream_near_, cudaStreamNonBlocking));
+  HFMM_CUDA_CHECK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+  HFMM_CUDA_CHECK(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+  ev_.resize(12);
+  for (auto& e : ev_) HFMM_CUDA_CHECK(cudaEventCreate(&e));
+
+  const int P = cfg.order;
+  const size_t tri = size_t(P + 1) * (P + 2) / 2;
+  std::vector<float> diag(P + 1), sub(P + 1), a(tri), b(tri);
+  build_legendre_coefficients(P, diag.data(), sub.data(), a.data(), b.data());
+  upload_legendre_constants(diag.data(), sub.data(), a.data(), b.data(), P);
+}
+
+Engine::~Engine() {
+  cudaSetDevice(cfg_.device);
+  for (auto& e : ev_) cudaEventDestroy(e);
+  if (ev_fork_) cudaEventDestroy(ev_fork_);
+  if (ev_join_) cudaEventDestroy(ev_join_);
+  if (stream_) cudaStreamDestroy(stream_);
+  if (stream_near_) cudaStreamDestroy(stream_near_);
+}
+
+void Engine::require_points() const {
+  if (!have_points_) throw Error(HFMM_ERR_CONFIG, "hfmm_cuda_set_points has not been called");
+}
+
+void Engine::upload_stage(TranslateStage& st, const std::vector<uint32_t>& src,
+                          const std::vector<uint32_t>& dst, const std::vector<uint32_t>& cls_of_pair,
+                          const std::vector<TranslateClass>& classes) {
+  // stable counting sort of the pairs by class, then batches of kTranslateBatch
+  const size_t np = src.size(), nc = classes.size();
+  std::vector<uint64_t> start(nc + 1, 0);
+  for (size_t i = 0; i < np; ++i) ++start[cls_of_pair[i] + 1];
+  for (size_t c = 0; c < nc; ++c) start[c + 1] += start[c];
+  std::vector<uint32_t> s_sorted(np), d_sorted(np);
+  {
+    std::vector<uint64_t> cur(start.begin(), start.end() - 1);
+    for (size_t i = 0; i < np; ++i) {
+      const uint64_t slot = cur[cls_of_pair[i]]++;
+      s_sorted[slot] = src[i];
+      d_sorted[slot] = dst[i];
+    }
+  }
+  std::vector<TranslateItem> items;
+  for (size_t c = 0; c < nc; ++c)
+    for (uint64_t b = start[c]; b < start[c + 1]; b += kTranslateBatch)
+      items.push_back({uint32_t(b), uint32_t(std::min<uint64_t>(kTranslateBatch, start[c + 1] - b)),
+                       uint32_t(c), 0u});
+  if (np >= (uint64_t(1) << 32)) throw Error(HFMM_ERR_CONFIG, "pair count exceeds 32-bit indexing");
+  st.n_items = uint32_t(items.size());
+  st.n_pairs = np;
+  st.items.upload(items, stream_);
+  st.classes.upload(classes, stream_);
+  st.pair_src.upload(s_sorted, stream_);
+  st.pair_dst.upload(d_sorted, stream_);
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+void Engine::build_translate_stages(const PairLists& pairs) {
+  const TreeArrays& t = tree_;
+  const int P = cfg_.order;
+  const double k = cfg_.wave_r;
+  TableRegistry reg;
+  auto scale = [&](int lvl) { return k * t.side(lvl); };
+
+  // ---- M2L: one class per distinct (lattice shift, level pair), as the reference de-duplicates
+  // translation matrices per lattice shift (traversal.cpp:152-166, 233-250)
+  const size_t nm2l = pairs.m2l_t.size();
+  have_far_ = nm2l > 0;
+  m2m_.clear();
+  l2l_.clear();
+  m2l_ = TranslateStage{};
+  stats_.m2l_shift_classes = 0;
+  if (!have_far_) return;
+
+  lmin_src_ = kMaxLevel + 1;
+  lmin_dst_ = kMaxLevel + 1;
+  std::vector<uint32_t> cls_of_pair(nm2l);
+  std::vector<TranslateClass> classes;
+  {
+    std::unordered_map<ShiftKey, uint32_t, ShiftKeyHash> ids;
+    ids.reserve(1 << 16);
+    for (size_t e = 0; e < nm2l; ++e) {
+      const uint32_t a = pairs.m2l_t[e], b = pairs.m2l_s[e];
+      const int la = t.level[a], lb = t.level[b], lmax = std::max(la, lb);
+      lmin_dst_ = std::min(lmin_dst_, la);
+      lmin_src_ = std::min(lmin_src_, lb);
+      auto c = [lmax](uint32_t i, int l) { return int64_t(2 * uint64_t(i) + 1) << (lmax - l); };
+      // t = centre(target) - centre(source) in half-sides of level lmax
+      const ShiftKey key{int32_t(c(t.ix[a], la) - c(t.ix[b], lb)), int32_t(c(t.iy[a], la) - c(t.iy[b], lb)),
+                         int32_t(c(t.iz[a], la) - c(t.iz[b], lb)), int16_t(la), int16_t(lb)};
+      auto [it, fresh] = ids.try_emplace(key, uint32_t(classes.size()));
+      if (fresh)
+        classes.push_back(make_class(reg, CoaxKind::m2l, key.dx, key.dy, key.dz, lb, la, lmax,
+                                     t.side(lmax) / 2, scale(lb), scale(la)));
+      cls_of_pair[e] = it->second;
+    }
+  }
+  stats_.m2l_shift_classes = classes.size();
+  upload_stage(m2l_, pairs.m2l_s, pairs.m2l_t, cls_of_pair, classes);
+
+  // ---- M2M: child level L -> parent, L from the deepest level up to lmin_src+1; the 8 octant
+  // shifts per level of the reference (expansion.cpp:200-222).  t = parent - child = -(+-h) per axis.
+  auto level_stage = [&](int L, bool upward) {
+    std::vector<uint32_t> src, dst, cls;
+    std::vector<TranslateClass> cl;
+    int cls_of_oct[8];
+    std::fill(cls_of_oct, cls_of_oct + 8, -1);
+    for (uint32_t c = t.level_offset[L]; c < t.level_offset[L + 1]; ++c) {
+      const int oct = int(t.ix[c] & 1) << 2 | int(t.iy[c] & 1) << 1 | int(t.iz[c] & 1);
+      if (cls_of_oct[oct] < 0) {
+        int64_t d[3] = {oct & 4 ? -1 : 1, oct & 2 ? -1 : 1, oct & 1 ? -1 : 1};  // parent - child
+        if (!upward)
+          for (auto& v : d) v = -v;
+        cls_of_oct[oct] = int(cl.size());
+        cl.push_back(upward ? make_class(reg, CoaxKind::m2m, d[0], d[1], d[2], L, L - 1, L,
+                                         t.side(L) / 2, scale(L), scale(L - 1))
+                            : make_class(reg, CoaxKind::l2l, d[0], d[1], d[2], L - 1, L, L,
+                                         t.side(L) / 2, scale(L - 1), scale(L)));
+      }
+      src.push_back(upward ? c : t.parent[c]);
+      dst.push_back(upward ? t.parent[c] : c);
+      cls.push_back(uint32_t(cls_of_oct[oct]));
+    }
+    TranslateStage st;
+    upload_stage(st, src, dst, cls, cl);
+    return st;
+  };
+  for (int L = t.max_level; L > lmin_src_; --L) m2m_.push_back(level_stage(L, true));
+  for (int L = lmin_dst_ + 1; L <= t.max_level; ++L) l2l_.push_back(level_stage(L, false));
+
+  // ---- tables
+  const size_t nrot = reg.rot_cos.size(), ncoax = reg.coax_specs.size();
+  stats_.rotation_tables = nrot;
+  stats_.coaxial_tables = ncoax;
+  std::vector<float> rot(nrot * size_t(rot_table_size(P)));
+  std::vector<float> coax(ncoax * size_t(coax_table_size(P)) * 2);
+  parallel_for(nrot, threads_, [&](size_t i) {
+    build_rotation_table(P, reg.rot_cos[i], rot.data() + i * size_t(rot_table_size(P)));
+  });
+  const CoaxBuilder builder(P);
+  parallel_for(ncoax, threads_, [&](size_t i) {
+    const auto& s = reg.coax_specs[i];
+    builder.build(s.kind, k, s.dist, s.s_src, s.s_dst, coax.data() + i * size_t(coax_table_size(P)) * 2);
+  });
+  rot_tables_.upload(rot, stream_);
+  coax_tables_.upload(coax, stream_);
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+void Engine::set_points(const double* xyz, size_t n) {
+  HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  const auto t0 = std::chrono::steady_clock::now();
+  have_points_ = false;
+  build_tree_host(tree_, xyz, n, cfg_.ncrit, leaf_cap_, threads_);
+  dual_tree_traversal_host(tree_, std::abs(cfg_.wave_r), cfg_.theta, cfg_.kd_max, pairs_, threads_);
+  const TreeArrays& t = tree_;
+  const size_t nc = t.n_cells();
+  const double k = cfg_.wave_r;
+  const int Lf = t.max_level;
+
+  // cells
+  std::vector<int4> geom(nc);
+  std::vector<uint2> cbody(nc);
+  for (size_t c = 0; c < nc; ++c) {
+    const int up = Lf - t.level[c];
+    geom[c] = make_int4(int((2 * t.ix[c] + 1) << up), int((2 * t.iy[c] + 1) << up),
+                        int((2 * t.iz[c] + 1) << up), int(t.level[c]));
+    cbody[c] = make_uint2(t.body_first[c], t.body_count[c]);
+  }
+  level_scale_host_.assign(kMaxLevel + 1, 0.f);
+  for (int l = 0; l <= kMaxLevel; ++l) level_scale_host_[l] = float(k * t.side(l));
+  kunit_ = float(k * t.side(Lf) / 2);
+
+  // bodies: leaf-relative, pre-scaled by k
+  std::vector<float4> pos(n);
+  parallel_for(t.leaves.size(), threads_, [&](size_t li) {
+    const uint32_t c = t.leaves[li];
+    const double s = t.side(t.level[c]);
+    const double cx = t.lo[0] + (t.ix[c] + 0.5) * s, cy = t.lo[1] + (t.iy[c] + 0.5) * s,
+                 cz = t.lo[2] + (t.iz[c] + 0.5) * s;
+    for (uint32_t b = t.body_first[c]; b < t.body_first[c] + t.body_count[c]; ++b) {
+      const double* p = xyz + 3 * size_t(t.index[b]);
+      pos[b] = make_float4(float(k * (p[0] - cx)), float(k * (p[1] - cy)), float(k * (p[2] - cz)), 0.f);
+    }
+  });
+
+  // near field: CSR by target leaf without the self pair (handled by the kernel's masked pass)
+  const size_t nleaf = t.leaves.size();
+  std::vector<uint32_t> leaf_slot(nc, 0xffffffffu);
+  for (size_t i = 0; i < nleaf; ++i) leaf_slot[t.leaves[i]] = uint32_t(i);
+  std::vector<uint32_t> off(nleaf + 1, 0);
+  uint64_t body_pairs = 0;
+  for (size_t e = 0; e < pairs_.p2p_t.size(); ++e) {
+    const uint32_t a = pairs_.p2p_t[e], b = pairs_.p2p_s[e];
+    body_pairs += uint64_t(t.body_count[a]) * t.body_count[b];
+    if (a != b) ++off[leaf_slot[a] + 1];
+  }
+  for (size_t i = 0; i < nleaf; ++i) off[i + 1] += off[i];
+  std::vector<uint32_t> srcs(off[nleaf]);
+  std::vector<uint64_t> work(nleaf, 0);
+  {
+    std::vector<uint32_t> cur(off.begin(), off.end() - 1);
+    for (size_t e = 0; e < pairs_.p2p_t.size(); ++e) {
+      const uint32_t a = pairs_.p2p_t[e], b = pairs_.p2p_s[e];
+      work[leaf_slot[a]] += t.body_count[b];
+      if (a != b) srcs[cur[leaf_slot[a]]++] = b;
+    }
+  }
+  // source leaves in ascending cell order: neighbouring bodies, neighbouring addresses
+  parallel_for(nleaf, threads_, [&](size_t i) { std::sort(srcs.begin() + off[i], srcs.begin() + off[i + 1]); });
+  std::vector<P2PTile> tiles;
+  std::vector<uint64_t> tile_work;
+  for (size_t i = 0; i < nleaf; ++i) {
+    const uint32_t c = t.leaves[i];
+    for (uint32_t b = 0; b < t.body_count[c]; b += 32) {
+      const uint32_t nt = std::min<uint32_t>(32, t.body_count[c] - b);
+      tiles.push_back({c, b, nt, uint32_t(i)});
+      tile_work.push_back(work[i] * nt);
+    }
+  }
+  {  // longest tiles first: the tail of the launch is filled with short ones
+    std::vector<uint32_t> order(tiles.size());
+    std::iota(order.begin(), order.end(), 0u);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](uint32_t x, uint32_t y) { return tile_work[x] > tile_work[y]; });
+    std::vector<P2PTile> sorted(tiles.size());
+    for (size_t i = 0; i < order.size(); ++i) sorted[i] = tiles[order[i]];
+    tiles.swap(sorted);
+  }
+  n_tiles_ = uint32_t(tiles.size());
+
+  body_pos_.upload(pos, stream_);
+  body_index_.upload(t.index, stream_);
+  cell_geom_.upload(geom, stream_);
+  cell_body_.upload(cbody, stream_);
+  level_scale_.upload(level_scale_host_, stream_);
+  p2p_tiles_.upload(tiles, stream_);
+  p2p_offset_.upload(off, stream_);
+  p2p_src_.upload(srcs, stream_);
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+
+  // far field
+  stride_ = coeff_stride(cfg_.order);
+  build_translate_stages(pairs_);
+  if (have_far_) {
+    std::vector<uint32_t> up, down;
+    for (uint32_t c : t.leaves) {
+      if (t.level[c] >= lmin_src_) up.push_back(c);
+      if (t.level[c] >= lmin_dst_) down.push_back(c);
+    }
+    n_p2m_leaves_ = uint32_t(up.size());
+    n_l2p_leaves_ = uint32_t(down.size());
+    p2m_leaves_.upload(up, stream_);
+    l2p_leaves_.upload(down, stream_);
+    multipole_.resize(nc * size_t(stride_));
+    local_.resize(nc * size_t(stride_));
+    multipole_.zero(stream_);
+    local_.zero(stream_);
+  } else {
+    n_p2m_leaves_ = n_l2p_leaves_ = 0;
+  }
+  body_q_.resize(n);
+  near_.resize(n);
+  far_.resize(n);
+  io64_.resize(n);
+  far_.zero(stream_);
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+
+  stats_.n_bodies = n;
+  stats_.n_cells = nc;
+  stats_.n_leaves = nleaf;
+  stats_.max_level = uint64_t(t.max_level);
+  stats_.m2l_pairs = pairs_.m2l_t.size();
+  stats_.p2p_pairs = pairs_.p2p_t.size();
+  stats_.p2p_body_pairs = body_pairs;
+  stats_.starved_cells = 0;
+  stats_.setup_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  stats_.device_bytes = device_bytes_counter();
+  have_points_ = true;
+}
+
+// one FMM evaluation, body_q_ (Morton order) -> near_, far_.  The near field runs on its own
+// stream, concurrently with the upward / translation / downward chain.
+void Engine::run_far_and_near() {
+  const bool timers = (cfg_.flags & HFMM_FLAG_PHASE_TIMERS) != 0;
+  uint64_t launches = 0;
+  HFMM_CUDA_CHECK(cudaEventRecord(ev_fork_, stream_));
+  HFMM_CUDA_CHECK(cudaStreamWaitEvent(stream_near_, ev_fork_, 0));
+
+  P2PArgs pa{};
+  pa.tiles = p2p_tiles_.get();
+  pa.n_tiles = n_tiles_;
+  pa.p2p_offset = p2p_offset_.get();
+  pa.p2p_src = p2p_src_.get();
+  pa.cell_geom = cell_geom_.get();
+  pa.cell_body = cell_body_.get();
+  pa.body_pos = body_pos_.get();
+  pa.body_q = body_q_.get();
+  pa.out = near_.get();
+  pa.kunit = kunit_;
+  pa.out_scale = float(cfg_.wave_r / (4.0 * kPi));
+  cudaStream_t sn = timers ? stream_ : stream_near_;  // serialise when timing phases
+  if (timers) HFMM_CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
+  launch_p2p(pa, sn);
+  ++launches;
+  if (timers) HFMM_CUDA_CHECK(cudaEventRecord(ev_[1], stream_));
+
+  if (have_far_) {
+    multipole_.zero(stream_);
+    local_.zero(stream_);
+    LeafExpansionArgs la{};
+    la.cell_geom = cell_geom_.get();
+    la.cell_body = cell_body_.get();
+    la.body_pos = body_pos_.get();
+    la.level_scale = level_scale_.get();
+    la.order = cfg_.order;
+    la.stride = stride_;
+    la.k = float(cfg_.wave_r);
+    la.leaves = p2m_leaves_.get();
+    la.n_leaves = n_p2m_leaves_;
+    if (timers) HFMM_CUDA_CHECK(cudaEventRecord(ev_[2], stream_));
+    launch_p2m(la, body_q_.get(), multipole_.get(), stream_);
+    ++launches;
+    if (timers) HFMM_CUDA_CHECK(cudaEventRecord(ev_[3], stream_));
+
+    auto run_stage = [&](const TranslateStage& st, const float2* src, float2* dst) {
+      TranslateArgs ta{};
+      ta.items = st.items.get();
+      ta.n_items = st.n_items;
+      ta.classes = st.classes.get();
+      ta.pair_src = st.pair_src.get();
+      ta.pair_dst = st.pair_dst.get();
+      ta.rot_tables = rot_tables_.get();
+      ta.coax_tables = coax_tables_.get();
+      ta.src = src;
+      ta.dst = dst;
+      ta.order = cfg_.order;
+      ta.stride = stride_;
+      launch_translate(ta, stream_);
+      if (st.n_items) ++launches;
+    };
+    for (const auto& st : m2m_) run_stage(st, multipole_.get(), multipole_.get());
+    if (timers) HFMM_CUDA_CHECK(cudaEventRecord(ev_[4], stream_));
+    run_stage(m2l_, multipole_.get(), local_.get());
+    if (timers) HFMM_CUDA_CHECK(cudaEventRecord(ev_[5], stream_));
+    for (const auto& st : l2l_) run_stage(st, local_.get(), local_.get());
+    if (timers) HFMM_CUDA_CHECK(cudaEventRecord(ev_[6], stream_));
+    la.leaves = l2p_leaves_.get();
+    la.n_leaves = n_l2p_leaves_;
+    launch_l2p(la, local_.get(), far_.get(), stream_);
+    ++launches;
+    if (timers) HFMM_CUDA_CHECK(cudaEventRecord(ev_[7], stream_));
+  }
+  HFMM_CUDA_CHECK(cudaEventRecord(ev_join_, stream_near_));
+  HFMM_CUDA_CHECK(cudaStreamWaitEvent(stream_, ev_join_, 0));
+  stats_.kernel_launches = launches + 2;  // + gather, scatter
+}
+
+void Engine::matvec_device(const void* q_dev, void* out_dev) {
+  require_points();
+  HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  const uint32_t n = tree_.n_bodies;
+  launch_gather_charges(nullptr, static_cast<const float2*>(q_dev), body_index_.get(), nullptr,
+                        body_q_.get(), n, stream_);
+  run_far_and_near();
+  launch_scatter_potentials(near_.get(), far_.get(), body_index_.get(), nullptr,
+                            static_cast<float2*>(out_dev), n, stream_);
+}
+
+void Engine::matvec_host(const double* q, double* out) {
+  require_points();
+  HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  const uint32_t n = tree_.n_bodies;
+  const bool timers = (cfg_.flags & HFMM_FLAG_PHASE_TIMERS) != 0;
+  HFMM_CUDA_CHECK(cudaEventRecord(ev_[10], stream_));
+  HFMM_CUDA_CHECK(cudaMemcpyAsync(io64_.get(), q, size_t(n) * sizeof(double2), cudaMemcpyHostToDevice, stream_));
+  launch_gather_charges(io64_.get(), nullptr, body_index_.get(), nullptr, body_q_.get(), n, stream_);
+  run_far_and_near();
+  launch_scatter_potentials(near_.get(), far_.get(), body_index_.get(), io64_.get(), nullptr, n, stream_);
+  HFMM_CUDA_CHECK(cudaMemcpyAsync(out, io64_.get(), size_t(n) * sizeof(double2), cudaMemcpyDeviceToHost, stream_));
+  HFMM_CUDA_CHECK(cudaEventRecord(ev_[11], stream_));
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  float ms = 0;
+  HFMM_CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[10], ev_[11]));
+  stats_.matvec_seconds = ms * 1e-3;
+  if (timers) {
+    auto dt = [&](int a, int b) {
+      float v = 0;
+      cudaEventElapsedTime(&v, ev_[a], ev_[b]);
+      return double(v) * 1e-3;
+    };
+    stats_.p2p_seconds = dt(0, 1);
+    if (have_far_) {
+      stats_.p2m_seconds = dt(2, 3);
+      stats_.m2m_seconds = dt(3, 4);
+      stats_.m2l_seconds = dt(4, 5);
+      stats_.l2l_seconds = dt(5, 6);
+      stats_.l2p_seconds = dt(6, 7);
+    }
+    stats_.upward_seconds = stats_.p2m_seconds + stats_.m2m_seconds;
+    stats_.interaction_seconds = stats_.m2l_seconds + stats_.p2p_seconds;
+    stats_.downward_seconds = stats_.l2l_seconds + stats_.l2p_seconds;
+  }
+}
+
+void Engine::sync() {
+  HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+void Engine::get_stats(hfmm_cuda_stats* out) {
+  stats_.device_bytes = device_bytes_counter();
+  *out = stats_;
+}
+
+void Engine::get_cells(uint32_t* out, size_t capacity) const {
+  require_points();
+  if (capacity < tree_.n_cells()) throw Error(HFMM_ERR_CONFIG, "cell buffer too small");
+  for (size_t c = 0; c < tree_.n_cells(); ++c) {
+    uint32_t* o = out + 8 * c;
+    o[0] = tree_.level[c]; o[1] = tree_.ix[c]; o[2] = tree_.iy[c]; o[3] = tree_.iz[c];
+    o[4] = tree_.body_first[c]; o[5] = tree_.body_count[c];
+    o[6] = tree_.child_first[c]; o[7] = tree_.child_count[c];
+  }
+}
+
+void Engine::get_body_order(uint32_t* out) const {
+  require_points();
+  std::copy(tree_.index.begin(), tree_.index.end(), out);
+}
+
+void Engine::get_pairs(int which, uint32_t* out, uint64_t* count) const {
+  require_points();
+  const auto& tt = which ? pairs_.p2p_t : pairs_.m2l_t;
+  const auto& ss = which ? pairs_.p2p_s : pairs_.m2l_s;
+  *count = tt.size();
+  if (!out) return;
+  for (size_t i = 0; i < tt.size(); ++i) {
+    out[2 * i] = tt[i];
+    out[2 * i + 1] = ss[i];
+  }
+}
+
+void Engine::get_expansions(int which, double* out) {
+  require_points();
+  HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  const int P = cfg_.order, dim = nm_total(P);
+  const size_t nc = tree_.n_cells();
+  std::fill(out, out + 2 * nc * size_t(dim), 0.0);
+  if (!have_far_) return;
+  std::vector<float2> host(nc * size_t(stride_));
+  (which ? local_ : multipole_).download(host.data(), host.size(), stream_);
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  // undo the level scaling: M = Mhat s^n/(2n+1)!!,  L = Lhat (2n-1)!!/s^n
+  for (size_t c = 0; c < nc; ++c) {
+    const long double s = (long double)cfg_.wave_r * tree_.side(tree_.level[c]);
+    for (int n = 0; n <= P; ++n) {
+      const long double f = which ? double_factorial(2 * n - 1) / powl(s, n)
+                                  : powl(s, n) / double_factorial(2 * n + 1);
+      for (int m = -n; m <= n; ++m) {
+        const float2 v = host[c * size_t(stride_) + nm_index(n, m)];
+        out[2 * (c * size_t(dim) + nm_index(n, m))] = double(f * v.x);
+        out[2 * (c * size_t(dim) + nm_index(n, m)) + 1] = double(f * v.y);
+      }
+    }
+  }
+}
+
+void compose_dense_from_tables(int order, double k, const double t[3], int kind, double s_src,
+                               double s_dst, double* out) {
+  using cd = std::complex<double>;
+  const int P = order, dim = nm_total(P);
+  const double r = std::sqrt(t[0] * t[0] + t[1] * t[1] + t[2] * t[2]);
+  const double rxy = std::sqrt(t[0] * t[0] + t[1] * t[1]);
+  const double cphi = rxy > 0 ? t[0] / rxy : 1.0, sphi = rxy > 0 ? t[1] / rxy : 0.0;
+  std::vector<float> rot(rot_table_size(P)), coax(size_t(coax_table_size(P)) * 2);
+  build_rotation_table(P, t[2] / r, rot.data());
+  const CoaxBuilder builder(P);
+  // kind 0: M2L with (s_src, s_dst); kind 1: regular shift expressed through the M2M scaling
+  builder.build(kind == 0 ? CoaxKind::m2l : CoaxKind::m2m, k, r, s_src, s_dst, coax.data());
+  std::vector<cd> ph(2 * P + 1);
+  for (int m = -P; m <= P; ++m) ph[m + P] = std::pow(cd(cphi, sphi), m);
+  // R[(n,m'),(n,m)] = E_n[m][m'] e^{i m phi};  Chat[(nu,m),(n,m)]
+  std::vector<cd> R(size_t(dim) * dim, 0), C(size_t(dim) * dim, 0);
+  for (int n = 0; n <= P; ++n) {
+    const int w = 2 * n + 1;
+    for (int m = -n; m <= n; ++m)
+      for (int mp = -n; mp <= n; ++mp)
+        R[size_t(nm_index(n, mp)) * dim + nm_index(n, m)] =
+            double(rot[rot_block_offset(n) + (m + n) * w + (mp + n)]) * ph[m + P];
+  }
+  for (int m = -P; m <= P; ++m) {
+    const int am = std::abs(m), w = P + 1 - am;
+    const float* blk = coax.data() + 2 * size_t(coax_block_offset(P, am));
+    for (int n = am; n <= P; ++n)
+      for (int nu = am; nu <= P; ++nu) {
+        const size_t e = size_t(n - am) * w + (nu - am);
+        // undo the scaling so the result is comparable with the reference's matrix
+        long double f;
+        if (kind == 0)
+          f = double_factorial(2 * nu - 1) * double_factorial(2 * n + 1) /
+              (powl(s_dst, nu) * powl(s_src, n));
+        else
+          f = powl(s_dst, nu) * double_factorial(2 * n + 1) /
+              (double_factorial(2 * nu + 1) * powl(s_src, n));
+        C[size_t(nm_index(nu, m)) * dim + nm_index(n, m)] =
+            cd(double(f * blk[2 * e]), double(f * blk[2 * e + 1]));
+      }
+  }
+  // T = R^H C R
+  std::vector<cd> CR(size_t(dim) * dim, 0);
+  for (int i = 0; i < dim; ++i)
+    for (int l = 0; l < dim; ++l) {
+      const cd c = C[size_t(i) * dim + l];
+      if (c == cd(0)) continue;
+      for (int j = 0; j < dim; ++j) CR[size_t(i) * dim + j] += c * R[size_t(l) * dim + j];
+    }
+  cd* T = reinterpret_cast<cd*>(out);
+  for (int i = 0; i < dim; ++i)
+    for (int j = 0; j < dim; ++j) {
+      cd s = 0;
+      for (int l = 0; l < dim; ++l) s += std::conj(R[size_t(l) * dim + i]) * CR[size_t(l) * dim + j];
+      T[size_t(i) * dim + j] = s;
+    }
+}
+
+}  // namespace hfmm_b200

@@ -1,0 +1,102 @@
+// engine.hpp — the handle behind the C ABI: owns the device-resident octree, interaction lists,
+// translation tables, expansions and streams, and orchestrates one FMM matvec
+// (reference fmm::execute_plan, src/traversal.cpp:208-279).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "device_utils.cuh"
+#include "host_tree.hpp"
+#include "kernels.cuh"
+
+namespace hfmm_b200 {
+
+struct TranslateStage {
+  // one batched-translation launch: M2L (all levels) or one level of M2M / L2L
+  DeviceBuffer<TranslateItem> items;
+  DeviceBuffer<TranslateClass> classes;
+  DeviceBuffer<uint32_t> pair_src, pair_dst;
+  uint32_t n_items = 0;
+  uint64_t n_pairs = 0;
+};
+
+class Engine {
+ public:
+  explicit Engine(const hfmm_cuda_config& cfg);
+  ~Engine();
+
+  void set_points(const double* xyz, size_t n);
+  void matvec_host(const double* q, double* out);
+  void matvec_device(const void* q_dev, void* out_dev);
+  void sync();
+  void get_stats(hfmm_cuda_stats* out);
+  void get_cells(uint32_t* out, size_t capacity) const;
+  void get_body_order(uint32_t* out) const;
+  void get_pairs(int which, uint32_t* out, uint64_t* count) const;
+  void get_expansions(int which, double* out);
+
+  std::string last_error;
+  const hfmm_cuda_config& config() const { return cfg_; }
+  uint32_t n_bodies() const { return tree_.n_bodies; }
+
+ private:
+  void require_points() const;
+  void run_far_and_near();  // body_q_ -> near_, far_
+  void build_translate_stages(const PairLists& pairs);
+  void upload_stage(TranslateStage& st, const std::vector<uint32_t>& src,
+                    const std::vector<uint32_t>& dst, const std::vector<uint32_t>& cls_of_pair,
+                    const std::vector<TranslateClass>& classes);
+
+  hfmm_cuda_config cfg_;
+  double leaf_cap_ = 0;
+  int threads_ = 1;
+  cudaStream_t stream_ = nullptr, stream_near_ = nullptr;
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+  std::vector<cudaEvent_t> ev_;  // phase timers
+
+  // host mirrors kept for introspection
+  TreeArrays tree_;
+  PairLists pairs_;
+  bool have_points_ = false;
+  hfmm_cuda_stats stats_{};
+
+  // device tree
+  DeviceBuffer<float4> body_pos_;
+  DeviceBuffer<uint32_t> body_index_;
+  DeviceBuffer<int4> cell_geom_;
+  DeviceBuffer<uint2> cell_body_;
+  DeviceBuffer<float> level_scale_;
+  std::vector<float> level_scale_host_;
+  // near field
+  DeviceBuffer<P2PTile> p2p_tiles_;
+  DeviceBuffer<uint32_t> p2p_offset_, p2p_src_;
+  uint32_t n_tiles_ = 0;
+  float kunit_ = 0;
+  // far field
+  int stride_ = 0;
+  int lmin_src_ = 0, lmin_dst_ = 0;
+  bool have_far_ = false;
+  DeviceBuffer<float2> multipole_, local_;
+  DeviceBuffer<uint32_t> p2m_leaves_, l2p_leaves_;
+  uint32_t n_p2m_leaves_ = 0, n_l2p_leaves_ = 0;
+  DeviceBuffer<float> rot_tables_, coax_tables_;
+  TranslateStage m2l_;
+  std::vector<TranslateStage> m2m_;  // deepest level first
+  std::vector<TranslateStage> l2l_;  // shallowest level first
+  // vectors
+  DeviceBuffer<float2> body_q_, near_, far_;
+  DeviceBuffer<double2> io64_;
+};
+
+// FP64 composition of the factored operator into a dense (P+1)^2 x (P+1)^2 matrix in the
+// reference's UNSCALED convention — used by the CPU-side table tests against
+// fmm::translation_matrix (expansion.cpp:95-124).  kind: 0 M2L (singular), 1 regular.
+void compose_dense_from_tables(int order, double k, const double t[3], int kind, double s_src,
+                               double s_dst, double* out_complex);
+
+}  // namespace hfmm_b200

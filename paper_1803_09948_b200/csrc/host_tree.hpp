@@ -1,0 +1,56 @@
+// host_tree.hpp — host C++ octree + dual-tree-traversal builder.
+//
+// Mirrors the semantics of the reference's build_tree (src/octree.cpp:53-182) and
+// dual_tree_traversal (src/traversal.cpp:36-97) — same box, same level-21 Morton keys, same split
+// rule, same admissibility and split-larger-cell rule, hence the same cell set and the same
+// (target, source) pair sets — but lays the tree out LEVEL BY LEVEL (cells of one level are
+// contiguous and key-sorted, siblings adjacent), the layout the device passes want, and walks the
+// two trees as a breadth-first pair frontier instead of a recursion.  This is the
+// HFMM_FLAG_HOST_TREE path; the device builder (tree_build.cu) produces the same arrays.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+namespace hfmm_b200 {
+
+struct TreeArrays {
+  double lo[3] = {0, 0, 0};
+  double width = 0;
+  uint32_t n_bodies = 0;
+  int max_level = 0;
+  size_t degenerate_leaves = 0;
+
+  std::vector<uint64_t> key;    // level-21 key per Morton slot
+  std::vector<uint32_t> index;  // Morton slot -> caller index (Body::index)
+
+  // cells, level order; cell 0 is the root
+  std::vector<uint8_t> level;
+  std::vector<uint32_t> ix, iy, iz;
+  std::vector<uint32_t> body_first, body_count;
+  std::vector<uint32_t> child_first, child_count;
+  std::vector<uint32_t> parent;
+  std::vector<uint32_t> level_offset;  // cells of level L are [level_offset[L], level_offset[L+1])
+  std::vector<uint32_t> leaves;        // ascending cell index
+
+  size_t n_cells() const { return level.size(); }
+  double side(int lvl) const { return width / double(uint64_t(1) << lvl); }
+};
+
+struct PairLists {
+  // admissible cell pairs (M2L) and leaf pairs (P2P), as flat (target, source) arrays
+  std::vector<uint32_t> m2l_t, m2l_s, p2p_t, p2p_s;
+};
+
+// level-21 key of p inside the cubified box (octree.cpp:25-51); throws Error(HFMM_ERR_DOMAIN)
+uint64_t morton_key21(const double p[3], const double lo[3], double width);
+
+// throws Error(HFMM_ERR_CONFIG) on n == 0 / ncrit < 1
+void build_tree_host(TreeArrays& tree, const double* xyz, size_t n, int ncrit, double leaf_cap,
+                     int threads);
+
+void dual_tree_traversal_host(const TreeArrays& tree, double kmag, double theta, double kd_max,
+                              PairLists& out, int threads);
+
+}  // namespace hfmm_b200

@@ -1,0 +1,99 @@
+// kernels.cuh — device data layout and launcher declarations of the hand-written sm_100a kernels.
+//
+// HBM layout (all arrays Morton / level ordered, structure-of-arrays):
+//   body_pos[slot]   float4  k * (x - centre(leaf(slot)))            leaf-relative, pre-scaled by k
+//   body_q[slot]     float2  charge of the current matvec (x[index] * far_weight[index])
+//   cell_geom[cell]  int4    (cx, cy, cz, level): lattice centre in half-sides of the finest level
+//   cell_body[cell]  uint2   (body_first, body_count)
+//   multipole/local  float2  [cell][coeff_stride(P)]  level-scaled coefficients (tables.hpp)
+// Leaf-relative positions keep x_i - x_j accurate to ~1e-9 (absolute FP32 coordinates in a box of
+// width 2 would cost 1e-7/|x_i-x_j| relative error on the nearest pairs).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace hfmm_b200 {
+
+// ---- P2P (near field, reference traversal.cpp:175-204 + kernel.hpp:16-23) --------------------
+struct P2PTile {
+  uint32_t leaf;      // target leaf cell id
+  uint32_t body_off;  // first target body of this tile, relative to the leaf's body_first
+  uint32_t n_t;       // targets in the tile (<= 32)
+  uint32_t list;      // index into p2p_offset (source leaves of `leaf`, self excluded)
+};
+
+struct P2PArgs {
+  const P2PTile* tiles;
+  uint32_t n_tiles;
+  const uint32_t* p2p_offset;  // CSR over target leaves
+  const uint32_t* p2p_src;     // source leaf cell ids (never the target leaf itself)
+  const int4* cell_geom;
+  const uint2* cell_body;
+  const float4* body_pos;
+  const float2* body_q;
+  float2* out;       // per Morton slot, overwritten (every body belongs to exactly one tile)
+  float kunit;       // k * half-side of the finest level: lattice units -> scaled coordinates
+  float out_scale;   // k / (4 pi)
+};
+void launch_p2p(const P2PArgs& a, cudaStream_t s);
+
+// ---- P2M / L2P (reference expansion.cpp:157-175, 283-300) -----------------------------------
+struct LeafExpansionArgs {
+  const uint32_t* leaves;  // leaf cell ids to process
+  uint32_t n_leaves;
+  const int4* cell_geom;
+  const uint2* cell_body;
+  const float4* body_pos;
+  const float* level_scale;  // s_l = k * side(l), indexed by level
+  int order;
+  int stride;                // coefficient row stride (complex elements)
+  float k;                   // real wavenumber
+};
+void launch_p2m(const LeafExpansionArgs& a, const float2* body_q, float2* multipole, cudaStream_t s);
+// out[slot] = sum over the leaf's local expansion (overwrites; bodies of unlisted leaves untouched)
+void launch_l2p(const LeafExpansionArgs& a, const float2* local, float2* out, cudaStream_t s);
+// Legendre recurrence coefficients -> __constant__ memory (tables.hpp build_legendre_coefficients)
+void upload_legendre_constants(const float* diag, const float* sub, const float* a, const float* b,
+                               int order);
+
+// ---- batched translation: M2M / M2L / L2L (reference expansion.cpp:95-139) -------------------
+struct TranslateClass {
+  uint32_t rot;   // rotation table id
+  uint32_t coax;  // coaxial table id
+  float cphi, sphi;
+};
+struct TranslateItem {
+  uint32_t pair_begin;
+  uint32_t count;  // <= kTranslateBatch pairs, all of one class
+  uint32_t cls;
+  uint32_t pad;
+};
+inline constexpr int kTranslateBatch = 32;
+
+struct TranslateArgs {
+  const TranslateItem* items;
+  uint32_t n_items;
+  const TranslateClass* classes;
+  const uint32_t* pair_src;
+  const uint32_t* pair_dst;
+  const float* rot_tables;   // [rot][rot_table_size(P)]
+  const float* coax_tables;  // [coax][2 * coax_table_size(P)]
+  const float2* src;         // expansions read
+  float2* dst;               // expansions accumulated into (atomically)
+  int order;
+  int stride;
+};
+void launch_translate(const TranslateArgs& a, cudaStream_t s);
+
+// ---- vector plumbing -------------------------------------------------------------------------
+// body_q[slot] = float2(q[index[slot]]) * weight[index[slot]] (weight may be null)
+void launch_gather_charges(const double2* q_caller, const float2* q_caller_f32,
+                           const uint32_t* index, const float* weight, float2* body_q, uint32_t n,
+                           cudaStream_t s);
+// out[index[slot]] = near[slot] + far[slot]; exactly one of out_f64 / out_f32 is written
+void launch_scatter_potentials(const float2* near, const float2* far, const uint32_t* index,
+                               double2* out_f64, float2* out_f32, uint32_t n, cudaStream_t s);
+
+}  // namespace hfmm_b200

@@ -1,0 +1,272 @@
+// kernels_expansion.cu — P2M and L2P on level-scaled FP32 expansions (sm_100a).
+//
+// Replaces reference p2m (src/expansion.cpp:157-175) and the L2P half of compute_locals
+// (src/expansion.cpp:283-300):
+//   M_n^m  = sum_b (i k q_b) j_n(k rho_b) conj Y_n^m(rho_b^)
+//   trg_b += sum_{n,m} L_n^m j_n(k |x_b|) Y_n^m(x_b^)
+// in the scaled basis of tables.hpp:  Mhat = M (2n+1)!!/s^n,  Lhat = L s^n/(2n-1)!!,  with the
+// scaled radial function  jhat_n(z; s) = j_n(z) (2n+1)!!/s^n = (z/s)^n * S_n(z^2),
+//   S_n(z^2) = sum_j (-z^2/2)^j / (j! (2n+3)(2n+5)...(2n+2j+1))      (special.cpp:18-34's series)
+// which is O(1) for every body of a leaf (z/s = rho/side <= sqrt(3)/2) at any depth of the tree.
+// Y_n^m uses the reference's orthonormal Legendre recurrences (special.cpp:80-112) in FP32.
+//
+// One warp per leaf; lanes are bodies.  P2M reduces each coefficient across lanes with shuffles;
+// L2P needs no reduction.
+#include "device_utils.cuh"
+#include "kernels.cuh"
+#include "tables.hpp"
+
+namespace hfmm_b200 {
+
+namespace {
+
+constexpr int kWarps = 4;
+constexpr int kMaxP = kMaxOrder;
+constexpr float kInvSqrt4Pi = 0.28209479177387814f;
+
+__constant__ float c_diag[kMaxP + 1];
+__constant__ float c_sub[kMaxP + 1];
+__constant__ float c_a[(kMaxP + 1) * (kMaxP + 2) / 2];
+__constant__ float c_b[(kMaxP + 1) * (kMaxP + 2) / 2];
+
+// jhat_n(z; s), n = 0..P, written to out[n * 32] (one shared-memory column per lane)
+__device__ void scaled_bessel(int P, float z, float s, float* out) {
+  if (z <= 2.0f) {
+    const float h = -0.5f * z * z;
+    const float t = z / s;
+    float tp = 1.0f;
+    for (int n = 0; n <= P; ++n) {
+      float term = 1.0f, sum = 1.0f;
+#pragma unroll 4
+      for (int j = 1; j <= 12; ++j) {
+        term *= h / float(j * (2 * n + 2 * j + 1));
+        sum += term;
+      }
+      out[n * 32] = tp * sum;
+      tp *= t;
+    }
+    return;
+  }
+  // beyond the low-frequency regime (only reachable with the kd gate off): Miller's downward
+  // recurrence in FP64, normalised by j_0 = sin z / z (special.cpp:36-53)
+  const double zd = z;
+  const int start = P + 24 + int(zd);
+  double above = 0.0, cur = 1e-280;
+  double keep[kMaxP + 1];
+  for (int n = start; n >= 0; --n) {
+    const double below = (2.0 * n + 3.0) / zd * cur - above;
+    above = cur;
+    cur = below;
+    if (n <= P) keep[n] = cur;
+    if (fabs(cur) > 1e250) {
+      cur *= 1e-250;
+      above *= 1e-250;
+      for (int i = n < P ? n : P; i <= P; ++i) keep[i] *= 1e-250;
+    }
+  }
+  const double scale = (sin(zd) / zd) / cur;
+  double f = 1.0;  // (2n+1)!!/s^n
+  for (int n = 0; n <= P; ++n) {
+    out[n * 32] = float(keep[n] * scale * f);
+    f *= (2.0 * n + 3.0) / double(s);
+  }
+}
+
+struct BodyFrame {
+  float ct, st, cphi, sphi, z;
+};
+
+__device__ __forceinline__ BodyFrame body_frame(const float4 p) {
+  BodyFrame f;
+  const float rxy2 = p.x * p.x + p.y * p.y;
+  const float r2 = rxy2 + p.z * p.z;
+  f.z = sqrtf(r2);
+  const float rxy = sqrtf(rxy2);
+  if (r2 > 0.0f) {
+    f.ct = p.z / f.z;
+    f.st = rxy / f.z;
+  } else {
+    f.ct = 1.0f;
+    f.st = 0.0f;
+  }
+  if (rxy2 > 0.0f) {
+    f.cphi = p.x / rxy;
+    f.sphi = p.y / rxy;
+  } else {  // atan2(0, 0) = 0 in the reference
+    f.cphi = 1.0f;
+    f.sphi = 0.0f;
+  }
+  return f;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(kWarps * 32)
+p2m_kernel(const LeafExpansionArgs a, const float2* __restrict__ body_q, float2* __restrict__ multipole) {
+  extern __shared__ float smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int P = a.order, dim = (P + 1) * (P + 1);
+  float* s_j = smem + warp * ((P + 1) * 32 + 2 * dim);  // [n][lane]
+  float2* s_acc = reinterpret_cast<float2*>(s_j + (P + 1) * 32);
+  const uint32_t li = blockIdx.x * kWarps + warp;
+  if (li >= a.n_leaves) return;
+  const uint32_t cell = a.leaves[li];
+  const uint2 cb = a.cell_body[cell];
+  const float s = a.level_scale[a.cell_geom[cell].w];
+  for (int i = lane; i < dim; i += 32) s_acc[i] = make_float2(0.f, 0.f);
+  __syncwarp();
+
+  for (uint32_t base = 0; base < cb.y; base += 32) {
+    const bool ok = base + lane < cb.y;
+    const float4 p = ok ? a.body_pos[cb.x + base + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float2 q = ok ? body_q[cb.x + base + lane] : make_float2(0.f, 0.f);
+    const BodyFrame f = body_frame(p);
+    scaled_bessel(P, f.z, s, s_j + lane);
+    // w = i k q
+    const float wr = -a.k * q.y, wi = a.k * q.x;
+    float cm = 1.0f, sm = 0.0f;     // cos(m phi), sin(m phi)
+    float pmm = kInvSqrt4Pi;        // Pbar_m^m
+    for (int m = 0; m <= P; ++m) {
+      if (m > 0) {
+        pmm *= c_diag[m] * f.st;
+        const float c2 = cm * f.cphi - sm * f.sphi;
+        sm = sm * f.cphi + cm * f.sphi;
+        cm = c2;
+      }
+      float p2 = 0.0f, p1 = pmm;  // Pbar_{n-2}^m, Pbar_{n-1}^m
+      for (int n = m; n <= P; ++n) {
+        float pn;
+        if (n == m) pn = pmm;
+        else if (n == m + 1) pn = c_sub[m] * f.ct * pmm;
+        else pn = c_a[n * (n + 1) / 2 + m] * f.ct * p1 - c_b[n * (n + 1) / 2 + m] * p2;
+        p2 = p1;
+        p1 = pn;
+        const float g = s_j[n * 32 + lane] * pn;
+        // +m: conj Y = Pbar (cm - i sm)
+        float vr = g * (wr * cm + wi * sm), vi = g * (wi * cm - wr * sm);
+        vr = warp_sum(vr);
+        vi = warp_sum(vi);
+        if (lane == 0) {
+          float2& d = s_acc[n * (n + 1) + m];
+          d.x += vr;
+          d.y += vi;
+        }
+        if (m > 0) {
+          // -m: conj Y_n^{-m} = (-1)^m Pbar (cm + i sm)
+          const float sg = (m & 1) ? -g : g;
+          float ur = sg * (wr * cm - wi * sm), ui = sg * (wi * cm + wr * sm);
+          ur = warp_sum(ur);
+          ui = warp_sum(ui);
+          if (lane == 0) {
+            float2& d = s_acc[n * (n + 1) - m];
+            d.x += ur;
+            d.y += ui;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  __syncwarp();
+  float2* dst = multipole + size_t(cell) * a.stride;
+  for (int i = lane; i < dim; i += 32) dst[i] = s_acc[i];
+}
+
+__global__ void __launch_bounds__(kWarps * 32)
+l2p_kernel(const LeafExpansionArgs a, const float2* __restrict__ local, float2* __restrict__ out) {
+  extern __shared__ float smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int P = a.order, dim = (P + 1) * (P + 1);
+  float* s_j = smem + warp * ((P + 1) * 32 + 2 * dim);
+  float2* s_loc = reinterpret_cast<float2*>(s_j + (P + 1) * 32);
+  const uint32_t li = blockIdx.x * kWarps + warp;
+  if (li >= a.n_leaves) return;
+  const uint32_t cell = a.leaves[li];
+  const uint2 cb = a.cell_body[cell];
+  const float s = a.level_scale[a.cell_geom[cell].w];
+  const float2* src = local + size_t(cell) * a.stride;
+  for (int i = lane; i < dim; i += 32) s_loc[i] = src[i];
+  __syncwarp();
+
+  for (uint32_t base = 0; base < cb.y; base += 32) {
+    const bool ok = base + lane < cb.y;
+    const float4 p = ok ? a.body_pos[cb.x + base + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const BodyFrame f = body_frame(p);
+    scaled_bessel(P, f.z, s, s_j + lane);
+    float accr = 0.0f, acci = 0.0f;
+    float cm = 1.0f, sm = 0.0f, pmm = kInvSqrt4Pi;
+    for (int m = 0; m <= P; ++m) {
+      if (m > 0) {
+        pmm *= c_diag[m] * f.st;
+        const float c2 = cm * f.cphi - sm * f.sphi;
+        sm = sm * f.cphi + cm * f.sphi;
+        cm = c2;
+      }
+      float p2 = 0.0f, p1 = pmm;
+      float sr = 0.0f, si = 0.0f;  // sum over n of g * (L^m, L^-m combination)
+      for (int n = m; n <= P; ++n) {
+        float pn;
+        if (n == m) pn = pmm;
+        else if (n == m + 1) pn = c_sub[m] * f.ct * pmm;
+        else pn = c_a[n * (n + 1) / 2 + m] * f.ct * p1 - c_b[n * (n + 1) / 2 + m] * p2;
+        p2 = p1;
+        p1 = pn;
+        // Lhat pairs with j_n (2n-1)!!/s^n = jhat_n / (2n+1)
+        const float g = s_j[n * 32 + lane] * pn / float(2 * n + 1);
+        const float2 lp = s_loc[n * (n + 1) + m];
+        if (m == 0) {
+          sr += g * lp.x;
+          si += g * lp.y;
+        } else {
+          const float2 lm = s_loc[n * (n + 1) - m];
+          const float sg = (m & 1) ? -1.0f : 1.0f;
+          // L^m (cm + i sm) + (-1)^m L^-m (cm - i sm)
+          const float er = lp.x + sg * lm.x, ei = lp.y + sg * lm.y;   // multiplies cm
+          const float dr = lp.x - sg * lm.x, di = lp.y - sg * lm.y;   // multiplies i sm
+          sr += g * (er * cm - di * sm);
+          si += g * (ei * cm + dr * sm);
+        }
+      }
+      accr += sr;
+      acci += si;
+    }
+    if (ok) out[cb.x + base + lane] = make_float2(accr, acci);
+    __syncwarp();
+  }
+}
+
+size_t leaf_smem_bytes(int order) {
+  const int dim = (order + 1) * (order + 1);
+  return size_t(kWarps) * ((order + 1) * 32 + 2 * dim) * sizeof(float);
+}
+
+}  // namespace
+
+void upload_legendre_constants(const float* diag, const float* sub, const float* a, const float* b,
+                               int order) {
+  const size_t tri = size_t(order + 1) * (order + 2) / 2;
+  HFMM_CUDA_CHECK(cudaMemcpyToSymbol(c_diag, diag, sizeof(float) * (order + 1)));
+  HFMM_CUDA_CHECK(cudaMemcpyToSymbol(c_sub, sub, sizeof(float) * (order + 1)));
+  HFMM_CUDA_CHECK(cudaMemcpyToSymbol(c_a, a, sizeof(float) * tri));
+  HFMM_CUDA_CHECK(cudaMemcpyToSymbol(c_b, b, sizeof(float) * tri));
+}
+
+void launch_p2m(const LeafExpansionArgs& a, const float2* body_q, float2* multipole, cudaStream_t s) {
+  if (a.n_leaves == 0) return;
+  const uint32_t blocks = (a.n_leaves + kWarps - 1) / kWarps;
+  p2m_kernel<<<blocks, kWarps * 32, leaf_smem_bytes(a.order), s>>>(a, body_q, multipole);
+  HFMM_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_l2p(const LeafExpansionArgs& a, const float2* local, float2* out, cudaStream_t s) {
+  if (a.n_leaves == 0) return;
+  const uint32_t blocks = (a.n_leaves + kWarps - 1) / kWarps;
+  l2p_kernel<<<blocks, kWarps * 32, leaf_smem_bytes(a.order), s>>>(a, local, out);
+  HFMM_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace hfmm_b200
