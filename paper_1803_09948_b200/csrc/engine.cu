@@ -300,10 +300,16 @@ void Engine::set_points(const double* xyz, size_t n) {
   }
   level_scale_host_.assign(kMaxLevel + 1, 0.f);
   for (int l = 0; l <= kMaxLevel; ++l) level_scale_host_[l] = float(k * t.side(l));
-  kunit_ = float(k * t.side(Lf) / 2);
+  kunit_d_ = k * t.side(Lf) / 2;
+  kunit_ = float(kunit_d_);
 
-  // bodies: leaf-relative, pre-scaled by k
-  std::vector<float4> pos(n);
+  // bodies: leaf-relative, pre-scaled by k; plus the hi/lo split on a power-of-two grid used for
+  // touching leaves (kernels.cuh).  Every hi value, hi offset and hi difference between touching
+  // leaves stays below 2^23 grid units, hence exactly representable in FP32.
+  double max_leaf_side = 0;
+  for (uint32_t c : t.leaves) max_leaf_side = std::max(max_leaf_side, t.side(t.level[c]));
+  grid_ = std::ldexp(1.0, int(std::ceil(std::log2(4.0 * k * max_leaf_side))) - 23);
+  std::vector<float4> pos(n), pos_hi(n), pos_lo(n);
   parallel_for(t.leaves.size(), threads_, [&](size_t li) {
     const uint32_t c = t.leaves[li];
     const double s = t.side(t.level[c]);
@@ -311,34 +317,50 @@ void Engine::set_points(const double* xyz, size_t n) {
                  cz = t.lo[2] + (t.iz[c] + 0.5) * s;
     for (uint32_t b = t.body_first[c]; b < t.body_first[c] + t.body_count[c]; ++b) {
       const double* p = xyz + 3 * size_t(t.index[b]);
-      pos[b] = make_float4(float(k * (p[0] - cx)), float(k * (p[1] - cy)), float(k * (p[2] - cz)), 0.f);
+      const double v[3] = {k * (p[0] - cx), k * (p[1] - cy), k * (p[2] - cz)};
+      double h[3];
+      for (int a = 0; a < 3; ++a) h[a] = std::rint(v[a] / grid_) * grid_;
+      pos[b] = make_float4(float(v[0]), float(v[1]), float(v[2]), 0.f);
+      pos_hi[b] = make_float4(float(h[0]), float(h[1]), float(h[2]), 0.f);
+      pos_lo[b] = make_float4(float(v[0] - h[0]), float(v[1] - h[1]), float(v[2] - h[2]), 0.f);
     }
   });
 
-  // near field: CSR by target leaf without the self pair (handled by the kernel's masked pass)
+  // near field: CSR by target leaf, touching source leaves (self included) first
   const size_t nleaf = t.leaves.size();
   std::vector<uint32_t> leaf_slot(nc, 0xffffffffu);
   for (size_t i = 0; i < nleaf; ++i) leaf_slot[t.leaves[i]] = uint32_t(i);
-  std::vector<uint32_t> off(nleaf + 1, 0);
+  auto touching = [&](uint32_t a, uint32_t b) {
+    const int64_t ha = int64_t(1) << (Lf - t.level[a]), hb = int64_t(1) << (Lf - t.level[b]);
+    return std::llabs(int64_t(geom[a].x) - geom[b].x) <= ha + hb &&
+           std::llabs(int64_t(geom[a].y) - geom[b].y) <= ha + hb &&
+           std::llabs(int64_t(geom[a].z) - geom[b].z) <= ha + hb;
+  };
+  std::vector<uint32_t> off(nleaf + 1, 0), split(nleaf, 0);
   uint64_t body_pairs = 0;
   for (size_t e = 0; e < pairs_.p2p_t.size(); ++e) {
     const uint32_t a = pairs_.p2p_t[e], b = pairs_.p2p_s[e];
     body_pairs += uint64_t(t.body_count[a]) * t.body_count[b];
-    if (a != b) ++off[leaf_slot[a] + 1];
+    ++off[leaf_slot[a] + 1];
+    if (touching(a, b)) ++split[leaf_slot[a]];
   }
   for (size_t i = 0; i < nleaf; ++i) off[i + 1] += off[i];
+  for (size_t i = 0; i < nleaf; ++i) split[i] += off[i];
   std::vector<uint32_t> srcs(off[nleaf]);
   std::vector<uint64_t> work(nleaf, 0);
   {
-    std::vector<uint32_t> cur(off.begin(), off.end() - 1);
+    std::vector<uint32_t> cur_touch(off.begin(), off.end() - 1), cur_far(split);
     for (size_t e = 0; e < pairs_.p2p_t.size(); ++e) {
       const uint32_t a = pairs_.p2p_t[e], b = pairs_.p2p_s[e];
       work[leaf_slot[a]] += t.body_count[b];
-      if (a != b) srcs[cur[leaf_slot[a]]++] = b;
+      srcs[touching(a, b) ? cur_touch[leaf_slot[a]]++ : cur_far[leaf_slot[a]]++] = b;
     }
   }
   // source leaves in ascending cell order: neighbouring bodies, neighbouring addresses
-  parallel_for(nleaf, threads_, [&](size_t i) { std::sort(srcs.begin() + off[i], srcs.begin() + off[i + 1]); });
+  parallel_for(nleaf, threads_, [&](size_t i) {
+    std::sort(srcs.begin() + off[i], srcs.begin() + split[i]);
+    std::sort(srcs.begin() + split[i], srcs.begin() + off[i + 1]);
+  });
   std::vector<P2PTile> tiles;
   std::vector<uint64_t> tile_work;
   for (size_t i = 0; i < nleaf; ++i) {
@@ -361,6 +383,9 @@ void Engine::set_points(const double* xyz, size_t n) {
   n_tiles_ = uint32_t(tiles.size());
 
   body_pos_.upload(pos, stream_);
+  body_hi_.upload(pos_hi, stream_);
+  body_lo_.upload(pos_lo, stream_);
+  p2p_split_.upload(split, stream_);
   body_index_.upload(t.index, stream_);
   cell_geom_.upload(geom, stream_);
   cell_body_.upload(cbody, stream_);
@@ -423,7 +448,12 @@ void Engine::run_far_and_near() {
   pa.tiles = p2p_tiles_.get();
   pa.n_tiles = n_tiles_;
   pa.p2p_offset = p2p_offset_.get();
+  pa.p2p_split = p2p_split_.get();
   pa.p2p_src = p2p_src_.get();
+  pa.body_hi = body_hi_.get();
+  pa.body_lo = body_lo_.get();
+  pa.kunit_d = kunit_d_;
+  pa.grid = grid_;
   pa.cell_geom = cell_geom_.get();
   pa.cell_body = cell_body_.get();
   pa.body_pos = body_pos_.get();

@@ -66,7 +66,7 @@ class Engine {
   hfmm_cuda_stats stats_{};
 
   // device tree
-  DeviceBuffer<float4> body_pos_;
+  DeviceBuffer<float4> body_pos_, body_hi_, body_lo_;
   DeviceBuffer<uint32_t> body_index_;
   DeviceBuffer<int4> cell_geom_;
   DeviceBuffer<uint2> cell_body_;
@@ -74,9 +74,10 @@ class Engine {
   std::vector<float> level_scale_host_;
   // near field
   DeviceBuffer<P2PTile> p2p_tiles_;
-  DeviceBuffer<uint32_t> p2p_offset_, p2p_src_;
+  DeviceBuffer<uint32_t> p2p_offset_, p2p_split_, p2p_src_;
   uint32_t n_tiles_ = 0;
   float kunit_ = 0;
+  double kunit_d_ = 0, grid_ = 1;
   // far field
   int stride_ = 0;
   int lmin_src_ = 0, lmin_dst_ = 0;

@@ -6,8 +6,14 @@
 //   cell_geom[cell]  int4    (cx, cy, cz, level): lattice centre in half-sides of the finest level
 //   cell_body[cell]  uint2   (body_first, body_count)
 //   multipole/local  float2  [cell][coeff_stride(P)]  level-scaled coefficients (tables.hpp)
+//   body_hi/body_lo  float4  the same coordinate split as hi + lo (hi on a power-of-two grid)
 // Leaf-relative positions keep x_i - x_j accurate to ~1e-9 (absolute FP32 coordinates in a box of
 // width 2 would cost 1e-7/|x_i-x_j| relative error on the nearest pairs).
+// That is still not enough for the closest pairs of a random set (1e3..1e6 times closer than the
+// mean spacing, and dominating the L2 norm of the potential): bodies of touching leaves are
+// therefore differenced as (hi_t - hi_s - o_hi) + (lo_t - lo_s - o_lo), the first bracket exact,
+// which gives x_i - x_j to FP32 RELATIVE accuracy — what the reference's Precision::f32 path gets
+// by differencing in FP64 before it narrows (kernel.hpp:18).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -27,14 +33,23 @@ struct P2PTile {
 struct P2PArgs {
   const P2PTile* tiles;
   uint32_t n_tiles;
-  const uint32_t* p2p_offset;  // CSR over target leaves
-  const uint32_t* p2p_src;     // source leaf cell ids (never the target leaf itself)
+  // CSR over target leaves.  Entries [offset[i], split[i]) are the TOUCHING source leaves (cubes
+  // share a face, edge or corner, the target leaf itself included): they can hold arbitrarily
+  // close body pairs and are evaluated with compensated coordinates.  [split[i], offset[i+1]) are
+  // the remaining source leaves (at least one cell apart), evaluated with plain FP32 coordinates.
+  const uint32_t* p2p_offset;
+  const uint32_t* p2p_split;
+  const uint32_t* p2p_src;     // source leaf cell ids
   const int4* cell_geom;
   const uint2* cell_body;
-  const float4* body_pos;
+  const float4* body_pos;      // float(k * x_rel)
+  const float4* body_hi;       // k * x_rel rounded to the grid `grid`
+  const float4* body_lo;       // k * x_rel - hi  (|lo| <= grid/2)
   const float2* body_q;
   float2* out;       // per Morton slot, overwritten (every body belongs to exactly one tile)
   float kunit;       // k * half-side of the finest level: lattice units -> scaled coordinates
+  double kunit_d;    // the same in FP64 (exact offsets for the compensated path)
+  double grid;       // power of two; hi parts and hi offsets are integer multiples of it
   float out_scale;   // k / (4 pi)
 };
 void launch_p2p(const P2PArgs& a, cudaStream_t s);

@@ -12,10 +12,13 @@
 //   * one warp-shuffle reduction per target at the very end.
 // Coordinates arrive pre-scaled by k and leaf-relative; the lattice offset between the two leaf
 // centres is added per source body.  G = (k/4pi) e^{iR'}/R' with R' = kR, the constant applied once
-// at the store.  Per pair: 3 FADD, 3 FFMA (R'^2), MUFU.RSQ, FMUL (R'), FMUL+MUFU.SIN, MUFU.COS,
-// 2 FMUL, 4 FFMA.  The self leaf needs the R == 0 mask and is a separate pass; all other leaves
-// cannot hold coincident bodies (same key => same leaf) and run unmasked with a 1e-30 floor that
-// only guards against NaN.
+// at the store.  Per pair (plain path): 3 FADD, 3 FFMA (R'^2), MUFU.RSQ, FMUL (R'), FMUL+MUFU.SIN,
+// MUFU.COS, 2 FMUL, 4 FFMA.
+//
+// Two passes per tile (kernels.cuh, P2PArgs):
+//   touching leaves (self included): compensated hi/lo coordinates, R == 0 masked — coincident
+//     bodies share a key, hence a leaf, so the mask is only ever needed here;
+//   all other leaves: plain FP32 coordinates, unmasked, a 1e-30 floor only guards against NaN.
 #include "device_utils.cuh"
 #include "kernels.cuh"
 
@@ -42,18 +45,8 @@ __device__ __forceinline__ float cos_approx(float x) {
   return y;
 }
 
-template <bool kMasked>
-__device__ __forceinline__ void pair_eval(const float4 t, float sx, float sy, float sz, float qr,
-                                          float qi, float& ar, float& ai) {
-  const float dx = t.x - sx, dy = t.y - sy, dz = t.z - sz;
-  float r2, rinv;
-  if (kMasked) {
-    r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-    rinv = r2 > 0.0f ? rsqrt_approx(r2) : 0.0f;
-  } else {
-    r2 = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, 1e-30f)));
-    rinv = rsqrt_approx(r2);
-  }
+__device__ __forceinline__ void green_accumulate(float r2, float rinv, float qr, float qi,
+                                                 float& ar, float& ai) {
   const float r = r2 * rinv;
   const float gr = rinv * cos_approx(r), gi = rinv * sin_approx(r);
   ar = fmaf(gr, qr, ar);
@@ -62,21 +55,76 @@ __device__ __forceinline__ void pair_eval(const float4 t, float sx, float sy, fl
   ai = fmaf(gi, qr, ai);
 }
 
-template <bool kMasked>
-__device__ __forceinline__ void accumulate_tile(const float4* __restrict__ tgt, uint32_t n_t,
-                                                float sx, float sy, float sz, float qr, float qi,
-                                                float (&ar)[kTile], float (&ai)[kTile]) {
+// plain path: one FP32 coordinate per axis
+__device__ __forceinline__ void accumulate_plain(const float4* __restrict__ tgt, uint32_t n_t,
+                                                 float sx, float sy, float sz, float qr, float qi,
+                                                 float (&ar)[kTile], float (&ai)[kTile]) {
 #pragma unroll
   for (int t = 0; t < kTile; ++t) {
     if (t < n_t) {  // warp-uniform
       const float4 tp = tgt[t];
-      pair_eval<kMasked>(tp, sx, sy, sz, qr, qi, ar[t], ai[t]);
+      const float dx = tp.x - sx, dy = tp.y - sy, dz = tp.z - sz;
+      const float r2 = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, 1e-30f)));
+      green_accumulate(r2, rsqrt_approx(r2), qr, qi, ar[t], ai[t]);
     }
   }
 }
 
+// compensated path: d = (hi_t - hi_s) + (lo_t - lo_s); the hi difference is exact (grid multiples)
+__device__ __forceinline__ void accumulate_compensated(const float4* __restrict__ thi,
+                                                       const float4* __restrict__ tlo, uint32_t n_t,
+                                                       float hx, float hy, float hz, float lx,
+                                                       float ly, float lz, float qr, float qi,
+                                                       float (&ar)[kTile], float (&ai)[kTile]) {
+#pragma unroll
+  for (int t = 0; t < kTile; ++t) {
+    if (t < n_t) {
+      const float4 th = thi[t], tl = tlo[t];
+      const float dx = (th.x - hx) + (tl.x - lx);
+      const float dy = (th.y - hy) + (tl.y - ly);
+      const float dz = (th.z - hz) + (tl.z - lz);
+      const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+      const float rinv = r2 > 0.0f ? rsqrt_approx(r2) : 0.0f;
+      green_accumulate(r2, rinv, qr, qi, ar[t], ai[t]);
+    }
+  }
+}
+
+struct LeafGroup {
+  // one lane = one source leaf of a group of up to 32
+  uint32_t first, count, incl, excl;
+};
+
+__device__ __forceinline__ LeafGroup scan_group(uint2 sb, int lane) {
+  LeafGroup g;
+  g.first = sb.x;
+  g.count = sb.y;
+  uint32_t incl = sb.y;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  g.incl = incl;
+  g.excl = incl - sb.y;
+  return g;
+}
+
+// lane-local: which leaf of the group owns flattened body index g (first lane with incl > g)
+__device__ __forceinline__ int owner_of(uint32_t incl, uint32_t g) {
+  int j = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1) {
+    const uint32_t v = __shfl_sync(0xffffffffu, incl, j + step - 1);
+    if (v <= g) j += step;
+  }
+  return j;
+}
+
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) p2p_kernel(const P2PArgs a) {
   __shared__ float4 s_tgt[kWarpsPerBlock][kTile];
+  __shared__ float4 s_thi[kWarpsPerBlock][kTile];
+  __shared__ float4 s_tlo[kWarpsPerBlock][kTile];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t tile_id = blockIdx.x * kWarpsPerBlock + warp;
   if (tile_id >= a.n_tiles) return;
@@ -84,26 +132,58 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) p2p_kernel(const P2PArgs 
   const int4 tg = a.cell_geom[tile.leaf];
   const uint2 tb = a.cell_body[tile.leaf];
   const uint32_t tslot = tb.x + tile.body_off + lane;
-  s_tgt[warp][lane] = lane < tile.n_t ? a.body_pos[tslot] : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  s_tgt[warp][lane] = lane < tile.n_t ? a.body_pos[tslot] : zero4;
+  s_thi[warp][lane] = lane < tile.n_t ? a.body_hi[tslot] : zero4;
+  s_tlo[warp][lane] = lane < tile.n_t ? a.body_lo[tslot] : zero4;
   __syncwarp();
-  const float4* tgt = s_tgt[warp];
 
   float ar[kTile], ai[kTile];
 #pragma unroll
   for (int t = 0; t < kTile; ++t) ar[t] = ai[t] = 0.0f;
 
-  // self leaf: same frame, coincident pairs masked
-  for (uint32_t base = 0; base < tb.y; base += 32) {
-    const uint32_t j = base + lane;
-    const bool ok = j < tb.y;
-    const float4 sp = ok ? a.body_pos[tb.x + j] : make_float4(1e4f, 1e4f, 1e4f, 0.f);
-    const float2 q = ok ? a.body_q[tb.x + j] : make_float2(0.f, 0.f);
-    accumulate_tile<true>(tgt, tile.n_t, sp.x, sp.y, sp.z, q.x, q.y, ar, ai);
+  const uint32_t lb = a.p2p_offset[tile.list], lsplit = a.p2p_split[tile.list],
+                 le = a.p2p_offset[tile.list + 1];
+
+  // ---- touching leaves: compensated coordinates, masked
+  for (uint32_t g0 = lb; g0 < lsplit; g0 += 32) {
+    const uint32_t e = g0 + lane;
+    const bool has = e < lsplit;
+    const uint32_t sc = has ? a.p2p_src[e] : tile.leaf;
+    const int4 sg = a.cell_geom[sc];
+    uint2 sb = a.cell_body[sc];
+    if (!has) sb.y = 0;
+    // exact offset in FP64, split on the grid: o = o_hi + o_lo
+    const double inv_grid = 1.0 / a.grid;
+    const double odx = double(sg.x - tg.x) * a.kunit_d, ody = double(sg.y - tg.y) * a.kunit_d,
+                 odz = double(sg.z - tg.z) * a.kunit_d;
+    const double ohx = rint(odx * inv_grid) * a.grid, ohy = rint(ody * inv_grid) * a.grid,
+                 ohz = rint(odz * inv_grid) * a.grid;
+    const float fhx = float(ohx), fhy = float(ohy), fhz = float(ohz);
+    const float flx = float(odx - ohx), fly = float(ody - ohy), flz = float(odz - ohz);
+    const LeafGroup grp = scan_group(sb, lane);
+    const uint32_t total = __shfl_sync(0xffffffffu, grp.incl, 31);
+    for (uint32_t c0 = 0; c0 < total; c0 += 32) {
+      const uint32_t g = c0 + lane;
+      const int j = owner_of(grp.incl, g);
+      const uint32_t first_j = __shfl_sync(0xffffffffu, grp.first, j);
+      const uint32_t excl_j = __shfl_sync(0xffffffffu, grp.excl, j);
+      const float hxj = __shfl_sync(0xffffffffu, fhx, j), hyj = __shfl_sync(0xffffffffu, fhy, j),
+                  hzj = __shfl_sync(0xffffffffu, fhz, j);
+      const float lxj = __shfl_sync(0xffffffffu, flx, j), lyj = __shfl_sync(0xffffffffu, fly, j),
+                  lzj = __shfl_sync(0xffffffffu, flz, j);
+      const bool ok = g < total;
+      const uint32_t slot = first_j + (g - excl_j);
+      const float4 sh = ok ? a.body_hi[slot] : make_float4(1e4f, 1e4f, 1e4f, 0.f);
+      const float4 sl = ok ? a.body_lo[slot] : zero4;
+      const float2 q = ok ? a.body_q[slot] : make_float2(0.f, 0.f);
+      accumulate_compensated(s_thi[warp], s_tlo[warp], tile.n_t, sh.x + hxj, sh.y + hyj, sh.z + hzj,
+                             sl.x + lxj, sl.y + lyj, sl.z + lzj, q.x, q.y, ar, ai);
+    }
   }
 
-  // listed source leaves, 32 leaves per group, bodies flattened across the group
-  const uint32_t lb = a.p2p_offset[tile.list], le = a.p2p_offset[tile.list + 1];
-  for (uint32_t g0 = lb; g0 < le; g0 += 32) {
+  // ---- all other source leaves: plain coordinates, bodies flattened across groups of 32 leaves
+  for (uint32_t g0 = lsplit; g0 < le; g0 += 32) {
     const uint32_t e = g0 + lane;
     const bool has = e < le;
     const uint32_t sc = has ? a.p2p_src[e] : tile.leaf;
@@ -113,24 +193,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) p2p_kernel(const P2PArgs 
     const float ox = float(sg.x - tg.x) * a.kunit;
     const float oy = float(sg.y - tg.y) * a.kunit;
     const float oz = float(sg.z - tg.z) * a.kunit;
-    uint32_t incl = sb.y;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const uint32_t excl = incl - sb.y;
-    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const LeafGroup grp = scan_group(sb, lane);
+    const uint32_t total = __shfl_sync(0xffffffffu, grp.incl, 31);
     for (uint32_t c0 = 0; c0 < total; c0 += 32) {
       const uint32_t g = c0 + lane;
-      int j = 0;  // first lane whose inclusive count exceeds g
-#pragma unroll
-      for (int step = 16; step >= 1; step >>= 1) {
-        const uint32_t v = __shfl_sync(0xffffffffu, incl, j + step - 1);
-        if (v <= g) j += step;
-      }
-      const uint32_t first_j = __shfl_sync(0xffffffffu, sb.x, j);
-      const uint32_t excl_j = __shfl_sync(0xffffffffu, excl, j);
+      const int j = owner_of(grp.incl, g);
+      const uint32_t first_j = __shfl_sync(0xffffffffu, grp.first, j);
+      const uint32_t excl_j = __shfl_sync(0xffffffffu, grp.excl, j);
       const float oxj = __shfl_sync(0xffffffffu, ox, j);
       const float oyj = __shfl_sync(0xffffffffu, oy, j);
       const float ozj = __shfl_sync(0xffffffffu, oz, j);
@@ -138,7 +207,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) p2p_kernel(const P2PArgs 
       const uint32_t slot = first_j + (g - excl_j);
       const float4 sp = ok ? a.body_pos[slot] : make_float4(1e4f, 1e4f, 1e4f, 0.f);
       const float2 q = ok ? a.body_q[slot] : make_float2(0.f, 0.f);
-      accumulate_tile<false>(tgt, tile.n_t, sp.x + oxj, sp.y + oyj, sp.z + ozj, q.x, q.y, ar, ai);
+      accumulate_plain(s_tgt[warp], tile.n_t, sp.x + oxj, sp.y + oyj, sp.z + ozj, q.x, q.y, ar, ai);
     }
   }
 
