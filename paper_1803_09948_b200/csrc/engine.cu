@@ -139,6 +139,10 @@ Engine::Engine(const hfmm_cuda_config& cfg) : cfg_(cfg) {
   std::vector<float> diag(P + 1), sub(P + 1), a(tri), b(tri);
   build_legendre_coefficients(P, diag.data(), sub.data(), a.data(), b.data());
   upload_legendre_constants(diag.data(), sub.data(), a.data(), b.data(), P);
+  TranslateSchedule sched{};
+  build_translate_schedule(P, &sched);
+  schedule_.upload(&sched, 1, stream_);
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
 }
 
 Engine::~Engine() {
@@ -172,9 +176,10 @@ void Engine::upload_stage(TranslateStage& st, const std::vector<uint32_t>& src,
     }
   }
   std::vector<TranslateItem> items;
+  const uint64_t batch = uint64_t(translate_batch_size(cfg_.order));
   for (size_t c = 0; c < nc; ++c)
-    for (uint64_t b = start[c]; b < start[c + 1]; b += kTranslateBatch)
-      items.push_back({uint32_t(b), uint32_t(std::min<uint64_t>(kTranslateBatch, start[c + 1] - b)),
+    for (uint64_t b = start[c]; b < start[c + 1]; b += batch)
+      items.push_back({uint32_t(b), uint32_t(std::min<uint64_t>(batch, start[c + 1] - b)),
                        uint32_t(c), 0u});
   if (np >= (uint64_t(1) << 32)) throw Error(HFMM_ERR_CONFIG, "pair count exceeds 32-bit indexing");
   st.n_items = uint32_t(items.size());
@@ -498,6 +503,7 @@ void Engine::run_far_and_near() {
       ta.dst = dst;
       ta.order = cfg_.order;
       ta.stride = stride_;
+      ta.schedule = schedule_.get();
       launch_translate(ta, stream_);
       if (st.n_items) ++launches;
     };
@@ -645,14 +651,14 @@ void compose_dense_from_tables(int order, double k, const double t[3], int kind,
   // R[(n,m'),(n,m)] = E_n[m][m'] e^{i m phi};  Chat[(nu,m),(n,m)]
   std::vector<cd> R(size_t(dim) * dim, 0), C(size_t(dim) * dim, 0);
   for (int n = 0; n <= P; ++n) {
-    const int w = 2 * n + 1;
+    const int w = rot_row_stride(n);
     for (int m = -n; m <= n; ++m)
       for (int mp = -n; mp <= n; ++mp)
         R[size_t(nm_index(n, mp)) * dim + nm_index(n, m)] =
             double(rot[rot_block_offset(n) + (m + n) * w + (mp + n)]) * ph[m + P];
   }
   for (int m = -P; m <= P; ++m) {
-    const int am = std::abs(m), w = P + 1 - am;
+    const int am = std::abs(m), w = coax_row_stride(P, am);
     const float* blk = coax.data() + 2 * size_t(coax_block_offset(P, am));
     for (int n = am; n <= P; ++n)
       for (int nu = am; nu <= P; ++nu) {

@@ -81,11 +81,23 @@ struct TranslateClass {
 };
 struct TranslateItem {
   uint32_t pair_begin;
-  uint32_t count;  // <= kTranslateBatch pairs, all of one class
+  uint32_t count;  // <= translate_batch_size(order) pairs, all of one class
   uint32_t cls;
   uint32_t pad;
 };
-inline constexpr int kTranslateBatch = 32;
+inline constexpr int kTranslateBatch = 32;   // pairs per work item (= lanes of a warp)
+inline constexpr int kTranslateWarps = 8;    // warps per CTA of the translation kernel
+inline constexpr int kTranslateMaxTasks = 160;
+
+// Per-order static schedule of the translation kernel: each stage is a list of tasks
+// (block | first row << 8 | rows << 16), grouped per warp.
+struct TranslateSchedule {
+  int rot_begin[kTranslateWarps + 1];
+  int coax_begin[kTranslateWarps + 1];
+  uint32_t rot_tasks[kTranslateMaxTasks];
+  uint32_t coax_tasks[kTranslateMaxTasks];
+};
+void build_translate_schedule(int order, TranslateSchedule* out);
 
 struct TranslateArgs {
   const TranslateItem* items;
@@ -95,12 +107,15 @@ struct TranslateArgs {
   const uint32_t* pair_dst;
   const float* rot_tables;   // [rot][rot_table_size(P)]
   const float* coax_tables;  // [coax][2 * coax_table_size(P)]
+  const TranslateSchedule* schedule;  // device pointer
   const float2* src;         // expansions read
   float2* dst;               // expansions accumulated into (atomically)
   int order;
   int stride;
 };
 void launch_translate(const TranslateArgs& a, cudaStream_t s);
+// pairs per work item expected by the kernel
+int translate_batch_size(int order);
 
 // ---- vector plumbing -------------------------------------------------------------------------
 // body_q[slot] = float2(q[index[slot]]) * weight[index[slot]] (weight may be null)

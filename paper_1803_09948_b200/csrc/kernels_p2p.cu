@@ -55,17 +55,25 @@ __device__ __forceinline__ void green_accumulate(float r2, float rinv, float qr,
   ai = fmaf(gi, qr, ai);
 }
 
+// Targets are walked in groups of kGroup: one warp-uniform branch per group, and kGroup
+// independent evaluations in a straight line so the MUFU / FMA latencies overlap.  Slots past n_t
+// inside the last group hold zero coordinates; their accumulators are never stored.
+constexpr int kGroup = 4;
+
 // plain path: one FP32 coordinate per axis
 __device__ __forceinline__ void accumulate_plain(const float4* __restrict__ tgt, uint32_t n_t,
                                                  float sx, float sy, float sz, float qr, float qi,
                                                  float (&ar)[kTile], float (&ai)[kTile]) {
 #pragma unroll
-  for (int t = 0; t < kTile; ++t) {
-    if (t < n_t) {  // warp-uniform
-      const float4 tp = tgt[t];
-      const float dx = tp.x - sx, dy = tp.y - sy, dz = tp.z - sz;
-      const float r2 = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, 1e-30f)));
-      green_accumulate(r2, rsqrt_approx(r2), qr, qi, ar[t], ai[t]);
+  for (int t0 = 0; t0 < kTile; t0 += kGroup) {
+    if (t0 < n_t) {  // warp-uniform
+#pragma unroll
+      for (int t = t0; t < t0 + kGroup; ++t) {
+        const float4 tp = tgt[t];
+        const float dx = tp.x - sx, dy = tp.y - sy, dz = tp.z - sz;
+        const float r2 = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, 1e-30f)));
+        green_accumulate(r2, rsqrt_approx(r2), qr, qi, ar[t], ai[t]);
+      }
     }
   }
 }
@@ -77,15 +85,18 @@ __device__ __forceinline__ void accumulate_compensated(const float4* __restrict_
                                                        float ly, float lz, float qr, float qi,
                                                        float (&ar)[kTile], float (&ai)[kTile]) {
 #pragma unroll
-  for (int t = 0; t < kTile; ++t) {
-    if (t < n_t) {
-      const float4 th = thi[t], tl = tlo[t];
-      const float dx = (th.x - hx) + (tl.x - lx);
-      const float dy = (th.y - hy) + (tl.y - ly);
-      const float dz = (th.z - hz) + (tl.z - lz);
-      const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      const float rinv = r2 > 0.0f ? rsqrt_approx(r2) : 0.0f;
-      green_accumulate(r2, rinv, qr, qi, ar[t], ai[t]);
+  for (int t0 = 0; t0 < kTile; t0 += kGroup) {
+    if (t0 < n_t) {
+#pragma unroll
+      for (int t = t0; t < t0 + kGroup; ++t) {
+        const float4 th = thi[t], tl = tlo[t];
+        const float dx = (th.x - hx) + (tl.x - lx);
+        const float dy = (th.y - hy) + (tl.y - ly);
+        const float dz = (th.z - hz) + (tl.z - lz);
+        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        const float rinv = r2 > 0.0f ? rsqrt_approx(r2) : 0.0f;
+        green_accumulate(r2, rinv, qr, qi, ar[t], ai[t]);
+      }
     }
   }
 }
@@ -128,7 +139,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) p2p_kernel(const P2PArgs 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t tile_id = blockIdx.x * kWarpsPerBlock + warp;
   if (tile_id >= a.n_tiles) return;
-  const P2PTile tile = a.tiles[tile_id];
+  P2PTile tile = a.tiles[tile_id];
+  tile.n_t = __shfl_sync(0xffffffffu, tile.n_t, 0);
   const int4 tg = a.cell_geom[tile.leaf];
   const uint2 tb = a.cell_body[tile.leaf];
   const uint32_t tslot = tb.x + tile.body_off + lane;

@@ -138,9 +138,10 @@ void build_rotation_table(int order, double cos_theta, float* out) {
     cp[i] = cp[i - 1] * c;
     sp[i] = sp[i - 1] * s;
   }
+  std::fill(out, out + rot_table_size(order), 0.0f);
   for (int n = 0; n <= order; ++n) {
     float* blk = out + rot_block_offset(n);
-    const int w = 2 * n + 1;
+    const int w = rot_row_stride(n);
     for (int a = -n; a <= n; ++a)        // first index of d^n_{a,b}
       for (int b = -n; b <= n; ++b) {    // second index
         const long double pre = sqrtl(factorial_ld(n + a) * factorial_ld(n - a) *
@@ -198,10 +199,11 @@ void CoaxBuilder::build(CoaxKind kind, double k, double dist, double s_src, doub
   }
   const long double ls = logl((long double)s_src), ld = logl((long double)s_dst), lz = logl(z);
   auto ldf = [](int n) { return logl(double_factorial(n)); };
-  int idx = 0;
+  std::fill(out, out + 2 * size_t(coax_table_size(P)), 0.0f);
   for (int m = 0; m <= P; ++m)
     for (int n = m; n <= P; ++n)
       for (int nu = m; nu <= P; ++nu) {
+        const int idx = coax_block_offset(P, m) + (n - m) * coax_row_stride(P, m) + (nu - m);
         const double* a = coef_.data() + offset_[slot(m, nu, n)];
         long double sr = 0, si = 0;
         int t = 0;
@@ -220,7 +222,6 @@ void CoaxBuilder::build(CoaxKind kind, double k, double dist, double s_src, doub
         }
         out[2 * idx] = float(sr);
         out[2 * idx + 1] = float(si);
-        ++idx;
       }
 }
 

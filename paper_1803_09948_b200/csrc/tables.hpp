@@ -34,17 +34,28 @@ double wigner3j(int j1, int j2, int j3, int m1, int m2, int m3);
 double wigner_d(int n, int mp, int m, double cos_beta);
 long double double_factorial(int n);  // n!! for odd n >= -1
 
-HFMM_HD inline int rot_block_offset(int n) { return n * (2 * n - 1) * (2 * n + 1) / 3; }  // sum_{j<n}(2j+1)^2
-HFMM_HD inline int rot_table_size(int p) { return rot_block_offset(p + 1); }
-// coaxial table: for m = 0..P a (P+1-m) x (P+1-m) complex block, laid out [n-m][nu-m]
-HFMM_HD inline int coax_block_offset(int p, int m) {
+// Table layouts are padded so the device can fetch 4 rotation coefficients (or 2 complex coaxial
+// coefficients) with one aligned 16-byte load:
+//   rotation block n : (2n+1) rows of rot_row_stride(n) floats, E_n[m][m'] at row m+n, column m'+n
+//   coaxial block m  : (P+1-m) rows of coax_row_stride(P,m) complex, Chat^m[n][nu] at row n-m,
+//                      column nu-m
+// padding entries are zero.
+HFMM_HD constexpr int rot_row_stride(int n) { return (2 * n + 1 + 3) & ~3; }
+HFMM_HD constexpr int rot_block_offset(int n) {
   int off = 0;
-  for (int j = 0; j < m; ++j) off += (p + 1 - j) * (p + 1 - j);
+  for (int j = 0; j < n; ++j) off += (2 * j + 1) * rot_row_stride(j);
   return off;
 }
-HFMM_HD inline int coax_table_size(int p) { return coax_block_offset(p, p + 1); }
+HFMM_HD constexpr int rot_table_size(int p) { return rot_block_offset(p + 1); }
+HFMM_HD constexpr int coax_row_stride(int p, int m) { return (p + 1 - m + 1) & ~1; }
+HFMM_HD constexpr int coax_block_offset(int p, int m) {
+  int off = 0;
+  for (int j = 0; j < m; ++j) off += (p + 1 - j) * coax_row_stride(p, j);
+  return off;
+}
+HFMM_HD constexpr int coax_table_size(int p) { return coax_block_offset(p, p + 1); }  // complex
 
-// E_n[m][m'] = d^n_{m,m'}(theta), blocks concatenated over n; forward rotation is
+// E_n[m][m'] = d^n_{m,m'}(theta), padded blocks concatenated over n; forward rotation is
 //   M'_n^{m'} = sum_m E_n[m][m'] e^{i m phi} M_n^m   (then  M = R^H M' for the inverse)
 void build_rotation_table(int order, double cos_theta, float* out);
 
