@@ -140,7 +140,16 @@ int hfmm_cuda_gmres(hfmm_cuda_t* h, const double* rhs, double* x, const hfmm_gmr
 int hfmm_cuda_evaluate_field(hfmm_cuda_t* h, const double* coeff, const double* obs, size_t nobs,
                              double* out);
 
+/* Fills the statistics of the tree/lists and the per-kernel device times of the LAST matvec (CUDA
+ * events recorded on the streams the kernels ran on; this call synchronises the handle). */
 int hfmm_cuda_get_stats(hfmm_cuda_t* h, hfmm_cuda_stats* out);
+
+/* ---- measurement helpers (bench.py): the handle launches on its own streams, which a caller's
+ * events cannot see, so the caller drives events recorded on the handle's main stream ---------- */
+int hfmm_cuda_timer_record(hfmm_cuda_t* h, int slot);                       /* slot in [0, 16) */
+int hfmm_cuda_timer_elapsed_ms(hfmm_cuda_t* h, int slot_a, int slot_b, double* ms); /* waits for b */
+int hfmm_cuda_flush_l2(hfmm_cuda_t* h);            /* writes a 256 MiB scratch buffer (L2 is 126 MB) */
+int hfmm_cuda_fp32_peak_tflops(hfmm_cuda_t* h, double* tflops); /* FFMA-only probe, 2 flop per FFMA */
 
 /* ---- introspection used by the parity tests (tree / list / expansion level checks) -------- */
 /* cells in the library's level order: 8 x u32 per cell = level, ix, iy, iz, body_first,

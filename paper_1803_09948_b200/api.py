@@ -142,6 +142,22 @@ class HfmmCuda:
     def sync(self):
         self._check(self.lib.hfmm_cuda_sync(self.h))
 
+    def timer_record(self, slot: int):
+        self._check(self.lib.hfmm_cuda_timer_record(self.h, int(slot)))
+
+    def timer_elapsed_ms(self, a: int, b: int) -> float:
+        ms = C.c_double()
+        self._check(self.lib.hfmm_cuda_timer_elapsed_ms(self.h, int(a), int(b), C.byref(ms)))
+        return ms.value
+
+    def flush_l2(self):
+        self._check(self.lib.hfmm_cuda_flush_l2(self.h))
+
+    def fp32_peak_tflops(self) -> float:
+        v = C.c_double()
+        self._check(self.lib.hfmm_cuda_fp32_peak_tflops(self.h, C.byref(v)))
+        return v.value
+
     def stats(self) -> dict:
         s = Stats()
         self._check(self.lib.hfmm_cuda_get_stats(self.h, C.byref(s)))

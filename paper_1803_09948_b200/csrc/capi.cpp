@@ -101,6 +101,26 @@ int hfmm_cuda_sync(hfmm_cuda_t* h) {
   return guarded(h, [&] { h->engine->sync(); });
 }
 
+int hfmm_cuda_timer_record(hfmm_cuda_t* h, int slot) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] { h->engine->timer_record(slot); });
+}
+
+int hfmm_cuda_timer_elapsed_ms(hfmm_cuda_t* h, int slot_a, int slot_b, double* ms) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] { *ms = h->engine->timer_elapsed_ms(slot_a, slot_b); });
+}
+
+int hfmm_cuda_flush_l2(hfmm_cuda_t* h) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] { h->engine->flush_l2(); });
+}
+
+int hfmm_cuda_fp32_peak_tflops(hfmm_cuda_t* h, double* tflops) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] { *tflops = h->engine->measure_fp32_peak_tflops(); });
+}
+
 int hfmm_cuda_get_stats(hfmm_cuda_t* h, hfmm_cuda_stats* out) {
   if (int rc = need(h)) return rc;
   return guarded(h, [&] { h->engine->get_stats(out); });

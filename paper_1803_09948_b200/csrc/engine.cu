@@ -133,6 +133,8 @@ Engine::Engine(const hfmm_cuda_config& cfg) : cfg_(cfg) {
   HFMM_CUDA_CHECK(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
   ev_.resize(12);
   for (auto& e : ev_) HFMM_CUDA_CHECK(cudaEventCreate(&e));
+  user_ev_.resize(16);
+  for (auto& e : user_ev_) HFMM_CUDA_CHECK(cudaEventCreate(&e));
 
   const int P = cfg.order;
   const size_t tri = size_t(P + 1) * (P + 2) / 2;
@@ -148,6 +150,7 @@ Engine::Engine(const hfmm_cuda_config& cfg) : cfg_(cfg) {
 Engine::~Engine() {
   cudaSetDevice(cfg_.device);
   for (auto& e : ev_) cudaEventDestroy(e);
+  for (auto& e : user_ev_) cudaEventDestroy(e);
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
   if (stream_) cudaStreamDestroy(stream_);
@@ -444,7 +447,10 @@ void Engine::set_points(const double* xyz, size_t n) {
 // one FMM evaluation, body_q_ (Morton order) -> near_, far_.  The near field runs on its own
 // stream, concurrently with the upward / translation / downward chain.
 void Engine::run_far_and_near() {
-  const bool timers = (cfg_.flags & HFMM_FLAG_PHASE_TIMERS) != 0;
+  // per-kernel CUDA events are always recorded on the stream each kernel is launched on (they cost
+  // nothing); HFMM_FLAG_PHASE_TIMERS additionally serialises the near field behind the far field
+  // so the per-kernel durations are free of overlap
+  const bool serial = (cfg_.flags & HFMM_FLAG_PHASE_TIMERS) != 0;
   uint64_t launches = 0;
   HFMM_CUDA_CHECK(cudaEventRecord(ev_fork_, stream_));
   HFMM_CUDA_CHECK(cudaStreamWaitEvent(stream_near_, ev_fork_, 0));
@@ -466,11 +472,11 @@ void Engine::run_far_and_near() {
   pa.out = near_.get();
   pa.kunit = kunit_;
   pa.out_scale = float(cfg_.wave_r / (4.0 * kPi));
-  cudaStream_t sn = timers ? stream_ : stream_near_;  // serialise when timing phases
-  if (timers) HFMM_CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
+  cudaStream_t sn = serial ? stream_ : stream_near_;
+  HFMM_CUDA_CHECK(cudaEventRecord(ev_[0], sn));
   launch_p2p(pa, sn);
   ++launches;
-  if (timers) HFMM_CUDA_CHECK(cudaEventRecord(ev_[1], stream_));
+  HFMM_CUDA_CHECK(cudaEventRecord(ev_[1], sn));
 
   if (have_far_) {
     multipole_.zero(stream_);
@@ -485,10 +491,10 @@ void Engine::run_far_and_near() {
     la.k = float(cfg_.wave_r);
     la.leaves = p2m_leaves_.get();
     la.n_leaves = n_p2m_leaves_;
-    if (timers) HFMM_CUDA_CHECK(cudaEventRecord(ev_[2], stream_));
+    HFMM_CUDA_CHECK(cudaEventRecord(ev_[2], stream_));
     launch_p2m(la, body_q_.get(), multipole_.get(), stream_);
     ++launches;
-    if (timers) HFMM_CUDA_CHECK(cudaEventRecord(ev_[3], stream_));
+    HFMM_CUDA_CHECK(cudaEventRecord(ev_[3], stream_));
 
     auto run_stage = [&](const TranslateStage& st, const float2* src, float2* dst) {
       TranslateArgs ta{};
@@ -508,67 +514,101 @@ void Engine::run_far_and_near() {
       if (st.n_items) ++launches;
     };
     for (const auto& st : m2m_) run_stage(st, multipole_.get(), multipole_.get());
-    if (timers) HFMM_CUDA_CHECK(cudaEventRecord(ev_[4], stream_));
+    HFMM_CUDA_CHECK(cudaEventRecord(ev_[4], stream_));
     run_stage(m2l_, multipole_.get(), local_.get());
-    if (timers) HFMM_CUDA_CHECK(cudaEventRecord(ev_[5], stream_));
+    HFMM_CUDA_CHECK(cudaEventRecord(ev_[5], stream_));
     for (const auto& st : l2l_) run_stage(st, local_.get(), local_.get());
-    if (timers) HFMM_CUDA_CHECK(cudaEventRecord(ev_[6], stream_));
+    HFMM_CUDA_CHECK(cudaEventRecord(ev_[6], stream_));
     la.leaves = l2p_leaves_.get();
     la.n_leaves = n_l2p_leaves_;
     launch_l2p(la, local_.get(), far_.get(), stream_);
     ++launches;
-    if (timers) HFMM_CUDA_CHECK(cudaEventRecord(ev_[7], stream_));
+    HFMM_CUDA_CHECK(cudaEventRecord(ev_[7], stream_));
   }
   HFMM_CUDA_CHECK(cudaEventRecord(ev_join_, stream_near_));
   HFMM_CUDA_CHECK(cudaStreamWaitEvent(stream_, ev_join_, 0));
   stats_.kernel_launches = launches + 2;  // + gather, scatter
+  timings_pending_ = true;
+}
+
+// reads the per-kernel events of the last matvec (synchronises the handle's stream)
+void Engine::collect_timings() {
+  if (!timings_pending_) return;
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  auto dt = [&](int a, int b) {
+    float v = 0;
+    cudaEventElapsedTime(&v, ev_[a], ev_[b]);
+    return double(v) * 1e-3;
+  };
+  stats_.p2p_seconds = dt(0, 1);
+  stats_.p2m_seconds = stats_.m2m_seconds = stats_.m2l_seconds = stats_.l2l_seconds = stats_.l2p_seconds = 0;
+  if (have_far_) {
+    stats_.p2m_seconds = dt(2, 3);
+    stats_.m2m_seconds = dt(3, 4);
+    stats_.m2l_seconds = dt(4, 5);
+    stats_.l2l_seconds = dt(5, 6);
+    stats_.l2p_seconds = dt(6, 7);
+  }
+  stats_.upward_seconds = stats_.p2m_seconds + stats_.m2m_seconds;
+  stats_.interaction_seconds = stats_.m2l_seconds + stats_.p2p_seconds;
+  stats_.downward_seconds = stats_.l2l_seconds + stats_.l2p_seconds;
+  stats_.matvec_seconds = dt(8, 9);
+  timings_pending_ = false;
 }
 
 void Engine::matvec_device(const void* q_dev, void* out_dev) {
   require_points();
   HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
   const uint32_t n = tree_.n_bodies;
+  HFMM_CUDA_CHECK(cudaEventRecord(ev_[8], stream_));
   launch_gather_charges(nullptr, static_cast<const float2*>(q_dev), body_index_.get(), nullptr,
                         body_q_.get(), n, stream_);
   run_far_and_near();
   launch_scatter_potentials(near_.get(), far_.get(), body_index_.get(), nullptr,
                             static_cast<float2*>(out_dev), n, stream_);
+  HFMM_CUDA_CHECK(cudaEventRecord(ev_[9], stream_));
 }
 
 void Engine::matvec_host(const double* q, double* out) {
   require_points();
   HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
   const uint32_t n = tree_.n_bodies;
-  const bool timers = (cfg_.flags & HFMM_FLAG_PHASE_TIMERS) != 0;
   HFMM_CUDA_CHECK(cudaEventRecord(ev_[10], stream_));
   HFMM_CUDA_CHECK(cudaMemcpyAsync(io64_.get(), q, size_t(n) * sizeof(double2), cudaMemcpyHostToDevice, stream_));
+  HFMM_CUDA_CHECK(cudaEventRecord(ev_[8], stream_));
   launch_gather_charges(io64_.get(), nullptr, body_index_.get(), nullptr, body_q_.get(), n, stream_);
   run_far_and_near();
   launch_scatter_potentials(near_.get(), far_.get(), body_index_.get(), io64_.get(), nullptr, n, stream_);
+  HFMM_CUDA_CHECK(cudaEventRecord(ev_[9], stream_));
   HFMM_CUDA_CHECK(cudaMemcpyAsync(out, io64_.get(), size_t(n) * sizeof(double2), cudaMemcpyDeviceToHost, stream_));
   HFMM_CUDA_CHECK(cudaEventRecord(ev_[11], stream_));
   HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+double Engine::measure_fp32_peak_tflops() {
+  HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  return run_fp32_peak_probe(stream_);
+}
+
+void Engine::timer_record(int slot) {
+  if (slot < 0 || slot >= int(user_ev_.size())) throw Error(HFMM_ERR_CONFIG, "timer slot out of range");
+  HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  HFMM_CUDA_CHECK(cudaEventRecord(user_ev_[slot], stream_));
+}
+
+double Engine::timer_elapsed_ms(int a, int b) {
+  if (a < 0 || b < 0 || a >= int(user_ev_.size()) || b >= int(user_ev_.size()))
+    throw Error(HFMM_ERR_CONFIG, "timer slot out of range");
+  HFMM_CUDA_CHECK(cudaEventSynchronize(user_ev_[b]));
   float ms = 0;
-  HFMM_CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[10], ev_[11]));
-  stats_.matvec_seconds = ms * 1e-3;
-  if (timers) {
-    auto dt = [&](int a, int b) {
-      float v = 0;
-      cudaEventElapsedTime(&v, ev_[a], ev_[b]);
-      return double(v) * 1e-3;
-    };
-    stats_.p2p_seconds = dt(0, 1);
-    if (have_far_) {
-      stats_.p2m_seconds = dt(2, 3);
-      stats_.m2m_seconds = dt(3, 4);
-      stats_.m2l_seconds = dt(4, 5);
-      stats_.l2l_seconds = dt(5, 6);
-      stats_.l2p_seconds = dt(6, 7);
-    }
-    stats_.upward_seconds = stats_.p2m_seconds + stats_.m2m_seconds;
-    stats_.interaction_seconds = stats_.m2l_seconds + stats_.p2p_seconds;
-    stats_.downward_seconds = stats_.l2l_seconds + stats_.l2p_seconds;
-  }
+  HFMM_CUDA_CHECK(cudaEventElapsedTime(&ms, user_ev_[a], user_ev_[b]));
+  return double(ms);
+}
+
+void Engine::flush_l2() {
+  HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  if (flush_.size() == 0) flush_.resize(size_t(256) << 20);  // 256 MiB > 126 MB of L2
+  HFMM_CUDA_CHECK(cudaMemsetAsync(flush_.get(), 1, flush_.size(), stream_));
 }
 
 void Engine::sync() {
@@ -577,6 +617,7 @@ void Engine::sync() {
 }
 
 void Engine::get_stats(hfmm_cuda_stats* out) {
+  collect_timings();
   stats_.device_bytes = device_bytes_counter();
   *out = stats_;
 }

@@ -34,6 +34,10 @@ class Engine {
   void matvec_host(const double* q, double* out);
   void matvec_device(const void* q_dev, void* out_dev);
   void sync();
+  void timer_record(int slot);
+  double timer_elapsed_ms(int a, int b);
+  void flush_l2();
+  double measure_fp32_peak_tflops();
   void get_stats(hfmm_cuda_stats* out);
   void get_cells(uint32_t* out, size_t capacity) const;
   void get_body_order(uint32_t* out) const;
@@ -47,6 +51,7 @@ class Engine {
  private:
   void require_points() const;
   void run_far_and_near();  // body_q_ -> near_, far_
+  void collect_timings();
   void build_translate_stages(const PairLists& pairs);
   void upload_stage(TranslateStage& st, const std::vector<uint32_t>& src,
                     const std::vector<uint32_t>& dst, const std::vector<uint32_t>& cls_of_pair,
@@ -57,7 +62,10 @@ class Engine {
   int threads_ = 1;
   cudaStream_t stream_ = nullptr, stream_near_ = nullptr;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
-  std::vector<cudaEvent_t> ev_;  // phase timers
+  std::vector<cudaEvent_t> ev_;       // per-kernel timers of the last matvec
+  std::vector<cudaEvent_t> user_ev_;  // caller-driven timers (hfmm_cuda_timer_*)
+  bool timings_pending_ = false;
+  DeviceBuffer<unsigned char> flush_;
 
   // host mirrors kept for introspection
   TreeArrays tree_;

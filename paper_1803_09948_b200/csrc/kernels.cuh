@@ -126,4 +126,7 @@ void launch_gather_charges(const double2* q_caller, const float2* q_caller_f32,
 void launch_scatter_potentials(const float2* near, const float2* far, const uint32_t* index,
                                double2* out_f64, float2* out_f32, uint32_t n, cudaStream_t s);
 
+// FFMA-only micro-benchmark; returns TFLOP/s (2 flop per FFMA)
+double run_fp32_peak_probe(cudaStream_t s);
+
 }  // namespace hfmm_b200

@@ -1,5 +1,7 @@
 // kernels_misc.cu — vector plumbing around the FMM: caller-order <-> Morton-order permutations
 // (reference solver.cpp:327-331), FP64 <-> FP32 conversion at the boundary.
+#include <algorithm>
+
 #include "device_utils.cuh"
 #include "kernels.cuh"
 
@@ -42,7 +44,51 @@ __global__ void scatter_potentials_kernel(const float2* __restrict__ near, const
     o32[i] = make_float2(a.x + b.x, a.y + b.y);
 }
 
+// FFMA-only probe: 16 independent chains per thread, no memory traffic.  Gives the FP32 roofline
+// denominator actually reachable on this part at its running clock (MEASURED_PEAKS.json carries no
+// FP32 entry; nominal is SMs x 128 lanes x 2 x clock).
+__global__ void __launch_bounds__(256) fp32_peak_kernel(float* out, int iters, float a, float b) {
+  float v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = float(threadIdx.x + i);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = fmaf(v[i], a, b);
+  }
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += v[i];
+  if (s == 123.456f) out[0] = s;  // never true; keeps the chains alive
+}
+
 }  // namespace
+
+double run_fp32_peak_probe(cudaStream_t s) {
+  int dev = 0, sms = 0;
+  HFMM_CUDA_CHECK(cudaGetDevice(&dev));
+  HFMM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  float* out = nullptr;
+  HFMM_CUDA_CHECK(cudaMalloc(&out, 4));
+  cudaEvent_t e0, e1;
+  HFMM_CUDA_CHECK(cudaEventCreate(&e0));
+  HFMM_CUDA_CHECK(cudaEventCreate(&e1));
+  const int iters = 1 << 14, blocks = sms * 8, threads = 256;
+  double best = 0;
+  for (int rep = 0; rep < 4; ++rep) {
+    HFMM_CUDA_CHECK(cudaEventRecord(e0, s));
+    fp32_peak_kernel<<<blocks, threads, 0, s>>>(out, iters, 0.999f, 0.001f);
+    HFMM_CUDA_CHECK(cudaEventRecord(e1, s));
+    HFMM_CUDA_CHECK(cudaEventSynchronize(e1));
+    float ms = 0;
+    HFMM_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+    const double flops = 2.0 * 16.0 * double(iters) * double(blocks) * threads;
+    if (rep > 0) best = std::max(best, flops / (double(ms) * 1e-3) * 1e-12);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  return best;
+}
 
 void launch_gather_charges(const double2* q64, const float2* q32, const uint32_t* index,
                            const float* weight, float2* body_q, uint32_t n, cudaStream_t s) {
