@@ -1,0 +1,104 @@
+"""CPU-side checks of the product library (no device): the C ABI surface, configuration errors,
+the host tree / dual-tree-traversal builder, and the FP32 translation tables."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+from checkers import rel_l2
+from paper_1803_09948_b200 import HfmmCuda, HfmmError, api, library_path
+from paper_1803_09948_b200.workloads import CONFIGS, icosphere_patches, make_points, plummer_points, sphere_points
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "hfmm_cuda.h")).read()
+    names = sorted(set(re.findall(r"\b(hfmm_cuda_[a-z0-9_]+)\s*\(", hdr)))
+    assert len(names) >= 20
+    lib = C.CDLL(library_path())
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    assert b"sm_100a" in api.load_library().hfmm_cuda_version()
+
+
+def test_config_errors_mirror_the_reference(gpu_available):
+    # traversal.cpp:16-21 (s >= c >= 1, 0 < theta <= 1), :212-213 (order >= 0): config_error
+    for kw in (dict(ncrit=0), dict(ncrit=64, grain=32), dict(theta=0.0), dict(theta=1.5),
+               dict(order=-1), dict(order=99), dict(wave_i=0.1)):
+        args = dict(k=1.0, order=4)
+        args.update(kw)
+        with pytest.raises(HfmmError) as e:
+            HfmmCuda(**args)
+        assert e.value.kind == "config_error"
+    if not gpu_available:
+        # no device: the product refuses loudly instead of falling back to a CPU path
+        with pytest.raises(HfmmError) as e:
+            HfmmCuda(k=1.0, order=4)
+        assert e.value.kind == "device_error"
+
+
+def _canon_cells(c):
+    a = c[:, :6].astype(np.int64)
+    return a[np.lexsort(a.T[::-1])]
+
+
+def _geo_pairs(cells, pairs):
+    key = lambda c: ((cells[c, 0].astype(np.int64) << 57) | (cells[c, 1].astype(np.int64) << 38)
+                     | (cells[c, 2].astype(np.int64) << 19) | cells[c, 3].astype(np.int64))
+    a = np.stack([key(pairs[:, 0]), key(pairs[:, 1])], 1)
+    return a[np.lexsort((a[:, 1], a[:, 0]))]
+
+
+@pytest.mark.parametrize("name,xyz,k,ncrit,cap,theta,kd", [
+    ("sphere", sphere_points(6000, 3), 4.0, 32, 0.25, 0.4, 1.0),
+    ("plummer", plummer_points(5000, 4, 0.05), 8.0, 16, 0.125, 0.35, 1.0),
+    ("nocap_gate", sphere_points(3000, 5), 4.0, 64, 0.0, 0.4, 1.0),
+    ("gate_off", sphere_points(3000, 6), 1.0, 24, 0.0, 0.5, 0.0),
+])
+def test_host_tree_and_lists_equal_the_oracle(oracle, name, xyz, k, ncrit, cap, theta, kd):
+    d = api.debug_host_tree(xyz, ncrit, cap, k, theta, kd)
+    f = oracle.fmm(xyz, k, 2, ncrit=ncrit, leaf_cap=cap, theta=theta, kd_max=kd)
+    assert (_canon_cells(d["cells"]) == _canon_cells(f.cells())).all()   # same cell set
+    assert (d["order"] == f.body_order()).all()                          # same Morton order
+    for which, nm in ((0, "m2l"), (1, "p2p")):                           # same pair sets
+        assert (_geo_pairs(d["cells"], d[nm]) == _geo_pairs(f.cells(), f.pair_set(which))).all()
+    # level-order invariants of the device layout: parents precede children, siblings contiguous
+    cells = d["cells"]
+    lv = cells[:, 0].astype(int)
+    assert (np.diff(lv) >= 0).all()
+    for c in np.nonzero(cells[:, 7])[0][:200]:
+        ch = cells[cells[c, 6]:cells[c, 6] + cells[c, 7]]
+        assert (ch[:, 0] == cells[c, 0] + 1).all()
+        assert ch[:, 5].sum() == cells[c, 5] and ch[0, 4] == cells[c, 4]
+
+
+@pytest.mark.parametrize("order", [4, 10, 14])
+def test_factored_tables_compose_to_the_dense_operator(oracle, order):
+    """R^H C R built from the FP32 device tables == the reference's dense translation matrix
+    (expansion.cpp:95-124), for M2L (singular) and M2M/L2L (regular) shifts, any level scales."""
+    rng = np.random.default_rng(order)
+    k = 3.0
+    shifts = [rng.uniform(-0.4, 0.4, 3), np.array([0, 0, 0.31]), np.array([0, 0, -0.31]),
+              np.array([0.2, 0, 0]), np.array([0.0625, -0.0625, 0.0625])]
+    for t in shifts:
+        for kind, sing, (ss, sd) in ((0, 1, (0.3, 0.15)), (1, 0, (0.2, 0.4))):
+            ref_T = oracle.translation_matrix(k, t, order, sing)
+            T = api.debug_compose_translation(order, k, t, kind, ss, sd)
+            assert np.abs(T - ref_T).max() <= 5e-7 * np.abs(ref_T).max(), (order, t, kind)
+
+
+def test_workload_generators():
+    c = CONFIGS["cfg2"]
+    assert c.n == 1_048_576 and c.k == 4.0 and c.order == 12 and c.resolved_leaf_cap() == 0.25
+    p = make_points(CONFIGS["cfg1"], 1000)
+    assert np.allclose(np.linalg.norm(p, axis=1), 1.0)
+    assert (make_points(CONFIGS["cfg1"], 1000) == p).all()                # seeded
+    pl = plummer_points(2000, 1, 0.05)
+    assert pl.min() >= 0 and pl.max() <= 1
+    ico = icosphere_patches(2)
+    assert ico.shape == (320, 6, 3) and np.allclose(np.linalg.norm(ico, axis=2), 1.0)
+    # config 3: 7 subdivisions -> 327,680 triangles -> 983,040 order-1 unknowns
+    assert 20 * 4 ** 7 == 327_680
