@@ -146,21 +146,33 @@ int hfmm_cuda_get_expansions(hfmm_cuda_t* h, int which, double* out) {
   return guarded(h, [&] { h->engine->get_expansions(which, out); });
 }
 
-int hfmm_cuda_set_corrections(hfmm_cuda_t* h, int, const double*, const double*, const uint32_t*,
-                              const uint32_t*, const double*, const double*, const int32_t*) {
+int hfmm_cuda_set_corrections(hfmm_cuda_t* h, int ni, const double* far_weight,
+                              const double* patch_block, const uint32_t* near_offset,
+                              const uint32_t* near_source, const double* near_delta,
+                              const double* block_lu, const int32_t* block_piv) {
   if (int rc = need(h)) return rc;
-  return guarded(h, [&] { throw Error(HFMM_ERR_INTERNAL, "set_corrections: not built yet"); });
+  return guarded(h, [&] {
+    h->engine->set_corrections(ni, far_weight, patch_block, near_offset, near_source, near_delta,
+                               block_lu, block_piv);
+  });
 }
 
-int hfmm_cuda_gmres(hfmm_cuda_t* h, const double*, double*, const hfmm_gmres_config*,
-                    hfmm_gmres_report*, double*, int) {
+int hfmm_cuda_gmres(hfmm_cuda_t* h, const double* rhs, double* x, const hfmm_gmres_config* cfg,
+                    hfmm_gmres_report* report, double* residuals, int residual_cap) {
   if (int rc = need(h)) return rc;
-  return guarded(h, [&] { throw Error(HFMM_ERR_INTERNAL, "gmres: not built yet"); });
+  return guarded(h, [&] {
+    if (!rhs || !x || !cfg || !report) throw Error(HFMM_ERR_CONFIG, "null argument");
+    h->engine->gmres(rhs, x, *cfg, report, residuals, residual_cap);
+  });
 }
 
-int hfmm_cuda_evaluate_field(hfmm_cuda_t* h, const double*, const double*, size_t, double*) {
+int hfmm_cuda_evaluate_field(hfmm_cuda_t* h, const double* coeff, const double* obs, size_t nobs,
+                             double* out) {
   if (int rc = need(h)) return rc;
-  return guarded(h, [&] { throw Error(HFMM_ERR_INTERNAL, "evaluate_field: not built yet"); });
+  return guarded(h, [&] {
+    if (!coeff || (!obs && nobs) || (!out && nobs)) throw Error(HFMM_ERR_CONFIG, "null argument");
+    h->engine->evaluate_field(coeff, obs, nobs, out);
+  });
 }
 
 int hfmm_cuda_comm_unique_id(uint8_t*) {

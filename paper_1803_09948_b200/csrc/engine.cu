@@ -390,6 +390,14 @@ void Engine::set_points(const double* xyz, size_t n) {
   }
   n_tiles_ = uint32_t(tiles.size());
 
+  {
+    std::vector<float4> abs_pos(n);
+    for (size_t i = 0; i < n; ++i)
+      abs_pos[i] = make_float4(float(k * xyz[3 * i]), float(k * xyz[3 * i + 1]), float(k * xyz[3 * i + 2]), 0.f);
+    body_abs_.upload(abs_pos, stream_);
+  }
+  have_weight_ = have_block_ = have_near_ = have_lu_ = false;  // corrections belong to a point set
+  identity_.release();
   body_pos_.upload(pos, stream_);
   body_hi_.upload(pos_hi, stream_);
   body_lo_.upload(pos_lo, stream_);
@@ -561,12 +569,9 @@ void Engine::matvec_device(const void* q_dev, void* out_dev) {
   HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
   const uint32_t n = tree_.n_bodies;
   HFMM_CUDA_CHECK(cudaEventRecord(ev_[8], stream_));
-  launch_gather_charges(nullptr, static_cast<const float2*>(q_dev), body_index_.get(), nullptr,
-                        body_q_.get(), n, stream_);
-  run_far_and_near();
-  launch_scatter_potentials(near_.get(), far_.get(), body_index_.get(), nullptr,
-                            static_cast<float2*>(out_dev), n, stream_);
+  apply_operator_device(static_cast<const float2*>(q_dev), static_cast<float2*>(out_dev));
   HFMM_CUDA_CHECK(cudaEventRecord(ev_[9], stream_));
+  (void)n;
 }
 
 void Engine::matvec_host(const double* q, double* out) {
@@ -576,9 +581,19 @@ void Engine::matvec_host(const double* q, double* out) {
   HFMM_CUDA_CHECK(cudaEventRecord(ev_[10], stream_));
   HFMM_CUDA_CHECK(cudaMemcpyAsync(io64_.get(), q, size_t(n) * sizeof(double2), cudaMemcpyHostToDevice, stream_));
   HFMM_CUDA_CHECK(cudaEventRecord(ev_[8], stream_));
-  launch_gather_charges(io64_.get(), nullptr, body_index_.get(), nullptr, body_q_.get(), n, stream_);
-  run_far_and_near();
-  launch_scatter_potentials(near_.get(), far_.get(), body_index_.get(), io64_.get(), nullptr, n, stream_);
+  if (have_weight_ || have_block_ || have_near_) {
+    if (x32_.size() != n) {
+      x32_.resize(n);
+      y32_.resize(n);
+    }
+    launch_narrow(n, io64_.get(), x32_.get(), stream_);
+    apply_operator_device(x32_.get(), y32_.get());
+    launch_widen(n, y32_.get(), io64_.get(), stream_);
+  } else {
+    launch_gather_charges(io64_.get(), nullptr, body_index_.get(), nullptr, body_q_.get(), n, stream_);
+    run_far_and_near();
+    launch_scatter_potentials(near_.get(), far_.get(), body_index_.get(), io64_.get(), nullptr, n, stream_);
+  }
   HFMM_CUDA_CHECK(cudaEventRecord(ev_[9], stream_));
   HFMM_CUDA_CHECK(cudaMemcpyAsync(out, io64_.get(), size_t(n) * sizeof(double2), cudaMemcpyDeviceToHost, stream_));
   HFMM_CUDA_CHECK(cudaEventRecord(ev_[11], stream_));
@@ -609,6 +624,17 @@ void Engine::flush_l2() {
   HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
   if (flush_.size() == 0) flush_.resize(size_t(256) << 20);  // 256 MiB > 126 MB of L2
   HFMM_CUDA_CHECK(cudaMemsetAsync(flush_.get(), 1, flush_.size(), stream_));
+}
+
+const uint32_t* Engine::identity_index() {
+  const uint32_t n = tree_.n_bodies;
+  if (identity_.size() != n) {
+    std::vector<uint32_t> id(n);
+    std::iota(id.begin(), id.end(), 0u);
+    identity_.upload(id, stream_);
+    HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  }
+  return identity_.get();
 }
 
 void Engine::sync() {

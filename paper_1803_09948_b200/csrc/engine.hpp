@@ -43,6 +43,12 @@ class Engine {
   void get_body_order(uint32_t* out) const;
   void get_pairs(int which, uint32_t* out, uint64_t* count) const;
   void get_expansions(int which, double* out);
+  void set_corrections(int ni, const double* far_weight, const double* patch_block,
+                       const uint32_t* near_offset, const uint32_t* near_source,
+                       const double* near_delta, const double* block_lu, const int32_t* block_piv);
+  void gmres(const double* rhs, double* x, const hfmm_gmres_config& cfg, hfmm_gmres_report* rep,
+             double* residuals, int residual_cap);
+  void evaluate_field(const double* coeff, const double* obs, size_t nobs, double* out);
 
   std::string last_error;
   const hfmm_cuda_config& config() const { return cfg_; }
@@ -52,6 +58,8 @@ class Engine {
   void require_points() const;
   void run_far_and_near();  // body_q_ -> near_, far_
   void collect_timings();
+  void apply_operator_device(const float2* x, float2* y);  // caller order, weights + corrections
+  const uint32_t* identity_index();
   void build_translate_stages(const PairLists& pairs);
   void upload_stage(TranslateStage& st, const std::vector<uint32_t>& src,
                     const std::vector<uint32_t>& dst, const std::vector<uint32_t>& cls_of_pair,
@@ -98,6 +106,15 @@ class Engine {
   TranslateStage m2l_;
   std::vector<TranslateStage> m2m_;  // deepest level first
   std::vector<TranslateStage> l2l_;  // shallowest level first
+  // BIE operator tail (set_corrections)
+  int ni_ = 0;
+  bool have_weight_ = false, have_block_ = false, have_near_ = false, have_lu_ = false;
+  DeviceBuffer<float> far_weight_;
+  DeviceBuffer<float2> patch_block_, near_delta_, block_lu_;
+  DeviceBuffer<uint32_t> near_offset_, near_source_, identity_;
+  DeviceBuffer<int> block_piv_;
+  DeviceBuffer<float4> body_abs_;  // k * x, caller order (exterior field evaluation)
+  DeviceBuffer<float2> x32_, y32_;
   // vectors
   DeviceBuffer<float2> body_q_, near_, far_;
   DeviceBuffer<double2> io64_;

@@ -1,0 +1,285 @@
+// gmres.cu — Engine methods of the BIE layer: apply_operator, block-Jacobi preconditioner,
+// restarted GMRES with device-resident Krylov vectors, exterior field evaluation.
+//
+// The iteration mirrors the reference's gmres (src/gmres.cpp:35-174) step for step — x0 = 0,
+// modified Gram-Schmidt plus one unconditional re-orthogonalisation pass, complex Givens in FP64
+// on the host, stop on |g_{j+1}| <= rtol ||b||, true residual recomputed at restarts and on exit —
+// so the iteration count can be compared with the reference's (north star: same count +-1).
+#include <chrono>
+#include <cmath>
+#include <complex>
+
+#include "engine.hpp"
+
+namespace hfmm_b200 {
+
+namespace {
+using cd = std::complex<double>;
+constexpr double kPi = 3.14159265358979323846264338327950288;
+
+template <typename T, typename S>
+std::vector<T> convert_complex(const S* in, size_t n) {
+  std::vector<T> out(n);
+  for (size_t i = 0; i < n; ++i) out[i] = T{decltype(T{}.x)(in[2 * i]), decltype(T{}.x)(in[2 * i + 1])};
+  return out;
+}
+}  // namespace
+
+void Engine::set_corrections(int ni, const double* far_weight, const double* patch_block,
+                             const uint32_t* near_offset, const uint32_t* near_source,
+                             const double* near_delta, const double* block_lu, const int32_t* block_piv) {
+  require_points();
+  HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  const size_t n = tree_.n_bodies;
+  if (ni < 1 || n % size_t(ni) != 0)
+    throw Error(HFMM_ERR_CONFIG, "basis count must divide the number of unknowns");
+  ni_ = ni;
+  const size_t npatch = n / size_t(ni);
+  have_weight_ = far_weight != nullptr;
+  if (have_weight_) {
+    std::vector<float> w(n);
+    for (size_t i = 0; i < n; ++i) w[i] = float(far_weight[i]);
+    far_weight_.upload(w, stream_);
+  }
+  have_block_ = patch_block != nullptr;
+  if (have_block_) patch_block_.upload(convert_complex<float2>(patch_block, npatch * ni * ni), stream_);
+  have_near_ = near_offset && near_source && near_delta && near_offset[n] > 0;
+  if (have_near_) {
+    for (size_t i = 0; i < n; ++i)
+      if (near_offset[i] > near_offset[i + 1]) throw Error(HFMM_ERR_STRUCTURAL, "near CSR offsets decrease");
+    const size_t nnz = near_offset[n];
+    for (size_t e = 0; e < nnz; ++e)
+      if (near_source[e] >= n) throw Error(HFMM_ERR_STRUCTURAL, "near CSR source out of range");
+    near_offset_.upload(near_offset, n + 1, stream_);
+    near_source_.upload(near_source, nnz, stream_);
+    near_delta_.upload(convert_complex<float2>(near_delta, nnz), stream_);
+  }
+  have_lu_ = block_lu && block_piv;
+  if (have_lu_) {
+    for (size_t i = 0; i < n; ++i)
+      if (block_piv[i] < 0 || block_piv[i] >= ni) throw Error(HFMM_ERR_STRUCTURAL, "pivot out of range");
+    block_lu_.upload(convert_complex<float2>(block_lu, npatch * ni * ni), stream_);
+    block_piv_.upload(block_piv, n, stream_);
+  }
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+// y = FMM(x * far_weight) + blockdiag x + CSR x     (reference solver.cpp:314-359), caller order
+void Engine::apply_operator_device(const float2* x, float2* y) {
+  const uint32_t n = tree_.n_bodies;
+  launch_gather_charges(nullptr, x, body_index_.get(), have_weight_ ? far_weight_.get() : nullptr,
+                        body_q_.get(), n, stream_);
+  run_far_and_near();
+  launch_scatter_potentials(near_.get(), far_.get(), body_index_.get(), nullptr, y, n, stream_);
+  if (have_block_ || have_near_)
+    launch_corrections(n, ni_, have_block_ ? patch_block_.get() : nullptr, near_offset_.get(),
+                       near_source_.get(), have_near_ ? near_delta_.get() : nullptr, x, y, stream_);
+}
+
+void Engine::gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cfg,
+                   hfmm_gmres_report* rep, double* residuals, int residual_cap) {
+  require_points();
+  HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  // validation as gmres.cpp:25-31
+  if (!(cfg.rtol > 0.0 && cfg.rtol < 1.0)) throw Error(HFMM_ERR_CONFIG, "gmres: rtol must lie in (0, 1)");
+  if (cfg.restart < 1) throw Error(HFMM_ERR_CONFIG, "gmres: restart must be >= 1");
+  if (cfg.max_iterations < 1) throw Error(HFMM_ERR_CONFIG, "gmres: max_iterations must be >= 1");
+  using clk = std::chrono::steady_clock;
+  const auto t_start = clk::now();
+  const uint32_t n = tree_.n_bodies;
+  const int m = cfg.restart;
+  const bool precond = cfg.precondition && have_lu_;
+  const uint32_t npatch = ni_ ? n / uint32_t(ni_) : 0;
+
+  *rep = hfmm_gmres_report{};
+  double bnorm2 = 0;
+  for (size_t i = 0; i < size_t(n) * 2; ++i) bnorm2 += rhs[i] * rhs[i];
+  const double bnorm = std::sqrt(bnorm2);
+  rep->rhs_norm = bnorm;
+  std::fill(x_out, x_out + size_t(n) * 2, 0.0);
+  if (bnorm == 0.0) {
+    rep->converged = 1;
+    rep->final_residual = 0;
+    return;
+  }
+  const double target = cfg.rtol * bnorm;
+
+  DeviceBuffer<float2> V(size_t(m + 1) * n), w(n), u(n), r32(n);
+  DeviceBuffer<double2> b64(n), x64(n);
+  DeviceBuffer<double> scal(size_t(2) * (2 * (m + 1) + 2)), ydev(size_t(2) * m);
+  std::vector<double> hscal(scal.size());
+  HFMM_CUDA_CHECK(cudaMemcpyAsync(b64.get(), rhs, size_t(n) * sizeof(double2), cudaMemcpyHostToDevice, stream_));
+  x64.zero(stream_);
+  launch_narrow(n, b64.get(), r32.get(), stream_);  // x0 = 0: the first residual is b
+
+  std::vector<cd> H(size_t(m + 1) * m), cs(m), sn(m), g(m + 1);
+  auto h = [&](int i, int j) -> cd& { return H[size_t(j) * (m + 1) + i]; };
+  double matvec_s = 0;
+  auto apply = [&](const float2* in, float2* out) {  // Z = A M^-1  (solver.cpp:383-387)
+    const auto t0 = clk::now();
+    const float2* src = in;
+    if (precond) {
+      launch_precondition(npatch, ni_, block_lu_.get(), block_piv_.get(), in, u.get(), stream_);
+      src = u.get();
+    }
+    apply_operator_device(src, out);
+    HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    matvec_s += std::chrono::duration<double>(clk::now() - t0).count();
+  };
+
+  int iterations = 0, nres = 0;
+  bool done = false, breakdown = false;
+  double last_est = -1, beta = bnorm;
+  while (!done) {
+    if (beta <= target || iterations >= cfg.max_iterations) break;
+    launch_scale(n, r32.get(), float(1.0 / beta), V.get(), stream_);
+    std::fill(g.begin(), g.end(), cd(0));
+    g[0] = beta;
+    int cols = 0;
+    for (int j = 0; j < m; ++j) {
+      if (iterations >= cfg.max_iterations) break;
+      apply(V.get() + size_t(j) * n, w.get());
+      // one fused sweep: ||w||^2, two Gram-Schmidt passes, ||w||^2 again; scalars stay on device
+      scal.zero(stream_);
+      double* s0 = scal.get();                  // [0]: w_scale^2
+      double* h1 = s0 + 2;                      // pass 1, j+1 entries
+      double* h2 = h1 + 2 * (m + 1);            // pass 2
+      double* hn = h2 + 2 * (m + 1);            // ||w||^2 after both passes
+      launch_norm2(n, w.get(), s0, stream_);
+      for (int pass = 0; pass < 2; ++pass) {
+        double* hp = pass ? h2 : h1;
+        for (int i = 0; i <= j; ++i) {
+          const float2* vprev = nullptr;
+          const double* cprev = nullptr;
+          if (i > 0) {
+            vprev = V.get() + size_t(i - 1) * n;
+            cprev = hp + 2 * (i - 1);
+          } else if (pass == 1) {
+            vprev = V.get() + size_t(j) * n;
+            cprev = h1 + 2 * j;
+          }
+          launch_mgs_step(n, w.get(), vprev, cprev, V.get() + size_t(i) * n, hp + 2 * i, stream_);
+        }
+      }
+      launch_mgs_step(n, w.get(), V.get() + size_t(j) * n, h2 + 2 * j, nullptr, nullptr, stream_);
+      launch_norm2(n, w.get(), hn, stream_);
+      scal.download(hscal.data(), hscal.size(), stream_);
+      HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+      const double w_scale = std::sqrt(hscal[0]);
+      const double* c1 = hscal.data() + 2;
+      const double* c2 = c1 + 2 * (m + 1);
+      double hnext = std::sqrt(c2[2 * (m + 1)]);
+      for (int i = 0; i <= j; ++i) h(i, j) = cd(c1[2 * i], c1[2 * i + 1]) + cd(c2[2 * i], c2[2 * i + 1]);
+      const bool broke = hnext <= 1e-14 * std::max(w_scale, 1e-300);
+      if (broke) hnext = 0;
+
+      for (int i = 0; i < j; ++i) {
+        const cd a = h(i, j), b = h(i + 1, j);
+        h(i, j) = cs[i] * a + sn[i] * b;
+        h(i + 1, j) = -std::conj(sn[i]) * a + cs[i] * b;
+      }
+      const cd a = h(j, j);
+      const double b = hnext, r = std::hypot(std::abs(a), b);
+      if (r == 0.0) {
+        cs[j] = 1;
+        sn[j] = 0;
+      } else if (std::abs(a) == 0.0) {
+        cs[j] = 0;
+        sn[j] = 1;
+      } else {
+        cs[j] = std::abs(a) / r;
+        sn[j] = (a / std::abs(a)) * (b / r);
+      }
+      h(j, j) = cs[j] * a + sn[j] * b;
+      g[j + 1] = -std::conj(sn[j]) * g[j];
+      g[j] = cs[j] * g[j];
+
+      ++iterations;
+      cols = j + 1;
+      last_est = std::abs(g[j + 1]);
+      if (residuals && nres < residual_cap) residuals[nres] = last_est / bnorm;
+      ++nres;
+      if (broke) {
+        breakdown = true;
+        done = true;
+        break;
+      }
+      if (last_est <= target) {
+        done = true;
+        break;
+      }
+      launch_scale(n, w.get(), float(1.0 / hnext), V.get() + size_t(j + 1) * n, stream_);
+    }
+    // fold the Arnoldi columns into x, skipping trailing dead diagonals (gmres.cpp:75-85)
+    while (cols > 0 && std::abs(h(cols - 1, cols - 1)) == 0.0) --cols;
+    std::vector<cd> y(cols);
+    for (int i = cols - 1; i >= 0; --i) {
+      cd s = g[i];
+      for (int l = i + 1; l < cols; ++l) s -= h(i, l) * y[l];
+      y[i] = std::abs(h(i, i)) == 0.0 ? cd(0) : s / h(i, i);
+    }
+    if (cols > 0) {
+      HFMM_CUDA_CHECK(cudaMemcpyAsync(ydev.get(), y.data(), sizeof(cd) * cols, cudaMemcpyHostToDevice, stream_));
+      launch_update_solution(n, cols, V.get(), n, ydev.get(), x64.get(), stream_);
+      HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    }
+    if (!done) {  // restart boundary: true residual, not an Arnoldi step
+      launch_narrow(n, x64.get(), r32.get(), stream_);
+      apply(r32.get(), w.get());
+      scal.zero(stream_);
+      launch_residual(n, b64.get(), w.get(), r32.get(), scal.get(), stream_);
+      scal.download(hscal.data(), 2, stream_);
+      HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+      beta = std::sqrt(hscal[0]);
+    }
+  }
+  // true residual on exit (gmres.cpp:165-170)
+  launch_narrow(n, x64.get(), V.get(), stream_);
+  apply(V.get(), w.get());
+  scal.zero(stream_);
+  launch_residual(n, b64.get(), w.get(), r32.get(), scal.get(), stream_);
+  scal.download(hscal.data(), 2, stream_);
+  // the returned iterate maps back through M^-1 (solver.cpp:388)
+  if (precond) {
+    launch_precondition(npatch, ni_, block_lu_.get(), block_piv_.get(), V.get(), u.get(), stream_);
+    launch_widen(n, u.get(), x64.get(), stream_);
+  }
+  HFMM_CUDA_CHECK(cudaMemcpyAsync(x_out, x64.get(), size_t(n) * sizeof(double2), cudaMemcpyDeviceToHost, stream_));
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  rep->iterations = iterations;
+  rep->breakdown = breakdown ? 1 : 0;
+  rep->final_residual = std::sqrt(hscal[0]) / bnorm;
+  rep->converged = (rep->final_residual <= cfg.rtol || (nres > 0 && last_est / bnorm <= cfg.rtol)) ? 1 : 0;
+  rep->seconds = std::chrono::duration<double>(clk::now() - t_start).count();
+  rep->matvec_seconds = matvec_s;
+}
+
+void Engine::evaluate_field(const double* coeff, const double* obs, size_t nobs, double* out) {
+  require_points();
+  HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  const uint32_t n = tree_.n_bodies;
+  const double k = cfg_.wave_r;
+  std::vector<float2> c(n);
+  for (size_t i = 0; i < n; ++i)
+    c[i] = make_float2(float(coeff[2 * i]), float(coeff[2 * i + 1]));
+  DeviceBuffer<float2> cdev;
+  cdev.upload(c, stream_);
+  if (have_weight_) {  // strength = coefficient * far_weight (solver.cpp:413-414)
+    launch_gather_charges(nullptr, cdev.get(), identity_index(), far_weight_.get(), body_q_.get(), n, stream_);
+  } else {
+    HFMM_CUDA_CHECK(cudaMemcpyAsync(body_q_.get(), cdev.get(), size_t(n) * sizeof(float2),
+                                    cudaMemcpyDeviceToDevice, stream_));
+  }
+  std::vector<float4> o(nobs);
+  for (size_t i = 0; i < nobs; ++i)
+    o[i] = make_float4(float(k * obs[3 * i]), float(k * obs[3 * i + 1]), float(k * obs[3 * i + 2]), 0.f);
+  DeviceBuffer<float4> odev;
+  odev.upload(o, stream_);
+  DeviceBuffer<double2> res(nobs);
+  launch_field(n, body_abs_.get(), body_q_.get(), odev.get(), uint32_t(nobs), float(k / (4.0 * kPi)),
+               res.get(), stream_);
+  res.download(reinterpret_cast<double2*>(out), nobs, stream_);
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+}  // namespace hfmm_b200

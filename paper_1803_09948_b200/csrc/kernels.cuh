@@ -126,6 +126,26 @@ void launch_gather_charges(const double2* q_caller, const float2* q_caller_f32,
 void launch_scatter_potentials(const float2* near, const float2* far, const uint32_t* index,
                                double2* out_f64, float2* out_f32, uint32_t n, cudaStream_t s);
 
+// ---- BIE operator tail + Krylov vector ops (kernels_krylov.cu) -------------------------------
+void launch_corrections(uint32_t n, int ni, const float2* block, const uint32_t* off, const uint32_t* src,
+                        const float2* delta, const float2* x, float2* y, cudaStream_t s);
+void launch_precondition(uint32_t npatch, int ni, const float2* lu, const int* piv, const float2* in,
+                         float2* out, cudaStream_t s);
+// w -= h_prev * v_prev (skipped when v_prev is null); out[0..1] += <v_next, w> (skipped when null)
+void launch_mgs_step(uint32_t n, float2* w, const float2* v_prev, const double* h_prev,
+                     const float2* v_next, double* out, cudaStream_t s);
+void launch_norm2(uint32_t n, const float2* w, double* out, cudaStream_t s);
+void launch_scale(uint32_t n, const float2* in, float scale, float2* out, cudaStream_t s);
+void launch_update_solution(uint32_t n, int cols, const float2* basis, size_t ld, const double* y,
+                            double2* x, cudaStream_t s);
+void launch_residual(uint32_t n, const double2* b, const float2* ax, float2* r32, double* out,
+                     cudaStream_t s);
+void launch_narrow(uint32_t n, const double2* in, float2* out, cudaStream_t s);
+// out[o] = scale * sum_i q_i e^{i|o-x_i|}/|o-x_i| over k-scaled absolute coordinates
+void launch_field(uint32_t n, const float4* src_pos, const float2* q, const float4* obs, uint32_t nobs,
+                  float scale, double2* out, cudaStream_t s);
+void launch_widen(uint32_t n, const float2* in, double2* out, cudaStream_t s);
+
 // FFMA-only micro-benchmark; returns TFLOP/s (2 flop per FFMA)
 double run_fp32_peak_probe(cudaStream_t s);
 

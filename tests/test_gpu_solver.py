@@ -1,0 +1,118 @@
+"""GPU: the BIE operator tail, block-Jacobi preconditioner, device GMRES and exterior field
+evaluation against the reference's fixtures (tests/golden/solver.npz) and, where the compiled
+reference travelled to the box, against a live mid-size system."""
+import os
+
+import numpy as np
+import pytest
+
+from checkers import have_ref, rel_l2
+from paper_1803_09948_b200 import HfmmCuda, HfmmError
+from paper_1803_09948_b200.workloads import icosphere_patches, sphere_points, charges
+
+pytestmark = pytest.mark.gpu
+G = np.load(os.path.join(os.path.dirname(__file__), "golden", "solver.npz"))
+
+
+def _bie_operator(g, prefix="bie_", **kw):
+    k, order = float(g[prefix + "k"]), int(g[prefix + "order"])
+    op = HfmmCuda(k=k, order=order, ncrit=16, theta=0.4, kd_max=1.0, leaf_cap=-1.0, **kw)
+    op.set_points(g[prefix + "xyz"])
+    op.set_corrections(int(g[prefix + "ni"]), far_weight=g[prefix + "far_weight"],
+                       patch_block=g[prefix + "patch_block"], near_offset=g[prefix + "near_offset"],
+                       near_source=g[prefix + "near_source"], near_delta=g[prefix + "near_delta"],
+                       block_lu=g[prefix + "block_lu"], block_piv=g[prefix + "block_piv"])
+    return op
+
+
+def test_apply_operator_matches_reference_fixture():
+    # reference solver.cpp:314-359: FMM(x * far_weight) + blockdiag + CSR; FP32 tolerance 1e-5
+    op = _bie_operator(G)
+    assert rel_l2(op.matvec(G["bie_x"]), G["bie_y"]) < 1e-5
+
+
+def test_gmres_iteration_parity_with_reference_fixture():
+    # north star: GMRES reaches 1e-4 in the reference's iteration count +-1
+    op = _bie_operator(G)
+    for precondition, it_ref, sol_ref in ((True, int(G["bie_iterations"]), G["bie_sol"]),
+                                          (False, int(G["bie_iterations_noprec"]), G["bie_sol_noprec"])):
+        x, rep = op.gmres(G["bie_rhs"], rtol=1e-4, restart=30, max_iterations=200,
+                          precondition=precondition)
+        assert rep["converged"] and rep["final_residual"] <= 1.05e-4
+        assert abs(rep["iterations"] - it_ref) <= 1, (rep["iterations"], it_ref)
+        assert rel_l2(x, sol_ref) < 2e-3          # both are 1e-4-residual solutions
+        assert np.all(np.diff(rep["residuals"]) <= 1e-12)   # GMRES residual estimates never grow
+
+
+def test_gmres_dense_fixture_and_report():
+    # plain (uncorrected) FMM operator on a point cloud: converges, true residual agrees
+    n, k = 3000, 2.0
+    xyz = sphere_points(n, 8)
+    op = HfmmCuda(k=k, order=8, ncrit=32)
+    op.set_points(xyz)
+    b = charges(n, 8)
+    # shifted operator I*c + A is what converges quickly; emulate with a diagonal block correction
+    blocks = np.full(n, 2000.0 + 0j)   # row sums of the kernel matrix are O(n / 4 pi) ~ 240
+    op.set_corrections(1, patch_block=blocks)
+    x, rep = op.gmres(b, rtol=1e-5, restart=20, max_iterations=200, precondition=False)
+    assert rep["converged"] and rep["iterations"] < 200
+    r = b - op.matvec(x)
+    assert abs(np.linalg.norm(r) / np.linalg.norm(b) - rep["final_residual"]) < 2e-6
+    assert rep["rhs_norm"] == pytest.approx(np.linalg.norm(b), rel=1e-12)
+    with pytest.raises(HfmmError) as e:
+        op.gmres(b, rtol=2.0)
+    assert e.value.kind == "config_error"       # gmres.cpp:25-31
+    x0, rep0 = op.gmres(np.zeros(n), rtol=1e-4)
+    assert rep0["converged"] and rep0["iterations"] == 0 and np.abs(x0).max() == 0
+
+
+def test_scattered_field_matches_reference_fixture():
+    op = _bie_operator(G)
+    f = op.evaluate_field(G["bie_sol"], G["bie_obs"])
+    assert rel_l2(f, G["bie_scattered"]) < 1e-5
+
+
+@pytest.mark.skipif(not have_ref(), reason="compiled reference not on this box")
+def test_midsize_system_against_oracle_gmres(oracle):
+    """320 curved triangles (960 unknowns): system built by the reference, GMRES run (a) on the
+    device and (b) by the oracle's restatement of gmres.cpp over the oracle's FMM matvec."""
+    from checkers import Ref
+
+    k, order = 3.0, 10
+    sysr = Ref().bie(icosphere_patches(2), 1, k, mode=2, use_tree=False)
+    xyz, fw = sysr.samples()
+    corr = sysr.corrections()
+    rhs = sysr.rhs((0, 0, 1))
+    op = HfmmCuda(k=k, order=order, ncrit=16)
+    op.set_points(xyz)
+    op.set_corrections(sysr.ni, far_weight=fw, **corr)
+    f = oracle.fmm(xyz, k, order, ncrit=16, leaf_cap=1.0 / k, theta=0.4, kd_max=1.0)
+
+    def minv(u):
+        return oracle.block_lu_solve(sysr.ni, corr["block_lu"], corr["block_piv"], u)
+
+    def z_cpu(u):       # FP64 operator
+        v = minv(u)
+        return oracle.apply_corrections(sysr.ni, corr["patch_block"], corr["near_offset"],
+                                        corr["near_source"], corr["near_delta"], v, f.matvec(v * fw))
+
+    def z_gpu(u):       # the device operator (FP32 arithmetic) under the oracle's FP64 Krylov loop
+        return op.matvec(minv(u))
+
+    # (1) without restarts the count matches the all-FP64 CPU solve within +-1
+    x_gpu, rep = op.gmres(rhs, rtol=1e-4, restart=300, max_iterations=300)
+    u, rep_o = oracle.gmres(z_cpu, rhs, rtol=1e-4, restart=300, max_iterations=300)
+    assert rep["converged"] and rep_o["converged"]
+    assert abs(rep["iterations"] - rep_o["iterations"]) <= 1, (rep["iterations"], rep_o["iterations"])
+    assert rel_l2(x_gpu, minv(u)) < 2e-3
+    # (2) restart 30: the device solver reproduces, within +-1, what the reference's algorithm does
+    # on the SAME (FP32) operator.  Against the all-FP64 operator this first-kind system (condition
+    # number ~1e5) shifts by a few iterations under ANY 3e-7 operator perturbation — measured:
+    # 56 (FP64) vs 59-60 (FP32 operator, or FP64 operator + 3e-7 noise); see DESIGN.md §7.
+    x30, rep30 = op.gmres(rhs, rtol=1e-4, restart=30, max_iterations=300)
+    _, rep30_same_op = oracle.gmres(z_gpu, rhs, rtol=1e-4, restart=30, max_iterations=300)
+    _, rep30_cpu = oracle.gmres(z_cpu, rhs, rtol=1e-4, restart=30, max_iterations=300)
+    assert rep30["converged"]
+    assert abs(rep30["iterations"] - rep30_same_op["iterations"]) <= 1
+    assert abs(rep30["iterations"] - rep30_cpu["iterations"]) <= 5
+    assert rel_l2(x30, x_gpu) < 2e-3
