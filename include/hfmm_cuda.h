@@ -164,13 +164,31 @@ int hfmm_cuda_get_pairs(hfmm_cuda_t* h, int which, uint32_t* out, uint64_t* coun
  * (M_n^m / L_n^m at index n(n+1)+m); out: n_cells x (P+1)^2 interleaved complex doubles */
 int hfmm_cuda_get_expansions(hfmm_cuda_t* h, int which, double* out);
 
-/* ---- multi-GPU (one process per GPU) ---------------------------------------- */
-/* 128-byte NCCL unique id, created on rank 0 and distributed by the caller's own plumbing */
-int hfmm_cuda_comm_unique_id(uint8_t id[128]);
-/* joins the communicator; must precede set_points.  With nranks > 1, set_points takes the GLOBAL
- * point set on every rank, the Morton order is cut into nranks contiguous ranges by estimated
- * work, and matvec exchanges the locally essential tree over NCCL. */
-int hfmm_cuda_comm_init(hfmm_cuda_t* h, const uint8_t id[128], int rank, int nranks);
+/* ---- multi-GPU: one process per GPU, Morton-partitioned ---------------------
+ * Stands in for the reference's simulated-rank layer (part::distributed_matvec, let.cpp:320-362).
+ * Every rank passes the GLOBAL point set to set_points after set_partition(rank, nranks): the
+ * tree and lists are identical on all ranks, the Morton order is cut into nranks contiguous body
+ * ranges balanced by estimated work, and each rank keeps only the work whose TARGETS it owns.
+ * One matvec is two device phases around one exchange that the caller performs with its own
+ * communicator (torch.distributed over NCCL in bench.py / paper_1803_09948_b200/distributed.py):
+ *   all-gather of the charge slices -> dist_upward -> all-gather of the owned multipole rows
+ *   (hfmm_cuda_partition describes them) -> dist_downward.                                    */
+typedef struct {
+  int32_t rank, nranks;
+  uint64_t n_bodies, body_first, body_count;     /* owned Morton slots                           */
+  int32_t level_first, level_last;               /* levels whose multipoles are exchanged        */
+  uint32_t cell_first[22], cell_count[22];       /* owned cells per level: contiguous rows        */
+  uint32_t level_cell_first[22], level_cell_count[22];
+  uint64_t coeff_stride;                         /* complex FP32 elements per expansion row       */
+  void* multipole_dev;                           /* [n_cells][coeff_stride] float2, device        */
+  uint64_t owned_m2l_pairs, owned_p2p_body_pairs;
+} hfmm_cuda_partition;
+int hfmm_cuda_set_partition(hfmm_cuda_t* h, int rank, int nranks);   /* before set_points */
+int hfmm_cuda_get_partition(hfmm_cuda_t* h, hfmm_cuda_partition* out);
+/* q_morton_dev: n float2, FULL charge vector in Morton order (hfmm_cuda_get_body_order) */
+int hfmm_cuda_dist_upward(hfmm_cuda_t* h, const void* q_morton_dev);
+/* out_morton_dev: n float2 in Morton order; only the owned slots are written */
+int hfmm_cuda_dist_downward(hfmm_cuda_t* h, void* out_morton_dev);
 
 const char* hfmm_cuda_version(void);
 

@@ -47,6 +47,16 @@ class Stats(C.Structure):
         return {n: getattr(self, n) for n, _ in self._fields_}
 
 
+class Partition(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("n_bodies", C.c_uint64),
+                ("body_first", C.c_uint64), ("body_count", C.c_uint64),
+                ("level_first", C.c_int32), ("level_last", C.c_int32),
+                ("cell_first", C.c_uint32 * 22), ("cell_count", C.c_uint32 * 22),
+                ("level_cell_first", C.c_uint32 * 22), ("level_cell_count", C.c_uint32 * 22),
+                ("coeff_stride", C.c_uint64), ("multipole_dev", C.c_void_p),
+                ("owned_m2l_pairs", C.c_uint64), ("owned_p2p_body_pairs", C.c_uint64)]
+
+
 class _GmresConfig(C.Structure):
     _fields_ = [("rtol", C.c_double), ("restart", C.c_int), ("max_iterations", C.c_int),
                 ("precondition", C.c_int)]
@@ -141,6 +151,21 @@ class HfmmCuda:
 
     def sync(self):
         self._check(self.lib.hfmm_cuda_sync(self.h))
+
+    # ---- multi-GPU (Morton partition; see paper_1803_09948_b200/distributed.py)
+    def set_partition(self, rank: int, nranks: int):
+        self._check(self.lib.hfmm_cuda_set_partition(self.h, int(rank), int(nranks)))
+
+    def partition(self) -> Partition:
+        p = Partition()
+        self._check(self.lib.hfmm_cuda_get_partition(self.h, C.byref(p)))
+        return p
+
+    def dist_upward(self, q_morton_dev_ptr: int):
+        self._check(self.lib.hfmm_cuda_dist_upward(self.h, C.c_void_p(q_morton_dev_ptr)))
+
+    def dist_downward(self, out_morton_dev_ptr: int):
+        self._check(self.lib.hfmm_cuda_dist_downward(self.h, C.c_void_p(out_morton_dev_ptr)))
 
     def timer_record(self, slot: int):
         self._check(self.lib.hfmm_cuda_timer_record(self.h, int(slot)))
@@ -252,6 +277,24 @@ def debug_compose_translation(order, k, t, kind, s_src=1.0, s_dst=1.0):
     if rc:
         raise HfmmError(rc, lib.hfmm_cuda_last_error(None).decode())
     return out
+
+
+def debug_partition(xyz, ncrit, leaf_cap, k, theta, kd_max, nranks, n_cells=None):
+    """(first[r], count[r], cell_rank, lcut) of the Morton partition, computed on the host"""
+    lib = load_library()
+    xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+    first = np.zeros(nranks, dtype=np.uint32)
+    count = np.zeros(nranks, dtype=np.uint32)
+    cells = np.full(n_cells or 0, -2, dtype=np.int32)
+    lcut = C.c_int32()
+    vp = lambda a: a.ctypes.data_as(C.c_void_p) if a.size else None
+    rc = lib.hfmm_debug_partition(xyz.ctypes.data_as(_dp), C.c_size_t(xyz.shape[0]), int(ncrit),
+                                  C.c_double(leaf_cap), C.c_double(k), C.c_double(theta),
+                                  C.c_double(kd_max), int(nranks), vp(first), vp(count), vp(cells),
+                                  C.c_size_t(cells.size), C.byref(lcut))
+    if rc:
+        raise HfmmError(rc, lib.hfmm_cuda_last_error(None).decode())
+    return first, count, cells, lcut.value
 
 
 def debug_host_tree(xyz, ncrit, leaf_cap, k, theta, kd_max):

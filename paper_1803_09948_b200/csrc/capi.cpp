@@ -175,13 +175,33 @@ int hfmm_cuda_evaluate_field(hfmm_cuda_t* h, const double* coeff, const double* 
   });
 }
 
-int hfmm_cuda_comm_unique_id(uint8_t*) {
-  g_create_error = "multi-GPU mode not built yet";
-  return HFMM_ERR_INTERNAL;
-}
-int hfmm_cuda_comm_init(hfmm_cuda_t* h, const uint8_t*, int, int) {
+int hfmm_cuda_set_partition(hfmm_cuda_t* h, int rank, int nranks) {
   if (int rc = need(h)) return rc;
-  return guarded(h, [&] { throw Error(HFMM_ERR_INTERNAL, "multi-GPU mode not built yet"); });
+  return guarded(h, [&] { h->engine->set_partition(rank, nranks); });
+}
+
+int hfmm_cuda_get_partition(hfmm_cuda_t* h, hfmm_cuda_partition* out) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] {
+    if (!out) throw Error(HFMM_ERR_CONFIG, "null argument");
+    h->engine->get_partition(out);
+  });
+}
+
+int hfmm_cuda_dist_upward(hfmm_cuda_t* h, const void* q_morton_dev) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] {
+    if (!q_morton_dev) throw Error(HFMM_ERR_CONFIG, "null vector");
+    h->engine->dist_upward(q_morton_dev);
+  });
+}
+
+int hfmm_cuda_dist_downward(hfmm_cuda_t* h, void* out_morton_dev) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] {
+    if (!out_morton_dev) throw Error(HFMM_ERR_CONFIG, "null vector");
+    h->engine->dist_downward(out_morton_dev);
+  });
 }
 
 const char* hfmm_cuda_version(void) { return "hfmm-b200 0.1 (sm_100a)"; }
@@ -231,6 +251,30 @@ int hfmm_debug_host_tree(const double* xyz, size_t n, int ncrit, double leaf_cap
         p2p_out[2 * i] = p.p2p_t[i];
         p2p_out[2 * i + 1] = p.p2p_s[i];
       }
+  });
+}
+
+// Morton partition of the host builder without a device: per-rank owned body ranges and
+// (optionally) the owning rank of every cell
+int hfmm_debug_partition(const double* xyz, size_t n, int ncrit, double leaf_cap, double k,
+                         double theta, double kd_max, int nranks, uint32_t* first, uint32_t* count,
+                         int32_t* cell_rank_out, size_t cells_capacity, int32_t* lcut_out) {
+  return guarded(nullptr, [&] {
+    hfmm_b200::TreeArrays t;
+    hfmm_b200::PairLists p;
+    hfmm_b200::build_tree_host(t, xyz, n, ncrit, leaf_cap, 4);
+    hfmm_b200::dual_tree_traversal_host(t, k, theta, kd_max, p, 4);
+    std::vector<int> cell_rank;
+    std::vector<uint32_t> f, c;
+    int lcut = 0;
+    hfmm_b200::compute_morton_partition(t, p, nranks, cell_rank, f, c, lcut);
+    for (int r = 0; r < nranks; ++r) {
+      first[r] = f[r];
+      count[r] = c[r];
+    }
+    if (cell_rank_out && cells_capacity >= cell_rank.size())
+      for (size_t i = 0; i < cell_rank.size(); ++i) cell_rank_out[i] = cell_rank[i];
+    if (lcut_out) *lcut_out = lcut;
   });
 }
 

@@ -131,7 +131,7 @@ Engine::Engine(const hfmm_cuda_config& cfg) : cfg_(cfg) {
   HFMM_CUDA_CHECK(cudaStreamCreateWithFlags(&stream_near_, cudaStreamNonBlocking));
   HFMM_CUDA_CHECK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
   HFMM_CUDA_CHECK(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
-  ev_.resize(12);
+  ev_.resize(14);
   for (auto& e : ev_) HFMM_CUDA_CHECK(cudaEventCreate(&e));
   user_ev_.resize(16);
   for (auto& e : user_ev_) HFMM_CUDA_CHECK(cudaEventCreate(&e));
@@ -211,18 +211,16 @@ void Engine::build_translate_stages(const PairLists& pairs) {
   stats_.m2l_shift_classes = 0;
   if (!have_far_) return;
 
-  lmin_src_ = kMaxLevel + 1;
-  lmin_dst_ = kMaxLevel + 1;
-  std::vector<uint32_t> cls_of_pair(nm2l);
+  std::vector<uint32_t> cls_of_pair, own_src, own_dst;
+  cls_of_pair.reserve(nm2l / size_t(nranks_) + 16);
   std::vector<TranslateClass> classes;
   {
     std::unordered_map<ShiftKey, uint32_t, ShiftKeyHash> ids;
     ids.reserve(1 << 16);
     for (size_t e = 0; e < nm2l; ++e) {
       const uint32_t a = pairs.m2l_t[e], b = pairs.m2l_s[e];
+      if (!owned_[a]) continue;  // this rank translates into its own target cells only
       const int la = t.level[a], lb = t.level[b], lmax = std::max(la, lb);
-      lmin_dst_ = std::min(lmin_dst_, la);
-      lmin_src_ = std::min(lmin_src_, lb);
       auto c = [lmax](uint32_t i, int l) { return int64_t(2 * uint64_t(i) + 1) << (lmax - l); };
       // t = centre(target) - centre(source) in half-sides of level lmax
       const ShiftKey key{int32_t(c(t.ix[a], la) - c(t.ix[b], lb)), int32_t(c(t.iy[a], la) - c(t.iy[b], lb)),
@@ -231,11 +229,14 @@ void Engine::build_translate_stages(const PairLists& pairs) {
       if (fresh)
         classes.push_back(make_class(reg, CoaxKind::m2l, key.dx, key.dy, key.dz, lb, la, lmax,
                                      t.side(lmax) / 2, scale(lb), scale(la)));
-      cls_of_pair[e] = it->second;
+      cls_of_pair.push_back(it->second);
+      own_src.push_back(b);
+      own_dst.push_back(a);
     }
   }
   stats_.m2l_shift_classes = classes.size();
-  upload_stage(m2l_, pairs.m2l_s, pairs.m2l_t, cls_of_pair, classes);
+  owned_m2l_pairs_ = own_src.size();
+  upload_stage(m2l_, own_src, own_dst, cls_of_pair, classes);
 
   // ---- M2M: child level L -> parent, L from the deepest level up to lmin_src+1; the 8 octant
   // shifts per level of the reference (expansion.cpp:200-222).  t = parent - child = -(+-h) per axis.
@@ -245,6 +246,7 @@ void Engine::build_translate_stages(const PairLists& pairs) {
     int cls_of_oct[8];
     std::fill(cls_of_oct, cls_of_oct + 8, -1);
     for (uint32_t c = t.level_offset[L]; c < t.level_offset[L + 1]; ++c) {
+      if (!owned_[c]) continue;
       const int oct = int(t.ix[c] & 1) << 2 | int(t.iy[c] & 1) << 1 | int(t.iz[c] & 1);
       if (cls_of_oct[oct] < 0) {
         int64_t d[3] = {oct & 4 ? -1 : 1, oct & 2 ? -1 : 1, oct & 1 ? -1 : 1};  // parent - child
@@ -286,6 +288,83 @@ void Engine::build_translate_stages(const PairLists& pairs) {
   HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
 }
 
+void Engine::set_partition(int rank, int nranks) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(HFMM_ERR_CONFIG, "rank out of range");
+  rank_ = rank;
+  nranks_ = nranks;
+  have_points_ = false;  // work lists depend on the partition: set_points must follow
+}
+
+// ownership of cells and bodies for this rank (host_tree.cpp: compute_morton_partition)
+void Engine::compute_partition() {
+  const size_t nc = tree_.n_cells();
+  owned_.assign(nc, 1);
+  own_first_ = 0;
+  own_count_ = tree_.n_bodies;
+  std::vector<int> cell_rank;
+  std::vector<uint32_t> first, count;
+  compute_morton_partition(tree_, pairs_, nranks_, cell_rank, first, count, lcut_);
+  if (nranks_ == 1) return;
+  own_first_ = first[rank_];
+  own_count_ = count[rank_];
+  for (size_t c = 0; c < nc; ++c) owned_[c] = cell_rank[c] == rank_;
+}
+
+void Engine::get_partition(hfmm_cuda_partition* out) {
+  require_points();
+  const TreeArrays& t = tree_;
+  *out = hfmm_cuda_partition{};
+  out->rank = rank_;
+  out->nranks = nranks_;
+  out->n_bodies = t.n_bodies;
+  out->body_first = own_first_;
+  out->body_count = own_count_;
+  out->coeff_stride = uint64_t(stride_);
+  out->multipole_dev = have_far_ ? multipole_.get() : nullptr;
+  out->level_first = have_far_ ? lmin_src_ : 0;
+  out->level_last = have_far_ ? t.max_level : -1;
+  out->owned_m2l_pairs = owned_m2l_pairs_;
+  out->owned_p2p_body_pairs = owned_body_pairs_;
+  for (int L = 0; L <= t.max_level && L < 22; ++L) {
+    out->level_cell_first[L] = t.level_offset[L];
+    out->level_cell_count[L] = t.level_offset[L + 1] - t.level_offset[L];
+    uint32_t f = 0xffffffffu, l = 0;
+    for (uint32_t c = t.level_offset[L]; c < t.level_offset[L + 1]; ++c)
+      if (owned_[c]) {
+        f = std::min(f, c);
+        l = std::max(l, c + 1);
+      }
+    out->cell_first[L] = f == 0xffffffffu ? t.level_offset[L] : f;
+    out->cell_count[L] = f == 0xffffffffu ? 0 : l - f;
+    // ownership follows contiguous body ranges, so owned cells of a level are contiguous too
+    for (uint32_t c = out->cell_first[L]; c < out->cell_first[L] + out->cell_count[L]; ++c)
+      if (!owned_[c]) throw Error(HFMM_ERR_STRUCTURAL, "owned cells of a level are not contiguous");
+  }
+}
+
+// distributed matvec, phase 1: q is the FULL charge vector in Morton order (the caller gathered
+// the ranks' slices); runs the near field of the owned leaves and the upward pass of the owned cells
+void Engine::dist_upward(const void* q_morton_dev) {
+  require_points();
+  HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  HFMM_CUDA_CHECK(cudaEventRecord(ev_[8], stream_));
+  HFMM_CUDA_CHECK(cudaMemcpyAsync(body_q_.get(), q_morton_dev, size_t(tree_.n_bodies) * sizeof(float2),
+                                  cudaMemcpyDeviceToDevice, stream_));
+  phase_upward();
+}
+
+// phase 2 (after the caller exchanged the owned multipole rows): M2L / L2L / L2P into the owned
+// cells, then out[slot] = near + far for the owned Morton slots (other slots untouched)
+void Engine::dist_downward(void* out_morton_dev) {
+  require_points();
+  HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  phase_downward();
+  launch_scatter_potentials(near_.get() + own_first_, far_.get() + own_first_,
+                            identity_index() + own_first_, nullptr,
+                            static_cast<float2*>(out_morton_dev), own_count_, stream_);
+  HFMM_CUDA_CHECK(cudaEventRecord(ev_[9], stream_));
+}
+
 void Engine::set_points(const double* xyz, size_t n) {
   HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
   const auto t0 = std::chrono::steady_clock::now();
@@ -296,6 +375,12 @@ void Engine::set_points(const double* xyz, size_t n) {
   const size_t nc = t.n_cells();
   const double k = cfg_.wave_r;
   const int Lf = t.max_level;
+  lmin_src_ = lmin_dst_ = kMaxLevel + 1;
+  for (size_t e = 0; e < pairs_.m2l_t.size(); ++e) {
+    lmin_dst_ = std::min(lmin_dst_, int(t.level[pairs_.m2l_t[e]]));
+    lmin_src_ = std::min(lmin_src_, int(t.level[pairs_.m2l_s[e]]));
+  }
+  compute_partition();
 
   // cells
   std::vector<int4> geom(nc);
@@ -345,10 +430,12 @@ void Engine::set_points(const double* xyz, size_t n) {
            std::llabs(int64_t(geom[a].z) - geom[b].z) <= ha + hb;
   };
   std::vector<uint32_t> off(nleaf + 1, 0), split(nleaf, 0);
-  uint64_t body_pairs = 0;
+  uint64_t body_pairs = 0, owned_body_pairs = 0;
   for (size_t e = 0; e < pairs_.p2p_t.size(); ++e) {
     const uint32_t a = pairs_.p2p_t[e], b = pairs_.p2p_s[e];
     body_pairs += uint64_t(t.body_count[a]) * t.body_count[b];
+    if (!owned_[a]) continue;
+    owned_body_pairs += uint64_t(t.body_count[a]) * t.body_count[b];
     ++off[leaf_slot[a] + 1];
     if (touching(a, b)) ++split[leaf_slot[a]];
   }
@@ -360,6 +447,7 @@ void Engine::set_points(const double* xyz, size_t n) {
     std::vector<uint32_t> cur_touch(off.begin(), off.end() - 1), cur_far(split);
     for (size_t e = 0; e < pairs_.p2p_t.size(); ++e) {
       const uint32_t a = pairs_.p2p_t[e], b = pairs_.p2p_s[e];
+      if (!owned_[a]) continue;
       work[leaf_slot[a]] += t.body_count[b];
       srcs[touching(a, b) ? cur_touch[leaf_slot[a]]++ : cur_far[leaf_slot[a]]++] = b;
     }
@@ -373,6 +461,7 @@ void Engine::set_points(const double* xyz, size_t n) {
   std::vector<uint64_t> tile_work;
   for (size_t i = 0; i < nleaf; ++i) {
     const uint32_t c = t.leaves[i];
+    if (!owned_[c]) continue;
     for (uint32_t b = 0; b < t.body_count[c]; b += 32) {
       const uint32_t nt = std::min<uint32_t>(32, t.body_count[c] - b);
       tiles.push_back({c, b, nt, uint32_t(i)});
@@ -417,6 +506,7 @@ void Engine::set_points(const double* xyz, size_t n) {
   if (have_far_) {
     std::vector<uint32_t> up, down;
     for (uint32_t c : t.leaves) {
+      if (!owned_[c]) continue;
       if (t.level[c] >= lmin_src_) up.push_back(c);
       if (t.level[c] >= lmin_dst_) down.push_back(c);
     }
@@ -445,6 +535,7 @@ void Engine::set_points(const double* xyz, size_t n) {
   stats_.m2l_pairs = pairs_.m2l_t.size();
   stats_.p2p_pairs = pairs_.p2p_t.size();
   stats_.p2p_body_pairs = body_pairs;
+  owned_body_pairs_ = owned_body_pairs;
   stats_.starved_cells = 0;
   stats_.setup_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -455,11 +546,17 @@ void Engine::set_points(const double* xyz, size_t n) {
 // one FMM evaluation, body_q_ (Morton order) -> near_, far_.  The near field runs on its own
 // stream, concurrently with the upward / translation / downward chain.
 void Engine::run_far_and_near() {
+  phase_upward();
+  phase_downward();
+}
+
+void Engine::phase_upward() {
   // per-kernel CUDA events are always recorded on the stream each kernel is launched on (they cost
   // nothing); HFMM_FLAG_PHASE_TIMERS additionally serialises the near field behind the far field
   // so the per-kernel durations are free of overlap
   const bool serial = (cfg_.flags & HFMM_FLAG_PHASE_TIMERS) != 0;
-  uint64_t launches = 0;
+  launches_ = 0;
+  uint64_t& launches = launches_;
   HFMM_CUDA_CHECK(cudaEventRecord(ev_fork_, stream_));
   HFMM_CUDA_CHECK(cudaStreamWaitEvent(stream_near_, ev_fork_, 0));
 
@@ -504,25 +601,41 @@ void Engine::run_far_and_near() {
     ++launches;
     HFMM_CUDA_CHECK(cudaEventRecord(ev_[3], stream_));
 
-    auto run_stage = [&](const TranslateStage& st, const float2* src, float2* dst) {
-      TranslateArgs ta{};
-      ta.items = st.items.get();
-      ta.n_items = st.n_items;
-      ta.classes = st.classes.get();
-      ta.pair_src = st.pair_src.get();
-      ta.pair_dst = st.pair_dst.get();
-      ta.rot_tables = rot_tables_.get();
-      ta.coax_tables = coax_tables_.get();
-      ta.src = src;
-      ta.dst = dst;
-      ta.order = cfg_.order;
-      ta.stride = stride_;
-      ta.schedule = schedule_.get();
-      launch_translate(ta, stream_);
-      if (st.n_items) ++launches;
-    };
     for (const auto& st : m2m_) run_stage(st, multipole_.get(), multipole_.get());
     HFMM_CUDA_CHECK(cudaEventRecord(ev_[4], stream_));
+  }
+}
+
+void Engine::run_stage(const TranslateStage& st, const float2* src, float2* dst) {
+  TranslateArgs ta{};
+  ta.items = st.items.get();
+  ta.n_items = st.n_items;
+  ta.classes = st.classes.get();
+  ta.pair_src = st.pair_src.get();
+  ta.pair_dst = st.pair_dst.get();
+  ta.rot_tables = rot_tables_.get();
+  ta.coax_tables = coax_tables_.get();
+  ta.src = src;
+  ta.dst = dst;
+  ta.order = cfg_.order;
+  ta.stride = stride_;
+  ta.schedule = schedule_.get();
+  launch_translate(ta, stream_);
+  if (st.n_items) ++launches_;
+}
+
+void Engine::phase_downward() {
+  uint64_t& launches = launches_;
+  if (have_far_) {
+    LeafExpansionArgs la{};
+    la.cell_geom = cell_geom_.get();
+    la.cell_body = cell_body_.get();
+    la.body_pos = body_pos_.get();
+    la.level_scale = level_scale_.get();
+    la.order = cfg_.order;
+    la.stride = stride_;
+    la.k = float(cfg_.wave_r);
+    HFMM_CUDA_CHECK(cudaEventRecord(ev_[12], stream_));
     run_stage(m2l_, multipole_.get(), local_.get());
     HFMM_CUDA_CHECK(cudaEventRecord(ev_[5], stream_));
     for (const auto& st : l2l_) run_stage(st, local_.get(), local_.get());
@@ -553,7 +666,7 @@ void Engine::collect_timings() {
   if (have_far_) {
     stats_.p2m_seconds = dt(2, 3);
     stats_.m2m_seconds = dt(3, 4);
-    stats_.m2l_seconds = dt(4, 5);
+    stats_.m2l_seconds = dt(12, 5);
     stats_.l2l_seconds = dt(5, 6);
     stats_.l2p_seconds = dt(6, 7);
   }

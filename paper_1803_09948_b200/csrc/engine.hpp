@@ -30,6 +30,10 @@ class Engine {
   explicit Engine(const hfmm_cuda_config& cfg);
   ~Engine();
 
+  void set_partition(int rank, int nranks);
+  void get_partition(hfmm_cuda_partition* out);
+  void dist_upward(const void* q_morton_dev);
+  void dist_downward(void* out_morton_dev);
   void set_points(const double* xyz, size_t n);
   void matvec_host(const double* q, double* out);
   void matvec_device(const void* q_dev, void* out_dev);
@@ -57,6 +61,10 @@ class Engine {
  private:
   void require_points() const;
   void run_far_and_near();  // body_q_ -> near_, far_
+  void phase_upward();      // near field (own stream) + P2M + M2M
+  void phase_downward();    // M2L + L2L + L2P, joins the near field
+  void run_stage(const TranslateStage& st, const float2* src, float2* dst);
+  void compute_partition();
   void collect_timings();
   void apply_operator_device(const float2* x, float2* y);  // caller order, weights + corrections
   const uint32_t* identity_index();
@@ -68,6 +76,11 @@ class Engine {
   hfmm_cuda_config cfg_;
   double leaf_cap_ = 0;
   int threads_ = 1;
+  // Morton partition (multi-GPU): this rank owns bodies [own_first_, own_first_ + own_count_)
+  int rank_ = 0, nranks_ = 1, lcut_ = 0;
+  uint32_t own_first_ = 0, own_count_ = 0;
+  std::vector<uint8_t> owned_;  // per cell
+  uint64_t owned_m2l_pairs_ = 0, owned_body_pairs_ = 0, launches_ = 0;
   cudaStream_t stream_ = nullptr, stream_near_ = nullptr;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   std::vector<cudaEvent_t> ev_;       // per-kernel timers of the last matvec

@@ -221,4 +221,66 @@ void dual_tree_traversal_host(const TreeArrays& t, double kmag, double theta, do
   }
 }
 
+void compute_morton_partition(const TreeArrays& t, const PairLists& pairs, int nranks,
+                              std::vector<int>& cell_rank, std::vector<uint32_t>& first,
+                              std::vector<uint32_t>& count, int& lcut) {
+  const size_t nc = t.n_cells();
+  int lmin = kMaxLevel + 1;
+  for (size_t e = 0; e < pairs.m2l_t.size(); ++e)
+    lmin = std::min({lmin, int(t.level[pairs.m2l_t[e]]), int(t.level[pairs.m2l_s[e]])});
+  lcut = lmin > kMaxLevel ? 0 : lmin;  // no far field at all: the units are the leaves
+  cell_rank.assign(nc, 0);
+  first.assign(nranks, 0);
+  count.assign(nranks, 0);
+  if (nranks <= 1) {
+    first[0] = 0;
+    count[0] = t.n_bodies;
+    return;
+  }
+  // unit of every cell: its ancestor at level lcut, or itself for shallower leaves
+  const uint32_t none = 0xffffffffu;
+  std::vector<uint32_t> unit(nc, none);
+  for (uint32_t c = 0; c < nc; ++c) {
+    if (t.level[c] == lcut || (t.level[c] < lcut && t.child_count[c] == 0)) unit[c] = c;
+    else if (t.level[c] > lcut) unit[c] = unit[t.parent[c]];
+  }
+  std::vector<double> weight(nc, 0.0);
+  const double w_pair = 1.0, w_m2l = 1600.0;  // kernel time per body pair : per M2L cell pair
+  for (size_t e = 0; e < pairs.p2p_t.size(); ++e) {
+    const uint32_t a = pairs.p2p_t[e], b = pairs.p2p_s[e];
+    weight[unit[a]] += w_pair * double(t.body_count[a]) * double(t.body_count[b]);
+  }
+  for (size_t e = 0; e < pairs.m2l_t.size(); ++e) weight[unit[pairs.m2l_t[e]]] += w_m2l;
+  std::vector<uint32_t> units;
+  for (uint32_t c = 0; c < nc; ++c)
+    if (unit[c] == c) units.push_back(c);
+  std::sort(units.begin(), units.end(),
+            [&](uint32_t x, uint32_t y) { return t.body_first[x] < t.body_first[y]; });
+  double total = 0;
+  for (uint32_t u : units) total += weight[u];
+  // a unit goes to the rank whose share contains the midpoint of its weight interval; ranks are
+  // monotone in Morton order, so every rank's units (and bodies) are contiguous
+  std::vector<int> unit_rank(nc, -1);
+  double acc = 0;
+  int prev = 0;
+  for (uint32_t u : units) {
+    const double mid = acc + 0.5 * weight[u];
+    int r = total > 0 ? int(mid / total * nranks) : 0;
+    r = std::min(std::max(r, prev), nranks - 1);
+    unit_rank[u] = prev = r;
+    acc += weight[u];
+  }
+  // body ranges: rank r starts where its first unit starts; empty ranks get empty ranges
+  std::vector<uint32_t> start(nranks + 1, t.n_bodies);
+  for (auto it = units.rbegin(); it != units.rend(); ++it) start[unit_rank[*it]] = t.body_first[*it];
+  for (int r = nranks - 1; r >= 0; --r)
+    if (start[r] > start[r + 1]) start[r] = start[r + 1];
+  start[0] = 0;
+  for (int r = 0; r < nranks; ++r) {
+    first[r] = start[r];
+    count[r] = start[r + 1] - start[r];
+  }
+  for (uint32_t c = 0; c < nc; ++c) cell_rank[c] = unit[c] == none ? -1 : unit_rank[unit[c]];
+}
+
 }  // namespace hfmm_b200

@@ -53,4 +53,16 @@ void build_tree_host(TreeArrays& tree, const double* xyz, size_t n, int ncrit, d
 void dual_tree_traversal_host(const TreeArrays& tree, double kmag, double theta, double kd_max,
                               PairLists& out, int threads);
 
+// Cuts the Morton order into nranks contiguous body ranges.  Cut points sit on the
+// boundaries of PARTITION UNITS = the cells of level `lcut` (the coarsest level that takes part in
+// any translation) plus the leaves above it, so every cell that owns an expansion belongs to
+// exactly one rank.  Units are weighed by the work their targets attract — the idea of the
+// reference's w = l + alpha r (partition.cpp:137-141) with both terms in measured kernel time:
+// near-field body pairs and M2L cell pairs.
+//   cell_rank[c] : owning rank, -1 for the cells above the cut (they hold no expansion)
+//   first/count  : owned Morton body range per rank (ranges tile [0, n) in rank order)
+void compute_morton_partition(const TreeArrays& tree, const PairLists& pairs, int nranks,
+                              std::vector<int>& cell_rank, std::vector<uint32_t>& first,
+                              std::vector<uint32_t>& count, int& lcut);
+
 }  // namespace hfmm_b200

@@ -1,0 +1,232 @@
+"""Multi-GPU FMM matvec: one process per GPU, Morton-partitioned targets, torch.distributed for the
+plumbing (NCCL over NVLink on GPUs; gloo in the CPU tests of the host-side logic).
+
+Data flow of one matvec on rank r (stands in for the reference's simulated
+part::distributed_matvec, let.cpp:320-362):
+
+  1. all-gather of the charge slices       q[first_r : first_r+count_r]  ->  full Morton vector
+  2. device phase 1 (dist_upward)          near field of the owned leaves on its own stream,
+                                           P2M + M2M of the owned cells
+  3. all-gather of the owned multipole rows (per level a contiguous row range per rank; this is the
+     locally-essential-tree exchange with the pruning dropped: on NVSwitch a full gather of the
+     multipoles is a few ms — 2.5 M cells x 1.4 KB at BASELINE config 5 — against ~100 ms of compute)
+  4. device phase 2 (dist_downward)        M2L / L2L / L2P into the owned cells, owned outputs
+
+The exchange helpers work on any tensors (CPU tensors under gloo in tests/test_distributed_gloo.py).
+"""
+from __future__ import annotations
+
+import os
+import time
+
+import numpy as np
+
+
+class DevicePointerTensor:
+    """exposes a raw device allocation of the library to torch through __cuda_array_interface__"""
+
+    def __init__(self, ptr: int, n_float32: int):
+        self.__cuda_array_interface__ = {"shape": (n_float32,), "typestr": "<f4",
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def allgather_ranges(dist, buf, ranges, rank, world, scratch=None):
+    """In-place all-gather of rank-owned row ranges of `buf` (first dim).
+
+    ranges[r] = list of (row_first, row_count) owned by rank r, same list length on every rank.
+    Owned rows are packed, exchanged with ONE padded all_gather_into_tensor, and the other ranks'
+    rows unpacked into place.  Returns the scratch buffers for reuse."""
+    import torch
+
+    rows = [sum(c for _, c in rr) for rr in ranges]
+    width = int(np.prod(buf.shape[1:])) if buf.dim() > 1 else 1
+    maxrows = max(max(rows), 1)
+    if scratch is None or scratch[0].shape[0] != maxrows * width:
+        scratch = (torch.empty(maxrows * width, dtype=buf.dtype, device=buf.device),
+                   torch.empty(world * maxrows * width, dtype=buf.dtype, device=buf.device))
+    send, recv = scratch
+    flat = buf.reshape(buf.shape[0], -1)
+    off = 0
+    for f, c in ranges[rank]:
+        if c:
+            send[off * width:(off + c) * width].copy_(flat[f:f + c].reshape(-1))
+            off += c
+    dist.all_gather_into_tensor(recv, send)
+    for r in range(world):
+        if r == rank:
+            continue
+        off = r * maxrows
+        for f, c in ranges[r]:
+            if c:
+                flat[f:f + c].copy_(recv[off * width:(off + c) * width].reshape(c, width))
+                off += c
+    return scratch
+
+
+class ShardedFmm:
+    """The FMM operator of one rank.  Vectors are sharded by Morton range: rank r holds
+    q[first_r : first_r + count_r] of the Morton-ordered charge vector and produces the same slice
+    of the potential."""
+
+    def __init__(self, op, dist, rank: int, world: int, device):
+        import torch
+
+        self.op, self.dist, self.rank, self.world, self.device = op, dist, rank, world, device
+        p = op.partition()
+        self.n = int(p.n_bodies)
+        mine = torch.tensor([p.body_first, p.body_count, p.level_first, p.level_last]
+                            + list(p.cell_first) + list(p.cell_count), dtype=torch.int64, device=device)
+        allp = torch.empty(world * mine.numel(), dtype=torch.int64, device=device)
+        dist.all_gather_into_tensor(allp, mine)
+        allp = allp.reshape(world, -1).cpu().numpy()
+        self.body_ranges = [[(int(a[0]), int(a[1]))] for a in allp]
+        self.first, self.count = self.body_ranges[rank][0]
+        lf, ll = int(p.level_first), int(p.level_last)
+        self.cell_ranges = [[(int(a[4 + L]), int(a[4 + 22 + L])) for L in range(lf, ll + 1)] for a in allp]
+        self.stride = int(p.coeff_stride)
+        n_cells = int(op.stats()["n_cells"])
+        self.q_full = torch.zeros(self.n, 2, dtype=torch.float32, device=device)
+        self.out_full = torch.zeros(self.n, 2, dtype=torch.float32, device=device)
+        self.multipole = None
+        if p.multipole_dev:
+            view = DevicePointerTensor(p.multipole_dev, n_cells * self.stride * 2)
+            self.multipole = torch.as_tensor(view, device=device).reshape(n_cells, self.stride * 2)
+        self._s1 = self._s2 = None
+        self.owned_m2l_pairs = int(p.owned_m2l_pairs)
+        self.owned_p2p_body_pairs = int(p.owned_p2p_body_pairs)
+
+    def matvec(self, q_local):
+        """q_local: (count, 2) float32 device tensor, the owned Morton slice -> same slice of A q"""
+        import torch
+
+        self.q_full[self.first:self.first + self.count].copy_(q_local)
+        self._s1 = allgather_ranges(self.dist, self.q_full, self.body_ranges, self.rank, self.world, self._s1)
+        torch.cuda.current_stream().synchronize()
+        self.op.dist_upward(self.q_full.data_ptr())
+        self.op.sync()
+        if self.multipole is not None:
+            self._s2 = allgather_ranges(self.dist, self.multipole, self.cell_ranges, self.rank,
+                                        self.world, self._s2)
+            torch.cuda.current_stream().synchronize()
+        self.op.dist_downward(self.out_full.data_ptr())
+        self.op.sync()
+        return self.out_full[self.first:self.first + self.count]
+
+
+def emulate_ranks_on_one_device(ops, q_morton):
+    """Runs the sharded matvec of `len(ops)` ranks sequentially on ONE GPU (each op was created with
+    set_partition(r, R) on the same global point set), replacing the two all-gathers by device
+    copies.  Used by the GPU tests: one B200 is all this environment has, and ranks that wait on one
+    another must not be run as concurrent kernels on a single device (B200_PROFILING.md)."""
+    import torch
+
+    parts = [op.partition() for op in ops]
+    n = int(parts[0].n_bodies)
+    dev = q_morton.device
+    out = torch.zeros(n, 2, dtype=torch.float32, device=dev)
+    n_cells = int(ops[0].stats()["n_cells"])
+    stride = int(parts[0].coeff_stride)
+    mp = []
+    for op, p in zip(ops, parts):
+        op.dist_upward(q_morton.data_ptr())     # every rank sees the gathered charges
+        op.sync()
+        mp.append(torch.as_tensor(DevicePointerTensor(p.multipole_dev, n_cells * stride * 2),
+                                  device=dev).reshape(n_cells, stride * 2) if p.multipole_dev else None)
+    for r, (op, p) in enumerate(zip(ops, parts)):     # multipole all-gather
+        if mp[r] is None:
+            continue
+        for s, ps in enumerate(parts):
+            if s == r:
+                continue
+            for L in range(int(ps.level_first), int(ps.level_last) + 1):
+                f, c = int(ps.cell_first[L]), int(ps.cell_count[L])
+                if c:
+                    mp[r][f:f + c].copy_(mp[s][f:f + c])
+    torch.cuda.synchronize()
+    for op, p in zip(ops, parts):
+        op.dist_downward(out.data_ptr())
+        op.sync()
+    return out, parts
+
+
+def bench_distributed(args, cfg, rank, world, metric, unit, workload_config, ClockSampler):
+    """bench.py --gpus N (N > 1): weak scaling, cfg.n points PER GPU, Morton-partitioned"""
+    import torch
+    import torch.distributed as dist
+
+    from . import HfmmCuda
+    from .workloads import charges, make_points
+
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = torch.device("cuda", local)
+    n_total = (args.n or cfg.n) * world
+    xyz = make_points(cfg, n_total)              # every rank builds the same global tree
+    op = HfmmCuda(k=cfg.k, order=cfg.order, ncrit=cfg.ncrit, theta=cfg.theta, kd_max=cfg.kd_max,
+                  leaf_cap=cfg.leaf_cap, device=local)
+    op.set_partition(rank, world)
+    t0 = time.perf_counter()
+    op.set_points(xyz)
+    setup = time.perf_counter() - t0
+    sh = ShardedFmm(op, dist, rank, world, device)
+    order = op.body_order()
+    q = charges(n_total, cfg.seed)[order[sh.first:sh.first + sh.count]]
+    q_local = torch.from_numpy(np.stack([q.real, q.imag], 1).astype(np.float32)).to(device)
+
+    sampler = ClockSampler(local)
+    if rank == 0:
+        sampler.start()
+    for _ in range(args.warmup):
+        sh.matvec(q_local)
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record()
+    for _ in range(args.steps):
+        y = sh.matvec(q_local)
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    wall_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    ms = torch.tensor([max(e0.elapsed_time(e1) / args.steps, 0.0), wall_ms], device=device)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    # end to end: owned charges come from / results go to pinned host memory every step
+    qh = torch.from_numpy(np.stack([q.real, q.imag], 1).astype(np.float32)).pin_memory()
+    oh = torch.empty_like(qh).pin_memory()
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        q_local.copy_(qh, non_blocking=True)
+        oh.copy_(sh.matvec(q_local), non_blocking=True)
+        torch.cuda.synchronize()
+    e2e = torch.tensor([(time.perf_counter() - t0) / args.steps], device=device)
+    dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+    st = op.stats()
+    work = torch.tensor([float(sh.owned_m2l_pairs), float(sh.owned_p2p_body_pairs), float(sh.count)],
+                        device=device)
+    allw = torch.empty(world * 3, device=device)
+    dist.all_gather_into_tensor(allw, work)
+    clocks = sampler.stop() if rank == 0 else None
+    dist.destroy_process_group()
+    if rank != 0:
+        return None
+    ms_step = float(ms[1])     # wall clock between barriers bounds the max over ranks
+    allw = allw.reshape(world, 3).cpu().numpy()
+    return {
+        "metric": metric, "value": n_total / ms_step * 1e-3, "unit": unit, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": workload_config(cfg, n_total, world),
+        "e2e": {"value": n_total / float(e2e[0]) * 1e-6, "unit": unit,
+                "ms_per_step": float(e2e[0]) * 1e3,
+                "h2d_bytes_per_step": int(sh.count) * 8, "d2h_bytes_per_step": int(sh.count) * 8},
+        "gpu_launches": int(st["kernel_launches"]) * args.steps,
+        "exchange": {"charges_bytes_per_rank": n_total * 8,
+                     "multipole_bytes_per_rank": int(sum(c for rr in sh.cell_ranges for _, c in rr)) * sh.stride * 8},
+        "balance": {"m2l_pairs": allw[:, 0].tolist(), "p2p_body_pairs": allw[:, 1].tolist(),
+                    "bodies": allw[:, 2].tolist()},
+        "device_ms_rank_max": float(ms[0]), "setup_seconds": setup, "clocks": clocks,
+    }
