@@ -253,6 +253,10 @@ def run_single(args, cfg):
 def run_multi(args, cfg, rank: int, world: int):
     from paper_1803_09948_b200.distributed import bench_distributed
 
+    if "RANK" not in os.environ:   # single process: stand up a 1-rank group
+        os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                          MASTER_PORT="29517")
+
     line = bench_distributed(args, cfg, rank, world, METRIC, UNIT, workload_config, ClockSampler)
     if rank == 0 and line is not None:
         print(json.dumps(line), flush=True)
@@ -268,6 +272,8 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override the point count (debug)")
     ap.add_argument("--ref-points", type=int, default=16384, help="sample size of the CPU arm")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-distributed", action="store_true",
+                    help="run the N > 1 code path even with one rank (exercises the exchange plumbing)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     rank = int(os.environ.get("RANK", "0"))
@@ -277,7 +283,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, CONFIGS[args.config or "cfg2"], rank)
         return
-    if args.gpus == 1 and world == 1:
+    if args.gpus == 1 and world == 1 and not args.force_distributed:
         run_single(args, cfg)
     else:
         run_multi(args, cfg, rank, world)

@@ -1,0 +1,271 @@
+// include/hfmm_b200.hpp — host C++ mirror of the reference's solver / kernel interface for the FMM
+// matvec path, implemented over the C ABI of include/hfmm_cuda.h (header only, C++17).
+//
+// The reference is a C++20 static library; its three seams for this path are
+//   B3  fmm::fmm_evaluate / fmm::execute_plan        include/hfmm/traversal.hpp:59-67
+//   B2  solver::apply_operator on a DiscreteSystem   include/hfmm/solver.hpp:44-95
+//   B1  solver::MatVec consumed by solver::gmres     include/hfmm/solver.hpp:118-124
+// This header offers the same names, argument meaning and error behaviour (the typed exceptions of
+// include/hfmm/common.hpp:43-55, rethrown from the C status codes) so reference call sites and the
+// reference's own tests read the same against the CUDA path.  When the reference's headers are on
+// the include path (HFMM_COMMON_HPP defined) its own types are used, so the two can be mixed.
+#pragma once
+
+#include <complex>
+#include <cstdint>
+#include <functional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "hfmm_cuda.h"
+
+namespace hfmm_b200 {
+
+#ifdef HFMM_COMMON_HPP
+using ::hfmm::cplx;
+using ::hfmm::Vec3;
+using ::hfmm::WaveNumber;
+using ::hfmm::config_error;
+using ::hfmm::singular_error;
+using ::hfmm::structural_error;
+using ::hfmm::accuracy_error;
+#else
+using cplx = std::complex<double>;
+struct Vec3 {
+  double x = 0, y = 0, z = 0;
+};
+struct WaveNumber {
+  double wave_r = 0, wave_i = 0;
+};
+struct config_error : std::runtime_error { using std::runtime_error::runtime_error; };
+struct singular_error : std::runtime_error { using std::runtime_error::runtime_error; };
+struct structural_error : std::runtime_error { using std::runtime_error::runtime_error; };
+struct accuracy_error : std::runtime_error { using std::runtime_error::runtime_error; };
+#endif
+struct device_error : std::runtime_error { using std::runtime_error::runtime_error; };
+
+namespace detail {
+[[noreturn]] inline void raise(int status, const std::string& msg) {
+  switch (status) {
+    case HFMM_ERR_CONFIG: throw config_error(msg);
+    case HFMM_ERR_SINGULAR: throw singular_error(msg);
+    case HFMM_ERR_STRUCTURAL: throw structural_error(msg);
+    case HFMM_ERR_ACCURACY: throw accuracy_error(msg);
+    case HFMM_ERR_DOMAIN: throw std::domain_error(msg);
+    case HFMM_ERR_DEVICE: throw device_error(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+}  // namespace detail
+
+namespace fmm {
+
+// include/hfmm/traversal.hpp:11-18
+struct TraversalConfig {
+  int s = 128;
+  int c = 128;
+  double theta = 0.5;
+  double kd_max = 1.0;
+  bool deterministic = true;  // accepted for source compatibility; the device path is one stream
+  int threads = 0;            //   "
+};
+
+// include/hfmm/traversal.hpp:44-52
+struct FmmStats {
+  std::size_t m2l_pairs = 0;
+  std::size_t p2p_pairs = 0;
+  std::size_t tasks = 0;
+  std::size_t starved_cells = 0;
+  double upward_seconds = 0;
+  double interaction_seconds = 0;
+  double downward_seconds = 0;
+};
+
+// include/hfmm/octree.hpp:31-39 (the fields the matvec reads and writes)
+struct Body {
+  Vec3 position{};
+  cplx src{};
+  cplx trg{};
+  std::int32_t patch_id = -1;
+  double weight = 1.0;
+  std::uint64_t key = 0;
+  std::uint32_t index = 0;
+};
+
+// Device-resident tree + plan: what build_tree (octree.hpp:84-90) and dual_tree_traversal
+// (traversal.hpp:40-42) produce, kept on the GPU.  Move-only like DiscreteSystem.
+class DeviceTree {
+ public:
+  DeviceTree(const std::vector<Vec3>& points, WaveNumber k, int order, const TraversalConfig& cfg,
+             double max_leaf_diameter = 0, int device = 0, int flags = 0) {
+    hfmm_cuda_config c{};
+    c.wave_r = k.wave_r;
+    c.wave_i = k.wave_i;
+    c.order = order;
+    c.ncrit = cfg.c;
+    c.grain = cfg.s;
+    c.theta = cfg.theta;
+    c.kd_max = cfg.kd_max;
+    c.leaf_cap = max_leaf_diameter;
+    c.device = device;
+    c.flags = flags;
+    if (int rc = hfmm_cuda_create(&h_, &c)) detail::raise(rc, hfmm_cuda_last_error(nullptr));
+    n_ = points.size();
+    static_assert(sizeof(Vec3) == 3 * sizeof(double), "Vec3 must be three packed doubles");
+    check(hfmm_cuda_set_points(h_, reinterpret_cast<const double*>(points.data()), n_));
+  }
+  DeviceTree(const DeviceTree&) = delete;
+  DeviceTree& operator=(const DeviceTree&) = delete;
+  DeviceTree(DeviceTree&& o) noexcept : h_(o.h_), n_(o.n_) { o.h_ = nullptr; }
+  ~DeviceTree() { hfmm_cuda_destroy(h_); }
+
+  std::size_t size() const { return n_; }
+  hfmm_cuda_t* handle() const { return h_; }
+  void check(int rc) const {
+    if (rc) detail::raise(rc, hfmm_cuda_last_error(h_));
+  }
+  FmmStats stats() const {
+    hfmm_cuda_stats s{};
+    check(hfmm_cuda_get_stats(h_, &s));
+    FmmStats f;
+    f.m2l_pairs = s.m2l_pairs;
+    f.p2p_pairs = s.p2p_pairs;
+    f.starved_cells = s.starved_cells;
+    f.upward_seconds = s.upward_seconds;
+    f.interaction_seconds = s.interaction_seconds;
+    f.downward_seconds = s.downward_seconds;
+    return f;
+  }
+
+ private:
+  hfmm_cuda_t* h_ = nullptr;
+  std::size_t n_ = 0;
+};
+
+// execute_plan (traversal.hpp:59-62): src in caller order -> trg in caller order, trg overwritten
+inline FmmStats execute_plan(DeviceTree& tree, const std::vector<cplx>& src, std::vector<cplx>& trg) {
+  if (src.size() != tree.size()) throw config_error("execute_plan: source vector length mismatch");
+  trg.assign(tree.size(), cplx(0));
+  tree.check(hfmm_cuda_matvec(tree.handle(), reinterpret_cast<const double*>(src.data()),
+                              reinterpret_cast<double*>(trg.data())));
+  return tree.stats();
+}
+
+// fmm_evaluate (traversal.hpp:65-67): traversal + execution in one call over Body records
+inline FmmStats fmm_evaluate(std::vector<Body>& bodies, WaveNumber k, int order,
+                             const TraversalConfig& cfg, double max_leaf_diameter = 0) {
+  std::vector<Vec3> pts(bodies.size());
+  std::vector<cplx> src(bodies.size()), trg;
+  for (std::size_t i = 0; i < bodies.size(); ++i) {
+    pts[i] = bodies[i].position;
+    src[i] = bodies[i].src;
+  }
+  DeviceTree tree(pts, k, order, cfg, max_leaf_diameter);
+  FmmStats st = execute_plan(tree, src, trg);
+  for (std::size_t i = 0; i < bodies.size(); ++i) bodies[i].trg = trg[i];
+  return st;
+}
+
+}  // namespace fmm
+
+namespace solver {
+
+// include/hfmm/solver.hpp:97-116
+struct GmresConfig {
+  double rtol = 1e-4;
+  int restart = 50;
+  int max_iterations = 500;
+  bool precondition = true;
+};
+struct SolveReport {
+  int iterations = 0;
+  bool converged = false;
+  bool breakdown = false;
+  double rhs_norm = 0;
+  double final_residual = -1;
+  double final_error = -1;
+  std::vector<double> residuals;
+  std::vector<double> seconds;
+  std::vector<double> matvec_seconds;
+};
+using MatVec = std::function<std::vector<cplx>(const std::vector<cplx>&)>;
+
+// The tree path of a DiscreteSystem (solver.hpp:44-81) on the device: the FMM operator plus the
+// precomputed sparse corrections and block-Jacobi factors the reference's build_system produced
+// (solver.cpp:80-230).  Those builders stay on the host and are passed in unchanged.
+class DeviceOperator {
+ public:
+  DeviceOperator(const std::vector<Vec3>& sample_positions, WaveNumber k, int expansion_order,
+                 const fmm::TraversalConfig& cfg, double leaf_diameter_cap = -1.0, int device = 0)
+      : tree_(sample_positions, k, expansion_order, cfg, leaf_diameter_cap, device) {}
+
+  // DiscreteSystem::far_weight / patch_block / near_* / block_lu / block_piv, any may be empty
+  void set_corrections(int basis_count, const std::vector<double>& far_weight,
+                       const std::vector<cplx>& patch_block, const std::vector<std::uint32_t>& near_offset,
+                       const std::vector<std::uint32_t>& near_source, const std::vector<cplx>& near_delta,
+                       const std::vector<cplx>& block_lu, const std::vector<int>& block_piv) {
+    auto d = [](const std::vector<cplx>& v) { return v.empty() ? nullptr : reinterpret_cast<const double*>(v.data()); };
+    tree_.check(hfmm_cuda_set_corrections(
+        tree_.handle(), basis_count, far_weight.empty() ? nullptr : far_weight.data(), d(patch_block),
+        near_offset.empty() ? nullptr : near_offset.data(), near_source.empty() ? nullptr : near_source.data(),
+        d(near_delta), d(block_lu), block_piv.empty() ? nullptr : block_piv.data()));
+  }
+  std::size_t size() const { return tree_.size(); }
+  fmm::DeviceTree& tree() { return tree_; }
+
+ private:
+  fmm::DeviceTree tree_;
+};
+
+// apply_operator (solver.hpp:95): length check -> config_error (solver.cpp:315-316)
+inline std::vector<cplx> apply_operator(DeviceOperator& sys, const std::vector<cplx>& x) {
+  if (x.size() != sys.size()) throw config_error("apply_operator: coefficient vector length mismatch");
+  std::vector<cplx> y(x.size());
+  sys.tree().check(hfmm_cuda_matvec(sys.tree().handle(), reinterpret_cast<const double*>(x.data()),
+                                    reinterpret_cast<double*>(y.data())));
+  return y;
+}
+
+inline MatVec as_matvec(DeviceOperator& sys) {
+  return [&sys](const std::vector<cplx>& v) { return apply_operator(sys, v); };
+}
+
+// gmres_solve (solver.hpp:129-131, solver.cpp:361-391) with device-resident Krylov vectors
+inline std::pair<std::vector<cplx>, SolveReport> gmres_solve(DeviceOperator& sys, const std::vector<cplx>& rhs,
+                                                             const GmresConfig& cfg) {
+  if (rhs.size() != sys.size()) throw config_error("gmres_solve: right-hand side length mismatch");
+  hfmm_gmres_config c{cfg.rtol, cfg.restart, cfg.max_iterations, cfg.precondition ? 1 : 0};
+  hfmm_gmres_report r{};
+  std::vector<cplx> x(rhs.size());
+  std::vector<double> res(std::size_t(cfg.max_iterations > 0 ? cfg.max_iterations : 0) + 1);
+  sys.tree().check(hfmm_cuda_gmres(sys.tree().handle(), reinterpret_cast<const double*>(rhs.data()),
+                                   reinterpret_cast<double*>(x.data()), &c, &r, res.data(), int(res.size())));
+  SolveReport rep;
+  rep.iterations = r.iterations;
+  rep.converged = r.converged != 0;
+  rep.breakdown = r.breakdown != 0;
+  rep.rhs_norm = r.rhs_norm;
+  rep.final_residual = r.final_residual;
+  res.resize(std::size_t(r.iterations));
+  rep.residuals = std::move(res);
+  rep.matvec_seconds.assign(1, r.matvec_seconds);
+  rep.seconds.assign(1, r.seconds);
+  return {std::move(x), std::move(rep)};
+}
+
+// evaluate_scattered_field (solver.hpp:137-140)
+inline std::vector<cplx> evaluate_scattered_field(DeviceOperator& sys, const std::vector<cplx>& solution,
+                                                  const std::vector<Vec3>& observations) {
+  if (solution.size() != sys.size())
+    throw config_error("evaluate_scattered_field: solution length mismatch");
+  std::vector<cplx> out(observations.size());
+  sys.tree().check(hfmm_cuda_evaluate_field(sys.tree().handle(), reinterpret_cast<const double*>(solution.data()),
+                                            reinterpret_cast<const double*>(observations.data()),
+                                            observations.size(), reinterpret_cast<double*>(out.data())));
+  return out;
+}
+
+}  // namespace solver
+}  // namespace hfmm_b200
