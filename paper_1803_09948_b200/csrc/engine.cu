@@ -11,6 +11,7 @@
 #include <unordered_map>
 
 #include "tables.hpp"
+#include "tree_build.cuh"
 
 namespace hfmm_b200 {
 
@@ -19,26 +20,7 @@ size_t& device_bytes_counter() {
   return bytes;
 }
 
-namespace {
-
-constexpr double kPi = 3.14159265358979323846264338327950288;
-
-template <typename Fn>
-void parallel_for(size_t n, int threads, Fn&& fn) {
-  const size_t parts = std::max<size_t>(1, std::min<size_t>(size_t(std::max(threads, 1)), n));
-  if (parts <= 1) {
-    for (size_t i = 0; i < n; ++i) fn(i);
-    return;
-  }
-  std::vector<std::thread> pool;
-  for (size_t p = 0; p < parts; ++p)
-    pool.emplace_back([&fn, n, p, parts] {
-      for (size_t i = p; i < n; i += parts) fn(i);
-    });
-  for (auto& t : pool) t.join();
-}
-
-int64_t gcd64(int64_t a, int64_t b) {
+static int64_t gcd64(int64_t a, int64_t b) {
   while (b) {
     const int64_t t = a % b;
     a = b;
@@ -76,7 +58,7 @@ struct TableRegistry {
   }
 };
 
-TranslateClass make_class(TableRegistry& reg, CoaxKind kind, int64_t dx, int64_t dy, int64_t dz,
+static TranslateClass make_class(TableRegistry& reg, CoaxKind kind, int64_t dx, int64_t dy, int64_t dz,
                           int lsrc, int ldst, int lunit, double unit, double s_src, double s_dst) {
   TranslateClass c;
   c.rot = reg.rot(dx, dy, dz);
@@ -86,6 +68,26 @@ TranslateClass make_class(TableRegistry& reg, CoaxKind kind, int64_t dx, int64_t
   c.sphi = rxy > 0 ? float(double(dy) / rxy) : 0.0f;
   return c;
 }
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846264338327950288;
+
+template <typename Fn>
+void parallel_for(size_t n, int threads, Fn&& fn) {
+  const size_t parts = std::max<size_t>(1, std::min<size_t>(size_t(std::max(threads, 1)), n));
+  if (parts <= 1) {
+    for (size_t i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (size_t p = 0; p < parts; ++p)
+    pool.emplace_back([&fn, n, p, parts] {
+      for (size_t i = p; i < n; i += parts) fn(i);
+    });
+  for (auto& t : pool) t.join();
+}
+
 
 struct ShiftKey {
   int32_t dx, dy, dz;
@@ -194,52 +196,82 @@ void Engine::upload_stage(TranslateStage& st, const std::vector<uint32_t>& src,
   HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
 }
 
-void Engine::build_translate_stages(const PairLists& pairs) {
+// M2L stage from host pair lists: one class per distinct (lattice shift, level pair), as the
+// reference de-duplicates translation matrices per lattice shift (traversal.cpp:152-166, 233-250)
+void Engine::build_m2l_stage_host(TableRegistry& reg, const PairLists& pairs) {
   const TreeArrays& t = tree_;
-  const int P = cfg_.order;
   const double k = cfg_.wave_r;
-  TableRegistry reg;
   auto scale = [&](int lvl) { return k * t.side(lvl); };
-
-  // ---- M2L: one class per distinct (lattice shift, level pair), as the reference de-duplicates
-  // translation matrices per lattice shift (traversal.cpp:152-166, 233-250)
   const size_t nm2l = pairs.m2l_t.size();
-  have_far_ = nm2l > 0;
-  m2m_.clear();
-  l2l_.clear();
-  m2l_ = TranslateStage{};
-  stats_.m2l_shift_classes = 0;
-  if (!have_far_) return;
-
   std::vector<uint32_t> cls_of_pair, own_src, own_dst;
   cls_of_pair.reserve(nm2l / size_t(nranks_) + 16);
   std::vector<TranslateClass> classes;
-  {
-    std::unordered_map<ShiftKey, uint32_t, ShiftKeyHash> ids;
-    ids.reserve(1 << 16);
-    for (size_t e = 0; e < nm2l; ++e) {
-      const uint32_t a = pairs.m2l_t[e], b = pairs.m2l_s[e];
-      if (!owned_[a]) continue;  // this rank translates into its own target cells only
-      const int la = t.level[a], lb = t.level[b], lmax = std::max(la, lb);
-      auto c = [lmax](uint32_t i, int l) { return int64_t(2 * uint64_t(i) + 1) << (lmax - l); };
-      // t = centre(target) - centre(source) in half-sides of level lmax
-      const ShiftKey key{int32_t(c(t.ix[a], la) - c(t.ix[b], lb)), int32_t(c(t.iy[a], la) - c(t.iy[b], lb)),
-                         int32_t(c(t.iz[a], la) - c(t.iz[b], lb)), int16_t(la), int16_t(lb)};
-      auto [it, fresh] = ids.try_emplace(key, uint32_t(classes.size()));
-      if (fresh)
-        classes.push_back(make_class(reg, CoaxKind::m2l, key.dx, key.dy, key.dz, lb, la, lmax,
-                                     t.side(lmax) / 2, scale(lb), scale(la)));
-      cls_of_pair.push_back(it->second);
-      own_src.push_back(b);
-      own_dst.push_back(a);
-    }
+  std::unordered_map<ShiftKey, uint32_t, ShiftKeyHash> ids;
+  ids.reserve(1 << 16);
+  for (size_t e = 0; e < nm2l; ++e) {
+    const uint32_t a = pairs.m2l_t[e], b = pairs.m2l_s[e];
+    if (!owned_[a]) continue;  // this rank translates into its own target cells only
+    const int la = t.level[a], lb = t.level[b], lmax = std::max(la, lb);
+    auto c = [lmax](uint32_t i, int l) { return int64_t(2 * uint64_t(i) + 1) << (lmax - l); };
+    // t = centre(target) - centre(source) in half-sides of level lmax
+    const ShiftKey key{int32_t(c(t.ix[a], la) - c(t.ix[b], lb)), int32_t(c(t.iy[a], la) - c(t.iy[b], lb)),
+                       int32_t(c(t.iz[a], la) - c(t.iz[b], lb)), int16_t(la), int16_t(lb)};
+    auto [it, fresh] = ids.try_emplace(key, uint32_t(classes.size()));
+    if (fresh)
+      classes.push_back(make_class(reg, CoaxKind::m2l, key.dx, key.dy, key.dz, lb, la, lmax,
+                                   t.side(lmax) / 2, scale(lb), scale(la)));
+    cls_of_pair.push_back(it->second);
+    own_src.push_back(b);
+    own_dst.push_back(a);
   }
   stats_.m2l_shift_classes = classes.size();
   owned_m2l_pairs_ = own_src.size();
   upload_stage(m2l_, own_src, own_dst, cls_of_pair, classes);
+}
 
-  // ---- M2M: child level L -> parent, L from the deepest level up to lmin_src+1; the 8 octant
-  // shifts per level of the reference (expansion.cpp:200-222).  t = parent - child = -(+-h) per axis.
+// M2L stage from the device builder's sorted pairs + run-length-encoded shift classes
+void Engine::build_m2l_stage_device(TableRegistry& reg, const FarClasses& fc) {
+  const TreeArrays& t = tree_;
+  const double k = cfg_.wave_r;
+  auto scale = [&](int lvl) { return k * t.side(lvl); };
+  std::vector<TranslateClass> classes(fc.count.size());
+  std::vector<TranslateItem> items;
+  const uint64_t batch = uint64_t(translate_batch_size(cfg_.order));
+  uint64_t begin = 0;
+  for (size_t c = 0; c < fc.count.size(); ++c) {
+    const int la = fc.lt[c], lb = fc.ls[c], lmax = std::max(la, lb);
+    classes[c] = make_class(reg, CoaxKind::m2l, fc.dx[c], fc.dy[c], fc.dz[c], lb, la, lmax,
+                            t.side(lmax) / 2, scale(lb), scale(la));
+    for (uint64_t b = 0; b < fc.count[c]; b += batch)
+      items.push_back({uint32_t(begin + b), uint32_t(std::min<uint64_t>(batch, fc.count[c] - b)),
+                       uint32_t(c), 0u});
+    begin += fc.count[c];
+  }
+  stats_.m2l_shift_classes = classes.size();
+  owned_m2l_pairs_ = fc.n_owned_pairs;
+  m2l_.n_items = uint32_t(items.size());
+  m2l_.n_pairs = fc.n_owned_pairs;
+  m2l_.items.upload(items, stream_);
+  m2l_.classes.upload(classes, stream_);
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+// M2M / L2L stages per level, translation tables, leaf lists, expansion storage
+void Engine::finish_far_field(TableRegistry& reg) {
+  const TreeArrays& t = tree_;
+  const int P = cfg_.order;
+  const double k = cfg_.wave_r;
+  const size_t nc = t.n_cells();
+  auto scale = [&](int lvl) { return k * t.side(lvl); };
+  m2m_.clear();
+  l2l_.clear();
+  if (!have_far_) {
+    n_p2m_leaves_ = n_l2p_leaves_ = 0;
+    stats_.rotation_tables = stats_.coaxial_tables = 0;
+    return;
+  }
+  // M2M: child level L -> parent, L from the deepest level up to lmin_src+1; the 8 octant shifts
+  // per level of the reference (expansion.cpp:200-222).  t = parent - child = -(+-h) per axis.
   auto level_stage = [&](int L, bool upward) {
     std::vector<uint32_t> src, dst, cls;
     std::vector<TranslateClass> cl;
@@ -269,7 +301,6 @@ void Engine::build_translate_stages(const PairLists& pairs) {
   for (int L = t.max_level; L > lmin_src_; --L) m2m_.push_back(level_stage(L, true));
   for (int L = lmin_dst_ + 1; L <= t.max_level; ++L) l2l_.push_back(level_stage(L, false));
 
-  // ---- tables
   const size_t nrot = reg.rot_cos.size(), ncoax = reg.coax_specs.size();
   stats_.rotation_tables = nrot;
   stats_.coaxial_tables = ncoax;
@@ -285,7 +316,74 @@ void Engine::build_translate_stages(const PairLists& pairs) {
   });
   rot_tables_.upload(rot, stream_);
   coax_tables_.upload(coax, stream_);
+
+  std::vector<uint32_t> up, down;
+  for (uint32_t c : t.leaves) {
+    if (!owned_[c]) continue;
+    if (t.level[c] >= lmin_src_) up.push_back(c);
+    if (t.level[c] >= lmin_dst_) down.push_back(c);
+  }
+  n_p2m_leaves_ = uint32_t(up.size());
+  n_l2p_leaves_ = uint32_t(down.size());
+  p2m_leaves_.upload(up, stream_);
+  l2p_leaves_.upload(down, stream_);
+  multipole_.resize(nc * size_t(stride_));
+  local_.resize(nc * size_t(stride_));
+  multipole_.zero(stream_);
+  local_.zero(stream_);
   HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+// cell geometry on the lattice, level scales, the hi/lo grid
+void Engine::upload_cell_geometry(std::vector<int4>& geom) {
+  const TreeArrays& t = tree_;
+  const size_t nc = t.n_cells();
+  const double k = cfg_.wave_r;
+  const int Lf = t.max_level;
+  geom.resize(nc);
+  std::vector<uint2> cbody(nc);
+  for (size_t c = 0; c < nc; ++c) {
+    const int up = Lf - t.level[c];
+    geom[c] = make_int4(int((2 * t.ix[c] + 1) << up), int((2 * t.iy[c] + 1) << up),
+                        int((2 * t.iz[c] + 1) << up), int(t.level[c]));
+    cbody[c] = make_uint2(t.body_first[c], t.body_count[c]);
+  }
+  level_scale_host_.assign(kMaxLevel + 1, 0.f);
+  for (int l = 0; l <= kMaxLevel; ++l) level_scale_host_[l] = float(k * t.side(l));
+  kunit_d_ = k * t.side(Lf) / 2;
+  kunit_ = float(kunit_d_);
+  // hi/lo split for touching leaves (kernels.cuh): every hi value, hi offset and hi difference
+  // between touching leaves stays below 2^23 grid units, hence exactly representable in FP32
+  double max_leaf_side = 0;
+  for (uint32_t c : t.leaves) max_leaf_side = std::max(max_leaf_side, t.side(t.level[c]));
+  grid_ = std::ldexp(1.0, int(std::ceil(std::log2(4.0 * k * max_leaf_side))) - 23);
+  cell_geom_.upload(geom, stream_);
+  cell_body_.upload(cbody, stream_);
+  level_scale_.upload(level_scale_host_, stream_);
+}
+
+// tiles of <= 32 targets per owned leaf, longest first (the tail of the launch fills with short ones)
+void Engine::build_tiles(const std::vector<uint64_t>& work) {
+  const TreeArrays& t = tree_;
+  std::vector<P2PTile> tiles;
+  std::vector<uint64_t> tile_work;
+  for (size_t i = 0; i < t.leaves.size(); ++i) {
+    const uint32_t c = t.leaves[i];
+    if (!owned_[c]) continue;
+    for (uint32_t b = 0; b < t.body_count[c]; b += 32) {
+      const uint32_t nt = std::min<uint32_t>(32, t.body_count[c] - b);
+      tiles.push_back({c, b, nt, uint32_t(i)});
+      tile_work.push_back(work[i] * nt);
+    }
+  }
+  std::vector<uint32_t> order(tiles.size());
+  std::iota(order.begin(), order.end(), 0u);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](uint32_t x, uint32_t y) { return tile_work[x] > tile_work[y]; });
+  std::vector<P2PTile> sorted(tiles.size());
+  for (size_t i = 0; i < order.size(); ++i) sorted[i] = tiles[order[i]];
+  n_tiles_ = uint32_t(sorted.size());
+  p2p_tiles_.upload(sorted, stream_);
 }
 
 void Engine::set_partition(int rank, int nranks) {
@@ -369,6 +467,93 @@ void Engine::set_points(const double* xyz, size_t n) {
   HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
   const auto t0 = std::chrono::steady_clock::now();
   have_points_ = false;
+  have_weight_ = have_block_ = have_near_ = have_lu_ = false;  // corrections belong to a point set
+  identity_.release();
+  dev_pairs_ = DevicePairs{};
+  pairs_ = PairLists{};
+  stride_ = coeff_stride(cfg_.order);
+  m2l_ = TranslateStage{};
+  if (cfg_.flags & HFMM_FLAG_HOST_TREE)
+    set_points_host(xyz, n);
+  else
+    set_points_device(xyz, n);
+  body_index_.upload(tree_.index, stream_);
+  body_q_.resize(n);
+  near_.resize(n);
+  far_.resize(n);
+  io64_.resize(n);
+  far_.zero(stream_);
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+
+  stats_.n_bodies = n;
+  stats_.n_cells = tree_.n_cells();
+  stats_.n_leaves = tree_.leaves.size();
+  stats_.max_level = uint64_t(tree_.max_level);
+  stats_.starved_cells = 0;
+  stats_.setup_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  stats_.device_bytes = device_bytes_counter();
+  have_points_ = true;
+}
+
+// ---- builder on the device (default): tree_build.cu -------------------------------------------
+void Engine::set_points_device(const double* xyz, size_t n) {
+  const double k = cfg_.wave_r;
+  DeviceBuffer<double> d_xyz;
+  DeviceBuffer<uint32_t> d_index;
+  build_tree_device(tree_, xyz, n, cfg_.ncrit, leaf_cap_, d_xyz, d_index, stream_);
+  const TreeArrays& t = tree_;
+  DeviceCells cells;
+  cells.upload(t, stream_);
+  dual_tree_traversal_device(t, cells, std::abs(k), cfg_.theta, cfg_.kd_max, dev_pairs_, stream_);
+  far_pair_level_range(dev_pairs_, cells, lmin_dst_, lmin_src_, stream_);
+  have_far_ = dev_pairs_.n_far > 0;
+  stats_.m2l_pairs = dev_pairs_.n_far;
+  stats_.p2p_pairs = dev_pairs_.n_near;
+
+  // Morton partition: units on the host, their work weights from the device pair lists
+  const size_t nc = t.n_cells();
+  owned_.assign(nc, 1);
+  own_first_ = 0;
+  own_count_ = t.n_bodies;
+  {
+    std::vector<uint32_t> unit;
+    lcut_ = partition_units(t, lmin_src_, lmin_dst_, unit);
+    if (nranks_ > 1) {
+      std::vector<double> weight;
+      partition_weights_device(dev_pairs_, cells, unit, weight, stream_);
+      std::vector<int> cell_rank;
+      std::vector<uint32_t> first, count;
+      partition_cuts(t, unit, weight, nranks_, cell_rank, first, count);
+      own_first_ = first[rank_];
+      own_count_ = count[rank_];
+      for (size_t c = 0; c < nc; ++c) owned_[c] = cell_rank[c] == rank_;
+    }
+  }
+
+  std::vector<int4> geom;
+  upload_cell_geometry(geom);
+  build_body_arrays_device(t, d_xyz, d_index, k, grid_, body_pos_, body_hi_, body_lo_, body_abs_, stream_);
+
+  NearLists nl;
+  build_near_lists_device(dev_pairs_, t, cells, owned_, p2p_offset_, p2p_split_, p2p_src_, nl, stream_);
+  stats_.p2p_body_pairs = nl.body_pairs;
+  owned_body_pairs_ = nl.owned_body_pairs;
+  build_tiles(nl.work);
+
+  TableRegistry reg;
+  stats_.m2l_shift_classes = 0;
+  owned_m2l_pairs_ = 0;
+  if (have_far_) {
+    FarClasses fc;
+    build_far_classes_device(dev_pairs_, cells, owned_, t.max_level, m2l_.pair_src, m2l_.pair_dst, fc, stream_);
+    build_m2l_stage_device(reg, fc);
+  }
+  finish_far_field(reg);
+}
+
+// ---- builder on the host (HFMM_FLAG_HOST_TREE): host_tree.cpp ---------------------------------
+void Engine::set_points_host(const double* xyz, size_t n) {
   build_tree_host(tree_, xyz, n, cfg_.ncrit, leaf_cap_, threads_);
   dual_tree_traversal_host(tree_, std::abs(cfg_.wave_r), cfg_.theta, cfg_.kd_max, pairs_, threads_);
   const TreeArrays& t = tree_;
@@ -380,29 +565,16 @@ void Engine::set_points(const double* xyz, size_t n) {
     lmin_dst_ = std::min(lmin_dst_, int(t.level[pairs_.m2l_t[e]]));
     lmin_src_ = std::min(lmin_src_, int(t.level[pairs_.m2l_s[e]]));
   }
+  have_far_ = !pairs_.m2l_t.empty();
+  stats_.m2l_pairs = pairs_.m2l_t.size();
+  stats_.p2p_pairs = pairs_.p2p_t.size();
   compute_partition();
 
-  // cells
-  std::vector<int4> geom(nc);
-  std::vector<uint2> cbody(nc);
-  for (size_t c = 0; c < nc; ++c) {
-    const int up = Lf - t.level[c];
-    geom[c] = make_int4(int((2 * t.ix[c] + 1) << up), int((2 * t.iy[c] + 1) << up),
-                        int((2 * t.iz[c] + 1) << up), int(t.level[c]));
-    cbody[c] = make_uint2(t.body_first[c], t.body_count[c]);
-  }
-  level_scale_host_.assign(kMaxLevel + 1, 0.f);
-  for (int l = 0; l <= kMaxLevel; ++l) level_scale_host_[l] = float(k * t.side(l));
-  kunit_d_ = k * t.side(Lf) / 2;
-  kunit_ = float(kunit_d_);
+  std::vector<int4> geom;
+  upload_cell_geometry(geom);
 
-  // bodies: leaf-relative, pre-scaled by k; plus the hi/lo split on a power-of-two grid used for
-  // touching leaves (kernels.cuh).  Every hi value, hi offset and hi difference between touching
-  // leaves stays below 2^23 grid units, hence exactly representable in FP32.
-  double max_leaf_side = 0;
-  for (uint32_t c : t.leaves) max_leaf_side = std::max(max_leaf_side, t.side(t.level[c]));
-  grid_ = std::ldexp(1.0, int(std::ceil(std::log2(4.0 * k * max_leaf_side))) - 23);
-  std::vector<float4> pos(n), pos_hi(n), pos_lo(n);
+  // bodies: leaf-relative, pre-scaled by k, plus the hi/lo split
+  std::vector<float4> pos(n), pos_hi(n), pos_lo(n), abs_pos(n);
   parallel_for(t.leaves.size(), threads_, [&](size_t li) {
     const uint32_t c = t.leaves[li];
     const double s = t.side(t.level[c]);
@@ -418,6 +590,8 @@ void Engine::set_points(const double* xyz, size_t n) {
       pos_lo[b] = make_float4(float(v[0] - h[0]), float(v[1] - h[1]), float(v[2] - h[2]), 0.f);
     }
   });
+  for (size_t i = 0; i < n; ++i)
+    abs_pos[i] = make_float4(float(k * xyz[3 * i]), float(k * xyz[3 * i + 1]), float(k * xyz[3 * i + 2]), 0.f);
 
   // near field: CSR by target leaf, touching source leaves (self included) first
   const size_t nleaf = t.leaves.size();
@@ -457,90 +631,24 @@ void Engine::set_points(const double* xyz, size_t n) {
     std::sort(srcs.begin() + off[i], srcs.begin() + split[i]);
     std::sort(srcs.begin() + split[i], srcs.begin() + off[i + 1]);
   });
-  std::vector<P2PTile> tiles;
-  std::vector<uint64_t> tile_work;
-  for (size_t i = 0; i < nleaf; ++i) {
-    const uint32_t c = t.leaves[i];
-    if (!owned_[c]) continue;
-    for (uint32_t b = 0; b < t.body_count[c]; b += 32) {
-      const uint32_t nt = std::min<uint32_t>(32, t.body_count[c] - b);
-      tiles.push_back({c, b, nt, uint32_t(i)});
-      tile_work.push_back(work[i] * nt);
-    }
-  }
-  {  // longest tiles first: the tail of the launch is filled with short ones
-    std::vector<uint32_t> order(tiles.size());
-    std::iota(order.begin(), order.end(), 0u);
-    std::stable_sort(order.begin(), order.end(),
-                     [&](uint32_t x, uint32_t y) { return tile_work[x] > tile_work[y]; });
-    std::vector<P2PTile> sorted(tiles.size());
-    for (size_t i = 0; i < order.size(); ++i) sorted[i] = tiles[order[i]];
-    tiles.swap(sorted);
-  }
-  n_tiles_ = uint32_t(tiles.size());
+  build_tiles(work);
+  stats_.p2p_body_pairs = body_pairs;
+  owned_body_pairs_ = owned_body_pairs;
 
-  {
-    std::vector<float4> abs_pos(n);
-    for (size_t i = 0; i < n; ++i)
-      abs_pos[i] = make_float4(float(k * xyz[3 * i]), float(k * xyz[3 * i + 1]), float(k * xyz[3 * i + 2]), 0.f);
-    body_abs_.upload(abs_pos, stream_);
-  }
-  have_weight_ = have_block_ = have_near_ = have_lu_ = false;  // corrections belong to a point set
-  identity_.release();
+  body_abs_.upload(abs_pos, stream_);
   body_pos_.upload(pos, stream_);
   body_hi_.upload(pos_hi, stream_);
   body_lo_.upload(pos_lo, stream_);
   p2p_split_.upload(split, stream_);
-  body_index_.upload(t.index, stream_);
-  cell_geom_.upload(geom, stream_);
-  cell_body_.upload(cbody, stream_);
-  level_scale_.upload(level_scale_host_, stream_);
-  p2p_tiles_.upload(tiles, stream_);
   p2p_offset_.upload(off, stream_);
   p2p_src_.upload(srcs, stream_);
   HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
 
-  // far field
-  stride_ = coeff_stride(cfg_.order);
-  build_translate_stages(pairs_);
-  if (have_far_) {
-    std::vector<uint32_t> up, down;
-    for (uint32_t c : t.leaves) {
-      if (!owned_[c]) continue;
-      if (t.level[c] >= lmin_src_) up.push_back(c);
-      if (t.level[c] >= lmin_dst_) down.push_back(c);
-    }
-    n_p2m_leaves_ = uint32_t(up.size());
-    n_l2p_leaves_ = uint32_t(down.size());
-    p2m_leaves_.upload(up, stream_);
-    l2p_leaves_.upload(down, stream_);
-    multipole_.resize(nc * size_t(stride_));
-    local_.resize(nc * size_t(stride_));
-    multipole_.zero(stream_);
-    local_.zero(stream_);
-  } else {
-    n_p2m_leaves_ = n_l2p_leaves_ = 0;
-  }
-  body_q_.resize(n);
-  near_.resize(n);
-  far_.resize(n);
-  io64_.resize(n);
-  far_.zero(stream_);
-  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
-
-  stats_.n_bodies = n;
-  stats_.n_cells = nc;
-  stats_.n_leaves = nleaf;
-  stats_.max_level = uint64_t(t.max_level);
-  stats_.m2l_pairs = pairs_.m2l_t.size();
-  stats_.p2p_pairs = pairs_.p2p_t.size();
-  stats_.p2p_body_pairs = body_pairs;
-  owned_body_pairs_ = owned_body_pairs;
-  stats_.starved_cells = 0;
-  stats_.setup_seconds =
-      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  stats_.device_bytes = device_bytes_counter();
-  have_points_ = true;
+  TableRegistry reg;
+  stats_.m2l_shift_classes = 0;
+  owned_m2l_pairs_ = 0;
+  if (have_far_) build_m2l_stage_host(reg, pairs_);
+  finish_far_field(reg);
 }
 
 // one FMM evaluation, body_q_ (Morton order) -> near_, far_.  The near field runs on its own
@@ -779,6 +887,15 @@ void Engine::get_body_order(uint32_t* out) const {
 
 void Engine::get_pairs(int which, uint32_t* out, uint64_t* count) const {
   require_points();
+  if (!(cfg_.flags & HFMM_FLAG_HOST_TREE)) {  // lists live on the device: copy on demand
+    const uint64_t np = which ? dev_pairs_.n_near : dev_pairs_.n_far;
+    *count = np;
+    if (!out || !np) return;
+    HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
+    HFMM_CUDA_CHECK(cudaMemcpy(out, (which ? dev_pairs_.near : dev_pairs_.far).get(), np * sizeof(uint2),
+                               cudaMemcpyDeviceToHost));
+    return;
+  }
   const auto& tt = which ? pairs_.p2p_t : pairs_.m2l_t;
   const auto& ss = which ? pairs_.p2p_s : pairs_.m2l_s;
   *count = tt.size();

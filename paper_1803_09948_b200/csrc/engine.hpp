@@ -13,8 +13,11 @@
 #include "device_utils.cuh"
 #include "host_tree.hpp"
 #include "kernels.cuh"
+#include "tree_build.cuh"
 
 namespace hfmm_b200 {
+
+struct TableRegistry;
 
 struct TranslateStage {
   // one batched-translation launch: M2L (all levels) or one level of M2M / L2L
@@ -68,7 +71,13 @@ class Engine {
   void collect_timings();
   void apply_operator_device(const float2* x, float2* y);  // caller order, weights + corrections
   const uint32_t* identity_index();
-  void build_translate_stages(const PairLists& pairs);
+  void set_points_host(const double* xyz, size_t n);
+  void set_points_device(const double* xyz, size_t n);
+  void build_m2l_stage_host(TableRegistry& reg, const PairLists& pairs);
+  void build_m2l_stage_device(TableRegistry& reg, const FarClasses& fc);
+  void finish_far_field(TableRegistry& reg);
+  void upload_cell_geometry(std::vector<int4>& geom);
+  void build_tiles(const std::vector<uint64_t>& work);
   void upload_stage(TranslateStage& st, const std::vector<uint32_t>& src,
                     const std::vector<uint32_t>& dst, const std::vector<uint32_t>& cls_of_pair,
                     const std::vector<TranslateClass>& classes);
@@ -90,7 +99,8 @@ class Engine {
 
   // host mirrors kept for introspection
   TreeArrays tree_;
-  PairLists pairs_;
+  PairLists pairs_;        // host builder only
+  DevicePairs dev_pairs_;  // device builder only
   bool have_points_ = false;
   hfmm_cuda_stats stats_{};
 

@@ -49,15 +49,7 @@ uint64_t morton_key21(const double p[3], const double lo[3], double width) {
   return key;
 }
 
-void build_tree_host(TreeArrays& t, const double* xyz, size_t n, int ncrit, double leaf_cap,
-                     int threads) {
-  if (n == 0) throw Error(HFMM_ERR_CONFIG, "no bodies to enclose");
-  if (ncrit < 1) throw Error(HFMM_ERR_CONFIG, "leaf capacity must be at least 1");
-  if (n >= (size_t(1) << 32)) throw Error(HFMM_ERR_CONFIG, "body count exceeds 32-bit indexing");
-  t = TreeArrays{};
-  t.n_bodies = uint32_t(n);
-
-  // cubified bounding box with the 1e-12 pad (reference: src/octree.cpp:53-70)
+void enclosing_box_host(const double* xyz, size_t n, double box_lo[3], double& width) {
   double lo[3] = {xyz[0], xyz[1], xyz[2]}, hi[3] = {xyz[0], xyz[1], xyz[2]};
   for (size_t i = 0; i < n; ++i)
     for (int a = 0; a < 3; ++a) {
@@ -69,8 +61,20 @@ void build_tree_host(TreeArrays& t, const double* xyz, size_t n, int ncrit, doub
   double w = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]});
   if (w <= 0) w = 1;
   w *= 1 + 1e-12;
-  for (int a = 0; a < 3; ++a) t.lo[a] = (lo[a] + hi[a]) / 2.0 - w / 2;
-  t.width = w;
+  for (int a = 0; a < 3; ++a) box_lo[a] = (lo[a] + hi[a]) / 2.0 - w / 2;
+  width = w;
+}
+
+void build_tree_host(TreeArrays& t, const double* xyz, size_t n, int ncrit, double leaf_cap,
+                     int threads) {
+  if (n == 0) throw Error(HFMM_ERR_CONFIG, "no bodies to enclose");
+  if (ncrit < 1) throw Error(HFMM_ERR_CONFIG, "leaf capacity must be at least 1");
+  if (n >= (size_t(1) << 32)) throw Error(HFMM_ERR_CONFIG, "body count exceeds 32-bit indexing");
+  t = TreeArrays{};
+  t.n_bodies = uint32_t(n);
+
+  enclosing_box_host(xyz, n, t.lo, t.width);
+  const double w = t.width;
 
   // keys, then order by (key, caller index) (reference: src/octree.cpp:164-171)
   struct KI {
@@ -221,36 +225,31 @@ void dual_tree_traversal_host(const TreeArrays& t, double kmag, double theta, do
   }
 }
 
-void compute_morton_partition(const TreeArrays& t, const PairLists& pairs, int nranks,
-                              std::vector<int>& cell_rank, std::vector<uint32_t>& first,
-                              std::vector<uint32_t>& count, int& lcut) {
+int partition_units(const TreeArrays& t, int lmin_src, int lmin_dst, std::vector<uint32_t>& unit) {
   const size_t nc = t.n_cells();
-  int lmin = kMaxLevel + 1;
-  for (size_t e = 0; e < pairs.m2l_t.size(); ++e)
-    lmin = std::min({lmin, int(t.level[pairs.m2l_t[e]]), int(t.level[pairs.m2l_s[e]])});
-  lcut = lmin > kMaxLevel ? 0 : lmin;  // no far field at all: the units are the leaves
-  cell_rank.assign(nc, 0);
-  first.assign(nranks, 0);
-  count.assign(nranks, 0);
-  if (nranks <= 1) {
-    first[0] = 0;
-    count[0] = t.n_bodies;
-    return;
-  }
-  // unit of every cell: its ancestor at level lcut, or itself for shallower leaves
+  const int lmin = std::min(lmin_src, lmin_dst);
+  const int lcut = lmin > kMaxLevel ? 0 : lmin;  // no far field at all: the units are the leaves
   const uint32_t none = 0xffffffffu;
-  std::vector<uint32_t> unit(nc, none);
+  unit.assign(nc, none);
   for (uint32_t c = 0; c < nc; ++c) {
     if (t.level[c] == lcut || (t.level[c] < lcut && t.child_count[c] == 0)) unit[c] = c;
     else if (t.level[c] > lcut) unit[c] = unit[t.parent[c]];
   }
-  std::vector<double> weight(nc, 0.0);
-  const double w_pair = 1.0, w_m2l = 1600.0;  // kernel time per body pair : per M2L cell pair
-  for (size_t e = 0; e < pairs.p2p_t.size(); ++e) {
-    const uint32_t a = pairs.p2p_t[e], b = pairs.p2p_s[e];
-    weight[unit[a]] += w_pair * double(t.body_count[a]) * double(t.body_count[b]);
+  return lcut;
+}
+
+void partition_cuts(const TreeArrays& t, const std::vector<uint32_t>& unit,
+                    const std::vector<double>& weight, int nranks, std::vector<int>& cell_rank,
+                    std::vector<uint32_t>& first, std::vector<uint32_t>& count) {
+  const size_t nc = t.n_cells();
+  const uint32_t none = 0xffffffffu;
+  cell_rank.assign(nc, 0);
+  first.assign(nranks, 0);
+  count.assign(nranks, 0);
+  if (nranks <= 1) {
+    count[0] = t.n_bodies;
+    return;
   }
-  for (size_t e = 0; e < pairs.m2l_t.size(); ++e) weight[unit[pairs.m2l_t[e]]] += w_m2l;
   std::vector<uint32_t> units;
   for (uint32_t c = 0; c < nc; ++c)
     if (unit[c] == c) units.push_back(c);
@@ -281,6 +280,27 @@ void compute_morton_partition(const TreeArrays& t, const PairLists& pairs, int n
     count[r] = start[r + 1] - start[r];
   }
   for (uint32_t c = 0; c < nc; ++c) cell_rank[c] = unit[c] == none ? -1 : unit_rank[unit[c]];
+}
+
+void compute_morton_partition(const TreeArrays& t, const PairLists& pairs, int nranks,
+                              std::vector<int>& cell_rank, std::vector<uint32_t>& first,
+                              std::vector<uint32_t>& count, int& lcut) {
+  int lmin_src = kMaxLevel + 1, lmin_dst = kMaxLevel + 1;
+  for (size_t e = 0; e < pairs.m2l_t.size(); ++e) {
+    lmin_dst = std::min(lmin_dst, int(t.level[pairs.m2l_t[e]]));
+    lmin_src = std::min(lmin_src, int(t.level[pairs.m2l_s[e]]));
+  }
+  std::vector<uint32_t> unit;
+  lcut = partition_units(t, lmin_src, lmin_dst, unit);
+  std::vector<double> weight(t.n_cells(), 0.0);
+  if (nranks > 1) {
+    for (size_t e = 0; e < pairs.p2p_t.size(); ++e) {
+      const uint32_t a = pairs.p2p_t[e], b = pairs.p2p_s[e];
+      weight[unit[a]] += kPartitionPairWeight * double(t.body_count[a]) * double(t.body_count[b]);
+    }
+    for (size_t e = 0; e < pairs.m2l_t.size(); ++e) weight[unit[pairs.m2l_t[e]]] += kPartitionM2lWeight;
+  }
+  partition_cuts(t, unit, weight, nranks, cell_rank, first, count);
 }
 
 }  // namespace hfmm_b200

@@ -46,6 +46,9 @@ struct PairLists {
 // level-21 key of p inside the cubified box (octree.cpp:25-51); throws Error(HFMM_ERR_DOMAIN)
 uint64_t morton_key21(const double p[3], const double lo[3], double width);
 
+// cubified bounding box with the 1e-12 pad (reference src/octree.cpp:53-70); throws on non-finite input
+void enclosing_box_host(const double* xyz, size_t n, double lo[3], double& width);
+
 // throws Error(HFMM_ERR_CONFIG) on n == 0 / ncrit < 1
 void build_tree_host(TreeArrays& tree, const double* xyz, size_t n, int ncrit, double leaf_cap,
                      int threads);
@@ -61,6 +64,15 @@ void dual_tree_traversal_host(const TreeArrays& tree, double kmag, double theta,
 // near-field body pairs and M2L cell pairs.
 //   cell_rank[c] : owning rank, -1 for the cells above the cut (they hold no expansion)
 //   first/count  : owned Morton body range per rank (ranges tile [0, n) in rank order)
+// the pieces of compute_morton_partition, so the device builder can supply the weights:
+//   partition_units -> unit cell of every cell (0xffffffff above the cut), returns lcut
+//   partition_cuts  -> ranks from per-unit weights
+inline constexpr double kPartitionPairWeight = 1.0;   // measured kernel time per near body pair ...
+inline constexpr double kPartitionM2lWeight = 1600.0; // ... against one M2L cell pair
+int partition_units(const TreeArrays& tree, int lmin_src, int lmin_dst, std::vector<uint32_t>& unit);
+void partition_cuts(const TreeArrays& tree, const std::vector<uint32_t>& unit,
+                    const std::vector<double>& weight, int nranks, std::vector<int>& cell_rank,
+                    std::vector<uint32_t>& first, std::vector<uint32_t>& count);
 void compute_morton_partition(const TreeArrays& tree, const PairLists& pairs, int nranks,
                               std::vector<int>& cell_rank, std::vector<uint32_t>& first,
                               std::vector<uint32_t>& count, int& lcut);

@@ -1,0 +1,727 @@
+// tree_build.cu — see tree_build.cuh
+#include "tree_build.cuh"
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "common.hpp"
+
+namespace hfmm_b200 {
+
+namespace {
+
+constexpr int kBlock = 256;
+inline uint32_t grid_for(uint64_t n) { return uint32_t((n + kBlock - 1) / kBlock); }
+
+struct TempStorage {
+  DeviceBuffer<unsigned char> buf;
+  void* get(size_t bytes) {
+    if (buf.size() < bytes) buf.resize(bytes + (bytes >> 2) + 256);
+    return buf.get();
+  }
+};
+
+// ---- K1: keys (reference src/octree.cpp:25-51) ----------------------------------------------
+__global__ void __launch_bounds__(kBlock)
+morton_keys_kernel(const double* __restrict__ xyz, uint32_t n, double lox, double loy, double loz,
+                   double scale, uint64_t* __restrict__ key, uint32_t* __restrict__ idx) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double lo[3] = {lox, loy, loz};
+  const long long nside = 1ll << kMaxLevel;
+  uint64_t g[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    long long v = (long long)(__dmul_rn(__dsub_rn(xyz[3 * size_t(i) + a], lo[a]), scale));
+    v = v < 0 ? 0 : (v >= nside ? nside - 1 : v);
+    g[a] = uint64_t(v);
+  }
+  uint64_t k = 0;
+  for (int b = kMaxLevel - 1; b >= 0; --b)
+    k = k << 3 | ((g[0] >> b & 1) << 2) | ((g[1] >> b & 1) << 1) | (g[2] >> b & 1);
+  key[i] = k;
+  idx[i] = i;
+}
+
+// ---- K2: one level of the top-down split (reference src/octree.cpp:85-137) ------------------
+struct CellArrays {
+  uint8_t* level;
+  uint32_t *ix, *iy, *iz, *body_first, *body_count, *child_first, *child_count, *parent;
+};
+
+__device__ __forceinline__ uint32_t lower_bound_digit(const uint64_t* key, uint32_t lo, uint32_t hi,
+                                                      int shift, uint32_t digit) {
+  while (lo < hi) {
+    const uint32_t mid = lo + ((hi - lo) >> 1);
+    if (uint32_t((key[mid] >> shift) & 7) < digit) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kBlock)
+split_count_kernel(CellArrays c, uint32_t c0, uint32_t c1, int level, int ncrit, bool over_diameter,
+                   const uint64_t* __restrict__ key, uint32_t* __restrict__ nchild,
+                   uint32_t* __restrict__ bounds) {
+  const uint32_t i = c0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= c1) return;
+  const uint32_t first = c.body_first[i], count = c.body_count[i];
+  const bool split = level < kMaxLevel && (int64_t(count) > int64_t(ncrit) || (over_diameter && count > 0));
+  uint32_t nc = 0;
+  if (split) {
+    const int shift = 3 * (kMaxLevel - 1 - level);
+    uint32_t* b = bounds + size_t(i - c0) * 9;
+    b[0] = first;
+    for (uint32_t d = 1; d < 8; ++d) b[d] = lower_bound_digit(key, b[d - 1], first + count, shift, d);
+    b[8] = first + count;
+    for (int d = 0; d < 8; ++d) nc += b[d + 1] > b[d];
+  }
+  nchild[i - c0] = nc;
+}
+
+__global__ void __launch_bounds__(kBlock)
+write_children_kernel(CellArrays c, uint32_t c0, uint32_t c1, int level,
+                      const uint32_t* __restrict__ nchild, const uint32_t* __restrict__ offs,
+                      const uint32_t* __restrict__ bounds) {
+  const uint32_t i = c0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= c1) return;
+  const uint32_t nc = nchild[i - c0];
+  if (nc == 0) {
+    c.child_first[i] = 0;
+    c.child_count[i] = 0;
+    return;
+  }
+  const uint32_t cf = c1 + offs[i - c0];
+  c.child_first[i] = cf;
+  c.child_count[i] = nc;
+  const uint32_t* b = bounds + size_t(i - c0) * 9;
+  uint32_t j = cf;
+  for (uint32_t d = 0; d < 8; ++d) {
+    if (b[d + 1] == b[d]) continue;
+    c.level[j] = uint8_t(level + 1);
+    c.ix[j] = c.ix[i] << 1 | (d >> 2 & 1);
+    c.iy[j] = c.iy[i] << 1 | (d >> 1 & 1);
+    c.iz[j] = c.iz[i] << 1 | (d & 1);
+    c.body_first[j] = b[d];
+    c.body_count[j] = b[d + 1] - b[d];
+    c.parent[j] = i;
+    ++j;
+  }
+}
+
+template <typename T>
+void grow(DeviceBuffer<T>& b, size_t keep, size_t want, cudaStream_t s) {
+  if (b.size() >= want) return;
+  DeviceBuffer<T> nb(want + want / 2);
+  if (keep) HFMM_CUDA_CHECK(cudaMemcpyAsync(nb.get(), b.get(), keep * sizeof(T), cudaMemcpyDeviceToDevice, s));
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
+  b = std::move(nb);
+}
+
+// ---- K3: pair frontier (reference src/traversal.cpp:45-79) -----------------------------------
+struct TraversalGeom {
+  double lo[3];
+  double side[kMaxLevel + 1];
+  double radius[kMaxLevel + 1];
+  unsigned char gated[kMaxLevel + 1];  // k * diameter > kd_max at this level
+  double theta;
+};
+
+struct PairSink {
+  uint2* data;
+  unsigned long long* count;
+  unsigned long long cap;
+};
+
+// reserves `cnt` slots for this lane; one atomic per warp
+__device__ __forceinline__ unsigned long long warp_reserve(unsigned long long* counter, uint32_t cnt) {
+  const int lane = threadIdx.x & 31;
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  unsigned long long base = 0;
+  if (lane == 31 && total) base = atomicAdd(counter, (unsigned long long)total);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  return base + (incl - cnt);
+}
+
+__global__ void __launch_bounds__(kBlock)
+traversal_kernel(const uint2* __restrict__ frontier, unsigned long long n_front, const uint8_t* __restrict__ lvl,
+                 const uint32_t* __restrict__ ix, const uint32_t* __restrict__ iy,
+                 const uint32_t* __restrict__ iz, const uint32_t* __restrict__ child_first,
+                 const uint32_t* __restrict__ child_count, const TraversalGeom g, PairSink next,
+                 PairSink far, PairSink near, int* __restrict__ overflow) {
+  const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = i < n_front;
+  uint32_t a = 0, b = 0, n_far = 0, n_near = 0, n_next = 0;
+  bool split_target = false;
+  if (live) {
+    const uint2 p = frontier[i];
+    a = p.x;
+    b = p.y;
+    const int la = lvl[a], lb = lvl[b];
+    bool adm = !(g.gated[la] || g.gated[lb]);
+    const double ra = g.radius[la], rb = g.radius[lb];
+    if (adm) {
+      // centres as lo + (i + 0.5) * side, differences, norm, threshold: every operation rounded
+      // on its own, the sequence of the reference (octree.cpp:116-119, traversal.cpp:49-50)
+      const double sa = g.side[la], sb = g.side[lb];
+      const double dx = __dsub_rn(__dadd_rn(g.lo[0], __dmul_rn(double(ix[a]) + 0.5, sa)),
+                                  __dadd_rn(g.lo[0], __dmul_rn(double(ix[b]) + 0.5, sb)));
+      const double dy = __dsub_rn(__dadd_rn(g.lo[1], __dmul_rn(double(iy[a]) + 0.5, sa)),
+                                  __dadd_rn(g.lo[1], __dmul_rn(double(iy[b]) + 0.5, sb)));
+      const double dz = __dsub_rn(__dadd_rn(g.lo[2], __dmul_rn(double(iz[a]) + 0.5, sa)),
+                                  __dadd_rn(g.lo[2], __dmul_rn(double(iz[b]) + 0.5, sb)));
+      const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+      adm = __dsqrt_rn(d2) > __ddiv_rn(__dadd_rn(ra, rb), g.theta);
+    }
+    const uint32_t ca = child_count[a], cb = child_count[b];
+    if (adm) n_far = 1;
+    else if (ca == 0 && cb == 0) n_near = 1;
+    else {
+      split_target = ca != 0 && (cb == 0 || ra > rb);  // ties open the source
+      n_next = split_target ? ca : cb;
+    }
+  }
+  const unsigned long long s_far = warp_reserve(far.count, n_far);
+  const unsigned long long s_near = warp_reserve(near.count, n_near);
+  const unsigned long long s_next = warp_reserve(next.count, n_next);
+  if (n_far) {
+    if (s_far < far.cap) far.data[s_far] = make_uint2(a, b);
+    else *overflow = 1;
+  }
+  if (n_near) {
+    if (s_near < near.cap) near.data[s_near] = make_uint2(a, b);
+    else *overflow = 1;
+  }
+  if (n_next) {
+    if (s_next + n_next <= next.cap) {
+      const uint32_t cf = split_target ? child_first[a] : child_first[b];
+      for (uint32_t c = 0; c < n_next; ++c)
+        next.data[s_next + c] = split_target ? make_uint2(cf + c, b) : make_uint2(a, cf + c);
+    } else {
+      *overflow = 1;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kBlock)
+level_range_kernel(const uint2* __restrict__ pairs, unsigned long long n, const uint8_t* __restrict__ lvl,
+                   int* __restrict__ out) {
+  int mt = kMaxLevel + 1, ms = kMaxLevel + 1;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint2 p = pairs[i];
+    mt = min(mt, int(lvl[p.x]));
+    ms = min(ms, int(lvl[p.y]));
+  }
+  atomicMin(out, mt);
+  atomicMin(out + 1, ms);
+}
+
+__global__ void __launch_bounds__(kBlock)
+weights_kernel(const uint2* __restrict__ far, unsigned long long n_far, const uint2* __restrict__ near,
+               unsigned long long n_near, const uint32_t* __restrict__ unit,
+               const uint32_t* __restrict__ body_count, double* __restrict__ weight) {
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n_far; i += stride)
+    atomicAdd(weight + unit[far[i].x], kPartitionM2lWeight);
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n_near; i += stride) {
+    const uint2 p = near[i];
+    atomicAdd(weight + unit[p.x], double(body_count[p.x]) * double(body_count[p.y]));
+  }
+}
+
+// ---- near lists ------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlock)
+near_keys_kernel(const uint2* __restrict__ near, unsigned long long n, const uint8_t* __restrict__ lvl,
+                 const uint32_t* __restrict__ ix, const uint32_t* __restrict__ iy,
+                 const uint32_t* __restrict__ iz, const uint32_t* __restrict__ body_count,
+                 const uint32_t* __restrict__ leaf_slot, const uint8_t* __restrict__ owned, int max_level,
+                 uint64_t* __restrict__ keys, unsigned long long* __restrict__ totals) {
+  const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long bp = 0, obp = 0, own = 0;
+  if (i < n) {
+    const uint2 p = near[i];
+    bp = (unsigned long long)body_count[p.x] * body_count[p.y];
+    uint64_t key = ~uint64_t(0);
+    if (owned[p.x]) {
+      own = 1;
+      obp = bp;
+      // cubes touch iff |centre difference| <= sum of half sides on every axis (lattice integers)
+      const int ua = max_level - int(lvl[p.x]), ub = max_level - int(lvl[p.y]);
+      const long long ha = 1ll << ua, hb = 1ll << ub;
+      auto c = [](uint32_t v, int up) { return (long long)(2ull * v + 1) << up; };
+      const bool touch = llabs(c(ix[p.x], ua) - c(ix[p.y], ub)) <= ha + hb &&
+                         llabs(c(iy[p.x], ua) - c(iy[p.y], ub)) <= ha + hb &&
+                         llabs(c(iz[p.x], ua) - c(iz[p.y], ub)) <= ha + hb;
+      key = uint64_t(leaf_slot[p.x]) << 32 | (touch ? 0u : 0x80000000u) | p.y;
+    }
+    keys[i] = key;
+  }
+  // block totals -> three atomics per warp
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    bp += __shfl_xor_sync(0xffffffffu, bp, o);
+    obp += __shfl_xor_sync(0xffffffffu, obp, o);
+    own += __shfl_xor_sync(0xffffffffu, own, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(totals, bp);
+    atomicAdd(totals + 1, obp);
+    atomicAdd(totals + 2, own);
+  }
+}
+
+__device__ __forceinline__ uint32_t lower_bound_u64(const uint64_t* a, uint32_t n, uint64_t v) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = lo + ((hi - lo) >> 1);
+    if (a[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kBlock)
+near_offsets_kernel(const uint64_t* __restrict__ keys, uint32_t n_owned, uint32_t n_leaf,
+                    uint32_t* __restrict__ offset, uint32_t* __restrict__ split) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > n_leaf) return;
+  offset[i] = lower_bound_u64(keys, n_owned, uint64_t(i) << 32);
+  if (i < n_leaf) split[i] = lower_bound_u64(keys, n_owned, uint64_t(i) << 32 | 0x80000000u);
+}
+
+__global__ void __launch_bounds__(kBlock)
+near_sources_kernel(const uint64_t* __restrict__ keys, uint32_t n_owned, uint32_t* __restrict__ src) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n_owned) src[i] = uint32_t(keys[i] & 0x7fffffffu);
+}
+
+__global__ void __launch_bounds__(kBlock)
+near_work_kernel(const uint32_t* __restrict__ offset, const uint32_t* __restrict__ src, uint32_t n_leaf,
+                 const uint32_t* __restrict__ body_count, unsigned long long* __restrict__ work) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_leaf) return;
+  unsigned long long w = 0;
+  for (uint32_t e = offset[i]; e < offset[i + 1]; ++e) w += body_count[src[e]];
+  work[i] = w;
+}
+
+// ---- far classes -----------------------------------------------------------------------------
+// key = lt(5) | ls(5) | dx+2^17 (18) | dy+2^17 (18) | dz+2^17 (18): same (level pair, lattice shift)
+// de-duplication as the reference's lattice_shift (src/traversal.cpp:152-166)
+constexpr int kShiftBias = 1 << 17;
+
+__global__ void __launch_bounds__(kBlock)
+far_keys_kernel(const uint2* __restrict__ far, unsigned long long n, const uint8_t* __restrict__ lvl,
+                const uint32_t* __restrict__ ix, const uint32_t* __restrict__ iy,
+                const uint32_t* __restrict__ iz, const uint8_t* __restrict__ owned,
+                uint64_t* __restrict__ keys, uint64_t* __restrict__ vals, int* __restrict__ flags) {
+  const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint2 p = far[i];
+  uint64_t key = ~uint64_t(0);
+  if (owned[p.x]) {
+    const int la = lvl[p.x], lb = lvl[p.y], lmax = max(la, lb);
+    auto c = [lmax](uint32_t v, int l) { return (long long)(2ull * v + 1) << (lmax - l); };
+    const long long dx = c(ix[p.x], la) - c(ix[p.y], lb), dy = c(iy[p.x], la) - c(iy[p.y], lb),
+                    dz = c(iz[p.x], la) - c(iz[p.y], lb);
+    if (llabs(dx) >= kShiftBias || llabs(dy) >= kShiftBias || llabs(dz) >= kShiftBias) *flags = 1;
+    key = uint64_t(la) << 59 | uint64_t(lb) << 54 | uint64_t(dx + kShiftBias) << 36 |
+          uint64_t(dy + kShiftBias) << 18 | uint64_t(dz + kShiftBias);
+  }
+  keys[i] = key;
+  vals[i] = uint64_t(p.x) << 32 | p.y;
+}
+
+__global__ void __launch_bounds__(kBlock)
+unpack_pairs_kernel(const uint64_t* __restrict__ vals, uint32_t n, uint32_t* __restrict__ src,
+                    uint32_t* __restrict__ dst) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  dst[i] = uint32_t(vals[i] >> 32);
+  src[i] = uint32_t(vals[i]);
+}
+
+// ---- bodies ----------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlock)
+leaf_bodies_kernel(const uint32_t* __restrict__ leaves, uint32_t n_leaf, const uint8_t* __restrict__ lvl,
+                   const uint32_t* __restrict__ ix, const uint32_t* __restrict__ iy,
+                   const uint32_t* __restrict__ iz, const uint32_t* __restrict__ body_first,
+                   const uint32_t* __restrict__ body_count, const double* __restrict__ xyz,
+                   const uint32_t* __restrict__ index, TraversalGeom g, double k, double grid,
+                   float4* __restrict__ pos, float4* __restrict__ hi, float4* __restrict__ lo) {
+  const uint32_t li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (li >= n_leaf) return;
+  const uint32_t c = leaves[li];
+  const double s = g.side[lvl[c]];
+  const double cx = __dadd_rn(g.lo[0], __dmul_rn(double(ix[c]) + 0.5, s)),
+               cy = __dadd_rn(g.lo[1], __dmul_rn(double(iy[c]) + 0.5, s)),
+               cz = __dadd_rn(g.lo[2], __dmul_rn(double(iz[c]) + 0.5, s));
+  const double inv = 1.0 / grid;
+  for (uint32_t b = body_first[c] + lane; b < body_first[c] + body_count[c]; b += 32) {
+    const double* p = xyz + 3 * size_t(index[b]);
+    const double v[3] = {__dmul_rn(k, __dsub_rn(p[0], cx)), __dmul_rn(k, __dsub_rn(p[1], cy)),
+                         __dmul_rn(k, __dsub_rn(p[2], cz))};
+    double h[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) h[a] = __dmul_rn(rint(__dmul_rn(v[a], inv)), grid);
+    pos[b] = make_float4(float(v[0]), float(v[1]), float(v[2]), 0.f);
+    hi[b] = make_float4(float(h[0]), float(h[1]), float(h[2]), 0.f);
+    lo[b] = make_float4(float(v[0] - h[0]), float(v[1] - h[1]), float(v[2] - h[2]), 0.f);
+  }
+}
+
+__global__ void __launch_bounds__(kBlock)
+abs_bodies_kernel(const double* __restrict__ xyz, uint32_t n, double k, float4* __restrict__ out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[i] = make_float4(float(k * xyz[3 * size_t(i)]), float(k * xyz[3 * size_t(i) + 1]),
+                       float(k * xyz[3 * size_t(i) + 2]), 0.f);
+}
+
+TraversalGeom make_geom(const TreeArrays& t, double kmag, double theta, double kd_max) {
+  TraversalGeom g{};
+  const double sqrt3h = std::sqrt(3.0) / 2;
+  for (int a = 0; a < 3; ++a) g.lo[a] = t.lo[a];
+  for (int l = 0; l <= kMaxLevel; ++l) {
+    g.side[l] = t.side(l);
+    g.radius[l] = g.side[l] * sqrt3h;
+    g.gated[l] = kd_max > 0 && kmag * (2 * g.radius[l]) > kd_max;
+  }
+  g.theta = theta;
+  return g;
+}
+
+}  // namespace
+
+void DeviceCells::upload(const TreeArrays& t, cudaStream_t s) {
+  level.upload(t.level, s);
+  ix.upload(t.ix, s);
+  iy.upload(t.iy, s);
+  iz.upload(t.iz, s);
+  child_first.upload(t.child_first, s);
+  child_count.upload(t.child_count, s);
+  body_count.upload(t.body_count, s);
+}
+
+void build_tree_device(TreeArrays& t, const double* xyz, size_t n, int ncrit, double leaf_cap,
+                       DeviceBuffer<double>& d_xyz, DeviceBuffer<uint32_t>& d_index, cudaStream_t s) {
+  if (n == 0) throw Error(HFMM_ERR_CONFIG, "no bodies to enclose");
+  if (ncrit < 1) throw Error(HFMM_ERR_CONFIG, "leaf capacity must be at least 1");
+  if (n >= (size_t(1) << 31)) throw Error(HFMM_ERR_CONFIG, "body count exceeds 31-bit indexing");
+  t = TreeArrays{};
+  t.n_bodies = uint32_t(n);
+  enclosing_box_host(xyz, n, t.lo, t.width);
+  d_xyz.upload(xyz, 3 * n, s);
+
+  // K1
+  DeviceBuffer<uint64_t> key_in(n), key_out(n);
+  DeviceBuffer<uint32_t> idx_in(n);
+  d_index.resize(n);
+  const double scale = double(uint64_t(1) << kMaxLevel) / t.width;
+  morton_keys_kernel<<<grid_for(n), kBlock, 0, s>>>(d_xyz.get(), uint32_t(n), t.lo[0], t.lo[1], t.lo[2],
+                                                    scale, key_in.get(), idx_in.get());
+  HFMM_CUDA_CHECK(cudaGetLastError());
+  TempStorage tmp;
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, key_in.get(), key_out.get(), idx_in.get(), d_index.get(),
+                                  int(n), 0, 3 * kMaxLevel, s);
+  HFMM_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.get(bytes), bytes, key_in.get(), key_out.get(),
+                                                  idx_in.get(), d_index.get(), int(n), 0, 3 * kMaxLevel, s));
+  key_in.release();
+  idx_in.release();
+
+  // K2
+  size_t cap = std::max<size_t>(4096, n / 4 + 1024);
+  DeviceBuffer<uint8_t> level(cap);
+  DeviceBuffer<uint32_t> ix(cap), iy(cap), iz(cap), bf(cap), bc(cap), cf(cap), cc(cap), par(cap);
+  {
+    const uint32_t zero = 0, cnt = uint32_t(n);
+    const uint8_t z8 = 0;
+    HFMM_CUDA_CHECK(cudaMemcpyAsync(level.get(), &z8, 1, cudaMemcpyHostToDevice, s));
+    for (auto* b : {&ix, &iy, &iz, &bf, &cf, &cc, &par})
+      HFMM_CUDA_CHECK(cudaMemcpyAsync(b->get(), &zero, 4, cudaMemcpyHostToDevice, s));
+    HFMM_CUDA_CHECK(cudaMemcpyAsync(bc.get(), &cnt, 4, cudaMemcpyHostToDevice, s));
+    HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
+  }
+  DeviceBuffer<uint32_t> nchild, offs, bounds, total_dev(2);
+  t.level_offset = {0, 1};
+  const double sqrt3 = std::sqrt(3.0);
+  uint32_t ncells = 1;
+  for (int lvl = 0;; ++lvl) {
+    const uint32_t c0 = t.level_offset[lvl], c1 = t.level_offset[lvl + 1], m = c1 - c0;
+    const bool over_diam = leaf_cap > 0 && t.side(lvl) * sqrt3 > leaf_cap;
+    if (nchild.size() < m) {
+      nchild.resize(m + m / 2);
+      offs.resize(m + m / 2 + 1);
+      bounds.resize(size_t(9) * (m + m / 2));
+    }
+    CellArrays ca{level.get(), ix.get(), iy.get(), iz.get(), bf.get(), bc.get(), cf.get(), cc.get(), par.get()};
+    split_count_kernel<<<grid_for(m), kBlock, 0, s>>>(ca, c0, c1, lvl, ncrit, over_diam, key_out.get(),
+                                                     nchild.get(), bounds.get());
+    HFMM_CUDA_CHECK(cudaGetLastError());
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, nchild.get(), offs.get(), int(m), s);
+    HFMM_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp.get(bytes), bytes, nchild.get(), offs.get(), int(m), s));
+    uint32_t last[2];
+    HFMM_CUDA_CHECK(cudaMemcpyAsync(&last[0], offs.get() + (m - 1), 4, cudaMemcpyDeviceToHost, s));
+    HFMM_CUDA_CHECK(cudaMemcpyAsync(&last[1], nchild.get() + (m - 1), 4, cudaMemcpyDeviceToHost, s));
+    HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
+    const uint32_t total = last[0] + last[1];
+    if (size_t(c1) + total > cap) {
+      cap = size_t(c1) + total;
+      grow(level, c1, cap, s);
+      for (auto* b : {&ix, &iy, &iz, &bf, &bc, &cf, &cc, &par}) grow(*b, c1, cap, s);
+      cap = level.size();
+      ca = CellArrays{level.get(), ix.get(), iy.get(), iz.get(), bf.get(), bc.get(), cf.get(), cc.get(), par.get()};
+    }
+    write_children_kernel<<<grid_for(m), kBlock, 0, s>>>(ca, c0, c1, lvl, nchild.get(), offs.get(), bounds.get());
+    HFMM_CUDA_CHECK(cudaGetLastError());
+    ncells = c1 + total;
+    if (total == 0) {
+      t.max_level = lvl;
+      break;
+    }
+    t.level_offset.push_back(ncells);
+  }
+  // host mirror
+  t.level.resize(ncells);
+  for (auto* v : {&t.ix, &t.iy, &t.iz, &t.body_first, &t.body_count, &t.child_first, &t.child_count, &t.parent})
+    v->resize(ncells);
+  t.index.resize(n);
+  level.download(t.level.data(), ncells, s);
+  ix.download(t.ix.data(), ncells, s);
+  iy.download(t.iy.data(), ncells, s);
+  iz.download(t.iz.data(), ncells, s);
+  bf.download(t.body_first.data(), ncells, s);
+  bc.download(t.body_count.data(), ncells, s);
+  cf.download(t.child_first.data(), ncells, s);
+  cc.download(t.child_count.data(), ncells, s);
+  par.download(t.parent.data(), ncells, s);
+  d_index.download(t.index.data(), n, s);
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
+  for (uint32_t c = 0; c < ncells; ++c)
+    if (t.child_count[c] == 0) {
+      t.leaves.push_back(c);
+      if (t.level[c] == kMaxLevel && int64_t(t.body_count[c]) > int64_t(ncrit)) ++t.degenerate_leaves;
+    }
+}
+
+void dual_tree_traversal_device(const TreeArrays& t, const DeviceCells& cells, double kmag, double theta,
+                                double kd_max, DevicePairs& out, cudaStream_t s) {
+  if (!(theta > 0) || theta > 1) throw Error(HFMM_ERR_CONFIG, "opening angle must satisfy 0 < theta <= 1");
+  const TraversalGeom g = make_geom(t, kmag, theta, kd_max);
+  const uint64_t n = t.n_bodies;
+  uint64_t cap_far = 16 * n + (1 << 20), cap_near = 8 * n + (1 << 20), cap_front = 16 * n + (1 << 20);
+  DeviceBuffer<unsigned long long> counters(4);
+  DeviceBuffer<int> overflow(1);
+  for (int attempt = 0; attempt < 6; ++attempt) {
+    out.far.resize(cap_far);
+    out.near.resize(cap_near);
+    DeviceBuffer<uint2> fa(cap_front), fb(cap_front);
+    counters.zero(s);
+    overflow.zero(s);
+    const uint2 root = make_uint2(0, 0);
+    HFMM_CUDA_CHECK(cudaMemcpyAsync(fa.get(), &root, sizeof(uint2), cudaMemcpyHostToDevice, s));
+    unsigned long long n_front = 1;
+    uint2 *cur = fa.get(), *nxt = fb.get();
+    int ovf = 0;
+    while (n_front > 0 && !ovf) {
+      HFMM_CUDA_CHECK(cudaMemsetAsync(counters.get() + 2, 0, sizeof(unsigned long long), s));
+      PairSink next{nxt, counters.get() + 2, cap_front}, far{out.far.get(), counters.get(), cap_far},
+          near{out.near.get(), counters.get() + 1, cap_near};
+      traversal_kernel<<<grid_for(n_front), kBlock, 0, s>>>(
+          cur, n_front, cells.level.get(), cells.ix.get(), cells.iy.get(), cells.iz.get(),
+          cells.child_first.get(), cells.child_count.get(), g, next, far, near, overflow.get());
+      HFMM_CUDA_CHECK(cudaGetLastError());
+      unsigned long long h[3];
+      HFMM_CUDA_CHECK(cudaMemcpyAsync(h, counters.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+      HFMM_CUDA_CHECK(cudaMemcpyAsync(&ovf, overflow.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+      HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
+      out.n_far = h[0];
+      out.n_near = h[1];
+      n_front = h[2];
+      std::swap(cur, nxt);
+    }
+    if (!ovf) return;
+    cap_far *= 2;
+    cap_near *= 2;
+    cap_front *= 2;
+  }
+  throw Error(HFMM_ERR_INTERNAL, "dual tree traversal: pair buffers overflowed repeatedly");
+}
+
+void far_pair_level_range(const DevicePairs& p, const DeviceCells& cells, int& lmin_dst, int& lmin_src,
+                          cudaStream_t s) {
+  int h[2] = {kMaxLevel + 1, kMaxLevel + 1};
+  if (p.n_far) {
+    DeviceBuffer<int> d(2);
+    HFMM_CUDA_CHECK(cudaMemcpyAsync(d.get(), h, sizeof(h), cudaMemcpyHostToDevice, s));
+    level_range_kernel<<<std::min<uint32_t>(grid_for(p.n_far), 2048), kBlock, 0, s>>>(
+        p.far.get(), p.n_far, cells.level.get(), d.get());
+    HFMM_CUDA_CHECK(cudaGetLastError());
+    d.download(h, 2, s);
+    HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
+  }
+  lmin_dst = h[0];
+  lmin_src = h[1];
+}
+
+void partition_weights_device(const DevicePairs& p, const DeviceCells& cells,
+                              const std::vector<uint32_t>& unit_of_cell, std::vector<double>& weight,
+                              cudaStream_t s) {
+  DeviceBuffer<uint32_t> unit;
+  unit.upload(unit_of_cell, s);
+  DeviceBuffer<double> w(unit_of_cell.size());
+  w.zero(s);
+  weights_kernel<<<2048, kBlock, 0, s>>>(p.far.get(), p.n_far, p.near.get(), p.n_near, unit.get(),
+                                         cells.body_count.get(), w.get());
+  HFMM_CUDA_CHECK(cudaGetLastError());
+  weight.resize(unit_of_cell.size());
+  w.download(weight.data(), weight.size(), s);
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+void build_near_lists_device(const DevicePairs& p, const TreeArrays& t, const DeviceCells& cells,
+                             const std::vector<uint8_t>& owned, DeviceBuffer<uint32_t>& offset,
+                             DeviceBuffer<uint32_t>& split, DeviceBuffer<uint32_t>& src, NearLists& out,
+                             cudaStream_t s) {
+  const uint32_t nleaf = uint32_t(t.leaves.size());
+  if (p.n_near >= (uint64_t(1) << 32)) throw Error(HFMM_ERR_CONFIG, "near pair count exceeds 32-bit indexing");
+  std::vector<uint32_t> slot(t.n_cells(), 0xffffffffu);
+  for (uint32_t i = 0; i < nleaf; ++i) slot[t.leaves[i]] = i;
+  DeviceBuffer<uint32_t> d_slot;
+  DeviceBuffer<uint8_t> d_owned;
+  d_slot.upload(slot, s);
+  d_owned.upload(owned, s);
+  DeviceBuffer<uint64_t> keys(std::max<uint64_t>(p.n_near, 1)), sorted(std::max<uint64_t>(p.n_near, 1));
+  DeviceBuffer<unsigned long long> totals(3);
+  totals.zero(s);
+  if (p.n_near) {
+    near_keys_kernel<<<grid_for(p.n_near), kBlock, 0, s>>>(
+        p.near.get(), p.n_near, cells.level.get(), cells.ix.get(), cells.iy.get(), cells.iz.get(),
+        cells.body_count.get(), d_slot.get(), d_owned.get(), t.max_level, keys.get(), totals.get());
+    HFMM_CUDA_CHECK(cudaGetLastError());
+    TempStorage tmp;
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, bytes, keys.get(), sorted.get(), int(p.n_near), 0, 64, s);
+    HFMM_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(tmp.get(bytes), bytes, keys.get(), sorted.get(),
+                                                   int(p.n_near), 0, 64, s));
+  }
+  unsigned long long h[3];
+  totals.download(h, 3, s);
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
+  out.body_pairs = h[0];
+  out.owned_body_pairs = h[1];
+  out.n_owned_pairs = h[2];
+  const uint32_t n_owned = uint32_t(h[2]);
+  offset.resize(nleaf + 1);
+  split.resize(std::max<uint32_t>(nleaf, 1));
+  src.resize(std::max<uint32_t>(n_owned, 1));
+  near_offsets_kernel<<<grid_for(nleaf + 1), kBlock, 0, s>>>(sorted.get(), n_owned, nleaf, offset.get(), split.get());
+  if (n_owned) near_sources_kernel<<<grid_for(n_owned), kBlock, 0, s>>>(sorted.get(), n_owned, src.get());
+  DeviceBuffer<unsigned long long> work(std::max<uint32_t>(nleaf, 1));
+  near_work_kernel<<<grid_for(nleaf), kBlock, 0, s>>>(offset.get(), src.get(), nleaf, cells.body_count.get(), work.get());
+  HFMM_CUDA_CHECK(cudaGetLastError());
+  std::vector<unsigned long long> hw(nleaf);
+  work.download(hw.data(), nleaf, s);
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
+  out.work.assign(hw.begin(), hw.end());
+}
+
+void build_far_classes_device(const DevicePairs& p, const DeviceCells& cells,
+                              const std::vector<uint8_t>& owned, int max_level,
+                              DeviceBuffer<uint32_t>& pair_src, DeviceBuffer<uint32_t>& pair_dst,
+                              FarClasses& out, cudaStream_t s) {
+  (void)max_level;
+  out = FarClasses{};
+  if (p.n_far == 0) return;
+  if (p.n_far >= (uint64_t(1) << 31)) throw Error(HFMM_ERR_CONFIG, "M2L pair count exceeds 31-bit indexing");
+  const int n = int(p.n_far);
+  DeviceBuffer<uint8_t> d_owned;
+  d_owned.upload(owned, s);
+  DeviceBuffer<uint64_t> k_in(n), k_out(n), v_in(n), v_out(n);
+  DeviceBuffer<int> flag(1);
+  flag.zero(s);
+  far_keys_kernel<<<grid_for(n), kBlock, 0, s>>>(p.far.get(), p.n_far, cells.level.get(), cells.ix.get(),
+                                                 cells.iy.get(), cells.iz.get(), d_owned.get(), k_in.get(),
+                                                 v_in.get(), flag.get());
+  HFMM_CUDA_CHECK(cudaGetLastError());
+  TempStorage tmp;
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, k_in.get(), k_out.get(), v_in.get(), v_out.get(), n, 0, 64, s);
+  HFMM_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.get(bytes), bytes, k_in.get(), k_out.get(), v_in.get(),
+                                                  v_out.get(), n, 0, 64, s));
+  k_in.release();
+  v_in.release();
+  DeviceBuffer<uint64_t> uniq(n);
+  DeviceBuffer<int> counts(n), nruns(1);
+  cub::DeviceRunLengthEncode::Encode(nullptr, bytes, k_out.get(), uniq.get(), counts.get(), nruns.get(), n, s);
+  HFMM_CUDA_CHECK(cub::DeviceRunLengthEncode::Encode(tmp.get(bytes), bytes, k_out.get(), uniq.get(),
+                                                     counts.get(), nruns.get(), n, s));
+  int h_flag = 0, h_runs = 0;
+  flag.download(&h_flag, 1, s);
+  nruns.download(&h_runs, 1, s);
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (h_flag)
+    throw Error(HFMM_ERR_INTERNAL,
+                "an M2L lattice shift exceeds the packed key range; rebuild with HFMM_FLAG_HOST_TREE");
+  std::vector<uint64_t> hk(h_runs);
+  std::vector<int> hc(h_runs);
+  uniq.download(hk.data(), h_runs, s);
+  counts.download(hc.data(), h_runs, s);
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
+  for (int r = 0; r < h_runs; ++r) {
+    if (hk[r] == ~uint64_t(0)) continue;  // pairs of targets other ranks own
+    out.lt.push_back(int16_t(hk[r] >> 59));
+    out.ls.push_back(int16_t((hk[r] >> 54) & 31));
+    out.dx.push_back(int32_t((hk[r] >> 36) & 0x3ffff) - kShiftBias);
+    out.dy.push_back(int32_t((hk[r] >> 18) & 0x3ffff) - kShiftBias);
+    out.dz.push_back(int32_t(hk[r] & 0x3ffff) - kShiftBias);
+    out.count.push_back(uint32_t(hc[r]));
+    out.n_owned_pairs += uint64_t(hc[r]);
+  }
+  const uint32_t no = uint32_t(out.n_owned_pairs);
+  pair_src.resize(std::max<uint32_t>(no, 1));
+  pair_dst.resize(std::max<uint32_t>(no, 1));
+  if (no) unpack_pairs_kernel<<<grid_for(no), kBlock, 0, s>>>(v_out.get(), no, pair_src.get(), pair_dst.get());
+  HFMM_CUDA_CHECK(cudaGetLastError());
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+void build_body_arrays_device(const TreeArrays& t, const DeviceBuffer<double>& d_xyz,
+                              const DeviceBuffer<uint32_t>& d_index, double k, double grid,
+                              DeviceBuffer<float4>& pos, DeviceBuffer<float4>& hi, DeviceBuffer<float4>& lo,
+                              DeviceBuffer<float4>& abs_pos, cudaStream_t s) {
+  const uint32_t n = t.n_bodies, nleaf = uint32_t(t.leaves.size());
+  pos.resize(n);
+  hi.resize(n);
+  lo.resize(n);
+  abs_pos.resize(n);
+  DeviceBuffer<uint32_t> leaves, ix, iy, iz, bf, bc;
+  DeviceBuffer<uint8_t> level;
+  leaves.upload(t.leaves, s);
+  level.upload(t.level, s);
+  ix.upload(t.ix, s);
+  iy.upload(t.iy, s);
+  iz.upload(t.iz, s);
+  bf.upload(t.body_first, s);
+  bc.upload(t.body_count, s);
+  const TraversalGeom g = make_geom(t, 0, 1, 0);
+  leaf_bodies_kernel<<<grid_for(uint64_t(nleaf) * 32), kBlock, 0, s>>>(
+      leaves.get(), nleaf, level.get(), ix.get(), iy.get(), iz.get(), bf.get(), bc.get(), d_xyz.get(),
+      d_index.get(), g, k, grid, pos.get(), hi.get(), lo.get());
+  abs_bodies_kernel<<<grid_for(n), kBlock, 0, s>>>(d_xyz.get(), n, k, abs_pos.get());
+  HFMM_CUDA_CHECK(cudaGetLastError());
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+}  // namespace hfmm_b200

@@ -121,3 +121,47 @@ def test_sharded_matvec_equals_single_domain(nranks):
     st = single.stats()
     assert sum(int(p.owned_m2l_pairs) for p in parts) == st["m2l_pairs"]
     assert sum(int(p.owned_p2p_body_pairs) for p in parts) == st["p2p_body_pairs"]
+
+
+def _geo_pairs(cells, pairs):
+    key = lambda c: ((cells[c, 0].astype(np.int64) << 57) | (cells[c, 1].astype(np.int64) << 38)
+                     | (cells[c, 2].astype(np.int64) << 19) | cells[c, 3].astype(np.int64))
+    a = np.stack([key(pairs[:, 0]), key(pairs[:, 1])], 1)
+    return a[np.lexsort((a[:, 1], a[:, 0]))]
+
+
+@pytest.mark.parametrize("case", ["pipeline", "sphere", "plummer", "gate_off"])
+def test_device_built_tree_and_lists_equal_the_reference(case):
+    """Tree and interaction lists built ON THE GPU (tree_build.cu) against the fixtures the
+    reference generated: same Morton order, same cell set, same M2L / P2P pair sets — including the
+    `pipeline` case whose theta = 0.5 lattice produces exact admissibility ties — and the same
+    results as the host builder (HFMM_FLAG_HOST_TREE)."""
+    import os
+
+    from paper_1803_09948_b200.api import HFMM_FLAG_HOST_TREE
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "fmm.npz"))
+    k, order, ncrit, cap, theta, kd = g[f"{case}_params"]
+    kw = dict(k=float(k), order=int(order), ncrit=int(ncrit), theta=float(theta), kd_max=float(kd),
+              leaf_cap=float(cap))
+    dev = HfmmCuda(**kw)
+    dev.set_points(g[f"{case}_xyz"])
+    host = HfmmCuda(flags=HFMM_FLAG_HOST_TREE, **kw)
+    host.set_points(g[f"{case}_xyz"])
+    ref_cells = g[f"{case}_cells"]
+    canon = lambda c: (lambda a: a[np.lexsort(a.T[::-1])])(c[:, :6].astype(np.int64))
+    assert (dev.body_order() == g[f"{case}_order"]).all()
+    assert (canon(dev.cells()) == canon(ref_cells)).all()
+    assert (dev.cells() == host.cells()).all()               # identical level-order numbering
+    for which, name in ((0, "m2l"), (1, "p2p")):
+        ref_pairs = _geo_pairs(ref_cells, g[f"{case}_{name}"])
+        assert (_geo_pairs(dev.cells(), dev.pairs(which)) == ref_pairs).all()
+        assert (_geo_pairs(host.cells(), host.pairs(which)) == ref_pairs).all()
+    sd, sh = dev.stats(), host.stats()
+    for key in ("n_cells", "n_leaves", "max_level", "m2l_pairs", "p2p_pairs", "p2p_body_pairs",
+                "m2l_shift_classes", "rotation_tables", "coaxial_tables"):
+        assert sd[key] == sh[key], key
+    q = g[f"{case}_q"]
+    yd, yh = dev.matvec(q), host.matvec(q)
+    assert rel_l2(yd, g[f"{case}_y"]) < TOL and rel_l2(yh, g[f"{case}_y"]) < TOL
+    assert rel_l2(yd, yh) < 2e-6
