@@ -28,6 +28,9 @@ __constant__ float c_diag[kMaxP + 1];
 __constant__ float c_sub[kMaxP + 1];
 __constant__ float c_a[(kMaxP + 1) * (kMaxP + 2) / 2];
 __constant__ float c_b[(kMaxP + 1) * (kMaxP + 2) / 2];
+// reciprocals of the series denominators j (2n + 2j + 1), n <= kMaxP, j = 1..12
+constexpr int kSeriesTerms = 12;
+__constant__ float c_series[(kMaxP + 1) * kSeriesTerms];
 
 // jhat_n(z; s), n = 0..P, written to out[n * 32] (one shared-memory column per lane)
 __device__ void scaled_bessel(int P, float z, float s, float* out) {
@@ -35,11 +38,13 @@ __device__ void scaled_bessel(int P, float z, float s, float* out) {
     const float h = -0.5f * z * z;
     const float t = z / s;
     float tp = 1.0f;
+    // |term_j / term_{j-1}| <= (z^2/2) / (j (2j+1)): 7 terms reach 1e-9 for z <= 1, 12 for z <= 2
+    const int terms = z <= 1.0f ? 7 : kSeriesTerms;
     for (int n = 0; n <= P; ++n) {
       float term = 1.0f, sum = 1.0f;
-#pragma unroll 4
-      for (int j = 1; j <= 12; ++j) {
-        term *= h / float(j * (2 * n + 2 * j + 1));
+      const float* inv = c_series + n * kSeriesTerms;
+      for (int j = 0; j < terms; ++j) {
+        term *= h * inv[j];
         sum += term;
       }
       out[n * 32] = tp * sum;
@@ -253,6 +258,11 @@ void upload_legendre_constants(const float* diag, const float* sub, const float*
   HFMM_CUDA_CHECK(cudaMemcpyToSymbol(c_sub, sub, sizeof(float) * (order + 1)));
   HFMM_CUDA_CHECK(cudaMemcpyToSymbol(c_a, a, sizeof(float) * tri));
   HFMM_CUDA_CHECK(cudaMemcpyToSymbol(c_b, b, sizeof(float) * tri));
+  float series[(kMaxP + 1) * kSeriesTerms];
+  for (int n = 0; n <= kMaxP; ++n)
+    for (int j = 1; j <= kSeriesTerms; ++j)
+      series[n * kSeriesTerms + j - 1] = float(1.0 / (double(j) * (2 * n + 2 * j + 1)));
+  HFMM_CUDA_CHECK(cudaMemcpyToSymbol(c_series, series, sizeof(series)));
 }
 
 void launch_p2m(const LeafExpansionArgs& a, const float2* body_q, float2* multipole, cudaStream_t s) {
