@@ -143,10 +143,7 @@ Engine::Engine(const hfmm_cuda_config& cfg) : cfg_(cfg) {
   std::vector<float> diag(P + 1), sub(P + 1), a(tri), b(tri);
   build_legendre_coefficients(P, diag.data(), sub.data(), a.data(), b.data());
   upload_legendre_constants(diag.data(), sub.data(), a.data(), b.data(), P);
-  TranslateSchedule sched{};
-  build_translate_schedule(P, &sched);
-  schedule_.upload(&sched, 1, stream_);
-  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  upload_translate_schedule(P);
 }
 
 Engine::~Engine() {
@@ -727,7 +724,6 @@ void Engine::run_stage(const TranslateStage& st, const float2* src, float2* dst)
   ta.dst = dst;
   ta.order = cfg_.order;
   ta.stride = stride_;
-  ta.schedule = schedule_.get();
   launch_translate(ta, stream_);
   if (st.n_items) ++launches_;
 }
@@ -948,11 +944,12 @@ void compose_dense_from_tables(int order, double k, const double t[3], int kind,
   // R[(n,m'),(n,m)] = E_n[m][m'] e^{i m phi};  Chat[(nu,m),(n,m)]
   std::vector<cd> R(size_t(dim) * dim, 0), C(size_t(dim) * dim, 0);
   for (int n = 0; n <= P; ++n) {
-    const int w = rot_row_stride(n);
+    const int w = 2 * n + 1;
+    std::vector<double> E(size_t(w) * w);
+    unfold_rotation_block(n, rot.data(), E.data());
     for (int m = -n; m <= n; ++m)
       for (int mp = -n; mp <= n; ++mp)
-        R[size_t(nm_index(n, mp)) * dim + nm_index(n, m)] =
-            double(rot[rot_block_offset(n) + (m + n) * w + (mp + n)]) * ph[m + P];
+        R[size_t(nm_index(n, mp)) * dim + nm_index(n, m)] = E[size_t(m + n) * w + (mp + n)] * ph[m + P];
   }
   for (int m = -P; m <= P; ++m) {
     const int am = std::abs(m), w = coax_row_stride(P, am);

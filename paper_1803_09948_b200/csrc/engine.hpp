@@ -125,7 +125,6 @@ class Engine {
   DeviceBuffer<uint32_t> p2m_leaves_, l2p_leaves_;
   uint32_t n_p2m_leaves_ = 0, n_l2p_leaves_ = 0;
   DeviceBuffer<float> rot_tables_, coax_tables_;
-  DeviceBuffer<TranslateSchedule> schedule_;
   TranslateStage m2l_;
   std::vector<TranslateStage> m2m_;  // deepest level first
   std::vector<TranslateStage> l2l_;  // shallowest level first

@@ -87,17 +87,30 @@ struct TranslateItem {
 };
 inline constexpr int kTranslateBatch = 32;   // pairs per work item (= lanes of a warp)
 inline constexpr int kTranslateWarps = 8;    // warps per CTA of the translation kernel
-inline constexpr int kTranslateMaxTasks = 160;
+inline constexpr int kTranslateMaxTasks = 80;
 
-// Per-order static schedule of the translation kernel: each stage is a list of tasks
-// (block | first row << 8 | rows << 16), grouped per warp.
+// Per-order static schedule of the translation kernel (kept in __constant__ memory): each stage is a
+// list of tasks grouped per warp; a task carries every shared-memory offset it needs.
+struct TranslateRotTask {
+  uint32_t e_off;    // first coefficient of the task's row tile (float offset in the window)
+  uint32_t in_rel;   // first input row of the folded sub-block, relative to the tile
+  uint32_t out_rel;  // first output row
+  uint32_t packed;   // row stride | inputs << 8 | rows << 16 | (first row odd) << 24
+};
+struct TranslateCoaxTask {
+  uint32_t c_off;    // first coefficient (float offset in the window)
+  uint32_t p_rel;    // input row (n = m) of the s / x_0 column, relative to the tile
+  uint32_t q_rel;    // input row (n = m) of the t column
+  uint32_t packed;   // row stride | inputs << 8 | m << 16 | first row << 22 | rows << 28
+};
 struct TranslateSchedule {
   int rot_begin[kTranslateWarps + 1];
   int coax_begin[kTranslateWarps + 1];
-  uint32_t rot_tasks[kTranslateMaxTasks];
-  uint32_t coax_tasks[kTranslateMaxTasks];
+  TranslateRotTask rot[kTranslateMaxTasks];
+  TranslateCoaxTask coax[kTranslateMaxTasks];
 };
 void build_translate_schedule(int order, TranslateSchedule* out);
+void upload_translate_schedule(int order);  // into the kernel's constant memory slot of `order`
 
 struct TranslateArgs {
   const TranslateItem* items;
@@ -107,7 +120,6 @@ struct TranslateArgs {
   const uint32_t* pair_dst;
   const float* rot_tables;   // [rot][rot_table_size(P)]
   const float* coax_tables;  // [coax][2 * coax_table_size(P)]
-  const TranslateSchedule* schedule;  // device pointer
   const float2* src;         // expansions read
   float2* dst;               // expansions accumulated into (atomically)
   int order;

@@ -18,10 +18,12 @@
 //     (TranslateSchedule); the code is small and loop-structured on purpose — a fully unrolled,
 //     order-specialised variant measured 7x SLOWER on B200 because its 256 KB of SASS starved
 //     the instruction cache (profiles/r01_notes.md);
+//   * rotations run on FOLDED vectors (tables.hpp): the +-m symmetry of the Wigner-d blocks halves
+//     their multiply-adds; vectors are folded in the gather and unfolded once before the reductions;
 //   * the inverse rotation reuses the same table through d^n_{mu,m'} = (-1)^{mu-m'} d^n_{m',mu};
 //   * pairs of one batch have different destinations: results leave through 16-byte vector
 //     reductions (RED.E.ADD.F32x4) into HBM/L2.
-// FP32 work per pair: 2 * 2*sum_n (2n+1)^2 + 4*sum_m (P+1-|m|)^2 FFMAs (17.6 k at P = 12) against
+// FP32 work per pair: 2 * 2*sum_n ((n+1)^2 + n^2) + 4*sum_m (P+1-|m|)^2 FFMAs (11.9 k at P = 12) against
 // 4 (P+1)^4 = 114 k for the reference's dense complex mat-vec.
 #include <algorithm>
 #include <vector>
@@ -47,11 +49,11 @@ __host__ __device__ inline SmemPlan smem_plan(int P) {
   s.dim = (P + 1) * (P + 1);
   s.rot_floats = rot_table_size(P);
   s.coax_c = coax_table_size(P);
-  s.phase_c = (2 * P + 2) & ~1;
+  s.phase_c = (P + 2) & ~1;
   s.tile_c = s.dim * kRow;
-  // rot | coax | phases | tile A | tile B | per-degree/order offsets (2 x 32 ints) | m-of-index
-  s.bytes = size_t(s.rot_floats) * 4 + size_t(s.coax_c + s.phase_c + 2 * s.tile_c) * 8 + 64 * 4 +
-            size_t((s.dim + 3) & ~3);
+  // rot | coax | phases | tile A | tile B | (n, m) of every gather unit (u16)
+  s.bytes = size_t(s.rot_floats) * 4 + size_t(s.coax_c + s.phase_c + 2 * s.tile_c) * 8 +
+            size_t(((P + 1) * (P + 2) / 2 * 2 + 15) & ~15);
   return s;
 }
 
@@ -64,12 +66,11 @@ __device__ __forceinline__ float4 lds4(const float* base, uint32_t off) {
   return *reinterpret_cast<const float4*>(base + off);
 }
 
-// ---- rotation task: rows [r0, r0+R) of block n;  out[r] = sum_k E[k][r0+r] * in[k] -------------
-// e_off / in_off / out_off / ph_off: float offsets into the shared-memory window `sm`
+// ---- rotation task: R output rows of one folded sub-block;  out[r] = sum_k E[k][r] * in[k] ------
+// e_off / in_off / out_off: float offsets into the shared-memory window `sm`
 template <int R, bool BACK>
-__device__ __forceinline__ void rot_task(float* __restrict__ sm, uint32_t e_off, uint32_t ws,
-                                         int w, uint32_t in_off, uint32_t out_off, uint32_t ph_off,
-                                         bool odd0) {
+__device__ __forceinline__ void rot_task(float* __restrict__ sm, uint32_t e_off, uint32_t ws, int w,
+                                         uint32_t in_off, uint32_t out_off, bool odd0) {
   float ar[R], ai[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) ar[r] = ai[r] = 0.0f;
@@ -105,7 +106,7 @@ __device__ __forceinline__ void rot_task(float* __restrict__ sm, uint32_t e_off,
     e_off += ws2;
     e1_off += ws2;
   }
-  {  // w is odd: one even-indexed input left
+  if (w & 1) {  // one even-indexed input left
     const float2 x0 = lds2(sm, in_off);
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
@@ -121,15 +122,10 @@ __device__ __forceinline__ void rot_task(float* __restrict__ sm, uint32_t e_off,
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    float2 o;
-    if (BACK) {
-      // (-1)^{row} of the symmetry, then e^{-i mu phi}
+    float2 o = make_float2(ar[r], ai[r]);
+    if (BACK) {  // (-1)^{row} of the symmetry
       const bool neg = ((r & 1) != 0) != odd0;
-      const float sr = neg ? -ar[r] : ar[r], si = neg ? -ai[r] : ai[r];
-      const float2 p = lds2(sm, ph_off + 2 * r);
-      o = make_float2(sr * p.x + si * p.y, si * p.x - sr * p.y);
-    } else {
-      o = make_float2(ar[r], ai[r]);
+      if (neg) o = make_float2(-ar[r], -ai[r]);
     }
     *reinterpret_cast<float2*>(sm + out_off + r * kRowF) = o;
   }
@@ -137,37 +133,35 @@ __device__ __forceinline__ void rot_task(float* __restrict__ sm, uint32_t e_off,
 
 template <bool BACK>
 __device__ __forceinline__ void rot_dispatch(int R, float* sm, uint32_t e_off, uint32_t ws, int w,
-                                             uint32_t in_off, uint32_t out_off, uint32_t ph_off,
-                                             bool odd0) {
+                                             uint32_t in_off, uint32_t out_off, bool odd0) {
   switch (R) {
-    case 1: rot_task<1, BACK>(sm, e_off, ws, w, in_off, out_off, ph_off, odd0); break;
-    case 2: rot_task<2, BACK>(sm, e_off, ws, w, in_off, out_off, ph_off, odd0); break;
-    case 3: rot_task<3, BACK>(sm, e_off, ws, w, in_off, out_off, ph_off, odd0); break;
-    case 4: rot_task<4, BACK>(sm, e_off, ws, w, in_off, out_off, ph_off, odd0); break;
-    case 5: rot_task<5, BACK>(sm, e_off, ws, w, in_off, out_off, ph_off, odd0); break;
-    case 6: rot_task<6, BACK>(sm, e_off, ws, w, in_off, out_off, ph_off, odd0); break;
-    case 7: rot_task<7, BACK>(sm, e_off, ws, w, in_off, out_off, ph_off, odd0); break;
-    case 8: rot_task<8, BACK>(sm, e_off, ws, w, in_off, out_off, ph_off, odd0); break;
-    case 9: rot_task<9, BACK>(sm, e_off, ws, w, in_off, out_off, ph_off, odd0); break;
-    case 10: rot_task<10, BACK>(sm, e_off, ws, w, in_off, out_off, ph_off, odd0); break;
-    case 11: rot_task<11, BACK>(sm, e_off, ws, w, in_off, out_off, ph_off, odd0); break;
-    default: rot_task<12, BACK>(sm, e_off, ws, w, in_off, out_off, ph_off, odd0); break;
+    case 1: rot_task<1, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
+    case 2: rot_task<2, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
+    case 3: rot_task<3, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
+    case 4: rot_task<4, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
+    case 5: rot_task<5, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
+    case 6: rot_task<6, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
+    case 7: rot_task<7, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
+    case 8: rot_task<8, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
+    case 9: rot_task<9, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
+    case 10: rot_task<10, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
+    case 11: rot_task<11, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
+    default: rot_task<12, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
   }
 }
 
-// ---- coaxial task: rows nu = m + r0 .. m + r0 + R - 1 of order m, columns +m and -m -----------
-// c_off: float offset of Chat^m[0][r0]; ws: row stride in floats; in_off/out_off: tile + lane
+// ---- coaxial task: rows nu = m + r0 .. m + r0 + R - 1 of order m, folded columns s_m and t_m ---
+// (for m = 0 only the single column x_0).  p_off / q_off: float offsets of the first input rows
+// (degree n = m) of the two columns; they advance by 2n+1 and 2n+2 rows per degree.
 template <int R, bool TWO>
 __device__ __forceinline__ void coax_task(float* __restrict__ sm, uint32_t c_off, uint32_t ws, int w,
-                                          int m, int r0, uint32_t in_off, uint32_t out_off) {
-  float pr[R], pi[R], qr[R], qi[R];  // +m and -m accumulators
+                                          int m, int r0, uint32_t p_off, uint32_t q_off,
+                                          uint32_t out_base) {
+  float pr[R], pi[R], qr[R], qi[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) pr[r] = pi[r] = qr[r] = qi[r] = 0.0f;
   constexpr uint32_t kRowF = 2 * kRow;
-  // input rows (n, +m) and (n, -m), n = m .. P: index n(n+1) +- m, advancing by 2n+2 rows
-  uint32_t p_off = in_off + uint32_t(m * (m + 1) + m) * kRowF;
-  uint32_t q_off = in_off + uint32_t(m * (m + 1) - m) * kRowF;
-  uint32_t step = uint32_t(2 * m + 2) * kRowF;
+  uint32_t step = uint32_t(2 * m + 1) * kRowF;
 #pragma unroll 1
   for (int k = w; k > 0; --k) {
     const float2 xp = lds2(sm, p_off);
@@ -199,85 +193,91 @@ __device__ __forceinline__ void coax_task(float* __restrict__ sm, uint32_t c_off
       }
     }
     p_off += step;
-    q_off += step;
+    q_off += step + kRowF;
     step += 2 * kRowF;
     c_off += ws;
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int nu = m + r0 + r;
-    *reinterpret_cast<float2*>(sm + out_off + uint32_t(nu * (nu + 1) + m) * kRowF) = make_float2(pr[r], pi[r]);
+    *reinterpret_cast<float2*>(sm + out_base + uint32_t(nu * nu + m) * kRowF) = make_float2(pr[r], pi[r]);
     if (TWO)
-      *reinterpret_cast<float2*>(sm + out_off + uint32_t(nu * (nu + 1) - m) * kRowF) = make_float2(qr[r], qi[r]);
+      *reinterpret_cast<float2*>(sm + out_base + uint32_t(nu * nu + nu + m) * kRowF) = make_float2(qr[r], qi[r]);
   }
 }
 
 template <bool TWO>
 __device__ __forceinline__ void coax_dispatch(int R, float* sm, uint32_t c_off, uint32_t ws, int w,
-                                              int m, int r0, uint32_t in_off, uint32_t out_off) {
+                                              int m, int r0, uint32_t p_off, uint32_t q_off,
+                                              uint32_t out_base) {
   switch (R) {
-    case 1: coax_task<1, TWO>(sm, c_off, ws, w, m, r0, in_off, out_off); break;
-    case 2: coax_task<2, TWO>(sm, c_off, ws, w, m, r0, in_off, out_off); break;
-    case 3: coax_task<3, TWO>(sm, c_off, ws, w, m, r0, in_off, out_off); break;
-    default: coax_task<4, TWO>(sm, c_off, ws, w, m, r0, in_off, out_off); break;
+    case 1: coax_task<1, TWO>(sm, c_off, ws, w, m, r0, p_off, q_off, out_base); break;
+    case 2: coax_task<2, TWO>(sm, c_off, ws, w, m, r0, p_off, q_off, out_base); break;
+    case 3: coax_task<3, TWO>(sm, c_off, ws, w, m, r0, p_off, q_off, out_base); break;
+    default: coax_task<4, TWO>(sm, c_off, ws, w, m, r0, p_off, q_off, out_base); break;
   }
 }
+
+// per-order static schedules live in constant memory: a task is four words, read with
+// warp-uniform addresses, so handing a task to a warp costs two LDC.64 and no arithmetic
+__constant__ TranslateSchedule c_sched[kMaxOrder + 1];
 
 // Persistent CTAs: each walks a contiguous range of work items (items are sorted by class, so the
 // tables in shared memory are reloaded only when the class changes).  The gather of the NEXT item
 // is issued into registers while the current item drains through its reductions, so the chain
 // item -> pair list -> source rows never sits on the critical path.
-template <int NG>  // source elements per lane of the gather: ceil((P+1)^2 / 8)
+template <int NU>  // (n, m >= 0) units per lane of the gather: ceil((P+1)(P+2)/2 / 8)
 __global__ void __launch_bounds__(kThreads, 2) translate_kernel(const TranslateArgs a) {
   extern __shared__ __align__(16) float smem[];
   const int P = a.order;
   const SmemPlan sp = smem_plan(P);
-  const int dim = sp.dim;
+  const int dim = sp.dim, n_units = (P + 1) * (P + 2) / 2;
   float* s_rot = smem;
   float2* s_coax = reinterpret_cast<float2*>(s_rot + sp.rot_floats);
-  float2* s_ph = s_coax + sp.coax_c;  // e^{i m phi}, index m + P
+  float2* s_ph = s_coax + sp.coax_c;  // e^{i m phi}, m = 0..P
   float2* A = s_ph + sp.phase_c;
   float2* B = A + sp.tile_c;
-  int* s_roff = reinterpret_cast<int*>(B + sp.tile_c);  // rotation block offsets per degree
-  int* s_coff = s_roff + 32;                             // coaxial block offsets per order
-  signed char* s_m = reinterpret_cast<signed char*>(s_coff + 32);  // order m of coefficient i
+  unsigned short* s_unit = reinterpret_cast<unsigned short*>(B + sp.tile_c);  // n << 8 | m per unit
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t it_begin = uint32_t(uint64_t(a.n_items) * blockIdx.x / gridDim.x);
   const uint32_t it_end = uint32_t(uint64_t(a.n_items) * (blockIdx.x + 1) / gridDim.x);
   if (it_begin >= it_end) return;
 
-  if (tid <= P) {
-    s_roff[tid] = rot_block_offset(tid);
-    s_coff[tid] = coax_block_offset(P, tid);
-  }
-  for (int i = tid; i < dim; i += kThreads) {
-    int n = int(sqrtf(float(i)));
-    while (n * n > i) --n;
-    while ((n + 1) * (n + 1) <= i) ++n;
-    s_m[i] = (signed char)(i - n * (n + 1));
+  for (int u = tid; u < n_units; u += kThreads) {
+    int n = int((sqrtf(8.0f * float(u) + 1.0f) - 1.0f) * 0.5f);
+    while (n * (n + 1) / 2 > u) --n;
+    while ((n + 1) * (n + 2) / 2 <= u) ++n;
+    s_unit[u] = (unsigned short)(n << 8 | (u - n * (n + 1) / 2));
   }
 
-  // gather mapping: 4 pairs x 8 lanes per warp (64-byte runs of a source row)
+  // gather mapping: 4 pairs x 8 lanes per warp; a lane owns units u = ge + 8 j, i.e. the two
+  // source coefficients (n, +m) and (n, -m) it folds into s_m and t_m
   const int gq = lane >> 3, ge = lane & 7, gp = warp * 4 + gq;
-  float2 gx[NG];
+  float2 gxp[NU], gxm[NU];
   auto issue_gather = [&](const TranslateItem& it) {
     const bool live = gp < int(it.count);
     const float2* row = live ? a.src + size_t(a.pair_src[it.pair_begin + gp]) * a.stride : nullptr;
 #pragma unroll
-    for (int j = 0; j < NG; ++j) {
-      const int i = ge + 8 * j;
-      gx[j] = (live && i < dim) ? row[i] : make_float2(0.f, 0.f);
+    for (int j = 0; j < NU; ++j) {
+      const int u = ge + 8 * j;
+      gxp[j] = gxm[j] = make_float2(0.f, 0.f);
+      if (live && u < n_units) {
+        const int n = s_unit[u] >> 8, m = s_unit[u] & 0xff, i = n * (n + 1) + m;
+        gxp[j] = row[i];
+        gxm[j] = row[i - 2 * m];
+      }
     }
   };
 
-  const TranslateSchedule* sched = a.schedule;
+  const TranslateSchedule& sched = c_sched[P];
   // float offsets of the regions inside the shared window
-  const uint32_t rot_f = 0, coax_f = uint32_t(sp.rot_floats),
-                 ph_f = coax_f + 2u * uint32_t(sp.coax_c),
+  const uint32_t coax_f = uint32_t(sp.rot_floats), ph_f = coax_f + 2u * uint32_t(sp.coax_c),
                  a_f = ph_f + 2u * uint32_t(sp.phase_c), b_f = a_f + 2u * uint32_t(sp.tile_c);
   constexpr uint32_t kRowF = 2 * kRow;
+  const uint32_t a_lane = a_f + 2 * lane, b_lane = b_f + 2 * lane;
 
+  __syncthreads();  // s_unit
   TranslateItem item = a.items[it_begin];
   issue_gather(item);
   uint32_t loaded_cls = 0xffffffffu;
@@ -292,27 +292,36 @@ __global__ void __launch_bounds__(kThreads, 2) translate_kernel(const TranslateA
       const float4* g_coax =
           reinterpret_cast<const float4*>(a.coax_tables + size_t(cls.coax) * sp.coax_c * 2);
       for (int i = tid; i < sp.coax_c / 2; i += kThreads) reinterpret_cast<float4*>(s_coax)[i] = g_coax[i];
-      if (tid <= 2 * P) {
-        const int m = tid - P, am = m < 0 ? -m : m;
+      if (tid <= P) {
         float cr = 1.f, ci = 0.f;
-        for (int j = 0; j < am; ++j) {
+        for (int j = 0; j < tid; ++j) {
           const float t = cr * cls.cphi - ci * cls.sphi;
           ci = ci * cls.cphi + cr * cls.sphi;
           cr = t;
         }
-        s_ph[tid] = make_float2(cr, m < 0 ? -ci : ci);
+        s_ph[tid] = make_float2(cr, ci);
       }
       loaded_cls = item.cls;
       __syncthreads();
     }
 
-    // stage 1: apply e^{i m phi} to the gathered sources, store element-major into A
+    // stage 1: e^{i m phi}, fold, store element-major into A
+    //   a = x_m e^{i m phi},  b = (-1)^m x_{-m} e^{-i m phi}:   s_m = a + b,  t_m = a - b
 #pragma unroll
-    for (int j = 0; j < NG; ++j) {
-      const int i = ge + 8 * j;
-      if (i < dim) {
-        const float2 x = gx[j], ph = s_ph[int(s_m[i]) + P];
-        A[i * kRow + gp] = make_float2(x.x * ph.x - x.y * ph.y, x.x * ph.y + x.y * ph.x);
+    for (int j = 0; j < NU; ++j) {
+      const int u = ge + 8 * j;
+      if (u < n_units) {
+        const int n = s_unit[u] >> 8, m = s_unit[u] & 0xff;
+        const float2 ph = s_ph[m], xp = gxp[j], xm = gxm[j];
+        if (m == 0) {
+          A[(n * n) * kRow + gp] = xp;
+        } else {
+          const float2 av = make_float2(xp.x * ph.x - xp.y * ph.y, xp.x * ph.y + xp.y * ph.x);
+          float2 bv = make_float2(xm.x * ph.x + xm.y * ph.y, xm.y * ph.x - xm.x * ph.y);
+          if (m & 1) bv = make_float2(-bv.x, -bv.y);
+          A[(n * n + m) * kRow + gp] = make_float2(av.x + bv.x, av.y + bv.y);
+          A[(n * n + n + m) * kRow + gp] = make_float2(av.x - bv.x, av.y - bv.y);
+        }
       }
     }
     __syncthreads();
@@ -322,97 +331,99 @@ __global__ void __launch_bounds__(kThreads, 2) translate_kernel(const TranslateA
     if (has_next) next = a.items[it + 1];
 
     // stage 2: forward rotation A -> B
-    for (int t = sched->rot_begin[warp]; t < sched->rot_begin[warp + 1]; ++t) {
-      const uint32_t task = sched->rot_tasks[t];
-      const int n = task & 0xff, r0 = (task >> 8) & 0xff, R = (task >> 16) & 0xff;
-      rot_dispatch<false>(R, smem, rot_f + s_roff[n] + r0, rot_row_stride(n), 2 * n + 1,
-                          a_f + uint32_t(n * n) * kRowF + 2 * lane,
-                          b_f + uint32_t(n * n + r0) * kRowF + 2 * lane, 0, false);
+    for (int t = sched.rot_begin[warp]; t < sched.rot_begin[warp + 1]; ++t) {
+      const TranslateRotTask d = sched.rot[t];
+      rot_dispatch<false>((d.packed >> 16) & 0xff, smem, d.e_off, d.packed & 0xff, (d.packed >> 8) & 0xff,
+                          a_lane + d.in_rel, b_lane + d.out_rel, false);
     }
     __syncthreads();
     // stage 3: coaxial translation B -> A
-    for (int t = sched->coax_begin[warp]; t < sched->coax_begin[warp + 1]; ++t) {
-      const uint32_t task = sched->coax_tasks[t];
-      const int m = task & 0xff, r0 = (task >> 8) & 0xff, R = (task >> 16) & 0xff;
-      const uint32_t c_off = coax_f + 2u * uint32_t(s_coff[m] + r0), cws = 2u * coax_row_stride(P, m);
+    for (int t = sched.coax_begin[warp]; t < sched.coax_begin[warp + 1]; ++t) {
+      const TranslateCoaxTask d = sched.coax[t];
+      const int m = (d.packed >> 16) & 0x3f, r0 = (d.packed >> 22) & 0x3f, R = d.packed >> 28;
       if (m == 0)
-        coax_dispatch<false>(R, smem, c_off, cws, P + 1 - m, m, r0, b_f + 2 * lane, a_f + 2 * lane);
+        coax_dispatch<false>(R, smem, d.c_off, d.packed & 0xff, (d.packed >> 8) & 0xff, m, r0,
+                             b_lane + d.p_rel, b_lane + d.q_rel, a_lane);
       else
-        coax_dispatch<true>(R, smem, c_off, cws, P + 1 - m, m, r0, b_f + 2 * lane, a_f + 2 * lane);
+        coax_dispatch<true>(R, smem, d.c_off, d.packed & 0xff, (d.packed >> 8) & 0xff, m, r0,
+                            b_lane + d.p_rel, b_lane + d.q_rel, a_lane);
     }
     __syncthreads();
-    // stage 4: inverse rotation A -> B, with e^{-i mu phi}
-    for (int t = sched->rot_begin[warp]; t < sched->rot_begin[warp + 1]; ++t) {
-      const uint32_t task = sched->rot_tasks[t];
-      const int n = task & 0xff, r0 = (task >> 8) & 0xff, R = (task >> 16) & 0xff;
-      rot_dispatch<true>(R, smem, rot_f + s_roff[n] + r0, rot_row_stride(n), 2 * n + 1,
-                         a_f + uint32_t(n * n) * kRowF + 2 * lane,
-                         b_f + uint32_t(n * n + r0) * kRowF + 2 * lane, ph_f + 2u * uint32_t(r0 - n + P),
-                         (r0 & 1) != 0);
+    // stage 4: inverse rotation A -> B (same table, sign-twiddled)
+    for (int t = sched.rot_begin[warp]; t < sched.rot_begin[warp + 1]; ++t) {
+      const TranslateRotTask d = sched.rot[t];
+      rot_dispatch<true>((d.packed >> 16) & 0xff, smem, d.e_off, d.packed & 0xff, (d.packed >> 8) & 0xff,
+                         a_lane + d.in_rel, b_lane + d.out_rel, (d.packed >> 24) & 1);
     }
     __syncthreads();
+    // stage 5a: unfold B -> A in the caller's coefficient order, with e^{-i mu phi}:
+    //   y_m = (u + v)/2 e^{-i m phi},   y_{-m} = (-1)^m (u - v)/2 e^{+i m phi}
+    for (int u = ge; u < n_units; u += 8) {
+      const int n = s_unit[u] >> 8, m = s_unit[u] & 0xff;
+      const float2 uu = B[(n * n + m) * kRow + gp];
+      if (m == 0) {
+        A[(n * n + n) * kRow + gp] = uu;
+      } else {
+        const float2 vv = B[(n * n + n + m) * kRow + gp], ph = s_ph[m];
+        const float2 yp = make_float2(0.5f * (uu.x + vv.x), 0.5f * (uu.y + vv.y));
+        float2 ym = make_float2(0.5f * (uu.x - vv.x), 0.5f * (uu.y - vv.y));
+        if (m & 1) ym = make_float2(-ym.x, -ym.y);
+        A[(n * n + n + m) * kRow + gp] = make_float2(yp.x * ph.x + yp.y * ph.y, yp.y * ph.x - yp.x * ph.y);
+        A[(n * n + n - m) * kRow + gp] = make_float2(ym.x * ph.x - ym.y * ph.y, ym.x * ph.y + ym.y * ph.x);
+      }
+    }
+    // a lane group reads back only what it wrote itself (same pair column gp): a warp-level
+    // barrier orders the stores of the 8 lanes of the group before the loads below
+    __syncwarp();
 
-    // stage 5: start the next item's gather, then accumulate this item into its destinations,
+    // stage 5b: start the next item's gather, then accumulate this item into its destinations,
     // two coefficients (16 bytes) per reduction
     if (has_next) issue_gather(next);
     if (gp < count) {
       float* dst = reinterpret_cast<float*>(a.dst + size_t(a.pair_dst[item.pair_begin + gp]) * a.stride);
       for (int i2 = ge; i2 < dim / 2; i2 += 8) {
-        const float2 lo = B[(2 * i2) * kRow + gp], hi = B[(2 * i2 + 1) * kRow + gp];
+        const float2 lo = A[(2 * i2) * kRow + gp], hi = A[(2 * i2 + 1) * kRow + gp];
         atomicAdd(reinterpret_cast<float4*>(dst) + i2, make_float4(lo.x, lo.y, hi.x, hi.y));
       }
       if ((dim & 1) && ge == 0)
-        atomicAdd(reinterpret_cast<float2*>(dst) + (dim - 1), B[(dim - 1) * kRow + gp]);
+        atomicAdd(reinterpret_cast<float2*>(dst) + (dim - 1), A[(dim - 1) * kRow + gp]);
     }
     item = next;
-    // no barrier here: the next stage 1 only writes A (last read in stage 4), and the barrier after
-    // it orders this stage's reads of B before the next stage 2 overwrites B
+    // the next stage 1 overwrites A: every warp must be done reading it
+    __syncthreads();
   }
 }
 
 }  // namespace
 
-// host side: cut the stages into tasks and hand them to the warps (longest processing time first)
+// host side: cut the stages into tasks, precompute every shared-memory offset a task needs, and
+// hand the tasks to the warps (longest processing time first)
 void build_translate_schedule(int P, TranslateSchedule* out) {
-  struct Task {
-    uint32_t code;
+  const SmemPlan sp = smem_plan(P);
+  const uint32_t kRowF = 2 * kRow, coax_f = uint32_t(sp.rot_floats);
+  struct RotT {
+    TranslateRotTask d;
     int cost;
   };
-  auto distribute = [](std::vector<Task>& tasks, uint32_t* flat, int* begin, int cap) {
-    std::stable_sort(tasks.begin(), tasks.end(), [](const Task& x, const Task& y) { return x.cost > y.cost; });
-    std::vector<std::vector<uint32_t>> per(kWarps);
-    long load[kWarps] = {};
-    for (const Task& t : tasks) {
-      int best = 0;
-      for (int w = 1; w < kWarps; ++w)
-        if (load[w] < load[best]) best = w;
-      per[best].push_back(t.code);
-      load[best] += t.cost;
-    }
-    int pos = 0;
-    for (int w = 0; w < kWarps; ++w) {
-      begin[w] = pos;
-      for (uint32_t c : per[w]) {
-        if (pos >= cap) throw Error(HFMM_ERR_INTERNAL, "translation schedule overflow");
-        flat[pos++] = c;
-      }
-    }
-    begin[kWarps] = pos;
+  struct CoaxT {
+    TranslateCoaxTask d;
+    int cost;
   };
-  std::vector<Task> rot, coax;
-  for (int n = 0; n <= P; ++n) {
-    const int w = 2 * n + 1;
-    // tiles start at multiples of 4 (aligned 16-byte coefficient loads) and hold <= 12 rows; the
-    // split minimising sum(2R + 6) (instructions per input step) is found by exhaustive search
-    int best_cost = 1 << 30, best_parts[8] = {}, best_n = 0;
+  std::vector<RotT> rot;
+  std::vector<CoaxT> coax;
+  // rows of a sub-block are cut into tiles that start at multiples of 4 (aligned 16-byte
+  // coefficient loads) and hold <= 12 rows; the split minimising sum(2R + 6) (instructions per
+  // input step) is found by exhaustive search
+  auto cut = [](int w, int parts[4]) {
+    int best_cost = 1 << 30, best_n = 0;
     for (int a = 0; a <= 12; a += 4)
       for (int b = 0; b <= 12; b += 4)
         for (int c = 0; c <= 12; c += 4) {
           const int last = w - a - b - c;
           if (last < 1 || last > 12) continue;
-          if ((a == 0 && (b || c)) || (b == 0 && c)) continue;  // leading parts first
-          int parts[4] = {a, b, c, last}, np = 0, cost = 0, tmp[4];
-          for (int v : parts)
+          if ((a == 0 && (b || c)) || (b == 0 && c)) continue;
+          int cand[4] = {a, b, c, last}, tmp[4], np = 0, cost = 0;
+          for (int v : cand)
             if (v) {
               tmp[np++] = v;
               cost += 2 * v + 6;
@@ -420,39 +431,87 @@ void build_translate_schedule(int P, TranslateSchedule* out) {
           if (cost < best_cost) {
             best_cost = cost;
             best_n = np;
-            for (int i = 0; i < np; ++i) best_parts[i] = tmp[i];
+            for (int i = 0; i < np; ++i) parts[i] = tmp[i];
           }
         }
-    int r0 = 0;
-    for (int i = 0; i < best_n; ++i) {
-      const int R = best_parts[i];
-      rot.push_back({uint32_t(n) | uint32_t(r0) << 8 | uint32_t(R) << 16, w * (2 * R + 6)});
-      r0 += R;
+    return best_n;
+  };
+  for (int n = 0; n <= P; ++n)
+    for (int part = 0; part < 2; ++part) {  // 0: plus system (n+1 rows), 1: minus system (n rows)
+      const int w = part ? n : n + 1;
+      if (w == 0) continue;
+      const int ws = part ? rot_minus_stride(n) : rot_plus_stride(n);
+      const int base = part ? n * n + n + 1 : n * n;
+      const int table = part ? rot_minus_offset(n) : rot_block_offset(n);
+      int parts[4], r0 = 0;
+      const int np = cut(w, parts);
+      for (int i = 0; i < np; ++i) {
+        const int R = parts[i];
+        TranslateRotTask d;
+        d.e_off = uint32_t(table + r0);
+        d.in_rel = uint32_t(base) * kRowF;
+        d.out_rel = uint32_t(base + r0) * kRowF;
+        d.packed = uint32_t(ws) | uint32_t(w) << 8 | uint32_t(R) << 16 | uint32_t(r0 & 1) << 24;
+        rot.push_back({d, w * (2 * R + 6) + 40});
+        r0 += R;
+      }
     }
-  }
   for (int m = 0; m <= P; ++m) {
     const int w = P + 1 - m;
     for (int r0 = 0; r0 < w; r0 += 4) {
       const int R = std::min(4, w - r0);
-      coax.push_back({uint32_t(m) | uint32_t(r0) << 8 | uint32_t(R) << 16, w * ((m ? 8 : 4) * R + 8)});
+      TranslateCoaxTask d;
+      d.c_off = coax_f + 2u * uint32_t(coax_block_offset(P, m) + r0);
+      d.p_rel = uint32_t(m * m + m) * kRowF;
+      d.q_rel = uint32_t(m * m + 2 * m) * kRowF;
+      d.packed = uint32_t(2 * coax_row_stride(P, m)) | uint32_t(w) << 8 | uint32_t(m) << 16 |
+                 uint32_t(r0) << 22 | uint32_t(R) << 28;
+      coax.push_back({d, w * ((m ? 8 : 4) * R + 8) + 40});
     }
   }
-  distribute(rot, out->rot_tasks, out->rot_begin, kTranslateMaxTasks);
-  distribute(coax, out->coax_tasks, out->coax_begin, kTranslateMaxTasks);
+  if (rot.size() > size_t(kTranslateMaxTasks) || coax.size() > size_t(kTranslateMaxTasks))
+    throw Error(HFMM_ERR_INTERNAL, "translation schedule overflow");
+  auto distribute = [](auto& tasks, auto* flat, int* begin) {
+    std::stable_sort(tasks.begin(), tasks.end(), [](const auto& x, const auto& y) { return x.cost > y.cost; });
+    std::vector<std::vector<int>> per(kWarps);
+    long load[kWarps] = {};
+    for (size_t i = 0; i < tasks.size(); ++i) {
+      int best = 0;
+      for (int w = 1; w < kWarps; ++w)
+        if (load[w] < load[best]) best = w;
+      per[best].push_back(int(i));
+      load[best] += tasks[i].cost;
+    }
+    int pos = 0;
+    for (int w = 0; w < kWarps; ++w) {
+      begin[w] = pos;
+      for (int i : per[w]) flat[pos++] = tasks[i].d;
+    }
+    begin[kWarps] = pos;
+  };
+  *out = TranslateSchedule{};
+  distribute(rot, out->rot, out->rot_begin);
+  distribute(coax, out->coax, out->coax_begin);
+}
+
+void upload_translate_schedule(int order) {
+  TranslateSchedule sched;
+  build_translate_schedule(order, &sched);
+  HFMM_CUDA_CHECK(cudaMemcpyToSymbol(c_sched, &sched, sizeof(sched), sizeof(sched) * size_t(order)));
 }
 
 int translate_batch_size(int) { return kTranslateBatch; }
 
 namespace {
-template <int NG>
-void launch_translate_ng(const TranslateArgs& a, cudaStream_t s, size_t bytes, int ctas) {
+template <int NU>
+void launch_translate_nu(const TranslateArgs& a, cudaStream_t s, size_t bytes, int ctas) {
   static int configured_for = -1;
   if (configured_for < int(bytes)) {
-    HFMM_CUDA_CHECK(cudaFuncSetAttribute(translate_kernel<NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    HFMM_CUDA_CHECK(cudaFuncSetAttribute(translate_kernel<NU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(bytes)));
     configured_for = int(bytes);
   }
-  translate_kernel<NG><<<ctas, kThreads, bytes, s>>>(a);
+  translate_kernel<NU><<<ctas, kThreads, bytes, s>>>(a);
   HFMM_CUDA_CHECK(cudaGetLastError());
 }
 }  // namespace
@@ -469,12 +528,12 @@ void launch_translate(const TranslateArgs& a, cudaStream_t s) {
   // persistent grid: two CTAs per SM when their shared memory fits (227 KB per SM), else one
   const int per_sm = 2 * (sp.bytes + 1024) <= 227 * 1024 ? 2 : 1;
   const int ctas = int(std::min<uint32_t>(a.n_items, uint32_t(per_sm * sm_count)));
-  const int ng = (sp.dim + 7) / 8;
-  if (ng <= 11) launch_translate_ng<11>(a, s, sp.bytes, ctas);        // P <= 8
-  else if (ng <= 16) launch_translate_ng<16>(a, s, sp.bytes, ctas);   // P <= 10
-  else if (ng <= 22) launch_translate_ng<22>(a, s, sp.bytes, ctas);   // P <= 12
-  else if (ng <= 29) launch_translate_ng<29>(a, s, sp.bytes, ctas);   // P <= 14
-  else launch_translate_ng<37>(a, s, sp.bytes, ctas);                 // P <= 16
+  const int nu = ((a.order + 1) * (a.order + 2) / 2 + 7) / 8;
+  if (nu <= 6) launch_translate_nu<6>(a, s, sp.bytes, ctas);         // P <= 8
+  else if (nu <= 9) launch_translate_nu<9>(a, s, sp.bytes, ctas);    // P <= 10
+  else if (nu <= 12) launch_translate_nu<12>(a, s, sp.bytes, ctas);  // P <= 12
+  else if (nu <= 15) launch_translate_nu<15>(a, s, sp.bytes, ctas);  // P <= 14
+  else launch_translate_nu<20>(a, s, sp.bytes, ctas);                // P <= 16
 }
 
 }  // namespace hfmm_b200

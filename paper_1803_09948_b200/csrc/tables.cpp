@@ -129,7 +129,7 @@ double wigner_d(int n, int mp, int m, double cos_beta) {
 }
 
 void build_rotation_table(int order, double cos_theta, float* out) {
-  // same explicit sum as wigner_d with the powers of cos(beta/2), sin(beta/2) tabulated once
+  // explicit Wigner sum with the powers of cos(beta/2), sin(beta/2) tabulated once
   const long double cb = std::clamp((long double)cos_theta, -1.0L, 1.0L);
   const long double c = sqrtl((1 + cb) / 2), s = sqrtl((1 - cb) / 2);
   std::vector<long double> cp(2 * order + 2), sp(2 * order + 2);
@@ -139,11 +139,12 @@ void build_rotation_table(int order, double cos_theta, float* out) {
     sp[i] = sp[i - 1] * s;
   }
   std::fill(out, out + rot_table_size(order), 0.0f);
+  std::vector<long double> d;
   for (int n = 0; n <= order; ++n) {
-    float* blk = out + rot_block_offset(n);
-    const int w = rot_row_stride(n);
-    for (int a = -n; a <= n; ++a)        // first index of d^n_{a,b}
-      for (int b = -n; b <= n; ++b) {    // second index
+    const int w = 2 * n + 1;
+    d.assign(size_t(w) * w, 0.0L);  // d[(a+n)*w + (b+n)] = d^n_{a,b}
+    for (int a = -n; a <= n; ++a)
+      for (int b = -n; b <= n; ++b) {
         const long double pre = sqrtl(factorial_ld(n + a) * factorial_ld(n - a) *
                                       factorial_ld(n + b) * factorial_ld(n - b));
         long double sum = 0;
@@ -153,9 +154,55 @@ void build_rotation_table(int order, double cos_theta, float* out) {
                                     factorial_ld(n - k - a) * factorial_ld(k - b + a));
           sum += ((k - b + a) & 1) ? -term : term;
         }
-        blk[(a + n) * w + (b + n)] = float(pre * sum);
+        d[size_t(a + n) * w + (b + n)] = pre * sum;
+      }
+    auto D = [&](int a, int b) { return d[size_t(a + n) * w + (b + n)]; };
+    // forward operator M_{r,k} = d_{k,r} (input k -> output r); a_{rk} = M_{r,k},
+    // b'_{rk} = (-1)^k M_{r,-k} = (-1)^k d_{-k,r}
+    float* plus = out + rot_block_offset(n);
+    float* minus = out + rot_minus_offset(n);
+    const int ps = rot_plus_stride(n), ms = rot_minus_stride(n);
+    for (int k = 0; k <= n; ++k)
+      for (int r = 0; r <= n; ++r) {
+        const long double a = D(k, r), bp = ((k & 1) ? -1.0L : 1.0L) * D(-k, r);
+        long double v;
+        if (k == 0) v = r == 0 ? a : 2 * a;   // x_0 feeds y_0 once and u_r = y_r + yt_{-r} twice
+        else if (r == 0) v = a;               // y_0 = a_00 x_0 + sum a_0k s_k
+        else v = a + bp;
+        plus[k * ps + r] = float(v);
+        if (k >= 1 && r >= 1) minus[(k - 1) * ms + (r - 1)] = float(a - bp);
       }
   }
+}
+
+void unfold_rotation_block(int n, const float* table, double* out) {
+  const int w = 2 * n + 1;
+  const float* plus = table + rot_block_offset(n);
+  const float* minus = table + rot_minus_offset(n);
+  const int ps = rot_plus_stride(n), ms = rot_minus_stride(n);
+  auto M = [&](int r, int k) -> double& { return out[size_t(k + n) * w + (r + n)]; };  // E[k][r]
+  for (int k = 0; k <= n; ++k)
+    for (int r = 0; r <= n; ++r) {
+      const double sp_ = plus[k * ps + r];
+      const double sm_ = (k >= 1 && r >= 1) ? minus[(k - 1) * ms + (r - 1)] : 0.0;
+      double a, bp;
+      if (k == 0) {
+        a = r == 0 ? sp_ : sp_ / 2;
+        bp = a;
+      } else if (r == 0) {
+        a = sp_;
+        bp = a;
+      } else {
+        a = (sp_ + sm_) / 2;
+        bp = (sp_ - sm_) / 2;
+      }
+      const double sk = (k & 1) ? -1.0 : 1.0, sr = (r & 1) ? -1.0 : 1.0;
+      M(r, k) = a;
+      if (k > 0) M(r, -k) = sk * bp;
+      if (r > 0) M(-r, k) = sr * bp;
+      if (r > 0 && k > 0) M(-r, -k) = sr * sk * a;
+      if (r > 0 && k == 0) M(-r, 0) = sr * a;
+    }
 }
 
 CoaxBuilder::CoaxBuilder(int order) : order_(order) {

@@ -35,17 +35,30 @@ double wigner_d(int n, int mp, int m, double cos_beta);
 long double double_factorial(int n);  // n!! for odd n >= -1
 
 // Table layouts are padded so the device can fetch 4 rotation coefficients (or 2 complex coaxial
-// coefficients) with one aligned 16-byte load:
-//   rotation block n : (2n+1) rows of rot_row_stride(n) floats, E_n[m][m'] at row m+n, column m'+n
-//   coaxial block m  : (P+1-m) rows of coax_row_stride(P,m) complex, Chat^m[n][nu] at row n-m,
-//                      column nu-m
-// padding entries are zero.
-HFMM_HD constexpr int rot_row_stride(int n) { return (2 * n + 1 + 3) & ~3; }
+// coefficients) with one aligned 16-byte load; padding entries are zero.
+//
+// Rotation tables are stored FOLDED.  With xt_{-m} = (-1)^m x_{-m} the symmetry
+// d^n_{-a,-b} = (-1)^{a-b} d^n_{a,b} splits a (2n+1)x(2n+1) block into
+//   plus  system, size n+1 : inputs  [x_0, s_1..s_n],  s_m = x_m + xt_{-m}
+//   minus system, size n   : inputs  [t_1..t_n],       t_m = x_m - xt_{-m}
+// whose outputs are the same combinations of the rotated vector — half the multiply-adds.  The
+// coaxial step acts identically on +m and -m, so it commutes with the folding and the whole
+// pipeline (rotate, translate, rotate back) runs on folded vectors; they are folded once when the
+// sources are gathered and unfolded once before the results are accumulated.
+//   block n : plus  (n+1) rows of rot_plus_stride(n)  floats, entry [k][r] = input k -> output r
+//             minus  n     rows of rot_minus_stride(n) floats, entry [k-1][r-1]
+// Folded vector layout of degree n (same 2n+1 slots): n^2 + 0 : x_0 | n^2 + m : s_m | n^2 + n + m : t_m
+HFMM_HD constexpr int rot_plus_stride(int n) { return (n + 1 + 3) & ~3; }
+HFMM_HD constexpr int rot_minus_stride(int n) { return (n + 3) & ~3; }
+HFMM_HD constexpr int rot_block_size(int n) {
+  return (n + 1) * rot_plus_stride(n) + n * rot_minus_stride(n);
+}
 HFMM_HD constexpr int rot_block_offset(int n) {
   int off = 0;
-  for (int j = 0; j < n; ++j) off += (2 * j + 1) * rot_row_stride(j);
+  for (int j = 0; j < n; ++j) off += rot_block_size(j);
   return off;
 }
+HFMM_HD constexpr int rot_minus_offset(int n) { return rot_block_offset(n) + (n + 1) * rot_plus_stride(n); }
 HFMM_HD constexpr int rot_table_size(int p) { return rot_block_offset(p + 1); }
 HFMM_HD constexpr int coax_row_stride(int p, int m) { return (p + 1 - m + 1) & ~1; }
 HFMM_HD constexpr int coax_block_offset(int p, int m) {
@@ -55,9 +68,13 @@ HFMM_HD constexpr int coax_block_offset(int p, int m) {
 }
 HFMM_HD constexpr int coax_table_size(int p) { return coax_block_offset(p, p + 1); }  // complex
 
-// E_n[m][m'] = d^n_{m,m'}(theta), padded blocks concatenated over n; forward rotation is
-//   M'_n^{m'} = sum_m E_n[m][m'] e^{i m phi} M_n^m   (then  M = R^H M' for the inverse)
+// Folded forward-rotation table for polar angle theta (layout above).  Unfolded, the forward
+// rotation is  M'_n^{m'} = sum_m d^n_{m,m'}(theta) e^{i m phi} M_n^m ; the inverse rotation uses the
+// same table through d^n_{mu,m'} = (-1)^{mu-m'} d^n_{m',mu}.
 void build_rotation_table(int order, double cos_theta, float* out);
+// the unfolded (2n+1)x(2n+1) block E_n[m][m'] = d^n_{m,m'} reconstructed from a folded table
+// (row-major, index (m+n)*(2n+1) + (m'+n)); used by the CPU-side table tests
+void unfold_rotation_block(int n, const float* folded_table, double* out);
 
 enum class CoaxKind { m2l, m2m, l2l };
 // Scaled coaxial coefficients Chat^m[n][nu] (complex, interleaved) for translation distance
