@@ -53,40 +53,50 @@ __host__ __device__ inline SmemPlan smem_plan(int P) {
   s.tile_c = s.dim * kRow;
   // rot | coax | phases | tile A | tile B | (n, m) of every gather unit (u16)
   s.bytes = size_t(s.rot_floats) * 4 + size_t(s.coax_c + s.phase_c + 2 * s.tile_c) * 8 +
-            size_t(((P + 1) * (P + 2) / 2 * 2 + 15) & ~15);
+            size_t(((P + 1) * (P + 2) / 2 * 6 + 15) & ~15);
   return s;
 }
 
-// Shared memory is addressed with 32-bit offsets from one base so the loops advance with a couple
-// of integer adds (generic 64-bit pointer arithmetic tripled the instruction count).
-__device__ __forceinline__ float2 lds2(const float* base, uint32_t off) {
-  return *reinterpret_cast<const float2*>(base + off);
+// Shared memory is addressed with 32-bit BYTE addresses in the shared window (explicit
+// ld.shared / st.shared), so the loops advance with one integer add per pointer and the loads use
+// register + immediate addressing (generic pointers cost an address computation per access).
+__device__ __forceinline__ float2 lds2(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+  return v;
 }
-__device__ __forceinline__ float4 lds4(const float* base, uint32_t off) {
-  return *reinterpret_cast<const float4*>(base + off);
+__device__ __forceinline__ float4 lds4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts2(uint32_t addr, float2 v) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
 }
 
 // ---- rotation task: R output rows of one folded sub-block;  out[r] = sum_k E[k][r] * in[k] ------
 // e_off / in_off / out_off: float offsets into the shared-memory window `sm`
 template <int R, bool BACK>
-__device__ __forceinline__ void rot_task(float* __restrict__ sm, uint32_t e_off, uint32_t ws, int w,
-                                         uint32_t in_off, uint32_t out_off, bool odd0) {
+__device__ __forceinline__ void rot_task(uint32_t e_addr, uint32_t ws_b, int w, uint32_t in_addr,
+                                         uint32_t out_addr, bool odd0) {
   float ar[R], ai[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) ar[r] = ai[r] = 0.0f;
   constexpr int NV = (R + 3) / 4;
-  constexpr uint32_t kRowF = 2 * kRow;  // floats per operand row
+  constexpr uint32_t kRowB = 8 * kRow;  // bytes per operand row
   // two inputs per trip; in the inverse rotation odd inputs enter negated ((-1)^k of the symmetry)
-  uint32_t e1_off = e_off + ws;
-  const uint32_t ws2 = 2 * ws;
+  uint32_t e1_addr = e_addr + ws_b;
+  const uint32_t ws2 = 2 * ws_b;
 #pragma unroll 1
   for (int trips = w >> 1; trips > 0; --trips) {
-    const float2 x0 = lds2(sm, in_off), x1 = lds2(sm, in_off + kRowF);
+    const float2 x0 = lds2(in_addr), x1 = lds2(in_addr + kRowB);
     float e0[NV * 4], e1[NV * 4];
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      const float4 a = lds4(sm, e_off + 4 * v);
-      const float4 b = lds4(sm, e1_off + 4 * v);
+      const float4 a = lds4(e_addr + 16 * v);
+      const float4 b = lds4(e1_addr + 16 * v);
       e0[4 * v] = a.x; e0[4 * v + 1] = a.y; e0[4 * v + 2] = a.z; e0[4 * v + 3] = a.w;
       e1[4 * v] = b.x; e1[4 * v + 1] = b.y; e1[4 * v + 2] = b.z; e1[4 * v + 3] = b.w;
     }
@@ -102,15 +112,15 @@ __device__ __forceinline__ void rot_task(float* __restrict__ sm, uint32_t e_off,
         ai[r] = fmaf(e1[r], x1.y, ai[r]);
       }
     }
-    in_off += 2 * kRowF;
-    e_off += ws2;
-    e1_off += ws2;
+    in_addr += 2 * kRowB;
+    e_addr += ws2;
+    e1_addr += ws2;
   }
   if (w & 1) {  // one even-indexed input left
-    const float2 x0 = lds2(sm, in_off);
+    const float2 x0 = lds2(in_addr);
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      const float4 a = lds4(sm, e_off + 4 * v);
+      const float4 a = lds4(e_addr + 16 * v);
       const float ev[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
       for (int j = 0; j < 4; ++j)
@@ -127,26 +137,26 @@ __device__ __forceinline__ void rot_task(float* __restrict__ sm, uint32_t e_off,
       const bool neg = ((r & 1) != 0) != odd0;
       if (neg) o = make_float2(-ar[r], -ai[r]);
     }
-    *reinterpret_cast<float2*>(sm + out_off + r * kRowF) = o;
+    sts2(out_addr + r * kRowB, o);
   }
 }
 
 template <bool BACK>
-__device__ __forceinline__ void rot_dispatch(int R, float* sm, uint32_t e_off, uint32_t ws, int w,
-                                             uint32_t in_off, uint32_t out_off, bool odd0) {
+__device__ __forceinline__ void rot_dispatch(int R, uint32_t e_addr, uint32_t ws_b, int w,
+                                             uint32_t in_addr, uint32_t out_addr, bool odd0) {
   switch (R) {
-    case 1: rot_task<1, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
-    case 2: rot_task<2, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
-    case 3: rot_task<3, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
-    case 4: rot_task<4, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
-    case 5: rot_task<5, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
-    case 6: rot_task<6, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
-    case 7: rot_task<7, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
-    case 8: rot_task<8, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
-    case 9: rot_task<9, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
-    case 10: rot_task<10, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
-    case 11: rot_task<11, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
-    default: rot_task<12, BACK>(sm, e_off, ws, w, in_off, out_off, odd0); break;
+    case 1: rot_task<1, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
+    case 2: rot_task<2, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
+    case 3: rot_task<3, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
+    case 4: rot_task<4, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
+    case 5: rot_task<5, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
+    case 6: rot_task<6, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
+    case 7: rot_task<7, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
+    case 8: rot_task<8, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
+    case 9: rot_task<9, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
+    case 10: rot_task<10, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
+    case 11: rot_task<11, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
+    default: rot_task<12, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
   }
 }
 
@@ -154,27 +164,26 @@ __device__ __forceinline__ void rot_dispatch(int R, float* sm, uint32_t e_off, u
 // (for m = 0 only the single column x_0).  p_off / q_off: float offsets of the first input rows
 // (degree n = m) of the two columns; they advance by 2n+1 and 2n+2 rows per degree.
 template <int R, bool TWO>
-__device__ __forceinline__ void coax_task(float* __restrict__ sm, uint32_t c_off, uint32_t ws, int w,
-                                          int m, int r0, uint32_t p_off, uint32_t q_off,
-                                          uint32_t out_base) {
+__device__ __forceinline__ void coax_task(uint32_t c_addr, uint32_t ws_b, int w, int m, int r0,
+                                          uint32_t p_addr, uint32_t q_addr, uint32_t out_base) {
   float pr[R], pi[R], qr[R], qi[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) pr[r] = pi[r] = qr[r] = qi[r] = 0.0f;
-  constexpr uint32_t kRowF = 2 * kRow;
-  uint32_t step = uint32_t(2 * m + 1) * kRowF;
+  constexpr uint32_t kRowB = 8 * kRow;
+  uint32_t step = uint32_t(2 * m + 1) * kRowB;
 #pragma unroll 1
   for (int k = w; k > 0; --k) {
-    const float2 xp = lds2(sm, p_off);
+    const float2 xp = lds2(p_addr);
     float2 xm = make_float2(0.f, 0.f);
-    if (TWO) xm = lds2(sm, q_off);
+    if (TWO) xm = lds2(q_addr);
     float cr[R], ci[R];
     if (R == 1) {
-      const float2 c = lds2(sm, c_off);
+      const float2 c = lds2(c_addr);
       cr[0] = c.x; ci[0] = c.y;
     } else {
 #pragma unroll
       for (int v = 0; v < (R + 1) / 2; ++v) {
-        const float4 c = lds4(sm, c_off + 4 * v);
+        const float4 c = lds4(c_addr + 16 * v);
         cr[2 * v] = c.x; ci[2 * v] = c.y;
         if (2 * v + 1 < R) { cr[2 * v + 1] = c.z; ci[2 * v + 1] = c.w; }
       }
@@ -192,29 +201,31 @@ __device__ __forceinline__ void coax_task(float* __restrict__ sm, uint32_t c_off
         qi[r] = fmaf(ci[r], xm.x, qi[r]);
       }
     }
-    p_off += step;
-    q_off += step + kRowF;
-    step += 2 * kRowF;
-    c_off += ws;
+    p_addr += step;
+    q_addr += step + kRowB;
+    step += 2 * kRowB;
+    c_addr += ws_b;
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int nu = m + r0 + r;
-    *reinterpret_cast<float2*>(sm + out_base + uint32_t(nu * nu + m) * kRowF) = make_float2(pr[r], pi[r]);
-    if (TWO)
-      *reinterpret_cast<float2*>(sm + out_base + uint32_t(nu * nu + nu + m) * kRowF) = make_float2(qr[r], qi[r]);
+    sts2(out_base + uint32_t(nu * nu + m) * kRowB, make_float2(pr[r], pi[r]));
+    if (TWO) sts2(out_base + uint32_t(nu * nu + nu + m) * kRowB, make_float2(qr[r], qi[r]));
   }
 }
 
 template <bool TWO>
-__device__ __forceinline__ void coax_dispatch(int R, float* sm, uint32_t c_off, uint32_t ws, int w,
-                                              int m, int r0, uint32_t p_off, uint32_t q_off,
-                                              uint32_t out_base) {
+__device__ __forceinline__ void coax_dispatch(int R, uint32_t c_addr, uint32_t ws_b, int w, int m,
+                                              int r0, uint32_t p_addr, uint32_t q_addr, uint32_t out_base) {
   switch (R) {
-    case 1: coax_task<1, TWO>(sm, c_off, ws, w, m, r0, p_off, q_off, out_base); break;
-    case 2: coax_task<2, TWO>(sm, c_off, ws, w, m, r0, p_off, q_off, out_base); break;
-    case 3: coax_task<3, TWO>(sm, c_off, ws, w, m, r0, p_off, q_off, out_base); break;
-    default: coax_task<4, TWO>(sm, c_off, ws, w, m, r0, p_off, q_off, out_base); break;
+    case 1: coax_task<1, TWO>(c_addr, ws_b, w, m, r0, p_addr, q_addr, out_base); break;
+    case 2: coax_task<2, TWO>(c_addr, ws_b, w, m, r0, p_addr, q_addr, out_base); break;
+    case 3: coax_task<3, TWO>(c_addr, ws_b, w, m, r0, p_addr, q_addr, out_base); break;
+    case 4: coax_task<4, TWO>(c_addr, ws_b, w, m, r0, p_addr, q_addr, out_base); break;
+    case 5: coax_task<5, TWO>(c_addr, ws_b, w, m, r0, p_addr, q_addr, out_base); break;
+    case 6: coax_task<6, TWO>(c_addr, ws_b, w, m, r0, p_addr, q_addr, out_base); break;
+    case 7: coax_task<7, TWO>(c_addr, ws_b, w, m, r0, p_addr, q_addr, out_base); break;
+    default: coax_task<8, TWO>(c_addr, ws_b, w, m, r0, p_addr, q_addr, out_base); break;
   }
 }
 
@@ -237,7 +248,10 @@ __global__ void __launch_bounds__(kThreads, 2) translate_kernel(const TranslateA
   float2* s_ph = s_coax + sp.coax_c;  // e^{i m phi}, m = 0..P
   float2* A = s_ph + sp.phase_c;
   float2* B = A + sp.tile_c;
-  unsigned short* s_unit = reinterpret_cast<unsigned short*>(B + sp.tile_c);  // n << 8 | m per unit
+  // per gather unit (n, m >= 0): raw index of (n, +m) << 16 | folded row of s_m;  t_m sits n rows
+  // further, (n, -m) sits 2m raw entries back
+  uint32_t* s_unit = reinterpret_cast<uint32_t*>(B + sp.tile_c);
+  unsigned char* s_um = reinterpret_cast<unsigned char*>(s_unit + n_units);  // (n << 4 | m) needs 2 bytes
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t it_begin = uint32_t(uint64_t(a.n_items) * blockIdx.x / gridDim.x);
@@ -248,7 +262,10 @@ __global__ void __launch_bounds__(kThreads, 2) translate_kernel(const TranslateA
     int n = int((sqrtf(8.0f * float(u) + 1.0f) - 1.0f) * 0.5f);
     while (n * (n + 1) / 2 > u) --n;
     while ((n + 1) * (n + 2) / 2 <= u) ++n;
-    s_unit[u] = (unsigned short)(n << 8 | (u - n * (n + 1) / 2));
+    const int m = u - n * (n + 1) / 2;
+    s_unit[u] = uint32_t(n * (n + 1) + m) << 16 | uint32_t(n * n + m);
+    s_um[2 * u] = (unsigned char)n;
+    s_um[2 * u + 1] = (unsigned char)m;
   }
 
   // gather mapping: 4 pairs x 8 lanes per warp; a lane owns units u = ge + 8 j, i.e. the two
@@ -263,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 2) translate_kernel(const TranslateA
       const int u = ge + 8 * j;
       gxp[j] = gxm[j] = make_float2(0.f, 0.f);
       if (live && u < n_units) {
-        const int n = s_unit[u] >> 8, m = s_unit[u] & 0xff, i = n * (n + 1) + m;
+        const int i = s_unit[u] >> 16, m = s_um[2 * u + 1];
         gxp[j] = row[i];
         gxm[j] = row[i - 2 * m];
       }
@@ -271,11 +288,10 @@ __global__ void __launch_bounds__(kThreads, 2) translate_kernel(const TranslateA
   };
 
   const TranslateSchedule& sched = c_sched[P];
-  // float offsets of the regions inside the shared window
-  const uint32_t coax_f = uint32_t(sp.rot_floats), ph_f = coax_f + 2u * uint32_t(sp.coax_c),
-                 a_f = ph_f + 2u * uint32_t(sp.phase_c), b_f = a_f + 2u * uint32_t(sp.tile_c);
-  constexpr uint32_t kRowF = 2 * kRow;
-  const uint32_t a_lane = a_f + 2 * lane, b_lane = b_f + 2 * lane;
+  // byte addresses inside the shared window
+  const uint32_t win = uint32_t(__cvta_generic_to_shared(smem));
+  const uint32_t a_lane = uint32_t(__cvta_generic_to_shared(A)) + 8 * lane,
+                 b_lane = uint32_t(__cvta_generic_to_shared(B)) + 8 * lane;
 
   __syncthreads();  // s_unit
   TranslateItem item = a.items[it_begin];
@@ -311,16 +327,16 @@ __global__ void __launch_bounds__(kThreads, 2) translate_kernel(const TranslateA
     for (int j = 0; j < NU; ++j) {
       const int u = ge + 8 * j;
       if (u < n_units) {
-        const int n = s_unit[u] >> 8, m = s_unit[u] & 0xff;
+        const int n = s_um[2 * u], m = s_um[2 * u + 1], fs = s_unit[u] & 0xffff;
         const float2 ph = s_ph[m], xp = gxp[j], xm = gxm[j];
         if (m == 0) {
-          A[(n * n) * kRow + gp] = xp;
+          A[fs * kRow + gp] = xp;
         } else {
           const float2 av = make_float2(xp.x * ph.x - xp.y * ph.y, xp.x * ph.y + xp.y * ph.x);
           float2 bv = make_float2(xm.x * ph.x + xm.y * ph.y, xm.y * ph.x - xm.x * ph.y);
           if (m & 1) bv = make_float2(-bv.x, -bv.y);
-          A[(n * n + m) * kRow + gp] = make_float2(av.x + bv.x, av.y + bv.y);
-          A[(n * n + n + m) * kRow + gp] = make_float2(av.x - bv.x, av.y - bv.y);
+          A[fs * kRow + gp] = make_float2(av.x + bv.x, av.y + bv.y);
+          A[(fs + n) * kRow + gp] = make_float2(av.x - bv.x, av.y - bv.y);
         }
       }
     }
@@ -333,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 2) translate_kernel(const TranslateA
     // stage 2: forward rotation A -> B
     for (int t = sched.rot_begin[warp]; t < sched.rot_begin[warp + 1]; ++t) {
       const TranslateRotTask d = sched.rot[t];
-      rot_dispatch<false>((d.packed >> 16) & 0xff, smem, d.e_off, d.packed & 0xff, (d.packed >> 8) & 0xff,
+      rot_dispatch<false>((d.packed >> 16) & 0xff, win + d.e_off, d.packed & 0xff, (d.packed >> 8) & 0xff,
                           a_lane + d.in_rel, b_lane + d.out_rel, false);
     }
     __syncthreads();
@@ -342,29 +358,29 @@ __global__ void __launch_bounds__(kThreads, 2) translate_kernel(const TranslateA
       const TranslateCoaxTask d = sched.coax[t];
       const int m = (d.packed >> 16) & 0x3f, r0 = (d.packed >> 22) & 0x3f, R = d.packed >> 28;
       if (m == 0)
-        coax_dispatch<false>(R, smem, d.c_off, d.packed & 0xff, (d.packed >> 8) & 0xff, m, r0,
+        coax_dispatch<false>(R, win + d.c_off, d.packed & 0xff, (d.packed >> 8) & 0xff, m, r0,
                              b_lane + d.p_rel, b_lane + d.q_rel, a_lane);
       else
-        coax_dispatch<true>(R, smem, d.c_off, d.packed & 0xff, (d.packed >> 8) & 0xff, m, r0,
+        coax_dispatch<true>(R, win + d.c_off, d.packed & 0xff, (d.packed >> 8) & 0xff, m, r0,
                             b_lane + d.p_rel, b_lane + d.q_rel, a_lane);
     }
     __syncthreads();
     // stage 4: inverse rotation A -> B (same table, sign-twiddled)
     for (int t = sched.rot_begin[warp]; t < sched.rot_begin[warp + 1]; ++t) {
       const TranslateRotTask d = sched.rot[t];
-      rot_dispatch<true>((d.packed >> 16) & 0xff, smem, d.e_off, d.packed & 0xff, (d.packed >> 8) & 0xff,
+      rot_dispatch<true>((d.packed >> 16) & 0xff, win + d.e_off, d.packed & 0xff, (d.packed >> 8) & 0xff,
                          a_lane + d.in_rel, b_lane + d.out_rel, (d.packed >> 24) & 1);
     }
     __syncthreads();
     // stage 5a: unfold B -> A in the caller's coefficient order, with e^{-i mu phi}:
     //   y_m = (u + v)/2 e^{-i m phi},   y_{-m} = (-1)^m (u - v)/2 e^{+i m phi}
     for (int u = ge; u < n_units; u += 8) {
-      const int n = s_unit[u] >> 8, m = s_unit[u] & 0xff;
-      const float2 uu = B[(n * n + m) * kRow + gp];
+      const int n = s_um[2 * u], m = s_um[2 * u + 1], fs = s_unit[u] & 0xffff;
+      const float2 uu = B[fs * kRow + gp];
       if (m == 0) {
         A[(n * n + n) * kRow + gp] = uu;
       } else {
-        const float2 vv = B[(n * n + n + m) * kRow + gp], ph = s_ph[m];
+        const float2 vv = B[(fs + n) * kRow + gp], ph = s_ph[m];
         const float2 yp = make_float2(0.5f * (uu.x + vv.x), 0.5f * (uu.y + vv.y));
         float2 ym = make_float2(0.5f * (uu.x - vv.x), 0.5f * (uu.y - vv.y));
         if (m & 1) ym = make_float2(-ym.x, -ym.y);
@@ -448,25 +464,27 @@ void build_translate_schedule(int P, TranslateSchedule* out) {
       for (int i = 0; i < np; ++i) {
         const int R = parts[i];
         TranslateRotTask d;
-        d.e_off = uint32_t(table + r0);
-        d.in_rel = uint32_t(base) * kRowF;
-        d.out_rel = uint32_t(base + r0) * kRowF;
-        d.packed = uint32_t(ws) | uint32_t(w) << 8 | uint32_t(R) << 16 | uint32_t(r0 & 1) << 24;
+        d.e_off = 4u * uint32_t(table + r0);
+        d.in_rel = 4u * uint32_t(base) * kRowF;
+        d.out_rel = 4u * uint32_t(base + r0) * kRowF;
+        d.packed = 4u * uint32_t(ws) | uint32_t(w) << 8 | uint32_t(R) << 16 | uint32_t(r0 & 1) << 24;
         rot.push_back({d, w * (2 * R + 6) + 40});
         r0 += R;
       }
     }
   for (int m = 0; m <= P; ++m) {
     const int w = P + 1 - m;
-    for (int r0 = 0; r0 < w; r0 += 4) {
+    // tiles of <= 4 rows (measured: 8-row tiles balance worse over the 8 warps and are slower)
+    for (int r0 = 0; r0 < w;) {
       const int R = std::min(4, w - r0);
       TranslateCoaxTask d;
-      d.c_off = coax_f + 2u * uint32_t(coax_block_offset(P, m) + r0);
-      d.p_rel = uint32_t(m * m + m) * kRowF;
-      d.q_rel = uint32_t(m * m + 2 * m) * kRowF;
-      d.packed = uint32_t(2 * coax_row_stride(P, m)) | uint32_t(w) << 8 | uint32_t(m) << 16 |
-                 uint32_t(r0) << 22 | uint32_t(R) << 28;
+      d.c_off = 4u * (coax_f + 2u * uint32_t(coax_block_offset(P, m) + r0));
+      d.p_rel = 4u * uint32_t(m * m + m) * kRowF;
+      d.q_rel = 4u * uint32_t(m * m + 2 * m) * kRowF;
+      d.packed = 4u * uint32_t(2 * coax_row_stride(P, m)) | uint32_t(w) << 8 | uint32_t(m) << 16 |
+                 uint32_t(r0) << 22 | uint32_t(R) << 28;  // R <= 8 fits bits 28..31
       coax.push_back({d, w * ((m ? 8 : 4) * R + 8) + 40});
+      r0 += R;
     }
   }
   if (rot.size() > size_t(kTranslateMaxTasks) || coax.size() > size_t(kTranslateMaxTasks))
