@@ -35,10 +35,10 @@ UNIT = "Mpoints/s"
 
 
 def m2l_flops_per_pair(order: int) -> tuple[int, int]:
-    """(executed, dense-equivalent) FP32 flops of one M2L cell pair (DESIGN.md §5):
-    executed = 2 flop x [2 rotations x 2 sum_n (2n+1)^2 real-x-complex MACs
-                         + 4 sum_m (P+1-|m|)^2 complex MACs]; dense = 8 (P+1)^4."""
-    rot = sum((2 * n + 1) ** 2 for n in range(order + 1))
+    """(executed, dense-equivalent) FP32 flops of one M2L cell pair (DESIGN.md §5.2):
+    executed = 2 flop x [2 rotations x 2 sum_n ((n+1)^2 + n^2) real-x-complex MACs (folded +-m blocks)
+                         + 4 sum_m (P+1-|m|)^2 complex MACs (coaxial step)];  dense = 8 (P+1)^4."""
+    rot = sum((n + 1) ** 2 + n ** 2 for n in range(order + 1))
     coax = sum((order + 1 - abs(m)) ** 2 for m in range(-order, order + 1))
     return 2 * (2 * 2 * rot + 4 * coax), 8 * (order + 1) ** 4
 
@@ -231,7 +231,17 @@ def run_single(args, cfg):
                            f"nominal 148x128x2x1.965 GHz = {nominal:.1f}",
             "flops_per_unit": ex, "units_per_launch": st0["m2l_pairs"],
             "dense_equivalent_tflops": st0["m2l_pairs"] * dense / kern["m2l"] * 1e-12 if kern["m2l"] else None,
-            "ms_per_launch": kern["m2l"] * 1e3, "traffic": None},
+            # the same launch counted with UNFOLDED rotation blocks, (2n+1)^2 instead of (n+1)^2 + n^2
+            "unfolded_rotation_equivalent_tflops": st0["m2l_pairs"] * 2 * (
+                4 * sum((2 * j + 1) ** 2 for j in range(cfg.order + 1))
+                + 4 * sum((cfg.order + 1 - abs(m)) ** 2 for m in range(-cfg.order, cfg.order + 1))
+            ) / kern["m2l"] * 1e-12 if kern["m2l"] else None,
+            "ms_per_launch": kern["m2l"] * 1e3,
+            # dram__bytes_read + dram__bytes_write of this launch from the committed ncu --set full
+            # capture of the same configuration (profiles/r01_ncu_cfg2_full.txt); algorithmic bytes
+            # are pairs x 2 x 8 (P+1)^2 (one source row read, one destination row reduced)
+            "traffic": 18.24e9 if (cfg.name == "cfg2" and n == cfg.n) else None,
+            "algorithmic_bytes": st0["m2l_pairs"] * 2 * 8 * (cfg.order + 1) ** 2},
         "kernels": {
             "p2p": {"ms": kern["p2p"] * 1e3, "tflops_24flop_per_pair": p2p_tf,
                     "frac_of_fp32_peak": p2p_tf / fp32_peak if fp32_peak else None,
