@@ -165,3 +165,84 @@ def test_device_built_tree_and_lists_equal_the_reference(case):
     yd, yh = dev.matvec(q), host.matvec(q)
     assert rel_l2(yd, g[f"{case}_y"]) < TOL and rel_l2(yh, g[f"{case}_y"]) < TOL
     assert rel_l2(yd, yh) < 2e-6
+
+
+# ---- edge cases (reference tests/test_fmm.cpp:897-939 "base cases", octree.cpp degenerate leaves) ----
+def _check_against_direct(oracle, xyz, q, k, order, tol=TOL, **kw):
+    op = HfmmCuda(k=k, order=order, **kw)
+    op.set_points(xyz)
+    y = op.matvec(q)
+    exact = oracle.direct_sum(xyz, q, k)
+    assert np.isfinite(y).all()
+    if np.linalg.norm(exact) > 0:
+        assert rel_l2(y, exact) < tol
+    else:
+        assert np.abs(y).max() == 0
+    return op
+
+
+def test_tiny_inputs(oracle):
+    rng = np.random.default_rng(3)
+    for n in (1, 2, 3, 17, 65):
+        xyz = rng.uniform(-1, 1, (n, 3))
+        q = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+        op = _check_against_direct(oracle, xyz, q, 1.5, 6, ncrit=4)
+        assert op.stats()["n_bodies"] == n
+
+
+def test_coincident_and_degenerate_geometry(oracle):
+    rng = np.random.default_rng(4)
+    q = rng.uniform(-1, 1, 300) + 1j * rng.uniform(-1, 1, 300)
+    # all bodies on one point: the box degenerates (width := 1), every pair is skipped (R = 0)
+    same = np.tile([[0.3, -0.2, 0.7]], (300, 1))
+    _check_against_direct(oracle, same, q, 2.0, 6, ncrit=16)
+    # 40 bodies on one point inside a cloud: an over-full leaf at level 21 (degenerate leaf)
+    cloud = rng.uniform(-1, 1, (300, 3))
+    cloud[:40] = cloud[0]
+    _check_against_direct(oracle, cloud, q, 2.0, 8, ncrit=16)
+    # collinear and coplanar sets
+    line = np.zeros((300, 3)); line[:, 0] = np.linspace(-1, 1, 300)
+    _check_against_direct(oracle, line, q, 3.0, 8, ncrit=8)
+    plane = rng.uniform(-1, 1, (300, 3)); plane[:, 2] = 0.25
+    _check_against_direct(oracle, plane, q, 3.0, 8, ncrit=8)
+
+
+@pytest.mark.parametrize("order", [0, 1, 2, 5, 16])
+def test_expansion_orders(oracle, order):
+    # any order up to the supported maximum; accuracy is checked against the oracle FMM at the
+    # SAME order (low orders truncate, they are not supposed to match the direct sum)
+    n, k = 2500, 2.0
+    xyz, q = sphere_points(n, 31), charges(n, 31)
+    op = HfmmCuda(k=k, order=order, ncrit=32)
+    op.set_points(xyz)
+    y = op.matvec(q)
+    y_ref = oracle.fmm(xyz, k, order, ncrit=32, leaf_cap=0.5, theta=0.4, kd_max=1.0).matvec(q)
+    assert rel_l2(y, y_ref) < TOL
+
+
+def test_leaf_capacity_extremes(oracle):
+    n, k = 1500, 2.0
+    xyz, q = sphere_points(n, 33), charges(n, 33)
+    for ncrit in (1, 7, 200, 5000):      # 5000 > n: a single leaf, pure direct sum
+        _check_against_direct(oracle, xyz, q, k, 10, ncrit=ncrit)
+
+
+def test_argument_errors():
+    from paper_1803_09948_b200 import HfmmError
+
+    op = HfmmCuda(k=1.0, order=4)
+    with pytest.raises(HfmmError) as e:      # matvec before set_points
+        op.lib.hfmm_cuda_matvec  # noqa: B018
+        op.n = 4
+        op.matvec(np.zeros(4))
+    assert e.value.kind == "config_error"
+    bad = np.zeros((10, 3)); bad[3, 1] = np.nan
+    with pytest.raises(HfmmError) as e:
+        op.set_points(bad)
+    assert e.value.kind == "domain_error"
+    with pytest.raises(HfmmError) as e:
+        op.set_points(np.zeros((0, 3)))
+    assert e.value.kind == "config_error"    # "no bodies to enclose" (octree.cpp:54)
+    op.set_points(np.random.default_rng(0).uniform(-1, 1, (50, 3)))
+    with pytest.raises(ValueError):
+        op.matvec(np.zeros(49))
