@@ -86,7 +86,7 @@ struct TranslateItem {
   uint32_t pad;
 };
 inline constexpr int kTranslateBatch = 32;   // pairs per work item (= lanes of a warp)
-inline constexpr int kTranslateWarps = 8;    // warps per CTA of the translation kernel
+inline constexpr int kTranslateWarps = 16;   // most warps per CTA of the translation kernel (8 or 16)
 inline constexpr int kTranslateMaxTasks = 80;
 
 // Per-order static schedule of the translation kernel (kept in __constant__ memory): each stage is a

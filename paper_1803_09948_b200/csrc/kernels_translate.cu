@@ -36,8 +36,7 @@ namespace hfmm_b200 {
 
 namespace {
 
-constexpr int kWarps = kTranslateWarps;
-constexpr int kThreads = kWarps * 32;
+
 constexpr int kRow = 34;  // float2 elements per operand row: 32 pairs + 2 pad (bank spread)
 
 struct SmemPlan {
@@ -74,6 +73,12 @@ __device__ __forceinline__ float4 lds4(uint32_t addr) {
 }
 __device__ __forceinline__ void sts2(uint32_t addr, float2 v) {
   asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
+}
+
+// warps per CTA: 8 with two CTAs per SM while two operand tile pairs fit the 227 KB of shared memory
+// (P <= 12), else ONE CTA of 16 warps per SM so the SM keeps 16 resident warps (P = 13..16)
+inline int translate_warps(int P) {
+  return 2 * (smem_plan(P).bytes + 1024) <= size_t(227) * 1024 ? 8 : 16;
 }
 
 // ---- rotation task: R output rows of one folded sub-block;  out[r] = sum_k E[k][r] * in[k] ------
@@ -237,8 +242,10 @@ __constant__ TranslateSchedule c_sched[kMaxOrder + 1];
 // tables in shared memory are reloaded only when the class changes).  The gather of the NEXT item
 // is issued into registers while the current item drains through its reductions, so the chain
 // item -> pair list -> source rows never sits on the critical path.
-template <int NU>  // (n, m >= 0) units per lane of the gather: ceil((P+1)(P+2)/2 / 8)
-__global__ void __launch_bounds__(kThreads, 2) translate_kernel(const TranslateArgs a) {
+template <int NU, int WARPS>  // NU: (n, m >= 0) gather units per lane = ceil((P+1)(P+2)/2 / WARPS)
+__global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? 2 : 1) translate_kernel(const TranslateArgs a) {
+  constexpr int kThreads = WARPS * 32;
+  constexpr int kLanesPerPair = WARPS;  // 32 pairs x WARPS lanes = all threads of the CTA
   extern __shared__ __align__(16) float smem[];
   const int P = a.order;
   const SmemPlan sp = smem_plan(P);
@@ -268,16 +275,16 @@ __global__ void __launch_bounds__(kThreads, 2) translate_kernel(const TranslateA
     s_um[2 * u + 1] = (unsigned char)m;
   }
 
-  // gather mapping: 4 pairs x 8 lanes per warp; a lane owns units u = ge + 8 j, i.e. the two
-  // source coefficients (n, +m) and (n, -m) it folds into s_m and t_m
-  const int gq = lane >> 3, ge = lane & 7, gp = warp * 4 + gq;
+  // gather mapping: 32/WARPS pairs x WARPS lanes per warp; a lane owns units u = ge + WARPS j, i.e.
+  // the two source coefficients (n, +m) and (n, -m) it folds into s_m and t_m
+  const int gq = lane / kLanesPerPair, ge = lane % kLanesPerPair, gp = warp * (32 / kLanesPerPair) + gq;
   float2 gxp[NU], gxm[NU];
   auto issue_gather = [&](const TranslateItem& it) {
     const bool live = gp < int(it.count);
     const float2* row = live ? a.src + size_t(a.pair_src[it.pair_begin + gp]) * a.stride : nullptr;
 #pragma unroll
     for (int j = 0; j < NU; ++j) {
-      const int u = ge + 8 * j;
+      const int u = ge + kLanesPerPair * j;
       gxp[j] = gxm[j] = make_float2(0.f, 0.f);
       if (live && u < n_units) {
         const int i = s_unit[u] >> 16, m = s_um[2 * u + 1];
@@ -325,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, 2) translate_kernel(const TranslateA
     //   a = x_m e^{i m phi},  b = (-1)^m x_{-m} e^{-i m phi}:   s_m = a + b,  t_m = a - b
 #pragma unroll
     for (int j = 0; j < NU; ++j) {
-      const int u = ge + 8 * j;
+      const int u = ge + kLanesPerPair * j;
       if (u < n_units) {
         const int n = s_um[2 * u], m = s_um[2 * u + 1], fs = s_unit[u] & 0xffff;
         const float2 ph = s_ph[m], xp = gxp[j], xm = gxm[j];
@@ -374,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 2) translate_kernel(const TranslateA
     __syncthreads();
     // stage 5a: unfold B -> A in the caller's coefficient order, with e^{-i mu phi}:
     //   y_m = (u + v)/2 e^{-i m phi},   y_{-m} = (-1)^m (u - v)/2 e^{+i m phi}
-    for (int u = ge; u < n_units; u += 8) {
+    for (int u = ge; u < n_units; u += kLanesPerPair) {
       const int n = s_um[2 * u], m = s_um[2 * u + 1], fs = s_unit[u] & 0xffff;
       const float2 uu = B[fs * kRow + gp];
       if (m == 0) {
@@ -389,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 2) translate_kernel(const TranslateA
       }
     }
     // a lane group reads back only what it wrote itself (same pair column gp): a warp-level
-    // barrier orders the stores of the 8 lanes of the group before the loads below
+    // barrier orders the stores of the lanes of the group before the loads below
     __syncwarp();
 
     // stage 5b: start the next item's gather, then accumulate this item into its destinations,
@@ -397,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 2) translate_kernel(const TranslateA
     if (has_next) issue_gather(next);
     if (gp < count) {
       float* dst = reinterpret_cast<float*>(a.dst + size_t(a.pair_dst[item.pair_begin + gp]) * a.stride);
-      for (int i2 = ge; i2 < dim / 2; i2 += 8) {
+      for (int i2 = ge; i2 < dim / 2; i2 += kLanesPerPair) {
         const float2 lo = A[(2 * i2) * kRow + gp], hi = A[(2 * i2 + 1) * kRow + gp];
         atomicAdd(reinterpret_cast<float4*>(dst) + i2, make_float4(lo.x, lo.y, hi.x, hi.y));
       }
@@ -416,6 +423,8 @@ __global__ void __launch_bounds__(kThreads, 2) translate_kernel(const TranslateA
 // hand the tasks to the warps (longest processing time first)
 void build_translate_schedule(int P, TranslateSchedule* out) {
   const SmemPlan sp = smem_plan(P);
+  const int kWarps = translate_warps(P);
+  const int max_rows = kWarps == 8 ? 12 : 8;  // 16 warps need more, smaller tasks to balance
   const uint32_t kRowF = 2 * kRow, coax_f = uint32_t(sp.rot_floats);
   struct RotT {
     TranslateRotTask d;
@@ -430,13 +439,13 @@ void build_translate_schedule(int P, TranslateSchedule* out) {
   // rows of a sub-block are cut into tiles that start at multiples of 4 (aligned 16-byte
   // coefficient loads) and hold <= 12 rows; the split minimising sum(2R + 6) (instructions per
   // input step) is found by exhaustive search
-  auto cut = [](int w, int parts[4]) {
+  auto cut = [max_rows](int w, int parts[4]) {
     int best_cost = 1 << 30, best_n = 0;
-    for (int a = 0; a <= 12; a += 4)
-      for (int b = 0; b <= 12; b += 4)
-        for (int c = 0; c <= 12; c += 4) {
+    for (int a = 0; a <= max_rows; a += 4)
+      for (int b = 0; b <= max_rows; b += 4)
+        for (int c = 0; c <= max_rows; c += 4) {
           const int last = w - a - b - c;
-          if (last < 1 || last > 12) continue;
+          if (last < 1 || last > max_rows) continue;
           if ((a == 0 && (b || c)) || (b == 0 && c)) continue;
           int cand[4] = {a, b, c, last}, tmp[4], np = 0, cost = 0;
           for (int v : cand)
@@ -489,10 +498,10 @@ void build_translate_schedule(int P, TranslateSchedule* out) {
   }
   if (rot.size() > size_t(kTranslateMaxTasks) || coax.size() > size_t(kTranslateMaxTasks))
     throw Error(HFMM_ERR_INTERNAL, "translation schedule overflow");
-  auto distribute = [](auto& tasks, auto* flat, int* begin) {
+  auto distribute = [kWarps](auto& tasks, auto* flat, int* begin) {
     std::stable_sort(tasks.begin(), tasks.end(), [](const auto& x, const auto& y) { return x.cost > y.cost; });
     std::vector<std::vector<int>> per(kWarps);
-    long load[kWarps] = {};
+    std::vector<long> load(kWarps, 0);
     for (size_t i = 0; i < tasks.size(); ++i) {
       int best = 0;
       for (int w = 1; w < kWarps; ++w)
@@ -505,7 +514,7 @@ void build_translate_schedule(int P, TranslateSchedule* out) {
       begin[w] = pos;
       for (int i : per[w]) flat[pos++] = tasks[i].d;
     }
-    begin[kWarps] = pos;
+    for (int w = kWarps; w <= kTranslateWarps; ++w) begin[w] = pos;
   };
   *out = TranslateSchedule{};
   distribute(rot, out->rot, out->rot_begin);
@@ -521,15 +530,15 @@ void upload_translate_schedule(int order) {
 int translate_batch_size(int) { return kTranslateBatch; }
 
 namespace {
-template <int NU>
+template <int NU, int WARPS>
 void launch_translate_nu(const TranslateArgs& a, cudaStream_t s, size_t bytes, int ctas) {
   static int configured_for = -1;
   if (configured_for < int(bytes)) {
-    HFMM_CUDA_CHECK(cudaFuncSetAttribute(translate_kernel<NU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(bytes)));
+    HFMM_CUDA_CHECK(cudaFuncSetAttribute(translate_kernel<NU, WARPS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
     configured_for = int(bytes);
   }
-  translate_kernel<NU><<<ctas, kThreads, bytes, s>>>(a);
+  translate_kernel<NU, WARPS><<<ctas, WARPS * 32, bytes, s>>>(a);
   HFMM_CUDA_CHECK(cudaGetLastError());
 }
 }  // namespace
@@ -543,15 +552,20 @@ void launch_translate(const TranslateArgs& a, cudaStream_t s) {
     HFMM_CUDA_CHECK(cudaGetDevice(&dev));
     HFMM_CUDA_CHECK(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev));
   }
-  // persistent grid: two CTAs per SM when their shared memory fits (227 KB per SM), else one
-  const int per_sm = 2 * (sp.bytes + 1024) <= 227 * 1024 ? 2 : 1;
-  const int ctas = int(std::min<uint32_t>(a.n_items, uint32_t(per_sm * sm_count)));
-  const int nu = ((a.order + 1) * (a.order + 2) / 2 + 7) / 8;
-  if (nu <= 6) launch_translate_nu<6>(a, s, sp.bytes, ctas);         // P <= 8
-  else if (nu <= 9) launch_translate_nu<9>(a, s, sp.bytes, ctas);    // P <= 10
-  else if (nu <= 12) launch_translate_nu<12>(a, s, sp.bytes, ctas);  // P <= 12
-  else if (nu <= 15) launch_translate_nu<15>(a, s, sp.bytes, ctas);  // P <= 14
-  else launch_translate_nu<20>(a, s, sp.bytes, ctas);                // P <= 16
+  // persistent grid: two 8-warp CTAs per SM, or one 16-warp CTA when the tiles are too large
+  const int warps = translate_warps(a.order);
+  const int ctas = int(std::min<uint32_t>(a.n_items, uint32_t((warps == 8 ? 2 : 1) * sm_count)));
+  const int units = (a.order + 1) * (a.order + 2) / 2;
+  if (warps == 8) {
+    const int nu = (units + 7) / 8;
+    if (nu <= 6) launch_translate_nu<6, 8>(a, s, sp.bytes, ctas);         // P <= 8
+    else if (nu <= 9) launch_translate_nu<9, 8>(a, s, sp.bytes, ctas);    // P <= 10
+    else launch_translate_nu<12, 8>(a, s, sp.bytes, ctas);                // P <= 12
+  } else {
+    const int nu = (units + 15) / 16;
+    if (nu <= 8) launch_translate_nu<8, 16>(a, s, sp.bytes, ctas);        // P <= 14
+    else launch_translate_nu<10, 16>(a, s, sp.bytes, ctas);               // P <= 16
+  }
 }
 
 }  // namespace hfmm_b200
