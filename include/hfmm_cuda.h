@@ -190,6 +190,25 @@ int hfmm_cuda_dist_upward(hfmm_cuda_t* h, const void* q_morton_dev);
 /* out_morton_dev: n float2 in Morton order; only the owned slots are written */
 int hfmm_cuda_dist_downward(hfmm_cuda_t* h, void* out_morton_dev);
 
+/* Restarted GMRES over Morton-sharded vectors: every rank holds the slice
+ * [body_first, body_first + body_count) of each Krylov vector; inner products are local FP64
+ * reductions followed by `allreduce_sum`; the operator is the two-phase matvec above.  The three
+ * exchanges are performed by the caller's communicator through these callbacks (NCCL via
+ * torch.distributed in distributed.py); the handle's stream is idle when a callback runs and the
+ * callback must have completed its device work when it returns.  The iteration itself is the
+ * reference's (gmres.cpp:35-174), so all ranks take identical branches: they see identical
+ * reduced scalars. */
+typedef struct {
+  void* user;
+  void (*allreduce_sum)(void* user, double* values, int count);  /* host doubles, in place      */
+  void (*gather_vector)(void* user, void* full_dev);             /* n float2, Morton order       */
+  void (*gather_multipoles)(void* user);                         /* rows of hfmm_cuda_partition  */
+} hfmm_dist_callbacks;
+/* rhs_owned / x_owned: body_count interleaved complex doubles, Morton order (host) */
+int hfmm_cuda_dist_gmres(hfmm_cuda_t* h, const double* rhs_owned, double* x_owned,
+                         const hfmm_gmres_config* cfg, hfmm_gmres_report* report, double* residuals,
+                         int residual_cap, const hfmm_dist_callbacks* cb);
+
 const char* hfmm_cuda_version(void);
 
 #ifdef __cplusplus

@@ -68,6 +68,16 @@ class _GmresReport(C.Structure):
                 ("matvec_seconds", C.c_double)]
 
 
+ALLREDUCE_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_double), C.c_int)
+GATHER_VECTOR_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
+GATHER_MULTIPOLES_FN = C.CFUNCTYPE(None, C.c_void_p)
+
+
+class _DistCallbacks(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("allreduce_sum", ALLREDUCE_FN),
+                ("gather_vector", GATHER_VECTOR_FN), ("gather_multipoles", GATHER_MULTIPOLES_FN)]
+
+
 def library_path() -> str:
     return _SO
 
@@ -239,6 +249,45 @@ class HfmmCuda:
         self._check(self.lib.hfmm_cuda_gmres(self.h, rhs.ctypes.data_as(_dp), x.ctypes.data_as(_dp),
                                              C.byref(cfg), C.byref(rep), res.ctypes.data_as(_dp),
                                              len(res)))
+        return x, dict(iterations=rep.iterations, converged=bool(rep.converged),
+                       breakdown=bool(rep.breakdown), rhs_norm=rep.rhs_norm,
+                       final_residual=rep.final_residual, seconds=rep.seconds,
+                       matvec_seconds=rep.matvec_seconds, residuals=res[:rep.iterations].copy())
+
+    def dist_gmres(self, rhs_owned, allreduce_sum, gather_vector, gather_multipoles, rtol=1e-4,
+                   restart=30, max_iterations=500, precondition=True):
+        """GMRES over Morton-sharded vectors.  rhs_owned: the owned Morton slice (complex128).
+        allreduce_sum(np.ndarray[float64]) reduces in place over the ranks; gather_vector(dev_ptr)
+        all-gathers the n-float2 Morton vector at dev_ptr; gather_multipoles() exchanges the owned
+        multipole rows.  Exceptions raised inside a callback abort the solve."""
+        rhs = _c128(rhs_owned)
+        x = np.zeros(rhs.shape[0], dtype=np.complex128)
+        cfg = _GmresConfig(rtol, restart, max_iterations, int(precondition))
+        rep = _GmresReport()
+        res = np.zeros(max_iterations + 1)
+        failure = []
+
+        def guard(fn):
+            def run(*args):
+                if failure:
+                    return
+                try:
+                    fn(*args)
+                except BaseException as e:  # a callback must not unwind through C
+                    failure.append(e)
+            return run
+
+        cb = _DistCallbacks(
+            None,
+            ALLREDUCE_FN(guard(lambda _u, p, c: allreduce_sum(np.ctypeslib.as_array(p, shape=(c,))))),
+            GATHER_VECTOR_FN(guard(lambda _u, ptr: gather_vector(int(ptr)))),
+            GATHER_MULTIPOLES_FN(guard(lambda _u: gather_multipoles())))
+        rc = self.lib.hfmm_cuda_dist_gmres(self.h, rhs.ctypes.data_as(_dp), x.ctypes.data_as(_dp),
+                                           C.byref(cfg), C.byref(rep), res.ctypes.data_as(_dp),
+                                           len(res), C.byref(cb))
+        if failure:
+            raise failure[0]
+        self._check(rc)
         return x, dict(iterations=rep.iterations, converged=bool(rep.converged),
                        breakdown=bool(rep.breakdown), rhs_norm=rep.rhs_norm,
                        final_residual=rep.final_residual, seconds=rep.seconds,

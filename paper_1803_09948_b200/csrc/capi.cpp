@@ -17,10 +17,16 @@ struct hfmm_cuda {
 namespace {
 thread_local std::string g_create_error;
 
+std::string g_stale_error;
+
 template <typename Fn>
 int guarded(hfmm_cuda* h, Fn&& fn) {
   std::string* sink = (h && h->engine) ? &h->engine->last_error : &g_create_error;
   try {
+    // the CUDA "last error" is per host thread and shared with every other CUDA user of the
+    // process (torch, the caller's own code): drop what they left so that the launch checks
+    // below report this call's errors only; the leftover stays readable for diagnosis
+    if (const char* stale = Engine::take_stale_cuda_error()) g_stale_error = stale;
     fn();
     return HFMM_OK;
   } catch (const Error& e) {
@@ -203,6 +209,20 @@ int hfmm_cuda_dist_downward(hfmm_cuda_t* h, void* out_morton_dev) {
     h->engine->dist_downward(out_morton_dev);
   });
 }
+
+int hfmm_cuda_dist_gmres(hfmm_cuda_t* h, const double* rhs_owned, double* x_owned,
+                         const hfmm_gmres_config* cfg, hfmm_gmres_report* report, double* residuals,
+                         int residual_cap, const hfmm_dist_callbacks* cb) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] {
+    if (!rhs_owned || !x_owned || !cfg || !report || !cb || !cb->allreduce_sum || !cb->gather_vector ||
+        !cb->gather_multipoles)
+      throw Error(HFMM_ERR_CONFIG, "null argument");
+    h->engine->dist_gmres(rhs_owned, x_owned, *cfg, report, residuals, residual_cap, *cb);
+  });
+}
+
+const char* hfmm_debug_stale_cuda_error(void) { return g_stale_error.c_str(); }
 
 const char* hfmm_cuda_version(void) { return "hfmm-b200 0.1 (sm_100a)"; }
 

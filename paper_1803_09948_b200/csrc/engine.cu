@@ -156,6 +156,11 @@ Engine::~Engine() {
   if (stream_near_) cudaStreamDestroy(stream_near_);
 }
 
+const char* Engine::take_stale_cuda_error() {
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? nullptr : cudaGetErrorName(e);
+}
+
 void Engine::require_points() const {
   if (!have_points_) throw Error(HFMM_ERR_CONFIG, "hfmm_cuda_set_points has not been called");
 }
@@ -761,8 +766,13 @@ void Engine::collect_timings() {
   if (!timings_pending_) return;
   HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
   auto dt = [&](int a, int b) {
+    // an interval whose events were not recorded by the last call (e.g. the bracketing pair
+    // after a two-phase matvec) reads as zero; drop the error so that it is not left behind
     float v = 0;
-    cudaEventElapsedTime(&v, ev_[a], ev_[b]);
+    if (cudaEventElapsedTime(&v, ev_[a], ev_[b]) != cudaSuccess) {
+      (void)cudaGetLastError();
+      v = 0;
+    }
     return double(v) * 1e-3;
   };
   stats_.p2p_seconds = dt(0, 1);

@@ -55,7 +55,12 @@ class Engine {
                        const double* near_delta, const double* block_lu, const int32_t* block_piv);
   void gmres(const double* rhs, double* x, const hfmm_gmres_config& cfg, hfmm_gmres_report* rep,
              double* residuals, int residual_cap);
+  // clears and returns the name of a non-sticky CUDA error left behind on this host thread (or null)
+  static const char* take_stale_cuda_error();
   void evaluate_field(const double* coeff, const double* obs, size_t nobs, double* out);
+  void dist_gmres(const double* rhs_owned, double* x_owned, const hfmm_gmres_config& cfg,
+                  hfmm_gmres_report* rep, double* residuals, int residual_cap,
+                  const hfmm_dist_callbacks& cb);
 
   std::string last_error;
   const hfmm_cuda_config& config() const { return cfg_; }

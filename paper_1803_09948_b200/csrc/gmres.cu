@@ -254,6 +254,209 @@ void Engine::gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cf
   rep->matvec_seconds = matvec_s;
 }
 
+// GMRES over Morton-sharded vectors; see hfmm_cuda.h.  Same iteration as Engine::gmres; every
+// inner product is followed by the caller's allreduce, so the modified-Gram-Schmidt sweep is not
+// fused here (one host round trip per coefficient, ~2(j+1)+2 small allreduces per iteration).
+void Engine::dist_gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cfg,
+                        hfmm_gmres_report* rep, double* residuals, int residual_cap,
+                        const hfmm_dist_callbacks& cb) {
+  require_points();
+  HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  if (!(cfg.rtol > 0.0 && cfg.rtol < 1.0)) throw Error(HFMM_ERR_CONFIG, "gmres: rtol must lie in (0, 1)");
+  if (cfg.restart < 1) throw Error(HFMM_ERR_CONFIG, "gmres: restart must be >= 1");
+  if (cfg.max_iterations < 1) throw Error(HFMM_ERR_CONFIG, "gmres: max_iterations must be >= 1");
+  using clk = std::chrono::steady_clock;
+  const auto t_start = clk::now();
+  const uint32_t n = tree_.n_bodies, mloc = own_count_, first = own_first_;
+  const int m = cfg.restart;
+  const bool precond = cfg.precondition && have_lu_;
+  const bool corr = have_block_ || have_near_;
+  const uint32_t npatch = ni_ ? n / uint32_t(ni_) : 0;
+  const size_t ml = std::max<uint32_t>(mloc, 1);
+
+  auto reduce = [&](double* v, int count) { cb.allreduce_sum(cb.user, v, count); };
+  *rep = hfmm_gmres_report{};
+  double b2[1] = {0};
+  for (size_t i = 0; i < size_t(mloc) * 2; ++i) b2[0] += rhs[i] * rhs[i];
+  reduce(b2, 1);
+  const double bnorm = std::sqrt(b2[0]);
+  rep->rhs_norm = bnorm;
+  std::fill(x_out, x_out + size_t(mloc) * 2, 0.0);
+  if (bnorm == 0.0) {
+    rep->converged = 1;
+    rep->final_residual = 0;
+    return;
+  }
+  const double target = cfg.rtol * bnorm;
+
+  DeviceBuffer<float2> V(size_t(m + 1) * ml), w(ml), r32(ml), full(n), vc(n), pc(n), yc(corr ? n : 1);
+  DeviceBuffer<double2> b64(ml), x64(ml);
+  DeviceBuffer<double> scal(4), ydev(size_t(2) * m);
+  HFMM_CUDA_CHECK(cudaMemcpyAsync(b64.get(), rhs, size_t(mloc) * sizeof(double2), cudaMemcpyHostToDevice, stream_));
+  x64.zero(stream_);
+  launch_narrow(mloc, b64.get(), r32.get(), stream_);
+
+  double matvec_s = 0;
+  // Z = A M^-1 on sharded vectors: gather the operand, precondition and correct redundantly in
+  // caller order (cheap streaming kernels), run the two FMM phases around the multipole exchange
+  auto apply = [&](const float2* in, float2* out) {
+    const auto t0 = clk::now();
+    HFMM_CUDA_CHECK(cudaMemcpyAsync(full.get() + first, in, size_t(mloc) * sizeof(float2),
+                                    cudaMemcpyDeviceToDevice, stream_));
+    HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    cb.gather_vector(cb.user, full.get());
+    launch_scatter_potentials(full.get(), nullptr, body_index_.get(), nullptr, vc.get(), n, stream_);
+    const float2* xc = vc.get();
+    if (precond) {
+      launch_precondition(npatch, ni_, block_lu_.get(), block_piv_.get(), vc.get(), pc.get(), stream_);
+      xc = pc.get();
+    }
+    launch_gather_charges(nullptr, xc, body_index_.get(), have_weight_ ? far_weight_.get() : nullptr,
+                          body_q_.get(), n, stream_);
+    phase_upward();
+    HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_near_));
+    if (have_far_) cb.gather_multipoles(cb.user);
+    phase_downward();
+    if (corr) {
+      yc.zero(stream_);
+      launch_corrections(n, ni_, have_block_ ? patch_block_.get() : nullptr, near_offset_.get(),
+                         near_source_.get(), have_near_ ? near_delta_.get() : nullptr, xc, yc.get(), stream_);
+    }
+    launch_combine_owned(near_.get() + first, far_.get() + first, corr ? yc.get() : nullptr,
+                         body_index_.get() + first, out, mloc, stream_);
+    HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    matvec_s += std::chrono::duration<double>(clk::now() - t0).count();
+  };
+  // <v, w> (v may be null: ||w||^2) reduced over all ranks
+  auto dot = [&](const float2* v, const float2* ww, double out[2]) {
+    scal.zero(stream_);
+    if (v) launch_mgs_step(mloc, const_cast<float2*>(ww), nullptr, nullptr, v, scal.get(), stream_);
+    else launch_norm2(mloc, ww, scal.get(), stream_);
+    scal.download(out, 2, stream_);
+    HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    reduce(out, 2);
+  };
+  auto axpy = [&](float2* ww, const float2* v, const double h[2]) {  // ww -= h v
+    HFMM_CUDA_CHECK(cudaMemcpyAsync(scal.get() + 2, h, 2 * sizeof(double), cudaMemcpyHostToDevice, stream_));
+    launch_mgs_step(mloc, ww, v, scal.get() + 2, nullptr, nullptr, stream_);
+  };
+
+  std::vector<cd> H(size_t(m + 1) * m), cs(m), sn(m), g(m + 1);
+  auto h = [&](int i, int j) -> cd& { return H[size_t(j) * (m + 1) + i]; };
+  int iterations = 0, nres = 0;
+  bool done = false, breakdown = false;
+  double last_est = -1, beta = bnorm, tmp[2];
+  while (!done) {
+    if (beta <= target || iterations >= cfg.max_iterations) break;
+    launch_scale(mloc, r32.get(), float(1.0 / beta), V.get(), stream_);
+    std::fill(g.begin(), g.end(), cd(0));
+    g[0] = beta;
+    int cols = 0;
+    for (int j = 0; j < m; ++j) {
+      if (iterations >= cfg.max_iterations) break;
+      apply(V.get() + size_t(j) * ml, w.get());
+      dot(nullptr, w.get(), tmp);
+      const double w_scale = std::sqrt(tmp[0]);
+      for (int pass = 0; pass < 2; ++pass)
+        for (int i = 0; i <= j; ++i) {
+          dot(V.get() + size_t(i) * ml, w.get(), tmp);
+          if (pass == 0) h(i, j) = cd(tmp[0], tmp[1]);
+          else h(i, j) += cd(tmp[0], tmp[1]);
+          axpy(w.get(), V.get() + size_t(i) * ml, tmp);
+        }
+      dot(nullptr, w.get(), tmp);
+      double hnext = std::sqrt(tmp[0]);
+      const bool broke = hnext <= 1e-14 * std::max(w_scale, 1e-300);
+      if (broke) hnext = 0;
+      for (int i = 0; i < j; ++i) {
+        const cd a = h(i, j), b = h(i + 1, j);
+        h(i, j) = cs[i] * a + sn[i] * b;
+        h(i + 1, j) = -std::conj(sn[i]) * a + cs[i] * b;
+      }
+      const cd a = h(j, j);
+      const double b = hnext, r = std::hypot(std::abs(a), b);
+      if (r == 0.0) {
+        cs[j] = 1;
+        sn[j] = 0;
+      } else if (std::abs(a) == 0.0) {
+        cs[j] = 0;
+        sn[j] = 1;
+      } else {
+        cs[j] = std::abs(a) / r;
+        sn[j] = (a / std::abs(a)) * (b / r);
+      }
+      h(j, j) = cs[j] * a + sn[j] * b;
+      g[j + 1] = -std::conj(sn[j]) * g[j];
+      g[j] = cs[j] * g[j];
+      ++iterations;
+      cols = j + 1;
+      last_est = std::abs(g[j + 1]);
+      if (residuals && nres < residual_cap) residuals[nres] = last_est / bnorm;
+      ++nres;
+      if (broke) {
+        breakdown = true;
+        done = true;
+        break;
+      }
+      if (last_est <= target) {
+        done = true;
+        break;
+      }
+      launch_scale(mloc, w.get(), float(1.0 / hnext), V.get() + size_t(j + 1) * ml, stream_);
+    }
+    while (cols > 0 && std::abs(h(cols - 1, cols - 1)) == 0.0) --cols;
+    std::vector<cd> y(cols);
+    for (int i = cols - 1; i >= 0; --i) {
+      cd s = g[i];
+      for (int l = i + 1; l < cols; ++l) s -= h(i, l) * y[l];
+      y[i] = std::abs(h(i, i)) == 0.0 ? cd(0) : s / h(i, i);
+    }
+    if (cols > 0) {
+      HFMM_CUDA_CHECK(cudaMemcpyAsync(ydev.get(), y.data(), sizeof(cd) * cols, cudaMemcpyHostToDevice, stream_));
+      launch_update_solution(mloc, cols, V.get(), ml, ydev.get(), x64.get(), stream_);
+      HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    }
+    if (!done) {
+      launch_narrow(mloc, x64.get(), r32.get(), stream_);
+      apply(r32.get(), w.get());
+      scal.zero(stream_);
+      launch_residual(mloc, b64.get(), w.get(), r32.get(), scal.get(), stream_);
+      scal.download(tmp, 2, stream_);
+      HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+      reduce(tmp, 1);
+      beta = std::sqrt(tmp[0]);
+    }
+  }
+  launch_narrow(mloc, x64.get(), V.get(), stream_);
+  apply(V.get(), w.get());
+  scal.zero(stream_);
+  launch_residual(mloc, b64.get(), w.get(), r32.get(), scal.get(), stream_);
+  scal.download(tmp, 2, stream_);
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  reduce(tmp, 1);
+  const double final_res = std::sqrt(tmp[0]) / bnorm;
+  if (precond) {
+    // the iterate maps back through M^-1: gather it, solve redundantly, keep the owned slots
+    HFMM_CUDA_CHECK(cudaMemcpyAsync(full.get() + first, V.get(), size_t(mloc) * sizeof(float2),
+                                    cudaMemcpyDeviceToDevice, stream_));
+    HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    cb.gather_vector(cb.user, full.get());
+    launch_scatter_potentials(full.get(), nullptr, body_index_.get(), nullptr, vc.get(), n, stream_);
+    launch_precondition(npatch, ni_, block_lu_.get(), block_piv_.get(), vc.get(), pc.get(), stream_);
+    launch_gather_charges(nullptr, pc.get(), body_index_.get(), nullptr, full.get(), n, stream_);
+    launch_widen(mloc, full.get() + first, x64.get(), stream_);
+  }
+  HFMM_CUDA_CHECK(cudaMemcpyAsync(x_out, x64.get(), size_t(mloc) * sizeof(double2), cudaMemcpyDeviceToHost, stream_));
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  rep->iterations = iterations;
+  rep->breakdown = breakdown ? 1 : 0;
+  rep->final_residual = final_res;
+  rep->converged = (final_res <= cfg.rtol || (nres > 0 && last_est / bnorm <= cfg.rtol)) ? 1 : 0;
+  rep->seconds = std::chrono::duration<double>(clk::now() - t_start).count();
+  rep->matvec_seconds = matvec_s;
+}
+
 void Engine::evaluate_field(const double* coeff, const double* obs, size_t nobs, double* out) {
   require_points();
   HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));

@@ -134,7 +134,7 @@ int translate_batch_size(int order);
 void launch_gather_charges(const double2* q_caller, const float2* q_caller_f32,
                            const uint32_t* index, const float* weight, float2* body_q, uint32_t n,
                            cudaStream_t s);
-// out[index[slot]] = near[slot] + far[slot]; exactly one of out_f64 / out_f32 is written
+// out[index[slot]] = near[slot] + far[slot] (far may be null); exactly one of out_f64 / out_f32 is written
 void launch_scatter_potentials(const float2* near, const float2* far, const uint32_t* index,
                                double2* out_f64, float2* out_f32, uint32_t n, cudaStream_t s);
 
@@ -157,6 +157,10 @@ void launch_narrow(uint32_t n, const double2* in, float2* out, cudaStream_t s);
 void launch_field(uint32_t n, const float4* src_pos, const float2* q, const float4* obs, uint32_t nobs,
                   float scale, double2* out, cudaStream_t s);
 void launch_widen(uint32_t n, const float2* in, double2* out, cudaStream_t s);
+
+// out[s] = near[s] + far[s] + corr[index[s]], s over the owned Morton slots (corr may be null)
+void launch_combine_owned(const float2* near, const float2* far, const float2* corr, const uint32_t* index,
+                          float2* out, uint32_t n, cudaStream_t s);
 
 // FFMA-only micro-benchmark; returns TFLOP/s (2 flop per FFMA)
 double run_fp32_peak_probe(cudaStream_t s);

@@ -36,7 +36,7 @@ __global__ void scatter_potentials_kernel(const float2* __restrict__ near, const
                                           float2* __restrict__ o32, uint32_t n) {
   const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
   if (slot >= n) return;
-  const float2 a = near[slot], b = far[slot];
+  const float2 a = near[slot], b = far ? far[slot] : make_float2(0.f, 0.f);
   const uint32_t i = index[slot];
   if (o64)
     o64[i] = make_double2(double(a.x) + double(b.x), double(a.y) + double(b.y));
@@ -61,7 +61,32 @@ __global__ void __launch_bounds__(256) fp32_peak_kernel(float* out, int iters, f
   if (s == 123.456f) out[0] = s;  // never true; keeps the chains alive
 }
 
+// out[s] = near[s] + far[s] + corr[index[s]] for the owned Morton slots (corr in caller order, may be null)
+__global__ void combine_owned_kernel(const float2* __restrict__ near, const float2* __restrict__ far,
+                                     const float2* __restrict__ corr, const uint32_t* __restrict__ index,
+                                     float2* __restrict__ out, uint32_t n) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  float2 v = near[s];
+  const float2 f = far[s];
+  v.x += f.x;
+  v.y += f.y;
+  if (corr) {
+    const float2 c = corr[index[s]];
+    v.x += c.x;
+    v.y += c.y;
+  }
+  out[s] = v;
+}
+
 }  // namespace
+
+void launch_combine_owned(const float2* near, const float2* far, const float2* corr, const uint32_t* index,
+                          float2* out, uint32_t n, cudaStream_t s) {
+  if (!n) return;
+  combine_owned_kernel<<<(n + 255) / 256, 256, 0, s>>>(near, far, corr, index, out, n);
+  HFMM_CUDA_CHECK(cudaGetLastError());
+}
 
 double run_fp32_peak_probe(cudaStream_t s) {
   int dev = 0, sms = 0;

@@ -113,6 +113,106 @@ class ShardedFmm:
         return self.out_full[self.first:self.first + self.count]
 
 
+    def gmres(self, rhs_local, rtol=1e-4, restart=30, max_iterations=500, precondition=True):
+        """Distributed GMRES: rhs_local / the returned solution are the owned
+        Morton slices (complex128 numpy).  Krylov vectors stay sharded on the GPUs; inner products
+        are all-reduced, operands and multipoles all-gathered, by this rank's communicator."""
+        import torch
+
+        def allreduce_sum(values):
+            t = torch.from_numpy(values).to(self.device)
+            self.dist.all_reduce(t)
+            values[:] = t.cpu().numpy()
+
+        def gather_vector(ptr):
+            full = torch.as_tensor(DevicePointerTensor(ptr, self.n * 2), device=self.device).reshape(self.n, 2)
+            self._s1 = allgather_ranges(self.dist, full, self.body_ranges, self.rank, self.world, self._s1)
+            torch.cuda.current_stream().synchronize()
+
+        def gather_multipoles():
+            if self.multipole is not None:
+                self._s2 = allgather_ranges(self.dist, self.multipole, self.cell_ranges, self.rank,
+                                            self.world, self._s2)
+                torch.cuda.current_stream().synchronize()
+
+        return self.op.dist_gmres(rhs_local, allreduce_sum, gather_vector, gather_multipoles, rtol=rtol,
+                                  restart=restart, max_iterations=max_iterations, precondition=precondition)
+
+
+def emulate_gmres_on_one_device(ops, rhs_morton, timeout=120.0, **kw):
+    """Distributed GMRES of `len(ops)` ranks on ONE GPU: one host thread per rank, the three
+    exchanges replaced by barrier-separated device copies between the handles.  No kernel ever waits
+    on another rank's kernel (every exchange happens on the host side of a stream synchronise), so
+    this is safe on a single device.  Returns the per-rank (x_owned, report) list."""
+    import threading
+
+    import torch
+
+    R = len(ops)
+    parts = [op.partition() for op in ops]
+    n = int(parts[0].n_bodies)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    n_cells = int(ops[0].stats()["n_cells"])
+    stride = int(parts[0].coeff_stride)
+    barrier = threading.Barrier(R, timeout=timeout)
+    scal = [None] * R
+    vec = [None] * R
+    mp = [torch.as_tensor(DevicePointerTensor(p.multipole_dev, n_cells * stride * 2),
+                          device=dev).reshape(n_cells, stride * 2) if p.multipole_dev else None for p in parts]
+    results, errors = [None] * R, []
+
+    def run(r):
+        torch.cuda.set_device(dev)
+        p = parts[r]
+
+        def allreduce_sum(values):
+            scal[r] = values.copy()
+            barrier.wait()
+            total = sum(scal[s] for s in range(R))     # same order on every rank: identical bits
+            barrier.wait()
+            values[:] = total
+
+        def gather_vector(ptr):
+            vec[r] = torch.as_tensor(DevicePointerTensor(ptr, n * 2), device=dev).reshape(n, 2)
+            barrier.wait()
+            for s, ps in enumerate(parts):
+                if s != r and ps.body_count:
+                    f, c = int(ps.body_first), int(ps.body_count)
+                    vec[r][f:f + c].copy_(vec[s][f:f + c])
+            torch.cuda.synchronize()
+            barrier.wait()
+
+        def gather_multipoles():
+            barrier.wait()
+            if mp[r] is not None:
+                for s, ps in enumerate(parts):
+                    if s == r:
+                        continue
+                    for L in range(int(ps.level_first), int(ps.level_last) + 1):
+                        f, c = int(ps.cell_first[L]), int(ps.cell_count[L])
+                        if c:
+                            mp[r][f:f + c].copy_(mp[s][f:f + c])
+            torch.cuda.synchronize()
+            barrier.wait()
+
+        try:
+            f, c = int(p.body_first), int(p.body_count)
+            results[r] = ops[r].dist_gmres(rhs_morton[f:f + c], allreduce_sum, gather_vector,
+                                           gather_multipoles, **kw)
+        except BaseException as e:
+            errors.append(e)
+            barrier.abort()
+
+    threads = [threading.Thread(target=run, args=(r,)) for r in range(R)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    return results
+
+
 def emulate_ranks_on_one_device(ops, q_morton):
     """Runs the sharded matvec of `len(ops)` ranks sequentially on ONE GPU (each op was created with
     set_partition(r, R) on the same global point set), replacing the two all-gathers by device

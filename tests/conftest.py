@@ -54,3 +54,18 @@ def _built_library():
     from paper_1803_09948_b200 import build_library
 
     build_library()
+
+
+def pytest_terminal_summary(terminalreporter):
+    # a CUDA error some other user of the process left behind (the library clears it at entry)
+    try:
+        import ctypes
+
+        from paper_1803_09948_b200.api import load_library
+        lib = load_library()
+        lib.hfmm_debug_stale_cuda_error.restype = ctypes.c_char_p
+        stale = lib.hfmm_debug_stale_cuda_error()
+        if stale:
+            terminalreporter.write_line("hfmm: stale CUDA error seen at API entry: " + stale.decode())
+    except Exception:
+        pass

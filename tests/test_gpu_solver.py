@@ -116,3 +116,40 @@ def test_midsize_system_against_oracle_gmres(oracle):
     assert abs(rep30["iterations"] - rep30_same_op["iterations"]) <= 1
     assert abs(rep30["iterations"] - rep30_cpu["iterations"]) <= 5
     assert rel_l2(x30, x_gpu) < 2e-3
+
+
+@pytest.mark.parametrize("ranks", [2, 3])
+def test_sharded_gmres_matches_single_domain(ranks):
+    """GMRES over Morton-sharded Krylov vectors (all-reduced inner products,
+    two-phase matvec) takes the single-domain iteration and returns the same solution.  Ranks are
+    host threads on one device, the exchanges barrier-separated device copies."""
+    from paper_1803_09948_b200.distributed import emulate_gmres_on_one_device
+
+    single = _bie_operator(G)
+    order = single.body_order()
+    ops = []
+    for r in range(ranks):
+        k, p = float(G["bie_k"]), int(G["bie_order"])
+        op = HfmmCuda(k=k, order=p, ncrit=16, theta=0.4, kd_max=1.0, leaf_cap=-1.0)
+        op.set_partition(r, ranks)
+        op.set_points(G["bie_xyz"])
+        op.set_corrections(int(G["bie_ni"]), far_weight=G["bie_far_weight"], patch_block=G["bie_patch_block"],
+                           near_offset=G["bie_near_offset"], near_source=G["bie_near_source"],
+                           near_delta=G["bie_near_delta"], block_lu=G["bie_block_lu"],
+                           block_piv=G["bie_block_piv"])
+        ops.append(op)
+    assert sum(int(op.partition().body_count) for op in ops) == len(order)
+    rhs_morton = np.asarray(G["bie_rhs"])[order]
+    for precondition in (True, False):
+        x1, rep1 = single.gmres(G["bie_rhs"], rtol=1e-4, restart=30, max_iterations=200,
+                                precondition=precondition)
+        res = emulate_gmres_on_one_device(ops, rhs_morton, rtol=1e-4, restart=30, max_iterations=200,
+                                          precondition=precondition)
+        x = np.concatenate([xr for xr, _ in res])
+        reps = [rep for _, rep in res]
+        assert all(rep["converged"] for rep in reps)
+        assert len({rep["iterations"] for rep in reps}) == 1          # ranks stay in lock step
+        assert abs(reps[0]["iterations"] - rep1["iterations"]) <= 1, (reps[0]["iterations"], rep1["iterations"])
+        assert reps[0]["final_residual"] <= 1.05e-4
+        assert rel_l2(x, x1[order]) < 2e-3
+        np.testing.assert_allclose(reps[0]["residuals"][:5], rep1["residuals"][:5], rtol=1e-4)
