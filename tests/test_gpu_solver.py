@@ -153,3 +153,49 @@ def test_sharded_gmres_matches_single_domain(ranks):
         assert reps[0]["final_residual"] <= 1.05e-4
         assert rel_l2(x, x1[order]) < 2e-3
         np.testing.assert_allclose(reps[0]["residuals"][:5], rep1["residuals"][:5], rtol=1e-4)
+
+
+def test_sharded_operator_over_nccl_world_of_one():
+    """The real ShardedFmm plumbing (torch.distributed NCCL collectives on tensors aliasing library
+    memory, ctypes callbacks) with the one GPU this box has: world_size 1."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1803_09948_b200.distributed import ShardedFmm
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dev = torch.device("cuda", 0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=dev)
+    try:
+        single = _bie_operator(G)
+        op = HfmmCuda(k=float(G["bie_k"]), order=int(G["bie_order"]), ncrit=16, theta=0.4, kd_max=1.0,
+                      leaf_cap=-1.0)
+        op.set_partition(0, 1)
+        op.set_points(G["bie_xyz"])
+        op.set_corrections(int(G["bie_ni"]), far_weight=G["bie_far_weight"], patch_block=G["bie_patch_block"],
+                           near_offset=G["bie_near_offset"], near_source=G["bie_near_source"],
+                           near_delta=G["bie_near_delta"], block_lu=G["bie_block_lu"],
+                           block_piv=G["bie_block_piv"])
+        sh = ShardedFmm(op, dist, 0, 1, dev)
+        order = op.body_order()
+        assert sh.count == len(order)
+        x1, rep1 = single.gmres(G["bie_rhs"], rtol=1e-4, restart=30, max_iterations=200)
+        x, rep = sh.gmres(np.asarray(G["bie_rhs"])[order], rtol=1e-4, restart=30, max_iterations=200)
+        assert rep["converged"] and abs(rep["iterations"] - rep1["iterations"]) <= 1
+        assert rel_l2(x, x1[order]) < 2e-3
+        # the two-phase FMM matvec (dist_upward / dist_downward carry no BIE tail) against the single-handle FMM
+        plain = HfmmCuda(k=float(G["bie_k"]), order=int(G["bie_order"]), ncrit=16, theta=0.4, kd_max=1.0,
+                         leaf_cap=-1.0)
+        plain.set_points(G["bie_xyz"])
+        q = charges(len(order), 3)
+        qm = q[order]
+        q_local = torch.from_numpy(np.stack([qm.real, qm.imag], 1).astype(np.float32)).to(dev)
+        y = sh.matvec(q_local).cpu().numpy()
+        assert rel_l2(y[:, 0] + 1j * y[:, 1], plain.matvec(q)[order]) < 2e-6
+    finally:
+        dist.destroy_process_group()
