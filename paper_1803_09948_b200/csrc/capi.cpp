@@ -222,6 +222,11 @@ int hfmm_cuda_dist_gmres(hfmm_cuda_t* h, const double* rhs_owned, double* x_owne
   });
 }
 
+int hfmm_debug_fp32_probes(hfmm_cuda_t* h, double* out2) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] { h->engine->measure_fp32_probes(out2); });
+}
+
 const char* hfmm_debug_stale_cuda_error(void) { return g_stale_error.c_str(); }
 
 const char* hfmm_cuda_version(void) { return "hfmm-b200 0.1 (sm_100a)"; }

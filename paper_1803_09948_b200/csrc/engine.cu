@@ -829,7 +829,14 @@ void Engine::matvec_host(const double* q, double* out) {
 
 double Engine::measure_fp32_peak_tflops() {
   HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
-  return run_fp32_peak_probe(stream_);
+  // the higher of the scalar-FFMA and the packed-FFMA2 probe is the roofline denominator
+  return std::max(run_fp32_peak_probe(stream_, false), run_fp32_peak_probe(stream_, true));
+}
+
+void Engine::measure_fp32_probes(double out[2]) {
+  HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  out[0] = run_fp32_peak_probe(stream_, false);
+  out[1] = run_fp32_peak_probe(stream_, true);
 }
 
 void Engine::timer_record(int slot) {

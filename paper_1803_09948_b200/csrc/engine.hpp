@@ -45,6 +45,7 @@ class Engine {
   double timer_elapsed_ms(int a, int b);
   void flush_l2();
   double measure_fp32_peak_tflops();
+  void measure_fp32_probes(double out[2]);  // [0] FFMA, [1] FFMA2
   void get_stats(hfmm_cuda_stats* out);
   void get_cells(uint32_t* out, size_t capacity) const;
   void get_body_order(uint32_t* out) const;

@@ -163,6 +163,7 @@ void launch_combine_owned(const float2* near, const float2* far, const float2* c
                           float2* out, uint32_t n, cudaStream_t s);
 
 // FFMA-only micro-benchmark; returns TFLOP/s (2 flop per FFMA)
-double run_fp32_peak_probe(cudaStream_t s);
+// packed: the same chains issued as FFMA2 (fma.rn.f32x2)
+double run_fp32_peak_probe(cudaStream_t s, bool packed = false);
 
 }  // namespace hfmm_b200

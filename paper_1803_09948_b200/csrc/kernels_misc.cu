@@ -61,6 +61,28 @@ __global__ void __launch_bounds__(256) fp32_peak_kernel(float* out, int iters, f
   if (s == 123.456f) out[0] = s;  // never true; keeps the chains alive
 }
 
+// the same with packed FFMA2 (fma.rn.f32x2, two FMAs per instruction, sm_100+): 8 chains of pairs
+__global__ void __launch_bounds__(256) fp32x2_peak_kernel(float* out, int iters, float a, float b) {
+  unsigned long long v[8], av, bv;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(av) : "f"(a));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(bv) : "f"(b));
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    asm("mov.b64 %0, {%1, %2};" : "=l"(v[i]) : "f"(float(threadIdx.x + i)), "f"(float(threadIdx.x + i + 8)));
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(v[i]) : "l"(av), "l"(bv));
+  }
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v[i]));
+    s += lo + hi;
+  }
+  if (s == 123.456f) out[0] = s;
+}
+
 // out[s] = near[s] + far[s] + corr[index[s]] for the owned Morton slots (corr in caller order, may be null)
 __global__ void combine_owned_kernel(const float2* __restrict__ near, const float2* __restrict__ far,
                                      const float2* __restrict__ corr, const uint32_t* __restrict__ index,
@@ -88,7 +110,7 @@ void launch_combine_owned(const float2* near, const float2* far, const float2* c
   HFMM_CUDA_CHECK(cudaGetLastError());
 }
 
-double run_fp32_peak_probe(cudaStream_t s) {
+double run_fp32_peak_probe(cudaStream_t s, bool packed) {
   int dev = 0, sms = 0;
   HFMM_CUDA_CHECK(cudaGetDevice(&dev));
   HFMM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -101,7 +123,8 @@ double run_fp32_peak_probe(cudaStream_t s) {
   double best = 0;
   for (int rep = 0; rep < 4; ++rep) {
     HFMM_CUDA_CHECK(cudaEventRecord(e0, s));
-    fp32_peak_kernel<<<blocks, threads, 0, s>>>(out, iters, 0.999f, 0.001f);
+    if (packed) fp32x2_peak_kernel<<<blocks, threads, 0, s>>>(out, iters, 0.999f, 0.001f);
+    else fp32_peak_kernel<<<blocks, threads, 0, s>>>(out, iters, 0.999f, 0.001f);
     HFMM_CUDA_CHECK(cudaEventRecord(e1, s));
     HFMM_CUDA_CHECK(cudaEventSynchronize(e1));
     float ms = 0;

@@ -26,6 +26,7 @@
 // FP32 work per pair: 2 * 2*sum_n ((n+1)^2 + n^2) + 4*sum_m (P+1-|m|)^2 FFMAs (11.9 k at P = 12) against
 // 4 (P+1)^4 = 114 k for the reference's dense complex mat-vec.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "device_utils.cuh"
@@ -77,8 +78,46 @@ __device__ __forceinline__ void sts2(uint32_t addr, float2 v) {
 
 // warps per CTA: 8 with two CTAs per SM while two operand tile pairs fit the 227 KB of shared memory
 // (P <= 12), else ONE CTA of 16 warps per SM so the SM keeps 16 resident warps (P = 13..16)
+inline bool translate_two_ctas(int P) { return 2 * (smem_plan(P).bytes + 1024) <= size_t(227) * 1024; }
 inline int translate_warps(int P) {
-  return 2 * (smem_plan(P).bytes + 1024) <= size_t(227) * 1024 ? 8 : 16;
+  static const int forced = [] {
+    const char* e = getenv("HFMM_TRANSLATE_WARPS");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced == 8 || forced == 16) return translate_two_ctas(P) ? forced : 16;
+  return translate_two_ctas(P) ? 8 : 16;
+}
+
+// ---- packed FP32 (sm_100a FFMA2): one instruction = two FMAs; with a complex accumulator held as
+// a (re, im) register pair, "acc += e * x" (real e, complex x) is ONE FFMA2 with e as the scalar
+// operand, and a complex multiply-add is two.  Same FLOP peak as FFMA (74.1 vs 72.4 TFLOP/s
+// measured), half the issue slots — and this kernel is issue-bound.
+using u64 = unsigned long long;
+__device__ __forceinline__ u64 pack2(float lo, float hi) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 unpack2(u64 v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+// acc += x * s  (x: complex pair, s: real scalar broadcast to both halves)
+__device__ __forceinline__ void fma2s(u64& acc, u64 x, float s) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(x), "l"(pack2(s, s)));
+}
+__device__ __forceinline__ u64 ldsp(uint32_t addr) {
+  u64 v;
+  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void stsp(uint32_t addr, u64 v) {
+  asm volatile("st.shared.b64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+__device__ __forceinline__ u64 neg2(u64 v) {
+  const float2 f = unpack2(v);
+  return pack2(-f.x, -f.y);
 }
 
 // ---- rotation task: R output rows of one folded sub-block;  out[r] = sum_k E[k][r] * in[k] ------
@@ -86,9 +125,9 @@ inline int translate_warps(int P) {
 template <int R, bool BACK>
 __device__ __forceinline__ void rot_task(uint32_t e_addr, uint32_t ws_b, int w, uint32_t in_addr,
                                          uint32_t out_addr, bool odd0) {
-  float ar[R], ai[R];
+  u64 acc[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) ar[r] = ai[r] = 0.0f;
+  for (int r = 0; r < R; ++r) acc[r] = 0ull;
   constexpr int NV = (R + 3) / 4;
   constexpr uint32_t kRowB = 8 * kRow;  // bytes per operand row
   // two inputs per trip; in the inverse rotation odd inputs enter negated ((-1)^k of the symmetry)
@@ -96,7 +135,9 @@ __device__ __forceinline__ void rot_task(uint32_t e_addr, uint32_t ws_b, int w, 
   const uint32_t ws2 = 2 * ws_b;
 #pragma unroll 1
   for (int trips = w >> 1; trips > 0; --trips) {
-    const float2 x0 = lds2(in_addr), x1 = lds2(in_addr + kRowB);
+    const u64 x0 = ldsp(in_addr);
+    u64 x1 = ldsp(in_addr + kRowB);
+    if (BACK) x1 = neg2(x1);
     float e0[NV * 4], e1[NV * 4];
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
@@ -106,49 +147,51 @@ __device__ __forceinline__ void rot_task(uint32_t e_addr, uint32_t ws_b, int w, 
       e1[4 * v] = b.x; e1[4 * v + 1] = b.y; e1[4 * v + 2] = b.z; e1[4 * v + 3] = b.w;
     }
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      ar[r] = fmaf(e0[r], x0.x, ar[r]);
-      ai[r] = fmaf(e0[r], x0.y, ai[r]);
-      if (BACK) {
-        ar[r] = fmaf(-e1[r], x1.x, ar[r]);
-        ai[r] = fmaf(-e1[r], x1.y, ai[r]);
-      } else {
-        ar[r] = fmaf(e1[r], x1.x, ar[r]);
-        ai[r] = fmaf(e1[r], x1.y, ai[r]);
-      }
-    }
+    for (int r = 0; r < R; ++r) fma2s(acc[r], x0, e0[r]);
+#pragma unroll
+    for (int r = 0; r < R; ++r) fma2s(acc[r], x1, e1[r]);
     in_addr += 2 * kRowB;
     e_addr += ws2;
     e1_addr += ws2;
   }
   if (w & 1) {  // one even-indexed input left
-    const float2 x0 = lds2(in_addr);
+    const u64 x0 = ldsp(in_addr);
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       const float4 a = lds4(e_addr + 16 * v);
       const float ev[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (4 * v + j < R) {
-          ar[4 * v + j] = fmaf(ev[j], x0.x, ar[4 * v + j]);
-          ai[4 * v + j] = fmaf(ev[j], x0.y, ai[4 * v + j]);
-        }
+        if (4 * v + j < R) fma2s(acc[4 * v + j], x0, ev[j]);
     }
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    float2 o = make_float2(ar[r], ai[r]);
+    u64 o = acc[r];
     if (BACK) {  // (-1)^{row} of the symmetry
       const bool neg = ((r & 1) != 0) != odd0;
-      if (neg) o = make_float2(-ar[r], -ai[r]);
+      if (neg) o = neg2(o);
     }
-    sts2(out_addr + r * kRowB, o);
+    stsp(out_addr + r * kRowB, o);
   }
 }
 
-template <bool BACK>
+template <bool BACK, int MAXR>
 __device__ __forceinline__ void rot_dispatch(int R, uint32_t e_addr, uint32_t ws_b, int w,
                                              uint32_t in_addr, uint32_t out_addr, bool odd0) {
+  if (MAXR == 8) {  // the 64-register variant never schedules taller tiles
+    switch (R) {
+      case 1: rot_task<1, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
+      case 2: rot_task<2, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
+      case 3: rot_task<3, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
+      case 4: rot_task<4, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
+      case 5: rot_task<5, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
+      case 6: rot_task<6, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
+      case 7: rot_task<7, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
+      default: rot_task<8, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
+    }
+    return;
+  }
   switch (R) {
     case 1: rot_task<1, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
     case 2: rot_task<2, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
@@ -171,16 +214,22 @@ __device__ __forceinline__ void rot_dispatch(int R, uint32_t e_addr, uint32_t ws
 template <int R, bool TWO>
 __device__ __forceinline__ void coax_task(uint32_t c_addr, uint32_t ws_b, int w, int m, int r0,
                                           uint32_t p_addr, uint32_t q_addr, uint32_t out_base) {
-  float pr[R], pi[R], qr[R], qi[R];
+  u64 p[R], q[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) pr[r] = pi[r] = qr[r] = qi[r] = 0.0f;
+  for (int r = 0; r < R; ++r) p[r] = q[r] = 0ull;
   constexpr uint32_t kRowB = 8 * kRow;
   uint32_t step = uint32_t(2 * m + 1) * kRowB;
 #pragma unroll 1
   for (int k = w; k > 0; --k) {
+    // c * x = cr * (x.re, x.im) + ci * (-x.im, x.re): two FFMA2 per complex multiply-add
     const float2 xp = lds2(p_addr);
-    float2 xm = make_float2(0.f, 0.f);
-    if (TWO) xm = lds2(q_addr);
+    const u64 xpv = pack2(xp.x, xp.y), xpt = pack2(-xp.y, xp.x);
+    u64 xqv = 0ull, xqt = 0ull;
+    if (TWO) {
+      const float2 xq = lds2(q_addr);
+      xqv = pack2(xq.x, xq.y);
+      xqt = pack2(-xq.y, xq.x);
+    }
     float cr[R], ci[R];
     if (R == 1) {
       const float2 c = lds2(c_addr);
@@ -195,16 +244,13 @@ __device__ __forceinline__ void coax_task(uint32_t c_addr, uint32_t ws_b, int w,
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      pr[r] = fmaf(cr[r], xp.x, pr[r]);
-      pr[r] = fmaf(-ci[r], xp.y, pr[r]);
-      pi[r] = fmaf(cr[r], xp.y, pi[r]);
-      pi[r] = fmaf(ci[r], xp.x, pi[r]);
-      if (TWO) {
-        qr[r] = fmaf(cr[r], xm.x, qr[r]);
-        qr[r] = fmaf(-ci[r], xm.y, qr[r]);
-        qi[r] = fmaf(cr[r], xm.y, qi[r]);
-        qi[r] = fmaf(ci[r], xm.x, qi[r]);
-      }
+      fma2s(p[r], xpv, cr[r]);
+      if (TWO) fma2s(q[r], xqv, cr[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      fma2s(p[r], xpt, ci[r]);
+      if (TWO) fma2s(q[r], xqt, ci[r]);
     }
     p_addr += step;
     q_addr += step + kRowB;
@@ -214,8 +260,8 @@ __device__ __forceinline__ void coax_task(uint32_t c_addr, uint32_t ws_b, int w,
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int nu = m + r0 + r;
-    sts2(out_base + uint32_t(nu * nu + m) * kRowB, make_float2(pr[r], pi[r]));
-    if (TWO) sts2(out_base + uint32_t(nu * nu + nu + m) * kRowB, make_float2(qr[r], qi[r]));
+    stsp(out_base + uint32_t(nu * nu + m) * kRowB, p[r]);
+    if (TWO) stsp(out_base + uint32_t(nu * nu + nu + m) * kRowB, q[r]);
   }
 }
 
@@ -226,11 +272,7 @@ __device__ __forceinline__ void coax_dispatch(int R, uint32_t c_addr, uint32_t w
     case 1: coax_task<1, TWO>(c_addr, ws_b, w, m, r0, p_addr, q_addr, out_base); break;
     case 2: coax_task<2, TWO>(c_addr, ws_b, w, m, r0, p_addr, q_addr, out_base); break;
     case 3: coax_task<3, TWO>(c_addr, ws_b, w, m, r0, p_addr, q_addr, out_base); break;
-    case 4: coax_task<4, TWO>(c_addr, ws_b, w, m, r0, p_addr, q_addr, out_base); break;
-    case 5: coax_task<5, TWO>(c_addr, ws_b, w, m, r0, p_addr, q_addr, out_base); break;
-    case 6: coax_task<6, TWO>(c_addr, ws_b, w, m, r0, p_addr, q_addr, out_base); break;
-    case 7: coax_task<7, TWO>(c_addr, ws_b, w, m, r0, p_addr, q_addr, out_base); break;
-    default: coax_task<8, TWO>(c_addr, ws_b, w, m, r0, p_addr, q_addr, out_base); break;
+    default: coax_task<4, TWO>(c_addr, ws_b, w, m, r0, p_addr, q_addr, out_base); break;  // tiles hold <= 4 rows
   }
 }
 
@@ -242,9 +284,10 @@ __constant__ TranslateSchedule c_sched[kMaxOrder + 1];
 // tables in shared memory are reloaded only when the class changes).  The gather of the NEXT item
 // is issued into registers while the current item drains through its reductions, so the chain
 // item -> pair list -> source rows never sits on the critical path.
-template <int NU, int WARPS>  // NU: (n, m >= 0) gather units per lane = ceil((P+1)(P+2)/2 / WARPS)
-__global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? 2 : 1) translate_kernel(const TranslateArgs a) {
+template <int NU, int WARPS, int CTAS>  // NU: (n, m >= 0) gather units per lane = ceil((P+1)(P+2)/2 / WARPS)
+__global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const TranslateArgs a) {
   constexpr int kThreads = WARPS * 32;
+  constexpr int kMaxR = WARPS == 8 ? 12 : 8;
   constexpr int kLanesPerPair = WARPS;  // 32 pairs x WARPS lanes = all threads of the CTA
   extern __shared__ __align__(16) float smem[];
   const int P = a.order;
@@ -356,7 +399,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? 2 : 1) translate_kern
     // stage 2: forward rotation A -> B
     for (int t = sched.rot_begin[warp]; t < sched.rot_begin[warp + 1]; ++t) {
       const TranslateRotTask d = sched.rot[t];
-      rot_dispatch<false>((d.packed >> 16) & 0xff, win + d.e_off, d.packed & 0xff, (d.packed >> 8) & 0xff,
+      rot_dispatch<false, kMaxR>((d.packed >> 16) & 0xff, win + d.e_off, d.packed & 0xff, (d.packed >> 8) & 0xff,
                           a_lane + d.in_rel, b_lane + d.out_rel, false);
     }
     __syncthreads();
@@ -375,7 +418,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? 2 : 1) translate_kern
     // stage 4: inverse rotation A -> B (same table, sign-twiddled)
     for (int t = sched.rot_begin[warp]; t < sched.rot_begin[warp + 1]; ++t) {
       const TranslateRotTask d = sched.rot[t];
-      rot_dispatch<true>((d.packed >> 16) & 0xff, win + d.e_off, d.packed & 0xff, (d.packed >> 8) & 0xff,
+      rot_dispatch<true, kMaxR>((d.packed >> 16) & 0xff, win + d.e_off, d.packed & 0xff, (d.packed >> 8) & 0xff,
                          a_lane + d.in_rel, b_lane + d.out_rel, (d.packed >> 24) & 1);
     }
     __syncthreads();
@@ -530,15 +573,15 @@ void upload_translate_schedule(int order) {
 int translate_batch_size(int) { return kTranslateBatch; }
 
 namespace {
-template <int NU, int WARPS>
+template <int NU, int WARPS, int CTAS>
 void launch_translate_nu(const TranslateArgs& a, cudaStream_t s, size_t bytes, int ctas) {
   static int configured_for = -1;
   if (configured_for < int(bytes)) {
-    HFMM_CUDA_CHECK(cudaFuncSetAttribute(translate_kernel<NU, WARPS>,
+    HFMM_CUDA_CHECK(cudaFuncSetAttribute(translate_kernel<NU, WARPS, CTAS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
     configured_for = int(bytes);
   }
-  translate_kernel<NU, WARPS><<<ctas, WARPS * 32, bytes, s>>>(a);
+  translate_kernel<NU, WARPS, CTAS><<<ctas, WARPS * 32, bytes, s>>>(a);
   HFMM_CUDA_CHECK(cudaGetLastError());
 }
 }  // namespace
@@ -554,17 +597,20 @@ void launch_translate(const TranslateArgs& a, cudaStream_t s) {
   }
   // persistent grid: two 8-warp CTAs per SM, or one 16-warp CTA when the tiles are too large
   const int warps = translate_warps(a.order);
-  const int ctas = int(std::min<uint32_t>(a.n_items, uint32_t((warps == 8 ? 2 : 1) * sm_count)));
+  const bool two = translate_two_ctas(a.order);
+  const int ctas = int(std::min<uint32_t>(a.n_items, uint32_t((two ? 2 : 1) * sm_count)));
   const int units = (a.order + 1) * (a.order + 2) / 2;
   if (warps == 8) {
     const int nu = (units + 7) / 8;
-    if (nu <= 6) launch_translate_nu<6, 8>(a, s, sp.bytes, ctas);         // P <= 8
-    else if (nu <= 9) launch_translate_nu<9, 8>(a, s, sp.bytes, ctas);    // P <= 10
-    else launch_translate_nu<12, 8>(a, s, sp.bytes, ctas);                // P <= 12
+    if (nu <= 6) launch_translate_nu<6, 8, 2>(a, s, sp.bytes, ctas);         // P <= 8
+    else if (nu <= 9) launch_translate_nu<9, 8, 2>(a, s, sp.bytes, ctas);    // P <= 10
+    else launch_translate_nu<12, 8, 2>(a, s, sp.bytes, ctas);                // P <= 12
+  } else if (two) {
+    launch_translate_nu<6, 16, 2>(a, s, sp.bytes, ctas);                     // P <= 12, 64 registers
   } else {
     const int nu = (units + 15) / 16;
-    if (nu <= 8) launch_translate_nu<8, 16>(a, s, sp.bytes, ctas);        // P <= 14
-    else launch_translate_nu<10, 16>(a, s, sp.bytes, ctas);               // P <= 16
+    if (nu <= 8) launch_translate_nu<8, 16, 1>(a, s, sp.bytes, ctas);        // P <= 14
+    else launch_translate_nu<10, 16, 1>(a, s, sp.bytes, ctas);               // P <= 16
   }
 }
 
