@@ -87,21 +87,28 @@ struct TranslateItem {
 };
 inline constexpr int kTranslateBatch = 32;   // pairs per work item (= lanes of a warp)
 inline constexpr int kTranslateWarps = 16;   // most warps per CTA of the translation kernel (8 or 16)
-inline constexpr int kTranslateMaxTasks = 80;
+inline constexpr int kTranslateMaxTasks = 40;
 
 // Per-order static schedule of the translation kernel (kept in __constant__ memory): each stage is a
-// list of tasks grouped per warp; a task carries every shared-memory offset it needs.
+// list of tasks grouped per warp.  A task is a PAIR of sub-tasks, one per half-warp (a lane owns two
+// of the 32 pairs of a batch); a sub-task carries every shared-memory offset it needs (bytes).
+struct TranslateRotSub {
+  uint32_t e_off;    // first coefficient of the sub-task's row tile (byte offset in the window)
+  uint32_t in_rel;   // first input row of the folded sub-block, relative to the tile (bytes)
+  uint32_t out_rel;  // first output row (bytes)
+  uint32_t packed;   // row stride (bytes) | inputs << 8 | rows stored << 16 | (first row odd) << 24 | template rows << 28
+};
 struct TranslateRotTask {
-  uint32_t e_off;    // first coefficient of the task's row tile (float offset in the window)
-  uint32_t in_rel;   // first input row of the folded sub-block, relative to the tile
-  uint32_t out_rel;  // first output row
-  uint32_t packed;   // row stride | inputs << 8 | rows << 16 | (first row odd) << 24
+  TranslateRotSub sub[2];
+};
+struct TranslateCoaxSub {
+  uint32_t c_off;    // first coefficient (byte offset in the window)
+  uint32_t p_rel;    // input row (n = m) of the s / x_0 column, relative to the tile (bytes)
+  uint32_t q_rel;    // input row (n = m) of the t column (bytes)
+  uint32_t packed;   // row stride (bytes) | inputs << 8 | m << 16 | first row << 22 | rows stored << 28
 };
 struct TranslateCoaxTask {
-  uint32_t c_off;    // first coefficient (float offset in the window)
-  uint32_t p_rel;    // input row (n = m) of the s / x_0 column, relative to the tile
-  uint32_t q_rel;    // input row (n = m) of the t column
-  uint32_t packed;   // row stride | inputs << 8 | m << 16 | first row << 22 | rows << 28
+  TranslateCoaxSub sub[2];
 };
 struct TranslateSchedule {
   int rot_begin[kTranslateWarps + 1];

@@ -38,10 +38,11 @@ namespace hfmm_b200 {
 namespace {
 
 
+constexpr int kZeroC = 4;  // complex zeros a finished half-warp keeps multiplying with (coaxial stage)
 constexpr int kRow = 34;  // float2 elements per operand row: 32 pairs + 2 pad (bank spread)
 
 struct SmemPlan {
-  int rot_floats, coax_c, phase_c, tile_c, dim;
+  int rot_floats, coax_c, phase_c, unfold_c, tile_c, dim;
   size_t bytes;
 };
 __host__ __device__ inline SmemPlan smem_plan(int P) {
@@ -50,9 +51,10 @@ __host__ __device__ inline SmemPlan smem_plan(int P) {
   s.rot_floats = rot_table_size(P);
   s.coax_c = coax_table_size(P);
   s.phase_c = (P + 2) & ~1;
+  s.unfold_c = 2 * (P + 1);  // one float4 per order m
   s.tile_c = s.dim * kRow;
-  // rot | coax | phases | tile A | tile B | (n, m) of every gather unit (u16)
-  s.bytes = size_t(s.rot_floats) * 4 + size_t(s.coax_c + s.phase_c + 2 * s.tile_c) * 8 +
+  // rot | coax | phases | unfold factors | zero row | tile A | tile B | (n, m) of every gather unit (u16)
+  s.bytes = size_t(s.rot_floats) * 4 + size_t(s.coax_c + s.phase_c + s.unfold_c + kZeroC + 2 * s.tile_c) * 8 +
             size_t(((P + 1) * (P + 2) / 2 * 6 + 15) & ~15);
   return s;
 }
@@ -79,14 +81,7 @@ __device__ __forceinline__ void sts2(uint32_t addr, float2 v) {
 // warps per CTA: 8 with two CTAs per SM while two operand tile pairs fit the 227 KB of shared memory
 // (P <= 12), else ONE CTA of 16 warps per SM so the SM keeps 16 resident warps (P = 13..16)
 inline bool translate_two_ctas(int P) { return 2 * (smem_plan(P).bytes + 1024) <= size_t(227) * 1024; }
-inline int translate_warps(int P) {
-  static const int forced = [] {
-    const char* e = getenv("HFMM_TRANSLATE_WARPS");
-    return e ? atoi(e) : 0;
-  }();
-  if (forced == 8 || forced == 16) return translate_two_ctas(P) ? forced : 16;
-  return translate_two_ctas(P) ? 8 : 16;
-}
+inline int translate_warps(int P) { return translate_two_ctas(P) ? 8 : 16; }
 
 // ---- packed FP32 (sm_100a FFMA2): one instruction = two FMAs; with a complex accumulator held as
 // a (re, im) register pair, "acc += e * x" (real e, complex x) is ONE FFMA2 with e as the scalar
@@ -107,6 +102,12 @@ __device__ __forceinline__ float2 unpack2(u64 v) {
 __device__ __forceinline__ void fma2s(u64& acc, u64 x, float s) {
   asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(x), "l"(pack2(s, s)));
 }
+// x * s
+__device__ __forceinline__ u64 mul2s(u64 x, float s) {
+  u64 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(pack2(s, s)));
+  return r;
+}
 __device__ __forceinline__ u64 ldsp(uint32_t addr) {
   u64 v;
   asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr));
@@ -115,19 +116,35 @@ __device__ __forceinline__ u64 ldsp(uint32_t addr) {
 __device__ __forceinline__ void stsp(uint32_t addr, u64 v) {
   asm volatile("st.shared.b64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
 }
+__device__ __forceinline__ void ldsp2(uint32_t addr, u64& a, u64& b) {
+  asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"(addr));
+}
+__device__ __forceinline__ void stsp2(uint32_t addr, u64 a, u64 b) {
+  asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(addr), "l"(a), "l"(b) : "memory");
+}
+// (re, im) -> i * (re, im) = (-im, re)
+__device__ __forceinline__ u64 rot90(u64 v) {
+  const float2 f = unpack2(v);
+  return pack2(-f.y, f.x);
+}
 __device__ __forceinline__ u64 neg2(u64 v) {
   const float2 f = unpack2(v);
   return pack2(-f.x, -f.y);
 }
 
-// ---- rotation task: R output rows of one folded sub-block;  out[r] = sum_k E[k][r] * in[k] ------
-// e_off / in_off / out_off: float offsets into the shared-memory window `sm`
+// ---- rotation task -----------------------------------------------------------------------------
+// A warp runs TWO sub-tasks at once, one per half-warp: R output rows of one folded sub-block each
+// (same number of inputs w), out[r] = sum_k E[k][r] * in[k].  A lane owns TWO pairs of the batch
+// (16 lanes x 2 = 32 pairs), so one 16-byte LDS brings both operands and every broadcast
+// coefficient feeds two FFMA2: the kernel is bound by shared-memory wavefronts (a broadcast
+// LDS.128 costs two), and this halves the coefficient traffic per multiply-add.
+// All addresses are per lane (they differ between the halves); rows >= nrows are not stored.
 template <int R, bool BACK>
 __device__ __forceinline__ void rot_task(uint32_t e_addr, uint32_t ws_b, int w, uint32_t in_addr,
-                                         uint32_t out_addr, bool odd0) {
-  u64 acc[R];
+                                         uint32_t out_addr, bool odd0, int nrows) {
+  u64 acc0[R], acc1[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) acc[r] = 0ull;
+  for (int r = 0; r < R; ++r) acc0[r] = acc1[r] = 0ull;
   constexpr int NV = (R + 3) / 4;
   constexpr uint32_t kRowB = 8 * kRow;  // bytes per operand row
   // two inputs per trip; in the inverse rotation odd inputs enter negated ((-1)^k of the symmetry)
@@ -135,9 +152,13 @@ __device__ __forceinline__ void rot_task(uint32_t e_addr, uint32_t ws_b, int w, 
   const uint32_t ws2 = 2 * ws_b;
 #pragma unroll 1
   for (int trips = w >> 1; trips > 0; --trips) {
-    const u64 x0 = ldsp(in_addr);
-    u64 x1 = ldsp(in_addr + kRowB);
-    if (BACK) x1 = neg2(x1);
+    u64 xa0, xa1, xb0, xb1;
+    ldsp2(in_addr, xa0, xa1);
+    ldsp2(in_addr + kRowB, xb0, xb1);
+    if (BACK) {
+      xb0 = neg2(xb0);
+      xb1 = neg2(xb1);
+    }
     float e0[NV * 4], e1[NV * 4];
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
@@ -147,132 +168,131 @@ __device__ __forceinline__ void rot_task(uint32_t e_addr, uint32_t ws_b, int w, 
       e1[4 * v] = b.x; e1[4 * v + 1] = b.y; e1[4 * v + 2] = b.z; e1[4 * v + 3] = b.w;
     }
 #pragma unroll
-    for (int r = 0; r < R; ++r) fma2s(acc[r], x0, e0[r]);
+    for (int r = 0; r < R; ++r) {
+      fma2s(acc0[r], xa0, e0[r]);
+      fma2s(acc1[r], xa1, e0[r]);
+    }
 #pragma unroll
-    for (int r = 0; r < R; ++r) fma2s(acc[r], x1, e1[r]);
+    for (int r = 0; r < R; ++r) {
+      fma2s(acc0[r], xb0, e1[r]);
+      fma2s(acc1[r], xb1, e1[r]);
+    }
     in_addr += 2 * kRowB;
     e_addr += ws2;
     e1_addr += ws2;
   }
   if (w & 1) {  // one even-indexed input left
-    const u64 x0 = ldsp(in_addr);
+    u64 xa0, xa1;
+    ldsp2(in_addr, xa0, xa1);
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       const float4 a = lds4(e_addr + 16 * v);
       const float ev[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (4 * v + j < R) fma2s(acc[4 * v + j], x0, ev[j]);
+        if (4 * v + j < R) {
+          fma2s(acc0[4 * v + j], xa0, ev[j]);
+          fma2s(acc1[4 * v + j], xa1, ev[j]);
+        }
     }
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    u64 o = acc[r];
+    u64 o0 = acc0[r], o1 = acc1[r];
     if (BACK) {  // (-1)^{row} of the symmetry
       const bool neg = ((r & 1) != 0) != odd0;
-      if (neg) o = neg2(o);
+      if (neg) {
+        o0 = neg2(o0);
+        o1 = neg2(o1);
+      }
     }
-    stsp(out_addr + r * kRowB, o);
+    if (r < nrows) stsp2(out_addr + r * kRowB, o0, o1);
   }
 }
 
-template <bool BACK, int MAXR>
+template <bool BACK>
 __device__ __forceinline__ void rot_dispatch(int R, uint32_t e_addr, uint32_t ws_b, int w,
-                                             uint32_t in_addr, uint32_t out_addr, bool odd0) {
-  if (MAXR == 8) {  // the 64-register variant never schedules taller tiles
-    switch (R) {
-      case 1: rot_task<1, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
-      case 2: rot_task<2, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
-      case 3: rot_task<3, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
-      case 4: rot_task<4, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
-      case 5: rot_task<5, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
-      case 6: rot_task<6, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
-      case 7: rot_task<7, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
-      default: rot_task<8, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
-    }
-    return;
-  }
+                                             uint32_t in_addr, uint32_t out_addr, bool odd0, int nrows) {
   switch (R) {
-    case 1: rot_task<1, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
-    case 2: rot_task<2, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
-    case 3: rot_task<3, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
-    case 4: rot_task<4, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
-    case 5: rot_task<5, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
-    case 6: rot_task<6, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
-    case 7: rot_task<7, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
-    case 8: rot_task<8, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
-    case 9: rot_task<9, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
-    case 10: rot_task<10, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
-    case 11: rot_task<11, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
-    default: rot_task<12, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0); break;
+    case 1: rot_task<1, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0, nrows); break;
+    case 2: rot_task<2, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0, nrows); break;
+    case 3: rot_task<3, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0, nrows); break;
+    case 4: rot_task<4, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0, nrows); break;
+    case 5: rot_task<5, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0, nrows); break;
+    case 6: rot_task<6, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0, nrows); break;
+    case 7: rot_task<7, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0, nrows); break;
+    default: rot_task<8, BACK>(e_addr, ws_b, w, in_addr, out_addr, odd0, nrows); break;
   }
 }
 
 // ---- coaxial task: rows nu = m + r0 .. m + r0 + R - 1 of order m, folded columns s_m and t_m ---
 // (for m = 0 only the single column x_0).  p_off / q_off: float offsets of the first input rows
 // (degree n = m) of the two columns; they advance by 2n+1 and 2n+2 rows per degree.
-template <int R, bool TWO>
-__device__ __forceinline__ void coax_task(uint32_t c_addr, uint32_t ws_b, int w, int m, int r0,
-                                          uint32_t p_addr, uint32_t q_addr, uint32_t out_base) {
-  u64 p[R], q[R];
+template <bool TWO>
+__device__ __forceinline__ void coax_task(uint32_t c_addr, uint32_t ws_b, int w, int wmax, int m, int r0,
+                                          int nrows, uint32_t p_addr, uint32_t q_addr, uint32_t out_base,
+                                          uint32_t zero_addr, uint32_t safe_addr) {
+  constexpr int R = 4;
+  u64 p0[R], p1[R], q0[R], q1[R];  // columns s_m (p) and t_m (q) of the lane's two pairs
 #pragma unroll
-  for (int r = 0; r < R; ++r) p[r] = q[r] = 0ull;
+  for (int r = 0; r < R; ++r) p0[r] = p1[r] = q0[r] = q1[r] = 0ull;
   constexpr uint32_t kRowB = 8 * kRow;
-  uint32_t step = uint32_t(2 * m + 1) * kRowB;
+  uint32_t step = uint32_t(2 * m + 1) * kRowB, dstep = 2 * kRowB, qx = kRowB;
 #pragma unroll 1
-  for (int k = w; k > 0; --k) {
+  for (int k = 0; k < wmax; ++k) {
+    if (k == w) {  // this half-warp's sub-task is shorter than its partner's: multiply zeros from here on
+      c_addr = zero_addr;
+      ws_b = 0;
+      p_addr = q_addr = safe_addr;
+      step = dstep = qx = 0;
+    }
     // c * x = cr * (x.re, x.im) + ci * (-x.im, x.re): two FFMA2 per complex multiply-add
-    const float2 xp = lds2(p_addr);
-    const u64 xpv = pack2(xp.x, xp.y), xpt = pack2(-xp.y, xp.x);
-    u64 xqv = 0ull, xqt = 0ull;
+    u64 xp0, xp1, xq0 = 0ull, xq1 = 0ull;
+    ldsp2(p_addr, xp0, xp1);
+    if (TWO) ldsp2(q_addr, xq0, xq1);
+    const u64 tp0 = rot90(xp0), tp1 = rot90(xp1);
+    u64 tq0 = 0ull, tq1 = 0ull;
     if (TWO) {
-      const float2 xq = lds2(q_addr);
-      xqv = pack2(xq.x, xq.y);
-      xqt = pack2(-xq.y, xq.x);
+      tq0 = rot90(xq0);
+      tq1 = rot90(xq1);
     }
     float cr[R], ci[R];
-    if (R == 1) {
-      const float2 c = lds2(c_addr);
-      cr[0] = c.x; ci[0] = c.y;
-    } else {
 #pragma unroll
-      for (int v = 0; v < (R + 1) / 2; ++v) {
-        const float4 c = lds4(c_addr + 16 * v);
-        cr[2 * v] = c.x; ci[2 * v] = c.y;
-        if (2 * v + 1 < R) { cr[2 * v + 1] = c.z; ci[2 * v + 1] = c.w; }
+    for (int v = 0; v < R / 2; ++v) {
+      const float4 c = lds4(c_addr + 16 * v);
+      cr[2 * v] = c.x; ci[2 * v] = c.y;
+      cr[2 * v + 1] = c.z; ci[2 * v + 1] = c.w;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      fma2s(p0[r], xp0, cr[r]);
+      fma2s(p1[r], xp1, cr[r]);
+      if (TWO) {
+        fma2s(q0[r], xq0, cr[r]);
+        fma2s(q1[r], xq1, cr[r]);
       }
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      fma2s(p[r], xpv, cr[r]);
-      if (TWO) fma2s(q[r], xqv, cr[r]);
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      fma2s(p[r], xpt, ci[r]);
-      if (TWO) fma2s(q[r], xqt, ci[r]);
+      fma2s(p0[r], tp0, ci[r]);
+      fma2s(p1[r], tp1, ci[r]);
+      if (TWO) {
+        fma2s(q0[r], tq0, ci[r]);
+        fma2s(q1[r], tq1, ci[r]);
+      }
     }
     p_addr += step;
-    q_addr += step + kRowB;
-    step += 2 * kRowB;
+    q_addr += step + qx;
+    step += dstep;
     c_addr += ws_b;
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int nu = m + r0 + r;
-    stsp(out_base + uint32_t(nu * nu + m) * kRowB, p[r]);
-    if (TWO) stsp(out_base + uint32_t(nu * nu + nu + m) * kRowB, q[r]);
-  }
-}
-
-template <bool TWO>
-__device__ __forceinline__ void coax_dispatch(int R, uint32_t c_addr, uint32_t ws_b, int w, int m,
-                                              int r0, uint32_t p_addr, uint32_t q_addr, uint32_t out_base) {
-  switch (R) {
-    case 1: coax_task<1, TWO>(c_addr, ws_b, w, m, r0, p_addr, q_addr, out_base); break;
-    case 2: coax_task<2, TWO>(c_addr, ws_b, w, m, r0, p_addr, q_addr, out_base); break;
-    case 3: coax_task<3, TWO>(c_addr, ws_b, w, m, r0, p_addr, q_addr, out_base); break;
-    default: coax_task<4, TWO>(c_addr, ws_b, w, m, r0, p_addr, q_addr, out_base); break;  // tiles hold <= 4 rows
+    if (r < nrows) {
+      stsp2(out_base + uint32_t(nu * nu + m) * kRowB, p0[r], p1[r]);
+      if (TWO) stsp2(out_base + uint32_t(nu * nu + nu + m) * kRowB, q0[r], q1[r]);
+    }
   }
 }
 
@@ -287,7 +307,6 @@ __constant__ TranslateSchedule c_sched[kMaxOrder + 1];
 template <int NU, int WARPS, int CTAS>  // NU: (n, m >= 0) gather units per lane = ceil((P+1)(P+2)/2 / WARPS)
 __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const TranslateArgs a) {
   constexpr int kThreads = WARPS * 32;
-  constexpr int kMaxR = WARPS == 8 ? 12 : 8;
   constexpr int kLanesPerPair = WARPS;  // 32 pairs x WARPS lanes = all threads of the CTA
   extern __shared__ __align__(16) float smem[];
   const int P = a.order;
@@ -296,7 +315,9 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
   float* s_rot = smem;
   float2* s_coax = reinterpret_cast<float2*>(s_rot + sp.rot_floats);
   float2* s_ph = s_coax + sp.coax_c;  // e^{i m phi}, m = 0..P
-  float2* A = s_ph + sp.phase_c;
+  float4* s_pu = reinterpret_cast<float4*>(s_ph + sp.phase_c);  // per m: (c, -s, sgn c, sgn s) / 2
+  float2* s_zero = s_ph + sp.phase_c + sp.unfold_c;
+  float2* A = s_zero + kZeroC;
   float2* B = A + sp.tile_c;
   // per gather unit (n, m >= 0): raw index of (n, +m) << 16 | folded row of s_m;  t_m sits n rows
   // further, (n, -m) sits 2m raw entries back
@@ -308,6 +329,7 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
   const uint32_t it_end = uint32_t(uint64_t(a.n_items) * (blockIdx.x + 1) / gridDim.x);
   if (it_begin >= it_end) return;
 
+  if (tid < kZeroC) s_zero[tid] = make_float2(0.f, 0.f);
   for (int u = tid; u < n_units; u += kThreads) {
     int n = int((sqrtf(8.0f * float(u) + 1.0f) - 1.0f) * 0.5f);
     while (n * (n + 1) / 2 > u) --n;
@@ -340,8 +362,14 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
   const TranslateSchedule& sched = c_sched[P];
   // byte addresses inside the shared window
   const uint32_t win = uint32_t(__cvta_generic_to_shared(smem));
-  const uint32_t a_lane = uint32_t(__cvta_generic_to_shared(A)) + 8 * lane,
-                 b_lane = uint32_t(__cvta_generic_to_shared(B)) + 8 * lane;
+  // a lane owns the pairs 2l, 2l+1 (l = lane mod 16) of the batch; the halves of a warp run
+  // different sub-tasks
+  const int half = lane >> 4;
+  constexpr uint32_t kRowB = 8 * kRow;
+  const uint32_t a_duo = uint32_t(__cvta_generic_to_shared(A)) + 16 * (lane & 15),
+                 b_duo = uint32_t(__cvta_generic_to_shared(B)) + 16 * (lane & 15),
+                 zero_addr = uint32_t(__cvta_generic_to_shared(s_zero)),
+                 pu_addr = uint32_t(__cvta_generic_to_shared(s_pu));
 
   __syncthreads();  // s_unit
   TranslateItem item = a.items[it_begin];
@@ -366,6 +394,8 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
           cr = t;
         }
         s_ph[tid] = make_float2(cr, ci);
+        const float sg = (tid & 1) ? -0.5f : 0.5f;
+        s_pu[tid] = tid ? make_float4(0.5f * cr, -0.5f * ci, sg * cr, sg * ci) : make_float4(1.f, 0.f, 1.f, 0.f);
       }
       loaded_cls = item.cls;
       __syncthreads();
@@ -398,49 +428,60 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
 
     // stage 2: forward rotation A -> B
     for (int t = sched.rot_begin[warp]; t < sched.rot_begin[warp + 1]; ++t) {
-      const TranslateRotTask d = sched.rot[t];
-      rot_dispatch<false, kMaxR>((d.packed >> 16) & 0xff, win + d.e_off, d.packed & 0xff, (d.packed >> 8) & 0xff,
-                          a_lane + d.in_rel, b_lane + d.out_rel, false);
+      const TranslateRotSub d0 = sched.rot[t].sub[0], d1 = sched.rot[t].sub[1];
+      const TranslateRotSub d = half ? d1 : d0;
+      rot_dispatch<false>(d0.packed >> 28, win + d.e_off, d.packed & 0xff, (d0.packed >> 8) & 0xff,
+                          a_duo + d.in_rel, b_duo + d.out_rel, false, (d.packed >> 16) & 0xff);
     }
     __syncthreads();
     // stage 3: coaxial translation B -> A
     for (int t = sched.coax_begin[warp]; t < sched.coax_begin[warp + 1]; ++t) {
-      const TranslateCoaxTask d = sched.coax[t];
-      const int m = (d.packed >> 16) & 0x3f, r0 = (d.packed >> 22) & 0x3f, R = d.packed >> 28;
-      if (m == 0)
-        coax_dispatch<false>(R, win + d.c_off, d.packed & 0xff, (d.packed >> 8) & 0xff, m, r0,
-                             b_lane + d.p_rel, b_lane + d.q_rel, a_lane);
+      const TranslateCoaxSub d0 = sched.coax[t].sub[0], d1 = sched.coax[t].sub[1];
+      const TranslateCoaxSub d = half ? d1 : d0;
+      const int w0 = (d0.packed >> 8) & 0xff, w1 = (d1.packed >> 8) & 0xff, wmax = max(w0, w1);
+      const int m = (d.packed >> 16) & 0x3f, r0 = (d.packed >> 22) & 0x3f, nrows = d.packed >> 28;
+      if (((d0.packed >> 16) & 0x3f) == 0)  // m = 0 sub-tasks are paired with each other
+        coax_task<false>(win + d.c_off, d.packed & 0xff, (d.packed >> 8) & 0xff, wmax, m, r0, nrows,
+                         b_duo + d.p_rel, b_duo + d.q_rel, a_duo, zero_addr, b_duo);
       else
-        coax_dispatch<true>(R, win + d.c_off, d.packed & 0xff, (d.packed >> 8) & 0xff, m, r0,
-                            b_lane + d.p_rel, b_lane + d.q_rel, a_lane);
+        coax_task<true>(win + d.c_off, d.packed & 0xff, (d.packed >> 8) & 0xff, wmax, m, r0, nrows,
+                        b_duo + d.p_rel, b_duo + d.q_rel, a_duo, zero_addr, b_duo);
     }
     __syncthreads();
     // stage 4: inverse rotation A -> B (same table, sign-twiddled)
     for (int t = sched.rot_begin[warp]; t < sched.rot_begin[warp + 1]; ++t) {
-      const TranslateRotTask d = sched.rot[t];
-      rot_dispatch<true, kMaxR>((d.packed >> 16) & 0xff, win + d.e_off, d.packed & 0xff, (d.packed >> 8) & 0xff,
-                         a_lane + d.in_rel, b_lane + d.out_rel, (d.packed >> 24) & 1);
+      const TranslateRotSub d0 = sched.rot[t].sub[0], d1 = sched.rot[t].sub[1];
+      const TranslateRotSub d = half ? d1 : d0;
+      rot_dispatch<true>(d0.packed >> 28, win + d.e_off, d.packed & 0xff, (d0.packed >> 8) & 0xff,
+                         a_duo + d.in_rel, b_duo + d.out_rel, (d.packed >> 24) & 1, (d.packed >> 16) & 0xff);
     }
     __syncthreads();
     // stage 5a: unfold B -> A in the caller's coefficient order, with e^{-i mu phi}:
     //   y_m = (u + v)/2 e^{-i m phi},   y_{-m} = (-1)^m (u - v)/2 e^{+i m phi}
-    for (int u = ge; u < n_units; u += kLanesPerPair) {
+    // lane = two pairs, one unit (n, m) per half-warp: conflict-free 16-byte accesses, half-warp
+    // uniform indices, packed arithmetic (s_pu holds the four real factors of order m)
+    for (int up = warp; 2 * up < n_units; up += WARPS) {
+      const int u = min(2 * up + half, n_units - 1);  // an odd unit count: the last unit is done twice
       const int n = s_um[2 * u], m = s_um[2 * u + 1], fs = s_unit[u] & 0xffff;
-      const float2 uu = B[fs * kRow + gp];
-      if (m == 0) {
-        A[(n * n + n) * kRow + gp] = uu;
-      } else {
-        const float2 vv = B[(fs + n) * kRow + gp], ph = s_ph[m];
-        const float2 yp = make_float2(0.5f * (uu.x + vv.x), 0.5f * (uu.y + vv.y));
-        float2 ym = make_float2(0.5f * (uu.x - vv.x), 0.5f * (uu.y - vv.y));
-        if (m & 1) ym = make_float2(-ym.x, -ym.y);
-        A[(n * n + n + m) * kRow + gp] = make_float2(yp.x * ph.x + yp.y * ph.y, yp.y * ph.x - yp.x * ph.y);
-        A[(n * n + n - m) * kRow + gp] = make_float2(ym.x * ph.x - ym.y * ph.y, ym.x * ph.y + ym.y * ph.x);
-      }
+      u64 u0, u1, v0 = 0ull, v1 = 0ull;
+      ldsp2(b_duo + uint32_t(fs) * kRowB, u0, u1);
+      if (m) ldsp2(b_duo + uint32_t(fs + n) * kRowB, v0, v1);
+      const float4 f = lds4(pu_addr + 16 * m);
+      u64 s0 = u0, s1 = u1, d0 = u0, d1 = u1;
+      fma2s(s0, v0, 1.0f);
+      fma2s(s1, v1, 1.0f);
+      fma2s(d0, v0, -1.0f);
+      fma2s(d1, v1, -1.0f);
+      u64 yp0 = mul2s(s0, f.x), yp1 = mul2s(s1, f.x), ym0 = mul2s(d0, f.z), ym1 = mul2s(d1, f.z);
+      fma2s(yp0, rot90(s0), f.y);
+      fma2s(yp1, rot90(s1), f.y);
+      fma2s(ym0, rot90(d0), f.w);
+      fma2s(ym1, rot90(d1), f.w);
+      const uint32_t c0 = a_duo + uint32_t(n * n + n) * kRowB;
+      stsp2(c0 + uint32_t(m) * kRowB, yp0, yp1);
+      stsp2(c0 - uint32_t(m) * kRowB, ym0, ym1);  // m = 0: the same row, the same value
     }
-    // a lane group reads back only what it wrote itself (same pair column gp): a warp-level
-    // barrier orders the stores of the lanes of the group before the loads below
-    __syncwarp();
+    __syncthreads();
 
     // stage 5b: start the next item's gather, then accumulate this item into its destinations,
     // two coefficients (16 bytes) per reduction
@@ -467,80 +508,120 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
 void build_translate_schedule(int P, TranslateSchedule* out) {
   const SmemPlan sp = smem_plan(P);
   const int kWarps = translate_warps(P);
-  const int max_rows = kWarps == 8 ? 12 : 8;  // 16 warps need more, smaller tasks to balance
-  const uint32_t kRowF = 2 * kRow, coax_f = uint32_t(sp.rot_floats);
+  constexpr int kMaxRows = 8;  // rows of a rotation tile (accumulators: 2 pairs x 8 rows x (re, im))
+  const uint32_t kRowB = 8 * kRow, coax_b = 4u * uint32_t(sp.rot_floats);
+
+  // ---- rotations: sub-task = (degree n, plus / minus system, tile of <= 8 rows starting at a
+  // multiple of 4).  The plus system of degree n and the minus system of degree n + 1 have the same
+  // shape ((n+1) x (n+1)), so their tiles pair up exactly; the plus system of degree P pairs its
+  // own tiles.
+  struct RotS {
+    TranslateRotSub d;
+    int w, rows;
+  };
+  auto rot_subs = [&](int n, int part) {
+    std::vector<RotS> v;
+    const int w = part ? n : n + 1;
+    const int ws = part ? rot_minus_stride(n) : rot_plus_stride(n);
+    const int base = part ? n * n + n + 1 : n * n;
+    const int table = part ? rot_minus_offset(n) : rot_block_offset(n);
+    for (int r0 = 0; r0 < w; r0 += kMaxRows) {
+      const int R = std::min(kMaxRows, w - r0);
+      RotS s;
+      s.d.e_off = 4u * uint32_t(table + r0);
+      s.d.in_rel = uint32_t(base) * kRowB;
+      s.d.out_rel = uint32_t(base + r0) * kRowB;
+      s.d.packed = 4u * uint32_t(ws) | uint32_t(w) << 8 | uint32_t(R) << 16 | uint32_t(r0 & 1) << 24;
+      s.w = w;
+      s.rows = R;
+      v.push_back(s);
+    }
+    return v;
+  };
   struct RotT {
     TranslateRotTask d;
     int cost;
+  };
+  std::vector<RotT> rot;
+  auto add_rot = [&rot](const RotS& x, const RotS* y) {
+    RotT t;
+    t.d.sub[0] = x.d;
+    int R = x.rows;
+    if (y) {
+      t.d.sub[1] = y->d;
+      R = std::max(R, y->rows);
+    } else {  // no partner: the second half-warp repeats the sub-task and stores nothing
+      t.d.sub[1] = x.d;
+      t.d.sub[1].packed &= ~(0xffu << 16);
+    }
+    t.d.sub[0].packed |= uint32_t(R) << 28;
+    t.cost = x.w * (4 * R + 8) + 4 * R + 40;
+    rot.push_back(t);
+  };
+  for (int n = 0; n < P; ++n) {
+    const auto plus = rot_subs(n, 0), minus = rot_subs(n + 1, 1);
+    for (size_t i = 0; i < plus.size(); ++i) add_rot(plus[i], &minus[i]);
+  }
+  {
+    const auto plus = rot_subs(P, 0);
+    for (size_t i = 0; i < plus.size(); i += 2) add_rot(plus[i], i + 1 < plus.size() ? &plus[i + 1] : nullptr);
+  }
+
+  // ---- coaxial step: sub-task = (order m, tile of <= 4 rows); tiles of one order pair up, the odd
+  // ones out are paired by decreasing length (the shorter half multiplies zeros at the end)
+  struct CoaxS {
+    TranslateCoaxSub d;
+    int w;
   };
   struct CoaxT {
     TranslateCoaxTask d;
     int cost;
   };
-  std::vector<RotT> rot;
   std::vector<CoaxT> coax;
-  // rows of a sub-block are cut into tiles that start at multiples of 4 (aligned 16-byte
-  // coefficient loads) and hold <= 12 rows; the split minimising sum(2R + 6) (instructions per
-  // input step) is found by exhaustive search
-  auto cut = [max_rows](int w, int parts[4]) {
-    int best_cost = 1 << 30, best_n = 0;
-    for (int a = 0; a <= max_rows; a += 4)
-      for (int b = 0; b <= max_rows; b += 4)
-        for (int c = 0; c <= max_rows; c += 4) {
-          const int last = w - a - b - c;
-          if (last < 1 || last > max_rows) continue;
-          if ((a == 0 && (b || c)) || (b == 0 && c)) continue;
-          int cand[4] = {a, b, c, last}, tmp[4], np = 0, cost = 0;
-          for (int v : cand)
-            if (v) {
-              tmp[np++] = v;
-              cost += 2 * v + 6;
-            }
-          if (cost < best_cost) {
-            best_cost = cost;
-            best_n = np;
-            for (int i = 0; i < np; ++i) parts[i] = tmp[i];
-          }
-        }
-    return best_n;
-  };
-  for (int n = 0; n <= P; ++n)
-    for (int part = 0; part < 2; ++part) {  // 0: plus system (n+1 rows), 1: minus system (n rows)
-      const int w = part ? n : n + 1;
-      if (w == 0) continue;
-      const int ws = part ? rot_minus_stride(n) : rot_plus_stride(n);
-      const int base = part ? n * n + n + 1 : n * n;
-      const int table = part ? rot_minus_offset(n) : rot_block_offset(n);
-      int parts[4], r0 = 0;
-      const int np = cut(w, parts);
-      for (int i = 0; i < np; ++i) {
-        const int R = parts[i];
-        TranslateRotTask d;
-        d.e_off = 4u * uint32_t(table + r0);
-        d.in_rel = 4u * uint32_t(base) * kRowF;
-        d.out_rel = 4u * uint32_t(base + r0) * kRowF;
-        d.packed = 4u * uint32_t(ws) | uint32_t(w) << 8 | uint32_t(R) << 16 | uint32_t(r0 & 1) << 24;
-        rot.push_back({d, w * (2 * R + 6) + 40});
-        r0 += R;
-      }
+  std::vector<CoaxS> odd;
+  auto add_coax = [&coax](const CoaxS& x, const CoaxS* y, bool two) {
+    CoaxT t;
+    t.d.sub[0] = x.d;
+    int w = x.w;
+    if (y) {
+      t.d.sub[1] = y->d;
+      w = std::max(w, y->w);
+    } else {
+      t.d.sub[1] = x.d;
+      t.d.sub[1].packed &= ~(0xfu << 28);
     }
+    t.cost = w * ((two ? 32 : 16) + 12) + 60;
+    coax.push_back(t);
+  };
   for (int m = 0; m <= P; ++m) {
     const int w = P + 1 - m;
-    // tiles of <= 4 rows (measured: 8-row tiles balance worse over the 8 warps and are slower)
-    for (int r0 = 0; r0 < w;) {
+    std::vector<CoaxS> tiles;
+    for (int r0 = 0; r0 < w; r0 += 4) {
       const int R = std::min(4, w - r0);
-      TranslateCoaxTask d;
-      d.c_off = 4u * (coax_f + 2u * uint32_t(coax_block_offset(P, m) + r0));
-      d.p_rel = 4u * uint32_t(m * m + m) * kRowF;
-      d.q_rel = 4u * uint32_t(m * m + 2 * m) * kRowF;
-      d.packed = 4u * uint32_t(2 * coax_row_stride(P, m)) | uint32_t(w) << 8 | uint32_t(m) << 16 |
-                 uint32_t(r0) << 22 | uint32_t(R) << 28;  // R <= 8 fits bits 28..31
-      coax.push_back({d, w * ((m ? 8 : 4) * R + 8) + 40});
-      r0 += R;
+      CoaxS s;
+      s.d.c_off = coax_b + 8u * uint32_t(coax_block_offset(P, m) + r0);
+      s.d.p_rel = uint32_t(m * m + m) * kRowB;
+      s.d.q_rel = uint32_t(m * m + 2 * m) * kRowB;
+      s.d.packed = 8u * uint32_t(coax_row_stride(P, m)) | uint32_t(w) << 8 | uint32_t(m) << 16 |
+                   uint32_t(r0) << 22 | uint32_t(R) << 28;
+      s.w = w;
+      tiles.push_back(s);
+    }
+    size_t i = 0;
+    for (; i + 1 < tiles.size(); i += 2) add_coax(tiles[i], &tiles[i + 1], m != 0);
+    if (i < tiles.size()) {
+      if (m == 0) add_coax(tiles[i], nullptr, false);  // x_0 column: single-column code path
+      else odd.push_back(tiles[i]);
     }
   }
+  std::stable_sort(odd.begin(), odd.end(), [](const CoaxS& x, const CoaxS& y) { return x.w > y.w; });
+  for (size_t i = 0; i < odd.size(); i += 2) add_coax(odd[i], i + 1 < odd.size() ? &odd[i + 1] : nullptr, true);
+
   if (rot.size() > size_t(kTranslateMaxTasks) || coax.size() > size_t(kTranslateMaxTasks))
     throw Error(HFMM_ERR_INTERNAL, "translation schedule overflow");
+  for (const auto& t : coax)
+    if ((t.d.sub[0].packed & 0xff) != (8u * uint32_t(coax_row_stride(P, (t.d.sub[0].packed >> 16) & 0x3f))))
+      throw Error(HFMM_ERR_INTERNAL, "coaxial row stride does not fit its field");
   auto distribute = [kWarps](auto& tasks, auto* flat, int* begin) {
     std::stable_sort(tasks.begin(), tasks.end(), [](const auto& x, const auto& y) { return x.cost > y.cost; });
     std::vector<std::vector<int>> per(kWarps);
@@ -605,8 +686,6 @@ void launch_translate(const TranslateArgs& a, cudaStream_t s) {
     if (nu <= 6) launch_translate_nu<6, 8, 2>(a, s, sp.bytes, ctas);         // P <= 8
     else if (nu <= 9) launch_translate_nu<9, 8, 2>(a, s, sp.bytes, ctas);    // P <= 10
     else launch_translate_nu<12, 8, 2>(a, s, sp.bytes, ctas);                // P <= 12
-  } else if (two) {
-    launch_translate_nu<6, 16, 2>(a, s, sp.bytes, ctas);                     // P <= 12, 64 registers
   } else {
     const int nu = (units + 15) / 16;
     if (nu <= 8) launch_translate_nu<8, 16, 1>(a, s, sp.bytes, ctas);        // P <= 14
