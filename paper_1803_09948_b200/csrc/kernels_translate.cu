@@ -51,7 +51,7 @@ __host__ __device__ inline SmemPlan smem_plan(int P) {
   s.rot_floats = rot_table_size(P);
   s.coax_c = coax_table_size(P);
   s.phase_c = (P + 2) & ~1;
-  s.unfold_c = 2 * (P + 1);  // one float4 per order m
+  s.unfold_c = 4 * (P + 1);  // two float4 per order m: fold factors, unfold factors
   s.tile_c = s.dim * kRow;
   // rot | coax | phases | unfold factors | zero row | tile A | tile B | (n, m) of every gather unit (u16)
   s.bytes = size_t(s.rot_floats) * 4 + size_t(s.coax_c + s.phase_c + s.unfold_c + kZeroC + 2 * s.tile_c) * 8 +
@@ -304,7 +304,7 @@ __constant__ TranslateSchedule c_sched[kMaxOrder + 1];
 // tables in shared memory are reloaded only when the class changes).  The gather of the NEXT item
 // is issued into registers while the current item drains through its reductions, so the chain
 // item -> pair list -> source rows never sits on the critical path.
-template <int NU, int WARPS, int CTAS>  // NU: (n, m >= 0) gather units per lane = ceil((P+1)(P+2)/2 / WARPS)
+template <int NU, int WARPS, int CTAS>  // NU >= 16-byte chunks of a source row per lane = ceil(ceil((P+1)^2 / 2) / WARPS)
 __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const TranslateArgs a) {
   constexpr int kThreads = WARPS * 32;
   constexpr int kLanesPerPair = WARPS;  // 32 pairs x WARPS lanes = all threads of the CTA
@@ -315,7 +315,8 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
   float* s_rot = smem;
   float2* s_coax = reinterpret_cast<float2*>(s_rot + sp.rot_floats);
   float2* s_ph = s_coax + sp.coax_c;  // e^{i m phi}, m = 0..P
-  float4* s_pu = reinterpret_cast<float4*>(s_ph + sp.phase_c);  // per m: (c, -s, sgn c, sgn s) / 2
+  float4* s_pu = reinterpret_cast<float4*>(s_ph + sp.phase_c);  // unfold, per m: (c, -s, sgn c, sgn s) / 2
+  float4* s_pf = s_pu + (P + 1);                                // fold,   per m: (c, s, sgn c, -sgn s)
   float2* s_zero = s_ph + sp.phase_c + sp.unfold_c;
   float2* A = s_zero + kZeroC;
   float2* B = A + sp.tile_c;
@@ -340,21 +341,30 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
     s_um[2 * u + 1] = (unsigned char)m;
   }
 
-  // gather mapping: 32/WARPS pairs x WARPS lanes per warp; a lane owns units u = ge + WARPS j, i.e.
-  // the two source coefficients (n, +m) and (n, -m) it folds into s_m and t_m
+  // gather mapping: 32/WARPS pairs x WARPS lanes per warp; a lane owns the 16-byte chunks
+  // c = ge + WARPS j of its pair's source row (coefficients 2c, 2c+1): coalesced LDG.128 into
+  // registers, later stored transposed (coefficient-major, raw order) into tile B
   const int gq = lane / kLanesPerPair, ge = lane % kLanesPerPair, gp = warp * (32 / kLanesPerPair) + gq;
-  float2 gxp[NU], gxm[NU];
+  const int n_chunks = (dim + 1) / 2;
+  float4 gx[NU];
   auto issue_gather = [&](const TranslateItem& it) {
     const bool live = gp < int(it.count);
-    const float2* row = live ? a.src + size_t(a.pair_src[it.pair_begin + gp]) * a.stride : nullptr;
+    const float4* row =
+        live ? reinterpret_cast<const float4*>(a.src + size_t(a.pair_src[it.pair_begin + gp]) * a.stride) : nullptr;
 #pragma unroll
     for (int j = 0; j < NU; ++j) {
-      const int u = ge + kLanesPerPair * j;
-      gxp[j] = gxm[j] = make_float2(0.f, 0.f);
-      if (live && u < n_units) {
-        const int i = s_unit[u] >> 16, m = s_um[2 * u + 1];
-        gxp[j] = row[i];
-        gxm[j] = row[i - 2 * m];
+      const int c = ge + kLanesPerPair * j;
+      gx[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (live && c < n_chunks) gx[j] = row[c];  // rows are padded to 32 bytes: the last chunk is whole
+    }
+  };
+  auto store_raw = [&]() {
+#pragma unroll
+    for (int j = 0; j < NU; ++j) {
+      const int c = ge + kLanesPerPair * j;
+      if (c < n_chunks) {
+        B[(2 * c) * kRow + gp] = make_float2(gx[j].x, gx[j].y);
+        if (2 * c + 1 < dim) B[(2 * c + 1) * kRow + gp] = make_float2(gx[j].z, gx[j].w);
       }
     }
   };
@@ -369,12 +379,14 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
   const uint32_t a_duo = uint32_t(__cvta_generic_to_shared(A)) + 16 * (lane & 15),
                  b_duo = uint32_t(__cvta_generic_to_shared(B)) + 16 * (lane & 15),
                  zero_addr = uint32_t(__cvta_generic_to_shared(s_zero)),
-                 pu_addr = uint32_t(__cvta_generic_to_shared(s_pu));
+                 pu_addr = uint32_t(__cvta_generic_to_shared(s_pu)),
+                 pf_addr = uint32_t(__cvta_generic_to_shared(s_pf));
 
-  __syncthreads();  // s_unit
   TranslateItem item = a.items[it_begin];
   issue_gather(item);
+  store_raw();
   uint32_t loaded_cls = 0xffffffffu;
+  __syncthreads();  // s_unit, the first item's operands
 
   for (uint32_t it = it_begin; it < it_end; ++it) {
     const int count = int(item.count);
@@ -396,29 +408,35 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
         s_ph[tid] = make_float2(cr, ci);
         const float sg = (tid & 1) ? -0.5f : 0.5f;
         s_pu[tid] = tid ? make_float4(0.5f * cr, -0.5f * ci, sg * cr, sg * ci) : make_float4(1.f, 0.f, 1.f, 0.f);
+        s_pf[tid] = tid ? make_float4(cr, ci, 2.f * sg * cr, -2.f * sg * ci) : make_float4(1.f, 0.f, 0.f, 0.f);
       }
       loaded_cls = item.cls;
       __syncthreads();
     }
 
-    // stage 1: e^{i m phi}, fold, store element-major into A
+    // stage 1: e^{i m phi} and fold, B (raw) -> A:
     //   a = x_m e^{i m phi},  b = (-1)^m x_{-m} e^{-i m phi}:   s_m = a + b,  t_m = a - b
-#pragma unroll
-    for (int j = 0; j < NU; ++j) {
-      const int u = ge + kLanesPerPair * j;
-      if (u < n_units) {
-        const int n = s_um[2 * u], m = s_um[2 * u + 1], fs = s_unit[u] & 0xffff;
-        const float2 ph = s_ph[m], xp = gxp[j], xm = gxm[j];
-        if (m == 0) {
-          A[fs * kRow + gp] = xp;
-        } else {
-          const float2 av = make_float2(xp.x * ph.x - xp.y * ph.y, xp.x * ph.y + xp.y * ph.x);
-          float2 bv = make_float2(xm.x * ph.x + xm.y * ph.y, xm.y * ph.x - xm.x * ph.y);
-          if (m & 1) bv = make_float2(-bv.x, -bv.y);
-          A[fs * kRow + gp] = make_float2(av.x + bv.x, av.y + bv.y);
-          A[(fs + n) * kRow + gp] = make_float2(av.x - bv.x, av.y - bv.y);
-        }
-      }
+    // same mapping as the unfold below (lane = two pairs, one unit per half-warp)
+    for (int up = warp; 2 * up < n_units; up += WARPS) {
+      const int u = min(2 * up + half, n_units - 1);
+      const int n = s_um[2 * u], m = s_um[2 * u + 1], fs = s_unit[u] & 0xffff;
+      const uint32_t c0 = b_duo + uint32_t(n * n + n) * kRowB;
+      u64 xp0, xp1, xm0 = 0ull, xm1 = 0ull;
+      ldsp2(c0 + uint32_t(m) * kRowB, xp0, xp1);
+      if (m) ldsp2(c0 - uint32_t(m) * kRowB, xm0, xm1);
+      const float4 f = lds4(pf_addr + 16 * m);
+      u64 a0 = mul2s(xp0, f.x), a1 = mul2s(xp1, f.x), b0 = mul2s(xm0, f.z), b1 = mul2s(xm1, f.z);
+      fma2s(a0, rot90(xp0), f.y);
+      fma2s(a1, rot90(xp1), f.y);
+      fma2s(b0, rot90(xm0), f.w);
+      fma2s(b1, rot90(xm1), f.w);
+      u64 t0 = a0, t1 = a1;
+      fma2s(a0, b0, 1.0f);
+      fma2s(a1, b1, 1.0f);
+      fma2s(t0, b0, -1.0f);
+      fma2s(t1, b1, -1.0f);
+      stsp2(a_duo + uint32_t(fs) * kRowB, a0, a1);
+      if (m) stsp2(a_duo + uint32_t(fs + n) * kRowB, t0, t1);
     }
     __syncthreads();
     // metadata of the next item (consumed in stage 5)
@@ -495,6 +513,8 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
       if ((dim & 1) && ge == 0)
         atomicAdd(reinterpret_cast<float2*>(dst) + (dim - 1), A[(dim - 1) * kRow + gp]);
     }
+    // tile B is free since the unfold: the next item's operands wait there
+    if (has_next) store_raw();
     item = next;
     // the next stage 1 overwrites A: every warp must be done reading it
     __syncthreads();
@@ -680,15 +700,14 @@ void launch_translate(const TranslateArgs& a, cudaStream_t s) {
   const int warps = translate_warps(a.order);
   const bool two = translate_two_ctas(a.order);
   const int ctas = int(std::min<uint32_t>(a.n_items, uint32_t((two ? 2 : 1) * sm_count)));
-  const int units = (a.order + 1) * (a.order + 2) / 2;
+  const int chunks = ((a.order + 1) * (a.order + 1) + 1) / 2;  // 16-byte chunks of one expansion
+  const int nu = (chunks + warps - 1) / warps;
   if (warps == 8) {
-    const int nu = (units + 7) / 8;
     if (nu <= 6) launch_translate_nu<6, 8, 2>(a, s, sp.bytes, ctas);         // P <= 8
-    else if (nu <= 9) launch_translate_nu<9, 8, 2>(a, s, sp.bytes, ctas);    // P <= 10
+    else if (nu <= 9) launch_translate_nu<9, 8, 2>(a, s, sp.bytes, ctas);    // P <= 11
     else launch_translate_nu<12, 8, 2>(a, s, sp.bytes, ctas);                // P <= 12
   } else {
-    const int nu = (units + 15) / 16;
-    if (nu <= 8) launch_translate_nu<8, 16, 1>(a, s, sp.bytes, ctas);        // P <= 14
+    if (nu <= 8) launch_translate_nu<8, 16, 1>(a, s, sp.bytes, ctas);        // P <= 15
     else launch_translate_nu<10, 16, 1>(a, s, sp.bytes, ctas);               // P <= 16
   }
 }
