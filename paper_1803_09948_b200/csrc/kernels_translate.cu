@@ -304,7 +304,7 @@ __constant__ TranslateSchedule c_sched[kMaxOrder + 1];
 // tables in shared memory are reloaded only when the class changes).  The gather of the NEXT item
 // is issued into registers while the current item drains through its reductions, so the chain
 // item -> pair list -> source rows never sits on the critical path.
-template <int NU, int WARPS, int CTAS>  // NU >= 16-byte chunks of a source row per lane = ceil(ceil((P+1)^2 / 2) / WARPS)
+template <int WARPS, int CTAS>
 __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const TranslateArgs a) {
   constexpr int kThreads = WARPS * 32;
   constexpr int kLanesPerPair = WARPS;  // 32 pairs x WARPS lanes = all threads of the CTA
@@ -341,33 +341,29 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
     s_um[2 * u + 1] = (unsigned char)m;
   }
 
-  // gather mapping: 32/WARPS pairs x WARPS lanes per warp; a lane owns the 16-byte chunks
-  // c = ge + WARPS j of its pair's source row (coefficients 2c, 2c+1): coalesced LDG.128 into
-  // registers, later stored transposed (coefficient-major, raw order) into tile B
+  // gather mapping: 32/WARPS pairs x WARPS lanes per warp; the lanes of a pair stream its source
+  // row (64-byte runs) with asynchronous 8-byte copies straight into tile B, transposed
+  // (coefficient-major, raw order): no staging registers, the copies drain under the reductions
   const int gq = lane / kLanesPerPair, ge = lane % kLanesPerPair, gp = warp * (32 / kLanesPerPair) + gq;
-  const int n_chunks = (dim + 1) / 2;
-  float4 gx[NU];
+  const uint32_t b_gather = uint32_t(__cvta_generic_to_shared(B)) + 8u * uint32_t(ge * kRow + gp);
   auto issue_gather = [&](const TranslateItem& it) {
-    const bool live = gp < int(it.count);
-    const float4* row =
-        live ? reinterpret_cast<const float4*>(a.src + size_t(a.pair_src[it.pair_begin + gp]) * a.stride) : nullptr;
-#pragma unroll
-    for (int j = 0; j < NU; ++j) {
-      const int c = ge + kLanesPerPair * j;
-      gx[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (live && c < n_chunks) gx[j] = row[c];  // rows are padded to 32 bytes: the last chunk is whole
-    }
-  };
-  auto store_raw = [&]() {
-#pragma unroll
-    for (int j = 0; j < NU; ++j) {
-      const int c = ge + kLanesPerPair * j;
-      if (c < n_chunks) {
-        B[(2 * c) * kRow + gp] = make_float2(gx[j].x, gx[j].y);
-        if (2 * c + 1 < dim) B[(2 * c + 1) * kRow + gp] = make_float2(gx[j].z, gx[j].w);
+    uint32_t dst = b_gather;
+    if (gp < int(it.count)) {
+      const float2* src = a.src + size_t(a.pair_src[it.pair_begin + gp]) * a.stride + ge;
+      for (int i = ge; i < dim; i += kLanesPerPair) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+        dst += 8u * kLanesPerPair * kRow;
+        src += kLanesPerPair;
+      }
+    } else {  // a partial batch: the idle columns stay finite
+      for (int i = ge; i < dim; i += kLanesPerPair) {
+        sts2(dst, make_float2(0.f, 0.f));
+        dst += 8u * kLanesPerPair * kRow;
       }
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
+  auto wait_gather = [&]() { asm volatile("cp.async.wait_all;" ::: "memory"); };
 
   const TranslateSchedule& sched = c_sched[P];
   // byte addresses inside the shared window
@@ -384,7 +380,7 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
 
   TranslateItem item = a.items[it_begin];
   issue_gather(item);
-  store_raw();
+  wait_gather();
   uint32_t loaded_cls = 0xffffffffu;
   __syncthreads();  // s_unit, the first item's operands
 
@@ -513,8 +509,8 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
       if ((dim & 1) && ge == 0)
         atomicAdd(reinterpret_cast<float2*>(dst) + (dim - 1), A[(dim - 1) * kRow + gp]);
     }
-    // tile B is free since the unfold: the next item's operands wait there
-    if (has_next) store_raw();
+    // the next item's operands (tile B is free since the unfold) must have landed
+    wait_gather();
     item = next;
     // the next stage 1 overwrites A: every warp must be done reading it
     __syncthreads();
@@ -674,15 +670,15 @@ void upload_translate_schedule(int order) {
 int translate_batch_size(int) { return kTranslateBatch; }
 
 namespace {
-template <int NU, int WARPS, int CTAS>
+template <int WARPS, int CTAS>
 void launch_translate_nu(const TranslateArgs& a, cudaStream_t s, size_t bytes, int ctas) {
   static int configured_for = -1;
   if (configured_for < int(bytes)) {
-    HFMM_CUDA_CHECK(cudaFuncSetAttribute(translate_kernel<NU, WARPS, CTAS>,
+    HFMM_CUDA_CHECK(cudaFuncSetAttribute(translate_kernel<WARPS, CTAS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
     configured_for = int(bytes);
   }
-  translate_kernel<NU, WARPS, CTAS><<<ctas, WARPS * 32, bytes, s>>>(a);
+  translate_kernel<WARPS, CTAS><<<ctas, WARPS * 32, bytes, s>>>(a);
   HFMM_CUDA_CHECK(cudaGetLastError());
 }
 }  // namespace
@@ -700,16 +696,8 @@ void launch_translate(const TranslateArgs& a, cudaStream_t s) {
   const int warps = translate_warps(a.order);
   const bool two = translate_two_ctas(a.order);
   const int ctas = int(std::min<uint32_t>(a.n_items, uint32_t((two ? 2 : 1) * sm_count)));
-  const int chunks = ((a.order + 1) * (a.order + 1) + 1) / 2;  // 16-byte chunks of one expansion
-  const int nu = (chunks + warps - 1) / warps;
-  if (warps == 8) {
-    if (nu <= 6) launch_translate_nu<6, 8, 2>(a, s, sp.bytes, ctas);         // P <= 8
-    else if (nu <= 9) launch_translate_nu<9, 8, 2>(a, s, sp.bytes, ctas);    // P <= 11
-    else launch_translate_nu<12, 8, 2>(a, s, sp.bytes, ctas);                // P <= 12
-  } else {
-    if (nu <= 8) launch_translate_nu<8, 16, 1>(a, s, sp.bytes, ctas);        // P <= 15
-    else launch_translate_nu<10, 16, 1>(a, s, sp.bytes, ctas);               // P <= 16
-  }
+  if (warps == 8) launch_translate_nu<8, 2>(a, s, sp.bytes, ctas);
+  else launch_translate_nu<16, 1>(a, s, sp.bytes, ctas);
 }
 
 }  // namespace hfmm_b200
