@@ -380,35 +380,44 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
 
   TranslateItem item = a.items[it_begin];
   issue_gather(item);
-  wait_gather();
   uint32_t loaded_cls = 0xffffffffu;
-  __syncthreads();  // s_unit, the first item's operands
+
+  // Tables of a shift class: asynchronous 16-byte copies, issued as soon as the previous item has
+  // left its last table-reading stage, so the fetch hides under its unfold and reductions; the
+  // (P + 1) fold / unfold factor quadruples are computed by the first threads behind the unfold.
+  auto fetch_tables = [&](const TranslateClass& cls) {
+    const float4* g_rot = reinterpret_cast<const float4*>(a.rot_tables + size_t(cls.rot) * sp.rot_floats);
+    const float4* g_coax = reinterpret_cast<const float4*>(a.coax_tables + size_t(cls.coax) * sp.coax_c * 2);
+    const uint32_t rot_s = uint32_t(__cvta_generic_to_shared(s_rot)), coax_s = uint32_t(__cvta_generic_to_shared(s_coax));
+    for (int i = tid; i < sp.rot_floats / 4; i += kThreads)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(rot_s + 16u * i), "l"(g_rot + i) : "memory");
+    for (int i = tid; i < sp.coax_c / 2; i += kThreads)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(coax_s + 16u * i), "l"(g_coax + i) : "memory");
+  };
+  auto store_factors = [&](const TranslateClass& cls) {
+    if (tid <= P) {
+      float cr = 1.f, ci = 0.f;
+      for (int j = 0; j < tid; ++j) {
+        const float t = cr * cls.cphi - ci * cls.sphi;
+        ci = ci * cls.cphi + cr * cls.sphi;
+        cr = t;
+      }
+      const float sg = (tid & 1) ? -0.5f : 0.5f;
+      s_pu[tid] = tid ? make_float4(0.5f * cr, -0.5f * ci, sg * cr, sg * ci) : make_float4(1.f, 0.f, 1.f, 0.f);
+      s_pf[tid] = tid ? make_float4(cr, ci, 2.f * sg * cr, -2.f * sg * ci) : make_float4(1.f, 0.f, 0.f, 0.f);
+    }
+  };
+  {
+    const TranslateClass cls = a.classes[item.cls];
+    fetch_tables(cls);
+    store_factors(cls);
+    loaded_cls = item.cls;
+  }
+  wait_gather();    // the first item's operands and tables
+  __syncthreads();  // ... and s_unit
 
   for (uint32_t it = it_begin; it < it_end; ++it) {
     const int count = int(item.count);
-    if (item.cls != loaded_cls) {  // CTA-uniform
-      // every warp is past the previous item's stage 4 (the last reader of the tables)
-      const TranslateClass cls = a.classes[item.cls];
-      const float4* g_rot = reinterpret_cast<const float4*>(a.rot_tables + size_t(cls.rot) * sp.rot_floats);
-      for (int i = tid; i < sp.rot_floats / 4; i += kThreads) reinterpret_cast<float4*>(s_rot)[i] = g_rot[i];
-      const float4* g_coax =
-          reinterpret_cast<const float4*>(a.coax_tables + size_t(cls.coax) * sp.coax_c * 2);
-      for (int i = tid; i < sp.coax_c / 2; i += kThreads) reinterpret_cast<float4*>(s_coax)[i] = g_coax[i];
-      if (tid <= P) {
-        float cr = 1.f, ci = 0.f;
-        for (int j = 0; j < tid; ++j) {
-          const float t = cr * cls.cphi - ci * cls.sphi;
-          ci = ci * cls.cphi + cr * cls.sphi;
-          cr = t;
-        }
-        s_ph[tid] = make_float2(cr, ci);
-        const float sg = (tid & 1) ? -0.5f : 0.5f;
-        s_pu[tid] = tid ? make_float4(0.5f * cr, -0.5f * ci, sg * cr, sg * ci) : make_float4(1.f, 0.f, 1.f, 0.f);
-        s_pf[tid] = tid ? make_float4(cr, ci, 2.f * sg * cr, -2.f * sg * ci) : make_float4(1.f, 0.f, 0.f, 0.f);
-      }
-      loaded_cls = item.cls;
-      __syncthreads();
-    }
 
     // stage 1: e^{i m phi} and fold, B (raw) -> A:
     //   a = x_m e^{i m phi},  b = (-1)^m x_{-m} e^{-i m phi}:   s_m = a + b,  t_m = a - b
@@ -470,6 +479,13 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
                          a_duo + d.in_rel, b_duo + d.out_rel, (d.packed >> 24) & 1, (d.packed >> 16) & 0xff);
     }
     __syncthreads();
+    // the tables have had their last reader: fetch the next class's behind the unfold
+    const bool new_cls = has_next && next.cls != loaded_cls;  // CTA-uniform
+    TranslateClass ncls{};
+    if (new_cls) {
+      ncls = a.classes[next.cls];
+      fetch_tables(ncls);
+    }
     // stage 5a: unfold B -> A in the caller's coefficient order, with e^{-i mu phi}:
     //   y_m = (u + v)/2 e^{-i m phi},   y_{-m} = (-1)^m (u - v)/2 e^{+i m phi}
     // lane = two pairs, one unit (n, m) per half-warp: conflict-free 16-byte accesses, half-warp
@@ -500,6 +516,10 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
     // stage 5b: start the next item's gather, then accumulate this item into its destinations,
     // two coefficients (16 bytes) per reduction
     if (has_next) issue_gather(next);
+    if (new_cls) {  // the unfold (last reader of the factors) is behind the barrier above
+      store_factors(ncls);
+      loaded_cls = next.cls;
+    }
     if (gp < count) {
       float* dst = reinterpret_cast<float*>(a.dst + size_t(a.pair_dst[item.pair_begin + gp]) * a.stride);
       for (int i2 = ge; i2 < dim / 2; i2 += kLanesPerPair) {
