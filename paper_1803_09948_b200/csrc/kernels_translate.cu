@@ -520,14 +520,19 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
       store_factors(ncls);
       loaded_cls = next.cls;
     }
-    if (gp < count) {
-      float* dst = reinterpret_cast<float*>(a.dst + size_t(a.pair_dst[item.pair_begin + gp]) * a.stride);
-      for (int i2 = ge; i2 < dim / 2; i2 += kLanesPerPair) {
-        const float2 lo = A[(2 * i2) * kRow + gp], hi = A[(2 * i2 + 1) * kRow + gp];
-        atomicAdd(reinterpret_cast<float4*>(dst) + i2, make_float4(lo.x, lo.y, hi.x, hi.y));
+    // reduction mapping: a warp takes 4 pairs x 8 lanes, laid out so that each half-warp reads 4
+    // consecutive coefficient pairs of 4 pairs (rows 2 i2 of tile A are 8 banks apart: conflict-free)
+    {
+      const int sq = (lane >> 2) & 3, se = (lane & 3) | ((lane >> 4) << 2), pr = 4 * (warp & 7) + sq;
+      if (pr < count) {
+        float* dst = reinterpret_cast<float*>(a.dst + size_t(a.pair_dst[item.pair_begin + pr]) * a.stride);
+        for (int i2 = se + 8 * (warp >> 3); i2 < dim / 2; i2 += WARPS) {
+          const float2 lo = A[(2 * i2) * kRow + pr], hi = A[(2 * i2 + 1) * kRow + pr];
+          atomicAdd(reinterpret_cast<float4*>(dst) + i2, make_float4(lo.x, lo.y, hi.x, hi.y));
+        }
+        if ((dim & 1) && se == 0 && warp < 8)
+          atomicAdd(reinterpret_cast<float2*>(dst) + (dim - 1), A[(dim - 1) * kRow + pr]);
       }
-      if ((dim & 1) && ge == 0)
-        atomicAdd(reinterpret_cast<float2*>(dst) + (dim - 1), A[(dim - 1) * kRow + gp]);
     }
     // the next item's operands (tile B is free since the unfold) must have landed
     wait_gather();
