@@ -227,7 +227,7 @@ def run_single(args, cfg):
             "kernel": "translate_kernel (M2L launch)", "bound": "fp32",
             "achieved": m2l_tf, "peak": fp32_peak, "unit": "TFLOP/s",
             "frac": m2l_tf / fp32_peak if fp32_peak else None,
-            "peak_source": "FFMA-only probe in this run (MEASURED_PEAKS.json has no FP32 entry); "
+            "peak_source": "higher of the FFMA and FFMA2 (fma.rn.f32x2) probes in this run (MEASURED_PEAKS.json has no FP32 entry); "
                            f"nominal 148x128x2x1.965 GHz = {nominal:.1f}",
             "flops_per_unit": ex, "units_per_launch": st0["m2l_pairs"],
             "dense_equivalent_tflops": st0["m2l_pairs"] * dense / kern["m2l"] * 1e-12 if kern["m2l"] else None,
@@ -238,9 +238,10 @@ def run_single(args, cfg):
             ) / kern["m2l"] * 1e-12 if kern["m2l"] else None,
             "ms_per_launch": kern["m2l"] * 1e3,
             # dram__bytes_read + dram__bytes_write of this launch from the committed ncu --set full
-            # capture of the same configuration (profiles/r01_ncu_cfg2_full.txt); algorithmic bytes
+            # capture of the same configuration (profiles/r01_ncu_translate_dual_cfg2_full.txt:
+            # 11.41 GB read + 5.51 GB written); algorithmic bytes
             # are pairs x 2 x 8 (P+1)^2 (one source row read, one destination row reduced)
-            "traffic": 18.24e9 if (cfg.name == "cfg2" and n == cfg.n) else None,
+            "traffic": 16.93e9 if (cfg.name == "cfg2" and n == cfg.n) else None,
             "algorithmic_bytes": st0["m2l_pairs"] * 2 * 8 * (cfg.order + 1) ** 2},
         "kernels": {
             "p2p": {"ms": kern["p2p"] * 1e3, "tflops_24flop_per_pair": p2p_tf,
