@@ -45,76 +45,114 @@ __device__ __forceinline__ float cos_approx(float x) {
   return y;
 }
 
-__device__ __forceinline__ void green_accumulate(float r2, float rinv, float qr, float qi,
-                                                 float& ar, float& ai) {
-  const float r = r2 * rinv;
-  const float gr = rinv * cos_approx(r), gi = rinv * sin_approx(r);
-  ar = fmaf(gr, qr, ar);
-  ar = fmaf(-gi, qi, ar);
-  ai = fmaf(gr, qi, ai);
-  ai = fmaf(gi, qr, ai);
+// ---- packed FP32 (sm_100a): add / mul / fma.rn.f32x2 work on a register PAIR per instruction at
+// the FP32 rate of two scalar instructions.  The kernel is issue-bound (3 MUFU + ~14 FP32
+// instructions per body pair), so TWO targets are evaluated per instruction stream: every
+// coordinate, distance and accumulator is a (target 2j, target 2j+1) pair; only the MUFU
+// evaluations (rsqrt, sin, cos) stay scalar.
+using u64 = unsigned long long;
+__device__ __forceinline__ u64 pack2(float lo, float hi) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 unpack2(u64 v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+  u64 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+  u64 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+  u64 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ void lds_2x2(uint32_t addr, u64& a, u64& b) {
+  asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"(addr));
 }
 
-// Targets are walked in groups of kGroup: one warp-uniform branch per group and kGroup independent
-// evaluations in a straight line, so the MUFU / FMA latencies overlap.  Target coordinates are read with explicit ld.shared from a
-// 32-bit shared address (register + immediate; the generic-pointer form re-derived the address in
-// every group).
+// source-side constants of one lane, broadcast to both halves of a pair
+struct SourceQ {
+  u64 qr, qi, nqi;
+};
+
+// acc += (rinv e^{i r2 rinv}) * q for a pair of targets
+__device__ __forceinline__ void green_accumulate2(u64 r2, u64 rinv, const SourceQ& q, u64& ar, u64& ai) {
+  const float2 r = unpack2(mul2(r2, rinv));
+  const u64 c = pack2(cos_approx(r.x), cos_approx(r.y)), s = pack2(sin_approx(r.x), sin_approx(r.y));
+  const u64 gr = mul2(rinv, c), gi = mul2(rinv, s);
+  ar = fma2(gr, q.qr, ar);
+  ar = fma2(gi, q.nqi, ar);
+  ai = fma2(gr, q.qi, ai);
+  ai = fma2(gi, q.qr, ai);
+}
+
+// Targets are walked in groups of 4 (two pairs): one warp-uniform branch per group, two independent
+// packed evaluations in a straight line.  Target coordinates live in shared memory as one array
+// per axis, so a 16-byte broadcast load brings the four x (y, z) of a group as two pairs.
 constexpr int kGroup = 4;
+constexpr int kPairs = kTile / 2;
 
-__device__ __forceinline__ float4 lds_f4(uint32_t addr) {
-  float4 v;
-  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(addr));
-  return v;
-}
-
-template <int N>
-__device__ __forceinline__ void plain_group(uint32_t tgt, int t0, float sx, float sy, float sz,
-                                            float qr, float qi, float (&ar)[kTile], float (&ai)[kTile]) {
-#pragma unroll
-  for (int j = 0; j < N; ++j) {
-    const float4 tp = lds_f4(tgt + 16 * (t0 + j));
-    const float dx = tp.x - sx, dy = tp.y - sy, dz = tp.z - sz;
-    const float r2 = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, 1e-30f)));
-    green_accumulate(r2, rsqrt_approx(r2), qr, qi, ar[t0 + j], ai[t0 + j]);
-  }
-}
-
-// plain path: one FP32 coordinate per axis.  Slots past n_t inside the last group hold zero
-// coordinates; their accumulators are never stored.
-__device__ __forceinline__ void accumulate_plain(uint32_t tgt, uint32_t n_t, float sx, float sy,
-                                                 float sz, float qr, float qi, float (&ar)[kTile],
-                                                 float (&ai)[kTile]) {
+// plain path: one FP32 coordinate per axis.  nsx = (-sx, -sx) etc.  Slots past n_t inside the last
+// group hold zero coordinates; their accumulators are never stored.
+__device__ __forceinline__ void accumulate_plain(uint32_t tx, uint32_t ty, uint32_t tz, uint32_t n_t,
+                                                 u64 nsx, u64 nsy, u64 nsz, const SourceQ& q,
+                                                 u64 (&ar)[kPairs], u64 (&ai)[kPairs]) {
+  const u64 tiny = pack2(1e-30f, 1e-30f);
 #pragma unroll
   for (int t0 = 0; t0 < kTile; t0 += kGroup)
-    if (t0 < n_t) plain_group<kGroup>(tgt, t0, sx, sy, sz, qr, qi, ar, ai);  // warp-uniform
-}
-
-template <int N>
-__device__ __forceinline__ void compensated_group(uint32_t thi, uint32_t tlo, int t0, float hx, float hy,
-                                                  float hz, float lx, float ly, float lz, float qr,
-                                                  float qi, float (&ar)[kTile], float (&ai)[kTile]) {
+    if (t0 < n_t) {  // warp-uniform
+      u64 x[2], y[2], z[2];
+      lds_2x2(tx + 4 * t0, x[0], x[1]);
+      lds_2x2(ty + 4 * t0, y[0], y[1]);
+      lds_2x2(tz + 4 * t0, z[0], z[1]);
 #pragma unroll
-  for (int j = 0; j < N; ++j) {
-    const float4 th = lds_f4(thi + 16 * (t0 + j)), tl = lds_f4(tlo + 16 * (t0 + j));
-    const float dx = (th.x - hx) + (tl.x - lx);
-    const float dy = (th.y - hy) + (tl.y - ly);
-    const float dz = (th.z - hz) + (tl.z - lz);
-    const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-    const float rinv = r2 > 0.0f ? rsqrt_approx(r2) : 0.0f;
-    green_accumulate(r2, rinv, qr, qi, ar[t0 + j], ai[t0 + j]);
-  }
+      for (int j = 0; j < 2; ++j) {
+        const u64 dx = add2(x[j], nsx), dy = add2(y[j], nsy), dz = add2(z[j], nsz);
+        const u64 r2 = fma2(dz, dz, fma2(dy, dy, fma2(dx, dx, tiny)));
+        const float2 r2s = unpack2(r2);
+        const u64 rinv = pack2(rsqrt_approx(r2s.x), rsqrt_approx(r2s.y));
+        green_accumulate2(r2, rinv, q, ar[t0 / 2 + j], ai[t0 / 2 + j]);
+      }
+    }
 }
 
-// compensated path: d = (hi_t - hi_s) + (lo_t - lo_s); the hi difference is exact (grid multiples)
-__device__ __forceinline__ void accumulate_compensated(uint32_t thi, uint32_t tlo, uint32_t n_t, float hx,
-                                                       float hy, float hz, float lx, float ly, float lz,
-                                                       float qr, float qi, float (&ar)[kTile],
-                                                       float (&ai)[kTile]) {
+// compensated path: d = (hi_t - hi_s) + (lo_t - lo_s); the hi difference is exact (grid multiples);
+// coincident bodies (R == 0) are masked
+__device__ __forceinline__ void accumulate_compensated(uint32_t thi, uint32_t tlo, uint32_t n_t, u64 nhx,
+                                                       u64 nhy, u64 nhz, u64 nlx, u64 nly, u64 nlz,
+                                                       const SourceQ& q, u64 (&ar)[kPairs],
+                                                       u64 (&ai)[kPairs]) {
 #pragma unroll
   for (int t0 = 0; t0 < kTile; t0 += kGroup)
-    if (t0 < n_t) compensated_group<kGroup>(thi, tlo, t0, hx, hy, hz, lx, ly, lz, qr, qi, ar, ai);
+    if (t0 < n_t) {
+      u64 hx[2], hy[2], hz[2], lx[2], ly[2], lz[2];
+      lds_2x2(thi + 4 * t0, hx[0], hx[1]);
+      lds_2x2(thi + 4 * (kTile + t0), hy[0], hy[1]);
+      lds_2x2(thi + 4 * (2 * kTile + t0), hz[0], hz[1]);
+      lds_2x2(tlo + 4 * t0, lx[0], lx[1]);
+      lds_2x2(tlo + 4 * (kTile + t0), ly[0], ly[1]);
+      lds_2x2(tlo + 4 * (2 * kTile + t0), lz[0], lz[1]);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const u64 dx = add2(add2(hx[j], nhx), add2(lx[j], nlx));
+        const u64 dy = add2(add2(hy[j], nhy), add2(ly[j], nly));
+        const u64 dz = add2(add2(hz[j], nhz), add2(lz[j], nlz));
+        const u64 r2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
+        const float2 r2s = unpack2(r2);
+        const u64 rinv = pack2(r2s.x > 0.0f ? rsqrt_approx(r2s.x) : 0.0f, r2s.y > 0.0f ? rsqrt_approx(r2s.y) : 0.0f);
+        green_accumulate2(r2, rinv, q, ar[t0 / 2 + j], ai[t0 / 2 + j]);
+      }
+    }
 }
 
 struct LeafGroup {
@@ -150,9 +188,10 @@ __device__ __forceinline__ int owner_of(uint32_t incl, uint32_t g) {
 
 // 128 registers per thread keep four CTAs (16 warps) per SM; measured: 134 registers (3 CTAs) cost 40 %
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) p2p_kernel(const P2PArgs a) {
-  __shared__ float4 s_tgt[kWarpsPerBlock][kTile];
-  __shared__ float4 s_thi[kWarpsPerBlock][kTile];
-  __shared__ float4 s_tlo[kWarpsPerBlock][kTile];
+  // target coordinates, one array per axis: [x | y | z][kTile]
+  __shared__ __align__(16) float s_tgt[kWarpsPerBlock][3 * kTile];
+  __shared__ __align__(16) float s_thi[kWarpsPerBlock][3 * kTile];
+  __shared__ __align__(16) float s_tlo[kWarpsPerBlock][3 * kTile];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t tile_id = blockIdx.x * kWarpsPerBlock + warp;
   if (tile_id >= a.n_tiles) return;
@@ -162,17 +201,21 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) p2p_kernel(const P2PAr
   const uint2 tb = a.cell_body[tile.leaf];
   const uint32_t tslot = tb.x + tile.body_off + lane;
   const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  s_tgt[warp][lane] = lane < tile.n_t ? a.body_pos[tslot] : zero4;
-  s_thi[warp][lane] = lane < tile.n_t ? a.body_hi[tslot] : zero4;
-  s_tlo[warp][lane] = lane < tile.n_t ? a.body_lo[tslot] : zero4;
+  {
+    const float4 tp = lane < tile.n_t ? a.body_pos[tslot] : zero4, th = lane < tile.n_t ? a.body_hi[tslot] : zero4,
+                 tl = lane < tile.n_t ? a.body_lo[tslot] : zero4;
+    s_tgt[warp][lane] = tp.x; s_tgt[warp][kTile + lane] = tp.y; s_tgt[warp][2 * kTile + lane] = tp.z;
+    s_thi[warp][lane] = th.x; s_thi[warp][kTile + lane] = th.y; s_thi[warp][2 * kTile + lane] = th.z;
+    s_tlo[warp][lane] = tl.x; s_tlo[warp][kTile + lane] = tl.y; s_tlo[warp][2 * kTile + lane] = tl.z;
+  }
   __syncwarp();
   const uint32_t a_tgt = uint32_t(__cvta_generic_to_shared(s_tgt[warp])),
                  a_thi = uint32_t(__cvta_generic_to_shared(s_thi[warp])),
                  a_tlo = uint32_t(__cvta_generic_to_shared(s_tlo[warp]));
 
-  float ar[kTile], ai[kTile];
+  u64 ar[kPairs], ai[kPairs];  // accumulators of targets (2j, 2j+1)
 #pragma unroll
-  for (int t = 0; t < kTile; ++t) ar[t] = ai[t] = 0.0f;
+  for (int t = 0; t < kPairs; ++t) ar[t] = ai[t] = 0ull;
 
   const uint32_t lb = a.p2p_offset[tile.list], lsplit = a.p2p_split[tile.list],
                  le = a.p2p_offset[tile.list + 1];
@@ -209,8 +252,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) p2p_kernel(const P2PAr
       const float4 sh = ok ? a.body_hi[slot] : make_float4(1e4f, 1e4f, 1e4f, 0.f);
       const float4 sl = ok ? a.body_lo[slot] : zero4;
       const float2 q = ok ? a.body_q[slot] : make_float2(0.f, 0.f);
-      accumulate_compensated(a_thi, a_tlo, tile.n_t, sh.x + hxj, sh.y + hyj, sh.z + hzj,
-                             sl.x + lxj, sl.y + lyj, sl.z + lzj, q.x, q.y, ar, ai);
+      const float hx = -(sh.x + hxj), hy = -(sh.y + hyj), hz = -(sh.z + hzj);
+      const float lx = -(sl.x + lxj), ly = -(sl.y + lyj), lz = -(sl.z + lzj);
+      const SourceQ sq{pack2(q.x, q.x), pack2(q.y, q.y), pack2(-q.y, -q.y)};
+      accumulate_compensated(a_thi, a_tlo, tile.n_t, pack2(hx, hx), pack2(hy, hy), pack2(hz, hz),
+                             pack2(lx, lx), pack2(ly, ly), pack2(lz, lz), sq, ar, ai);
     }
   }
 
@@ -239,7 +285,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) p2p_kernel(const P2PAr
       const uint32_t slot = first_j + (g - excl_j);
       const float4 sp = ok ? a.body_pos[slot] : make_float4(1e4f, 1e4f, 1e4f, 0.f);
       const float2 q = ok ? a.body_q[slot] : make_float2(0.f, 0.f);
-      accumulate_plain(a_tgt, tile.n_t, sp.x + oxj, sp.y + oyj, sp.z + ozj, q.x, q.y, ar, ai);
+      const float sx = -(sp.x + oxj), sy = -(sp.y + oyj), sz = -(sp.z + ozj);
+      const SourceQ sq{pack2(q.x, q.x), pack2(q.y, q.y), pack2(-q.y, -q.y)};
+      accumulate_plain(a_tgt, a_tgt + 4 * kTile, a_tgt + 8 * kTile, tile.n_t, pack2(sx, sx), pack2(sy, sy),
+                       pack2(sz, sz), sq, ar, ai);
     }
   }
 
@@ -248,7 +297,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) p2p_kernel(const P2PAr
 #pragma unroll
   for (int t = 0; t < kTile; ++t) {
     if (t < tile.n_t) {
-      float vr = ar[t], vi = ai[t];
+      const float2 pr = unpack2(ar[t / 2]), pi = unpack2(ai[t / 2]);
+      float vr = (t & 1) ? pr.y : pr.x, vi = (t & 1) ? pi.y : pi.x;
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) {
         vr += __shfl_xor_sync(0xffffffffu, vr, o);
