@@ -1035,3 +1035,224 @@ void ho_block_lu_solve(long npatch, int ni, const double* block_lu, const int* b
     }
   }
 }
+
+/* ============================ correction builders ==========================================
+ * ref: src/solver.cpp:78-230 (build_patch_blocks, build_near_corrections), src/geometry.cpp:9-45
+ * (centroid, diameter, shape6, map_to_physical), include/hfmm/kernel.hpp:16-23 (green_t). */
+typedef struct { double x, y, z; } v3;
+
+/* ref: geometry.cpp:22-27, 40-45 */
+static v3 hc_map(const double* node, double z, double e) {
+  const double l1 = 1.0 - z - e, l2 = z, l3 = e;
+  const double n[6] = {l1 * (2 * l1 - 1), l2 * (2 * l2 - 1), l3 * (2 * l3 - 1), 4 * l1 * l2, 4 * l2 * l3, 4 * l3 * l1};
+  v3 r = {0, 0, 0};
+  for (int k = 0; k < 6; ++k) {
+    r.x += n[k] * node[3 * k];
+    r.y += n[k] * node[3 * k + 1];
+    r.z += n[k] * node[3 * k + 2];
+  }
+  return r;
+}
+/* ref: geometry.cpp:9-20 */
+static double hc_diameter(const double* node) {
+  v3 c = {0, 0, 0};
+  for (int k = 0; k < 6; ++k) { c.x += node[3 * k]; c.y += node[3 * k + 1]; c.z += node[3 * k + 2]; }
+  c.x /= 6.0; c.y /= 6.0; c.z /= 6.0;
+  double r = 0;
+  for (int k = 0; k < 6; ++k) {
+    const double dx = node[3 * k] - c.x, dy = node[3 * k + 1] - c.y, dz = node[3 * k + 2] - c.z;
+    const double d = sqrt(dx * dx + dy * dy + dz * dz);
+    if (d > r) r = d;
+  }
+  return 2.0 * r;
+}
+/* ref: kernel.hpp:16-23 */
+static zc hc_green(v3 a, v3 b, double kr, double ki) {
+  const double dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z;
+  const double R = sqrt(dx * dx + dy * dy + dz * dz);
+  const double amp = exp(-ki * R) / (4.0 * HO_PI * R);
+  const double ph = kr * R;
+  return amp * cos(ph) + I * (amp * sin(ph));
+}
+static double hc_norm2(v3 a, v3 b) {
+  const double dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z;
+  return dx * dx + dy * dy + dz * dz;
+}
+/* ref: solver.cpp:40-43 */
+static double hc_threshold(const ho_correction_rules* r, size_t patch) {
+  return r->near_patch_distance < 0 ? 2.0 * hc_diameter(r->nodes + 18 * patch) : r->near_patch_distance;
+}
+
+void ho_correction_samples(const ho_correction_rules* r, double* xyz) {
+  const int ni = r->basis_count;
+  for (size_t p = 0; p < r->n_patches; ++p)
+    for (int j = 0; j < ni; ++j) {
+      const v3 v = hc_map(r->nodes + 18 * p, r->sample_ref[2 * j], r->sample_ref[2 * j + 1]);
+      xyz[3 * (p * ni + j)] = v.x;
+      xyz[3 * (p * ni + j) + 1] = v.y;
+      xyz[3 * (p * ni + j) + 2] = v.z;
+    }
+}
+
+/* ref: solver.cpp:45-62 */
+static int hc_lu_factor(zc* a, int* piv, int n) {
+  for (int c = 0; c < n; ++c) {
+    int best = c;
+    for (int r = c + 1; r < n; ++r)
+      if (cabs(a[r * n + c]) > cabs(a[best * n + c])) best = r;
+    piv[c] = best;
+    if (best != c)
+      for (int m = 0; m < n; ++m) { zc t = a[c * n + m]; a[c * n + m] = a[best * n + m]; a[best * n + m] = t; }
+    if (a[c * n + c] == 0) return 1;
+    for (int r = c + 1; r < n; ++r) {
+      a[r * n + c] /= a[c * n + c];
+      for (int m = c + 1; m < n; ++m) a[r * n + m] -= a[r * n + c] * a[c * n + m];
+    }
+  }
+  return 0;
+}
+
+/* ref: solver.cpp:80-128 */
+int ho_build_patch_blocks(const ho_correction_rules* r, double kr, double ki, double* patch_block,
+                          double* block_lu, int* block_piv) {
+  const int ni = r->basis_count;
+  const int self_terms = r->mode != 0;
+  zc* PB = (zc*)patch_block;
+  zc* LU = (zc*)block_lu;
+  int singular = 0;
+  size_t* first = (size_t*)malloc(sizeof(size_t) * (ni + 1));
+  first[0] = 0;
+  for (int j = 0; j < ni; ++j) first[j + 1] = first[j] + (self_terms ? (size_t)r->self_npts[j] : 0);
+  for (size_t p = 0; p < r->n_patches; ++p) {
+    const double* node = r->nodes + 18 * p;
+    zc* block = PB + p * ni * ni;
+    v3 s[16];
+    for (int j = 0; j < ni; ++j) s[j] = hc_map(node, r->sample_ref[2 * j], r->sample_ref[2 * j + 1]);
+    for (int j = 0; j < ni; ++j) {
+      for (int n = 0; n < ni; ++n) {
+        block[j * ni + n] = 0;
+        if (hc_norm2(s[j], s[n]) > 0.0) block[j * ni + n] -= hc_green(s[j], s[n], kr, ki) * r->far_weight[n];
+      }
+      if (!self_terms) continue;
+      zc* row = LU + (p * (size_t)ni + j) * ni;
+      for (int n = 0; n < ni; ++n) row[n] = 0;
+      const v3 obs = s[j];
+      for (size_t q = first[j]; q < first[j + 1]; ++q) {
+        const v3 rp = hc_map(node, r->self_pts[3 * q], r->self_pts[3 * q + 1]);
+        if (hc_norm2(obs, rp) == 0.0) continue;
+        const zc g = hc_green(obs, rp, kr, ki);
+        const double w = r->self_pts[3 * q + 2];
+        for (int n = 0; n < ni; ++n) row[n] += w * r->self_basis[q * ni + n] * g;
+      }
+      for (int n = 0; n < ni; ++n) block[j * ni + n] += row[n];
+    }
+    if (self_terms) singular |= hc_lu_factor(LU + p * (size_t)ni * ni, block_piv + p * ni, ni);
+  }
+  free(first);
+  return singular;
+}
+
+/* ref: solver.cpp:13-17 */
+static unsigned long long hc_cell_key(long long cx, long long cy, long long cz) {
+  const unsigned long long mask = (1ull << 21) - 1;
+  return (((unsigned long long)cx & mask) << 42) | (((unsigned long long)cy & mask) << 21) | ((unsigned long long)cz & mask);
+}
+typedef struct { unsigned long long key; unsigned idx; } hc_entry;
+static int hc_entry_cmp(const void* a, const void* b) {
+  const hc_entry* x = (const hc_entry*)a; const hc_entry* y = (const hc_entry*)b;
+  if (x->key != y->key) return x->key < y->key ? -1 : 1;
+  return x->idx < y->idx ? -1 : (x->idx > y->idx);
+}
+static int hc_u32_cmp(const void* a, const void* b) {
+  const unsigned x = *(const unsigned*)a, y = *(const unsigned*)b;
+  return x < y ? -1 : (x > y);
+}
+
+/* ref: solver.cpp:132-186 (the hash grid is replaced by a sorted key array: same candidate sets) */
+long ho_build_near_lists(const ho_correction_rules* r, unsigned* near_offset, unsigned** near_source) {
+  const int ni = r->basis_count;
+  const size_t n = (size_t)r->n_patches * ni;
+  for (size_t i = 0; i <= n; ++i) near_offset[i] = 0;
+  *near_source = NULL;
+  if (r->mode != 2) return 0;
+  double* thr = (double*)malloc(sizeof(double) * (r->n_patches ? r->n_patches : 1));
+  double h = 0;
+  for (size_t p = 0; p < r->n_patches; ++p) { thr[p] = hc_threshold(r, p); if (thr[p] > h) h = thr[p]; }
+  if (h <= 0.0) { free(thr); return 0; }
+  double* xyz = (double*)malloc(sizeof(double) * 3 * (n ? n : 1));
+  ho_correction_samples(r, xyz);
+  hc_entry* grid = (hc_entry*)malloc(sizeof(hc_entry) * (n ? n : 1));
+  for (size_t i = 0; i < n; ++i) {
+    grid[i].key = hc_cell_key((long long)floor(xyz[3 * i] / h), (long long)floor(xyz[3 * i + 1] / h), (long long)floor(xyz[3 * i + 2] / h));
+    grid[i].idx = (unsigned)i;
+  }
+  qsort(grid, n, sizeof(hc_entry), hc_entry_cmp);
+  size_t cap = 1024, nnz = 0;
+  unsigned* out = (unsigned*)malloc(sizeof(unsigned) * cap);
+  for (size_t m = 0; m < n; ++m) {
+    const size_t begin = nnz;
+    const v3 t = {xyz[3 * m], xyz[3 * m + 1], xyz[3 * m + 2]};
+    const long long cx = (long long)floor(t.x / h), cy = (long long)floor(t.y / h), cz = (long long)floor(t.z / h);
+    for (long long dx = -1; dx <= 1; ++dx)
+      for (long long dy = -1; dy <= 1; ++dy)
+        for (long long dz = -1; dz <= 1; ++dz) {
+          const unsigned long long key = hc_cell_key(cx + dx, cy + dy, cz + dz);
+          size_t lo = 0, hi = n;
+          while (lo < hi) { const size_t mid = (lo + hi) / 2; if (grid[mid].key < key) lo = mid + 1; else hi = mid; }
+          for (size_t e = lo; e < n && grid[e].key == key; ++e) {
+            const unsigned s = grid[e].idx;
+            if (s / ni == m / ni) continue;
+            const v3 sp = {xyz[3 * s], xyz[3 * s + 1], xyz[3 * s + 2]};
+            const double r2 = hc_norm2(t, sp);
+            if (r2 == 0.0) continue;
+            const double th = thr[s / ni];
+            if (th > 0.0 && r2 <= th * th) {
+              if (nnz == cap) { cap *= 2; out = (unsigned*)realloc(out, sizeof(unsigned) * cap); }
+              out[nnz++] = s;
+            }
+          }
+        }
+    qsort(out + begin, nnz - begin, sizeof(unsigned), hc_u32_cmp);
+    near_offset[m + 1] = (unsigned)nnz;
+  }
+  free(thr); free(xyz); free(grid);
+  *near_source = out;
+  return (long)nnz;
+}
+
+/* ref: solver.cpp:194-230 */
+void ho_build_near_deltas(const ho_correction_rules* r, double kr, double ki, const unsigned* near_offset,
+                          const unsigned* near_source, double* near_delta) {
+  const int ni = r->basis_count;
+  const size_t n = (size_t)r->n_patches * ni;
+  zc* D = (zc*)near_delta;
+  double* xyz = (double*)malloc(sizeof(double) * 3 * (n ? n : 1));
+  ho_correction_samples(r, xyz);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (long m = 0; m < (long)n; ++m) {
+    zc acc[16];
+    const v3 t = {xyz[3 * m], xyz[3 * m + 1], xyz[3 * m + 2]};
+    unsigned idx = near_offset[m];
+    while (idx < near_offset[m + 1]) {
+      const unsigned sp = near_source[idx] / (unsigned)ni;
+      unsigned end = idx + 1;
+      while (end < near_offset[m + 1] && near_source[end] / (unsigned)ni == sp) ++end;
+      const double* node = r->nodes + 18 * (size_t)sp;
+      for (int nn = 0; nn < ni; ++nn) acc[nn] = 0;
+      for (int q = 0; q < r->near_npts; ++q) {
+        const v3 rp = hc_map(node, r->near_pts[3 * q], r->near_pts[3 * q + 1]);
+        const zc g = hc_green(t, rp, kr, ki);
+        const double w = r->near_pts[3 * q + 2];
+        for (int nn = 0; nn < ni; ++nn) acc[nn] += w * r->near_basis[q * ni + nn] * g;
+      }
+      for (; idx < end; ++idx) {
+        const unsigned s = near_source[idx];
+        const v3 sx = {xyz[3 * s], xyz[3 * s + 1], xyz[3 * s + 2]};
+        D[idx] = acc[s % (unsigned)ni] - hc_green(t, sx, kr, ki) * r->far_weight[s % (unsigned)ni];
+      }
+    }
+  }
+  free(xyz);
+}
+
+void ho_free(void* p) { free(p); }

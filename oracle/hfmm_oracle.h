@@ -66,6 +66,36 @@ void ho_apply_corrections(long n, int ni, const double* patch_block, const unsig
 void ho_block_lu_solve(long npatch, int ni, const double* block_lu, const int* block_piv,
                        double* x);
 
+
+/* ---- correction builders (setup of the BIE operator; ref: src/solver.cpp:78-230) ---------------
+ * The quadrature / interpolation tables are geometry.cpp's, passed in by the caller; field for
+ * field the layout of hfmm_correction_rules in include/hfmm_cuda.h. */
+typedef struct {
+  int basis_count;
+  int mode; /* 0 none, 1 self_only, 2 self_near */
+  unsigned long long n_patches;
+  const double* nodes;      /* n_patches x 6 x 3 */
+  const double* sample_ref; /* ni x 2 */
+  const double* far_weight; /* ni */
+  double near_patch_distance;
+  int near_npts;
+  const double* near_pts;   /* near_npts x 3 */
+  const double* near_basis; /* near_npts x ni */
+  const int* self_npts;     /* ni */
+  const double* self_pts;
+  const double* self_basis;
+} ho_correction_rules;
+/* sample positions (build_system, solver.cpp:283-294): xyz[n_patches * ni][3] */
+void ho_correction_samples(const ho_correction_rules* r, double* xyz);
+/* returns 0, or 1 when a self block is singular; block_lu / block_piv may be null when mode == 0 */
+int ho_build_patch_blocks(const ho_correction_rules* r, double kr, double ki, double* patch_block,
+                          double* block_lu, int* block_piv);
+/* near_offset[n + 1]; *near_source is malloc'd (release with ho_free); returns nnz */
+long ho_build_near_lists(const ho_correction_rules* r, unsigned* near_offset, unsigned** near_source);
+void ho_build_near_deltas(const ho_correction_rules* r, double kr, double ki, const unsigned* near_offset,
+                          const unsigned* near_source, double* near_delta);
+void ho_free(void* p);
+
 #ifdef __cplusplus
 }
 #endif

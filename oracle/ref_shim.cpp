@@ -435,4 +435,42 @@ int ref_mie_soft_sphere(double radius, double kr, double ki, long nobs, const do
   });
 }
 
+// quadrature / interpolation tables of geometry.cpp, the inputs of the correction builders
+// (solver.cpp:80-230): exported so tests can hand the reference's own rules to the device builder
+int ref_geom_basis(int order, double* nodes, double* weights) {
+  const auto& b = geom::lagrange_basis(order);
+  for (int j = 0; j < b.count(); ++j) {
+    if (nodes) {
+      nodes[2 * j] = b.nodes()[j][0];
+      nodes[2 * j + 1] = b.nodes()[j][1];
+    }
+    if (weights) weights[j] = b.weights()[j];
+  }
+  return b.count();
+}
+void ref_geom_basis_eval(int order, double zeta, double eta, double* out) {
+  const auto v = geom::lagrange_basis(order).eval(zeta, eta);
+  std::memcpy(out, v.data(), sizeof(double) * v.size());
+}
+int ref_geom_gauss_rule(int npoints, double* pts) {  // pts: npoints x (zeta, eta, weight)
+  const auto& r = geom::gauss_rule(npoints);
+  if (pts)
+    for (size_t i = 0; i < r.pts.size(); ++i) {
+      pts[3 * i] = r.pts[i].zeta;
+      pts[3 * i + 1] = r.pts[i].eta;
+      pts[3 * i + 2] = r.pts[i].weight;
+    }
+  return int(r.pts.size());
+}
+int ref_geom_duffy_rule(double zeta0, double eta0, int n_per_dim, double* pts) {
+  const auto r = geom::duffy_rule(zeta0, eta0, n_per_dim);
+  if (pts)
+    for (size_t i = 0; i < r.size(); ++i) {
+      pts[3 * i] = r[i].zeta;
+      pts[3 * i + 1] = r[i].eta;
+      pts[3 * i + 2] = r[i].weight;
+    }
+  return int(r.size());
+}
+
 }  // extern "C"

@@ -68,6 +68,31 @@ class _GmresReport(C.Structure):
                 ("matvec_seconds", C.c_double)]
 
 
+class CorrectionRules(C.Structure):
+    """hfmm_correction_rules (include/hfmm_cuda.h): the inputs of the correction builders"""
+    _fields_ = [("basis_count", C.c_int), ("mode", C.c_int), ("n_patches", C.c_uint64),
+                ("nodes", C.c_void_p), ("sample_ref", C.c_void_p), ("far_weight", C.c_void_p),
+                ("near_patch_distance", C.c_double), ("near_npts", C.c_int),
+                ("near_pts", C.c_void_p), ("near_basis", C.c_void_p), ("self_npts", C.c_void_p),
+                ("self_pts", C.c_void_p), ("self_basis", C.c_void_p)]
+
+
+def make_correction_rules(patches, tables, mode=2, near_patch_distance=-1.0):
+    """patches: (n_patches, 6, 3); tables: dict with sample_ref (ni, 2), far_weight (ni,), near_pts
+    (q, 3), near_basis (q, ni), self_npts (ni,), self_pts (sum, 3), self_basis (sum, ni) — the
+    reference's geometry.cpp rules.  Returns (struct, keep-alive list)."""
+    f8 = lambda a: np.ascontiguousarray(a, dtype=np.float64)
+    keep = [f8(patches), f8(tables["sample_ref"]), f8(tables["far_weight"]), f8(tables["near_pts"]),
+            f8(tables["near_basis"]), np.ascontiguousarray(tables["self_npts"], dtype=np.int32),
+            f8(tables["self_pts"]), f8(tables["self_basis"])]
+    ptr = lambda a: a.ctypes.data_as(C.c_void_p) if a.size else None
+    ni = int(keep[2].shape[0])
+    r = CorrectionRules(ni, int(mode), int(keep[0].shape[0]), ptr(keep[0]), ptr(keep[1]), ptr(keep[2]),
+                        float(near_patch_distance), int(keep[3].shape[0]), ptr(keep[3]), ptr(keep[4]),
+                        ptr(keep[5]), ptr(keep[6]), ptr(keep[7]))
+    return r, keep
+
+
 ALLREDUCE_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_double), C.c_int)
 GATHER_VECTOR_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
 GATHER_MULTIPOLES_FN = C.CFUNCTYPE(None, C.c_void_p)

@@ -181,6 +181,9 @@ class Oracle(_Base):
     def __init__(self):
         self.lib = C.CDLL(build_oracle())
 
+    def build_corrections(self, patches, tables, k, mode=2, near_patch_distance=-1.0):
+        return _oracle_build_corrections(self.lib, patches, tables, k, mode, near_patch_distance)
+
     def sph_jn(self, nmax, z):
         out = np.zeros(nmax + 1)
         self.lib.ho_sph_jn(nmax, C.c_double(z), _d(out))
@@ -263,8 +266,66 @@ class _VoidLib:
         return getattr(self._lib, name)
 
 
+def _oracle_build_corrections(lib, patches, tables, k, mode=2, near_patch_distance=-1.0):
+    from paper_1803_09948_b200.api import make_correction_rules
+    r, keep = make_correction_rules(patches, tables, mode, near_patch_distance)
+    ni, npatch = r.basis_count, int(r.n_patches)
+    n = ni * npatch
+    xyz = np.zeros((n, 3))
+    lib.ho_correction_samples(C.byref(r), _d(xyz))
+    pb = np.zeros(npatch * ni * ni, dtype=np.complex128)
+    lu = np.zeros(npatch * ni * ni if mode else 0, dtype=np.complex128)
+    piv = np.zeros(npatch * ni if mode else 0, dtype=np.int32)
+    vp = lambda a: a.ctypes.data_as(C.c_void_p) if a.size else None
+    lib.ho_build_patch_blocks.restype = C.c_int
+    rc = lib.ho_build_patch_blocks(C.byref(r), C.c_double(k), C.c_double(0.0), vp(pb), vp(lu), vp(piv))
+    assert rc == 0, "singular self block"
+    off = np.zeros(n + 1, dtype=np.uint32)
+    srcp = C.POINTER(C.c_uint32)()
+    lib.ho_build_near_lists.restype = C.c_long
+    nnz = lib.ho_build_near_lists(C.byref(r), vp(off), C.byref(srcp))
+    src = np.ctypeslib.as_array(srcp, shape=(nnz,)).copy() if nnz else np.zeros(0, dtype=np.uint32)
+    if nnz:
+        lib.ho_free(srcp)
+    dl = np.zeros(nnz, dtype=np.complex128)
+    if nnz:
+        lib.ho_build_near_deltas(C.byref(r), C.c_double(k), C.c_double(0.0), vp(off), vp(src), vp(dl))
+    return dict(xyz=xyz, patch_block=pb, block_lu=lu, block_piv=piv, near_offset=off, near_source=src,
+                near_delta=dl)
+
+
 class Ref(_Base):
     prefix = "ref"
+
+    def correction_tables(self, basis_order, near_rule=25, self_rule=8):
+        """geometry.cpp's interpolation / quadrature tables in the layout of hfmm_correction_rules"""
+        L = self.lib
+        ni = L.ref_geom_basis(basis_order, None, None)
+        nodes, w = np.zeros((ni, 2)), np.zeros(ni)
+        L.ref_geom_basis(basis_order, _d(nodes), _d(w))
+
+        def basis_at(pts):
+            out = np.zeros((len(pts), ni))
+            for i, (z, e, _) in enumerate(pts):
+                row = np.zeros(ni)
+                L.ref_geom_basis_eval(basis_order, C.c_double(z), C.c_double(e), _d(row))
+                out[i] = row
+            return out
+
+        nq = L.ref_geom_gauss_rule(near_rule, None)
+        near = np.zeros((nq, 3))
+        L.ref_geom_gauss_rule(near_rule, _d(near))
+        self_pts, self_npts = [], []
+        for j in range(ni):
+            m = L.ref_geom_duffy_rule(C.c_double(nodes[j, 0]), C.c_double(nodes[j, 1]), self_rule, None)
+            p = np.zeros((m, 3))
+            L.ref_geom_duffy_rule(C.c_double(nodes[j, 0]), C.c_double(nodes[j, 1]), self_rule, _d(p))
+            self_pts.append(p)
+            self_npts.append(m)
+        self_pts = np.concatenate(self_pts)
+        return dict(sample_ref=nodes, far_weight=w, near_pts=near, near_basis=basis_at(near),
+                    self_npts=np.array(self_npts, dtype=np.int32), self_pts=self_pts,
+                    self_basis=basis_at(self_pts))
 
     def __init__(self):
         if not have_ref():

@@ -112,7 +112,15 @@ def gmres_and_bie():
                bie_residuals=rep2["residuals"], bie_sol_noprec=sol0,
                bie_iterations_noprec=rep0["iterations"], bie_obs=obs, bie_scattered=scat,
                bie_order=8, bie_ni=sysr.ni, **{f"bie_{k_}": v for k_, v in corr.items()})
+    # inputs of the correction builders (solver.cpp:80-230): geometry.cpp's tables for the basis above
+    out.update({f"bie_rule_{k_}": v for k_, v in R.correction_tables(1).items()})
     np.savez_compressed(os.path.join(HERE, "solver.npz"), **out)
+    # second-order basis (6 functions per patch) on the 20-triangle icosphere: corrections only
+    p2 = icosphere_patches(0)
+    sys2 = R.bie(p2, 2, 1.5, mode=2, use_tree=False, order=6, ncrit=16, theta=0.4, kd_max=1.0)
+    o2 = dict(patches=p2, k=1.5, xyz=sys2.samples()[0], **sys2.corrections())
+    o2.update({f"rule_{k_}": v for k_, v in R.correction_tables(2).items()})
+    np.savez_compressed(os.path.join(HERE, "corrections_order2.npz"), **o2)
 
 
 if __name__ == "__main__":

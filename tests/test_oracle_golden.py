@@ -145,3 +145,27 @@ def test_operator_tail_and_preconditioner_match_reference_fixture(oracle):
     sol = oracle.block_lu_solve(ni, g["bie_block_lu"], g["bie_block_piv"], u)
     assert rep["iterations"] == int(g["bie_iterations"])
     assert rel_l2(sol, g["bie_sol"]) < 1e-9
+
+
+def _tables(g, prefix):
+    keys = ("sample_ref", "far_weight", "near_pts", "near_basis", "self_npts", "self_pts", "self_basis")
+    return {k: g[prefix + k] for k in keys}
+
+
+@pytest.mark.parametrize("case", ["order1", "order2"])
+def test_correction_builders_match_reference_fixture(oracle, case):
+    """build_patch_blocks / build_near_corrections (solver.cpp:80-230) restated in the oracle against
+    arrays the reference produced; the quadrature tables are the reference's (stored with the fixture)"""
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    if case == "order1":
+        g = np.load(os.path.join(here, "solver.npz"))
+        patches, k, tables, pre = g["bie_patches"], float(g["bie_k"]), _tables(g, "bie_rule_"), "bie_"
+    else:
+        g = np.load(os.path.join(here, "corrections_order2.npz"))
+        patches, k, tables, pre = g["patches"], float(g["k"]), _tables(g, "rule_"), ""
+    got = oracle.build_corrections(patches, tables, k)
+    assert np.array_equal(got["xyz"], g[pre + "xyz"])
+    for key in ("near_offset", "near_source", "block_piv"):
+        assert np.array_equal(got[key], g[pre + key]), key
+    for key in ("patch_block", "block_lu", "near_delta"):
+        assert np.abs(got[key] - g[pre + key]).max() <= 1e-15 * np.abs(g[pre + key]).max(), key
