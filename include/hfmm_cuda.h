@@ -190,6 +190,35 @@ int hfmm_cuda_dist_upward(hfmm_cuda_t* h, const void* q_morton_dev);
 /* out_morton_dev: n float2 in Morton order; only the owned slots are written */
 int hfmm_cuda_dist_downward(hfmm_cuda_t* h, void* out_morton_dev);
 
+/* ---- correction builders on the device ------------------------------
+ * Replace build_patch_blocks (proj/core/src/solver.cpp:80-128) and build_near_corrections
+ * (solver.cpp:132-230).  The quadrature and interpolation tables are the reference's own
+ * (geom::lagrange_basis, geom::gauss_rule, geom::duffy_rule of geometry.cpp), passed as arrays. */
+typedef struct {
+  int basis_count;            /* LagrangeBasis::count(): 3, 6 or 12 */
+  int mode;                   /* SingularityMode: 0 none, 1 self_only, 2 self_near */
+  uint64_t n_patches;
+  const double* nodes;        /* n_patches x 6 x 3: CurvilinearPatch::node (geometry.hpp:14-15) */
+  const double* sample_ref;   /* basis_count x (zeta, eta): LagrangeBasis::nodes() */
+  const double* far_weight;   /* basis_count: LagrangeBasis::weights() */
+  double near_patch_distance; /* KernelConfig::near_patch_distance; < 0: twice the patch diameter */
+  int near_npts;              /* gauss_rule(KernelConfig::near_rule) */
+  const double* near_pts;     /* near_npts x (zeta, eta, weight) */
+  const double* near_basis;   /* near_npts x basis_count: basis.eval at the rule points */
+  const int32_t* self_npts;   /* basis_count: size of duffy_rule centred on interpolation node j */
+  const double* self_pts;     /* the Duffy rules, concatenated: sum(self_npts) x (zeta, eta, weight) */
+  const double* self_basis;   /* sum(self_npts) x basis_count */
+} hfmm_correction_rules;
+/* Requires hfmm_cuda_set_points on the samples (patch-major: sample p * basis_count + j is
+ * interpolation node j of patch p, solver.cpp:283-294).  Builds the arrays in FP64 on the device and
+ * installs them as the handle's corrections (as hfmm_cuda_set_corrections would); *near_nnz receives
+ * the length of the near CSR.  singular_error when a self block is singular (solver.cpp:55-56). */
+int hfmm_cuda_build_corrections(hfmm_cuda_t* h, const hfmm_correction_rules* rules, uint64_t* near_nnz);
+/* the FP64 arrays of the last build, in the reference's layout (DiscreteSystem, solver.hpp:60-90);
+ * any pointer may be null */
+int hfmm_cuda_get_corrections(hfmm_cuda_t* h, double* patch_block, double* block_lu, int32_t* block_piv,
+                              uint32_t* near_offset, uint32_t* near_source, double* near_delta);
+
 /* Restarted GMRES over Morton-sharded vectors: every rank holds the slice
  * [body_first, body_first + body_count) of each Krylov vector; inner products are local FP64
  * reductions followed by `allreduce_sum`; the operator is the two-phase matvec above.  The three

@@ -318,6 +318,27 @@ class HfmmCuda:
                        final_residual=rep.final_residual, seconds=rep.seconds,
                        matvec_seconds=rep.matvec_seconds, residuals=res[:rep.iterations].copy())
 
+    def build_corrections(self, patches, tables, mode=2, near_patch_distance=-1.0, fetch=True):
+        """Correction arrays built on the device from the patches and the reference's rule tables
+        (see make_correction_rules) and installed as this operator's corrections."""
+        r, keep = make_correction_rules(patches, tables, mode, near_patch_distance)
+        nnz = C.c_uint64(0)
+        self._check(self.lib.hfmm_cuda_build_corrections(self.h, C.byref(r), C.byref(nnz)))
+        nnz = int(nnz.value)
+        if not fetch:
+            return nnz
+        ni, npatch = r.basis_count, int(r.n_patches)
+        n = ni * npatch
+        pb = np.zeros(n * ni, dtype=np.complex128)
+        lu = np.zeros(n * ni if mode else 0, dtype=np.complex128)
+        piv = np.zeros(n if mode else 0, dtype=np.int32)
+        off = np.zeros(n + 1, dtype=np.uint32)
+        src = np.zeros(nnz, dtype=np.uint32)
+        dl = np.zeros(nnz, dtype=np.complex128)
+        vp = lambda a: a.ctypes.data_as(C.c_void_p) if a.size else None
+        self._check(self.lib.hfmm_cuda_get_corrections(self.h, vp(pb), vp(lu), vp(piv), vp(off), vp(src), vp(dl)))
+        return dict(patch_block=pb, block_lu=lu, block_piv=piv, near_offset=off, near_source=src, near_delta=dl)
+
     def evaluate_field(self, coeff, obs):
         coeff = _c128(coeff)
         obs = np.ascontiguousarray(obs, dtype=np.float64)

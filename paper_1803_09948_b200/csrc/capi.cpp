@@ -210,6 +210,22 @@ int hfmm_cuda_dist_downward(hfmm_cuda_t* h, void* out_morton_dev) {
   });
 }
 
+int hfmm_cuda_build_corrections(hfmm_cuda_t* h, const hfmm_correction_rules* rules, uint64_t* near_nnz) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] {
+    if (!rules) throw Error(HFMM_ERR_CONFIG, "null rules");
+    h->engine->build_corrections(*rules, near_nnz);
+  });
+}
+
+int hfmm_cuda_get_corrections(hfmm_cuda_t* h, double* patch_block, double* block_lu, int32_t* block_piv,
+                              uint32_t* near_offset, uint32_t* near_source, double* near_delta) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] {
+    h->engine->get_corrections(patch_block, block_lu, block_piv, near_offset, near_source, near_delta);
+  });
+}
+
 int hfmm_cuda_dist_gmres(hfmm_cuda_t* h, const double* rhs_owned, double* x_owned,
                          const hfmm_gmres_config* cfg, hfmm_gmres_report* report, double* residuals,
                          int residual_cap, const hfmm_dist_callbacks* cb) {

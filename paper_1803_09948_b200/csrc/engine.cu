@@ -470,6 +470,7 @@ void Engine::set_points(const double* xyz, size_t n) {
   const auto t0 = std::chrono::steady_clock::now();
   have_points_ = false;
   have_weight_ = have_block_ = have_near_ = have_lu_ = false;  // corrections belong to a point set
+  release_correction_store();
   identity_.release();
   dev_pairs_ = DevicePairs{};
   pairs_ = PairLists{};

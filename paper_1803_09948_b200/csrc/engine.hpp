@@ -59,6 +59,10 @@ class Engine {
   // clears and returns the name of a non-sticky CUDA error left behind on this host thread (or null)
   static const char* take_stale_cuda_error();
   void evaluate_field(const double* coeff, const double* obs, size_t nobs, double* out);
+  // correction builders on the device (corrections_build.cu; reference solver.cpp:80-230)
+  void build_corrections(const hfmm_correction_rules& rules, uint64_t* near_nnz);
+  void get_corrections(double* patch_block, double* block_lu, int* block_piv, uint32_t* near_offset,
+                       uint32_t* near_source, double* near_delta);
   void dist_gmres(const double* rhs_owned, double* x_owned, const hfmm_gmres_config& cfg,
                   hfmm_gmres_report* rep, double* residuals, int residual_cap,
                   const hfmm_dist_callbacks& cb);
@@ -135,6 +139,9 @@ class Engine {
   std::vector<TranslateStage> m2m_;  // deepest level first
   std::vector<TranslateStage> l2l_;  // shallowest level first
   // BIE operator tail (set_corrections)
+  struct CorrectionStore;  // FP64 results of build_corrections
+  std::shared_ptr<CorrectionStore> corrections64_;  // shared_ptr: deleter bound where the type is complete
+  void release_correction_store();
   int ni_ = 0;
   bool have_weight_ = false, have_block_ = false, have_near_ = false, have_lu_ = false;
   DeviceBuffer<float> far_weight_;

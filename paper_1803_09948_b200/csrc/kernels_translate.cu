@@ -62,11 +62,6 @@ __host__ __device__ inline SmemPlan smem_plan(int P) {
 // Shared memory is addressed with 32-bit BYTE addresses in the shared window (explicit
 // ld.shared / st.shared), so the loops advance with one integer add per pointer and the loads use
 // register + immediate addressing (generic pointers cost an address computation per access).
-__device__ __forceinline__ float2 lds2(uint32_t addr) {
-  float2 v;
-  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
-  return v;
-}
 __device__ __forceinline__ float4 lds4(uint32_t addr) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -107,14 +102,6 @@ __device__ __forceinline__ u64 mul2s(u64 x, float s) {
   u64 r;
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(pack2(s, s)));
   return r;
-}
-__device__ __forceinline__ u64 ldsp(uint32_t addr) {
-  u64 v;
-  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr));
-  return v;
-}
-__device__ __forceinline__ void stsp(uint32_t addr, u64 v) {
-  asm volatile("st.shared.b64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
 }
 __device__ __forceinline__ void ldsp2(uint32_t addr, u64& a, u64& b) {
   asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"(addr));

@@ -199,3 +199,62 @@ def test_sharded_operator_over_nccl_world_of_one():
         assert rel_l2(y[:, 0] + 1j * y[:, 1], plain.matvec(q)[order]) < 2e-6
     finally:
         dist.destroy_process_group()
+
+
+# ---- the correction builders on the device ---------------------------
+def _tables(g, prefix):
+    keys = ("sample_ref", "far_weight", "near_pts", "near_basis", "self_npts", "self_pts", "self_basis")
+    return {k: g[prefix + k] for k in keys}
+
+
+def _check_corrections(got, want, tol=2e-13):
+    # lists, pivots: exact; values: FP64 with device exp / sin / cos (an ulp from glibc's)
+    for key in ("near_offset", "near_source", "block_piv"):
+        assert np.array_equal(got[key], want[key]), key
+    for key in ("patch_block", "block_lu", "near_delta"):
+        assert got[key].shape == want[key].shape, key
+        assert np.abs(got[key] - want[key]).max() <= tol * np.abs(want[key]).max(), key
+
+
+@pytest.mark.parametrize("case", ["order1", "order2"])
+def test_device_correction_builders_match_reference_fixture(case):
+    """build_patch_blocks / build_near_corrections (solver.cpp:80-230) on the GPU against the arrays
+    the reference produced (rule tables stored with the fixture)"""
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    if case == "order1":
+        g, pre, rp, order = G, "bie_", "bie_rule_", int(G["bie_order"])
+    else:
+        g, pre, rp, order = np.load(os.path.join(here, "corrections_order2.npz")), "", "rule_", 6
+    k = float(g[pre + "k"])
+    op = HfmmCuda(k=k, order=order, ncrit=16, theta=0.4, kd_max=1.0, leaf_cap=-1.0)
+    op.set_points(g[pre + "xyz"])
+    got = op.build_corrections(g[pre + "patches"], _tables(g, rp), mode=2)
+    _check_corrections(got, {key: g[pre + key] for key in got})
+    if case == "order1":
+        # the installed (FP32) corrections reproduce the reference's operator and solve
+        assert rel_l2(op.matvec(G["bie_x"]), G["bie_y"]) < 1e-5
+        x, rep = op.gmres(G["bie_rhs"], rtol=1e-4, restart=30, max_iterations=200)
+        assert rep["converged"] and abs(rep["iterations"] - int(G["bie_iterations"])) <= 1
+    # modes: no near lists for self_only, no LU for none
+    only = op.build_corrections(g[pre + "patches"], _tables(g, rp), mode=1)
+    assert only["near_source"].size == 0 and np.array_equal(only["block_piv"], g[pre + "block_piv"])
+    none = op.build_corrections(g[pre + "patches"], _tables(g, rp), mode=0)
+    assert none["block_lu"].size == 0 and np.abs(none["patch_block"]).max() > 0
+    with pytest.raises(HfmmError) as e:
+        op.build_corrections(g[pre + "patches"][:-1], _tables(g, rp))
+    assert e.value.kind == "config_error"
+
+
+def test_device_correction_builders_against_oracle_midsize(oracle):
+    """1,280 curved triangles, second-order basis (7,680 unknowns): device builder against the oracle's
+    restatement (itself bit-identical to the reference, tests/test_oracle_golden.py)"""
+    g2 = np.load(os.path.join(os.path.dirname(__file__), "golden", "corrections_order2.npz"))
+    tables = _tables(g2, "rule_")
+    patches = icosphere_patches(3)
+    k = 3.0
+    want = oracle.build_corrections(patches, tables, k)
+    op = HfmmCuda(k=k, order=8, ncrit=32)
+    op.set_points(want["xyz"])
+    got = op.build_corrections(patches, tables)
+    _check_corrections(got, want)
+    assert got["near_source"].size > 1_000_000
