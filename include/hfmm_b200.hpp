@@ -193,8 +193,9 @@ struct SolveReport {
 using MatVec = std::function<std::vector<cplx>(const std::vector<cplx>&)>;
 
 // The tree path of a DiscreteSystem (solver.hpp:44-81) on the device: the FMM operator plus the
-// precomputed sparse corrections and block-Jacobi factors the reference's build_system produced
-// (solver.cpp:80-230).  Those builders stay on the host and are passed in unchanged.
+// sparse corrections and block-Jacobi factors of build_system (solver.cpp:80-230): either the
+// reference's host-built arrays passed in unchanged (set_corrections) or built on the device from
+// the patches and geometry.cpp's rule tables (build_corrections).
 class DeviceOperator {
  public:
   DeviceOperator(const std::vector<Vec3>& sample_positions, WaveNumber k, int expansion_order,
@@ -211,6 +212,16 @@ class DeviceOperator {
         tree_.handle(), basis_count, far_weight.empty() ? nullptr : far_weight.data(), d(patch_block),
         near_offset.empty() ? nullptr : near_offset.data(), near_source.empty() ? nullptr : near_source.data(),
         d(near_delta), d(block_lu), block_piv.empty() ? nullptr : block_piv.data()));
+  }
+  // build_patch_blocks + build_near_corrections on the device.  `nodes`: 6 x Vec3 per patch
+  // (CurvilinearPatch::node); the tables are geom::lagrange_basis(order).nodes() / .weights(),
+  // geom::gauss_rule(KernelConfig::near_rule) and geom::duffy_rule(node_j, KernelConfig::self_rule)
+  // with basis.eval at their points (see hfmm_correction_rules).  Returns the near CSR length.
+  // singular_error when a self block is singular (solver.cpp:55-56).
+  std::uint64_t build_corrections(const hfmm_correction_rules& rules) {
+    std::uint64_t nnz = 0;
+    tree_.check(hfmm_cuda_build_corrections(tree_.handle(), &rules, &nnz));
+    return nnz;
   }
   std::size_t size() const { return tree_.size(); }
   fmm::DeviceTree& tree() { return tree_; }

@@ -556,7 +556,11 @@ void dual_tree_traversal_device(const TreeArrays& t, const DeviceCells& cells, d
     cap_near *= 2;
     cap_front *= 2;
   }
-  throw Error(HFMM_ERR_INTERNAL, "dual tree traversal: pair buffers overflowed repeatedly");
+  // more than ~500 pairs per body: the kd_max gate forbids every coarse translation (k x box >> kd_max)
+  // and the lists degenerate towards all pairs of finest-level cells, as they do in the reference
+  throw Error(HFMM_ERR_STRUCTURAL,
+              "dual tree traversal: interaction lists exceed 512 pairs per body (kd_max too small for this "
+              "wavenumber and domain?)");
 }
 
 void far_pair_level_range(const DevicePairs& p, const DeviceCells& cells, int& lmin_dst, int& lmin_src,

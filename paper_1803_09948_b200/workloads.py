@@ -123,3 +123,20 @@ def icosphere_patches(subdivisions: int, radius: float = 1.0) -> np.ndarray:
         mids.append(m / np.linalg.norm(m, axis=1, keepdims=True))
     patches = np.concatenate([tri, np.stack(mids, 1)], axis=1) * radius
     return np.ascontiguousarray(patches, dtype=np.float64)
+
+
+def patch_samples(patches: np.ndarray, sample_ref: np.ndarray) -> np.ndarray:
+    """Positions of the interpolation nodes (zeta, eta) of every patch, patch-major — the samples of
+    the reference's build_system (solver.cpp:283-294) through its quadratic map
+    (geometry.cpp:22-45), evaluated in the same operation order (bit-identical)."""
+    patches = np.asarray(patches, dtype=np.float64)
+    out = np.zeros((patches.shape[0], len(sample_ref), 3))
+    for j, (z, e) in enumerate(np.asarray(sample_ref, dtype=np.float64)):
+        l1, l2, l3 = 1.0 - z - e, z, e
+        n = [l1 * (2 * l1 - 1), l2 * (2 * l2 - 1), l3 * (2 * l3 - 1), 4 * l1 * l2, 4 * l2 * l3, 4 * l3 * l1]
+        r = np.zeros((patches.shape[0], 3))
+        for k in range(6):
+            r += n[k] * patches[:, k, :]
+        out[:, j, :] = r
+    return out.reshape(-1, 3)
+
