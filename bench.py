@@ -258,7 +258,46 @@ def run_single(args, cfg):
     }
     if cpu:
         line["cpu_baseline"] = cpu
+    if not args.no_bie and cfg.name == "cfg2" and n == cfg.n:
+        del op
+        line["bie_solve"] = run_bie_solve()
     print(json.dumps(line), flush=True)
+
+
+def run_bie_solve(subdivisions: int = 7, k: float = 4.0, order: int = 12):
+    """BASELINE.json configs[2] end to end on the device (reported next to the headline metric, not
+    part of it): icosphere with 327,680 curved triangles, order-1 basis (983,040 unknowns), tree +
+    interaction lists + singular / near corrections built by the library, GMRES(30) to 1e-4 on the
+    plane wave e^{ikz}.  The quadrature tables are the reference's geometry.cpp rules stored with the
+    fixtures (tests/golden/solver.npz); block-Jacobi is off (it slows GMRES(30) down on this
+    first-kind system, in the reference as well: BASELINE.md section 2, 104 vs 67 iterations)."""
+    import numpy as np
+
+    from paper_1803_09948_b200 import HfmmCuda
+    from paper_1803_09948_b200.workloads import icosphere_patches, patch_samples
+
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "tests", "golden", "solver.npz"))
+    tables = {key: g["bie_rule_" + key] for key in ("sample_ref", "far_weight", "near_pts", "near_basis",
+                                                    "self_npts", "self_pts", "self_basis")}
+    patches = icosphere_patches(subdivisions)
+    xyz = patch_samples(patches, tables["sample_ref"])
+    op = HfmmCuda(k=k, order=order, ncrit=64, theta=0.4, kd_max=1.0, leaf_cap=-1.0, device=0)
+    t0 = time.perf_counter()
+    op.set_points(xyz)
+    t_tree = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    nnz = op.build_corrections(patches, tables, mode=2, fetch=False)
+    t_corr = time.perf_counter() - t0
+    rhs = np.exp(1j * k * xyz[:, 2])
+    t0 = time.perf_counter()
+    x, rep = op.gmres(rhs, rtol=1e-4, restart=30, max_iterations=1000, precondition=False)
+    t_solve = time.perf_counter() - t0
+    return {"workload": "BASELINE.json configs[2]: BIE GMRES solve, sound-soft unit sphere, plane wave e^{ikz}",
+            "triangles": int(len(patches)), "unknowns": int(len(xyz)), "k": k, "order": order,
+            "near_correction_nnz": int(nnz), "tree_and_lists_seconds": t_tree, "corrections_seconds": t_corr,
+            "gmres": {"rtol": 1e-4, "restart": 30, "block_jacobi": False, "iterations": int(rep["iterations"]),
+                      "converged": bool(rep["converged"]), "final_residual": float(rep["final_residual"])},
+            "solve_seconds": t_solve, "checksum": float(np.abs(x).sum())}
 
 
 def run_multi(args, cfg, rank: int, world: int):
@@ -283,6 +322,7 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override the point count (debug)")
     ap.add_argument("--ref-points", type=int, default=16384, help="sample size of the CPU arm")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-bie", action="store_true", help="skip the configs[2] BIE solve reported next to the headline")
     ap.add_argument("--force-distributed", action="store_true",
                     help="run the N > 1 code path even with one rank (exercises the exchange plumbing)")
     args = ap.parse_args()

@@ -258,3 +258,26 @@ def test_device_correction_builders_against_oracle_midsize(oracle):
     got = op.build_corrections(patches, tables)
     _check_corrections(got, want)
     assert got["near_source"].size > 1_000_000
+
+
+@pytest.mark.skipif(not have_ref(), reason="the analytic Mie series lives in the compiled reference")
+def test_config3_pipeline_on_device_against_mie_series(ref):
+    """BASELINE config 3 at 20,480 triangles (61,440 unknowns), everything on the device: tree, lists,
+    corrections, GMRES(30) to 1e-4; scattered field at r = 4 against oracle::mie_soft_sphere
+    (oracle.cpp:11-59).  The mismatch is the discretisation error of the order-1 quadrature."""
+    from paper_1803_09948_b200.workloads import patch_samples
+
+    k = 4.0
+    tables = _tables(G, "bie_rule_")
+    patches = icosphere_patches(5)
+    xyz = patch_samples(patches, tables["sample_ref"])
+    op = HfmmCuda(k=k, order=12, ncrit=64, theta=0.4, kd_max=1.0, leaf_cap=-1.0)
+    op.set_points(xyz)
+    assert op.build_corrections(patches, tables, fetch=False) > 0
+    x, rep = op.gmres(np.exp(1j * k * xyz[:, 2]), rtol=1e-4, restart=30, max_iterations=600, precondition=False)
+    assert rep["converged"] and rep["final_residual"] <= 1.05e-4
+    th = np.linspace(0, np.pi, 37)
+    obs = np.stack([4 * np.sin(th), 0 * th, 4 * np.cos(th)], 1)
+    scat = -op.evaluate_field(x, obs)       # physical field = minus the layer sum (solver.hpp:134-136)
+    mie = ref.mie_soft_sphere(1.0, k, np.stack([4 + 0 * th, th, 0 * th], 1))
+    assert rel_l2(scat, mie) < 0.035
