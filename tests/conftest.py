@@ -65,7 +65,7 @@ def pytest_terminal_summary(terminalreporter):
         lib = load_library()
         lib.hfmm_debug_stale_cuda_error.restype = ctypes.c_char_p
         stale = lib.hfmm_debug_stale_cuda_error()
-        if stale:
+        if stale and _cuda_device_count() > 0:
             terminalreporter.write_line("hfmm: stale CUDA error seen at API entry: " + stale.decode())
     except Exception:
         pass
