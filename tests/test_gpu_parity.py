@@ -246,3 +246,23 @@ def test_argument_errors():
     op.set_points(np.random.default_rng(0).uniform(-1, 1, (50, 3)))
     with pytest.raises(ValueError):
         op.matvec(np.zeros(49))
+
+
+def test_interaction_lists_cover_every_body_pair_exactly_once():
+    """reference tests/test_fmm.cpp:865-895 (once-cover): the M2L cell pairs and the P2P leaf pairs of
+    the device-built lists tile the (target body, source body) matrix — each entry exactly once"""
+    n = 700
+    xyz = np.concatenate([sphere_points(n - 200, 21), 0.3 * sphere_points(200, 22) + 0.1])
+    op = HfmmCuda(k=3.0, order=4, ncrit=12, theta=0.5, kd_max=1.0, leaf_cap=-1.0)
+    op.set_points(xyz)
+    cells = op.cells()
+    first, count = cells[:, 4].astype(np.int64), cells[:, 5].astype(np.int64)
+    cover = np.zeros((n, n), dtype=np.int32)
+    for which in (0, 1):
+        for t, s in op.pairs(which):
+            cover[first[t]:first[t] + count[t], first[s]:first[s] + count[s]] += 1
+    assert cover.min() == 1 and cover.max() == 1
+    # P2P pairs join leaves only; no M2L pair has a cell wider than the kd gate allows
+    leaf = cells[:, 7] == 0
+    p2p = op.pairs(1)
+    assert leaf[p2p[:, 0]].all() and leaf[p2p[:, 1]].all()
