@@ -190,6 +190,22 @@ int hfmm_cuda_dist_upward(hfmm_cuda_t* h, const void* q_morton_dev);
 /* out_morton_dev: n float2 in Morton order; only the owned slots are written */
 int hfmm_cuda_dist_downward(hfmm_cuda_t* h, void* out_morton_dev);
 
+/* ---- repartitioning loop (reference partition.cpp:137-227) -------
+ * measure_weights -> w = l + alpha r -> Morton cuts -> run -> update_alpha -> re-cut.  The work
+ * estimates come from the interaction lists of the current point set; alpha is searched by the
+ * caller's driver from measured matvec times (max over ranks). */
+/* per body, caller order: local[i] = bodies of the P2P partner leaves of i's leaf, remote[i] = number
+ * of M2L pairs of all cells holding i (measure_weights, partition.cpp:143-163) */
+int hfmm_cuda_measure_weights(hfmm_cuda_t* h, double* local, double* remote);
+/* balance the Morton cuts of hfmm_cuda_set_partition by sum(l + alpha r) (apply_weights,
+ * partition.cpp:165-173); alpha < 0 (default) balances by measured kernel cost per list entry instead.
+ * Takes effect at the next hfmm_cuda_set_points. */
+int hfmm_cuda_set_partition_alpha(hfmm_cuda_t* h, double alpha);
+/* next alpha to try given the history of (alpha, runtime) samples: golden-section replay over
+ * [0, alpha_max], the best measured alpha once the bracket is tight (update_alpha,
+ * partition.cpp:175-227).  config_error on an empty history or alpha_max <= 0. */
+int hfmm_partition_update_alpha(const double* alpha, const double* runtime, int n, double alpha_max, double* next);
+
 /* ---- correction builders on the device ------------------------------
  * Replace build_patch_blocks (proj/core/src/solver.cpp:80-128) and build_near_corrections
  * (solver.cpp:132-230).  The quadrature and interpolation tables are the reference's own

@@ -1256,3 +1256,74 @@ void ho_build_near_deltas(const ho_correction_rules* r, double kr, double ki, co
 }
 
 void ho_free(void* p) { free(p); }
+
+/* ============================ repartitioning loop ==========================================
+ * ref: src/partition.cpp:143-163 (measure_weights), :175-227 (update_alpha) */
+void ho_measure_weights(const ho_fmm* h, double* local, double* remote) {
+  for (long i = 0; i < h->n; ++i) local[i] = remote[i] = 0.0;
+  for (long e = 0; e < h->n_p2p;) {
+    const uint32_t t = h->p2p_t[e];
+    double partners = 0;
+    long f = e;
+    for (; f < h->n_p2p && h->p2p_t[f] == t; ++f) partners += (double)h->cells[h->p2p_s[f]].body_count;
+    const cell_t* c = &h->cells[t];
+    for (uint32_t b = c->body_first; b < c->body_first + c->body_count; ++b) local[h->index[b]] += partners;
+    e = f;
+  }
+  for (long e = 0; e < h->n_m2l;) {
+    const uint32_t t = h->m2l_t[e];
+    long f = e;
+    while (f < h->n_m2l && h->m2l_t[f] == t) ++f;
+    const double pairs = (double)(f - e);
+    const cell_t* c = &h->cells[t];
+    for (uint32_t b = c->body_first; b < c->body_first + c->body_count; ++b) remote[h->index[b]] += pairs;
+    e = f;
+  }
+}
+
+int ho_update_alpha(const double* alpha, const double* runtime, int n, double alpha_max, double* next) {
+  if (n < 1 || !(alpha_max > 0)) return 1;
+  const double inv_phi = 0.6180339887498948;
+  const int budget = 12;
+  const double tol = 1e-12 * (alpha_max > 1.0 ? alpha_max : 1.0);
+  char* used = (char*)calloc((size_t)n, 1);
+#define HO_TAKE(a, out)                                              \
+  do {                                                               \
+    (out) = -1;                                                      \
+    for (int i_ = 0; i_ < n; ++i_)                                   \
+      if (!used[i_] && fabs(alpha[i_] - (a)) <= tol) {               \
+        used[i_] = 1;                                                \
+        (out) = i_;                                                  \
+        break;                                                       \
+      }                                                              \
+  } while (0)
+  double lo = 0, hi = alpha_max;
+  double x1 = hi - inv_phi * (hi - lo), x2 = lo + inv_phi * (hi - lo);
+  int s1, s2;
+  HO_TAKE(x1, s1);
+  if (s1 < 0) { *next = x1; free(used); return 0; }
+  HO_TAKE(x2, s2);
+  if (s2 < 0) { *next = x2; free(used); return 0; }
+  for (int probes = 2; probes < budget && hi - lo > 1e-6 * alpha_max;) {
+    if (runtime[s1] < runtime[s2]) {
+      hi = x2; x2 = x1; s2 = s1;
+      x1 = hi - inv_phi * (hi - lo);
+      HO_TAKE(x1, s1);
+      if (s1 < 0) { *next = x1; free(used); return 0; }
+    } else {
+      lo = x1; x1 = x2; s1 = s2;
+      x2 = lo + inv_phi * (hi - lo);
+      HO_TAKE(x2, s2);
+      if (s2 < 0) { *next = x2; free(used); return 0; }
+    }
+    ++probes;
+  }
+#undef HO_TAKE
+  int arg = 0;
+  for (int i = 1; i < n; ++i)
+    if (runtime[i] < runtime[arg]) arg = i;
+  *next = alpha[arg];
+  free(used);
+  return 0;
+}
+

@@ -67,6 +67,12 @@ void ho_block_lu_solve(long npatch, int ni, const double* block_lu, const int* b
                        double* x);
 
 
+/* ---- repartitioning loop (ref: src/partition.cpp:137-227) -------------------------------------- */
+/* per-body work estimates in caller order: local = P2P partners, remote = M2L pairs of every cell above the body */
+void ho_measure_weights(const ho_fmm* h, double* local, double* remote);
+/* golden-section replay over [0, alpha_max]; returns 0, or 1 for invalid arguments */
+int ho_update_alpha(const double* alpha, const double* runtime, int n, double alpha_max, double* next);
+
 /* ---- correction builders (setup of the BIE operator; ref: src/solver.cpp:78-230) ---------------
  * The quadrature / interpolation tables are geometry.cpp's, passed in by the caller; field for
  * field the layout of hfmm_correction_rules in include/hfmm_cuda.h. */

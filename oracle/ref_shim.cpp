@@ -473,4 +473,18 @@ int ref_geom_duffy_rule(double zeta0, double eta0, int n_per_dim, double* pts) {
   return int(r.size());
 }
 
+// repartitioning loop (partition.cpp:137-227): per-body work estimates and the alpha search
+void ref_measure_weights(const RefFmm* h, double* local, double* remote) {
+  const auto w = part::measure_weights(h->tree, h->plan);
+  std::memcpy(local, w.local.data(), sizeof(double) * w.local.size());
+  std::memcpy(remote, w.remote.data(), sizeof(double) * w.remote.size());
+}
+int ref_update_alpha(const double* alpha, const double* runtime, int n, double alpha_max, double* next) {
+  return guarded([&] {
+    std::vector<part::AlphaSample> hist(n);
+    for (int i = 0; i < n; ++i) hist[i] = part::AlphaSample{alpha[i], runtime[i]};
+    *next = part::update_alpha(hist, alpha_max);
+  });
+}
+
 }  // extern "C"

@@ -191,6 +191,16 @@ class HfmmCuda:
     def set_partition(self, rank: int, nranks: int):
         self._check(self.lib.hfmm_cuda_set_partition(self.h, int(rank), int(nranks)))
 
+    def set_partition_alpha(self, alpha: float):
+        """Morton cuts balanced by the reference's w = l + alpha r (alpha < 0: default cost model)"""
+        self._check(self.lib.hfmm_cuda_set_partition_alpha(self.h, C.c_double(alpha)))
+
+    def measure_weights(self):
+        """(local, remote) work estimates per body, caller order (reference measure_weights)"""
+        local, remote = np.zeros(self.n), np.zeros(self.n)
+        self._check(self.lib.hfmm_cuda_measure_weights(self.h, local.ctypes.data_as(_dp), remote.ctypes.data_as(_dp)))
+        return local, remote
+
     def partition(self) -> Partition:
         p = Partition()
         self._check(self.lib.hfmm_cuda_get_partition(self.h, C.byref(p)))
@@ -361,6 +371,19 @@ class HfmmCuda:
 
 
 # ---- host-only debug helpers (no device needed) used by the CPU-side tests -------------------
+def update_alpha(alphas, runtimes, alpha_max: float = 2.0) -> float:
+    """next alpha of the repartitioning loop (reference update_alpha, partition.cpp:175-227)"""
+    lib = load_library()
+    a = np.ascontiguousarray(alphas, dtype=np.float64)
+    r = np.ascontiguousarray(runtimes, dtype=np.float64)
+    out = C.c_double()
+    rc = lib.hfmm_partition_update_alpha(a.ctypes.data_as(_dp), r.ctypes.data_as(_dp), len(a),
+                                         C.c_double(alpha_max), C.byref(out))
+    if rc:
+        raise HfmmError(rc, "update_alpha: empty history or non-positive alpha_max")
+    return out.value
+
+
 def debug_compose_translation(order, k, t, kind, s_src=1.0, s_dst=1.0):
     lib = load_library()
     dim = (order + 1) ** 2

@@ -210,6 +210,26 @@ int hfmm_cuda_dist_downward(hfmm_cuda_t* h, void* out_morton_dev) {
   });
 }
 
+int hfmm_cuda_set_partition_alpha(hfmm_cuda_t* h, double alpha) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] { h->engine->set_partition_alpha(alpha); });
+}
+
+int hfmm_cuda_measure_weights(hfmm_cuda_t* h, double* local, double* remote) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] {
+    if (!local || !remote) throw Error(HFMM_ERR_CONFIG, "null weight array");
+    h->engine->measure_weights(local, remote);
+  });
+}
+
+int hfmm_partition_update_alpha(const double* alpha, const double* runtime, int n, double alpha_max, double* next) {
+  return guarded(nullptr, [&] {
+    if (!next) throw Error(HFMM_ERR_CONFIG, "null output");
+    *next = hfmm_b200::partition_update_alpha(alpha, runtime, n, alpha_max);
+  });
+}
+
 int hfmm_cuda_build_corrections(hfmm_cuda_t* h, const hfmm_correction_rules* rules, uint64_t* near_nnz) {
   if (int rc = need(h)) return rc;
   return guarded(h, [&] {
@@ -308,7 +328,7 @@ int hfmm_debug_partition(const double* xyz, size_t n, int ncrit, double leaf_cap
     std::vector<int> cell_rank;
     std::vector<uint32_t> f, c;
     int lcut = 0;
-    hfmm_b200::compute_morton_partition(t, p, nranks, cell_rank, f, c, lcut);
+    hfmm_b200::compute_morton_partition(t, p, nranks, -1.0, cell_rank, f, c, lcut);
     for (int r = 0; r < nranks; ++r) {
       first[r] = f[r];
       count[r] = c[r];

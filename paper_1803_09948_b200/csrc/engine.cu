@@ -388,6 +388,11 @@ void Engine::build_tiles(const std::vector<uint64_t>& work) {
   p2p_tiles_.upload(sorted, stream_);
 }
 
+void Engine::set_partition_alpha(double alpha) {
+  if (alpha != alpha) throw Error(HFMM_ERR_CONFIG, "alpha must be a number");
+  partition_alpha_ = alpha;  // takes effect at the next set_points
+}
+
 void Engine::set_partition(int rank, int nranks) {
   if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(HFMM_ERR_CONFIG, "rank out of range");
   rank_ = rank;
@@ -403,7 +408,7 @@ void Engine::compute_partition() {
   own_count_ = tree_.n_bodies;
   std::vector<int> cell_rank;
   std::vector<uint32_t> first, count;
-  compute_morton_partition(tree_, pairs_, nranks_, cell_rank, first, count, lcut_);
+  compute_morton_partition(tree_, pairs_, nranks_, partition_alpha_, cell_rank, first, count, lcut_);
   if (nranks_ == 1) return;
   own_first_ = first[rank_];
   own_count_ = count[rank_];
@@ -524,7 +529,7 @@ void Engine::set_points_device(const double* xyz, size_t n) {
     lcut_ = partition_units(t, lmin_src_, lmin_dst_, unit);
     if (nranks_ > 1) {
       std::vector<double> weight;
-      partition_weights_device(dev_pairs_, cells, unit, weight, stream_);
+      partition_weights_device(dev_pairs_, cells, unit, partition_alpha_, weight, stream_);
       std::vector<int> cell_rank;
       std::vector<uint32_t> first, count;
       partition_cuts(t, unit, weight, nranks_, cell_rank, first, count);
@@ -897,6 +902,32 @@ void Engine::get_cells(uint32_t* out, size_t capacity) const {
 void Engine::get_body_order(uint32_t* out) const {
   require_points();
   std::copy(tree_.index.begin(), tree_.index.end(), out);
+}
+
+// reference measure_weights (partition.cpp:143-163): per body, caller order;
+// local = bodies of the P2P partners of its leaf, remote = M2L pairs of every cell that holds it
+void Engine::measure_weights(double* local, double* remote) const {
+  require_points();
+  const TreeArrays& t = tree_;
+  const size_t nc = t.n_cells();
+  std::vector<double> partners(nc, 0.0), lists(nc, 0.0);
+  for (int which = 0; which < 2; ++which) {
+    uint64_t np = 0;
+    get_pairs(which, nullptr, &np);
+    std::vector<uint32_t> pr(2 * np);
+    if (np) get_pairs(which, pr.data(), &np);
+    for (uint64_t e = 0; e < np; ++e) {
+      if (which) partners[pr[2 * e]] += double(t.body_count[pr[2 * e + 1]]);
+      else lists[pr[2 * e]] += 1.0;
+    }
+  }
+  // cells are stored level by level, parents first: one sweep accumulates the lists of the ancestors
+  for (size_t c = 1; c < nc; ++c) lists[c] += lists[t.parent[c]];
+  for (uint32_t c : t.leaves)
+    for (uint32_t b = t.body_first[c]; b < t.body_first[c] + t.body_count[c]; ++b) {
+      local[t.index[b]] = partners[c];
+      remote[t.index[b]] = lists[c];
+    }
 }
 
 void Engine::get_pairs(int which, uint32_t* out, uint64_t* count) const {

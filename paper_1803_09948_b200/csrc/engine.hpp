@@ -34,6 +34,8 @@ class Engine {
   ~Engine();
 
   void set_partition(int rank, int nranks);
+  void set_partition_alpha(double alpha);  // < 0: default work model
+  void measure_weights(double* local, double* remote) const;
   void get_partition(hfmm_cuda_partition* out);
   void dist_upward(const void* q_morton_dev);
   void dist_downward(void* out_morton_dev);
@@ -98,6 +100,7 @@ class Engine {
   // Morton partition (multi-GPU): this rank owns bodies [own_first_, own_first_ + own_count_)
   int rank_ = 0, nranks_ = 1, lcut_ = 0;
   uint32_t own_first_ = 0, own_count_ = 0;
+  double partition_alpha_ = -1.0;
   std::vector<uint8_t> owned_;  // per cell
   uint64_t owned_m2l_pairs_ = 0, owned_body_pairs_ = 0, launches_ = 0;
   cudaStream_t stream_ = nullptr, stream_near_ = nullptr;

@@ -282,7 +282,7 @@ void partition_cuts(const TreeArrays& t, const std::vector<uint32_t>& unit,
   for (uint32_t c = 0; c < nc; ++c) cell_rank[c] = unit[c] == none ? -1 : unit_rank[unit[c]];
 }
 
-void compute_morton_partition(const TreeArrays& t, const PairLists& pairs, int nranks,
+void compute_morton_partition(const TreeArrays& t, const PairLists& pairs, int nranks, double alpha,
                               std::vector<int>& cell_rank, std::vector<uint32_t>& first,
                               std::vector<uint32_t>& count, int& lcut) {
   int lmin_src = kMaxLevel + 1, lmin_dst = kMaxLevel + 1;
@@ -298,9 +298,53 @@ void compute_morton_partition(const TreeArrays& t, const PairLists& pairs, int n
       const uint32_t a = pairs.p2p_t[e], b = pairs.p2p_s[e];
       weight[unit[a]] += kPartitionPairWeight * double(t.body_count[a]) * double(t.body_count[b]);
     }
-    for (size_t e = 0; e < pairs.m2l_t.size(); ++e) weight[unit[pairs.m2l_t[e]]] += kPartitionM2lWeight;
+    for (size_t e = 0; e < pairs.m2l_t.size(); ++e)
+      weight[unit[pairs.m2l_t[e]]] += alpha < 0 ? kPartitionM2lWeight : alpha * double(t.body_count[pairs.m2l_t[e]]);
   }
   partition_cuts(t, unit, weight, nranks, cell_rank, first, count);
+}
+
+double partition_update_alpha(const double* alpha, const double* runtime, int n, double alpha_max) {
+  if (n < 1 || !alpha || !runtime) throw Error(HFMM_ERR_CONFIG, "alpha history must not be empty");
+  if (!(alpha_max > 0)) throw Error(HFMM_ERR_CONFIG, "alpha_max must be positive");
+  constexpr double inv_phi = 0.6180339887498948;
+  constexpr int budget = 12;
+  const double tol = 1e-12 * std::max(1.0, alpha_max);
+  std::vector<char> used(n, 0);
+  // first unused sample measured at `a`, or -1: the search has not probed there yet
+  auto take = [&](double a) {
+    for (int i = 0; i < n; ++i)
+      if (!used[i] && std::abs(alpha[i] - a) <= tol) {
+        used[i] = 1;
+        return i;
+      }
+    return -1;
+  };
+  double lo = 0, hi = alpha_max;
+  double x1 = hi - inv_phi * (hi - lo), x2 = lo + inv_phi * (hi - lo);
+  int s1 = take(x1);
+  if (s1 < 0) return x1;
+  int s2 = take(x2);
+  if (s2 < 0) return x2;
+  for (int probes = 2; probes < budget && hi - lo > 1e-6 * alpha_max; ++probes) {
+    if (runtime[s1] < runtime[s2]) {  // the minimum lies left of x2
+      hi = x2;
+      x2 = x1;
+      s2 = s1;
+      x1 = hi - inv_phi * (hi - lo);
+      if ((s1 = take(x1)) < 0) return x1;
+    } else {
+      lo = x1;
+      x1 = x2;
+      s1 = s2;
+      x2 = lo + inv_phi * (hi - lo);
+      if ((s2 = take(x2)) < 0) return x2;
+    }
+  }
+  int best = 0;  // earliest minimum: a flat curve changes nothing
+  for (int i = 1; i < n; ++i)
+    if (runtime[i] < runtime[best]) best = i;
+  return alpha[best];
 }
 
 }  // namespace hfmm_b200

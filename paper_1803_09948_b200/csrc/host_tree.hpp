@@ -73,8 +73,13 @@ int partition_units(const TreeArrays& tree, int lmin_src, int lmin_dst, std::vec
 void partition_cuts(const TreeArrays& tree, const std::vector<uint32_t>& unit,
                     const std::vector<double>& weight, int nranks, std::vector<int>& cell_rank,
                     std::vector<uint32_t>& first, std::vector<uint32_t>& count);
-void compute_morton_partition(const TreeArrays& tree, const PairLists& pairs, int nranks,
+// alpha: see partition_weights_device
+void compute_morton_partition(const TreeArrays& tree, const PairLists& pairs, int nranks, double alpha,
                               std::vector<int>& cell_rank, std::vector<uint32_t>& first,
                               std::vector<uint32_t>& count, int& lcut);
+
+// Next alpha to try: golden-section replay over [0, alpha_max] against the measured history
+// (reference update_alpha, partition.cpp:175-227).  Throws config_error like the reference.
+double partition_update_alpha(const double* alpha, const double* runtime, int n, double alpha_max);
 
 }  // namespace hfmm_b200

@@ -228,10 +228,12 @@ level_range_kernel(const uint2* __restrict__ pairs, unsigned long long n, const 
 __global__ void __launch_bounds__(kBlock)
 weights_kernel(const uint2* __restrict__ far, unsigned long long n_far, const uint2* __restrict__ near,
                unsigned long long n_near, const uint32_t* __restrict__ unit,
-               const uint32_t* __restrict__ body_count, double* __restrict__ weight) {
+               const uint32_t* __restrict__ body_count, double alpha, double* __restrict__ weight) {
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  // alpha < 0: measured kernel-time ratio per M2L pair; alpha >= 0: the reference's per-body estimate
+  // w = l + alpha r summed over the bodies of the target cell (partition.cpp:137-163)
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n_far; i += stride)
-    atomicAdd(weight + unit[far[i].x], kPartitionM2lWeight);
+    atomicAdd(weight + unit[far[i].x], alpha < 0 ? kPartitionM2lWeight : alpha * double(body_count[far[i].x]));
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n_near; i += stride) {
     const uint2 p = near[i];
     atomicAdd(weight + unit[p.x], double(body_count[p.x]) * double(body_count[p.y]));
@@ -580,14 +582,14 @@ void far_pair_level_range(const DevicePairs& p, const DeviceCells& cells, int& l
 }
 
 void partition_weights_device(const DevicePairs& p, const DeviceCells& cells,
-                              const std::vector<uint32_t>& unit_of_cell, std::vector<double>& weight,
-                              cudaStream_t s) {
+                              const std::vector<uint32_t>& unit_of_cell, double alpha,
+                              std::vector<double>& weight, cudaStream_t s) {
   DeviceBuffer<uint32_t> unit;
   unit.upload(unit_of_cell, s);
   DeviceBuffer<double> w(unit_of_cell.size());
   w.zero(s);
   weights_kernel<<<2048, kBlock, 0, s>>>(p.far.get(), p.n_far, p.near.get(), p.n_near, unit.get(),
-                                         cells.body_count.get(), w.get());
+                                         cells.body_count.get(), alpha, w.get());
   HFMM_CUDA_CHECK(cudaGetLastError());
   weight.resize(unit_of_cell.size());
   w.download(weight.data(), weight.size(), s);

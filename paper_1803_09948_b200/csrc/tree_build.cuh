@@ -52,9 +52,10 @@ void far_pair_level_range(const DevicePairs& p, const DeviceCells& cells, int& l
                           cudaStream_t s);
 
 // per-unit work weights of the Morton partition (host_tree.hpp: compute_morton_partition)
+// alpha < 0: default model; alpha >= 0: the reference's w = l + alpha r per body (partition.cpp:137-163)
 void partition_weights_device(const DevicePairs& p, const DeviceCells& cells,
-                              const std::vector<uint32_t>& unit_of_cell, std::vector<double>& weight,
-                              cudaStream_t s);
+                              const std::vector<uint32_t>& unit_of_cell, double alpha,
+                              std::vector<double>& weight, cudaStream_t s);
 
 struct NearLists {
   uint64_t n_owned_pairs = 0, body_pairs = 0, owned_body_pairs = 0;

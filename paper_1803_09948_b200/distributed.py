@@ -139,6 +139,35 @@ class ShardedFmm:
                                   restart=restart, max_iterations=max_iterations, precondition=precondition)
 
 
+class Repartitioner:
+    """The reference's repartitioning loop (partition.cpp:137-227) around
+    a sharded operator: time a window of matvecs (max over ranks), record (alpha, runtime), ask
+    update_alpha for the next alpha, re-cut the Morton partition with w = l + alpha r.  Re-cutting
+    rebuilds the rank's lists (set_points, ~0.2 s per million points), so it is done between
+    GMRES restarts, when only the iterate and the right-hand side have to be re-sharded."""
+
+    def __init__(self, make_operator, alpha_max: float = 2.0):
+        # make_operator(alpha) -> a ShardedFmm (or anything whose matvec is timed by the caller)
+        self.make_operator, self.alpha_max = make_operator, alpha_max
+        self.alphas, self.runtimes = [], []
+        inv_phi = 0.6180339887498948
+        self.alpha = alpha_max - inv_phi * alpha_max      # the search's first probe
+        self.operator = make_operator(self.alpha)
+
+    def record(self, runtime_max_over_ranks: float) -> bool:
+        """Feeds one measurement; returns True when the partition was re-cut (alpha changed)."""
+        from .api import update_alpha
+
+        self.alphas.append(self.alpha)
+        self.runtimes.append(float(runtime_max_over_ranks))
+        nxt = update_alpha(self.alphas, self.runtimes, self.alpha_max)
+        if abs(nxt - self.alpha) <= 1e-12 * max(1.0, self.alpha_max):
+            return False
+        self.alpha = nxt
+        self.operator = self.make_operator(nxt)
+        return True
+
+
 def emulate_gmres_on_one_device(ops, rhs_morton, timeout=120.0, **kw):
     """Distributed GMRES of `len(ops)` ranks on ONE GPU: one host thread per rank, the three
     exchanges replaced by barrier-separated device copies between the handles.  No kernel ever waits

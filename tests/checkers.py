@@ -65,6 +65,12 @@ class _Fmm:
         self._f("box")(self.h, _d(out))
         return out
 
+    def measure_weights(self):
+        """partition.cpp:143-163: (local, remote) per body, caller order"""
+        local, remote = np.zeros(self.n), np.zeros(self.n)
+        getattr(self.lib, f"{self.p}_measure_weights")(self.h, _d(local), _d(remote))
+        return local, remote
+
     def body_order(self):
         out = np.zeros(self.n, dtype=np.uint32)
         self._f("body_order")(self.h, out.ctypes.data_as(C.c_void_p))
@@ -264,6 +270,16 @@ class _VoidLib:
 
     def __getattr__(self, name):
         return getattr(self._lib, name)
+
+
+def update_alpha(lib, prefix, alpha, runtime, alpha_max=2.0):
+    """partition.cpp:175-227 through the reference (prefix "ref") or the oracle ("ho")"""
+    a = np.ascontiguousarray(alpha, dtype=np.float64)
+    r = np.ascontiguousarray(runtime, dtype=np.float64)
+    out = C.c_double()
+    rc = getattr(lib, f"{prefix}_update_alpha")(_d(a), _d(r), len(a), C.c_double(alpha_max), C.byref(out))
+    assert rc == 0
+    return out.value
 
 
 def _oracle_build_corrections(lib, patches, tables, k, mode=2, near_patch_distance=-1.0):

@@ -266,3 +266,41 @@ def test_interaction_lists_cover_every_body_pair_exactly_once():
     leaf = cells[:, 7] == 0
     p2p = op.pairs(1)
     assert leaf[p2p[:, 0]].all() and leaf[p2p[:, 1]].all()
+
+
+def test_measured_weights_and_alpha_cuts(oracle):
+    """per-body work estimates equal the reference's measure_weights
+    (through the oracle restatement, pinned in tests/test_oracle_vs_reference.py); Morton cuts balanced
+    by w = l + alpha r still reproduce the single-domain matvec and balance that estimate"""
+    import torch
+
+    from paper_1803_09948_b200.distributed import emulate_ranks_on_one_device
+
+    n, k, order = 20000, 6.0, 6
+    xyz, q = plummer_points(n, 12), charges(n, 12)
+    single = HfmmCuda(k=k, order=order, ncrit=32, theta=0.4)
+    single.set_points(xyz)
+    fo = oracle.fmm(xyz, k, order, ncrit=32, leaf_cap=1.0 / k, theta=0.4, kd_max=1.0)
+    lo, ro = fo.measure_weights()
+    l, r = single.measure_weights()
+    assert np.array_equal(l, lo) and np.array_equal(r, ro)
+    y1 = single.matvec(q)
+    order_m = single.body_order()
+    for alpha in (0.0, 40.0):
+        ops = []
+        for rank in range(3):
+            op = HfmmCuda(k=k, order=order, ncrit=32, theta=0.4)
+            op.set_partition(rank, 3)
+            op.set_partition_alpha(alpha)
+            op.set_points(xyz)
+            ops.append(op)
+        qm = q[order_m]
+        qd = torch.from_numpy(np.stack([qm.real, qm.imag], 1).astype(np.float32)).cuda()
+        out, parts = emulate_ranks_on_one_device(ops, qd)
+        y = out.cpu().numpy()
+        assert rel_l2(y[:, 0] + 1j * y[:, 1], y1[order_m]) < 3e-6
+        # the cuts balance the chosen estimate: no rank holds more than 45 % of sum(l + alpha r)
+        w = (l + alpha * r)[order_m]
+        tot = [w[int(p.body_first):int(p.body_first) + int(p.body_count)].sum() for p in parts]
+        assert max(tot) / sum(tot) < 0.45
+

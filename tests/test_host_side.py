@@ -102,3 +102,34 @@ def test_workload_generators():
     assert ico.shape == (320, 6, 3) and np.allclose(np.linalg.norm(ico, axis=2), 1.0)
     # config 3: 7 subdivisions -> 327,680 triangles -> 983,040 order-1 unknowns
     assert 20 * 4 ** 7 == 327_680
+
+
+def test_update_alpha_matches_the_oracle_and_converges(oracle):
+    """hfmm_partition_update_alpha (host logic, no GPU): the reference's golden-section replay
+    (partition.cpp:175-227) — same answers as the oracle restatement on arbitrary histories, and the
+    driver loop homes in on the minimum of a noisy runtime curve"""
+    from checkers import update_alpha as checker_update_alpha
+    from paper_1803_09948_b200.api import HfmmError, update_alpha
+
+    rng = np.random.default_rng(17)
+    for _ in range(200):
+        m = int(rng.integers(1, 10))
+        amax = float(rng.choice([0.5, 2.0, 64.0]))
+        a, t = rng.uniform(0, amax, m), rng.uniform(1, 2, m)
+        if rng.random() < 0.5:   # histories that follow the search path exercise the deeper branches
+            a[0] = amax - 0.6180339887498948 * amax
+            if m > 1:
+                a[1] = 0.6180339887498948 * amax
+        assert update_alpha(a, t, amax) == checker_update_alpha(oracle.lib, "ho", a, t, amax)
+    hist_a, hist_t = [], []
+    alpha = 2.0 - 0.6180339887498948 * 2.0
+    for _ in range(14):
+        hist_a.append(alpha)
+        hist_t.append((alpha - 1.3) ** 2 + 0.5)
+        alpha = update_alpha(hist_a, hist_t, 2.0)
+    assert abs(alpha - 1.3) < 0.02
+    for bad in (([], [], 2.0), ([0.5], [1.0], 0.0)):
+        with pytest.raises(HfmmError) as e:
+            update_alpha(*bad)
+        assert e.value.kind == "config_error"
+

@@ -38,3 +38,36 @@ def test_simulated_ranks_reproduce_single_domain(oracle, ref):
         yd, let_bytes = ref.distributed_matvec(xyz, q, 2.0, 8, nr, ncrit=32, leaf_cap=0.5)
         assert rel_l2(yd, y1) < 1e-8
         assert (let_bytes > 0).all()
+
+
+def test_repartitioning_loop_pieces(oracle, ref):
+    """measure_weights and update_alpha (partition.cpp:143-227): oracle restatement vs the reference"""
+    from checkers import update_alpha
+    from paper_1803_09948_b200.workloads import plummer_points, sphere_points
+
+    for xyz, k, cap in ((sphere_points(3000, 3), 3.0, 1.0 / 3.0), (plummer_points(2500, 4), 6.0, 0.0)):
+        fo = oracle.fmm(xyz, k, 6, ncrit=24, leaf_cap=cap, theta=0.4, kd_max=1.0)
+        fr = ref.fmm(xyz, k, 6, ncrit=24, leaf_cap=cap, theta=0.4, kd_max=1.0)
+        lo, ro = fo.measure_weights()
+        lr, rr = fr.measure_weights()
+        assert np.array_equal(lo, lr) and np.array_equal(ro, rr)
+        assert lo.sum() == fo.counts()["p2p_body_pairs"]
+    rng = np.random.default_rng(5)
+    curve = lambda a: (a - 0.7) ** 2 + 1.0
+    hist_a, hist_t = [], []
+    for step in range(16):       # replay the search the way the driver would: probe, measure, ask again
+        a_ref = update_alpha(ref.lib, "ref", hist_a, hist_t) if hist_a else None
+        if hist_a:
+            a_or = update_alpha(oracle.lib, "ho", hist_a, hist_t)
+            assert a_or == a_ref
+            nxt = a_ref
+        else:
+            nxt = 2.0 - 0.6180339887498948 * 2.0
+        hist_a.append(nxt)
+        hist_t.append(curve(nxt) + 1e-3 * rng.standard_normal())
+    assert abs(hist_a[-1] - 0.7) < 0.05
+    for _ in range(50):          # arbitrary histories
+        m = int(rng.integers(1, 9))
+        a, t = rng.uniform(0, 2, m), rng.uniform(1, 2, m)
+        assert update_alpha(oracle.lib, "ho", a, t) == update_alpha(ref.lib, "ref", a, t)
+
