@@ -46,7 +46,8 @@ enum {
 };
 
 /* POD mirror of WaveNumber (common.hpp:37-40), TraversalConfig (traversal.hpp:11-18) and the
- * build_tree arguments (octree.hpp:84-90).  wave_i must be 0 in this release. */
+ * build_tree arguments (octree.hpp:84-90).  k = wave_r + i wave_i (WaveNumber,
+ * common.hpp:36-40): wave_r > 0, |wave_i| <= 4 wave_r; wave_i > 0 is attenuation e^{-wave_i R}. */
 typedef struct {
   double wave_r, wave_i;
   int order;       /* expansion order P (execute_plan `order`, traversal.hpp:59-62)           */

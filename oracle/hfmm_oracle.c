@@ -874,6 +874,26 @@ void ho_direct_sum(long n, const double* xyz, const double* q, double k, long nt
   }
 }
 
+/* complex wavenumber k = kr + i ki (ref: include/hfmm/kernel.hpp:16-23: amp = exp(-ki R) / (4 pi R)) */
+void ho_direct_sum_complex_k(long n, const double* xyz, const double* q, double kr, double ki, long nt,
+                             const long long* target_index, double* out) {
+#pragma omp parallel for schedule(static)
+  for (long t = 0; t < nt; ++t) {
+    const long long ti = target_index ? target_index[t] : t;
+    const double* pt = xyz + 3 * ti;
+    zc acc = 0;
+    for (long j = 0; j < n; ++j) {
+      const double dx = pt[0] - xyz[3 * j], dy = pt[1] - xyz[3 * j + 1], dz = pt[2] - xyz[3 * j + 2];
+      const double r2 = dx * dx + dy * dy + dz * dz;
+      if (r2 == 0) continue;
+      const double R = sqrt(r2), amp = exp(-ki * R) / (4.0 * HO_PI * R), ph = kr * R;
+      acc += (amp * cos(ph) + I * amp * sin(ph)) * (q[2 * j] + I * q[2 * j + 1]);
+    }
+    out[2 * t] = creal(acc);
+    out[2 * t + 1] = cimag(acc);
+  }
+}
+
 /* ------------------------------------------------------------------------------------------
  * GMRES — ref: src/gmres.cpp:35-174.  x0 = 0; modified Gram-Schmidt plus one unconditional
  * re-orthogonalisation pass; complex Givens; stop on |g_{j+1}| <= rtol*||b||; true residual

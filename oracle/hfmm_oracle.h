@@ -67,6 +67,10 @@ void ho_block_lu_solve(long npatch, int ni, const double* block_lu, const int* b
                        double* x);
 
 
+/* direct sum for a complex wavenumber kr + i ki (kernel.hpp:16-23) */
+void ho_direct_sum_complex_k(long n, const double* xyz, const double* q, double kr, double ki, long nt,
+                             const long long* target_index, double* out);
+
 /* ---- repartitioning loop (ref: src/partition.cpp:137-227) -------------------------------------- */
 /* per-body work estimates in caller order: local = P2P partners, remote = M2L pairs of every cell above the body */
 void ho_measure_weights(const ho_fmm* h, double* local, double* remote);

@@ -146,6 +146,8 @@ class HfmmCuda:
                  kd_max: float = 1.0, leaf_cap: float = -1.0, grain: int | None = None,
                  device: int = 0, flags: int = 0, wave_i: float = 0.0):
         self.lib = load_library()
+        if np.iscomplexobj(k):        # k = k_r + i k_i (attenuation), the reference's WaveNumber
+            k, wave_i = float(np.real(k)), float(np.imag(k))
         cfg = _Config(float(k), float(wave_i), int(order), int(ncrit),
                       int(grain if grain is not None else ncrit), float(theta), float(kd_max),
                       float(leaf_cap), int(device), int(flags))
@@ -389,9 +391,9 @@ def debug_compose_translation(order, k, t, kind, s_src=1.0, s_dst=1.0):
     dim = (order + 1) ** 2
     out = np.zeros((dim, dim), dtype=np.complex128)
     t = np.ascontiguousarray(t, dtype=np.float64)
-    rc = lib.hfmm_debug_compose_translation(int(order), C.c_double(k), t.ctypes.data_as(_dp),
-                                            int(kind), C.c_double(s_src), C.c_double(s_dst),
-                                            out.ctypes.data_as(_dp))
+    rc = lib.hfmm_debug_compose_translation_ck(int(order), C.c_double(np.real(k)), C.c_double(np.imag(k)),
+                                               t.ctypes.data_as(_dp), int(kind), C.c_double(s_src),
+                                               C.c_double(s_dst), out.ctypes.data_as(_dp))
     if rc:
         raise HfmmError(rc, lib.hfmm_cuda_last_error(None).decode())
     return out

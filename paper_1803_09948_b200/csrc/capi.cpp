@@ -278,6 +278,14 @@ int hfmm_debug_compose_translation(int order, double k, const double* t, int kin
   });
 }
 
+int hfmm_debug_compose_translation_ck(int order, double kr, double ki, const double* t, int kind, double s_src,
+                                      double s_dst, double* out) {
+  return guarded(nullptr, [&] {
+    if (order < 0 || order > hfmm_b200::kMaxOrder) throw Error(HFMM_ERR_CONFIG, "order out of range");
+    hfmm_b200::compose_dense_from_tables(order, kr, t, kind, s_src, s_dst, out, ki);
+  });
+}
+
 // tree + lists of the host builder without touching a device: counts[0..4] = cells, leaves,
 // m2l pairs, p2p leaf pairs, max level
 int hfmm_debug_host_tree(const double* xyz, size_t n, int ncrit, double leaf_cap, double k,

@@ -117,11 +117,15 @@ Engine::Engine(const hfmm_cuda_config& cfg) : cfg_(cfg) {
   if (cfg.order < 0) throw Error(HFMM_ERR_CONFIG, "expansion order must be non-negative");
   if (cfg.order > kMaxOrder)
     throw Error(HFMM_ERR_CONFIG, "expansion order above the supported maximum (16)");
-  if (cfg.wave_i != 0) throw Error(HFMM_ERR_CONFIG, "complex wavenumbers (wave_i != 0) unsupported");
-  if (!(cfg.wave_r > 0)) throw Error(HFMM_ERR_CONFIG, "wavenumber must be positive");
+  // complex wavenumber k = wave_r + i wave_i (common.hpp:36-40): coordinates are scaled by wave_r,
+  // so the real part must be positive; wave_i (attenuation) enters the radial functions, the
+  // translation tables and the near-field amplitude
+  if (!(cfg.wave_r > 0)) throw Error(HFMM_ERR_CONFIG, "the real part of the wavenumber must be positive");
+  if (!(cfg.wave_i == cfg.wave_i) || std::abs(cfg.wave_i) > 4.0 * cfg.wave_r)
+    throw Error(HFMM_ERR_CONFIG, "wave_i must be finite with |wave_i| <= 4 wave_r");
   if (cfg.kd_max < 0) throw Error(HFMM_ERR_CONFIG, "kd_max must be non-negative");
   leaf_cap_ = cfg.leaf_cap;
-  if (leaf_cap_ < 0) leaf_cap_ = cfg.kd_max > 0 ? cfg.kd_max / std::abs(cfg.wave_r) : 0.0;
+  if (leaf_cap_ < 0) leaf_cap_ = cfg.kd_max > 0 ? cfg.kd_max / std::hypot(cfg.wave_r, cfg.wave_i) : 0.0;  // kd_max / |k|
   threads_ = int(std::max(1u, std::thread::hardware_concurrency()));
 
   int ndev = 0;
@@ -314,7 +318,8 @@ void Engine::finish_far_field(TableRegistry& reg) {
   const CoaxBuilder builder(P);
   parallel_for(ncoax, threads_, [&](size_t i) {
     const auto& s = reg.coax_specs[i];
-    builder.build(s.kind, k, s.dist, s.s_src, s.s_dst, coax.data() + i * size_t(coax_table_size(P)) * 2);
+    builder.build(s.kind, k, s.dist, s.s_src, s.s_dst, coax.data() + i * size_t(coax_table_size(P)) * 2,
+                  cfg_.wave_i);
   });
   rot_tables_.upload(rot, stream_);
   coax_tables_.upload(coax, stream_);
@@ -513,7 +518,8 @@ void Engine::set_points_device(const double* xyz, size_t n) {
   const TreeArrays& t = tree_;
   DeviceCells cells;
   cells.upload(t, stream_);
-  dual_tree_traversal_device(t, cells, std::abs(k), cfg_.theta, cfg_.kd_max, dev_pairs_, stream_);
+  dual_tree_traversal_device(t, cells, std::hypot(cfg_.wave_r, cfg_.wave_i), cfg_.theta, cfg_.kd_max, dev_pairs_,
+                             stream_);  // the gate uses |k| (traversal.cpp:86)
   far_pair_level_range(dev_pairs_, cells, lmin_dst_, lmin_src_, stream_);
   have_far_ = dev_pairs_.n_far > 0;
   stats_.m2l_pairs = dev_pairs_.n_far;
@@ -563,7 +569,7 @@ void Engine::set_points_device(const double* xyz, size_t n) {
 // ---- builder on the host (HFMM_FLAG_HOST_TREE): host_tree.cpp ---------------------------------
 void Engine::set_points_host(const double* xyz, size_t n) {
   build_tree_host(tree_, xyz, n, cfg_.ncrit, leaf_cap_, threads_);
-  dual_tree_traversal_host(tree_, std::abs(cfg_.wave_r), cfg_.theta, cfg_.kd_max, pairs_, threads_);
+  dual_tree_traversal_host(tree_, std::hypot(cfg_.wave_r, cfg_.wave_i), cfg_.theta, cfg_.kd_max, pairs_, threads_);
   const TreeArrays& t = tree_;
   const size_t nc = t.n_cells();
   const double k = cfg_.wave_r;
@@ -693,6 +699,7 @@ void Engine::phase_upward() {
   pa.out = near_.get();
   pa.kunit = kunit_;
   pa.out_scale = float(cfg_.wave_r / (4.0 * kPi));
+  pa.damp = float(cfg_.wave_i / cfg_.wave_r * 1.4426950408889634);
   cudaStream_t sn = serial ? stream_ : stream_near_;
   HFMM_CUDA_CHECK(cudaEventRecord(ev_[0], sn));
   launch_p2p(pa, sn);
@@ -710,6 +717,7 @@ void Engine::phase_upward() {
     la.order = cfg_.order;
     la.stride = stride_;
     la.k = float(cfg_.wave_r);
+    la.k_imag = float(cfg_.wave_i);
     la.leaves = p2m_leaves_.get();
     la.n_leaves = n_p2m_leaves_;
     HFMM_CUDA_CHECK(cudaEventRecord(ev_[2], stream_));
@@ -750,6 +758,7 @@ void Engine::phase_downward() {
     la.order = cfg_.order;
     la.stride = stride_;
     la.k = float(cfg_.wave_r);
+    la.k_imag = float(cfg_.wave_i);
     HFMM_CUDA_CHECK(cudaEventRecord(ev_[12], stream_));
     run_stage(m2l_, multipole_.get(), local_.get());
     HFMM_CUDA_CHECK(cudaEventRecord(ev_[5], stream_));
@@ -977,7 +986,7 @@ void Engine::get_expansions(int which, double* out) {
 }
 
 void compose_dense_from_tables(int order, double k, const double t[3], int kind, double s_src,
-                               double s_dst, double* out) {
+                               double s_dst, double* out, double k_imag) {
   using cd = std::complex<double>;
   const int P = order, dim = nm_total(P);
   const double r = std::sqrt(t[0] * t[0] + t[1] * t[1] + t[2] * t[2]);
@@ -987,7 +996,7 @@ void compose_dense_from_tables(int order, double k, const double t[3], int kind,
   build_rotation_table(P, t[2] / r, rot.data());
   const CoaxBuilder builder(P);
   // kind 0: M2L with (s_src, s_dst); kind 1: regular shift expressed through the M2M scaling
-  builder.build(kind == 0 ? CoaxKind::m2l : CoaxKind::m2m, k, r, s_src, s_dst, coax.data());
+  builder.build(kind == 0 ? CoaxKind::m2l : CoaxKind::m2m, k, r, s_src, s_dst, coax.data(), k_imag);
   std::vector<cd> ph(2 * P + 1);
   for (int m = -P; m <= P; ++m) ph[m + P] = std::pow(cd(cphi, sphi), m);
   // R[(n,m'),(n,m)] = E_n[m][m'] e^{i m phi};  Chat[(nu,m),(n,m)]

@@ -162,6 +162,6 @@ class Engine {
 // reference's UNSCALED convention — used by the CPU-side table tests against
 // fmm::translation_matrix (expansion.cpp:95-124).  kind: 0 M2L (singular), 1 regular.
 void compose_dense_from_tables(int order, double k, const double t[3], int kind, double s_src,
-                               double s_dst, double* out_complex);
+                               double s_dst, double* out_complex, double k_imag = 0.0);
 
 }  // namespace hfmm_b200

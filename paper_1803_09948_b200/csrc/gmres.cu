@@ -480,7 +480,7 @@ void Engine::evaluate_field(const double* coeff, const double* obs, size_t nobs,
   odev.upload(o, stream_);
   DeviceBuffer<double2> res(nobs);
   launch_field(n, body_abs_.get(), body_q_.get(), odev.get(), uint32_t(nobs), float(k / (4.0 * kPi)),
-               res.get(), stream_);
+               float(cfg_.wave_i / cfg_.wave_r), res.get(), stream_);
   res.download(reinterpret_cast<double2*>(out), nobs, stream_);
   HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
 }

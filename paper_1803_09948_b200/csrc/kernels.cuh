@@ -51,6 +51,7 @@ struct P2PArgs {
   double kunit_d;    // the same in FP64 (exact offsets for the compensated path)
   double grid;       // power of two; hi parts and hi offsets are integer multiples of it
   float out_scale;   // k / (4 pi)
+  float damp;        // (k_i / k_r) log2(e): complex wavenumber, amplitude 2^{-damp R'}; 0 for real k
 };
 void launch_p2p(const P2PArgs& a, cudaStream_t s);
 
@@ -64,7 +65,8 @@ struct LeafExpansionArgs {
   const float* level_scale;  // s_l = k * side(l), indexed by level
   int order;
   int stride;                // coefficient row stride (complex elements)
-  float k;                   // real wavenumber
+  float k;                   // Re k
+  float k_imag;              // Im k (attenuation); 0 selects the real-argument kernels
 };
 void launch_p2m(const LeafExpansionArgs& a, const float2* body_q, float2* multipole, cudaStream_t s);
 // out[slot] = sum over the leaf's local expansion (overwrites; bodies of unlisted leaves untouched)
@@ -160,9 +162,10 @@ void launch_update_solution(uint32_t n, int cols, const float2* basis, size_t ld
 void launch_residual(uint32_t n, const double2* b, const float2* ax, float2* r32, double* out,
                      cudaStream_t s);
 void launch_narrow(uint32_t n, const double2* in, float2* out, cudaStream_t s);
-// out[o] = scale * sum_i q_i e^{i|o-x_i|}/|o-x_i| over k-scaled absolute coordinates
+// out[o] = scale * sum_i q_i e^{i|o-x_i|} e^{-eps |o-x_i|}/|o-x_i| over k_r-scaled absolute coordinates
+// (eps = k_i / k_r, 0 for a real wavenumber)
 void launch_field(uint32_t n, const float4* src_pos, const float2* q, const float4* obs, uint32_t nobs,
-                  float scale, double2* out, cudaStream_t s);
+                  float scale, float eps, double2* out, cudaStream_t s);
 void launch_widen(uint32_t n, const float2* in, double2* out, cudaStream_t s);
 
 // out[s] = near[s] + far[s] + corr[index[s]], s over the owned Morton slots (corr may be null)

@@ -77,6 +77,76 @@ __device__ void scaled_bessel(int P, float z, float s, float* out) {
   }
 }
 
+// complex wavenumber k = k_r (1 + i eps), eps = k_i / k_r: the argument is z = kappa z' with z' = k_r rho
+// the stored (real) coordinate and kappa = 1 + i eps; the same series in complex arithmetic
+// (reference special.cpp:16-54 takes a complex argument throughout)
+__device__ void scaled_bessel_complex(int P, float zr, float eps, float s, float* out_re, float* out_im) {
+  const float zmod = zr * sqrtf(1.0f + eps * eps);
+  if (zmod <= 2.0f) {
+    // h = -z^2 / 2 = -(1 - eps^2 + 2 i eps) z'^2 / 2,   t = z / s
+    const float hr = -0.5f * zr * zr * (1.0f - eps * eps), hi = -zr * zr * eps;
+    const float tr = zr / s, ti = tr * eps;
+    float pr = 1.0f, pi = 0.0f;
+    const int terms = zmod <= 1.0f ? 7 : kSeriesTerms;
+    for (int n = 0; n <= P; ++n) {
+      float ter = 1.0f, tei = 0.0f, sr = 1.0f, si = 0.0f;
+      const float* inv = c_series + n * kSeriesTerms;
+      for (int j = 0; j < terms; ++j) {
+        const float ar = hr * inv[j], ai = hi * inv[j];
+        const float nr = ter * ar - tei * ai;
+        tei = ter * ai + tei * ar;
+        ter = nr;
+        sr += ter;
+        si += tei;
+      }
+      out_re[n * 32] = pr * sr - pi * si;
+      out_im[n * 32] = pr * si + pi * sr;
+      const float qr = pr * tr - pi * ti;
+      pi = pr * ti + pi * tr;
+      pr = qr;
+    }
+    return;
+  }
+  // Miller's downward recurrence in complex FP64, normalised by j_0 = sin z / z
+  const double zx = zr, zy = double(zr) * eps;
+  const double zn2 = zx * zx + zy * zy;
+  const double ix = zx / zn2, iy = -zy / zn2;  // 1 / z
+  const int start = P + 24 + int(sqrt(zn2));
+  double ax = 0, ay = 0, cx = 1e-280, cy = 0;
+  double kx[kMaxP + 1], ky[kMaxP + 1];
+  for (int n = start; n >= 0; --n) {
+    const double f = 2.0 * n + 3.0;
+    const double mx = f * (ix * cx - iy * cy), my = f * (ix * cy + iy * cx);
+    const double bx = mx - ax, by = my - ay;
+    ax = cx;
+    ay = cy;
+    cx = bx;
+    cy = by;
+    if (n <= P) {
+      kx[n] = cx;
+      ky[n] = cy;
+    }
+    if (fabs(cx) + fabs(cy) > 1e250) {
+      cx *= 1e-250; cy *= 1e-250; ax *= 1e-250; ay *= 1e-250;
+      for (int i = n < P ? n : P; i <= P; ++i) {
+        kx[i] *= 1e-250;
+        ky[i] *= 1e-250;
+      }
+    }
+  }
+  // sin(x + i y) = sin x cosh y + i cos x sinh y
+  const double snx = sin(zx) * cosh(zy), sny = cos(zx) * sinh(zy);
+  const double j0x = snx * ix - sny * iy, j0y = snx * iy + sny * ix;
+  const double cn2 = cx * cx + cy * cy;
+  const double scx = (j0x * cx + j0y * cy) / cn2, scy = (j0y * cx - j0x * cy) / cn2;  // j_0 / cur
+  double f = 1.0;  // (2n+1)!!/s^n
+  for (int n = 0; n <= P; ++n) {
+    out_re[n * 32] = float((kx[n] * scx - ky[n] * scy) * f);
+    out_im[n * 32] = float((kx[n] * scy + ky[n] * scx) * f);
+    f *= (2.0 * n + 3.0) / double(s);
+  }
+}
+
 struct BodyFrame {
   float ct, st, cphi, sphi, z;
 };
@@ -110,13 +180,18 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+// CK: complex wavenumber (radial functions and the i k q weight are complex)
+template <bool CK>
 __global__ void __launch_bounds__(kWarps * 32)
 p2m_kernel(const LeafExpansionArgs a, const float2* __restrict__ body_q, float2* __restrict__ multipole) {
   extern __shared__ float smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int P = a.order, dim = (P + 1) * (P + 1);
-  float* s_j = smem + warp * ((P + 1) * 32 + 2 * dim);  // [n][lane]
-  float2* s_acc = reinterpret_cast<float2*>(s_j + (P + 1) * 32);
+  constexpr int kPlanes = CK ? 2 : 1;
+  float* s_j = smem + warp * (kPlanes * (P + 1) * 32 + 2 * dim);  // [n][lane] (+ imaginary plane)
+  float* s_ji = s_j + (P + 1) * 32;
+  float2* s_acc = reinterpret_cast<float2*>(s_j + kPlanes * (P + 1) * 32);
+  const float eps = CK ? a.k_imag / a.k : 0.0f;
   const uint32_t li = blockIdx.x * kWarps + warp;
   if (li >= a.n_leaves) return;
   const uint32_t cell = a.leaves[li];
@@ -130,9 +205,10 @@ p2m_kernel(const LeafExpansionArgs a, const float2* __restrict__ body_q, float2*
     const float4 p = ok ? a.body_pos[cb.x + base + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
     const float2 q = ok ? body_q[cb.x + base + lane] : make_float2(0.f, 0.f);
     const BodyFrame f = body_frame(p);
-    scaled_bessel(P, f.z, s, s_j + lane);
+    if (CK) scaled_bessel_complex(P, f.z, eps, s, s_j + lane, s_ji + lane);
+    else scaled_bessel(P, f.z, s, s_j + lane);
     // w = i k q
-    const float wr = -a.k * q.y, wi = a.k * q.x;
+    const float wr = -a.k * q.y - (CK ? a.k_imag * q.x : 0.0f), wi = a.k * q.x - (CK ? a.k_imag * q.y : 0.0f);
     float cm = 1.0f, sm = 0.0f;     // cos(m phi), sin(m phi)
     float pmm = kInvSqrt4Pi;        // Pbar_m^m
     for (int m = 0; m <= P; ++m) {
@@ -150,9 +226,10 @@ p2m_kernel(const LeafExpansionArgs a, const float2* __restrict__ body_q, float2*
         else pn = c_a[n * (n + 1) / 2 + m] * f.ct * p1 - c_b[n * (n + 1) / 2 + m] * p2;
         p2 = p1;
         p1 = pn;
-        const float g = s_j[n * 32 + lane] * pn;
+        const float g = s_j[n * 32 + lane] * pn, gi = CK ? s_ji[n * 32 + lane] * pn : 0.0f;
         // +m: conj Y = Pbar (cm - i sm)
-        float vr = g * (wr * cm + wi * sm), vi = g * (wi * cm - wr * sm);
+        const float br = wr * cm + wi * sm, bi = wi * cm - wr * sm;
+        float vr = g * br - gi * bi, vi = g * bi + gi * br;
         vr = warp_sum(vr);
         vi = warp_sum(vi);
         if (lane == 0) {
@@ -162,8 +239,9 @@ p2m_kernel(const LeafExpansionArgs a, const float2* __restrict__ body_q, float2*
         }
         if (m > 0) {
           // -m: conj Y_n^{-m} = (-1)^m Pbar (cm + i sm)
-          const float sg = (m & 1) ? -g : g;
-          float ur = sg * (wr * cm - wi * sm), ui = sg * (wi * cm + wr * sm);
+          const float sg = (m & 1) ? -1.0f : 1.0f;
+          const float er = wr * cm - wi * sm, ei = wi * cm + wr * sm;
+          float ur = sg * (g * er - gi * ei), ui = sg * (g * ei + gi * er);
           ur = warp_sum(ur);
           ui = warp_sum(ui);
           if (lane == 0) {
@@ -181,13 +259,17 @@ p2m_kernel(const LeafExpansionArgs a, const float2* __restrict__ body_q, float2*
   for (int i = lane; i < dim; i += 32) dst[i] = s_acc[i];
 }
 
+template <bool CK>
 __global__ void __launch_bounds__(kWarps * 32)
 l2p_kernel(const LeafExpansionArgs a, const float2* __restrict__ local, float2* __restrict__ out) {
   extern __shared__ float smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int P = a.order, dim = (P + 1) * (P + 1);
-  float* s_j = smem + warp * ((P + 1) * 32 + 2 * dim);
-  float2* s_loc = reinterpret_cast<float2*>(s_j + (P + 1) * 32);
+  constexpr int kPlanes = CK ? 2 : 1;
+  float* s_j = smem + warp * (kPlanes * (P + 1) * 32 + 2 * dim);
+  float* s_ji = s_j + (P + 1) * 32;
+  float2* s_loc = reinterpret_cast<float2*>(s_j + kPlanes * (P + 1) * 32);
+  const float eps = CK ? a.k_imag / a.k : 0.0f;
   const uint32_t li = blockIdx.x * kWarps + warp;
   if (li >= a.n_leaves) return;
   const uint32_t cell = a.leaves[li];
@@ -201,7 +283,8 @@ l2p_kernel(const LeafExpansionArgs a, const float2* __restrict__ local, float2* 
     const bool ok = base + lane < cb.y;
     const float4 p = ok ? a.body_pos[cb.x + base + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
     const BodyFrame f = body_frame(p);
-    scaled_bessel(P, f.z, s, s_j + lane);
+    if (CK) scaled_bessel_complex(P, f.z, eps, s, s_j + lane, s_ji + lane);
+    else scaled_bessel(P, f.z, s, s_j + lane);
     float accr = 0.0f, acci = 0.0f;
     float cm = 1.0f, sm = 0.0f, pmm = kInvSqrt4Pi;
     for (int m = 0; m <= P; ++m) {
@@ -222,18 +305,20 @@ l2p_kernel(const LeafExpansionArgs a, const float2* __restrict__ local, float2* 
         p1 = pn;
         // Lhat pairs with j_n (2n-1)!!/s^n = jhat_n / (2n+1)
         const float g = s_j[n * 32 + lane] * pn / float(2 * n + 1);
+        const float gi = CK ? s_ji[n * 32 + lane] * pn / float(2 * n + 1) : 0.0f;
         const float2 lp = s_loc[n * (n + 1) + m];
         if (m == 0) {
-          sr += g * lp.x;
-          si += g * lp.y;
+          sr += g * lp.x - gi * lp.y;
+          si += g * lp.y + gi * lp.x;
         } else {
           const float2 lm = s_loc[n * (n + 1) - m];
           const float sg = (m & 1) ? -1.0f : 1.0f;
           // L^m (cm + i sm) + (-1)^m L^-m (cm - i sm)
           const float er = lp.x + sg * lm.x, ei = lp.y + sg * lm.y;   // multiplies cm
           const float dr = lp.x - sg * lm.x, di = lp.y - sg * lm.y;   // multiplies i sm
-          sr += g * (er * cm - di * sm);
-          si += g * (ei * cm + dr * sm);
+          const float xr = er * cm - di * sm, xi = ei * cm + dr * sm;
+          sr += g * xr - gi * xi;
+          si += g * xi + gi * xr;
         }
       }
       accr += sr;
@@ -244,9 +329,9 @@ l2p_kernel(const LeafExpansionArgs a, const float2* __restrict__ local, float2* 
   }
 }
 
-size_t leaf_smem_bytes(int order) {
+size_t leaf_smem_bytes(int order, bool complex_k) {
   const int dim = (order + 1) * (order + 1);
-  return size_t(kWarps) * ((order + 1) * 32 + 2 * dim) * sizeof(float);
+  return size_t(kWarps) * ((complex_k ? 2 : 1) * (order + 1) * 32 + 2 * dim) * sizeof(float);
 }
 
 }  // namespace
@@ -268,14 +353,20 @@ void upload_legendre_constants(const float* diag, const float* sub, const float*
 void launch_p2m(const LeafExpansionArgs& a, const float2* body_q, float2* multipole, cudaStream_t s) {
   if (a.n_leaves == 0) return;
   const uint32_t blocks = (a.n_leaves + kWarps - 1) / kWarps;
-  p2m_kernel<<<blocks, kWarps * 32, leaf_smem_bytes(a.order), s>>>(a, body_q, multipole);
+  if (a.k_imag != 0.0f)
+    p2m_kernel<true><<<blocks, kWarps * 32, leaf_smem_bytes(a.order, true), s>>>(a, body_q, multipole);
+  else
+    p2m_kernel<false><<<blocks, kWarps * 32, leaf_smem_bytes(a.order, false), s>>>(a, body_q, multipole);
   HFMM_CUDA_CHECK(cudaGetLastError());
 }
 
 void launch_l2p(const LeafExpansionArgs& a, const float2* local, float2* out, cudaStream_t s) {
   if (a.n_leaves == 0) return;
   const uint32_t blocks = (a.n_leaves + kWarps - 1) / kWarps;
-  l2p_kernel<<<blocks, kWarps * 32, leaf_smem_bytes(a.order), s>>>(a, local, out);
+  if (a.k_imag != 0.0f)
+    l2p_kernel<true><<<blocks, kWarps * 32, leaf_smem_bytes(a.order, true), s>>>(a, local, out);
+  else
+    l2p_kernel<false><<<blocks, kWarps * 32, leaf_smem_bytes(a.order, false), s>>>(a, local, out);
   HFMM_CUDA_CHECK(cudaGetLastError());
 }
 

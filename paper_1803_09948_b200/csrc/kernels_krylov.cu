@@ -210,7 +210,7 @@ widen_kernel(uint32_t n, const float2* __restrict__ in, double2* __restrict__ ou
 // plain single-layer sum at exterior points (solver.cpp:393-419): one block per observation
 __global__ void __launch_bounds__(kBlock)
 field_kernel(uint32_t n, const float4* __restrict__ src_pos, const float2* __restrict__ q,
-             const float4* __restrict__ obs, float scale, double2* __restrict__ out) {
+             const float4* __restrict__ obs, float scale, float eps, double2* __restrict__ out) {
   const float4 o = obs[blockIdx.x];
   double re = 0, im = 0;
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
@@ -219,7 +219,8 @@ field_kernel(uint32_t n, const float4* __restrict__ src_pos, const float2* __res
     const float dx = o.x - p.x, dy = o.y - p.y, dz = o.z - p.z;
     const float r2 = dx * dx + dy * dy + dz * dz;
     if (r2 > 0.f) {
-      const float rinv = rsqrtf(r2), r = r2 * rinv;
+      const float r0 = rsqrtf(r2), r = r2 * r0;
+      const float rinv = eps != 0.0f ? r0 * expf(-eps * r) : r0;  // complex k: e^{-k_i R} (kernel.hpp:20)
       float sn, cs;
       sincosf(r, &sn, &cs);
       const float gr = rinv * cs, gi = rinv * sn;
@@ -282,9 +283,9 @@ void launch_residual(uint32_t n, const double2* b, const float2* ax, float2* r32
   HFMM_CUDA_CHECK(cudaGetLastError());
 }
 void launch_field(uint32_t n, const float4* src_pos, const float2* q, const float4* obs, uint32_t nobs,
-                  float scale, double2* out, cudaStream_t s) {
+                  float scale, float eps, double2* out, cudaStream_t s) {
   if (!n || !nobs) return;
-  field_kernel<<<nobs, kBlock, 0, s>>>(n, src_pos, q, obs, scale, out);
+  field_kernel<<<nobs, kBlock, 0, s>>>(n, src_pos, q, obs, scale, eps, out);
   HFMM_CUDA_CHECK(cudaGetLastError());
 }
 void launch_narrow(uint32_t n, const double2* in, float2* out, cudaStream_t s) {

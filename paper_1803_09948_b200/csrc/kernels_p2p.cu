@@ -34,6 +34,11 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float sin_approx(float x) {
   float y;
   asm("sin.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -85,9 +90,13 @@ struct SourceQ {
   u64 qr, qi, nqi;
 };
 
-// acc += (rinv e^{i r2 rinv}) * q for a pair of targets
-__device__ __forceinline__ void green_accumulate2(u64 r2, u64 rinv, const SourceQ& q, u64& ar, u64& ai) {
+// acc += (rinv e^{i r2 rinv}) * q for a pair of targets.  DAMP: complex wavenumber k_r + i k_i, the
+// amplitude decays as e^{-k_i R} = 2^{-damp R'} with R' = k_r R (kernel.hpp:20), one more MUFU
+template <bool DAMP>
+__device__ __forceinline__ void green_accumulate2(u64 r2, u64 rinv, const SourceQ& q, float damp, u64& ar,
+                                                  u64& ai) {
   const float2 r = unpack2(mul2(r2, rinv));
+  if (DAMP) rinv = mul2(rinv, pack2(ex2_approx(-damp * r.x), ex2_approx(-damp * r.y)));
   const u64 c = pack2(cos_approx(r.x), cos_approx(r.y)), s = pack2(sin_approx(r.x), sin_approx(r.y));
   const u64 gr = mul2(rinv, c), gi = mul2(rinv, s);
   ar = fma2(gr, q.qr, ar);
@@ -104,8 +113,9 @@ constexpr int kPairs = kTile / 2;
 
 // plain path: one FP32 coordinate per axis.  nsx = (-sx, -sx) etc.  Slots past n_t inside the last
 // group hold zero coordinates; their accumulators are never stored.
+template <bool DAMP>
 __device__ __forceinline__ void accumulate_plain(uint32_t tx, uint32_t ty, uint32_t tz, uint32_t n_t,
-                                                 u64 nsx, u64 nsy, u64 nsz, const SourceQ& q,
+                                                 u64 nsx, u64 nsy, u64 nsz, const SourceQ& q, float damp,
                                                  u64 (&ar)[kPairs], u64 (&ai)[kPairs]) {
   const u64 tiny = pack2(1e-30f, 1e-30f);
 #pragma unroll
@@ -121,16 +131,17 @@ __device__ __forceinline__ void accumulate_plain(uint32_t tx, uint32_t ty, uint3
         const u64 r2 = fma2(dz, dz, fma2(dy, dy, fma2(dx, dx, tiny)));
         const float2 r2s = unpack2(r2);
         const u64 rinv = pack2(rsqrt_approx(r2s.x), rsqrt_approx(r2s.y));
-        green_accumulate2(r2, rinv, q, ar[t0 / 2 + j], ai[t0 / 2 + j]);
+        green_accumulate2<DAMP>(r2, rinv, q, damp, ar[t0 / 2 + j], ai[t0 / 2 + j]);
       }
     }
 }
 
 // compensated path: d = (hi_t - hi_s) + (lo_t - lo_s); the hi difference is exact (grid multiples);
 // coincident bodies (R == 0) are masked
+template <bool DAMP>
 __device__ __forceinline__ void accumulate_compensated(uint32_t thi, uint32_t tlo, uint32_t n_t, u64 nhx,
                                                        u64 nhy, u64 nhz, u64 nlx, u64 nly, u64 nlz,
-                                                       const SourceQ& q, u64 (&ar)[kPairs],
+                                                       const SourceQ& q, float damp, u64 (&ar)[kPairs],
                                                        u64 (&ai)[kPairs]) {
 #pragma unroll
   for (int t0 = 0; t0 < kTile; t0 += kGroup)
@@ -150,7 +161,7 @@ __device__ __forceinline__ void accumulate_compensated(uint32_t thi, uint32_t tl
         const u64 r2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
         const float2 r2s = unpack2(r2);
         const u64 rinv = pack2(r2s.x > 0.0f ? rsqrt_approx(r2s.x) : 0.0f, r2s.y > 0.0f ? rsqrt_approx(r2s.y) : 0.0f);
-        green_accumulate2(r2, rinv, q, ar[t0 / 2 + j], ai[t0 / 2 + j]);
+        green_accumulate2<DAMP>(r2, rinv, q, damp, ar[t0 / 2 + j], ai[t0 / 2 + j]);
       }
     }
 }
@@ -187,6 +198,7 @@ __device__ __forceinline__ int owner_of(uint32_t incl, uint32_t g) {
 }
 
 // 128 registers per thread keep four CTAs (16 warps) per SM; measured: 134 registers (3 CTAs) cost 40 %
+template <bool DAMP>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) p2p_kernel(const P2PArgs a) {
   // target coordinates, one array per axis: [x | y | z][kTile]
   __shared__ __align__(16) float s_tgt[kWarpsPerBlock][3 * kTile];
@@ -255,8 +267,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) p2p_kernel(const P2PAr
       const float hx = -(sh.x + hxj), hy = -(sh.y + hyj), hz = -(sh.z + hzj);
       const float lx = -(sl.x + lxj), ly = -(sl.y + lyj), lz = -(sl.z + lzj);
       const SourceQ sq{pack2(q.x, q.x), pack2(q.y, q.y), pack2(-q.y, -q.y)};
-      accumulate_compensated(a_thi, a_tlo, tile.n_t, pack2(hx, hx), pack2(hy, hy), pack2(hz, hz),
-                             pack2(lx, lx), pack2(ly, ly), pack2(lz, lz), sq, ar, ai);
+      accumulate_compensated<DAMP>(a_thi, a_tlo, tile.n_t, pack2(hx, hx), pack2(hy, hy), pack2(hz, hz),
+                                   pack2(lx, lx), pack2(ly, ly), pack2(lz, lz), sq, a.damp, ar, ai);
     }
   }
 
@@ -287,8 +299,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) p2p_kernel(const P2PAr
       const float2 q = ok ? a.body_q[slot] : make_float2(0.f, 0.f);
       const float sx = -(sp.x + oxj), sy = -(sp.y + oyj), sz = -(sp.z + ozj);
       const SourceQ sq{pack2(q.x, q.x), pack2(q.y, q.y), pack2(-q.y, -q.y)};
-      accumulate_plain(a_tgt, a_tgt + 4 * kTile, a_tgt + 8 * kTile, tile.n_t, pack2(sx, sx), pack2(sy, sy),
-                       pack2(sz, sz), sq, ar, ai);
+      accumulate_plain<DAMP>(a_tgt, a_tgt + 4 * kTile, a_tgt + 8 * kTile, tile.n_t, pack2(sx, sx), pack2(sy, sy),
+                             pack2(sz, sz), sq, a.damp, ar, ai);
     }
   }
 
@@ -318,7 +330,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) p2p_kernel(const P2PAr
 void launch_p2p(const P2PArgs& a, cudaStream_t s) {
   if (a.n_tiles == 0) return;
   const uint32_t blocks = (a.n_tiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  p2p_kernel<<<blocks, kWarpsPerBlock * 32, 0, s>>>(a);
+  if (a.damp != 0.0f) p2p_kernel<true><<<blocks, kWarpsPerBlock * 32, 0, s>>>(a);
+  else p2p_kernel<false><<<blocks, kWarpsPerBlock * 32, 0, s>>>(a);
   HFMM_CUDA_CHECK(cudaGetLastError());
 }
 

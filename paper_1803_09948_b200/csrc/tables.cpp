@@ -89,6 +89,61 @@ void sph_hn_scaled(int nmax, double z, double* re, double* im) {
   }
 }
 
+// the same two functions for a complex argument (complex wavenumber k = k_r + i k_i,
+// reference src/special.cpp:16-65 takes cplx z throughout)
+using cld = std::complex<long double>;
+void sph_jn_cld(int nmax, cld z, cld* out) {
+  if (std::abs(z) < 1.0L) {
+    const cld h = 0.5L * z * z;
+    cld zn = 1;
+    long double df = 1;
+    for (int n = 0; n <= nmax; ++n) {
+      cld term = 1, sum = 1;
+      for (int j = 1; j < 60; ++j) {
+        term *= -h / ((long double)j * (2 * n + 2 * j + 1));
+        sum += term;
+        if (std::abs(term) < 1e-22L * std::abs(sum)) break;
+      }
+      out[n] = zn / df * sum;
+      zn *= z;
+      df *= (2 * n + 3);
+    }
+    return;
+  }
+  const int start = nmax + 24 + int(std::abs(z));
+  cld above = 0, cur = 1e-40L;
+  std::vector<cld> keep(nmax + 1);
+  for (int n = start; n >= 0; --n) {
+    const cld below = (2.0L * n + 3.0L) / z * cur - above;
+    above = cur;
+    cur = below;
+    if (n <= nmax) keep[n] = cur;
+    if (std::abs(cur) > 1e2000L) {
+      cur *= 1e-2000L;
+      above *= 1e-2000L;
+      for (int i = std::min(n, nmax); i <= nmax; ++i) keep[i] *= 1e-2000L;
+    }
+  }
+  const cld scale = (std::sin(z) / z) / cur;
+  for (int n = 0; n <= nmax; ++n) out[n] = keep[n] * scale;
+}
+// hhat_n = h_n(z) z^{n+1} / (2n-1)!!, complex z
+void sph_hn_scaled_cld(int nmax, cld z, cld* out) {
+  const cld e = std::exp(cld(0, 1) * z);
+  cld h0 = cld(0, -1) * e;          // h_0 z
+  cld h1 = -e * (z + cld(0, 1));    // h_1 z^2
+  out[0] = h0;
+  if (nmax == 0) return;
+  out[1] = h1;
+  const cld z2 = z * z;
+  for (int n = 1; n < nmax; ++n) {
+    const cld hn = h1 - z2 / ((2.0L * n + 1) * (2.0L * n - 1)) * h0;
+    h0 = h1;
+    h1 = hn;
+    out[n + 1] = hn;
+  }
+}
+
 // Racah's single-sum formula with log-factorials (as reference src/special.cpp:126-155)
 double wigner3j(int j1, int j2, int j3, int m1, int m2, int m3) {
   if (m1 + m2 + m3 != 0) return 0;
@@ -229,20 +284,39 @@ size_t CoaxBuilder::slot(int m, int nu, int n) const {
 }
 
 void CoaxBuilder::build(CoaxKind kind, double k, double dist, double s_src, double s_dst,
-                        float* out) const {
+                        float* out, double k_imag) const {
   const int P = order_, lmax = 2 * P;
-  const long double z = (long double)k * dist;
-  // radial factors in a form that cannot overflow: rad[lam] * radscale(lam) = z_lam(k dist)
+  // z = (k + i k_imag) dist.  The radial factors are kept in a form that cannot overflow:
+  // rad[lam] * radscale(lam) = z_lam(z), radscale positive (|z| powers), phases inside rad
+  const cld zc = cld((long double)k, (long double)k_imag) * (long double)dist;
+  const long double z = std::abs(zc);
   std::vector<long double> rr(lmax + 1), ri(lmax + 1, 0.0L);
-  if (kind == CoaxKind::m2l) {
-    std::vector<double> hr(lmax + 1), hi(lmax + 1);
-    sph_hn_scaled(lmax, double(z), hr.data(), hi.data());
-    for (int l = 0; l <= lmax; ++l) {
-      rr[l] = hr[l];
-      ri[l] = hi[l];
+  if (k_imag == 0.0) {
+    if (kind == CoaxKind::m2l) {
+      std::vector<double> hr(lmax + 1), hi(lmax + 1);
+      sph_hn_scaled(lmax, double(z), hr.data(), hi.data());
+      for (int l = 0; l <= lmax; ++l) {
+        rr[l] = hr[l];
+        ri[l] = hi[l];
+      }
+    } else {
+      sph_jn_ld(lmax, z, rr.data());
     }
   } else {
-    sph_jn_ld(lmax, z, rr.data());
+    std::vector<cld> rad(lmax + 1);
+    if (kind == CoaxKind::m2l) {
+      // h_lam = hhat_lam (2 lam - 1)!! / z^{lam+1}: the modulus of z^{lam+1} goes into the log scale
+      // below, its phase stays here
+      sph_hn_scaled_cld(lmax, zc, rad.data());
+      const long double arg = std::arg(zc);
+      for (int l = 0; l <= lmax; ++l) rad[l] *= std::polar(1.0L, -(l + 1) * arg);
+    } else {
+      sph_jn_cld(lmax, zc, rad.data());
+    }
+    for (int l = 0; l <= lmax; ++l) {
+      rr[l] = rad[l].real();
+      ri[l] = rad[l].imag();
+    }
   }
   const long double ls = logl((long double)s_src), ld = logl((long double)s_dst), lz = logl(z);
   auto ldf = [](int n) { return logl(double_factorial(n)); };

@@ -83,7 +83,9 @@ enum class CoaxKind { m2l, m2m, l2l };
 class CoaxBuilder {
  public:
   explicit CoaxBuilder(int order);
-  void build(CoaxKind kind, double k, double dist, double s_src, double s_dst, float* out) const;
+  // k + i k_imag: the (complex) wavenumber; the level scales s_src / s_dst are Re(k) * side
+  void build(CoaxKind kind, double k, double dist, double s_src, double s_dst, float* out,
+             double k_imag = 0.0) const;
   int order() const { return order_; }
 
  private:

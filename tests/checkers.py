@@ -237,7 +237,11 @@ class Oracle(_Base):
         return _Fmm(_VoidLib(self.lib), "ho", C.c_void_p(h), xyz.shape[0])
 
     def _direct(self, n, xyz, q, k, nt, tp, out):
-        self.lib.ho_direct_sum(C.c_long(n), _d(xyz), q.ctypes.data_as(_dp), C.c_double(k),
+        if np.imag(k) != 0:
+            self.lib.ho_direct_sum_complex_k(C.c_long(n), _d(xyz), q.ctypes.data_as(_dp), C.c_double(np.real(k)),
+                                             C.c_double(np.imag(k)), C.c_long(nt), tp, out.ctypes.data_as(_dp))
+            return
+        self.lib.ho_direct_sum(C.c_long(n), _d(xyz), q.ctypes.data_as(_dp), C.c_double(np.real(k)),
                                C.c_long(nt), tp, out.ctypes.data_as(_dp))
 
     def apply_corrections(self, ni, patch_block, near_offset, near_source, near_delta, x, y):
@@ -366,7 +370,7 @@ class Ref(_Base):
         dim = (order + 1) ** 2
         out = np.zeros((dim, dim), dtype=np.complex128)
         t = np.ascontiguousarray(t, dtype=np.float64)
-        rc = self.lib.ref_translation_matrix(C.c_double(k), C.c_double(0), _d(t), order,
+        rc = self.lib.ref_translation_matrix(C.c_double(np.real(k)), C.c_double(np.imag(k)), _d(t), order,
                                              int(singular), out.ctypes.data_as(_dp))
         assert rc == 0, self.err()
         return out
@@ -395,15 +399,15 @@ class Ref(_Base):
         xyz = np.ascontiguousarray(xyz, dtype=np.float64)
         h = C.c_void_p()
         threads = threads or (os.cpu_count() or 1)
-        rc = self.lib.ref_fmm_create(C.byref(h), C.c_long(xyz.shape[0]), _d(xyz), C.c_double(k),
-                                     C.c_double(0), order, ncrit, C.c_double(leaf_cap),
+        rc = self.lib.ref_fmm_create(C.byref(h), C.c_long(xyz.shape[0]), _d(xyz), C.c_double(np.real(k)),
+                                     C.c_double(np.imag(k)), order, ncrit, C.c_double(leaf_cap),
                                      int(s or ncrit), C.c_double(theta), C.c_double(kd_max), threads)
         assert rc == 0, self.err()
         return _Fmm(self.lib, "ref", h, xyz.shape[0])
 
     def _direct(self, n, xyz, q, k, nt, tp, out):
-        rc = self.lib.ref_direct_sum(C.c_long(n), _d(xyz), q.ctypes.data_as(_dp), C.c_double(k),
-                                     C.c_double(0), C.c_long(nt), tp, out.ctypes.data_as(_dp))
+        rc = self.lib.ref_direct_sum(C.c_long(n), _d(xyz), q.ctypes.data_as(_dp), C.c_double(np.real(k)),
+                                     C.c_double(np.imag(k)), C.c_long(nt), tp, out.ctypes.data_as(_dp))
         assert rc == 0, self.err()
 
     def distributed_matvec(self, xyz, q, k, order, nranks, ncrit=64, leaf_cap=0.0, theta=0.4,

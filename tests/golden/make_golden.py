@@ -50,9 +50,17 @@ def translations():
     M = R.p2m(pts, q, center, k, 8)
     far = np.array([[1.2, 0.4, -0.8], [-2.0, 0.1, 0.3]])
     mv = np.array([R.eval_expansion(0, 8, M, center, p, k) for p in far])
+    # complex wavenumber (attenuation): dense matrices for the factored-table composition test
+    kc, Pc = 3.0 + 0.8j, 7
+    cshifts = np.array([[0.21, -0.33, 0.27], [0, 0, 0.31], [0, 0, -0.31], [0.2, 0, 0],
+                        [0.0625, -0.0625, 0.0625], [0.3, 0.1, -0.2]])
+    ckinds = np.array([0, 0, 1, 1, 0, 1])            # 0: singular (M2L), 1: regular (M2M / L2L)
+    cT = np.stack([R.translation_matrix(kc, t, Pc, 1 if kind == 0 else 0) for t, kind in zip(cshifts, ckinds)])
     np.savez_compressed(os.path.join(HERE, "translations.npz"), k=k, order=P, shifts=shifts,
                         singular=sing, regular=reg, p2m_pts=pts, p2m_q=q, p2m_center=center,
-                        p2m_order=8, p2m_coeff=M, eval_points=far, eval_multipole=mv)
+                        p2m_order=8, p2m_coeff=M, eval_points=far, eval_multipole=mv,
+                        complex_k=kc, complex_order=Pc, complex_shifts=cshifts, complex_kinds=ckinds,
+                        complex_T=cT)
 
 
 def fmm_cases():

@@ -304,3 +304,38 @@ def test_measured_weights_and_alpha_cuts(oracle):
         tot = [w[int(p.body_first):int(p.body_first) + int(p.body_count)].sum() for p in parts]
         assert max(tot) / sum(tot) < 0.45
 
+
+
+@pytest.mark.parametrize("k", [2.0 + 0.5j, 4.0 + 0.05j, 1.0 + 1.5j])
+def test_complex_wavenumber(oracle, k):
+    """k = k_r + i k_i (attenuation, common.hpp:36-40; e^{-k_i R} in kernel.hpp:20): near field,
+    expansions with complex radial functions and complex translation tables against the FP64 direct
+    sum, and against the compiled reference's FMM at the same order where it travelled to the box"""
+    from checkers import have_ref
+
+    n, order = 5000, 12
+    xyz = np.concatenate([sphere_points(n - 1500, 31), 0.4 * sphere_points(1500, 32) + 0.05])
+    q = charges(n, 31)
+    op = HfmmCuda(k=k, order=order, ncrit=40, theta=0.4, kd_max=1.0, leaf_cap=-1.0)
+    op.set_points(xyz)
+    y = op.matvec(q)
+    st = op.stats()
+    assert st["m2l_pairs"] > 0 and st["p2p_pairs"] > 0
+    exact = oracle.direct_sum(xyz, q, k)
+    assert rel_l2(y, exact) < 1e-5
+    # near field alone (gate closed: every pair is evaluated directly)
+    near = HfmmCuda(k=k, order=4, ncrit=50, kd_max=1e-9, leaf_cap=0.0)
+    near.set_points(xyz[:2500])
+    assert near.stats()["m2l_pairs"] == 0
+    assert rel_l2(near.matvec(q[:2500]), oracle.direct_sum(xyz[:2500], q[:2500], k)) < 2e-6
+    # exterior field evaluation uses the same damped kernel
+    obs = np.array([[3.0, 0.5, -1.0], [0.0, 0.0, 2.5], [-2.0, 2.0, 2.0]])
+    d = np.linalg.norm(obs[:, None, :] - xyz[None, :, :], axis=2)
+    want = (np.exp(1j * k * d) / (4 * np.pi * d)) @ q
+    assert rel_l2(op.evaluate_field(q, obs), want) < 5e-6
+    if have_ref():
+        from checkers import Ref
+        f = Ref().fmm(xyz, k, order, ncrit=40, leaf_cap=1.0 / abs(k), theta=0.4, kd_max=1.0)
+        c = f.counts()
+        assert st["m2l_pairs"] == c["m2l_pairs"] and st["p2p_body_pairs"] == c["p2p_body_pairs"]
+        assert rel_l2(y, f.matvec(q)) < 1e-5

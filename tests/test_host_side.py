@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
 def test_config_errors_mirror_the_reference(gpu_available):
     # traversal.cpp:16-21 (s >= c >= 1, 0 < theta <= 1), :212-213 (order >= 0): config_error
     for kw in (dict(ncrit=0), dict(ncrit=64, grain=32), dict(theta=0.0), dict(theta=1.5),
-               dict(order=-1), dict(order=99), dict(wave_i=0.1)):
+               dict(order=-1), dict(order=99), dict(k=-1.0), dict(wave_i=float("nan")), dict(wave_i=9.0)):
         args = dict(k=1.0, order=4)
         args.update(kw)
         with pytest.raises(HfmmError) as e:
@@ -88,6 +88,18 @@ def test_factored_tables_compose_to_the_dense_operator(oracle, order):
             ref_T = oracle.translation_matrix(k, t, order, sing)
             T = api.debug_compose_translation(order, k, t, kind, ss, sd)
             assert np.abs(T - ref_T).max() <= 5e-7 * np.abs(ref_T).max(), (order, t, kind)
+
+
+def test_factored_tables_for_a_complex_wavenumber():
+    """the same composition for k = k_r + i k_i against dense matrices the reference produced
+    (tests/golden/translations.npz, complex_* entries; translation_matrix takes a complex k throughout)"""
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "translations.npz"))
+    k = complex(g["complex_k"])
+    order = int(g["complex_order"])
+    for t, kind, ref_T in zip(g["complex_shifts"], g["complex_kinds"], g["complex_T"]):
+        ss, sd = (0.3, 0.15) if kind == 0 else (0.2, 0.4)
+        T = api.debug_compose_translation(order, k, t, int(kind), ss, sd)
+        assert np.abs(T - ref_T).max() <= 5e-7 * np.abs(ref_T).max(), (t, kind)
 
 
 def test_workload_generators():
