@@ -184,6 +184,22 @@ def run_single(args, cfg):
         for k in acc:
             acc[k] += st[f"{k}_seconds"]
     kern = {k: v / args.steps for k, v in acc.items()}
+    # the near field runs beside M2L on the same SMs (co-resident CTAs), so its event interval above
+    # is stretched over the whole M2L launch: kernel-alone durations come from a second handle that
+    # serialises the near field behind the far field (HFMM_FLAG_PHASE_TIMERS)
+    from paper_1803_09948_b200.api import HFMM_FLAG_PHASE_TIMERS
+    ops = HfmmCuda(k=cfg.k, order=cfg.order, ncrit=cfg.ncrit, theta=cfg.theta, kd_max=cfg.kd_max,
+                   leaf_cap=cfg.leaf_cap, device=0, flags=HFMM_FLAG_PHASE_TIMERS)
+    ops.set_points(xyz)
+    alone = {k: 0.0 for k in acc}
+    for it in range(args.steps + 1):
+        ops.matvec_device(q_dev.data_ptr(), out_dev.data_ptr())
+        sts = ops.stats()
+        if it:  # the first one warms up
+            for k in alone:
+                alone[k] += sts[f"{k}_seconds"]
+    alone = {k: v / args.steps for k, v in alone.items()}
+    del ops
 
     # ---- end to end through the C ABI with pinned host buffers
     qh = torch.from_numpy(q.copy()).pin_memory()
@@ -201,7 +217,8 @@ def run_single(args, cfg):
     nominal = 148 * 128 * 2 * 1.965e9 * 1e-12
     ex, dense = m2l_flops_per_pair(cfg.order)
     m2l_tf = st0["m2l_pairs"] * ex / kern["m2l"] * 1e-12 if kern["m2l"] > 0 else 0.0
-    p2p_tf = st0["p2p_body_pairs"] * 24 / kern["p2p"] * 1e-12 if kern["p2p"] > 0 else 0.0
+    m2l_tf_alone = st0["m2l_pairs"] * ex / alone["m2l"] * 1e-12 if alone["m2l"] > 0 else 0.0
+    p2p_tf = st0["p2p_body_pairs"] * 24 / alone["p2p"] * 1e-12 if alone["p2p"] > 0 else 0.0
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -237,21 +254,28 @@ def run_single(args, cfg):
                 + 4 * sum((cfg.order + 1 - abs(m)) ** 2 for m in range(-cfg.order, cfg.order + 1))
             ) / kern["m2l"] * 1e-12 if kern["m2l"] else None,
             "ms_per_launch": kern["m2l"] * 1e3,
+            # the same launch timed alone (near field serialised behind it): in the timed region one
+            # near-field CTA shares every SM with the two M2L CTAs
+            "ms_per_launch_alone": alone["m2l"] * 1e3, "achieved_alone": m2l_tf_alone,
+            "frac_alone": m2l_tf_alone / fp32_peak if fp32_peak else None,
             # dram__bytes_read + dram__bytes_write of this launch from the committed ncu --set full
             # capture of the same configuration (profiles/r01_ncu_translate_dual_cfg2_full.txt:
             # 11.41 GB read + 5.51 GB written); algorithmic bytes
             # are pairs x 2 x 8 (P+1)^2 (one source row read, one destination row reduced)
             "traffic": 16.93e9 if (cfg.name == "cfg2" and n == cfg.n) else None,
             "algorithmic_bytes": st0["m2l_pairs"] * 2 * 8 * (cfg.order + 1) ** 2},
+        # kernel-alone durations (near field serialised behind the far field); "ms_in_step" is the event
+        # interval inside the timed region, where P2P is co-resident with M2L
         "kernels": {
-            "p2p": {"ms": kern["p2p"] * 1e3, "tflops_24flop_per_pair": p2p_tf,
+            "p2p": {"ms": alone["p2p"] * 1e3, "ms_in_step": kern["p2p"] * 1e3, "tflops_24flop_per_pair": p2p_tf,
                     "frac_of_fp32_peak": p2p_tf / fp32_peak if fp32_peak else None,
                     "body_pairs": st0["p2p_body_pairs"]},
-            "m2l": {"ms": kern["m2l"] * 1e3, "tflops_executed": m2l_tf, "pairs": st0["m2l_pairs"]},
-            **{k: {"ms": kern[k] * 1e3, "gbs": tree_bytes[k] / kern[k] * 1e-9 if kern[k] else None,
-                   "frac_of_hbm": tree_bytes[k] / kern[k] * 1e-9 / hbm if kern[k] else None}
+            "m2l": {"ms": alone["m2l"] * 1e3, "ms_in_step": kern["m2l"] * 1e3, "tflops_executed": m2l_tf_alone,
+                    "pairs": st0["m2l_pairs"]},
+            **{k: {"ms": alone[k] * 1e3, "gbs": tree_bytes[k] / alone[k] * 1e-9 if alone[k] else None,
+                   "frac_of_hbm": tree_bytes[k] / alone[k] * 1e-9 / hbm if alone[k] else None}
                for k in ("p2m", "m2m", "l2l", "l2p")},
-            "matvec_device_ms": kern["matvec"] * 1e3},
+            "matvec_device_ms": kern["matvec"] * 1e3, "matvec_device_ms_serialised": alone["matvec"] * 1e3},
         "tree": {k: st0[k] for k in ("n_cells", "n_leaves", "max_level", "m2l_pairs", "p2p_pairs",
                                      "p2p_body_pairs", "m2l_shift_classes")},
         "setup_seconds": st0["setup_seconds"], "clocks": clocks,

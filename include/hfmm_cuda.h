@@ -42,7 +42,10 @@ enum {
    * (debug toggle kept until list statistics match the reference exactly) */
   HFMM_FLAG_HOST_TREE = 1 << 0,
   /* time each phase with CUDA events (fills hfmm_cuda_stats seconds); costs a few syncs */
-  HFMM_FLAG_PHASE_TIMERS = 1 << 1
+  HFMM_FLAG_PHASE_TIMERS = 1 << 1,
+  /* enqueue the near field before the far field.  Default: behind the persistent M2L launch, so one
+   * near-field CTA runs beside the two M2L CTAs of every SM (MUFU-bound next to shared-memory-bound) */
+  HFMM_FLAG_NEAR_FIRST = 1 << 2
 };
 
 /* POD mirror of WaveNumber (common.hpp:37-40), TraversalConfig (traversal.hpp:11-18) and the

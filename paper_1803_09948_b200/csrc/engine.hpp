@@ -101,6 +101,8 @@ class Engine {
   int rank_ = 0, nranks_ = 1, lcut_ = 0;
   uint32_t own_first_ = 0, own_count_ = 0;
   double partition_alpha_ = -1.0;
+  P2PArgs p2p_args_{};
+  bool p2p_late_ = false;
   std::vector<uint8_t> owned_;  // per cell
   uint64_t owned_m2l_pairs_ = 0, owned_body_pairs_ = 0, launches_ = 0;
   cudaStream_t stream_ = nullptr, stream_near_ = nullptr;

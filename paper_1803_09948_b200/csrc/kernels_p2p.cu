@@ -27,7 +27,7 @@ namespace hfmm_b200 {
 namespace {
 
 constexpr int kTile = 32;
-constexpr int kWarpsPerBlock = 4;
+constexpr int kWarpsPerBlock = 2;
 
 __device__ __forceinline__ float rsqrt_approx(float x) {
   float y;
@@ -199,7 +199,7 @@ __device__ __forceinline__ int owner_of(uint32_t incl, uint32_t g) {
 
 // 128 registers per thread keep four CTAs (16 warps) per SM; measured: 134 registers (3 CTAs) cost 40 %
 template <bool DAMP>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) p2p_kernel(const P2PArgs a) {
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 8) p2p_kernel(const P2PArgs a) {
   // target coordinates, one array per axis: [x | y | z][kTile]
   __shared__ __align__(16) float s_tgt[kWarpsPerBlock][3 * kTile];
   __shared__ __align__(16) float s_thi[kWarpsPerBlock][3 * kTile];
