@@ -134,8 +134,12 @@ Engine::Engine(const hfmm_cuda_config& cfg) : cfg_(cfg) {
     throw Error(HFMM_ERR_DEVICE, "no CUDA device available (this library has no CPU fallback)");
   if (cfg.device < 0 || cfg.device >= ndev) throw Error(HFMM_ERR_CONFIG, "device ordinal out of range");
   HFMM_CUDA_CHECK(cudaSetDevice(cfg.device));
-  HFMM_CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-  HFMM_CUDA_CHECK(cudaStreamCreateWithFlags(&stream_near_, cudaStreamNonBlocking));
+  // the far-field stream outranks the near-field stream: when both have blocks waiting, freed SM
+  // resources go to the (few, persistent) M2L CTAs first and the near field fills what is left
+  int prio_lo = 0, prio_hi = 0;
+  HFMM_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  HFMM_CUDA_CHECK(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, prio_hi));
+  HFMM_CUDA_CHECK(cudaStreamCreateWithPriority(&stream_near_, cudaStreamNonBlocking, prio_lo));
   HFMM_CUDA_CHECK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
   HFMM_CUDA_CHECK(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
   ev_.resize(14);
