@@ -194,6 +194,14 @@ int hfmm_cuda_dist_upward(hfmm_cuda_t* h, const void* q_morton_dev);
 /* out_morton_dev: n float2 in Morton order; only the owned slots are written */
 int hfmm_cuda_dist_downward(hfmm_cuda_t* h, void* out_morton_dev);
 
+/* Locally essential trees (reference extract_let, let.cpp:150-253): per cell (n_cells entries, the
+ * order of hfmm_cuda_get_cells), bit p of far_mask says rank p needs the cell's multipole (it is the
+ * source of an M2L pair whose target p owns), bit p of near_mask says rank p needs the bodies of the
+ * leaf; cell_rank is the owner.  All ranks compute identical masks from the global lists, so the
+ * send list "my cells with bit p" and the receive list "p's cells with my bit" match without any
+ * handshake.  At most 64 ranks. */
+int hfmm_cuda_get_exchange_masks(hfmm_cuda_t* h, uint64_t* far_mask, uint64_t* near_mask, int32_t* cell_rank);
+
 /* ---- repartitioning loop (reference partition.cpp:137-227) -------
  * measure_weights -> w = l + alpha r -> Morton cuts -> run -> update_alpha -> re-cut.  The work
  * estimates come from the interaction lists of the current point set; alpha is searched by the

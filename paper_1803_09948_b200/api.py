@@ -204,6 +204,17 @@ class HfmmCuda:
         self._check(self.lib.hfmm_cuda_measure_weights(self.h, local.ctypes.data_as(_dp), remote.ctypes.data_as(_dp)))
         return local, remote
 
+    def exchange_masks(self):
+        """(far_mask, near_mask, cell_rank) per cell: which ranks need a cell's multipole / a leaf's
+        bodies (locally essential trees), and who owns it"""
+        nc = self.stats()["n_cells"]
+        far, near = np.zeros(nc, dtype=np.uint64), np.zeros(nc, dtype=np.uint64)
+        rank = np.zeros(nc, dtype=np.int32)
+        self._check(self.lib.hfmm_cuda_get_exchange_masks(self.h, far.ctypes.data_as(C.c_void_p),
+                                                          near.ctypes.data_as(C.c_void_p),
+                                                          rank.ctypes.data_as(C.c_void_p)))
+        return far, near, rank
+
     def partition(self) -> Partition:
         p = Partition()
         self._check(self.lib.hfmm_cuda_get_partition(self.h, C.byref(p)))

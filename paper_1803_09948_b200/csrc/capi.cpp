@@ -210,6 +210,14 @@ int hfmm_cuda_dist_downward(hfmm_cuda_t* h, void* out_morton_dev) {
   });
 }
 
+int hfmm_cuda_get_exchange_masks(hfmm_cuda_t* h, uint64_t* far_mask, uint64_t* near_mask, int32_t* cell_rank) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] {
+    if (!far_mask || !near_mask || !cell_rank) throw Error(HFMM_ERR_CONFIG, "null mask array");
+    h->engine->get_exchange_masks(far_mask, near_mask, cell_rank);
+  });
+}
+
 int hfmm_cuda_set_partition_alpha(hfmm_cuda_t* h, double alpha) {
   if (int rc = need(h)) return rc;
   return guarded(h, [&] { h->engine->set_partition_alpha(alpha); });

@@ -419,6 +419,7 @@ void Engine::compute_partition() {
   std::vector<int> cell_rank;
   std::vector<uint32_t> first, count;
   compute_morton_partition(tree_, pairs_, nranks_, partition_alpha_, cell_rank, first, count, lcut_);
+  cell_rank_.assign(cell_rank.begin(), cell_rank.end());
   if (nranks_ == 1) return;
   own_first_ = first[rank_];
   own_count_ = count[rank_];
@@ -547,6 +548,9 @@ void Engine::set_points_device(const double* xyz, size_t n) {
       own_first_ = first[rank_];
       own_count_ = count[rank_];
       for (size_t c = 0; c < nc; ++c) owned_[c] = cell_rank[c] == rank_;
+      cell_rank_.assign(cell_rank.begin(), cell_rank.end());
+    } else {
+      cell_rank_.assign(nc, 0);
     }
   }
 
@@ -931,6 +935,28 @@ void Engine::get_cells(uint32_t* out, size_t capacity) const {
 void Engine::get_body_order(uint32_t* out) const {
   require_points();
   std::copy(tree_.index.begin(), tree_.index.end(), out);
+}
+
+// Locally essential tree of every rank, as bit masks (reference extract_let, let.cpp:150-253, is
+// sender-initiated the same way): bit p of far_mask[c] says rank p translates FROM cell c (c is a
+// source of an M2L pair whose target p owns), bit p of near_mask[c] says rank p evaluates the
+// bodies of leaf c directly.  Every rank holds the global lists, so all ranks compute the same
+// masks and derive matching send / receive lists without communicating.
+void Engine::get_exchange_masks(uint64_t* far_mask, uint64_t* near_mask, int32_t* cell_rank) const {
+  require_points();
+  if (nranks_ > 64) throw Error(HFMM_ERR_CONFIG, "exchange masks hold at most 64 ranks");
+  const size_t nc = tree_.n_cells();
+  std::fill(far_mask, far_mask + nc, uint64_t(0));
+  std::fill(near_mask, near_mask + nc, uint64_t(0));
+  for (size_t c = 0; c < nc; ++c) cell_rank[c] = cell_rank_.empty() ? 0 : cell_rank_[c];
+  for (int which = 0; which < 2; ++which) {
+    uint64_t np = 0;
+    get_pairs(which, nullptr, &np);
+    std::vector<uint32_t> pr(2 * np);
+    if (np) get_pairs(which, pr.data(), &np);
+    uint64_t* mask = which ? near_mask : far_mask;
+    for (uint64_t e = 0; e < np; ++e) mask[pr[2 * e + 1]] |= uint64_t(1) << cell_rank[pr[2 * e]];
+  }
 }
 
 // reference measure_weights (partition.cpp:143-163): per body, caller order;

@@ -36,6 +36,7 @@ class Engine {
   void set_partition(int rank, int nranks);
   void set_partition_alpha(double alpha);  // < 0: default work model
   void measure_weights(double* local, double* remote) const;
+  void get_exchange_masks(uint64_t* far_mask, uint64_t* near_mask, int32_t* cell_rank) const;
   void get_partition(hfmm_cuda_partition* out);
   void dist_upward(const void* q_morton_dev);
   void dist_downward(void* out_morton_dev);
@@ -104,6 +105,7 @@ class Engine {
   P2PArgs p2p_args_{};
   bool p2p_late_ = false;
   std::vector<uint8_t> owned_;  // per cell
+  std::vector<int32_t> cell_rank_;  // per cell: owning rank of the Morton partition
   uint64_t owned_m2l_pairs_ = 0, owned_body_pairs_ = 0, launches_ = 0;
   cudaStream_t stream_ = nullptr, stream_near_ = nullptr;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;

@@ -4,13 +4,16 @@ plumbing (NCCL over NVLink on GPUs; gloo in the CPU tests of the host-side logic
 Data flow of one matvec on rank r (stands in for the reference's simulated
 part::distributed_matvec, let.cpp:320-362):
 
-  1. all-gather of the charge slices       q[first_r : first_r+count_r]  ->  full Morton vector
-  2. device phase 1 (dist_upward)          near field of the owned leaves on its own stream,
-                                           P2M + M2M of the owned cells
-  3. all-gather of the owned multipole rows (per level a contiguous row range per rank; this is the
-     locally-essential-tree exchange with the pruning dropped: on NVSwitch a full gather of the
-     multipoles is a few ms — 2.5 M cells x 1.4 KB at BASELINE config 5 — against ~100 ms of compute)
-  4. device phase 2 (dist_downward)        M2L / L2L / L2P into the owned cells, owned outputs
+  1. charge exchange                       the bodies of the leaves on this rank's near lists
+  2. device phase 1 (dist_upward)          P2M + M2M of the owned cells
+  3. multipole exchange                    the multipoles this rank's M2L lists translate from
+  4. device phase 2 (dist_downward)        M2L / L2L / L2P into the owned cells, near field of the
+                                           owned leaves beside M2L, owned outputs
+Exchanges 1 and 3 are the locally-essential-tree exchange (sender-initiated like the reference's
+extract_let): every rank holds the global lists, derives matching send / receive index lists from
+them (let_index_lists) and ships the rows with ONE all_to_all_single each.  pruned=False falls back
+to all-gathering everything (per level a contiguous row range per rank; on NVSwitch even that is a
+few ms — 2.5 M cells x 1.4 KB at BASELINE config 5 — against ~100 ms of compute).
 
 The exchange helpers work on any tensors (CPU tensors under gloo in tests/test_distributed_gloo.py).
 """
@@ -63,12 +66,62 @@ def allgather_ranges(dist, buf, ranges, rank, world, scratch=None):
     return scratch
 
 
+def let_index_lists(op, rank: int, world: int):
+    """Send / receive index lists of the locally-essential-tree exchange of `rank` (reference
+    extract_let, let.cpp:150-253, sender-initiated): for every peer p
+      send_cells[p]  own cells whose multipole p translates from     recv_cells[p]  p's cells this rank needs
+      send_bodies[p] Morton slots of own leaves p sums directly      recv_bodies[p] slots of p's leaves needed here
+    Every rank derives them from the same global masks, so send_*[p] here equals recv_*[rank] on p,
+    element for element (ascending cell order)."""
+    far, near, owner = op.exchange_masks()
+    cells = op.cells()
+    first, count = cells[:, 4].astype(np.int64), cells[:, 5].astype(np.int64)
+    me = np.uint64(1) << np.uint64(rank)
+
+    def slots(leaves):
+        if len(leaves) == 0:
+            return np.zeros(0, dtype=np.int64)
+        return np.concatenate([np.arange(first[c], first[c] + count[c]) for c in leaves])
+
+    out = dict(send_cells=[], recv_cells=[], send_bodies=[], recv_bodies=[])
+    mine = owner == rank
+    for p in range(world):
+        bit = np.uint64(1) << np.uint64(p)
+        theirs = owner == p
+        if p == rank:
+            for k in out:
+                out[k].append(np.zeros(0, dtype=np.int64))
+            continue
+        out["send_cells"].append(np.nonzero(mine & ((far & bit) != 0))[0].astype(np.int64))
+        out["recv_cells"].append(np.nonzero(theirs & ((far & me) != 0))[0].astype(np.int64))
+        out["send_bodies"].append(slots(np.nonzero(mine & ((near & bit) != 0))[0]))
+        out["recv_bodies"].append(slots(np.nonzero(theirs & ((near & me) != 0))[0]))
+    return out
+
+
+def exchange_rows(dist, buf, send_idx, recv_idx, device):
+    """One all_to_all_single with uneven splits: rows buf[send_idx[p]] go to rank p, the rows received
+    from p land in buf[recv_idx[p]] (in place; the index lists are device int64 tensors)."""
+    import torch
+
+    width = buf.shape[1]
+    send = torch.cat([buf[i] for i in send_idx]) if sum(len(i) for i in send_idx) else buf.new_zeros((0, width))
+    n_recv = sum(len(i) for i in recv_idx)
+    recv = buf.new_empty((n_recv, width))
+    dist.all_to_all_single(recv, send, output_split_sizes=[len(i) for i in recv_idx],
+                           input_split_sizes=[len(i) for i in send_idx])
+    if n_recv:
+        buf[torch.cat(recv_idx)] = recv
+
+
 class ShardedFmm:
     """The FMM operator of one rank.  Vectors are sharded by Morton range: rank r holds
     q[first_r : first_r + count_r] of the Morton-ordered charge vector and produces the same slice
     of the potential."""
 
-    def __init__(self, op, dist, rank: int, world: int, device):
+    def __init__(self, op, dist, rank: int, world: int, device, pruned: bool = False):
+        """pruned: exchange only the locally essential rows (all_to_all with index lists) instead of
+        all-gathering every charge and every multipole"""
         import torch
 
         self.op, self.dist, self.rank, self.world, self.device = op, dist, rank, world, device
@@ -92,6 +145,13 @@ class ShardedFmm:
             view = DevicePointerTensor(p.multipole_dev, n_cells * self.stride * 2)
             self.multipole = torch.as_tensor(view, device=device).reshape(n_cells, self.stride * 2)
         self._s1 = self._s2 = None
+        self.pruned = pruned and world > 1
+        if self.pruned:
+            lists = let_index_lists(op, rank, world)
+            to_dev = lambda v: [torch.from_numpy(a).to(device) for a in v]
+            self.let = {k: to_dev(v) for k, v in lists.items()}
+            self.let_bytes = {"charges": int(sum(len(a) for a in lists["recv_bodies"])) * 8,
+                              "multipoles": int(sum(len(a) for a in lists["recv_cells"])) * self.stride * 8}
         self.owned_m2l_pairs = int(p.owned_m2l_pairs)
         self.owned_p2p_body_pairs = int(p.owned_p2p_body_pairs)
 
@@ -100,13 +160,19 @@ class ShardedFmm:
         import torch
 
         self.q_full[self.first:self.first + self.count].copy_(q_local)
-        self._s1 = allgather_ranges(self.dist, self.q_full, self.body_ranges, self.rank, self.world, self._s1)
+        if self.pruned:
+            exchange_rows(self.dist, self.q_full, self.let["send_bodies"], self.let["recv_bodies"], self.device)
+        else:
+            self._s1 = allgather_ranges(self.dist, self.q_full, self.body_ranges, self.rank, self.world, self._s1)
         torch.cuda.current_stream().synchronize()
         self.op.dist_upward(self.q_full.data_ptr())
         self.op.sync()
         if self.multipole is not None:
-            self._s2 = allgather_ranges(self.dist, self.multipole, self.cell_ranges, self.rank,
-                                        self.world, self._s2)
+            if self.pruned:
+                exchange_rows(self.dist, self.multipole, self.let["send_cells"], self.let["recv_cells"], self.device)
+            else:
+                self._s2 = allgather_ranges(self.dist, self.multipole, self.cell_ranges, self.rank,
+                                            self.world, self._s2)
             torch.cuda.current_stream().synchronize()
         self.op.dist_downward(self.out_full.data_ptr())
         self.op.sync()
@@ -131,8 +197,12 @@ class ShardedFmm:
 
         def gather_multipoles():
             if self.multipole is not None:
-                self._s2 = allgather_ranges(self.dist, self.multipole, self.cell_ranges, self.rank,
-                                            self.world, self._s2)
+                if self.pruned:
+                    exchange_rows(self.dist, self.multipole, self.let["send_cells"], self.let["recv_cells"],
+                                  self.device)
+                else:
+                    self._s2 = allgather_ranges(self.dist, self.multipole, self.cell_ranges, self.rank,
+                                                self.world, self._s2)
                 torch.cuda.current_stream().synchronize()
 
         return self.op.dist_gmres(rhs_local, allreduce_sum, gather_vector, gather_multipoles, rtol=rtol,
@@ -242,7 +312,7 @@ def emulate_gmres_on_one_device(ops, rhs_morton, timeout=120.0, **kw):
     return results
 
 
-def emulate_ranks_on_one_device(ops, q_morton):
+def emulate_ranks_on_one_device(ops, q_morton, pruned: bool = False):
     """Runs the sharded matvec of `len(ops)` ranks sequentially on ONE GPU (each op was created with
     set_partition(r, R) on the same global point set), replacing the two all-gathers by device
     copies.  Used by the GPU tests: one B200 is all this environment has, and ranks that wait on one
@@ -256,8 +326,21 @@ def emulate_ranks_on_one_device(ops, q_morton):
     n_cells = int(ops[0].stats()["n_cells"])
     stride = int(parts[0].coeff_stride)
     mp = []
-    for op, p in zip(ops, parts):
-        op.dist_upward(q_morton.data_ptr())     # every rank sees the gathered charges
+    lets = [let_index_lists(op, r, len(ops)) for r, op in enumerate(ops)] if pruned else None
+    for r, (op, p) in enumerate(zip(ops, parts)):
+        if pruned:
+            # a rank sees its own charges and the bodies of the leaves on its near lists, nothing else
+            qr = torch.full_like(q_morton, float("nan"))
+            f, c = int(p.body_first), int(p.body_count)
+            qr[f:f + c] = q_morton[f:f + c]
+            for s in range(len(ops)):
+                idx = torch.from_numpy(lets[r]["recv_bodies"][s]).to(dev)
+                assert np.array_equal(lets[r]["recv_bodies"][s], lets[s]["send_bodies"][r])
+                qr[idx] = q_morton[idx]
+            qr = torch.nan_to_num(qr, nan=1e30)   # a body that is read without having been received poisons the result
+            op.dist_upward(qr.data_ptr())
+        else:
+            op.dist_upward(q_morton.data_ptr())     # every rank sees the gathered charges
         op.sync()
         mp.append(torch.as_tensor(DevicePointerTensor(p.multipole_dev, n_cells * stride * 2),
                                   device=dev).reshape(n_cells, stride * 2) if p.multipole_dev else None)
@@ -266,6 +349,12 @@ def emulate_ranks_on_one_device(ops, q_morton):
             continue
         for s, ps in enumerate(parts):
             if s == r:
+                continue
+            if pruned:
+                idx = torch.from_numpy(lets[r]["recv_cells"][s]).to(dev)
+                assert np.array_equal(lets[r]["recv_cells"][s], lets[s]["send_cells"][r])
+                if len(idx):
+                    mp[r][idx] = mp[s][idx]
                 continue
             for L in range(int(ps.level_first), int(ps.level_last) + 1):
                 f, c = int(ps.cell_first[L]), int(ps.cell_count[L])
@@ -298,7 +387,7 @@ def bench_distributed(args, cfg, rank, world, metric, unit, workload_config, Clo
     t0 = time.perf_counter()
     op.set_points(xyz)
     setup = time.perf_counter() - t0
-    sh = ShardedFmm(op, dist, rank, world, device)
+    sh = ShardedFmm(op, dist, rank, world, device, pruned=True)
     order = op.body_order()
     q = charges(n_total, cfg.seed)[order[sh.first:sh.first + sh.count]]
     q_local = torch.from_numpy(np.stack([q.real, q.imag], 1).astype(np.float32)).to(device)
@@ -353,8 +442,12 @@ def bench_distributed(args, cfg, rank, world, metric, unit, workload_config, Clo
                 "ms_per_step": float(e2e[0]) * 1e3,
                 "h2d_bytes_per_step": int(sh.count) * 8, "d2h_bytes_per_step": int(sh.count) * 8},
         "gpu_launches": int(st["kernel_launches"]) * args.steps,
-        "exchange": {"charges_bytes_per_rank": n_total * 8,
-                     "multipole_bytes_per_rank": int(sum(c for rr in sh.cell_ranges for _, c in rr)) * sh.stride * 8},
+        # rank 0's receive volume per matvec: locally essential rows only (full gather in brackets)
+        "exchange": {"kind": "locally essential tree, all_to_all" if sh.pruned else "all-gather",
+                     "charges_bytes_per_rank": sh.let_bytes["charges"] if sh.pruned else n_total * 8,
+                     "multipole_bytes_per_rank": sh.let_bytes["multipoles"] if sh.pruned else
+                     int(sum(c for rr in sh.cell_ranges for _, c in rr)) * sh.stride * 8,
+                     "full_gather_bytes_per_rank": n_total * 8 + int(sum(c for rr in sh.cell_ranges for _, c in rr)) * sh.stride * 8},
         "balance": {"m2l_pairs": allw[:, 0].tolist(), "p2p_body_pairs": allw[:, 1].tolist(),
                     "bodies": allw[:, 2].tolist()},
         "device_ms_rank_max": float(ms[0]), "setup_seconds": setup, "clocks": clocks,

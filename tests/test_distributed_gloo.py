@@ -74,7 +74,24 @@ def _worker(rank, world, port, q):
         v[br[rank][0][0]:br[rank][0][0] + br[rank][0][1]] = float(rank + 1)
         allgather_ranges(dist, v, br, rank, world)
         ok2 = bool((v[:9] == 1).all() and (v[9:] == 2).all())
-        q.put((rank, ok1 and ok2 and scratch is not None))
+        # locally-essential-tree exchange: uneven all_to_all with index lists (rows sent to the peer /
+        # rows received from it), in place
+        from paper_1803_09948_b200.distributed import exchange_rows
+        truth = torch.arange(12 * 3, dtype=torch.float32).reshape(12, 3)
+        own = [torch.tensor([0, 1, 2, 3, 4, 5]), torch.tensor([6, 7, 8, 9, 10, 11])]
+        need = [torch.tensor([7, 10, 11]), torch.tensor([1, 4])]      # rows rank r needs from the other rank
+        buf = torch.full((12, 3), -1.0)
+        buf[own[rank]] = truth[own[rank]]
+        empty = torch.zeros(0, dtype=torch.int64)
+        send = [empty, empty]
+        recv = [empty, empty]
+        send[1 - rank] = need[1 - rank]
+        recv[1 - rank] = need[rank]
+        exchange_rows(dist, buf, send, recv, "cpu")
+        have = torch.cat([own[rank], need[rank]])
+        rest = torch.tensor([i for i in range(12) if i not in set(have.tolist())])
+        ok3 = bool((buf[have] == truth[have]).all() and (buf[rest] == -1).all())
+        q.put((rank, ok1 and ok2 and ok3 and scratch is not None))
     finally:
         dist.destroy_process_group()
 
