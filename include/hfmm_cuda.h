@@ -77,6 +77,7 @@ typedef struct {
   double matvec_seconds;       /* whole device-side matvec                                   */
   uint64_t kernel_launches;    /* kernels launched by the last matvec                        */
   uint64_t device_bytes;       /* HBM held by the handle                                     */
+  uint64_t m2l_batches;        /* work items of the M2L launch: <= 32 pairs of one shift class */
 } hfmm_cuda_stats;
 
 typedef struct hfmm_cuda hfmm_cuda_t;

@@ -174,29 +174,59 @@ void Engine::require_points() const {
   if (!have_points_) throw Error(HFMM_ERR_CONFIG, "hfmm_cuda_set_points has not been called");
 }
 
+// Classes that share the rotation table (polar angle) and the coaxial table (levels, distance) differ
+// only in azimuth — lattice shifts related by quarter turns about z and by reflections — and are
+// batched together: the kernel carries e^{i m phi} per pair.  Returns the order in which the classes
+// are laid out (group by group) and the group of every class.
+static void group_classes(const std::vector<TranslateClass>& classes, std::vector<uint32_t>& order,
+                          std::vector<uint32_t>& group_of) {
+  const size_t nc = classes.size();
+  order.resize(nc);
+  for (size_t c = 0; c < nc; ++c) order[c] = uint32_t(c);
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) {
+    return classes[x].rot != classes[y].rot ? classes[x].rot < classes[y].rot : classes[x].coax < classes[y].coax;
+  });
+  group_of.assign(nc, 0);
+  uint32_t g = 0;
+  for (size_t i = 0; i < nc; ++i) {
+    if (i && (classes[order[i]].rot != classes[order[i - 1]].rot || classes[order[i]].coax != classes[order[i - 1]].coax)) ++g;
+    group_of[order[i]] = g;
+  }
+}
+
 void Engine::upload_stage(TranslateStage& st, const std::vector<uint32_t>& src,
                           const std::vector<uint32_t>& dst, const std::vector<uint32_t>& cls_of_pair,
                           const std::vector<TranslateClass>& classes) {
-  // stable counting sort of the pairs by class, then batches of kTranslateBatch
+  // stable counting sort of the pairs by class (classes laid out group by group), then batches of
+  // kTranslateBatch pairs cut per table group
   const size_t np = src.size(), nc = classes.size();
+  std::vector<uint32_t> order, group_of;
+  group_classes(classes, order, group_of);
+  std::vector<uint32_t> pos_of(nc);  // position of a class in the grouped layout
+  for (size_t i = 0; i < nc; ++i) pos_of[order[i]] = uint32_t(i);
   std::vector<uint64_t> start(nc + 1, 0);
-  for (size_t i = 0; i < np; ++i) ++start[cls_of_pair[i] + 1];
+  for (size_t i = 0; i < np; ++i) ++start[pos_of[cls_of_pair[i]] + 1];
   for (size_t c = 0; c < nc; ++c) start[c + 1] += start[c];
-  std::vector<uint32_t> s_sorted(np), d_sorted(np);
+  std::vector<uint32_t> s_sorted(np), d_sorted(np), c_sorted(np);
   {
     std::vector<uint64_t> cur(start.begin(), start.end() - 1);
     for (size_t i = 0; i < np; ++i) {
-      const uint64_t slot = cur[cls_of_pair[i]]++;
+      const uint64_t slot = cur[pos_of[cls_of_pair[i]]]++;
       s_sorted[slot] = src[i];
       d_sorted[slot] = dst[i];
+      c_sorted[slot] = cls_of_pair[i];
     }
   }
   std::vector<TranslateItem> items;
   const uint64_t batch = uint64_t(translate_batch_size(cfg_.order));
-  for (size_t c = 0; c < nc; ++c)
-    for (uint64_t b = start[c]; b < start[c + 1]; b += batch)
-      items.push_back({uint32_t(b), uint32_t(std::min<uint64_t>(batch, start[c + 1] - b)),
-                       uint32_t(c), 0u});
+  for (size_t i = 0; i < nc;) {
+    size_t j = i;
+    while (j < nc && group_of[order[j]] == group_of[order[i]]) ++j;
+    for (uint64_t b = start[i]; b < start[j]; b += batch)
+      items.push_back({uint32_t(b), uint32_t(std::min<uint64_t>(batch, start[j] - b)), c_sorted[b],
+                       group_of[order[i]]});
+    i = j;
+  }
   if (np >= (uint64_t(1) << 32)) throw Error(HFMM_ERR_CONFIG, "pair count exceeds 32-bit indexing");
   st.n_items = uint32_t(items.size());
   st.n_pairs = np;
@@ -204,6 +234,7 @@ void Engine::upload_stage(TranslateStage& st, const std::vector<uint32_t>& src,
   st.classes.upload(classes, stream_);
   st.pair_src.upload(s_sorted, stream_);
   st.pair_dst.upload(d_sorted, stream_);
+  st.pair_cls.upload(c_sorted, stream_);
   HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
 }
 
@@ -245,19 +276,44 @@ void Engine::build_m2l_stage_device(TableRegistry& reg, const FarClasses& fc) {
   const TreeArrays& t = tree_;
   const double k = cfg_.wave_r;
   auto scale = [&](int lvl) { return k * t.side(lvl); };
-  std::vector<TranslateClass> classes(fc.count.size());
-  std::vector<TranslateItem> items;
-  const uint64_t batch = uint64_t(translate_batch_size(cfg_.order));
-  uint64_t begin = 0;
-  for (size_t c = 0; c < fc.count.size(); ++c) {
+  const size_t nc = fc.count.size();
+  std::vector<TranslateClass> classes(nc);
+  for (size_t c = 0; c < nc; ++c) {
     const int la = fc.lt[c], lb = fc.ls[c], lmax = std::max(la, lb);
     classes[c] = make_class(reg, CoaxKind::m2l, fc.dx[c], fc.dy[c], fc.dz[c], lb, la, lmax,
                             t.side(lmax) / 2, scale(lb), scale(la));
-    for (uint64_t b = 0; b < fc.count[c]; b += batch)
-      items.push_back({uint32_t(begin + b), uint32_t(std::min<uint64_t>(batch, fc.count[c] - b)),
-                       uint32_t(c), 0u});
-    begin += fc.count[c];
   }
+  // the device builder left the pairs sorted class by class; lay the classes out group by group
+  // (group_classes) by moving whole class segments, and record the class of every pair
+  std::vector<uint32_t> order, group_of;
+  group_classes(classes, order, group_of);
+  std::vector<uint64_t> old_start(nc + 1, 0);
+  for (size_t c = 0; c < nc; ++c) old_start[c + 1] = old_start[c] + fc.count[c];
+  std::vector<uint32_t> seg_new(nc + 1, 0), seg_old(nc), seg_cls(nc);
+  std::vector<TranslateItem> items;
+  const uint64_t batch = uint64_t(translate_batch_size(cfg_.order));
+  uint64_t pos = 0;
+  for (size_t i = 0; i < nc;) {
+    size_t j = i;
+    const uint64_t group_begin = pos;
+    while (j < nc && group_of[order[j]] == group_of[order[i]]) {
+      seg_new[j] = uint32_t(pos);
+      seg_old[j] = uint32_t(old_start[order[j]]);
+      seg_cls[j] = order[j];
+      pos += fc.count[order[j]];
+      ++j;
+    }
+    for (uint64_t b = group_begin; b < pos; b += batch) {
+      // class of the batch's first pair: the segment that holds position b
+      size_t s = i;
+      while (s + 1 < j && seg_new[s + 1] <= b) ++s;
+      items.push_back({uint32_t(b), uint32_t(std::min<uint64_t>(batch, pos - b)), seg_cls[s], group_of[order[i]]});
+    }
+    i = j;
+  }
+  seg_new[nc] = uint32_t(pos);
+  if (pos >= (uint64_t(1) << 32)) throw Error(HFMM_ERR_CONFIG, "pair count exceeds 32-bit indexing");
+  regroup_pairs_device(seg_new, seg_old, seg_cls, pos, m2l_.pair_src, m2l_.pair_dst, m2l_.pair_cls, stream_);
   stats_.m2l_shift_classes = classes.size();
   owned_m2l_pairs_ = fc.n_owned_pairs;
   m2l_.n_items = uint32_t(items.size());
@@ -754,6 +810,7 @@ void Engine::run_stage(const TranslateStage& st, const float2* src, float2* dst)
   ta.classes = st.classes.get();
   ta.pair_src = st.pair_src.get();
   ta.pair_dst = st.pair_dst.get();
+  ta.pair_cls = st.pair_cls.get();
   ta.rot_tables = rot_tables_.get();
   ta.coax_tables = coax_tables_.get();
   ta.src = src;
@@ -918,6 +975,7 @@ void Engine::sync() {
 void Engine::get_stats(hfmm_cuda_stats* out) {
   collect_timings();
   stats_.device_bytes = device_bytes_counter();
+  stats_.m2l_batches = m2l_.n_items;
   *out = stats_;
 }
 

@@ -23,7 +23,7 @@ struct TranslateStage {
   // one batched-translation launch: M2L (all levels) or one level of M2M / L2L
   DeviceBuffer<TranslateItem> items;
   DeviceBuffer<TranslateClass> classes;
-  DeviceBuffer<uint32_t> pair_src, pair_dst;
+  DeviceBuffer<uint32_t> pair_src, pair_dst, pair_cls;  // pair_cls: shift class of every pair
   uint32_t n_items = 0;
   uint64_t n_pairs = 0;
 };

@@ -83,9 +83,9 @@ struct TranslateClass {
 };
 struct TranslateItem {
   uint32_t pair_begin;
-  uint32_t count;  // <= translate_batch_size(order) pairs, all of one class
-  uint32_t cls;
-  uint32_t pad;
+  uint32_t count;  // <= translate_batch_size(order) pairs of one table group
+  uint32_t cls;    // class of the first pair
+  uint32_t group;  // table group: classes with the same rotation and coaxial table (they differ in azimuth)
 };
 inline constexpr int kTranslateBatch = 32;   // pairs per work item (= lanes of a warp)
 inline constexpr int kTranslateWarps = 16;   // most warps per CTA of the translation kernel (8 or 16)
@@ -127,6 +127,7 @@ struct TranslateArgs {
   const TranslateClass* classes;
   const uint32_t* pair_src;
   const uint32_t* pair_dst;
+  const uint32_t* pair_cls;  // shift class of every pair (azimuth phases)
   const float* rot_tables;   // [rot][rot_table_size(P)]
   const float* coax_tables;  // [coax][2 * coax_table_size(P)]
   const float2* src;         // expansions read

@@ -50,8 +50,8 @@ __host__ __device__ inline SmemPlan smem_plan(int P) {
   s.dim = (P + 1) * (P + 1);
   s.rot_floats = rot_table_size(P);
   s.coax_c = coax_table_size(P);
-  s.phase_c = (P + 2) & ~1;
-  s.unfold_c = 4 * (P + 1);  // two float4 per order m: fold factors, unfold factors
+  s.phase_c = (P + 1) * 32;  // e^{i m phi} of every pair of the batch: [m][pair]
+  s.unfold_c = 0;
   s.tile_c = s.dim * kRow;
   // rot | coax | phases | unfold factors | zero row | tile A | tile B | (n, m) of every gather unit (u16)
   s.bytes = size_t(s.rot_floats) * 4 + size_t(s.coax_c + s.phase_c + s.unfold_c + kZeroC + 2 * s.tile_c) * 8 +
@@ -301,9 +301,9 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
   const int dim = sp.dim, n_units = (P + 1) * (P + 2) / 2;
   float* s_rot = smem;
   float2* s_coax = reinterpret_cast<float2*>(s_rot + sp.rot_floats);
-  float2* s_ph = s_coax + sp.coax_c;  // e^{i m phi}, m = 0..P
-  float4* s_pu = reinterpret_cast<float4*>(s_ph + sp.phase_c);  // unfold, per m: (c, -s, sgn c, sgn s) / 2
-  float4* s_pf = s_pu + (P + 1);                                // fold,   per m: (c, s, sgn c, -sgn s)
+  // e^{i m phi_p} for every pair p of the batch, [m][pair]: a batch may mix shift classes that share the
+  // rotation and coaxial tables (same polar angle and distance) and differ only in azimuth
+  float2* s_ph = s_coax + sp.coax_c;
   float2* s_zero = s_ph + sp.phase_c + sp.unfold_c;
   float2* A = s_zero + kZeroC;
   float2* B = A + sp.tile_c;
@@ -362,12 +362,11 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
   const uint32_t a_duo = uint32_t(__cvta_generic_to_shared(A)) + 16 * (lane & 15),
                  b_duo = uint32_t(__cvta_generic_to_shared(B)) + 16 * (lane & 15),
                  zero_addr = uint32_t(__cvta_generic_to_shared(s_zero)),
-                 pu_addr = uint32_t(__cvta_generic_to_shared(s_pu)),
-                 pf_addr = uint32_t(__cvta_generic_to_shared(s_pf));
+                 ph_duo = uint32_t(__cvta_generic_to_shared(s_ph)) + 16 * (lane & 15);
 
   TranslateItem item = a.items[it_begin];
   issue_gather(item);
-  uint32_t loaded_cls = 0xffffffffu;
+  uint32_t loaded_grp = 0xffffffffu;  // table group (rotation + coaxial table) resident in shared memory
 
   // Tables of a shift class: asynchronous 16-byte copies, issued as soon as the previous item has
   // left its last table-reading stage, so the fetch hides under its unfold and reductions; the
@@ -381,24 +380,29 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
     for (int i = tid; i < sp.coax_c / 2; i += kThreads)
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(coax_s + 16u * i), "l"(g_coax + i) : "memory");
   };
-  auto store_factors = [&](const TranslateClass& cls) {
-    if (tid <= P) {
+  // azimuth phases of the pairs of an item: thread p < 32 walks e^{i m phi} of pair p up the orders
+  auto store_phases = [&](const TranslateItem& it) {
+    if (tid < 32) {
+      float cphi = 1.f, sphi = 0.f;
+      if (tid < int(it.count)) {
+        const TranslateClass c = a.classes[a.pair_cls[it.pair_begin + tid]];
+        cphi = c.cphi;
+        sphi = c.sphi;
+      }
       float cr = 1.f, ci = 0.f;
-      for (int j = 0; j < tid; ++j) {
-        const float t = cr * cls.cphi - ci * cls.sphi;
-        ci = ci * cls.cphi + cr * cls.sphi;
+      for (int m = 0; m <= P; ++m) {
+        s_ph[m * 32 + tid] = make_float2(cr, ci);
+        const float t = cr * cphi - ci * sphi;
+        ci = ci * cphi + cr * sphi;
         cr = t;
       }
-      const float sg = (tid & 1) ? -0.5f : 0.5f;
-      s_pu[tid] = tid ? make_float4(0.5f * cr, -0.5f * ci, sg * cr, sg * ci) : make_float4(1.f, 0.f, 1.f, 0.f);
-      s_pf[tid] = tid ? make_float4(cr, ci, 2.f * sg * cr, -2.f * sg * ci) : make_float4(1.f, 0.f, 0.f, 0.f);
     }
   };
   {
-    const TranslateClass cls = a.classes[item.cls];
+    const TranslateClass cls = a.classes[a.pair_cls[item.pair_begin]];
     fetch_tables(cls);
-    store_factors(cls);
-    loaded_cls = item.cls;
+    store_phases(item);
+    loaded_grp = item.group;
   }
   wait_gather();    // the first item's operands and tables
   __syncthreads();  // ... and s_unit
@@ -416,12 +420,13 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
       u64 xp0, xp1, xm0 = 0ull, xm1 = 0ull;
       ldsp2(c0 + uint32_t(m) * kRowB, xp0, xp1);
       if (m) ldsp2(c0 - uint32_t(m) * kRowB, xm0, xm1);
-      const float4 f = lds4(pf_addr + 16 * m);
-      u64 a0 = mul2s(xp0, f.x), a1 = mul2s(xp1, f.x), b0 = mul2s(xm0, f.z), b1 = mul2s(xm1, f.z);
-      fma2s(a0, rot90(xp0), f.y);
-      fma2s(a1, rot90(xp1), f.y);
-      fma2s(b0, rot90(xm0), f.w);
-      fma2s(b1, rot90(xm1), f.w);
+      const float4 ph = lds4(ph_duo + 256 * m);  // (c, s) of the lane's two pairs
+      const float sg = (m & 1) ? -1.0f : 1.0f;
+      u64 a0 = mul2s(xp0, ph.x), a1 = mul2s(xp1, ph.z), b0 = mul2s(xm0, sg * ph.x), b1 = mul2s(xm1, sg * ph.z);
+      fma2s(a0, rot90(xp0), ph.y);
+      fma2s(a1, rot90(xp1), ph.w);
+      fma2s(b0, rot90(xm0), -sg * ph.y);
+      fma2s(b1, rot90(xm1), -sg * ph.w);
       u64 t0 = a0, t1 = a1;
       fma2s(a0, b0, 1.0f);
       fma2s(a1, b1, 1.0f);
@@ -467,33 +472,33 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
     }
     __syncthreads();
     // the tables have had their last reader: fetch the next class's behind the unfold
-    const bool new_cls = has_next && next.cls != loaded_cls;  // CTA-uniform
-    TranslateClass ncls{};
-    if (new_cls) {
-      ncls = a.classes[next.cls];
-      fetch_tables(ncls);
+    const bool new_grp = has_next && next.group != loaded_grp;  // CTA-uniform
+    if (new_grp) {
+      fetch_tables(a.classes[a.pair_cls[next.pair_begin]]);
+      loaded_grp = next.group;
     }
     // stage 5a: unfold B -> A in the caller's coefficient order, with e^{-i mu phi}:
     //   y_m = (u + v)/2 e^{-i m phi},   y_{-m} = (-1)^m (u - v)/2 e^{+i m phi}
     // lane = two pairs, one unit (n, m) per half-warp: conflict-free 16-byte accesses, half-warp
-    // uniform indices, packed arithmetic (s_pu holds the four real factors of order m)
+    // uniform indices, packed arithmetic
     for (int up = warp; 2 * up < n_units; up += WARPS) {
       const int u = min(2 * up + half, n_units - 1);  // an odd unit count: the last unit is done twice
       const int n = s_um[2 * u], m = s_um[2 * u + 1], fs = s_unit[u] & 0xffff;
       u64 u0, u1, v0 = 0ull, v1 = 0ull;
       ldsp2(b_duo + uint32_t(fs) * kRowB, u0, u1);
       if (m) ldsp2(b_duo + uint32_t(fs + n) * kRowB, v0, v1);
-      const float4 f = lds4(pu_addr + 16 * m);
+      const float4 ph = lds4(ph_duo + 256 * m);  // (c, s) of the lane's two pairs
+      const float h = m ? 0.5f : 1.0f, hs = (m & 1) ? -h : h;
       u64 s0 = u0, s1 = u1, d0 = u0, d1 = u1;
       fma2s(s0, v0, 1.0f);
       fma2s(s1, v1, 1.0f);
       fma2s(d0, v0, -1.0f);
       fma2s(d1, v1, -1.0f);
-      u64 yp0 = mul2s(s0, f.x), yp1 = mul2s(s1, f.x), ym0 = mul2s(d0, f.z), ym1 = mul2s(d1, f.z);
-      fma2s(yp0, rot90(s0), f.y);
-      fma2s(yp1, rot90(s1), f.y);
-      fma2s(ym0, rot90(d0), f.w);
-      fma2s(ym1, rot90(d1), f.w);
+      u64 yp0 = mul2s(s0, h * ph.x), yp1 = mul2s(s1, h * ph.z), ym0 = mul2s(d0, hs * ph.x), ym1 = mul2s(d1, hs * ph.z);
+      fma2s(yp0, rot90(s0), -h * ph.y);
+      fma2s(yp1, rot90(s1), -h * ph.w);
+      fma2s(ym0, rot90(d0), hs * ph.y);
+      fma2s(ym1, rot90(d1), hs * ph.w);
       const uint32_t c0 = a_duo + uint32_t(n * n + n) * kRowB;
       stsp2(c0 + uint32_t(m) * kRowB, yp0, yp1);
       stsp2(c0 - uint32_t(m) * kRowB, ym0, ym1);  // m = 0: the same row, the same value
@@ -503,10 +508,7 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
     // stage 5b: start the next item's gather, then accumulate this item into its destinations,
     // two coefficients (16 bytes) per reduction
     if (has_next) issue_gather(next);
-    if (new_cls) {  // the unfold (last reader of the factors) is behind the barrier above
-      store_factors(ncls);
-      loaded_cls = next.cls;
-    }
+    if (has_next) store_phases(next);  // the unfold (last reader of the phases) is behind the barrier above
     // reduction mapping: a warp takes 4 pairs x 8 lanes, laid out so that each half-warp reads 4
     // consecutive coefficient pairs of 4 pairs (rows 2 i2 of tile A are 8 banks apart: conflict-free)
     {

@@ -730,4 +730,44 @@ void build_body_arrays_device(const TreeArrays& t, const DeviceBuffer<double>& d
   HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
+namespace {
+__global__ void __launch_bounds__(kBlock)
+regroup_kernel(const uint32_t* __restrict__ seg_new, const uint32_t* __restrict__ seg_old,
+               const uint32_t* __restrict__ seg_cls, uint32_t n_seg, uint32_t n,
+               const uint32_t* __restrict__ src_in, const uint32_t* __restrict__ dst_in,
+               uint32_t* __restrict__ src_out, uint32_t* __restrict__ dst_out, uint32_t* __restrict__ cls_out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t lo = 0, hi = n_seg;  // last segment with seg_new <= i
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (seg_new[mid] <= i) lo = mid;
+    else hi = mid;
+  }
+  const uint32_t from = seg_old[lo] + (i - seg_new[lo]);
+  src_out[i] = src_in[from];
+  dst_out[i] = dst_in[from];
+  cls_out[i] = seg_cls[lo];
+}
+}  // namespace
+
+void regroup_pairs_device(const std::vector<uint32_t>& seg_new, const std::vector<uint32_t>& seg_old,
+                          const std::vector<uint32_t>& seg_cls, uint64_t n_pairs,
+                          DeviceBuffer<uint32_t>& pair_src, DeviceBuffer<uint32_t>& pair_dst,
+                          DeviceBuffer<uint32_t>& pair_cls, cudaStream_t s) {
+  pair_cls.resize(std::max<uint64_t>(n_pairs, 1));
+  if (!n_pairs) return;
+  DeviceBuffer<uint32_t> d_new, d_old, d_cls, src_out(n_pairs), dst_out(n_pairs);
+  d_new.upload(seg_new, s);
+  d_old.upload(seg_old, s);
+  d_cls.upload(seg_cls, s);
+  regroup_kernel<<<grid_for(n_pairs), kBlock, 0, s>>>(d_new.get(), d_old.get(), d_cls.get(), uint32_t(seg_old.size()),
+                                                      uint32_t(n_pairs), pair_src.get(), pair_dst.get(), src_out.get(),
+                                                      dst_out.get(), pair_cls.get());
+  HFMM_CUDA_CHECK(cudaGetLastError());
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
+  pair_src = std::move(src_out);
+  pair_dst = std::move(dst_out);
+}
+
 }  // namespace hfmm_b200

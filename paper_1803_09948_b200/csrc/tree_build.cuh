@@ -81,6 +81,13 @@ void build_far_classes_device(const DevicePairs& p, const DeviceCells& cells,
                               DeviceBuffer<uint32_t>& pair_src, DeviceBuffer<uint32_t>& pair_dst,
                               FarClasses& out, cudaStream_t s);
 
+// Reorders the class-sorted pairs segment by segment: the pairs of new segment s (positions
+// seg_new[s] .. seg_new[s+1]) come from old positions seg_old[s] ..; pair_cls receives seg_cls[s]
+void regroup_pairs_device(const std::vector<uint32_t>& seg_new, const std::vector<uint32_t>& seg_old,
+                          const std::vector<uint32_t>& seg_cls, uint64_t n_pairs,
+                          DeviceBuffer<uint32_t>& pair_src, DeviceBuffer<uint32_t>& pair_dst,
+                          DeviceBuffer<uint32_t>& pair_cls, cudaStream_t s);
+
 // leaf-relative, k-scaled coordinates and their hi/lo split (kernels.cuh), plus absolute ones
 void build_body_arrays_device(const TreeArrays& tree, const DeviceBuffer<double>& d_xyz,
                               const DeviceBuffer<uint32_t>& d_index, double k, double grid,
