@@ -178,6 +178,9 @@ void Engine::require_points() const {
 // only in azimuth — lattice shifts related by quarter turns about z and by reflections — and are
 // batched together: the kernel carries e^{i m phi} per pair.  Returns the order in which the classes
 // are laid out (group by group) and the group of every class.
+// batches per table group must save at least 3 % of the batches to pay for the per-pair phases
+static constexpr double kMixedBatchGain = 0.97;
+
 static void group_classes(const std::vector<TranslateClass>& classes, std::vector<uint32_t>& order,
                           std::vector<uint32_t>& group_of) {
   const size_t nc = classes.size();
@@ -217,15 +220,29 @@ void Engine::upload_stage(TranslateStage& st, const std::vector<uint32_t>& src,
       c_sorted[slot] = cls_of_pair[i];
     }
   }
-  std::vector<TranslateItem> items;
+  // batches: per table group when that saves batches (partially filled ones cost as much as full
+  // ones), else per class — one class per batch keeps the cheaper per-class phases in the kernel
   const uint64_t batch = uint64_t(translate_batch_size(cfg_.order));
-  for (size_t i = 0; i < nc;) {
-    size_t j = i;
-    while (j < nc && group_of[order[j]] == group_of[order[i]]) ++j;
-    for (uint64_t b = start[i]; b < start[j]; b += batch)
-      items.push_back({uint32_t(b), uint32_t(std::min<uint64_t>(batch, start[j] - b)), c_sorted[b],
+  auto cut = [&](bool per_group) {
+    std::vector<TranslateItem> out;
+    for (size_t i = 0; i < nc;) {
+      size_t j = i + 1;
+      while (per_group && j < nc && group_of[order[j]] == group_of[order[i]]) ++j;
+      for (uint64_t b = start[i]; b < start[j]; b += batch)
+        out.push_back({uint32_t(b), uint32_t(std::min<uint64_t>(batch, start[j] - b)), c_sorted[b],
                        group_of[order[i]]});
-    i = j;
+      i = j;
+    }
+    return out;
+  };
+  std::vector<TranslateItem> items = cut(true);
+  st.mixed = true;
+  {
+    std::vector<TranslateItem> per_class = cut(false);
+    if (double(items.size()) > kMixedBatchGain * double(per_class.size())) {
+      items.swap(per_class);
+      st.mixed = false;
+    }
   }
   if (np >= (uint64_t(1) << 32)) throw Error(HFMM_ERR_CONFIG, "pair count exceeds 32-bit indexing");
   st.n_items = uint32_t(items.size());
@@ -290,7 +307,7 @@ void Engine::build_m2l_stage_device(TableRegistry& reg, const FarClasses& fc) {
   std::vector<uint64_t> old_start(nc + 1, 0);
   for (size_t c = 0; c < nc; ++c) old_start[c + 1] = old_start[c] + fc.count[c];
   std::vector<uint32_t> seg_new(nc + 1, 0), seg_old(nc), seg_cls(nc);
-  std::vector<TranslateItem> items;
+  std::vector<TranslateItem> items, per_class;
   const uint64_t batch = uint64_t(translate_batch_size(cfg_.order));
   uint64_t pos = 0;
   for (size_t i = 0; i < nc;) {
@@ -300,6 +317,9 @@ void Engine::build_m2l_stage_device(TableRegistry& reg, const FarClasses& fc) {
       seg_new[j] = uint32_t(pos);
       seg_old[j] = uint32_t(old_start[order[j]]);
       seg_cls[j] = order[j];
+      for (uint64_t b = 0; b < fc.count[order[j]]; b += batch)
+        per_class.push_back({uint32_t(pos + b), uint32_t(std::min<uint64_t>(batch, fc.count[order[j]] - b)),
+                             order[j], group_of[order[i]]});
       pos += fc.count[order[j]];
       ++j;
     }
@@ -312,6 +332,9 @@ void Engine::build_m2l_stage_device(TableRegistry& reg, const FarClasses& fc) {
     i = j;
   }
   seg_new[nc] = uint32_t(pos);
+  // batches per table group only when that saves batches (see upload_stage)
+  m2l_.mixed = double(items.size()) <= kMixedBatchGain * double(per_class.size());
+  if (!m2l_.mixed) items.swap(per_class);
   if (pos >= (uint64_t(1) << 32)) throw Error(HFMM_ERR_CONFIG, "pair count exceeds 32-bit indexing");
   regroup_pairs_device(seg_new, seg_old, seg_cls, pos, m2l_.pair_src, m2l_.pair_dst, m2l_.pair_cls, stream_);
   stats_.m2l_shift_classes = classes.size();
@@ -811,6 +834,7 @@ void Engine::run_stage(const TranslateStage& st, const float2* src, float2* dst)
   ta.pair_src = st.pair_src.get();
   ta.pair_dst = st.pair_dst.get();
   ta.pair_cls = st.pair_cls.get();
+  ta.mixed = st.mixed ? 1 : 0;
   ta.rot_tables = rot_tables_.get();
   ta.coax_tables = coax_tables_.get();
   ta.src = src;

@@ -26,6 +26,7 @@ struct TranslateStage {
   DeviceBuffer<uint32_t> pair_src, pair_dst, pair_cls;  // pair_cls: shift class of every pair
   uint32_t n_items = 0;
   uint64_t n_pairs = 0;
+  bool mixed = false;  // batches mix the classes of a table group (per-pair azimuth phases in the kernel)
 };
 
 class Engine {

@@ -134,6 +134,7 @@ struct TranslateArgs {
   float2* dst;               // expansions accumulated into (atomically)
   int order;
   int stride;
+  int mixed;                 // batches mix classes of a table group (per-pair phases) / one class per batch
 };
 void launch_translate(const TranslateArgs& a, cudaStream_t s);
 // pairs per work item expected by the kernel

@@ -291,7 +291,9 @@ __constant__ TranslateSchedule c_sched[kMaxOrder + 1];
 // tables in shared memory are reloaded only when the class changes).  The gather of the NEXT item
 // is issued into registers while the current item drains through its reductions, so the chain
 // item -> pair list -> source rows never sits on the critical path.
-template <int WARPS, int CTAS>
+// MIXED: the batches of this launch mix shift classes of one table group (per-pair azimuth phases);
+// otherwise every batch holds one class and the phases are per class (broadcast)
+template <int WARPS, int CTAS, bool MIXED>
 __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const TranslateArgs a) {
   constexpr int kThreads = WARPS * 32;
   constexpr int kLanesPerPair = WARPS;  // 32 pairs x WARPS lanes = all threads of the CTA
@@ -362,7 +364,8 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
   const uint32_t a_duo = uint32_t(__cvta_generic_to_shared(A)) + 16 * (lane & 15),
                  b_duo = uint32_t(__cvta_generic_to_shared(B)) + 16 * (lane & 15),
                  zero_addr = uint32_t(__cvta_generic_to_shared(s_zero)),
-                 ph_duo = uint32_t(__cvta_generic_to_shared(s_ph)) + 16 * (lane & 15);
+                 ph_duo = uint32_t(__cvta_generic_to_shared(s_ph)) + (MIXED ? 16 * (lane & 15) : 0);
+  constexpr uint32_t kPhaseRowB = MIXED ? 256 : 8;  // [m][pair] or [m]
 
   TranslateItem item = a.items[it_begin];
   issue_gather(item);
@@ -381,7 +384,23 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(coax_s + 16u * i), "l"(g_coax + i) : "memory");
   };
   // azimuth phases of the pairs of an item: thread p < 32 walks e^{i m phi} of pair p up the orders
+  uint32_t loaded_cls = 0xffffffffu;
   auto store_phases = [&](const TranslateItem& it) {
+    if (!MIXED) {  // one class per batch: e^{i m phi} of the class, recomputed when the class changes
+      if (it.cls == loaded_cls) return;
+      loaded_cls = it.cls;
+      if (tid <= P) {
+        const TranslateClass c = a.classes[it.cls];
+        float cr = 1.f, ci = 0.f;
+        for (int j = 0; j < tid; ++j) {
+          const float t = cr * c.cphi - ci * c.sphi;
+          ci = ci * c.cphi + cr * c.sphi;
+          cr = t;
+        }
+        s_ph[tid] = make_float2(cr, ci);
+      }
+      return;
+    }
     if (tid < 32) {
       float cphi = 1.f, sphi = 0.f;
       if (tid < int(it.count)) {
@@ -397,6 +416,13 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
         cr = t;
       }
     }
+  };
+  // (c, s) of the lane's two pairs for order m
+  auto load_phase = [&](int m) {
+    if (MIXED) return lds4(ph_duo + kPhaseRowB * m);
+    float2 p;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(p.x), "=f"(p.y) : "r"(ph_duo + kPhaseRowB * m));
+    return make_float4(p.x, p.y, p.x, p.y);
   };
   {
     const TranslateClass cls = a.classes[a.pair_cls[item.pair_begin]];
@@ -420,7 +446,7 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
       u64 xp0, xp1, xm0 = 0ull, xm1 = 0ull;
       ldsp2(c0 + uint32_t(m) * kRowB, xp0, xp1);
       if (m) ldsp2(c0 - uint32_t(m) * kRowB, xm0, xm1);
-      const float4 ph = lds4(ph_duo + 256 * m);  // (c, s) of the lane's two pairs
+      const float4 ph = load_phase(m);
       const float sg = (m & 1) ? -1.0f : 1.0f;
       u64 a0 = mul2s(xp0, ph.x), a1 = mul2s(xp1, ph.z), b0 = mul2s(xm0, sg * ph.x), b1 = mul2s(xm1, sg * ph.z);
       fma2s(a0, rot90(xp0), ph.y);
@@ -487,7 +513,7 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
       u64 u0, u1, v0 = 0ull, v1 = 0ull;
       ldsp2(b_duo + uint32_t(fs) * kRowB, u0, u1);
       if (m) ldsp2(b_duo + uint32_t(fs + n) * kRowB, v0, v1);
-      const float4 ph = lds4(ph_duo + 256 * m);  // (c, s) of the lane's two pairs
+      const float4 ph = load_phase(m);
       const float h = m ? 0.5f : 1.0f, hs = (m & 1) ? -h : h;
       u64 s0 = u0, s1 = u1, d0 = u0, d1 = u1;
       fma2s(s0, v0, 1.0f);
@@ -684,15 +710,15 @@ void upload_translate_schedule(int order) {
 int translate_batch_size(int) { return kTranslateBatch; }
 
 namespace {
-template <int WARPS, int CTAS>
+template <int WARPS, int CTAS, bool MIXED>
 void launch_translate_nu(const TranslateArgs& a, cudaStream_t s, size_t bytes, int ctas) {
   static int configured_for = -1;
   if (configured_for < int(bytes)) {
-    HFMM_CUDA_CHECK(cudaFuncSetAttribute(translate_kernel<WARPS, CTAS>,
+    HFMM_CUDA_CHECK(cudaFuncSetAttribute(translate_kernel<WARPS, CTAS, MIXED>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
     configured_for = int(bytes);
   }
-  translate_kernel<WARPS, CTAS><<<ctas, WARPS * 32, bytes, s>>>(a);
+  translate_kernel<WARPS, CTAS, MIXED><<<ctas, WARPS * 32, bytes, s>>>(a);
   HFMM_CUDA_CHECK(cudaGetLastError());
 }
 }  // namespace
@@ -710,8 +736,13 @@ void launch_translate(const TranslateArgs& a, cudaStream_t s) {
   const int warps = translate_warps(a.order);
   const bool two = translate_two_ctas(a.order);
   const int ctas = int(std::min<uint32_t>(a.n_items, uint32_t((two ? 2 : 1) * sm_count)));
-  if (warps == 8) launch_translate_nu<8, 2>(a, s, sp.bytes, ctas);
-  else launch_translate_nu<16, 1>(a, s, sp.bytes, ctas);
+  if (warps == 8) {
+    if (a.mixed) launch_translate_nu<8, 2, true>(a, s, sp.bytes, ctas);
+    else launch_translate_nu<8, 2, false>(a, s, sp.bytes, ctas);
+  } else {
+    if (a.mixed) launch_translate_nu<16, 1, true>(a, s, sp.bytes, ctas);
+    else launch_translate_nu<16, 1, false>(a, s, sp.bytes, ctas);
+  }
 }
 
 }  // namespace hfmm_b200
