@@ -140,3 +140,22 @@ def patch_samples(patches: np.ndarray, sample_ref: np.ndarray) -> np.ndarray:
         out[:, j, :] = r
     return out.reshape(-1, 3)
 
+
+def mie_soft_sphere(radius: float, k: float, r, theta) -> np.ndarray:
+    """Scattered field of the plane wave e^{ikz} off a sound-soft sphere, the classical series
+        u_s(r, theta) = - sum_n i^n (2n + 1) j_n(ka) / h_n(ka) h_n(kr) P_n(cos theta)
+    (the analytic oracle of BASELINE config 3; the reference carries the same series in
+    oracle.cpp:11-59).  r, theta: observation radii (>= radius) and polar angles."""
+    from scipy.special import eval_legendre, spherical_jn, spherical_yn
+
+    r, theta = np.broadcast_arrays(np.asarray(r, dtype=np.float64), np.asarray(theta, dtype=np.float64))
+    ka = k * radius
+    nmax = int(ka + 8.0 * np.cbrt(ka) + 16.0)
+    n = np.arange(nmax + 1)
+    h = lambda z: spherical_jn(n, z) + 1j * spherical_yn(n, z)
+    ratio = spherical_jn(n, ka) / h(ka)
+    out = np.zeros(r.shape, dtype=np.complex128)
+    for idx in np.ndindex(r.shape):
+        out[idx] = -np.sum((2 * n + 1) * (1j ** n) * ratio * h(k * r[idx]) * eval_legendre(n, np.cos(theta[idx])))
+    return out
+

@@ -71,3 +71,16 @@ def test_repartitioning_loop_pieces(oracle, ref):
         a, t = rng.uniform(0, 2, m), rng.uniform(1, 2, m)
         assert update_alpha(oracle.lib, "ho", a, t) == update_alpha(ref.lib, "ref", a, t)
 
+
+def test_mie_series_of_the_package_is_the_reference_s(ref):
+    """workloads.mie_soft_sphere (scipy) against oracle::mie_soft_sphere (oracle.cpp:11-59)"""
+    from paper_1803_09948_b200.workloads import mie_soft_sphere
+
+    th = np.linspace(0, np.pi, 19)
+    for k, r in ((1.0, 1.0), (4.0, 4.0), (12.0, 2.5)):
+        want = ref.mie_soft_sphere(1.0, k, np.stack([r + 0 * th, th, 0 * th], 1))
+        assert rel_l2(mie_soft_sphere(1.0, k, r, th), want) < 1e-12
+    # boundary condition on the sphere: incident + scattered = 0 (test_oracle.cpp:47-57)
+    tot = np.exp(1j * 4.0 * np.cos(th)) + mie_soft_sphere(1.0, 4.0, 1.0, th)
+    assert np.abs(tot).max() < 1e-10
+
