@@ -74,8 +74,66 @@ void ho_sph_jn(int nmax, double z, double* out) {
   free(keep);
 }
 
+/* the same for a complex argument (the reference's sph_jn takes cplx z: special.cpp:7-54) */
+static zc sph_j0_z(zc z) {
+  if (cabs(z) < 1e-6) {
+    const zc z2 = z * z;
+    return 1.0 - z2 / 6.0 + z2 * z2 / 120.0;
+  }
+  return csin(z) / z;
+}
+static void sph_jn_z(int nmax, zc z, zc* out) {
+  const double az = cabs(z);
+  if (az < 0.5) {
+    const zc h = 0.5 * z * z;
+    zc zpow = 1.0;
+    double dfact = 1.0;
+    for (int n = 0; n <= nmax; ++n) {
+      zc term = 1.0, sum = 1.0;
+      for (int j = 1; j < 40; ++j) {
+        term *= -h / (double)(j * (2 * n + 2 * j + 1));
+        sum += term;
+        if (cabs(term) < 1e-18 * cabs(sum)) break;
+      }
+      out[n] = zpow / dfact * sum;
+      zpow *= z;
+      dfact *= (double)(2 * n + 3);
+    }
+    return;
+  }
+  const int start = nmax + 16 + (int)az;
+  zc above = 0.0, cur = 1e-30;
+  zc* keep = (zc*)calloc((size_t)nmax + 1, sizeof(zc));
+  for (int n = start; n >= 0; --n) {
+    const zc below = (2.0 * n + 3.0) / z * cur - above;
+    above = cur;
+    cur = below;
+    if (n <= nmax) keep[n] = cur;
+    if (cabs(cur) > 1e250) {
+      cur *= 1e-250;
+      above *= 1e-250;
+      for (int i = n < nmax ? n : nmax; i <= nmax; ++i) keep[i] *= 1e-250;
+    }
+  }
+  const zc scale = sph_j0_z(z) / cur;
+  for (int n = 0; n <= nmax; ++n) out[n] = keep[n] * scale;
+  free(keep);
+}
+
+/* j_n for a real or complex argument (a real argument keeps the real-arithmetic path) */
+static void radial_j(int nmax, zc z, zc* out) {
+  if (cimag(z) == 0.0) {
+    double* jr = (double*)malloc(sizeof(double) * ((size_t)nmax + 1));
+    ho_sph_jn(nmax, creal(z), jr);
+    for (int n = 0; n <= nmax; ++n) out[n] = jr[n];
+    free(jr);
+  } else {
+    sph_jn_z(nmax, z, out);
+  }
+}
+
 /* ref: src/special.cpp:56-65 — h0 = -i e^{iz}/z, h1 = -e^{iz}(z+i)/z^2, upward recurrence */
-static void sph_hn_c(int nmax, double z, zc* out) {
+static void sph_hn_c(int nmax, zc z, zc* out) {
   const zc e = cexp(I * z);
   out[0] = -I * e / z;
   if (nmax == 0) return;
@@ -227,19 +285,15 @@ static const zc kIpow[4] = {1, I, -1, -I};
 
 /* ref: src/expansion.cpp:95-124 — T[(nu,mu),(n,m)] = sum_lam i^(nu+lam-n) G z_lam(k|t|)
  * Y_lam^(m-mu)(t^), z = j (regular) or h (singular); row-major dim x dim. */
-static void translation_matrix_c(double k, const double t[3], int order, int singular, zc* T) {
+static void translation_matrix_c(zc k, const double t[3], int order, int singular, zc* T) {
   const gaunt_t* g = gaunt_get(order);
   const int dim = nmdim(order), lmax = 2 * order;
-  const double z = k * sqrt(t[0] * t[0] + t[1] * t[1] + t[2] * t[2]);
+  const zc z = k * sqrt(t[0] * t[0] + t[1] * t[1] + t[2] * t[2]);
   zc* rad = (zc*)malloc(sizeof(zc) * (lmax + 1));
   if (singular)
     sph_hn_c(lmax, z, rad);
-  else {
-    double* jr = (double*)malloc(sizeof(double) * (lmax + 1));
-    ho_sph_jn(lmax, z, jr);
-    for (int l = 0; l <= lmax; ++l) rad[l] = jr[l];
-    free(jr);
-  }
+  else
+    radial_j(lmax, z, rad);
   zc* harm = (zc*)malloc(sizeof(zc) * nmdim(lmax));
   ynm_c(lmax, t, harm);
   for (int nu = 0; nu <= order; ++nu)
@@ -260,6 +314,10 @@ static void translation_matrix_c(double k, const double t[3], int order, int sin
 void ho_translation_matrix(double k, const double t[3], int order, int singular, double* out) {
   translation_matrix_c(k, t, order, singular, (zc*)out);
 }
+void ho_translation_matrix_complex_k(double kr, double ki, const double t[3], int order, int singular,
+                                     double* out) {
+  translation_matrix_c(kr + I * ki, t, order, singular, (zc*)out);
+}
 
 /* ref: src/expansion.cpp:126-139 — out += T * in */
 static void apply_dense(const zc* T, int dim, const zc* in, zc* out) {
@@ -272,13 +330,13 @@ static void apply_dense(const zc* T, int dim, const zc* in, zc* out) {
 }
 
 /* ref: src/expansion.cpp:157-175 — M_n^m += (i k q) j_n(k rho) conj Y_n^m(rho^) */
-static void p2m_c(long n, const double* xyz, const zc* q, const double c[3], double k, int order,
+static void p2m_c(long n, const double* xyz, const zc* q, const double c[3], zc k, int order,
                   zc* M) {
-  double* rad = (double*)malloc(sizeof(double) * (order + 1));
+  zc* rad = (zc*)malloc(sizeof(zc) * (order + 1));
   zc* harm = (zc*)malloc(sizeof(zc) * nmdim(order));
   for (long b = 0; b < n; ++b) {
     const double rho[3] = {xyz[3 * b] - c[0], xyz[3 * b + 1] - c[1], xyz[3 * b + 2] - c[2]};
-    ho_sph_jn(order, k * sqrt(rho[0] * rho[0] + rho[1] * rho[1] + rho[2] * rho[2]), rad);
+    radial_j(order, k * sqrt(rho[0] * rho[0] + rho[1] * rho[1] + rho[2] * rho[2]), rad);
     ynm_c(order, rho, harm);
     const zc w = I * k * q[b];
     for (int d = 0; d <= order; ++d)
@@ -295,18 +353,15 @@ void ho_p2m(long n, const double* xyz, const double* q, const double center[3], 
 
 /* ref: src/expansion.cpp:177-195 — sum coeff * (h_n or j_n)(k r) Y_n^m(r^) */
 static zc eval_c(int local, int order, const zc* coeff, const double c[3], const double p[3],
-                 double k) {
+                 zc k) {
   const double d[3] = {p[0] - c[0], p[1] - c[1], p[2] - c[2]};
   const double r = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
   zc* harm = (zc*)malloc(sizeof(zc) * nmdim(order));
   zc* rad = (zc*)malloc(sizeof(zc) * (order + 1));
   ynm_c(order, d, harm);
-  if (local) {
-    double* jr = (double*)malloc(sizeof(double) * (order + 1));
-    ho_sph_jn(order, k * r, jr);
-    for (int n = 0; n <= order; ++n) rad[n] = jr[n];
-    free(jr);
-  } else
+  if (local)
+    radial_j(order, k * r, rad);
+  else
     sph_hn_c(order, k * r, rad);
   zc s = 0;
   for (int n = 0; n <= order; ++n)
@@ -334,7 +389,7 @@ typedef struct {
 
 struct ho_fmm {
   long n;
-  double k, theta, kd_max;
+  double k, ki, theta, kd_max; /* wavenumber k + i ki */
   int order, ncrit;
   double lo[3], width;
   double* pos;    /* Morton order, 3n */
@@ -511,7 +566,7 @@ static void pl_push(pairlist_t* p, uint32_t t, uint32_t s) {
 /* ref: src/traversal.cpp:45-51 — wavenumber gate then centre-distance test */
 static int admissible(const ho_fmm* h, const cell_t* a, const cell_t* b) {
   if (h->kd_max > 0 &&
-      (fabs(h->k) * 2 * a->radius > h->kd_max || fabs(h->k) * 2 * b->radius > h->kd_max))
+      (hypot(h->k, h->ki) * 2 * a->radius > h->kd_max || hypot(h->k, h->ki) * 2 * b->radius > h->kd_max))
     return 0;
   const double d[3] = {a->c[0] - b->c[0], a->c[1] - b->c[1], a->c[2] - b->c[2]};
   return sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]) > (a->radius + b->radius) / h->theta;
@@ -556,10 +611,16 @@ static void group_by_target(const pairlist_t* in, long ncells, uint32_t** ot, ui
 
 ho_fmm* ho_fmm_create(long n, const double* xyz, double k, int order, int ncrit,
                       double leaf_cap, double theta, double kd_max) {
+  return ho_fmm_create_complex_k(n, xyz, k, 0.0, order, ncrit, leaf_cap, theta, kd_max);
+}
+/* complex wavenumber kr + i ki (common.hpp:36-40); gates use |k| (traversal.cpp:86) */
+ho_fmm* ho_fmm_create_complex_k(long n, const double* xyz, double k, double ki, int order, int ncrit,
+                                double leaf_cap, double theta, double kd_max) {
   if (n < 1 || ncrit < 1 || !(theta > 0) || theta > 1 || order < 0) return NULL;
   ho_fmm* h = (ho_fmm*)calloc(1, sizeof(ho_fmm));
   h->n = n;
   h->k = k;
+  h->ki = ki;
   h->order = order;
   h->ncrit = ncrit;
   h->theta = theta;
@@ -666,7 +727,7 @@ static void shift_matrix(const ho_fmm* h, int level, int oct, int upward, zc* T)
   double t[3] = {oct & 4 ? -hs : hs, oct & 2 ? -hs : hs, oct & 1 ? -hs : hs};
   if (!upward)
     for (int a = 0; a < 3; ++a) t[a] = -t[a];
-  translation_matrix_c(h->k, t, h->order, 0, T);
+  translation_matrix_c(h->k + I * h->ki, t, h->order, 0, T);
 }
 
 /* ref: src/traversal.cpp:175-204 + include/hfmm/kernel.hpp:16-23 — per target body, sources in
@@ -694,7 +755,7 @@ static void near_field(const ho_fmm* h, const zc* src, zc* trg, int f32) {
             if (ddx * ddx + ddy * ddy + ddz * ddz == 0) continue;
             const float dx = (float)ddx, dy = (float)ddy, dz = (float)ddz;
             const float R = sqrtf(dx * dx + dy * dy + dz * dz);
-            const float amp = expf(-0.0f * R) / ((float)(4.0 * HO_PI) * R);
+            const float amp = expf((float)(-h->ki) * R) / ((float)(4.0 * HO_PI) * R);
             const float ph = (float)h->k * R;
             const float gr = amp * cosf(ph), gi = amp * sinf(ph);
             const float qr = (float)creal(src[bj]), qi = (float)cimag(src[bj]);
@@ -713,7 +774,7 @@ static void near_field(const ho_fmm* h, const zc* src, zc* trg, int f32) {
             const double r2 = dx * dx + dy * dy + dz * dz;
             if (r2 == 0) continue;
             const double R = sqrt(r2);
-            const double amp = 1.0 / (4.0 * HO_PI * R);
+            const double amp = exp(-h->ki * R) / (4.0 * HO_PI * R);
             acc += (amp * cos(h->k * R) + I * amp * sin(h->k * R)) * src[bj];
           }
         }
@@ -744,7 +805,7 @@ int ho_fmm_matvec(ho_fmm* h, const double* q, int f32_p2p, double* out) {
     const cell_t* c = &h->cells[i];
     zc* M = h->multipole + (size_t)i * dim;
     if (c->child_count == 0) {
-      p2m_c(c->body_count, h->pos + 3 * c->body_first, src + c->body_first, c->c, h->k, h->order, M);
+      p2m_c(c->body_count, h->pos + 3 * c->body_first, src + c->body_first, c->c, h->k + I * h->ki, h->order, M);
     } else {
       for (uint32_t j = 0; j < c->child_count; ++j) {
         const cell_t* ch = &h->cells[c->child_first + j];
@@ -788,7 +849,7 @@ int ho_fmm_matvec(ho_fmm* h, const double* q, int f32_p2p, double* out) {
     const shiftkey_t* r = &sk[shift_rep[s]];
     const double unit = h->width / (double)((uint64_t)1 << r->lmax) / 2;
     const double t[3] = {r->x * unit, r->y * unit, r->z * unit};
-    translation_matrix_c(h->k, t, h->order, 1, mats + (size_t)s * dim * dim);
+    translation_matrix_c(h->k + I * h->ki, t, h->order, 1, mats + (size_t)s * dim * dim);
   }
   {
     long ngroups = 0;
@@ -833,7 +894,7 @@ int ho_fmm_matvec(ho_fmm* h, const double* q, int f32_p2p, double* out) {
     const cell_t* c = &h->cells[h->leaves[li]];
     const zc* L = h->local + (size_t)h->leaves[li] * dim;
     for (uint32_t b = c->body_first; b < c->body_first + c->body_count; ++b)
-      trg[b] += eval_c(1, h->order, L, c->c, h->pos + 3 * b, h->k);
+      trg[b] += eval_c(1, h->order, L, c->c, h->pos + 3 * b, h->k + I * h->ki);
   }
   h->seconds[2] = now_s() - t2;
 

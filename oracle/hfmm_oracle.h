@@ -67,6 +67,12 @@ void ho_block_lu_solve(long npatch, int ni, const double* block_lu, const int* b
                        double* x);
 
 
+/* complex wavenumber kr + i ki (common.hpp:36-40): the reference's special functions, translation
+ * matrices and kernels take cplx k throughout */
+ho_fmm* ho_fmm_create_complex_k(long n, const double* xyz, double kr, double ki, int order, int ncrit,
+                                double leaf_cap, double theta, double kd_max);
+void ho_translation_matrix_complex_k(double kr, double ki, const double t[3], int order, int singular,
+                                     double* out);
 /* direct sum for a complex wavenumber kr + i ki (kernel.hpp:16-23) */
 void ho_direct_sum_complex_k(long n, const double* xyz, const double* q, double kr, double ki, long nt,
                              const long long* target_index, double* out);

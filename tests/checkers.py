@@ -204,7 +204,11 @@ class Oracle(_Base):
         dim = (order + 1) ** 2
         out = np.zeros((dim, dim), dtype=np.complex128)
         t = np.ascontiguousarray(t, dtype=np.float64)
-        self.lib.ho_translation_matrix(C.c_double(k), _d(t), order, int(singular), out.ctypes.data_as(_dp))
+        if np.imag(k) != 0:
+            self.lib.ho_translation_matrix_complex_k(C.c_double(np.real(k)), C.c_double(np.imag(k)), _d(t), order,
+                                                     int(singular), out.ctypes.data_as(_dp))
+        else:
+            self.lib.ho_translation_matrix(C.c_double(np.real(k)), _d(t), order, int(singular), out.ctypes.data_as(_dp))
         return out
 
     def p2m(self, xyz, q, center, k, order):
@@ -227,9 +231,10 @@ class Oracle(_Base):
 
     def fmm(self, xyz, k, order, ncrit=64, leaf_cap=0.0, theta=0.4, kd_max=1.0, s=None, threads=0):
         xyz = np.ascontiguousarray(xyz, dtype=np.float64)
-        self.lib.ho_fmm_create.restype = C.c_void_p
-        h = self.lib.ho_fmm_create(C.c_long(xyz.shape[0]), _d(xyz), C.c_double(k), order, ncrit,
-                                   C.c_double(leaf_cap), C.c_double(theta), C.c_double(kd_max))
+        self.lib.ho_fmm_create_complex_k.restype = C.c_void_p
+        h = self.lib.ho_fmm_create_complex_k(C.c_long(xyz.shape[0]), _d(xyz), C.c_double(np.real(k)),
+                                             C.c_double(np.imag(k)), order, ncrit, C.c_double(leaf_cap),
+                                             C.c_double(theta), C.c_double(kd_max))
         assert h, "ho_fmm_create rejected the configuration"
         for name in ("counts", "cells", "box", "body_order", "plan", "matvec", "seconds",
                      "expansions", "destroy"):

@@ -94,6 +94,18 @@ def fmm_cases():
     np.savez_compressed(os.path.join(HERE, "fmm.npz"), **out)
 
 
+def fmm_complex_wavenumber():
+    # k = k_r + i k_i (attenuation): the reference's pipeline takes a complex wavenumber throughout
+    xyz = np.concatenate([sphere_points(900, 8), 0.4 * sphere_points(300, 9) + 0.05])
+    k, order = 2.0 + 0.5j, 8
+    q = charges(len(xyz), 77)
+    f = R.fmm(xyz, k, order, ncrit=24, leaf_cap=1.0 / abs(k), theta=0.4, kd_max=1.0, threads=1)
+    cnt = f.counts()
+    np.savez_compressed(os.path.join(HERE, "fmm_complex_k.npz"), xyz=xyz, q=q, k=k, order=order, ncrit=24,
+                        leaf_cap=1.0 / abs(k), theta=0.4, kd_max=1.0, y=f.matvec(q),
+                        direct=R.direct_sum(xyz, q, k), m2l_pairs=cnt["m2l_pairs"], p2p_body_pairs=cnt["p2p_body_pairs"])
+
+
 def gmres_and_bie():
     rng = np.random.default_rng(11)
     n = 48
@@ -131,10 +143,15 @@ def gmres_and_bie():
     np.savez_compressed(os.path.join(HERE, "corrections_order2.npz"), **o2)
 
 
+if __name__ == "__main__" and "--complex-only" in sys.argv:
+    fmm_complex_wavenumber()
+    sys.exit(0)
+
 if __name__ == "__main__":
     special()
     translations()
     fmm_cases()
+    fmm_complex_wavenumber()
     gmres_and_bie()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):

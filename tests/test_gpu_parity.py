@@ -359,6 +359,12 @@ def test_complex_wavenumber(oracle, k):
     assert st["m2l_pairs"] > 0 and st["p2p_pairs"] > 0
     exact = oracle.direct_sum(xyz, q, k)
     assert rel_l2(y, exact) < 1e-5
+    # the oracle's FMM at the same order (bit-identical to the reference's for complex k as well,
+    # tests/test_oracle_golden.py): identical lists, FP32 distance of the potentials
+    fo = oracle.fmm(xyz, k, order, ncrit=40, leaf_cap=1.0 / abs(k), theta=0.4, kd_max=1.0)
+    co = fo.counts()
+    assert st["m2l_pairs"] == co["m2l_pairs"] and st["p2p_body_pairs"] == co["p2p_body_pairs"]
+    assert rel_l2(y, fo.matvec(q)) < 1e-5
     # near field alone (gate closed: every pair is evaluated directly)
     near = HfmmCuda(k=k, order=4, ncrit=50, kd_max=1e-9, leaf_cap=0.0)
     near.set_points(xyz[:2500])
