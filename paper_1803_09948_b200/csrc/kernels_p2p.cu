@@ -8,12 +8,17 @@
 //     leaves of the tile's list, so lanes stay full however few bodies a leaf holds
 //     (mean 18 per leaf at BASELINE config 2);
 //   * every lane keeps one complex accumulator PER TARGET in registers (statically unrolled),
-//     target coordinates are broadcast from shared memory;
+//     target coordinates are broadcast from shared memory, one array per axis;
+//   * TWO targets are evaluated per packed instruction (add / mul / fma.rn.f32x2): coordinates,
+//     distances and accumulators are (target 2j, target 2j+1) register pairs, only the MUFU
+//     evaluations stay scalar.  ncu: the XU (MUFU) pipe is the busiest unit (65 %) — three MUFU per
+//     pair (rsqrt, sin, cos) are the floor;
 //   * one warp-shuffle reduction per target at the very end.
-// Coordinates arrive pre-scaled by k and leaf-relative; the lattice offset between the two leaf
-// centres is added per source body.  G = (k/4pi) e^{iR'}/R' with R' = kR, the constant applied once
-// at the store.  Per pair (plain path): 3 FADD, 3 FFMA (R'^2), MUFU.RSQ, FMUL (R'), FMUL+MUFU.SIN,
-// MUFU.COS, 2 FMUL, 4 FFMA.
+// Coordinates arrive pre-scaled by k_r and leaf-relative; the lattice offset between the two leaf
+// centres is added per source body.  G = (k_r/4pi) e^{iR'}/R' with R' = k_r R, the constant applied
+// once at the store; a complex wavenumber adds the amplitude 2^{-damp R'} (one more MUFU, second
+// kernel instantiation).  CTAs hold two warps: one such CTA fits beside the two persistent M2L
+// CTAs of an SM, which is how the near field hides under M2L (engine.cu, phase_downward).
 //
 // Two passes per tile (kernels.cuh, P2PArgs):
 //   touching leaves (self included): compensated hi/lo coordinates, R == 0 masked — coincident

@@ -3,27 +3,41 @@
 // Replaces the reference's dense translate (src/expansion.cpp:126-139) of a Gaunt-built matrix
 // (src/expansion.cpp:95-124) by the factored, truncation-identical operator of tables.hpp:
 //     out += e^{-i mu phi} · E^T · Chat(k|t|) · E · e^{i m phi} · in
-// applied to a BATCH of 32 (source, destination) cell pairs that share one lattice shift, so the
-// rotation table E (real Wigner-d, block diagonal in n) and the coaxial table Chat (diagonal in m)
-// are staged once in shared memory and reused by every pair of the batch.
+// applied to a BATCH of 32 (source, destination) cell pairs that share the rotation table E (real
+// Wigner-d, block diagonal in n) and the coaxial table Chat (diagonal in m): one shift class, or —
+// where that fills the batches better — several classes of one table group that differ only in
+// azimuth (e^{i m phi} is carried per pair).  Both tables sit in shared memory for the whole group.
 //
-// Work layout of one CTA (8 warps, one batch):
-//   * operands live in two element-major shared tiles [coefficient][pair] (ping-pong): lane = pair,
-//     so a warp reads one coefficient of its 32 pairs with a conflict-free LDS.64;
-//   * every stage is cut into TASKS = a block (degree n for the rotations, order |m| for the
-//     coaxial step) times a tile of up to 12 (4) output rows.  A task keeps its output rows in
-//     registers and runs ONE runtime loop over the block's inputs: per step one LDS.64 (the input
-//     of the lane's pair) and R/4 broadcast LDS.128 (coefficients) feed 2R (8R coaxial) FFMAs;
-//   * tasks are handed to the warps by a host-side longest-processing-time schedule
-//     (TranslateSchedule); the code is small and loop-structured on purpose — a fully unrolled,
-//     order-specialised variant measured 7x SLOWER on B200 because its 256 KB of SASS starved
-//     the instruction cache (profiles/r01_notes.md);
+// What bounds the kernel is the shared-memory data pipe (ncu: l1tex__data_pipe_lsu_wavefronts 67-70 %
+// of peak, FMA pipe 37 %): a warp-uniform coefficient LDS.128 costs two wavefronts for 16 bytes.  The
+// layout below exists to spend as few wavefronts and instructions per multiply-add as possible.
+//
+// Work layout of one CTA (8 warps x 2 CTAs per SM up to P = 12, else 16 warps x 1), one batch:
+//   * operands live in two element-major shared tiles [coefficient][pair] (ping-pong); a LANE OWNS
+//     TWO PAIRS (16 lanes x 2 = 32), so one 16-byte LDS brings both operands and every broadcast
+//     coefficient feeds two multiply-adds; the halves of a warp run different sub-tasks;
+//   * all arithmetic is packed fma.rn.f32x2 (FFMA2): a complex accumulator is one register pair, a
+//     real coefficient the scalar operand, a complex multiply-add two instructions (same FLOP rate
+//     as FFMA, half the issue slots);
+//   * six barrier-separated stages per batch: gather (cp.async 8-byte copies straight into tile B,
+//     issued one batch ahead) | fold with e^{i m phi} (B -> A) | forward rotation (A -> B) |
+//     coaxial translation (B -> A) | inverse rotation (A -> B) | unfold (B -> A) + RED.E.ADD.F32x4
+//     into the destination rows;
+//   * the three arithmetic stages are cut into TASKS = pairs of sub-tasks (a tile of <= 8 rows of one
+//     folded rotation block, the plus system of degree n paired with the minus system of degree
+//     n + 1: same shape; or a tile of <= 4 rows of one order m of the coaxial step, both folded
+//     columns at once).  A sub-task keeps its output rows in registers and runs ONE runtime loop
+//     over the block's inputs.  Tasks are handed to the warps by a host-side
+//     longest-processing-time schedule kept in __constant__ memory (TranslateSchedule); the code is
+//     small and loop-structured on purpose — a fully unrolled, order-specialised variant measured
+//     3x SLOWER on B200 because its 256 KB of SASS starved the instruction cache
+//     (profiles/r01_notes.md);
 //   * rotations run on FOLDED vectors (tables.hpp): the +-m symmetry of the Wigner-d blocks halves
-//     their multiply-adds; vectors are folded in the gather and unfolded once before the reductions;
-//   * the inverse rotation reuses the same table through d^n_{mu,m'} = (-1)^{mu-m'} d^n_{m',mu};
-//   * pairs of one batch have different destinations: results leave through 16-byte vector
-//     reductions (RED.E.ADD.F32x4) into HBM/L2.
-// FP32 work per pair: 2 * 2*sum_n ((n+1)^2 + n^2) + 4*sum_m (P+1-|m|)^2 FFMAs (11.9 k at P = 12) against
+//     their multiply-adds; the inverse rotation reuses the same table through
+//     d^n_{mu,m'} = (-1)^{mu-m'} d^n_{m',mu};
+//   * CTAs are persistent and walk a contiguous range of batches; the next group's tables are
+//     fetched with cp.async behind the unfold.
+// FP32 work per pair: 2 * 2*sum_n ((n+1)^2 + n^2) + 4*sum_m (P+1-|m|)^2 FMAs (11.75 k at P = 12) against
 // 4 (P+1)^4 = 114 k for the reference's dense complex mat-vec.
 #include <algorithm>
 #include <cstdlib>
