@@ -31,6 +31,7 @@ __constant__ float c_b[(kMaxP + 1) * (kMaxP + 2) / 2];
 // reciprocals of the series denominators j (2n + 2j + 1), n <= kMaxP, j = 1..12
 constexpr int kSeriesTerms = 12;
 __constant__ float c_series[(kMaxP + 1) * kSeriesTerms];
+__constant__ float c_inv_odd[kMaxP + 1];  // 1 / (2n + 1)
 
 // jhat_n(z; s), n = 0..P, written to out[n * 32] (one shared-memory column per lane)
 __device__ void scaled_bessel(int P, float z, float s, float* out) {
@@ -304,8 +305,9 @@ l2p_kernel(const LeafExpansionArgs a, const float2* __restrict__ local, float2* 
         p2 = p1;
         p1 = pn;
         // Lhat pairs with j_n (2n-1)!!/s^n = jhat_n / (2n+1)
-        const float g = s_j[n * 32 + lane] * pn / float(2 * n + 1);
-        const float gi = CK ? s_ji[n * 32 + lane] * pn / float(2 * n + 1) : 0.0f;
+        const float pw = pn * c_inv_odd[n];
+        const float g = s_j[n * 32 + lane] * pw;
+        const float gi = CK ? s_ji[n * 32 + lane] * pw : 0.0f;
         const float2 lp = s_loc[n * (n + 1) + m];
         if (m == 0) {
           sr += g * lp.x - gi * lp.y;
@@ -348,6 +350,9 @@ void upload_legendre_constants(const float* diag, const float* sub, const float*
     for (int j = 1; j <= kSeriesTerms; ++j)
       series[n * kSeriesTerms + j - 1] = float(1.0 / (double(j) * (2 * n + 2 * j + 1)));
   HFMM_CUDA_CHECK(cudaMemcpyToSymbol(c_series, series, sizeof(series)));
+  float inv_odd[kMaxP + 1];
+  for (int n = 0; n <= kMaxP; ++n) inv_odd[n] = float(1.0 / (2.0 * n + 1.0));
+  HFMM_CUDA_CHECK(cudaMemcpyToSymbol(c_inv_odd, inv_odd, sizeof(inv_odd)));
 }
 
 void launch_p2m(const LeafExpansionArgs& a, const float2* body_q, float2* multipole, cudaStream_t s) {
