@@ -10,6 +10,7 @@
 // restated here (the restatement lives in hfmm_oracle.c).
 #include <algorithm>
 #include <cstring>
+#include <fstream>
 #include <memory>
 #include <string>
 #include <vector>
@@ -18,6 +19,7 @@
 #include "hfmm/kernel.hpp"
 #include "hfmm/let.hpp"
 #include "hfmm/mesh_gen.hpp"
+#include "hfmm/mesh_io.hpp"
 #include "hfmm/octree.hpp"
 #include "hfmm/oracle.hpp"
 #include "hfmm/partition.hpp"
@@ -484,6 +486,21 @@ int ref_update_alpha(const double* alpha, const double* runtime, int n, double a
     std::vector<part::AlphaSample> hist(n);
     for (int i = 0; i < n; ++i) hist[i] = part::AlphaSample{alpha[i], runtime[i]};
     *next = part::update_alpha(hist, alpha_max);
+  });
+}
+
+// mesh files of mesh_io.cpp written by the reference itself (fixtures for the readers of the CLI)
+int ref_write_sphere_mesh(double radius, int segments, int rings, const char* gmsh_path, const char* binary_path) {
+  return guarded([&] {
+    const auto mesh = meshio::sphere_mesh(radius, segments, rings);
+    if (gmsh_path) {
+      std::ofstream f(gmsh_path);
+      meshio::write_gmsh(mesh, f);
+    }
+    if (binary_path) {
+      std::ofstream f(binary_path, std::ios::binary);
+      meshio::write_binary(mesh, f);
+    }
   });
 }
 

@@ -2,6 +2,7 @@
 / cmd_scaling): thin drivers over the C ABI, everything heavy runs in libhfmm_b200.so on the GPU.
 
   python -m paper_1803_09948_b200 solve   --subdivisions 5 --k 4      sphere scattering, Mie check
+  python -m paper_1803_09948_b200 solve   --mesh sphere.msh --k 2      the same on a mesh file (meshio.py)
   python -m paper_1803_09948_b200 matvec  --config cfg2 [--n N]        one BASELINE FMM configuration
   python -m paper_1803_09948_b200 info                                 library version, device probes
 
@@ -32,7 +33,12 @@ def cmd_solve(a):
     from .workloads import icosphere_patches, mie_soft_sphere, patch_samples
 
     tables = _load_rules(a.rules)
-    patches = icosphere_patches(a.subdivisions, a.radius)
+    if a.mesh:       # GMSH MSH 2.2 ASCII or the reference's binary block format (meshio.py)
+        from .meshio import read_mesh
+        patches = read_mesh(a.mesh)
+        a.radius = float(np.linalg.norm(patches.reshape(-1, 3), axis=1).max())   # Mie check: a sphere about the origin
+    else:
+        patches = icosphere_patches(a.subdivisions, a.radius)
     xyz = patch_samples(patches, tables["sample_ref"])
     op = HfmmCuda(k=a.k, order=a.order, ncrit=a.ncrit, theta=a.theta, kd_max=a.kd_max, leaf_cap=-1.0)
     t0 = time.perf_counter(); op.set_points(xyz); t_tree = time.perf_counter() - t0
@@ -107,6 +113,7 @@ def main(argv=None):
     sub = ap.add_subparsers(dest="cmd", required=True)
     s = sub.add_parser("solve", help="plane-wave scattering off a sound-soft sphere, checked against the Mie series")
     s.add_argument("--subdivisions", type=int, default=5)
+    s.add_argument("--mesh", default=None, help="mesh file (MSH 2.2 ASCII with 6-node triangles, or HFMMMESH binary) instead of the icosphere")
     s.add_argument("--radius", type=float, default=1.0)
     s.add_argument("--k", type=float, default=4.0)
     s.add_argument("--order", type=int, default=12)

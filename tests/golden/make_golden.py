@@ -106,6 +106,14 @@ def fmm_complex_wavenumber():
                         direct=R.direct_sum(xyz, q, k), m2l_pairs=cnt["m2l_pairs"], p2p_body_pairs=cnt["p2p_body_pairs"])
 
 
+def mesh_files():
+    # the reference's two mesh formats, written by the reference itself (mesh_io.cpp)
+    import ctypes as C
+    rc = R.lib.ref_write_sphere_mesh(C.c_double(1.0), 8, 5, os.path.join(HERE, "sphere_8x5.msh").encode(),
+                                     os.path.join(HERE, "sphere_8x5.hfmm").encode())
+    assert rc == 0
+
+
 def gmres_and_bie():
     rng = np.random.default_rng(11)
     n = 48
@@ -152,6 +160,7 @@ if __name__ == "__main__":
     translations()
     fmm_cases()
     fmm_complex_wavenumber()
+    mesh_files()
     gmres_and_bie()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):

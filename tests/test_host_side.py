@@ -145,3 +145,44 @@ def test_update_alpha_matches_the_oracle_and_converges(oracle):
             update_alpha(*bad)
         assert e.value.kind == "config_error"
 
+
+def test_mesh_ingestion_reads_the_reference_s_files(tmp_path):
+    """meshio.py against files the reference wrote (tests/golden/sphere_8x5.msh / .hfmm, mesh_io.cpp):
+    both encodings carry the same elements, the writers reproduce the files byte for byte, rank blocks
+    tile the mesh, and the parser's refusals carry the reference's error kinds"""
+    from paper_1803_09948_b200 import meshio
+
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    g, b = os.path.join(here, "sphere_8x5.msh"), os.path.join(here, "sphere_8x5.hfmm")
+    a, skipped = meshio.read_gmsh(g)
+    assert a.shape == (64, 6, 3) and skipped == 0
+    assert np.array_equal(a, meshio.read_binary(b)) and np.array_equal(a, meshio.read_mesh(b))
+    assert np.allclose(np.linalg.norm(a.reshape(-1, 3), axis=1), 1.0, atol=1e-12)
+    meshio.write_gmsh(a, tmp_path / "w.msh")
+    assert meshio.write_binary(a, tmp_path / "w.hfmm") == 32 + 144 * 64
+    assert open(tmp_path / "w.msh").read() == open(g).read()
+    assert open(tmp_path / "w.hfmm", "rb").read() == open(b, "rb").read()
+    parts = [meshio.read_binary(b, r, 5) for r in range(5)]
+    assert [len(p) for p in parts] == [(r + 1) * 64 // 5 - r * 64 // 5 for r in range(5)]
+    assert np.array_equal(np.concatenate(parts), a)
+    # other element types are skipped and counted; unknown sections are skipped
+    text = open(g).read().replace("$Elements\n64\n", "$Elements\n65\n900 15 2 0 0 1\n")
+    text = text.replace("$Nodes", "$Comments\nanything\n$EndComments\n$Nodes", 1)
+    (tmp_path / "mixed.msh").write_text(text)
+    a2, skipped2 = meshio.read_gmsh(tmp_path / "mixed.msh")
+    assert skipped2 == 1 and np.array_equal(a2, a)
+    for bad, kind in ((text.replace("2.2 0 8", "4.1 0 8"), "format_error"),
+                      (text.replace("$EndNodes", "$EndNods"), "parse_error"),
+                      (open(g).read().replace(" 9 2 0 0 1 ", " 9 2 0 0 99999 ", 1), "structural_error")):
+        (tmp_path / "bad.msh").write_text(bad)
+        with pytest.raises(meshio.MeshError) as e:
+            meshio.read_gmsh(tmp_path / "bad.msh")
+        assert e.value.kind == kind, (kind, str(e.value))
+    (tmp_path / "bad.hfmm").write_bytes(b"NOTAMESH" + bytes(24))
+    with pytest.raises(meshio.MeshError) as e:
+        meshio.read_binary(tmp_path / "bad.hfmm")
+    assert e.value.kind == "format_error"
+    with pytest.raises(meshio.MeshError) as e:
+        meshio.read_binary(b, 3, 3)
+    assert e.value.kind == "config_error"
+
