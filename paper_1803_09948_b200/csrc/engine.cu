@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstring>
 #include <cstdlib>
 #include <cmath>
 #include <complex>
@@ -179,7 +180,14 @@ void Engine::require_points() const {
 // batched together: the kernel carries e^{i m phi} per pair.  Returns the order in which the classes
 // are laid out (group by group) and the group of every class.
 // batches per table group must save at least 3 % of the batches to pay for the per-pair phases
-static constexpr double kMixedBatchGain = 0.97;
+// (HFMM_BATCHING=group|class forces one layout: used by the tests to run both kernel instantiations)
+static constexpr double kMixedBatchGainDefault = 0.97;
+static double mixed_batch_gain() {
+  const char* e = getenv("HFMM_BATCHING");
+  if (e && !strcmp(e, "group")) return 1e9;
+  if (e && !strcmp(e, "class")) return -1.0;
+  return kMixedBatchGainDefault;
+}
 
 static void group_classes(const std::vector<TranslateClass>& classes, std::vector<uint32_t>& order,
                           std::vector<uint32_t>& group_of) {
@@ -239,7 +247,7 @@ void Engine::upload_stage(TranslateStage& st, const std::vector<uint32_t>& src,
   st.mixed = true;
   {
     std::vector<TranslateItem> per_class = cut(false);
-    if (double(items.size()) > kMixedBatchGain * double(per_class.size())) {
+    if (double(items.size()) > mixed_batch_gain() * double(per_class.size())) {
       items.swap(per_class);
       st.mixed = false;
     }
@@ -333,7 +341,7 @@ void Engine::build_m2l_stage_device(TableRegistry& reg, const FarClasses& fc) {
   }
   seg_new[nc] = uint32_t(pos);
   // batches per table group only when that saves batches (see upload_stage)
-  m2l_.mixed = double(items.size()) <= kMixedBatchGain * double(per_class.size());
+  m2l_.mixed = double(items.size()) <= mixed_batch_gain() * double(per_class.size());
   if (!m2l_.mixed) items.swap(per_class);
   if (pos >= (uint64_t(1) << 32)) throw Error(HFMM_ERR_CONFIG, "pair count exceeds 32-bit indexing");
   regroup_pairs_device(seg_new, seg_old, seg_cls, pos, m2l_.pair_src, m2l_.pair_dst, m2l_.pair_cls, stream_);

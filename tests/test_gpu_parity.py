@@ -381,3 +381,23 @@ def test_complex_wavenumber(oracle, k):
         c = f.counts()
         assert st["m2l_pairs"] == c["m2l_pairs"] and st["p2p_body_pairs"] == c["p2p_body_pairs"]
         assert rel_l2(y, f.matvec(q)) < 1e-5
+
+
+@pytest.mark.parametrize("order", [6, 13])
+def test_both_batch_layouts_of_the_translation_kernel(oracle, monkeypatch, order):
+    """batches cut per table group (per-pair azimuth phases) and per shift class (per-class phases) are two
+    instantiations of the kernel; the library picks by batch count — force each and compare (order 13
+    runs the 16-warp variant)"""
+    n, k = 9000, 5.0
+    xyz, q = plummer_points(n, 41), charges(n, 41)
+    res, batches = {}, {}
+    for layout in ("group", "class"):
+        monkeypatch.setenv("HFMM_BATCHING", layout)
+        op = HfmmCuda(k=k, order=order, ncrit=32)
+        op.set_points(xyz)
+        res[layout] = op.matvec(q)
+        batches[layout] = op.stats()["m2l_batches"]
+    assert batches["group"] < batches["class"]
+    assert rel_l2(res["group"], res["class"]) < 1e-6
+    tg = np.arange(0, n, 23)
+    assert rel_l2(res["class"][tg], oracle.direct_sum(xyz, q, k, tg)) < (2e-5 if order == 6 else 2e-6)
