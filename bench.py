@@ -86,28 +86,36 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(loaded)}
 
 
-def cpu_reference_arm(cfg, n_sample: int, steps: int, warmup: int) -> dict:
+def cpu_reference_arm(cfg, n_sample: int, steps: int, warmup: int, budget_s: float = 0.0) -> dict:
     """The reference's own CPU implementation (oracle/_ref when it compiled, else our C port) on a
-    bounded sample of the workload, all host threads."""
+    bounded sample of the workload, all host threads.  With a budget the number of timed matvecs is
+    cut so that the whole arm ends inside it (the first matvec is always run)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from checkers import Oracle, Ref, have_ref
 
     kind = "reference" if have_ref() else "port"
     eng = Ref() if have_ref() else Oracle()
+    n_sample = min(n_sample, cfg.n)
     xyz, q = make_points(cfg, n_sample), charges(n_sample, cfg.seed)
     cores = os.cpu_count() or 1
     f = eng.fmm(xyz, cfg.k, cfg.order, ncrit=cfg.ncrit, leaf_cap=cfg.resolved_leaf_cap(),
                 theta=cfg.theta, kd_max=cfg.kd_max, threads=cores)
+    t_start = time.perf_counter()
     for _ in range(warmup):
         f.matvec(q)
     t0 = time.perf_counter()
-    for _ in range(steps):
+    done = 0
+    while done < max(steps, 1):
         f.matvec(q)
-    dt = (time.perf_counter() - t0) / max(steps, 1)
+        done += 1
+        per = (time.perf_counter() - t_start) / (warmup + done)
+        if budget_s and time.perf_counter() - t_start + per > budget_s:
+            break
+    dt = (time.perf_counter() - t0) / done
     return {"value": n_sample / dt * 1e-6, "unit": UNIT, "cores": cores, "kind": kind,
-            "seconds_per_matvec": dt,
+            "seconds_per_matvec": dt, "steps": done,
             "sample": f"{n_sample} of {cfg.n} points, same distribution/k/P/ncrit/theta/kd_max/cap; "
-                      f"{steps} matvec(s) after {warmup} warm-up; FP64, std::thread x{cores}"
+                      f"{done} matvec(s) after {warmup} warm-up; FP64, std::thread x{cores}"
                       if kind == "reference" else
                       f"{n_sample} of {cfg.n} points; C port with OpenMP x{cores}"}
 
@@ -115,13 +123,15 @@ def cpu_reference_arm(cfg, n_sample: int, steps: int, warmup: int) -> dict:
 def run_reference(args, cfg, rank: int):
     if rank != 0:
         return
-    n_sample = args.ref_points
-    # The reference rebuilds one dense translation matrix per distinct shift on every call
-    # (traversal.cpp:252-256), which costs 13-20 s per matvec on 8 cores whatever the sample size;
-    # the arm is therefore budgeted to ~150 s: at most 7 timed matvecs and 1 warm-up.
-    steps = max(1, min(args.steps, 7))
+    # The sample is a quarter of the points (262,144 of cfg 2's 1,048,576): the reference rebuilds one
+    # dense translation matrix per distinct shift on every call (traversal.cpp:252-256), a cost that
+    # does not shrink with the sample (6 s per matvec on 16 cores), so a small sample would understate
+    # its throughput: measured 0.0026 / 0.0052 / 0.0059 Mpoints/s at 16 k / 131 k / 262 k points.
+    # One matvec takes ~45 s on 16 cores; the arm is budgeted to ~170 s: at most one warm-up and as
+    # many of the requested timed matvecs as fit.
     warmup = min(args.warmup, 1)
-    base = cpu_reference_arm(cfg, n_sample, steps, warmup)
+    base = cpu_reference_arm(cfg, args.ref_arm_points, max(1, min(args.steps, 7)), warmup, budget_s=170.0)
+    steps = base["steps"]
     line = {
         "impl": "reference", "metric": METRIC, "value": base["value"], "unit": UNIT,
         "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
@@ -353,7 +363,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default=None, help="cfg1|cfg2|cfg4|cfg5 (default: cfg2 at N=1, cfg5 weak at N>1)")
     ap.add_argument("--n", type=int, default=None, help="override the point count (debug)")
-    ap.add_argument("--ref-points", type=int, default=16384, help="sample size of the CPU arm")
+    ap.add_argument("--ref-points", type=int, default=131072,
+                    help="sample size of the cpu_baseline leg of the default arm (one matvec, ~25 s on 16 cores)")
+    ap.add_argument("--ref-arm-points", type=int, default=262144, help="sample size of --impl reference")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-bie", action="store_true", help="skip the configs[2] BIE solve reported next to the headline")
     ap.add_argument("--force-distributed", action="store_true",
