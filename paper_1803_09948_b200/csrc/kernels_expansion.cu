@@ -175,12 +175,6 @@ __device__ __forceinline__ BodyFrame body_frame(const float4 p) {
   return f;
 }
 
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
 // CK: complex wavenumber (radial functions and the i k q weight are complex)
 template <bool CK>
 __global__ void __launch_bounds__(kWarps * 32)
@@ -200,6 +194,8 @@ p2m_kernel(const LeafExpansionArgs a, const float2* __restrict__ body_q, float2*
   const float s = a.level_scale[a.cell_geom[cell].w];
   for (int i = lane; i < dim; i += 32) s_acc[i] = make_float2(0.f, 0.f);
   __syncwarp();
+  float* s_accf = reinterpret_cast<float*>(s_acc);
+  const bool hi16 = (lane & 16) != 0, hi8 = (lane & 8) != 0, writer = (lane & 7) == 0;
 
   for (uint32_t base = 0; base < cb.y; base += 32) {
     const bool ok = base + lane < cb.y;
@@ -230,27 +226,25 @@ p2m_kernel(const LeafExpansionArgs a, const float2* __restrict__ body_q, float2*
         const float g = s_j[n * 32 + lane] * pn, gi = CK ? s_ji[n * 32 + lane] * pn : 0.0f;
         // +m: conj Y = Pbar (cm - i sm)
         const float br = wr * cm + wi * sm, bi = wi * cm - wr * sm;
-        float vr = g * br - gi * bi, vi = g * bi + gi * br;
-        vr = warp_sum(vr);
-        vi = warp_sum(vi);
-        if (lane == 0) {
-          float2& d = s_acc[n * (n + 1) + m];
-          d.x += vr;
-          d.y += vi;
-        }
+        const float vr = g * br - gi * bi, vi = g * bi + gi * br;
+        // -m: conj Y_n^{-m} = (-1)^m Pbar (cm + i sm)   (m = 0: slots 2, 3 carry zeros and are not stored)
+        float ur = 0.0f, ui = 0.0f;
         if (m > 0) {
-          // -m: conj Y_n^{-m} = (-1)^m Pbar (cm + i sm)
           const float sg = (m & 1) ? -1.0f : 1.0f;
           const float er = wr * cm - wi * sm, ei = wi * cm + wr * sm;
-          float ur = sg * (g * er - gi * ei), ui = sg * (g * ei + gi * er);
-          ur = warp_sum(ur);
-          ui = warp_sum(ui);
-          if (lane == 0) {
-            float2& d = s_acc[n * (n + 1) - m];
-            d.x += ur;
-            d.y += ui;
-          }
+          ur = sg * (g * er - gi * ei);
+          ui = sg * (g * ei + gi * er);
         }
+        // four sums over the 32 bodies in one butterfly: the first two exchanges halve the number of
+        // values a lane carries (6 shuffles instead of 20; the pairing order, hence the rounding, is
+        // that of four separate reductions); lanes 0 / 8 / 16 / 24 end up with Re(+m), Im(+m), Re(-m), Im(-m)
+        const float k0 = hi16 ? ur : vr, s0 = hi16 ? vr : ur, k1 = hi16 ? ui : vi, s1 = hi16 ? vi : ui;
+        const float b0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 16), b1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 16);
+        float c = (hi8 ? b1 : b0) + __shfl_xor_sync(0xffffffffu, hi8 ? b0 : b1, 8);
+        c += __shfl_xor_sync(0xffffffffu, c, 4);
+        c += __shfl_xor_sync(0xffffffffu, c, 2);
+        c += __shfl_xor_sync(0xffffffffu, c, 1);
+        if (writer && (m > 0 || !hi16)) s_accf[2 * (n * (n + 1) + (hi16 ? -m : m)) + (hi8 ? 1 : 0)] += c;
       }
     }
     __syncwarp();
