@@ -309,24 +309,25 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 8) p2p_kernel(const P2PAr
     }
   }
 
-  // per-target reduction over the 32 source lanes; lane t keeps target t
-  float out_r = 0.f, out_i = 0.f;
+  // per-target reduction over the 32 source lanes; lane t keeps target t.  One butterfly for all 32
+  // targets: at every exchange a lane hands over the half of its values that its partner keeps
+  // (16 + 8 + 4 + 2 packed pairs, then the two halves of the last pair: 31 shuffled words per array
+  // instead of 160); the pairing order — hence the rounding — is that of 32 separate reductions.
 #pragma unroll
-  for (int t = 0; t < kTile; ++t) {
-    if (t < tile.n_t) {
-      const float2 pr = unpack2(ar[t / 2]), pi = unpack2(ai[t / 2]);
-      float vr = (t & 1) ? pr.y : pr.x, vi = (t & 1) ? pi.y : pi.x;
+  for (int half = kPairs / 2, o = 16; half >= 1; half >>= 1, o >>= 1) {
+    const bool up = (lane & o) != 0;
 #pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) {
-        vr += __shfl_xor_sync(0xffffffffu, vr, o);
-        vi += __shfl_xor_sync(0xffffffffu, vi, o);
-      }
-      if (lane == t) {
-        out_r = vr;
-        out_i = vi;
-      }
+    for (int i = 0; i < half; ++i) {
+      const u64 kr = up ? ar[i + half] : ar[i], sr = up ? ar[i] : ar[i + half];
+      const u64 ki = up ? ai[i + half] : ai[i], si = up ? ai[i] : ai[i + half];
+      ar[i] = add2(kr, __shfl_xor_sync(0xffffffffu, sr, o));
+      ai[i] = add2(ki, __shfl_xor_sync(0xffffffffu, si, o));
     }
   }
+  const float2 pr = unpack2(ar[0]), pi = unpack2(ai[0]);
+  const bool odd = (lane & 1) != 0;
+  const float out_r = (odd ? pr.y : pr.x) + __shfl_xor_sync(0xffffffffu, odd ? pr.x : pr.y, 1);
+  const float out_i = (odd ? pi.y : pi.x) + __shfl_xor_sync(0xffffffffu, odd ? pi.x : pi.y, 1);
   if (lane < tile.n_t) a.out[tslot] = make_float2(out_r * a.out_scale, out_i * a.out_scale);
 }
 
