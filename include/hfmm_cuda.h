@@ -45,7 +45,14 @@ enum {
   HFMM_FLAG_PHASE_TIMERS = 1 << 1,
   /* enqueue the near field before the far field.  Default: behind the persistent M2L launch, so one
    * near-field CTA runs beside the two M2L CTAs of every SM (MUFU-bound next to shared-memory-bound) */
-  HFMM_FLAG_NEAR_FIRST = 1 << 2
+  HFMM_FLAG_NEAR_FIRST = 1 << 2,
+  /* run-to-run reproducible results (TraversalConfig::deterministic, traversal.hpp:11-22: per-target
+   * ordered accumulation).  M2M and M2L stage one row per cell pair and add the rows of every
+   * destination cell in list order instead of using floating-point atomics; costs three extra passes
+   * over the staged rows (cfg 2: +40 % per matvec) and up to HFMM_ORDERED_STAGING_MB (environment,
+   * default 4096) MiB of device memory.  The near field, the leaf passes and the Krylov reductions
+   * are ordered in every mode. */
+  HFMM_FLAG_DETERMINISTIC = 1 << 3
 };
 
 /* POD mirror of WaveNumber (common.hpp:37-40), TraversalConfig (traversal.hpp:11-18) and the

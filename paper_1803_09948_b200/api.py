@@ -14,6 +14,7 @@ _SO = os.path.join(_HERE, "libhfmm_b200.so")
 HFMM_FLAG_HOST_TREE = 1 << 0
 HFMM_FLAG_PHASE_TIMERS = 1 << 1
 HFMM_FLAG_NEAR_FIRST = 1 << 2
+HFMM_FLAG_DETERMINISTIC = 1 << 3
 
 _STATUS = {1: "config_error", 2: "singular_error", 3: "structural_error", 4: "accuracy_error",
            5: "domain_error", 6: "device_error", 9: "internal_error"}

@@ -205,9 +205,39 @@ static void group_classes(const std::vector<TranslateClass>& classes, std::vecto
   }
 }
 
+// HFMM_FLAG_DETERMINISTIC: cut the stage into ranges of whole batches that fit the staging buffer and
+// sort every range's pairs by destination (stable) for the ordered reduction (run_stage)
+void Engine::plan_ordered_reduce(TranslateStage& st, const std::vector<TranslateItem>& items) {
+  st.ordered.clear();
+  st.row_of_pair.release();
+  if (!(cfg_.flags & HFMM_FLAG_DETERMINISTIC) || items.empty()) return;
+  size_t budget_mb = 4096;
+  if (const char* e = getenv("HFMM_ORDERED_STAGING_MB")) budget_mb = std::max<size_t>(1, strtoull(e, nullptr, 10));
+  const uint64_t row_bytes = uint64_t(stride_) * sizeof(float2);
+  const uint64_t max_rows = std::max<uint64_t>(translate_batch_size(cfg_.order), (budget_mb << 20) / row_bytes);
+  const uint64_t total = uint64_t(items.back().pair_begin) + items.back().count;
+  st.row_of_pair.resize(total);
+  uint64_t most = 0;
+  for (size_t i = 0; i < items.size();) {
+    TranslateStage::OrderedRange r;
+    r.item_begin = uint32_t(i);
+    r.pair_begin = items[i].pair_begin;
+    uint64_t rows = 0;
+    while (i < items.size() && rows + items[i].count <= max_rows) rows += items[i++].count;
+    r.n_items = uint32_t(i) - r.item_begin;
+    r.n_pairs = uint32_t(rows);
+    launch_range_rows(st.row_of_pair.get(), r.pair_begin, r.n_pairs, stream_);
+    r.n_segs = build_ordered_reduce_device(st.pair_dst.get(), r.pair_begin, r.n_pairs, r.perm, r.seg_dst,
+                                           r.seg_begin, stream_);
+    most = std::max(most, rows);
+    st.ordered.push_back(std::move(r));
+  }
+  if (ordered_staging_.size() < most * stride_) ordered_staging_.resize(most * stride_);
+}
+
 void Engine::upload_stage(TranslateStage& st, const std::vector<uint32_t>& src,
                           const std::vector<uint32_t>& dst, const std::vector<uint32_t>& cls_of_pair,
-                          const std::vector<TranslateClass>& classes) {
+                          const std::vector<TranslateClass>& classes, bool ordered) {
   // stable counting sort of the pairs by class (classes laid out group by group), then batches of
   // kTranslateBatch pairs cut per table group
   const size_t np = src.size(), nc = classes.size();
@@ -260,6 +290,7 @@ void Engine::upload_stage(TranslateStage& st, const std::vector<uint32_t>& src,
   st.pair_src.upload(s_sorted, stream_);
   st.pair_dst.upload(d_sorted, stream_);
   st.pair_cls.upload(c_sorted, stream_);
+  if (ordered) plan_ordered_reduce(st, items);
   HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
 }
 
@@ -293,7 +324,7 @@ void Engine::build_m2l_stage_host(TableRegistry& reg, const PairLists& pairs) {
   }
   stats_.m2l_shift_classes = classes.size();
   owned_m2l_pairs_ = own_src.size();
-  upload_stage(m2l_, own_src, own_dst, cls_of_pair, classes);
+  upload_stage(m2l_, own_src, own_dst, cls_of_pair, classes, true);
 }
 
 // M2L stage from the device builder's sorted pairs + run-length-encoded shift classes
@@ -352,6 +383,7 @@ void Engine::build_m2l_stage_device(TableRegistry& reg, const FarClasses& fc) {
   m2l_.items.upload(items, stream_);
   m2l_.classes.upload(classes, stream_);
   HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  plan_ordered_reduce(m2l_, items);
 }
 
 // M2M / L2L stages per level, translation tables, leaf lists, expansion storage
@@ -393,7 +425,7 @@ void Engine::finish_far_field(TableRegistry& reg) {
       cls.push_back(uint32_t(cls_of_oct[oct]));
     }
     TranslateStage st;
-    upload_stage(st, src, dst, cls, cl);
+    upload_stage(st, src, dst, cls, cl, upward);
     return st;
   };
   for (int L = t.max_level; L > lmin_src_; --L) m2m_.push_back(level_stage(L, true));
@@ -849,6 +881,24 @@ void Engine::run_stage(const TranslateStage& st, const float2* src, float2* dst)
   ta.dst = dst;
   ta.order = cfg_.order;
   ta.stride = stride_;
+  if (!st.ordered.empty()) {
+    // deterministic accumulation: every pair adds into its own (zeroed) staging row — one
+    // contribution per row, so the atomics of the kernel have nothing to reorder — and the rows of a
+    // destination are then summed in pair order
+    const uint32_t dim = uint32_t(cfg_.order + 1) * uint32_t(cfg_.order + 1);
+    for (const auto& r : st.ordered) {
+      HFMM_CUDA_CHECK(cudaMemsetAsync(ordered_staging_.get(), 0, size_t(r.n_pairs) * stride_ * sizeof(float2), stream_));
+      ta.items = st.items.get() + r.item_begin;
+      ta.n_items = r.n_items;
+      ta.pair_dst = st.row_of_pair.get();
+      ta.dst = ordered_staging_.get();
+      launch_translate(ta, stream_);
+      launch_ordered_reduce(ordered_staging_.get(), r.perm.get(), r.seg_begin.get(), r.seg_dst.get(), r.n_segs, dst,
+                            uint32_t(stride_), dim, stream_);
+      launches_ += 2;
+    }
+    return;
+  }
   launch_translate(ta, stream_);
   if (st.n_items) ++launches_;
 }

@@ -27,6 +27,16 @@ struct TranslateStage {
   uint32_t n_items = 0;
   uint64_t n_pairs = 0;
   bool mixed = false;  // batches mix the classes of a table group (per-pair azimuth phases in the kernel)
+  // HFMM_FLAG_DETERMINISTIC: the stage runs range by range (whole batches, as many pairs as the staging
+  // buffer has rows) into one staging row per pair; an ordered reduction then adds the rows of every
+  // destination in pair order (the reference's per-target ordered accumulation, traversal.hpp:20-22)
+  struct OrderedRange {
+    uint32_t item_begin = 0, n_items = 0, n_pairs = 0, n_segs = 0;
+    uint64_t pair_begin = 0;
+    DeviceBuffer<uint32_t> perm, seg_dst, seg_begin;
+  };
+  std::vector<OrderedRange> ordered;
+  DeviceBuffer<uint32_t> row_of_pair;  // staging row of every pair (index inside its range)
 };
 
 class Engine {
@@ -92,9 +102,10 @@ class Engine {
   void finish_far_field(TableRegistry& reg);
   void upload_cell_geometry(std::vector<int4>& geom);
   void build_tiles(const std::vector<uint64_t>& work);
+  void plan_ordered_reduce(TranslateStage& st, const std::vector<TranslateItem>& items);
   void upload_stage(TranslateStage& st, const std::vector<uint32_t>& src,
                     const std::vector<uint32_t>& dst, const std::vector<uint32_t>& cls_of_pair,
-                    const std::vector<TranslateClass>& classes);
+                    const std::vector<TranslateClass>& classes, bool ordered = false);
 
   hfmm_cuda_config cfg_;
   double leaf_cap_ = 0;
@@ -140,6 +151,7 @@ class Engine {
   int lmin_src_ = 0, lmin_dst_ = 0;
   bool have_far_ = false;
   DeviceBuffer<float2> multipole_, local_;
+  DeviceBuffer<float2> ordered_staging_;  // HFMM_FLAG_DETERMINISTIC: one row per pair of the largest range
   DeviceBuffer<uint32_t> p2m_leaves_, l2p_leaves_;
   uint32_t n_p2m_leaves_ = 0, n_l2p_leaves_ = 0;
   DeviceBuffer<float> rot_tables_, coax_tables_;

@@ -106,7 +106,8 @@ void Engine::gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cf
 
   DeviceBuffer<float2> V(size_t(m + 1) * n), w(n), u(n), r32(n);
   DeviceBuffer<double2> b64(n), x64(n);
-  DeviceBuffer<double> scal(size_t(2) * (2 * (m + 1) + 2)), ydev(size_t(2) * m);
+  DeviceBuffer<double> scal(size_t(2) * (2 * (m + 1) + 2)), ydev(size_t(2) * m), red(reduce_scratch_doubles());
+  red.zero(stream_);
   std::vector<double> hscal(scal.size());
   HFMM_CUDA_CHECK(cudaMemcpyAsync(b64.get(), rhs, size_t(n) * sizeof(double2), cudaMemcpyHostToDevice, stream_));
   x64.zero(stream_);
@@ -145,7 +146,7 @@ void Engine::gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cf
       double* h1 = s0 + 2;                      // pass 1, j+1 entries
       double* h2 = h1 + 2 * (m + 1);            // pass 2
       double* hn = h2 + 2 * (m + 1);            // ||w||^2 after both passes
-      launch_norm2(n, w.get(), s0, stream_);
+      launch_norm2(n, w.get(), s0, red.get(), stream_);
       for (int pass = 0; pass < 2; ++pass) {
         double* hp = pass ? h2 : h1;
         for (int i = 0; i <= j; ++i) {
@@ -158,11 +159,11 @@ void Engine::gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cf
             vprev = V.get() + size_t(j) * n;
             cprev = h1 + 2 * j;
           }
-          launch_mgs_step(n, w.get(), vprev, cprev, V.get() + size_t(i) * n, hp + 2 * i, stream_);
+          launch_mgs_step(n, w.get(), vprev, cprev, V.get() + size_t(i) * n, hp + 2 * i, red.get(), stream_);
         }
       }
-      launch_mgs_step(n, w.get(), V.get() + size_t(j) * n, h2 + 2 * j, nullptr, nullptr, stream_);
-      launch_norm2(n, w.get(), hn, stream_);
+      launch_mgs_step(n, w.get(), V.get() + size_t(j) * n, h2 + 2 * j, nullptr, nullptr, red.get(), stream_);
+      launch_norm2(n, w.get(), hn, red.get(), stream_);
       scal.download(hscal.data(), hscal.size(), stream_);
       HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
       const double w_scale = std::sqrt(hscal[0]);
@@ -227,7 +228,7 @@ void Engine::gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cf
       launch_narrow(n, x64.get(), r32.get(), stream_);
       apply(r32.get(), w.get());
       scal.zero(stream_);
-      launch_residual(n, b64.get(), w.get(), r32.get(), scal.get(), stream_);
+      launch_residual(n, b64.get(), w.get(), r32.get(), scal.get(), red.get(), stream_);
       scal.download(hscal.data(), 2, stream_);
       HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
       beta = std::sqrt(hscal[0]);
@@ -237,7 +238,7 @@ void Engine::gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cf
   launch_narrow(n, x64.get(), V.get(), stream_);
   apply(V.get(), w.get());
   scal.zero(stream_);
-  launch_residual(n, b64.get(), w.get(), r32.get(), scal.get(), stream_);
+  launch_residual(n, b64.get(), w.get(), r32.get(), scal.get(), red.get(), stream_);
   scal.download(hscal.data(), 2, stream_);
   // the returned iterate maps back through M^-1 (solver.cpp:388)
   if (precond) {
@@ -291,7 +292,8 @@ void Engine::dist_gmres(const double* rhs, double* x_out, const hfmm_gmres_confi
 
   DeviceBuffer<float2> V(size_t(m + 1) * ml), w(ml), r32(ml), full(n), vc(n), pc(n), yc(corr ? n : 1);
   DeviceBuffer<double2> b64(ml), x64(ml);
-  DeviceBuffer<double> scal(4), ydev(size_t(2) * m);
+  DeviceBuffer<double> scal(4), ydev(size_t(2) * m), red(reduce_scratch_doubles());
+  red.zero(stream_);
   HFMM_CUDA_CHECK(cudaMemcpyAsync(b64.get(), rhs, size_t(mloc) * sizeof(double2), cudaMemcpyHostToDevice, stream_));
   x64.zero(stream_);
   launch_narrow(mloc, b64.get(), r32.get(), stream_);
@@ -331,15 +333,15 @@ void Engine::dist_gmres(const double* rhs, double* x_out, const hfmm_gmres_confi
   // <v, w> (v may be null: ||w||^2) reduced over all ranks
   auto dot = [&](const float2* v, const float2* ww, double out[2]) {
     scal.zero(stream_);
-    if (v) launch_mgs_step(mloc, const_cast<float2*>(ww), nullptr, nullptr, v, scal.get(), stream_);
-    else launch_norm2(mloc, ww, scal.get(), stream_);
+    if (v) launch_mgs_step(mloc, const_cast<float2*>(ww), nullptr, nullptr, v, scal.get(), red.get(), stream_);
+    else launch_norm2(mloc, ww, scal.get(), red.get(), stream_);
     scal.download(out, 2, stream_);
     HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
     reduce(out, 2);
   };
   auto axpy = [&](float2* ww, const float2* v, const double h[2]) {  // ww -= h v
     HFMM_CUDA_CHECK(cudaMemcpyAsync(scal.get() + 2, h, 2 * sizeof(double), cudaMemcpyHostToDevice, stream_));
-    launch_mgs_step(mloc, ww, v, scal.get() + 2, nullptr, nullptr, stream_);
+    launch_mgs_step(mloc, ww, v, scal.get() + 2, nullptr, nullptr, red.get(), stream_);
   };
 
   std::vector<cd> H(size_t(m + 1) * m), cs(m), sn(m), g(m + 1);
@@ -421,7 +423,7 @@ void Engine::dist_gmres(const double* rhs, double* x_out, const hfmm_gmres_confi
       launch_narrow(mloc, x64.get(), r32.get(), stream_);
       apply(r32.get(), w.get());
       scal.zero(stream_);
-      launch_residual(mloc, b64.get(), w.get(), r32.get(), scal.get(), stream_);
+      launch_residual(mloc, b64.get(), w.get(), r32.get(), scal.get(), red.get(), stream_);
       scal.download(tmp, 2, stream_);
       HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
       reduce(tmp, 1);
@@ -431,7 +433,7 @@ void Engine::dist_gmres(const double* rhs, double* x_out, const hfmm_gmres_confi
   launch_narrow(mloc, x64.get(), V.get(), stream_);
   apply(V.get(), w.get());
   scal.zero(stream_);
-  launch_residual(mloc, b64.get(), w.get(), r32.get(), scal.get(), stream_);
+  launch_residual(mloc, b64.get(), w.get(), r32.get(), scal.get(), red.get(), stream_);
   scal.download(tmp, 2, stream_);
   HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
   reduce(tmp, 1);

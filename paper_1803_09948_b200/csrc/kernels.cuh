@@ -149,20 +149,31 @@ void launch_gather_charges(const double2* q_caller, const float2* q_caller_f32,
 void launch_scatter_potentials(const float2* near, const float2* far, const uint32_t* index,
                                double2* out_f64, float2* out_f32, uint32_t n, cudaStream_t s);
 
+// Deterministic accumulation: dst row seg_dst[s] += the staged rows perm[seg_begin[s] .. seg_begin[s+1])
+// in that order (one warp per segment; no atomics).  Rows are `stride` float2 apart, `dim` are used.
+void launch_ordered_reduce(const float2* staging, const uint32_t* perm, const uint32_t* seg_begin,
+                           const uint32_t* seg_dst, uint32_t n_segs, float2* dst, uint32_t stride,
+                           uint32_t dim, cudaStream_t s);
+// row_of_pair[i] = i - begin for i in [begin, begin + n)
+void launch_range_rows(uint32_t* row_of_pair, uint64_t begin, uint32_t n, cudaStream_t s);
+
 // ---- BIE operator tail + Krylov vector ops (kernels_krylov.cu) -------------------------------
 void launch_corrections(uint32_t n, int ni, const float2* block, const uint32_t* off, const uint32_t* src,
                         const float2* delta, const float2* x, float2* y, cudaStream_t s);
 void launch_precondition(uint32_t npatch, int ni, const float2* lu, const int* piv, const float2* in,
                          float2* out, cudaStream_t s);
+// The reducing kernels (mgs_step, norm2, residual) sum in a fixed order (reproducible run to run):
+// scratch = reduce_scratch_doubles() zero-initialised doubles, private to the stream.
+size_t reduce_scratch_doubles();
 // w -= h_prev * v_prev (skipped when v_prev is null); out[0..1] += <v_next, w> (skipped when null)
 void launch_mgs_step(uint32_t n, float2* w, const float2* v_prev, const double* h_prev,
-                     const float2* v_next, double* out, cudaStream_t s);
-void launch_norm2(uint32_t n, const float2* w, double* out, cudaStream_t s);
+                     const float2* v_next, double* out, double* scratch, cudaStream_t s);
+void launch_norm2(uint32_t n, const float2* w, double* out, double* scratch, cudaStream_t s);
 void launch_scale(uint32_t n, const float2* in, float scale, float2* out, cudaStream_t s);
 void launch_update_solution(uint32_t n, int cols, const float2* basis, size_t ld, const double* y,
                             double2* x, cudaStream_t s);
 void launch_residual(uint32_t n, const double2* b, const float2* ax, float2* r32, double* out,
-                     cudaStream_t s);
+                     double* scratch, cudaStream_t s);
 void launch_narrow(uint32_t n, const double2* in, float2* out, cudaStream_t s);
 // out[o] = scale * sum_i q_i e^{i|o-x_i|} e^{-eps |o-x_i|}/|o-x_i| over k_r-scaled absolute coordinates
 // (eps = k_i / k_r, 0 for a real wavenumber)

@@ -17,6 +17,7 @@ namespace hfmm_b200 {
 namespace {
 
 constexpr int kBlock = 256;
+constexpr uint32_t kReduceBlocks = 148u * 8u;  // most blocks a reducing kernel is launched with
 
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
@@ -24,26 +25,50 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-// block-wide sum of a (re, im) pair, then one atomicAdd per block into out[0], out[1]
-__device__ __forceinline__ void block_accumulate(double re, double im, double* out) {
+// block-wide sum of a (re, im) pair (fixed order)
+__device__ __forceinline__ void block_sum(double& re, double& im) {
   __shared__ double s_re[kBlock / 32], s_im[kBlock / 32];
   re = warp_sum_d(re);
   im = warp_sum_d(im);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();  // the previous use of s_re / s_im is over
   if (lane == 0) {
     s_re[warp] = re;
     s_im[warp] = im;
   }
   __syncthreads();
-  if (warp == 0) {
-    re = lane < kBlock / 32 ? s_re[lane] : 0.0;
-    im = lane < kBlock / 32 ? s_im[lane] : 0.0;
-    re = warp_sum_d(re);
-    im = warp_sum_d(im);
-    if (lane == 0) {
-      atomicAdd(out, re);
-      atomicAdd(out + 1, im);
-    }
+  re = lane < kBlock / 32 ? s_re[lane] : 0.0;
+  im = lane < kBlock / 32 ? s_im[lane] : 0.0;
+  re = warp_sum_d(re);
+  im = warp_sum_d(im);
+}
+
+// Grid-wide sum into out[0], out[1] with a run-to-run reproducible result: every block parks its
+// partial in scratch, and the block that arrives last (a ticket counter behind the partials) adds
+// them up in block order — no floating-point atomics, whose order would change between runs
+// (the reference accumulates in a fixed order too: gmres.cpp:13-23).
+__device__ __forceinline__ void grid_accumulate(double re, double im, double* out, double* scratch) {
+  __shared__ bool s_last;
+  block_sum(re, im);
+  unsigned* ticket = reinterpret_cast<unsigned*>(scratch + 2 * kReduceBlocks);
+  if (threadIdx.x == 0) {
+    scratch[2 * blockIdx.x] = re;
+    scratch[2 * blockIdx.x + 1] = im;
+    __threadfence();
+    s_last = atomicInc(ticket, gridDim.x - 1) == gridDim.x - 1;  // wraps to 0 for the next launch
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  re = im = 0.0;
+  for (uint32_t b = threadIdx.x; b < gridDim.x; b += kBlock) {
+    re += __ldcg(scratch + 2 * b);
+    im += __ldcg(scratch + 2 * b + 1);
+  }
+  block_sum(re, im);
+  if (threadIdx.x == 0) {
+    out[0] += re;
+    out[1] += im;
   }
 }
 
@@ -118,7 +143,8 @@ precondition_kernel(uint32_t npatch, int ni, const float2* __restrict__ lu, cons
 // w -= h_prev * v_prev (if v_prev), then out += conj(v_next) . w (if v_next)
 __global__ void __launch_bounds__(kBlock)
 mgs_step_kernel(uint32_t n, float2* __restrict__ w, const float2* __restrict__ v_prev,
-                const double* __restrict__ h_prev, const float2* __restrict__ v_next, double* out) {
+                const double* __restrict__ h_prev, const float2* __restrict__ v_next, double* out,
+                double* scratch) {
   double re = 0, im = 0;
   float hr = 0.f, hi = 0.f;
   if (v_prev) {
@@ -139,17 +165,18 @@ mgs_step_kernel(uint32_t n, float2* __restrict__ w, const float2* __restrict__ v
       im += double(v.x) * x.y - double(v.y) * x.x;
     }
   }
-  if (v_next) block_accumulate(re, im, out);
+  if (v_next) grid_accumulate(re, im, out, scratch);
 }
 
 // out[0] += ||w||^2
-__global__ void __launch_bounds__(kBlock) norm2_kernel(uint32_t n, const float2* __restrict__ w, double* out) {
+__global__ void __launch_bounds__(kBlock)
+norm2_kernel(uint32_t n, const float2* __restrict__ w, double* out, double* scratch) {
   double s = 0;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const float2 x = w[i];
     s += double(x.x) * x.x + double(x.y) * x.y;
   }
-  block_accumulate(s, 0.0, out);
+  grid_accumulate(s, 0.0, out, scratch);
 }
 
 __global__ void __launch_bounds__(kBlock)
@@ -179,7 +206,7 @@ update_solution_kernel(uint32_t n, int cols, const float2* __restrict__ basis, s
 // r = b - ax (FP64), r32 = float(r), out[0] += ||r||^2
 __global__ void __launch_bounds__(kBlock)
 residual_kernel(uint32_t n, const double2* __restrict__ b, const float2* __restrict__ ax,
-                float2* __restrict__ r32, double* out) {
+                float2* __restrict__ r32, double* out, double* scratch) {
   double s = 0;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const double2 bb = b[i];
@@ -188,7 +215,7 @@ residual_kernel(uint32_t n, const double2* __restrict__ b, const float2* __restr
     r32[i] = make_float2(float(rr), float(ri));
     s += rr * rr + ri * ri;
   }
-  block_accumulate(s, 0.0, out);
+  grid_accumulate(s, 0.0, out, scratch);
 }
 
 __global__ void __launch_bounds__(kBlock)
@@ -228,18 +255,16 @@ field_kernel(uint32_t n, const float4* __restrict__ src_pos, const float2* __res
       im += double(gr * c.y + gi * c.x);
     }
   }
-  __shared__ double acc[2];
-  if (threadIdx.x == 0) acc[0] = acc[1] = 0.0;
-  __syncthreads();
-  block_accumulate(re, im, acc);
-  __syncthreads();
-  if (threadIdx.x == 0) out[blockIdx.x] = make_double2(acc[0] * scale, acc[1] * scale);
+  block_sum(re, im);
+  if (threadIdx.x == 0) out[blockIdx.x] = make_double2(re * scale, im * scale);
 }
 
 inline uint32_t grid_for(uint32_t n) { return (n + kBlock - 1) / kBlock; }
-inline uint32_t reduce_grid(uint32_t n) { return std::min<uint32_t>(grid_for(n), 148u * 8u); }
+inline uint32_t reduce_grid(uint32_t n) { return std::min<uint32_t>(grid_for(n), kReduceBlocks); }
 
 }  // namespace
+
+size_t reduce_scratch_doubles() { return 2 * kReduceBlocks + 1; }
 
 void launch_corrections(uint32_t n, int ni, const float2* block, const uint32_t* off, const uint32_t* src,
                         const float2* delta, const float2* x, float2* y, cudaStream_t s) {
@@ -255,14 +280,14 @@ void launch_precondition(uint32_t npatch, int ni, const float2* lu, const int* p
   HFMM_CUDA_CHECK(cudaGetLastError());
 }
 void launch_mgs_step(uint32_t n, float2* w, const float2* v_prev, const double* h_prev,
-                     const float2* v_next, double* out, cudaStream_t s) {
+                     const float2* v_next, double* out, double* scratch, cudaStream_t s) {
   if (!n) return;
-  mgs_step_kernel<<<reduce_grid(n), kBlock, 0, s>>>(n, w, v_prev, h_prev, v_next, out);
+  mgs_step_kernel<<<reduce_grid(n), kBlock, 0, s>>>(n, w, v_prev, h_prev, v_next, out, scratch);
   HFMM_CUDA_CHECK(cudaGetLastError());
 }
-void launch_norm2(uint32_t n, const float2* w, double* out, cudaStream_t s) {
+void launch_norm2(uint32_t n, const float2* w, double* out, double* scratch, cudaStream_t s) {
   if (!n) return;
-  norm2_kernel<<<reduce_grid(n), kBlock, 0, s>>>(n, w, out);
+  norm2_kernel<<<reduce_grid(n), kBlock, 0, s>>>(n, w, out, scratch);
   HFMM_CUDA_CHECK(cudaGetLastError());
 }
 void launch_scale(uint32_t n, const float2* in, float scale, float2* out, cudaStream_t s) {
@@ -277,9 +302,9 @@ void launch_update_solution(uint32_t n, int cols, const float2* basis, size_t ld
   HFMM_CUDA_CHECK(cudaGetLastError());
 }
 void launch_residual(uint32_t n, const double2* b, const float2* ax, float2* r32, double* out,
-                     cudaStream_t s) {
+                     double* scratch, cudaStream_t s) {
   if (!n) return;
-  residual_kernel<<<reduce_grid(n), kBlock, 0, s>>>(n, b, ax, r32, out);
+  residual_kernel<<<reduce_grid(n), kBlock, 0, s>>>(n, b, ax, r32, out, scratch);
   HFMM_CUDA_CHECK(cudaGetLastError());
 }
 void launch_field(uint32_t n, const float4* src_pos, const float2* q, const float4* obs, uint32_t nobs,

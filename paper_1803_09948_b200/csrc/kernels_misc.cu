@@ -152,4 +152,61 @@ void launch_scatter_potentials(const float2* near, const float2* far, const uint
   HFMM_CUDA_CHECK(cudaGetLastError());
 }
 
+namespace {
+constexpr int kReduceWarps = 4;
+constexpr int kMaxChunks = (kMaxOrder + 1) * (kMaxOrder + 1) / 32 + 1;
+
+__global__ void __launch_bounds__(kReduceWarps * 32)
+ordered_reduce_kernel(const float2* __restrict__ staging, const uint32_t* __restrict__ perm,
+                      const uint32_t* __restrict__ seg_begin, const uint32_t* __restrict__ seg_dst,
+                      uint32_t n_segs, float2* __restrict__ dst, uint32_t stride, uint32_t dim) {
+  const uint32_t seg = blockIdx.x * kReduceWarps + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (seg >= n_segs) return;
+  float2* out = dst + size_t(seg_dst[seg]) * stride;
+  float2 acc[kMaxChunks];
+#pragma unroll
+  for (int u = 0; u < kMaxChunks; ++u) {
+    const uint32_t c = lane + 32u * u;
+    acc[u] = c < dim ? out[c] : make_float2(0.f, 0.f);
+  }
+  for (uint32_t j = seg_begin[seg]; j < seg_begin[seg + 1]; ++j) {
+    const float2* row = staging + size_t(perm[j]) * stride;
+#pragma unroll
+    for (int u = 0; u < kMaxChunks; ++u) {
+      const uint32_t c = lane + 32u * u;
+      if (c < dim) {
+        const float2 v = row[c];
+        acc[u].x += v.x;
+        acc[u].y += v.y;
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kMaxChunks; ++u) {
+    const uint32_t c = lane + 32u * u;
+    if (c < dim) out[c] = acc[u];
+  }
+}
+
+__global__ void range_rows_kernel(uint32_t* out, uint32_t n) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = i;
+}
+}  // namespace
+
+void launch_ordered_reduce(const float2* staging, const uint32_t* perm, const uint32_t* seg_begin,
+                           const uint32_t* seg_dst, uint32_t n_segs, float2* dst, uint32_t stride,
+                           uint32_t dim, cudaStream_t s) {
+  if (!n_segs) return;
+  ordered_reduce_kernel<<<(n_segs + kReduceWarps - 1) / kReduceWarps, kReduceWarps * 32, 0, s>>>(
+      staging, perm, seg_begin, seg_dst, n_segs, dst, stride, dim);
+  HFMM_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_range_rows(uint32_t* row_of_pair, uint64_t begin, uint32_t n, cudaStream_t s) {
+  if (!n) return;
+  range_rows_kernel<<<(n + 255) / 256, 256, 0, s>>>(row_of_pair + begin, n);
+  HFMM_CUDA_CHECK(cudaGetLastError());
+}
+
 }  // namespace hfmm_b200

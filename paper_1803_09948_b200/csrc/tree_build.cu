@@ -751,6 +751,50 @@ regroup_kernel(const uint32_t* __restrict__ seg_new, const uint32_t* __restrict_
 }
 }  // namespace
 
+namespace {
+__global__ void iota_kernel(uint32_t n, uint32_t* out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = i;
+}
+}  // namespace
+
+uint32_t build_ordered_reduce_device(const uint32_t* pair_dst, uint64_t begin, uint32_t n,
+                                     DeviceBuffer<uint32_t>& perm, DeviceBuffer<uint32_t>& seg_dst,
+                                     DeviceBuffer<uint32_t>& seg_begin, cudaStream_t s) {
+  if (!n) return 0;
+  DeviceBuffer<uint32_t> idx(n), keys(n), uniq(n);
+  DeviceBuffer<int> counts(n), nruns(1);
+  perm.resize(n);
+  iota_kernel<<<grid_for(n), kBlock, 0, s>>>(n, idx.get());
+  HFMM_CUDA_CHECK(cudaGetLastError());
+  TempStorage tmp;
+  size_t bytes = 0;
+  // LSD radix sort: stable, so the pairs of one destination stay in pair order
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, pair_dst + begin, keys.get(), idx.get(), perm.get(), int(n), 0, 32, s);
+  HFMM_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.get(bytes), bytes, pair_dst + begin, keys.get(), idx.get(),
+                                                  perm.get(), int(n), 0, 32, s));
+  cub::DeviceRunLengthEncode::Encode(nullptr, bytes, keys.get(), uniq.get(), counts.get(), nruns.get(), int(n), s);
+  HFMM_CUDA_CHECK(cub::DeviceRunLengthEncode::Encode(tmp.get(bytes), bytes, keys.get(), uniq.get(), counts.get(),
+                                                     nruns.get(), int(n), s));
+  int h_runs = 0;
+  nruns.download(&h_runs, 1, s);
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
+  seg_dst.resize(size_t(h_runs));
+  seg_begin.resize(size_t(h_runs) + 1);
+  HFMM_CUDA_CHECK(cudaMemcpyAsync(seg_dst.get(), uniq.get(), size_t(h_runs) * 4, cudaMemcpyDeviceToDevice, s));
+  DeviceBuffer<int> offs(size_t(h_runs) + 1);
+  // exclusive sum over h_runs + 1 entries: the last one is the total (counts has n >= h_runs + 1 slots
+  // unless every pair has its own destination; pad through a copy)
+  DeviceBuffer<int> padded(size_t(h_runs) + 1);
+  padded.zero(s);
+  HFMM_CUDA_CHECK(cudaMemcpyAsync(padded.get(), counts.get(), size_t(h_runs) * 4, cudaMemcpyDeviceToDevice, s));
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, padded.get(), offs.get(), h_runs + 1, s);
+  HFMM_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp.get(bytes), bytes, padded.get(), offs.get(), h_runs + 1, s));
+  HFMM_CUDA_CHECK(cudaMemcpyAsync(seg_begin.get(), offs.get(), (size_t(h_runs) + 1) * 4, cudaMemcpyDeviceToDevice, s));
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
+  return uint32_t(h_runs);
+}
+
 void regroup_pairs_device(const std::vector<uint32_t>& seg_new, const std::vector<uint32_t>& seg_old,
                           const std::vector<uint32_t>& seg_cls, uint64_t n_pairs,
                           DeviceBuffer<uint32_t>& pair_src, DeviceBuffer<uint32_t>& pair_dst,

@@ -88,6 +88,14 @@ void regroup_pairs_device(const std::vector<uint32_t>& seg_new, const std::vecto
                           DeviceBuffer<uint32_t>& pair_src, DeviceBuffer<uint32_t>& pair_dst,
                           DeviceBuffer<uint32_t>& pair_cls, cudaStream_t s);
 
+// Deterministic accumulation (HFMM_FLAG_DETERMINISTIC): for the pairs [begin, begin + n) of a stage,
+// perm = their range-relative indices sorted by destination (stable: ties keep pair order), cut into
+// one segment per destination: seg_dst[s], perm slots seg_begin[s] .. seg_begin[s + 1].  Returns the
+// number of segments.
+uint32_t build_ordered_reduce_device(const uint32_t* pair_dst, uint64_t begin, uint32_t n,
+                                     DeviceBuffer<uint32_t>& perm, DeviceBuffer<uint32_t>& seg_dst,
+                                     DeviceBuffer<uint32_t>& seg_begin, cudaStream_t s);
+
 // leaf-relative, k-scaled coordinates and their hi/lo split (kernels.cuh), plus absolute ones
 void build_body_arrays_device(const TreeArrays& tree, const DeviceBuffer<double>& d_xyz,
                               const DeviceBuffer<uint32_t>& d_index, double k, double grid,

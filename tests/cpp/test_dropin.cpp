@@ -9,6 +9,7 @@
 //   GMRES over the tree operator  reference tests/test_solver.cpp:480-494
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <random>
 
 #include "hfmm_b200.hpp"
@@ -87,6 +88,17 @@ int main() {
   for (int i = 0; i < n; ++i) ax[i] = a * ax[i] + ay[i];
   CHECK(rel_l2(az, ax) < 5e-6);
   CHECK(st.m2l_pairs > 0 && st.p2p_pairs > 0);
+
+  // bitwise determinism (test_fmm.cpp:1024-1050): TraversalConfig::deterministic is true by default,
+  // a replay and a second tree give the same bits
+  std::vector<cplx> az2, az3;
+  fmm::execute_plan(tree, z, az2);
+  CHECK(std::memcmp(az.data(), az2.data(), n * sizeof(cplx)) == 0);
+  {
+    fmm::DeviceTree tree2(pts, WaveNumber{k, 0}, 10, cfg, 0.5);
+    fmm::execute_plan(tree2, z, az3);
+    CHECK(std::memcmp(az.data(), az3.data(), n * sizeof(cplx)) == 0);
+  }
 
   // malformed configurations are config_error, as in the reference
   auto throws_config = [&](fmm::TraversalConfig c, int order) {

@@ -401,3 +401,30 @@ def test_both_batch_layouts_of_the_translation_kernel(oracle, monkeypatch, order
     assert rel_l2(res["group"], res["class"]) < 1e-6
     tg = np.arange(0, n, 23)
     assert rel_l2(res["class"][tg], oracle.direct_sum(xyz, q, k, tg)) < (2e-5 if order == 6 else 2e-6)
+
+
+def test_deterministic_flag_gives_bitwise_reproducible_results(monkeypatch):
+    """TraversalConfig::deterministic (traversal.hpp:11-22) / test_fmm.cpp:1024-1050: with the flag the
+    far field adds the contributions of every cell in list order (staged rows + ordered reduction, no
+    floating-point atomics): repeated matvecs and fresh handles agree to the last bit, with either
+    tree builder, and with the staging buffer cut into many ranges"""
+    from paper_1803_09948_b200.api import HFMM_FLAG_DETERMINISTIC, HFMM_FLAG_HOST_TREE
+    n, k = 20000, 5.0
+    xyz, q = plummer_points(n, 77), charges(n, 77)
+    ref_op = HfmmCuda(k=k, order=8, ncrit=32)
+    ref_op.set_points(xyz)
+    y_default = ref_op.matvec(q)
+    for flags, budget in ((HFMM_FLAG_DETERMINISTIC, None), (HFMM_FLAG_DETERMINISTIC | HFMM_FLAG_HOST_TREE, None),
+                          (HFMM_FLAG_DETERMINISTIC, "1")):
+        if budget:
+            monkeypatch.setenv("HFMM_ORDERED_STAGING_MB", budget)
+        runs = []
+        for _ in range(2):
+            op = HfmmCuda(k=k, order=8, ncrit=32, flags=flags)
+            op.set_points(xyz)
+            runs.append(op.matvec(q))
+            runs.append(op.matvec(q))
+        for y in runs[1:]:
+            assert np.array_equal(y, runs[0])
+        assert rel_l2(runs[0], y_default) < 1e-6
+        monkeypatch.delenv("HFMM_ORDERED_STAGING_MB", raising=False)

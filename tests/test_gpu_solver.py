@@ -307,3 +307,27 @@ def test_device_correction_builders_edge_cases(oracle):
         x = charges(len(want["xyz"]), 5)
         y = op.matvec(x)
         assert np.isfinite(y).all()
+
+
+def test_deterministic_gmres_history_is_bitwise_reproducible():
+    """with HFMM_FLAG_DETERMINISTIC two solves (fresh handles, corrections rebuilt on the device) give the
+    same residual history and solution to the last bit; the Krylov reductions sum block partials in
+    block order in every mode (gmres.cpp:13-23 accumulates in index order)"""
+    from paper_1803_09948_b200.api import HFMM_FLAG_DETERMINISTIC
+    from paper_1803_09948_b200.workloads import patch_samples
+
+    k = 4.0
+    tables = _tables(G, "bie_rule_")
+    patches = icosphere_patches(3)
+    xyz = patch_samples(patches, tables["sample_ref"])
+    runs = []
+    for _ in range(2):
+        op = HfmmCuda(k=k, order=10, ncrit=32, theta=0.4, kd_max=1.0, leaf_cap=-1.0, flags=HFMM_FLAG_DETERMINISTIC)
+        op.set_points(xyz)
+        op.build_corrections(patches, tables, fetch=False)
+        x, rep = op.gmres(np.exp(1j * k * xyz[:, 2]), rtol=1e-4, restart=30, max_iterations=300, precondition=True)
+        assert rep["converged"]
+        runs.append((x, rep["residuals"].copy(), rep["iterations"]))
+    assert runs[0][2] == runs[1][2]
+    assert np.array_equal(runs[0][1], runs[1][1])
+    assert np.array_equal(runs[0][0], runs[1][0])
