@@ -69,7 +69,7 @@ struct TraversalConfig {
   double theta = 0.5;
   double kd_max = 1.0;
   bool deterministic = true;  // -> HFMM_FLAG_DETERMINISTIC: ordered accumulation, bitwise reproducible
-                              //    (+40 % per matvec); false: floating-point atomics in M2M / M2L
+                              //    (+22 % per matvec); false: floating-point atomics in M2M / M2L
   int threads = 0;            // accepted for source compatibility (host threads of the table builder)
 };
 

@@ -48,8 +48,8 @@ enum {
   HFMM_FLAG_NEAR_FIRST = 1 << 2,
   /* run-to-run reproducible results (TraversalConfig::deterministic, traversal.hpp:11-22: per-target
    * ordered accumulation).  M2M and M2L stage one row per cell pair and add the rows of every
-   * destination cell in list order instead of using floating-point atomics; costs three extra passes
-   * over the staged rows (cfg 2: +40 % per matvec) and up to HFMM_ORDERED_STAGING_MB (environment,
+   * destination cell in list order instead of using floating-point atomics; costs two extra passes
+   * over the staged rows (cfg 2: +22 % per matvec) and up to HFMM_ORDERED_STAGING_MB (environment,
    * default 4096) MiB of device memory.  The near field, the leaf passes and the Krylov reductions
    * are ordered in every mode. */
   HFMM_FLAG_DETERMINISTIC = 1 << 3

@@ -30,6 +30,7 @@ def _load_rules(path: str):
 
 def cmd_solve(a):
     from . import HfmmCuda
+    from .api import HFMM_FLAG_DETERMINISTIC
     from .workloads import icosphere_patches, mie_soft_sphere, patch_samples
 
     tables = _load_rules(a.rules)
@@ -40,7 +41,8 @@ def cmd_solve(a):
     else:
         patches = icosphere_patches(a.subdivisions, a.radius)
     xyz = patch_samples(patches, tables["sample_ref"])
-    op = HfmmCuda(k=a.k, order=a.order, ncrit=a.ncrit, theta=a.theta, kd_max=a.kd_max, leaf_cap=-1.0)
+    op = HfmmCuda(k=a.k, order=a.order, ncrit=a.ncrit, theta=a.theta, kd_max=a.kd_max, leaf_cap=-1.0,
+                  flags=HFMM_FLAG_DETERMINISTIC if a.deterministic else 0)
     t0 = time.perf_counter(); op.set_points(xyz); t_tree = time.perf_counter() - t0
     t0 = time.perf_counter(); nnz = op.build_corrections(patches, tables, mode=2, fetch=False); t_corr = time.perf_counter() - t0
     rhs = np.exp(1j * a.k * xyz[:, 2])
@@ -64,12 +66,14 @@ def cmd_solve(a):
 
 def cmd_matvec(a):
     from . import HfmmCuda
+    from .api import HFMM_FLAG_DETERMINISTIC
     from .workloads import CONFIGS, charges, make_points
 
     cfg = CONFIGS[a.config]
     n = a.n or cfg.n
     xyz, q = make_points(cfg, n), charges(n, cfg.seed)
-    op = HfmmCuda(k=cfg.k, order=cfg.order, ncrit=cfg.ncrit, theta=cfg.theta, kd_max=cfg.kd_max, leaf_cap=cfg.leaf_cap)
+    op = HfmmCuda(k=cfg.k, order=cfg.order, ncrit=cfg.ncrit, theta=cfg.theta, kd_max=cfg.kd_max, leaf_cap=cfg.leaf_cap,
+                  flags=HFMM_FLAG_DETERMINISTIC if a.deterministic else 0)
     op.set_points(xyz)
     y = op.matvec(q)
     t0 = time.perf_counter()
@@ -124,6 +128,7 @@ def main(argv=None):
     s.add_argument("--restart", type=int, default=30)
     s.add_argument("--max-iterations", type=int, default=1000)
     s.add_argument("--block-jacobi", action="store_true")
+    s.add_argument("--deterministic", action="store_true", help="ordered accumulation: bitwise reproducible runs")
     s.add_argument("--observations", type=int, default=37)
     s.add_argument("--obs-radius", type=float, default=4.0, help="in sphere radii")
     s.add_argument("--rules", default=os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
@@ -133,6 +138,7 @@ def main(argv=None):
     m.add_argument("--config", default="cfg2")
     m.add_argument("--n", type=int, default=None)
     m.add_argument("--repeat", type=int, default=5)
+    m.add_argument("--deterministic", action="store_true", help="ordered accumulation: bitwise reproducible runs")
     m.add_argument("--check", type=int, default=64)
     m.set_defaults(fn=cmd_matvec)
     i = sub.add_parser("info", help="library version and device probes")

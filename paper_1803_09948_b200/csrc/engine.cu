@@ -882,12 +882,11 @@ void Engine::run_stage(const TranslateStage& st, const float2* src, float2* dst)
   ta.order = cfg_.order;
   ta.stride = stride_;
   if (!st.ordered.empty()) {
-    // deterministic accumulation: every pair adds into its own (zeroed) staging row — one
-    // contribution per row, so the atomics of the kernel have nothing to reorder — and the rows of a
-    // destination are then summed in pair order
+    // deterministic accumulation: every pair writes its own staging row (plain stores in place of the
+    // atomics) and the rows of a destination are then summed in pair order
     const uint32_t dim = uint32_t(cfg_.order + 1) * uint32_t(cfg_.order + 1);
     for (const auto& r : st.ordered) {
-      HFMM_CUDA_CHECK(cudaMemsetAsync(ordered_staging_.get(), 0, size_t(r.n_pairs) * stride_ * sizeof(float2), stream_));
+      ta.staged = 1;
       ta.items = st.items.get() + r.item_begin;
       ta.n_items = r.n_items;
       ta.pair_dst = st.row_of_pair.get();

@@ -135,6 +135,7 @@ struct TranslateArgs {
   int order;
   int stride;
   int mixed;                 // batches mix classes of a table group (per-pair phases) / one class per batch
+  int staged;                // every pair owns its dst row (deterministic mode): plain stores instead of atomics
 };
 void launch_translate(const TranslateArgs& a, cudaStream_t s);
 // pairs per work item expected by the kernel

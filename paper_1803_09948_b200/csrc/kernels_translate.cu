@@ -40,6 +40,7 @@
 // FP32 work per pair: 2 * 2*sum_n ((n+1)^2 + n^2) + 4*sum_m (P+1-|m|)^2 FMAs (11.75 k at P = 12) against
 // 4 (P+1)^4 = 114 k for the reference's dense complex mat-vec.
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <vector>
 
@@ -307,7 +308,8 @@ __constant__ TranslateSchedule c_sched[kMaxOrder + 1];
 // item -> pair list -> source rows never sits on the critical path.
 // MIXED: the batches of this launch mix shift classes of one table group (per-pair azimuth phases);
 // otherwise every batch holds one class and the phases are per class (broadcast)
-template <int WARPS, int CTAS, bool MIXED>
+// STAGED: every pair owns its destination row (deterministic mode): plain stores instead of RED
+template <int WARPS, int CTAS, bool MIXED, bool STAGED>
 __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const TranslateArgs a) {
   constexpr int kThreads = WARPS * 32;
   constexpr int kLanesPerPair = WARPS;  // 32 pairs x WARPS lanes = all threads of the CTA
@@ -557,10 +559,14 @@ __global__ void __launch_bounds__(WARPS * 32, CTAS) translate_kernel(const Trans
         float* dst = reinterpret_cast<float*>(a.dst + size_t(a.pair_dst[item.pair_begin + pr]) * a.stride);
         for (int i2 = se + 8 * (warp >> 3); i2 < dim / 2; i2 += WARPS) {
           const float2 lo = A[(2 * i2) * kRow + pr], hi = A[(2 * i2 + 1) * kRow + pr];
-          atomicAdd(reinterpret_cast<float4*>(dst) + i2, make_float4(lo.x, lo.y, hi.x, hi.y));
+          const float4 v = make_float4(lo.x, lo.y, hi.x, hi.y);
+          if (STAGED) reinterpret_cast<float4*>(dst)[i2] = v;  // one row per pair: nothing to add to
+          else atomicAdd(reinterpret_cast<float4*>(dst) + i2, v);
         }
-        if ((dim & 1) && se == 0 && warp < 8)
-          atomicAdd(reinterpret_cast<float2*>(dst) + (dim - 1), A[(dim - 1) * kRow + pr]);
+        if ((dim & 1) && se == 0 && warp < 8) {
+          if (STAGED) reinterpret_cast<float2*>(dst)[dim - 1] = A[(dim - 1) * kRow + pr];
+          else atomicAdd(reinterpret_cast<float2*>(dst) + (dim - 1), A[(dim - 1) * kRow + pr]);
+        }
       }
     }
     // the next item's operands (tile B is free since the unfold) must have landed
@@ -724,15 +730,15 @@ void upload_translate_schedule(int order) {
 int translate_batch_size(int) { return kTranslateBatch; }
 
 namespace {
-template <int WARPS, int CTAS, bool MIXED>
+template <int WARPS, int CTAS, bool MIXED, bool STAGED>
 void launch_translate_nu(const TranslateArgs& a, cudaStream_t s, size_t bytes, int ctas) {
   static int configured_for = -1;
   if (configured_for < int(bytes)) {
-    HFMM_CUDA_CHECK(cudaFuncSetAttribute(translate_kernel<WARPS, CTAS, MIXED>,
+    HFMM_CUDA_CHECK(cudaFuncSetAttribute(translate_kernel<WARPS, CTAS, MIXED, STAGED>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
     configured_for = int(bytes);
   }
-  translate_kernel<WARPS, CTAS, MIXED><<<ctas, WARPS * 32, bytes, s>>>(a);
+  translate_kernel<WARPS, CTAS, MIXED, STAGED><<<ctas, WARPS * 32, bytes, s>>>(a);
   HFMM_CUDA_CHECK(cudaGetLastError());
 }
 }  // namespace
@@ -750,13 +756,18 @@ void launch_translate(const TranslateArgs& a, cudaStream_t s) {
   const int warps = translate_warps(a.order);
   const bool two = translate_two_ctas(a.order);
   const int ctas = int(std::min<uint32_t>(a.n_items, uint32_t((two ? 2 : 1) * sm_count)));
-  if (warps == 8) {
-    if (a.mixed) launch_translate_nu<8, 2, true>(a, s, sp.bytes, ctas);
-    else launch_translate_nu<8, 2, false>(a, s, sp.bytes, ctas);
-  } else {
-    if (a.mixed) launch_translate_nu<16, 1, true>(a, s, sp.bytes, ctas);
-    else launch_translate_nu<16, 1, false>(a, s, sp.bytes, ctas);
-  }
+  auto pick = [&](auto warps_c, auto ctas_c) {
+    constexpr int W = decltype(warps_c)::value, C = decltype(ctas_c)::value;
+    if (a.mixed) {
+      if (a.staged) launch_translate_nu<W, C, true, true>(a, s, sp.bytes, ctas);
+      else launch_translate_nu<W, C, true, false>(a, s, sp.bytes, ctas);
+    } else {
+      if (a.staged) launch_translate_nu<W, C, false, true>(a, s, sp.bytes, ctas);
+      else launch_translate_nu<W, C, false, false>(a, s, sp.bytes, ctas);
+    }
+  };
+  if (warps == 8) pick(std::integral_constant<int, 8>{}, std::integral_constant<int, 2>{});
+  else pick(std::integral_constant<int, 16>{}, std::integral_constant<int, 1>{});
 }
 
 }  // namespace hfmm_b200
