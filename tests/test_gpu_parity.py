@@ -428,3 +428,31 @@ def test_deterministic_flag_gives_bitwise_reproducible_results(monkeypatch):
             assert np.array_equal(y, runs[0])
         assert rel_l2(runs[0], y_default) < 1e-6
         monkeypatch.delenv("HFMM_ORDERED_STAGING_MB", raising=False)
+
+
+def test_sharded_matvec_with_ordered_accumulation_is_reproducible():
+    """HFMM_FLAG_DETERMINISTIC on every rank of the (emulated) sharded matvec: two runs agree bit for
+    bit — each rank reduces the pairs of its own targets in list order, the exchanges copy bits"""
+    import torch
+
+    from paper_1803_09948_b200.api import HFMM_FLAG_DETERMINISTIC
+    from paper_1803_09948_b200.distributed import emulate_ranks_on_one_device
+
+    n, k, order, nranks = 20000, 4.0, 8, 3
+    xyz, q = sphere_points(n, 21), charges(n, 21)
+    outs = []
+    for _ in range(2):
+        ops = []
+        for r in range(nranks):
+            op = HfmmCuda(k=k, order=order, flags=HFMM_FLAG_DETERMINISTIC)
+            op.set_partition(r, nranks)
+            op.set_points(xyz)
+            ops.append(op)
+        qm = q[ops[0].body_order()]
+        q_dev = torch.from_numpy(np.stack([qm.real, qm.imag], 1).astype(np.float32)).cuda()
+        out, _ = emulate_ranks_on_one_device(ops, q_dev, pruned=True)
+        outs.append(out.cpu().numpy())
+        out, _ = emulate_ranks_on_one_device(ops, q_dev, pruned=True)
+        outs.append(out.cpu().numpy())
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
