@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <cstdlib>
 #include <cmath>
@@ -428,25 +429,39 @@ void Engine::finish_far_field(TableRegistry& reg) {
     upload_stage(st, src, dst, cls, cl, upward);
     return st;
   };
+  const bool trace = getenv("HFMM_SETUP_TRACE") != nullptr;
+  auto t_prev = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    cudaStreamSynchronize(stream_);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[hfmm setup]   %-26s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t_prev).count());
+    t_prev = now;
+  };
   for (int L = t.max_level; L > lmin_src_; --L) m2m_.push_back(level_stage(L, true));
   for (int L = lmin_dst_ + 1; L <= t.max_level; ++L) l2l_.push_back(level_stage(L, false));
+  mark("M2M / L2L stages");
 
   const size_t nrot = reg.rot_cos.size(), ncoax = reg.coax_specs.size();
   stats_.rotation_tables = nrot;
   stats_.coaxial_tables = ncoax;
   std::vector<float> rot(nrot * size_t(rot_table_size(P)));
   std::vector<float> coax(ncoax * size_t(coax_table_size(P)) * 2);
+  mark("table buffers");
   parallel_for(nrot, threads_, [&](size_t i) {
     build_rotation_table(P, reg.rot_cos[i], rot.data() + i * size_t(rot_table_size(P)));
   });
-  const CoaxBuilder builder(P);
+  mark("rotation tables");
+  const CoaxBuilder& builder = CoaxBuilder::shared(P);
   parallel_for(ncoax, threads_, [&](size_t i) {
     const auto& s = reg.coax_specs[i];
     builder.build(s.kind, k, s.dist, s.s_src, s.s_dst, coax.data() + i * size_t(coax_table_size(P)) * 2,
                   cfg_.wave_i);
   });
+  mark("coaxial tables");
   rot_tables_.upload(rot, stream_);
   coax_tables_.upload(coax, stream_);
+  mark("table upload");
 
   std::vector<uint32_t> up, down;
   for (uint32_t c : t.leaves) {
@@ -463,6 +478,7 @@ void Engine::finish_far_field(TableRegistry& reg) {
   multipole_.zero(stream_);
   local_.zero(stream_);
   HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  mark("leaf lists + expansions");
 }
 
 // cell geometry on the lattice, level scales, the hi/lo grid
@@ -637,15 +653,27 @@ void Engine::set_points(const double* xyz, size_t n) {
 // ---- builder on the device (default): tree_build.cu -------------------------------------------
 void Engine::set_points_device(const double* xyz, size_t n) {
   const double k = cfg_.wave_r;
+  // HFMM_SETUP_TRACE=1: wall time of every setup phase on stderr (synchronises after each)
+  const bool trace = getenv("HFMM_SETUP_TRACE") != nullptr;
+  auto t_prev = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    cudaStreamSynchronize(stream_);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[hfmm setup] %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t_prev).count());
+    t_prev = now;
+  };
   DeviceBuffer<double> d_xyz;
   DeviceBuffer<uint32_t> d_index;
   build_tree_device(tree_, xyz, n, cfg_.ncrit, leaf_cap_, d_xyz, d_index, stream_);
+  mark("tree");
   const TreeArrays& t = tree_;
   DeviceCells cells;
   cells.upload(t, stream_);
   dual_tree_traversal_device(t, cells, std::hypot(cfg_.wave_r, cfg_.wave_i), cfg_.theta, cfg_.kd_max, dev_pairs_,
                              stream_);  // the gate uses |k| (traversal.cpp:86)
   far_pair_level_range(dev_pairs_, cells, lmin_dst_, lmin_src_, stream_);
+  mark("traversal");
   have_far_ = dev_pairs_.n_far > 0;
   stats_.m2l_pairs = dev_pairs_.n_far;
   stats_.p2p_pairs = dev_pairs_.n_near;
@@ -676,12 +704,14 @@ void Engine::set_points_device(const double* xyz, size_t n) {
   std::vector<int4> geom;
   upload_cell_geometry(geom);
   build_body_arrays_device(t, d_xyz, d_index, k, grid_, body_pos_, body_hi_, body_lo_, body_abs_, stream_);
+  mark("partition + body arrays");
 
   NearLists nl;
   build_near_lists_device(dev_pairs_, t, cells, owned_, p2p_offset_, p2p_split_, p2p_src_, nl, stream_);
   stats_.p2p_body_pairs = nl.body_pairs;
   owned_body_pairs_ = nl.owned_body_pairs;
   build_tiles(nl.work);
+  mark("near lists + tiles");
 
   TableRegistry reg;
   stats_.m2l_shift_classes = 0;
@@ -689,9 +719,12 @@ void Engine::set_points_device(const double* xyz, size_t n) {
   if (have_far_) {
     FarClasses fc;
     build_far_classes_device(dev_pairs_, cells, owned_, t.max_level, m2l_.pair_src, m2l_.pair_dst, fc, stream_);
+    mark("far classes (sort)");
     build_m2l_stage_device(reg, fc);
+    mark("M2L stage (classes, batches)");
   }
   finish_far_field(reg);
+  mark("tables + M2M/L2L + storage");
 }
 
 // ---- builder on the host (HFMM_FLAG_HOST_TREE): host_tree.cpp ---------------------------------
@@ -1179,7 +1212,7 @@ void compose_dense_from_tables(int order, double k, const double t[3], int kind,
   const double cphi = rxy > 0 ? t[0] / rxy : 1.0, sphi = rxy > 0 ? t[1] / rxy : 0.0;
   std::vector<float> rot(rot_table_size(P)), coax(size_t(coax_table_size(P)) * 2);
   build_rotation_table(P, t[2] / r, rot.data());
-  const CoaxBuilder builder(P);
+  const CoaxBuilder& builder = CoaxBuilder::shared(P);
   // kind 0: M2L with (s_src, s_dst); kind 1: regular shift expressed through the M2M scaling
   builder.build(kind == 0 ? CoaxKind::m2l : CoaxKind::m2m, k, r, s_src, s_dst, coax.data(), k_imag);
   std::vector<cd> ph(2 * P + 1);

@@ -5,6 +5,9 @@
 #include <cmath>
 #include <complex>
 #include <cstdlib>
+#include <map>
+#include <memory>
+#include <mutex>
 
 #include "common.hpp"
 
@@ -194,19 +197,27 @@ void build_rotation_table(int order, double cos_theta, float* out) {
     sp[i] = sp[i - 1] * s;
   }
   std::fill(out, out + rot_table_size(order), 0.0f);
+  // 1 / i! and sqrt(i!) once per process (the sums below are multiplications only)
+  static long double inv_fact[128], root_fact[128];
+  static const bool ready = [] {
+    for (int i = 0; i < 128; ++i) {
+      inv_fact[i] = 1.0L / factorial_ld(i);
+      root_fact[i] = sqrtl(factorial_ld(i));
+    }
+    return true;
+  }();
+  (void)ready;
   std::vector<long double> d;
   for (int n = 0; n <= order; ++n) {
     const int w = 2 * n + 1;
-    d.assign(size_t(w) * w, 0.0L);  // d[(a+n)*w + (b+n)] = d^n_{a,b}
+    d.assign(size_t(w) * w, 0.0L);  // d[(a+n)*w + (b+n)] = d^n_{a,b}; only b >= 0 is read below
     for (int a = -n; a <= n; ++a)
-      for (int b = -n; b <= n; ++b) {
-        const long double pre = sqrtl(factorial_ld(n + a) * factorial_ld(n - a) *
-                                      factorial_ld(n + b) * factorial_ld(n - b));
+      for (int b = 0; b <= n; ++b) {
+        const long double pre = root_fact[n + a] * root_fact[n - a] * root_fact[n + b] * root_fact[n - b];
         long double sum = 0;
         for (int k = std::max(0, b - a); k <= std::min(n + b, n - a); ++k) {
-          const long double term = cp[2 * n - 2 * k + b - a] * sp[2 * k - b + a] /
-                                   (factorial_ld(n + b - k) * factorial_ld(k) *
-                                    factorial_ld(n - k - a) * factorial_ld(k - b + a));
+          const long double term = cp[2 * n - 2 * k + b - a] * sp[2 * k - b + a] * inv_fact[n + b - k] *
+                                   inv_fact[k] * inv_fact[n - k - a] * inv_fact[k - b + a];
           sum += ((k - b + a) & 1) ? -term : term;
         }
         d[size_t(a + n) * w + (b + n)] = pre * sum;
@@ -279,6 +290,15 @@ CoaxBuilder::CoaxBuilder(int order) : order_(order) {
   offset_.back() = uint32_t(coef_.size());
 }
 
+const CoaxBuilder& CoaxBuilder::shared(int order) {
+  static std::mutex mu;
+  static std::map<int, std::unique_ptr<CoaxBuilder>> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto& slot = cache[order];
+  if (!slot) slot = std::make_unique<CoaxBuilder>(order);
+  return *slot;
+}
+
 size_t CoaxBuilder::slot(int m, int nu, int n) const {
   return (size_t(m) * (order_ + 1) + nu) * (order_ + 1) + n;
 }
@@ -318,26 +338,45 @@ void CoaxBuilder::build(CoaxKind kind, double k, double dist, double s_src, doub
       ri[l] = rad[l].imag();
     }
   }
-  const long double ls = logl((long double)s_src), ld = logl((long double)s_dst), lz = logl(z);
-  auto ldf = [](int n) { return logl(double_factorial(n)); };
+  // positive scale multiplying A * rad, as a product of three factors (per lam, per nu, per n):
+  //   M2L: (2 lam - 1)!! / z^{lam+1}  *  s_dst^nu / (2 nu - 1)!!  *  s_src^n / (2n + 1)!!
+  //   M2M: 1                          *  (2 nu + 1)!! / s_dst^nu   *  s_src^n / (2n + 1)!!
+  //   L2L: 1                          *  s_dst^nu / (2 nu - 1)!!  *  (2n - 1)!! / s_src^n
+  // long double carries 15 bits of exponent: none of the factors can overflow or vanish for
+  // orders <= kMaxOrder and the box sizes the gates admit (|log10| of a factor stays below ~200)
+  std::vector<long double> f_lam(lmax + 1, 1.0L), f_nu(P + 1), f_n(P + 1);
+  {
+    long double zp = z, sd = 1.0L, ss = 1.0L;  // z^{lam+1}, s_dst^nu, s_src^n
+    for (int lam = 0; lam <= lmax; ++lam) {
+      if (kind == CoaxKind::m2l) f_lam[lam] = double_factorial(2 * lam - 1) / zp;
+      zp *= z;
+    }
+    for (int j = 0; j <= P; ++j) {
+      if (kind == CoaxKind::m2l) {
+        f_nu[j] = sd / double_factorial(2 * j - 1);
+        f_n[j] = ss / double_factorial(2 * j + 1);
+      } else if (kind == CoaxKind::m2m) {
+        f_nu[j] = double_factorial(2 * j + 1) / sd;
+        f_n[j] = ss / double_factorial(2 * j + 1);
+      } else {
+        f_nu[j] = sd / double_factorial(2 * j - 1);
+        f_n[j] = double_factorial(2 * j - 1) / ss;
+      }
+      sd *= (long double)s_dst;
+      ss *= (long double)s_src;
+    }
+  }
   std::fill(out, out + 2 * size_t(coax_table_size(P)), 0.0f);
   for (int m = 0; m <= P; ++m)
     for (int n = m; n <= P; ++n)
       for (int nu = m; nu <= P; ++nu) {
         const int idx = coax_block_offset(P, m) + (n - m) * coax_row_stride(P, m) + (nu - m);
         const double* a = coef_.data() + offset_[slot(m, nu, n)];
+        const long double fnn = f_nu[nu] * f_n[n];
         long double sr = 0, si = 0;
         int t = 0;
         for (int lam = std::abs(n - nu); lam <= n + nu; lam += 2, ++t) {
-          long double lg;  // log of the positive scale multiplying A * rad
-          if (kind == CoaxKind::m2l)
-            lg = ldf(2 * lam - 1) - ldf(2 * nu - 1) - ldf(2 * n + 1) + nu * ld + n * ls -
-                 (lam + 1) * lz;
-          else if (kind == CoaxKind::m2m)
-            lg = ldf(2 * nu + 1) - nu * ld + n * ls - ldf(2 * n + 1);
-          else
-            lg = nu * ld - ldf(2 * nu - 1) + ldf(2 * n - 1) - n * ls;
-          const long double f = expl(lg) * a[t];
+          const long double f = fnn * f_lam[lam] * a[t];
           sr += f * rr[lam];
           si += f * ri[lam];
         }

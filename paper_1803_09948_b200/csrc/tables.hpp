@@ -83,6 +83,8 @@ enum class CoaxKind { m2l, m2m, l2l };
 class CoaxBuilder {
  public:
   explicit CoaxBuilder(int order);
+  // the builder of an order, constructed once per process (its 3j products depend on the order only)
+  static const CoaxBuilder& shared(int order);
   // k + i k_imag: the (complex) wavenumber; the level scales s_src / s_dst are Re(k) * side
   void build(CoaxKind kind, double k, double dist, double s_src, double s_dst, float* out,
              double k_imag = 0.0) const;
