@@ -8,6 +8,7 @@ import pytest
 
 from checkers import have_ref, rel_l2
 from paper_1803_09948_b200 import HfmmCuda, HfmmError
+from paper_1803_09948_b200.api import HFMM_FLAG_DETERMINISTIC
 from paper_1803_09948_b200.workloads import icosphere_patches, sphere_points, charges
 
 pytestmark = pytest.mark.gpu
@@ -31,9 +32,11 @@ def test_apply_operator_matches_reference_fixture():
     assert rel_l2(op.matvec(G["bie_x"]), G["bie_y"]) < 1e-5
 
 
-def test_gmres_iteration_parity_with_reference_fixture():
-    # north star: GMRES reaches 1e-4 in the reference's iteration count +-1
-    op = _bie_operator(G)
+@pytest.mark.parametrize("flags", [0, 1 << 3], ids=["atomics", "deterministic"])
+def test_gmres_iteration_parity_with_reference_fixture(flags):
+    # north star: GMRES reaches 1e-4 in the reference's iteration count +-1 (in the default mode and
+    # with HFMM_FLAG_DETERMINISTIC = 1 << 3, the reference's ordered accumulation)
+    op = _bie_operator(G, flags=flags)
     for precondition, it_ref, sol_ref in ((True, int(G["bie_iterations"]), G["bie_sol"]),
                                           (False, int(G["bie_iterations_noprec"]), G["bie_sol_noprec"])):
         x, rep = op.gmres(G["bie_rhs"], rtol=1e-4, restart=30, max_iterations=200,
@@ -83,7 +86,8 @@ def test_midsize_system_against_oracle_gmres(oracle):
     xyz, fw = sysr.samples()
     corr = sysr.corrections()
     rhs = sysr.rhs((0, 0, 1))
-    op = HfmmCuda(k=k, order=order, ncrit=16)
+    # ordered accumulation: "the same operator" below must be a function, not a run-to-run variable
+    op = HfmmCuda(k=k, order=order, ncrit=16, flags=HFMM_FLAG_DETERMINISTIC)
     op.set_points(xyz)
     op.set_corrections(sysr.ni, far_weight=fw, **corr)
     f = oracle.fmm(xyz, k, order, ncrit=16, leaf_cap=1.0 / k, theta=0.4, kd_max=1.0)
