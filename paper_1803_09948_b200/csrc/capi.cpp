@@ -4,6 +4,7 @@
 #include <new>
 #include <string>
 
+#include "device_utils.cuh"
 #include "engine.hpp"
 #include "hfmm_cuda.h"
 
@@ -27,6 +28,8 @@ int guarded(hfmm_cuda* h, Fn&& fn) {
     // process (torch, the caller's own code): drop what they left so that the launch checks
     // below report this call's errors only; the leftover stays readable for diagnosis
     if (const char* stale = Engine::take_stale_cuda_error()) g_stale_error = stale;
+    // buffers created or dropped inside the call are ordered on the handle's stream (device_utils.cuh)
+    hfmm_b200::AllocStreamScope scope((h && h->engine) ? h->engine->stream() : nullptr);
     fn();
     return HFMM_OK;
   } catch (const Error& e) {
@@ -70,8 +73,11 @@ int hfmm_cuda_create(hfmm_cuda_t** out, const hfmm_cuda_config* cfg) {
 
 void hfmm_cuda_destroy(hfmm_cuda_t* h) {
   if (!h) return;
+  const int device = h->engine ? h->engine->device() : -1;
   delete h->engine;
   delete h;
+  // the last handle returns the pooled device memory to the driver
+  if (device >= 0 && !Engine::any_engine_alive()) hfmm_b200::trim_memory_pool(device);
 }
 
 const char* hfmm_cuda_last_error(const hfmm_cuda_t* h) {

@@ -22,6 +22,27 @@ namespace hfmm_b200 {
 // bytes currently held through DeviceBuffer on this process (reported in hfmm_cuda_stats)
 size_t& device_bytes_counter();
 
+// Stream-ordered allocation.  Inside a library call the calling thread carries the handle's stream
+// (AllocStreamScope, set by the C API wrapper): buffers then come from the device's memory pool with
+// cudaMallocAsync and return to it with cudaFreeAsync in that stream's order — no device-wide
+// synchronisation per cudaFree and no trip into the driver's address-space management per buffer
+// (rebuilding a point set frees and allocates ~50 buffers: 0.07 s, against 0.1-0.8 s with
+// cudaMalloc / cudaFree).  All work that touches a buffer is ordered on the handle's stream (the
+// near-field stream joins it at the end of every matvec), so freeing in that stream's order is
+// safe.  Outside a scope (handle construction and destruction) the synchronous calls are used;
+// cudaFree accepts pool allocations.  The pool keeps freed memory while a handle is alive and is
+// trimmed when the last one goes (configure_memory_pool / trim_memory_pool).
+cudaStream_t& alloc_stream();
+struct AllocStreamScope {
+  cudaStream_t prev;
+  explicit AllocStreamScope(cudaStream_t s) : prev(alloc_stream()) { alloc_stream() = s; }
+  ~AllocStreamScope() { alloc_stream() = prev; }
+  AllocStreamScope(const AllocStreamScope&) = delete;
+  AllocStreamScope& operator=(const AllocStreamScope&) = delete;
+};
+void configure_memory_pool(int device);
+void trim_memory_pool(int device);
+
 template <typename T>
 class DeviceBuffer {
  public:
@@ -46,14 +67,18 @@ class DeviceBuffer {
     if (n == n_) return;
     release();
     if (n) {
-      HFMM_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&ptr_), n * sizeof(T)));
+      if (cudaStream_t s = alloc_stream())
+        HFMM_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&ptr_), n * sizeof(T), s));
+      else
+        HFMM_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&ptr_), n * sizeof(T)));
       device_bytes_counter() += n * sizeof(T);
     }
     n_ = n;
   }
   void release() {
     if (ptr_) {
-      cudaFree(ptr_);
+      if (cudaStream_t s = alloc_stream()) cudaFreeAsync(ptr_, s);
+      else cudaFree(ptr_);
       device_bytes_counter() -= n_ * sizeof(T);
     }
     ptr_ = nullptr;

@@ -2,6 +2,7 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -17,6 +18,35 @@
 #include "tree_build.cuh"
 
 namespace hfmm_b200 {
+
+cudaStream_t& alloc_stream() {
+  thread_local cudaStream_t s = nullptr;
+  return s;
+}
+
+namespace {
+std::atomic<int> g_live_engines{0};
+}
+
+void configure_memory_pool(int device) {
+  cudaMemPool_t pool = nullptr;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return;
+  }
+  uint64_t keep = ~uint64_t(0);  // freed buffers stay in the pool while a handle lives
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+}
+
+void trim_memory_pool(int device) {
+  cudaMemPool_t pool = nullptr;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return;
+  }
+  cudaDeviceSynchronize();
+  cudaMemPoolTrimTo(pool, 0);
+}
 
 size_t& device_bytes_counter() {
   static size_t bytes = 0;
@@ -142,6 +172,8 @@ Engine::Engine(const hfmm_cuda_config& cfg) : cfg_(cfg) {
   HFMM_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   HFMM_CUDA_CHECK(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, prio_hi));
   HFMM_CUDA_CHECK(cudaStreamCreateWithPriority(&stream_near_, cudaStreamNonBlocking, prio_lo));
+  configure_memory_pool(cfg_.device);
+  ++g_live_engines;
   HFMM_CUDA_CHECK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
   HFMM_CUDA_CHECK(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
   ev_.resize(14);
@@ -157,8 +189,12 @@ Engine::Engine(const hfmm_cuda_config& cfg) : cfg_(cfg) {
   upload_translate_schedule(P);
 }
 
+void Engine::release_device_state() { --g_live_engines; }
+bool Engine::any_engine_alive() { return g_live_engines.load() > 0; }
+
 Engine::~Engine() {
   cudaSetDevice(cfg_.device);
+  release_device_state();
   for (auto& e : ev_) cudaEventDestroy(e);
   for (auto& e : user_ev_) cudaEventDestroy(e);
   if (ev_fork_) cudaEventDestroy(ev_fork_);
@@ -619,6 +655,9 @@ void Engine::dist_downward(void* out_morton_dev) {
 void Engine::set_points(const double* xyz, size_t n) {
   HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
   const auto t0 = std::chrono::steady_clock::now();
+  // the buffers of the previous point set are freed in stream_'s order: nothing on the near-field
+  // stream may still be reading them (a matvec joins it into stream_; a half-finished two-phase one does not)
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_near_));
   have_points_ = false;
   have_weight_ = have_block_ = have_near_ = have_lu_ = false;  // corrections belong to a point set
   release_correction_store();

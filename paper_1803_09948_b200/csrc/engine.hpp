@@ -43,6 +43,9 @@ class Engine {
  public:
   explicit Engine(const hfmm_cuda_config& cfg);
   ~Engine();
+  cudaStream_t stream() const { return stream_; }   // the stream every allocation is ordered on
+  int device() const { return cfg_.device; }
+  static bool any_engine_alive();
 
   void set_partition(int rank, int nranks);
   void set_partition_alpha(double alpha);  // < 0: default work model
@@ -87,6 +90,7 @@ class Engine {
 
  private:
   void require_points() const;
+  void release_device_state();
   void run_far_and_near();  // body_q_ -> near_, far_
   void phase_upward();      // near field (own stream) + P2M + M2M
   void phase_downward();    // M2L + L2L + L2P, joins the near field
