@@ -20,6 +20,12 @@ struct Error : std::runtime_error {
   Error(int s, const std::string& msg) : std::runtime_error(msg), status(s) {}
 };
 
+// a size limit of the DEVICE tree / list builder (packed 64-bit sort keys): Engine::set_points falls
+// back to the host builder, which has none
+struct DeviceBuilderLimit : Error {
+  using Error::Error;
+};
+
 inline int nm_index(int n, int m) { return n * (n + 1) + m; }
 inline int nm_total(int p) { return (p + 1) * (p + 1); }
 // row stride (in complex elements) of the device expansion arrays: padded to 4 complex = 32 B

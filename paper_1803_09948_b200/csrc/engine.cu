@@ -652,6 +652,8 @@ void Engine::dist_downward(void* out_morton_dev) {
   HFMM_CUDA_CHECK(cudaEventRecord(ev_[9], stream_));
 }
 
+static constexpr size_t kHostFallbackBodies = size_t(1) << 18;
+
 void Engine::set_points(const double* xyz, size_t n) {
   HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
   const auto t0 = std::chrono::steady_clock::now();
@@ -666,10 +668,27 @@ void Engine::set_points(const double* xyz, size_t n) {
   pairs_ = PairLists{};
   stride_ = coeff_stride(cfg_.order);
   m2l_ = TranslateStage{};
-  if (cfg_.flags & HFMM_FLAG_HOST_TREE)
+  host_lists_ = (cfg_.flags & HFMM_FLAG_HOST_TREE) != 0;
+  if (host_lists_) {
     set_points_host(xyz, n);
-  else
-    set_points_device(xyz, n);
+  } else {
+    try {
+      set_points_device(xyz, n);
+    } catch (const DeviceBuilderLimit&) {
+      // ... and lists beyond the device traversal's capacity (a gate that forbids every coarse
+      // translation) are left to it for moderate sizes only: at a million points that configuration
+      // is a mistake to report, not hours of host work to start
+      if (n > kHostFallbackBodies) throw;
+      host_lists_ = true;
+      // very deep trees (clusters of coincident points driving the octree to its last levels) have
+      // shifts the device builder's packed sort keys cannot hold: the host builder produces the same
+      // tree and lists without that limit (setup only; the matvec is unaffected)
+      dev_pairs_ = DevicePairs{};
+      pairs_ = PairLists{};
+      m2l_ = TranslateStage{};
+      set_points_host(xyz, n);
+    }
+  }
   body_index_.upload(tree_.index, stream_);
   body_q_.resize(n);
   near_.resize(n);
@@ -1198,7 +1217,7 @@ void Engine::measure_weights(double* local, double* remote) const {
 
 void Engine::get_pairs(int which, uint32_t* out, uint64_t* count) const {
   require_points();
-  if (!(cfg_.flags & HFMM_FLAG_HOST_TREE)) {  // lists live on the device: copy on demand
+  if (!host_lists_) {  // lists live on the device: copy on demand
     const uint64_t np = which ? dev_pairs_.n_near : dev_pairs_.n_far;
     *count = np;
     if (!out || !np) return;

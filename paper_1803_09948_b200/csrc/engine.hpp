@@ -120,6 +120,7 @@ class Engine {
   double partition_alpha_ = -1.0;
   P2PArgs p2p_args_{};
   bool p2p_late_ = false;
+  bool host_lists_ = false;  // the pair lists of the current point set live on the host (host builder)
   std::vector<uint8_t> owned_;  // per cell
   std::vector<int32_t> cell_rank_;  // per cell: owning rank of the Morton partition
   uint64_t owned_m2l_pairs_ = 0, owned_body_pairs_ = 0, launches_ = 0;

@@ -138,8 +138,11 @@ __device__ void scaled_bessel_complex(int P, float zr, float eps, float s, float
   // sin(x + i y) = sin x cosh y + i cos x sinh y
   const double snx = sin(zx) * cosh(zy), sny = cos(zx) * sinh(zy);
   const double j0x = snx * ix - sny * iy, j0y = snx * iy + sny * ix;
-  const double cn2 = cx * cx + cy * cy;
-  const double scx = (j0x * cx + j0y * cy) / cn2, scy = (j0y * cx - j0x * cy) / cn2;  // j_0 / cur
+  // j_0 / cur with cur scaled to unit size first: |cur| ranges over 1e-280 .. 1e250, its square would
+  // leave the FP64 range (the gate-off regime with wide leaves is the only one that gets here)
+  const double cm = fmax(fabs(cx), fabs(cy));
+  const double ux = cx / cm, uy = cy / cm, un2 = ux * ux + uy * uy;
+  const double scx = (j0x * ux + j0y * uy) / un2 / cm, scy = (j0y * ux - j0x * uy) / un2 / cm;
   double f = 1.0;  // (2n+1)!!/s^n
   for (int n = 0; n <= P; ++n) {
     out_re[n * 32] = float((kx[n] * scx - ky[n] * scy) * f);

@@ -560,9 +560,9 @@ void dual_tree_traversal_device(const TreeArrays& t, const DeviceCells& cells, d
   }
   // more than ~500 pairs per body: the kd_max gate forbids every coarse translation (k x box >> kd_max)
   // and the lists degenerate towards all pairs of finest-level cells, as they do in the reference
-  throw Error(HFMM_ERR_STRUCTURAL,
-              "dual tree traversal: interaction lists exceed 512 pairs per body (kd_max too small for this "
-              "wavenumber and domain?)");
+  throw DeviceBuilderLimit(HFMM_ERR_STRUCTURAL,
+                           "dual tree traversal: interaction lists exceed 512 pairs per body (kd_max too small for "
+                           "this wavenumber and domain?)");
 }
 
 void far_pair_level_range(const DevicePairs& p, const DeviceCells& cells, int& lmin_dst, int& lmin_src,
@@ -678,8 +678,8 @@ void build_far_classes_device(const DevicePairs& p, const DeviceCells& cells,
   nruns.download(&h_runs, 1, s);
   HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
   if (h_flag)
-    throw Error(HFMM_ERR_INTERNAL,
-                "an M2L lattice shift exceeds the packed key range; rebuild with HFMM_FLAG_HOST_TREE");
+    throw DeviceBuilderLimit(HFMM_ERR_INTERNAL,
+                             "an M2L lattice shift exceeds the packed key range; rebuild with HFMM_FLAG_HOST_TREE");
   std::vector<uint64_t> hk(h_runs);
   std::vector<int> hc(h_runs);
   uniq.download(hk.data(), h_runs, s);

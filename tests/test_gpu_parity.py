@@ -456,3 +456,42 @@ def test_sharded_matvec_with_ordered_accumulation_is_reproducible():
         outs.append(out.cpu().numpy())
     for o in outs[1:]:
         assert np.array_equal(o, outs[0])
+
+
+def test_complex_wavenumber_with_wide_leaves(oracle):
+    """gate off (kd_max = 0) and no leaf cap: the leaf expansions leave the low-frequency series and run
+    the complex Miller recurrence (special.cpp:36-53 with a complex argument), whose normalisation
+    once squared a 1e250-scaled iterate (found by scripts/fuzz_parity.py).  Far from the regime the
+    truncated expansion is accurate in, so parity is against the oracle's FMM — the reference's
+    pipeline in FP64 — not against the direct sum"""
+    rng = np.random.default_rng(51)
+    n = 6000
+    xyz = rng.uniform(-1, 1, size=(n, 3))
+    q = charges(n, 51)
+    for k, order in ((12 + 0.6j, 4), (6 + 3j, 8)):
+        op = HfmmCuda(k=k, order=order, ncrit=64, theta=0.4, kd_max=0.0, leaf_cap=0.0)
+        op.set_points(xyz)
+        y = op.matvec(q)
+        assert np.isfinite(y).all()
+        assert op.stats()["m2l_pairs"] > 0
+        y64 = oracle.fmm(xyz, k, order, ncrit=64, leaf_cap=0.0, theta=0.4, kd_max=0.0).matvec(q)
+        assert rel_l2(y, y64) < 1e-5
+
+
+def test_deep_tree_of_coincident_points_falls_back_to_the_host_builder(oracle):
+    """clusters of more than ncrit coincident points drive the octree to its last level; the lattice
+    shifts of such a tree do not fit the device builder's packed sort keys, and set_points then uses the
+    host builder (same tree, same lists) instead of failing"""
+    rng = np.random.default_rng(104)
+    base = rng.uniform(-1, 1, size=(160, 3))
+    xyz = base[rng.integers(0, len(base), 500)]
+    q = charges(500, 104)
+    op = HfmmCuda(k=1 + 2j, order=10, ncrit=4, theta=0.3, kd_max=2.0, leaf_cap=0.0)
+    op.set_points(xyz)
+    st = op.stats()
+    assert st["max_level"] >= 20 and st["m2l_pairs"] > 0
+    y = op.matvec(q)
+    assert rel_l2(y, oracle.direct_sum(xyz, q, 1 + 2j)) < 3e-6
+    host = HfmmCuda(k=1 + 2j, order=10, ncrit=4, theta=0.3, kd_max=2.0, leaf_cap=0.0, flags=1)
+    host.set_points(xyz)
+    assert (host.stats()["m2l_pairs"], host.stats()["p2p_pairs"]) == (st["m2l_pairs"], st["p2p_pairs"])
