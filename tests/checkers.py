@@ -303,7 +303,7 @@ def _oracle_build_corrections(lib, patches, tables, k, mode=2, near_patch_distan
     piv = np.zeros(npatch * ni if mode else 0, dtype=np.int32)
     vp = lambda a: a.ctypes.data_as(C.c_void_p) if a.size else None
     lib.ho_build_patch_blocks.restype = C.c_int
-    rc = lib.ho_build_patch_blocks(C.byref(r), C.c_double(k), C.c_double(0.0), vp(pb), vp(lu), vp(piv))
+    rc = lib.ho_build_patch_blocks(C.byref(r), C.c_double(np.real(k)), C.c_double(np.imag(k)), vp(pb), vp(lu), vp(piv))
     assert rc == 0, "singular self block"
     off = np.zeros(n + 1, dtype=np.uint32)
     srcp = C.POINTER(C.c_uint32)()
@@ -314,7 +314,7 @@ def _oracle_build_corrections(lib, patches, tables, k, mode=2, near_patch_distan
         lib.ho_free(srcp)
     dl = np.zeros(nnz, dtype=np.complex128)
     if nnz:
-        lib.ho_build_near_deltas(C.byref(r), C.c_double(k), C.c_double(0.0), vp(off), vp(src), vp(dl))
+        lib.ho_build_near_deltas(C.byref(r), C.c_double(np.real(k)), C.c_double(np.imag(k)), vp(off), vp(src), vp(dl))
     return dict(xyz=xyz, patch_block=pb, block_lu=lu, block_piv=piv, near_offset=off, near_source=src,
                 near_delta=dl)
 
