@@ -23,7 +23,10 @@ struct Error : std::runtime_error {
 // a size limit of the DEVICE tree / list builder (packed 64-bit sort keys): Engine::set_points falls
 // back to the host builder, which has none
 struct DeviceBuilderLimit : Error {
-  using Error::Error;
+  // any_size: the host builder handles the input at the usual cost (O(N)); otherwise the lists
+  // themselves are huge and the fallback is taken for moderate point counts only
+  bool any_size;
+  DeviceBuilderLimit(int s, const std::string& msg, bool any) : Error(s, msg), any_size(any) {}
 };
 
 inline int nm_index(int n, int m) { return n * (n + 1) + m; }

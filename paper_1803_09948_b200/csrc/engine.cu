@@ -674,11 +674,11 @@ void Engine::set_points(const double* xyz, size_t n) {
   } else {
     try {
       set_points_device(xyz, n);
-    } catch (const DeviceBuilderLimit&) {
+    } catch (const DeviceBuilderLimit& lim) {
       // ... and lists beyond the device traversal's capacity (a gate that forbids every coarse
       // translation) are left to it for moderate sizes only: at a million points that configuration
       // is a mistake to report, not hours of host work to start
-      if (n > kHostFallbackBodies) throw;
+      if (!lim.any_size && n > kHostFallbackBodies) throw;
       host_lists_ = true;
       // very deep trees (clusters of coincident points driving the octree to its last levels) have
       // shifts the device builder's packed sort keys cannot hold: the host builder produces the same

@@ -562,7 +562,8 @@ void dual_tree_traversal_device(const TreeArrays& t, const DeviceCells& cells, d
   // and the lists degenerate towards all pairs of finest-level cells, as they do in the reference
   throw DeviceBuilderLimit(HFMM_ERR_STRUCTURAL,
                            "dual tree traversal: interaction lists exceed 512 pairs per body (kd_max too small for "
-                           "this wavenumber and domain?)");
+                           "this wavenumber and domain?)",
+                           false);
 }
 
 void far_pair_level_range(const DevicePairs& p, const DeviceCells& cells, int& lmin_dst, int& lmin_src,
@@ -679,7 +680,8 @@ void build_far_classes_device(const DevicePairs& p, const DeviceCells& cells,
   HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
   if (h_flag)
     throw DeviceBuilderLimit(HFMM_ERR_INTERNAL,
-                             "an M2L lattice shift exceeds the packed key range; rebuild with HFMM_FLAG_HOST_TREE");
+                             "an M2L lattice shift exceeds the packed key range; rebuild with HFMM_FLAG_HOST_TREE",
+                             true);
   std::vector<uint64_t> hk(h_runs);
   std::vector<int> hc(h_runs);
   uniq.download(hk.data(), h_runs, s);

@@ -12,7 +12,8 @@ from paper_1803_09948_b200.api import HFMM_FLAG_DETERMINISTIC, HFMM_FLAG_HOST_TR
 
 seed = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 cases = int(sys.argv[2]) if len(sys.argv) > 2 else 60
-only = int(sys.argv[3]) if len(sys.argv) > 3 else -1   # run just this case (the random stream is still drawn for all)
+only = int(sys.argv[3]) if len(sys.argv) > 3 else -1   # run just this case
+sizes = [int(v) for v in sys.argv[4].split(",")] if len(sys.argv) > 4 else [1, 2, 7, 63, 500, 3000, 12000, 40000]
 oracle = Oracle()
 # FP32 pipeline: truncation error of the expansion at order P plus ~1e-6 of rounding
 def bound(order, theta):
@@ -27,7 +28,7 @@ for case in range(cases):
     if only >= 0 and case != only:
         continue
     rng = np.random.default_rng([seed, case])   # every case has its own stream: reproducible alone
-    n = int(rng.choice([1, 2, 7, 63, 500, 3000, 12000, 40000]))
+    n = int(rng.choice(sizes))
     kind = rng.choice(["sphere", "cube", "plummer", "line", "two_clusters", "duplicates"])
     if kind == "sphere":
         v = rng.normal(size=(n, 3)); xyz = v / np.linalg.norm(v, axis=1, keepdims=True)
@@ -47,7 +48,7 @@ for case in range(cases):
     if rng.uniform() < 0.2:
         k = complex(k, k * float(rng.choice([0.05, 0.5, 2.0])))
     order = int(rng.choice([2, 4, 6, 8, 10, 12, 13, 16]))
-    ncrit = int(rng.choice([4, 16, 32, 64, 200]))
+    ncrit = int(rng.choice([4, 16, 32, 64, 200] if n < 100000 else [32, 64, 200]))   # (tiny leaves at 1e5+ points: 1e9 M2L pairs)
     theta = float(rng.choice([0.3, 0.4, 0.5, 0.7]))
     kd_max = float(rng.choice([0.0, 1.0, 2.0]))
     leaf_cap = float(rng.choice([-1.0, 0.0]))
@@ -107,5 +108,7 @@ for case in range(cases):
     assert (st2["m2l_pairs"], st2["p2p_pairs"], st2["n_cells"]) == (st["m2l_pairs"], st["p2p_pairs"], st["n_cells"]), desc
     y2 = op2.matvec(q)
     d = np.linalg.norm(y2 - y) / max(np.linalg.norm(y), 1e-300)
-    assert d < 2e-6, (desc, d)
+    # FP32 accumulation order: ~1e-7 typically, up to a few 1e-6 where the gate leaves thousands of
+    # low-order translations per cell (1.1e9 pairs at 150 k points: 3.7e-6 between atomic and ordered sums)
+    assert d < 1e-5, (desc, d)
 print(f"{cases} cases ok in {time.time()-t0:.0f} s; worst err/tol {worst:.2f}")
