@@ -38,8 +38,11 @@ typedef enum {
 } hfmm_status;
 
 enum {
-  /* build tree + interaction lists with the host C++ builder instead of the device builder
-   * (debug toggle kept until list statistics match the reference exactly) */
+  /* build tree + interaction lists with the host C++ builder instead of the device builder (same
+   * tree, same lists; cross-check and fallback).  Without the flag set_points still switches to the
+   * host builder by itself when the device builder's packed sort keys cannot hold a lattice shift
+   * (trees that reach the last levels) or, up to 262,144 points, when the lists exceed its 512 pairs
+   * per body */
   HFMM_FLAG_HOST_TREE = 1 << 0,
   /* time each phase with CUDA events (fills hfmm_cuda_stats seconds); costs a few syncs */
   HFMM_FLAG_PHASE_TIMERS = 1 << 1,
