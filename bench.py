@@ -274,10 +274,10 @@ def run_single(args, cfg):
             "ms_per_launch_alone": alone["m2l"] * 1e3, "achieved_alone": m2l_tf_alone,
             "frac_alone": m2l_tf_alone / fp32_peak if fp32_peak else None,
             # dram__bytes_read + dram__bytes_write of this launch from the committed ncu --set full
-            # capture of the same configuration (profiles/r01_ncu_translate_mixed_cfg2_full.txt:
-            # 11.16 GB read + 5.61 GB written); algorithmic bytes
+            # capture of the same configuration (profiles/r01_ncu_final_cfg2_full.txt:
+            # 11.12 GB read + 5.57 GB written); algorithmic bytes
             # are pairs x 2 x 8 (P+1)^2 (one source row read, one destination row reduced)
-            "traffic": 16.77e9 if (cfg.name == "cfg2" and n == cfg.n) else None,
+            "traffic": 16.69e9 if (cfg.name == "cfg2" and n == cfg.n) else None,
             "algorithmic_bytes": st0["m2l_pairs"] * 2 * 8 * (cfg.order + 1) ** 2},
         # kernel-alone durations (near field serialised behind the far field); "ms_in_step" is the event
         # interval inside the timed region, where P2P is co-resident with M2L
