@@ -84,3 +84,33 @@ def test_mie_series_of_the_package_is_the_reference_s(ref):
     tot = np.exp(1j * 4.0 * np.cos(th)) + mie_soft_sphere(1.0, 4.0, 1.0, th)
     assert np.abs(tot).max() < 1e-10
 
+
+
+def test_random_configurations_bitwise(oracle, ref):
+    """the oracle's FMM pipeline against the compiled reference on random point sets (coincident points,
+    near-collinear sets, single bodies), real and complex wavenumbers, gates on and off, leaf caps:
+    identical to the last bit (deterministic accumulation on both sides)"""
+    for case in range(14):
+        rng = np.random.default_rng([3, case])
+        n = int(rng.choice([1, 5, 60, 400, 1500]))
+        kind = rng.choice(["cube", "sphere", "dup", "line"])
+        if kind == "cube":
+            xyz = rng.uniform(-1, 1, (n, 3))
+        elif kind == "sphere":
+            v = rng.normal(size=(n, 3))
+            xyz = v / np.linalg.norm(v, axis=1, keepdims=True)
+        elif kind == "dup":
+            base = rng.uniform(-1, 1, (max(1, n // 3), 3))
+            xyz = base[rng.integers(0, len(base), n)]
+        else:
+            xyz = np.stack([rng.uniform(0, 3, n), 1e-3 * rng.normal(size=n), np.zeros(n)], 1)
+        q = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+        k = float(rng.choice([0.3, 1.0, 4.0, 9.0]))
+        if rng.uniform() < 0.3:
+            k = complex(k, 0.3 * k)
+        kw = dict(ncrit=int(rng.choice([4, 16, 64])), theta=float(rng.choice([0.3, 0.5, 0.7])),
+                  kd_max=float(rng.choice([0.0, 1.0, 2.0])), leaf_cap=float(rng.choice([0.0, 0.3])))
+        order = int(rng.choice([2, 5, 8, 11]))
+        yo = oracle.fmm(xyz, k, order, **kw).matvec(q)
+        yr = ref.fmm(xyz, k, order, threads=4, **kw).matvec(q)
+        assert np.array_equal(yo, yr), (case, n, kind, k, order, kw)
