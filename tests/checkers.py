@@ -457,7 +457,7 @@ class RefBie:
         patches = np.ascontiguousarray(patches, dtype=np.float64)
         self.h = C.c_void_p()
         rc = self.lib.ref_bie_create(C.byref(self.h), C.c_long(patches.shape[0]), _d(patches),
-                                     basis_order, C.c_double(k), C.c_double(0), mode, int(use_tree),
+                                     basis_order, C.c_double(np.real(k)), C.c_double(np.imag(k)), mode, int(use_tree),
                                      order, ncrit, ncrit, C.c_double(theta), C.c_double(kd_max),
                                      C.c_double(leaf_cap), threads)
         assert rc == 0, ref.err()

@@ -114,3 +114,21 @@ def test_random_configurations_bitwise(oracle, ref):
         yo = oracle.fmm(xyz, k, order, **kw).matvec(q)
         yr = ref.fmm(xyz, k, order, threads=4, **kw).matvec(q)
         assert np.array_equal(yo, yr), (case, n, kind, k, order, kw)
+
+
+def test_correction_builders_with_complex_wavenumber_bitwise(oracle, ref):
+    """build_patch_blocks / build_near_corrections of the oracle against the compiled reference for
+    complex wavenumbers, both basis orders, all singularity modes (the device builders are checked
+    against the oracle by the GPU tests and scripts/fuzz_bie.py)"""
+    from paper_1803_09948_b200.workloads import icosphere_patches
+
+    patches = icosphere_patches(1) * np.array([1.0, 0.8, 1.3])
+    for basis_order in (1, 2):
+        tables = ref.correction_tables(basis_order)
+        for k in (2.0 + 0.6j, 0.5 + 1.0j):
+            for mode in (0, 1, 2):
+                want = ref.bie(patches, basis_order, k, mode=mode, use_tree=False).corrections()
+                got = oracle.build_corrections(patches, tables, k, mode=mode)
+                for key in ("patch_block", "block_lu", "block_piv", "near_offset", "near_source", "near_delta"):
+                    if want.get(key) is not None:
+                        assert np.array_equal(got[key], np.asarray(want[key])), (basis_order, k, mode, key)
