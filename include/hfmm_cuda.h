@@ -88,6 +88,11 @@ typedef struct {
   uint64_t kernel_launches;    /* kernels launched by the last matvec                        */
   uint64_t device_bytes;       /* HBM held by the handle                                     */
   uint64_t m2l_batches;        /* work items of the M2L launch: <= 32 pairs of one shift class */
+  uint64_t host_tree_used;     /* 1: tree and lists of this point set were built by the host builder
+                                  (HFMM_FLAG_HOST_TREE, or the device builder's limits, see the flag) */
+  uint64_t p2p_mode;           /* near-field kernel variant: 0 three MUFU per pair (any R'), 1..3 bounded
+                                  R' with sin(R')/R' (and cos) as polynomials on the FMA pipe            */
+  double near_r2_max;          /* bound on (k_r |x_i - x_j|)^2 over the near lists (selects p2p_mode)  */
 } hfmm_cuda_stats;
 
 typedef struct hfmm_cuda hfmm_cuda_t;

@@ -43,7 +43,8 @@ class Stats(C.Structure):
                 ("setup_seconds", "upward_seconds", "interaction_seconds", "downward_seconds",
                  "p2p_seconds", "m2l_seconds", "p2m_seconds", "m2m_seconds", "l2l_seconds",
                  "l2p_seconds", "matvec_seconds")] + \
-               [("kernel_launches", C.c_uint64), ("device_bytes", C.c_uint64), ("m2l_batches", C.c_uint64)]
+               [("kernel_launches", C.c_uint64), ("device_bytes", C.c_uint64), ("m2l_batches", C.c_uint64),
+                ("host_tree_used", C.c_uint64), ("p2p_mode", C.c_uint64), ("near_r2_max", C.c_double)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

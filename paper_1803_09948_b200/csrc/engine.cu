@@ -545,6 +545,21 @@ void Engine::upload_cell_geometry(std::vector<int4>& geom) {
   level_scale_.upload(level_scale_host_, stream_);
 }
 
+// Near-field kernel variant (kernels.cuh, P2PArgs::mode).  max_r2_lattice bounds the squared distance
+// of any evaluated body pair in half-sides of the finest level; with a leaf cap in force (the
+// reference's solver path) R' = k_r R stays below ~4 and sin(R')/R' runs as a polynomial on the FMA pipe.
+// HFMM_P2P_MODE=0..3 forces a variant (tests and experiments; polynomial modes need the bound).
+void Engine::select_near_kernel(uint64_t max_r2_lattice) {
+  near_r2_max_ = double(max_r2_lattice) * kunit_d_ * kunit_d_ * (1.0 + 1e-5);
+  const bool bounded = near_r2_max_ <= double(kP2PPolyMaxR2);
+  p2p_mode_ = bounded ? P2P_MODE_SINC_POLY : P2P_MODE_MUFU;
+  if (const char* e = getenv("HFMM_P2P_MODE")) {
+    const int m = atoi(e);
+    if (m == P2P_MODE_MUFU || (bounded && m >= 0 && m <= P2P_MODE_ALL_POLY)) p2p_mode_ = m;
+  }
+  fit_p2p_polynomials(std::max(near_r2_max_, 1e-3), p2p_sinc_, p2p_cos_);
+}
+
 // tiles of <= 32 targets per owned leaf, longest first (the tail of the launch fills with short ones)
 void Engine::build_tiles(const std::vector<uint64_t>& work) {
   const TreeArrays& t = tree_;
@@ -768,6 +783,7 @@ void Engine::set_points_device(const double* xyz, size_t n) {
   build_near_lists_device(dev_pairs_, t, cells, owned_, p2p_offset_, p2p_split_, p2p_src_, nl, stream_);
   stats_.p2p_body_pairs = nl.body_pairs;
   owned_body_pairs_ = nl.owned_body_pairs;
+  select_near_kernel(nl.max_r2_lattice);
   build_tiles(nl.work);
   mark("near lists + tiles");
 
@@ -837,12 +853,19 @@ void Engine::set_points_host(const double* xyz, size_t n) {
            std::llabs(int64_t(geom[a].z) - geom[b].z) <= ha + hb;
   };
   std::vector<uint32_t> off(nleaf + 1, 0), split(nleaf, 0);
-  uint64_t body_pairs = 0, owned_body_pairs = 0;
+  uint64_t body_pairs = 0, owned_body_pairs = 0, max_r2_lattice = 0;
   for (size_t e = 0; e < pairs_.p2p_t.size(); ++e) {
     const uint32_t a = pairs_.p2p_t[e], b = pairs_.p2p_s[e];
     body_pairs += uint64_t(t.body_count[a]) * t.body_count[b];
     if (!owned_[a]) continue;
     owned_body_pairs += uint64_t(t.body_count[a]) * t.body_count[b];
+    {
+      const uint64_t hs = (uint64_t(1) << (Lf - t.level[a])) + (uint64_t(1) << (Lf - t.level[b]));
+      const uint64_t fx = uint64_t(std::llabs(int64_t(geom[a].x) - geom[b].x)) + hs,
+                     fy = uint64_t(std::llabs(int64_t(geom[a].y) - geom[b].y)) + hs,
+                     fz = uint64_t(std::llabs(int64_t(geom[a].z) - geom[b].z)) + hs;
+      max_r2_lattice = std::max(max_r2_lattice, fx * fx + fy * fy + fz * fz);
+    }
     ++off[leaf_slot[a] + 1];
     if (touching(a, b)) ++split[leaf_slot[a]];
   }
@@ -865,6 +888,7 @@ void Engine::set_points_host(const double* xyz, size_t n) {
     std::sort(srcs.begin() + split[i], srcs.begin() + off[i + 1]);
   });
   build_tiles(work);
+  select_near_kernel(max_r2_lattice);
   stats_.p2p_body_pairs = body_pairs;
   owned_body_pairs_ = owned_body_pairs;
 
@@ -919,6 +943,9 @@ void Engine::phase_upward() {
   pa.kunit = kunit_;
   pa.out_scale = float(cfg_.wave_r / (4.0 * kPi));
   pa.damp = float(cfg_.wave_i / cfg_.wave_r * 1.4426950408889634);
+  pa.mode = p2p_mode_;
+  std::copy(p2p_sinc_, p2p_sinc_ + 8, pa.sinc_c);
+  std::copy(p2p_cos_, p2p_cos_ + 8, pa.cos_c);
   p2p_args_ = pa;
   // The near field (MUFU-bound, no shared-memory traffic) and M2L (shared-memory-bound) complement
   // each other, but only if they are co-resident: enqueued first, the 14 k P2P CTAs fill every SM
@@ -1148,6 +1175,9 @@ void Engine::get_stats(hfmm_cuda_stats* out) {
   collect_timings();
   stats_.device_bytes = device_bytes_counter();
   stats_.m2l_batches = m2l_.n_items;
+  stats_.host_tree_used = host_lists_ ? 1 : 0;
+  stats_.p2p_mode = uint64_t(p2p_mode_);
+  stats_.near_r2_max = near_r2_max_;
   *out = stats_;
 }
 

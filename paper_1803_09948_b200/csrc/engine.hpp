@@ -106,6 +106,7 @@ class Engine {
   void finish_far_field(TableRegistry& reg);
   void upload_cell_geometry(std::vector<int4>& geom);
   void build_tiles(const std::vector<uint64_t>& work);
+  void select_near_kernel(uint64_t max_r2_lattice);
   void plan_ordered_reduce(TranslateStage& st, const std::vector<TranslateItem>& items);
   void upload_stage(TranslateStage& st, const std::vector<uint32_t>& src,
                     const std::vector<uint32_t>& dst, const std::vector<uint32_t>& cls_of_pair,
@@ -149,6 +150,9 @@ class Engine {
   DeviceBuffer<P2PTile> p2p_tiles_;
   DeviceBuffer<uint32_t> p2p_offset_, p2p_split_, p2p_src_;
   uint32_t n_tiles_ = 0;
+  int p2p_mode_ = 0;           // P2P_MODE_*
+  double near_r2_max_ = 0;     // bound on R'^2 over the owned near lists
+  float p2p_sinc_[8] = {}, p2p_cos_[8] = {};
   float kunit_ = 0;
   double kunit_d_ = 0, grid_ = 1;
   // far field

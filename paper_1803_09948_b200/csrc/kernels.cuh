@@ -52,7 +52,20 @@ struct P2PArgs {
   double grid;       // power of two; hi parts and hi offsets are integer multiples of it
   float out_scale;   // k / (4 pi)
   float damp;        // (k_i / k_r) log2(e): complex wavenumber, amplitude 2^{-damp R'}; 0 for real k
+  // Bounded near field: when every listed leaf pair keeps R'^2 = |k_r (x_i - x_j)|^2 <= r2_max (the
+  // engine computes the exact bound from the lattice, set_points), sin(R')/R' is evaluated as a
+  // degree-6 polynomial in R'^2 on the FMA pipe (sinc_c, fitted to [0, r2_max] at setup) and only
+  // rsqrt and cos stay on the MUFU pipe: two MUFU per pair instead of three.  mode 0 keeps the
+  // general three-MUFU evaluation (unbounded R': no leaf cap, gate-blocked leaves).
+  int mode;          // P2P_MODE_*
+  float sinc_c[8];   // sin(sqrt(u))/sqrt(u) ~ sum_i sinc_c[i] u^i on [0, r2_max]
+  float cos_c[8];    // cos(sqrt(u))         ~ sum_i cos_c[i] u^i
 };
+enum { P2P_MODE_MUFU = 0, P2P_MODE_SINC_POLY = 1, P2P_MODE_SINC_POLY_EXPANDED = 2, P2P_MODE_ALL_POLY = 3 };
+constexpr int kP2PPolyDegree = 6;
+constexpr float kP2PPolyMaxR2 = 16.0f;  // beyond R' = 4 the polynomial loses to FP32 cancellation: mode 0
+// least-squares-free near-minimax fit (Chebyshev interpolation) of sinc / cos in u = R'^2 on [0, r2_max]
+void fit_p2p_polynomials(double r2_max, float sinc_c[8], float cos_c[8]);
 void launch_p2p(const P2PArgs& a, cudaStream_t s);
 
 // ---- P2M / L2P (reference expansion.cpp:157-175, 283-300) -----------------------------------

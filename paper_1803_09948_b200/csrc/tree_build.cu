@@ -248,7 +248,7 @@ near_keys_kernel(const uint2* __restrict__ near, unsigned long long n, const uin
                  const uint32_t* __restrict__ leaf_slot, const uint8_t* __restrict__ owned, int max_level,
                  uint64_t* __restrict__ keys, unsigned long long* __restrict__ totals) {
   const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-  unsigned long long bp = 0, obp = 0, own = 0;
+  unsigned long long bp = 0, obp = 0, own = 0, far2 = 0;
   if (i < n) {
     const uint2 p = near[i];
     bp = (unsigned long long)body_count[p.x] * body_count[p.y];
@@ -260,10 +260,14 @@ near_keys_kernel(const uint2* __restrict__ near, unsigned long long n, const uin
       const int ua = max_level - int(lvl[p.x]), ub = max_level - int(lvl[p.y]);
       const long long ha = 1ll << ua, hb = 1ll << ub;
       auto c = [](uint32_t v, int up) { return (long long)(2ull * v + 1) << up; };
-      const bool touch = llabs(c(ix[p.x], ua) - c(ix[p.y], ub)) <= ha + hb &&
-                         llabs(c(iy[p.x], ua) - c(iy[p.y], ub)) <= ha + hb &&
-                         llabs(c(iz[p.x], ua) - c(iz[p.y], ub)) <= ha + hb;
+      const long long ax = llabs(c(ix[p.x], ua) - c(ix[p.y], ub)), ay = llabs(c(iy[p.x], ua) - c(iy[p.y], ub)),
+                      az = llabs(c(iz[p.x], ua) - c(iz[p.y], ub));
+      const bool touch = ax <= ha + hb && ay <= ha + hb && az <= ha + hb;
       key = uint64_t(leaf_slot[p.x]) << 32 | (touch ? 0u : 0x80000000u) | p.y;
+      // farthest two bodies of the two cubes can be apart, squared, in half-sides of the finest level
+      const unsigned long long fx = (unsigned long long)(ax + ha + hb), fy = (unsigned long long)(ay + ha + hb),
+                               fz = (unsigned long long)(az + ha + hb);
+      far2 = fx * fx + fy * fy + fz * fz;
     }
     keys[i] = key;
   }
@@ -273,11 +277,13 @@ near_keys_kernel(const uint2* __restrict__ near, unsigned long long n, const uin
     bp += __shfl_xor_sync(0xffffffffu, bp, o);
     obp += __shfl_xor_sync(0xffffffffu, obp, o);
     own += __shfl_xor_sync(0xffffffffu, own, o);
+    far2 = max(far2, __shfl_xor_sync(0xffffffffu, far2, o));
   }
   if ((threadIdx.x & 31) == 0) {
     atomicAdd(totals, bp);
     atomicAdd(totals + 1, obp);
     atomicAdd(totals + 2, own);
+    atomicMax(totals + 3, far2);
   }
 }
 
@@ -610,7 +616,7 @@ void build_near_lists_device(const DevicePairs& p, const TreeArrays& t, const De
   d_slot.upload(slot, s);
   d_owned.upload(owned, s);
   DeviceBuffer<uint64_t> keys(std::max<uint64_t>(p.n_near, 1)), sorted(std::max<uint64_t>(p.n_near, 1));
-  DeviceBuffer<unsigned long long> totals(3);
+  DeviceBuffer<unsigned long long> totals(4);
   totals.zero(s);
   if (p.n_near) {
     near_keys_kernel<<<grid_for(p.n_near), kBlock, 0, s>>>(
@@ -623,12 +629,13 @@ void build_near_lists_device(const DevicePairs& p, const TreeArrays& t, const De
     HFMM_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(tmp.get(bytes), bytes, keys.get(), sorted.get(),
                                                    int(p.n_near), 0, 64, s));
   }
-  unsigned long long h[3];
-  totals.download(h, 3, s);
+  unsigned long long h[4];
+  totals.download(h, 4, s);
   HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
   out.body_pairs = h[0];
   out.owned_body_pairs = h[1];
   out.n_owned_pairs = h[2];
+  out.max_r2_lattice = h[3];
   const uint32_t n_owned = uint32_t(h[2]);
   offset.resize(nleaf + 1);
   split.resize(std::max<uint32_t>(nleaf, 1));

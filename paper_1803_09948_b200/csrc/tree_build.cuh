@@ -59,6 +59,9 @@ void partition_weights_device(const DevicePairs& p, const DeviceCells& cells,
 
 struct NearLists {
   uint64_t n_owned_pairs = 0, body_pairs = 0, owned_body_pairs = 0;
+  // bound on the squared distance of any two bodies of an owned near pair, in half-sides of the
+  // finest level (the cubes' farthest corners): selects the bounded near-field kernel (kernels.cuh)
+  uint64_t max_r2_lattice = 0;
   std::vector<uint64_t> work;  // per leaf slot: sum of source body counts
 };
 // CSR by target leaf slot, touching source leaves first, sources ascending inside each part;
