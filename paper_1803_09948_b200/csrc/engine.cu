@@ -314,7 +314,7 @@ void Engine::upload_stage(TranslateStage& st, const std::vector<uint32_t>& src,
   st.mixed = true;
   {
     std::vector<TranslateItem> per_class = cut(false);
-    if (double(items.size()) > mixed_batch_gain() * double(per_class.size())) {
+    if (!translate64_supported(cfg_.order) && double(items.size()) > mixed_batch_gain() * double(per_class.size())) {
       items.swap(per_class);
       st.mixed = false;
     }
@@ -409,7 +409,7 @@ void Engine::build_m2l_stage_device(TableRegistry& reg, const FarClasses& fc) {
   }
   seg_new[nc] = uint32_t(pos);
   // batches per table group only when that saves batches (see upload_stage)
-  m2l_.mixed = double(items.size()) <= mixed_batch_gain() * double(per_class.size());
+  m2l_.mixed = translate64_supported(cfg_.order) || double(items.size()) <= mixed_batch_gain() * double(per_class.size());
   if (!m2l_.mixed) items.swap(per_class);
   if (pos >= (uint64_t(1) << 32)) throw Error(HFMM_ERR_CONFIG, "pair count exceeds 32-bit indexing");
   regroup_pairs_device(seg_new, seg_old, seg_cls, pos, m2l_.pair_src, m2l_.pair_dst, m2l_.pair_cls, stream_);

@@ -154,6 +154,31 @@ void launch_translate(const TranslateArgs& a, cudaStream_t s);
 // pairs per work item expected by the kernel
 int translate_batch_size(int order);
 
+// ---- the 64-pair in-place translation kernel (kernels_translate64.cu), orders <= 12 ------------
+inline constexpr int kTranslate64Warps = 8;
+inline constexpr int kTranslate64MaxOrder = 12;
+inline constexpr int kTranslate64MaxUnits = 96;   // (P+1)(P+2)/2 <= 91 units (n, m >= 0), rounded to lanes
+inline constexpr int kTranslate64MaxTasks = 32;
+// one whole folded system of a degree (rotations) or one folded column of an order (coaxial step)
+struct Translate64Task {
+  uint32_t tab_off;  // first coefficient row: byte offset in the shared-memory window
+  uint16_t ws_b;     // coefficient row stride, bytes
+  uint16_t row0;     // tile row of input / output 0
+  int16_t step;      // rotations: +1 / -1 per index; coaxial: 2m + 2, growing by 2 per degree
+  uint8_t w;         // inputs = outputs
+  uint8_t pad;
+};
+struct Translate64Schedule {
+  int rot_begin[kTranslate64Warps + 1];
+  int coax_begin[kTranslate64Warps + 1];
+  Translate64Task rot[kTranslate64MaxTasks];
+  Translate64Task coax[kTranslate64MaxTasks];
+};
+bool translate64_supported(int order);       // HFMM_TRANSLATE=32 selects the 32-pair kernel for every order
+void build_translate64_schedule(int order, Translate64Schedule* out);
+void upload_translate64_schedule(int order);
+void launch_translate64(const TranslateArgs& a, cudaStream_t s);
+
 // ---- vector plumbing -------------------------------------------------------------------------
 // body_q[slot] = float2(q[index[slot]]) * weight[index[slot]] (weight may be null)
 void launch_gather_charges(const double2* q_caller, const float2* q_caller_f32,

@@ -722,12 +722,13 @@ void build_translate_schedule(int P, TranslateSchedule* out) {
 }
 
 void upload_translate_schedule(int order) {
+  upload_translate64_schedule(order);
   TranslateSchedule sched;
   build_translate_schedule(order, &sched);
   HFMM_CUDA_CHECK(cudaMemcpyToSymbol(c_sched, &sched, sizeof(sched), sizeof(sched) * size_t(order)));
 }
 
-int translate_batch_size(int) { return kTranslateBatch; }
+int translate_batch_size(int order) { return translate64_supported(order) ? 64 : kTranslateBatch; }
 
 namespace {
 template <int WARPS, int CTAS, bool MIXED, bool STAGED>
@@ -745,6 +746,10 @@ void launch_translate_nu(const TranslateArgs& a, cudaStream_t s, size_t bytes, i
 
 void launch_translate(const TranslateArgs& a, cudaStream_t s) {
   if (a.n_items == 0) return;
+  if (translate64_supported(a.order)) {
+    launch_translate64(a, s);
+    return;
+  }
   const SmemPlan sp = smem_plan(a.order);
   static int sm_count = 0;
   if (!sm_count) {
