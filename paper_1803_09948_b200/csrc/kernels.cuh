@@ -157,6 +157,7 @@ int translate_batch_size(int order);
 // ---- the 64-pair in-place translation kernel (kernels_translate64.cu), orders <= 12 ------------
 inline constexpr int kTranslate64Warps = 8;
 inline constexpr int kTranslate64MaxOrder = 12;
+inline constexpr int kTranslate64MaxDim = 169;     // (P+1)^2 at the largest order
 inline constexpr int kTranslate64MaxUnits = 96;   // (P+1)(P+2)/2 <= 91 units (n, m >= 0), rounded to lanes
 inline constexpr int kTranslate64MaxTasks = 32;
 // one whole folded system of a degree (rotations) or one folded column of an order (coaxial step)

@@ -55,10 +55,10 @@ __host__ __device__ inline Plan64 plan64(int P) {
   s.n_units = (P + 1) * (P + 2) / 2;
   s.rot_floats = rot_table_size(P);
   s.coax_c = coax_table_size(P);
-  s.phase_pitch = (P + 2) & ~1;  // float2 per pair, rows 16-byte aligned
+  s.phase_pitch = kBatch64;  // e^{i m phi}: [m][pair]
   s.off_coax = 4u * uint32_t(s.rot_floats);
   s.off_phase = s.off_coax + 8u * uint32_t(s.coax_c);
-  s.off_tile = (s.off_phase + 8u * uint32_t(kBatch64 * s.phase_pitch) + 15u) & ~15u;
+  s.off_tile = (s.off_phase + 8u * uint32_t((P + 1) * s.phase_pitch) + 15u) & ~15u;
   s.off_unit = (s.off_tile + kPitchB * uint32_t(s.dim) + 15u) & ~15u;
   s.bytes = size_t(s.off_unit) + size_t((4 * s.n_units + 15) & ~15);
   return s;
@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(kTranslate64Warps * 32, 2) translate64_kernel(
   const int p_first = warp * kPairsPerWarp;
   uint32_t my_src = 0, my_dst = 0;
   bool my_live = false;
-  // e^{i m phi} of the warp's pairs, [pair][m] (pitch sp.phase_pitch): written and read by this warp only
+  // e^{i m phi} of every pair of the batch, [m][pair]; each warp fills the columns of its own pairs
   auto load_pairs = [&](const TranslateItem& it) {
     my_live = false;
     if (lane < kPairsPerWarp) {
@@ -309,21 +309,20 @@ __global__ void __launch_bounds__(kTranslate64Warps * 32, 2) translate64_kernel(
         sphi = c.sphi;
       }
       float cr = 1.f, ci = 0.f;
-      const uint32_t base = ph_base + 8u * uint32_t(p * sp.phase_pitch);
+      uint32_t dst = ph_base + 8u * uint32_t(p);
       for (int m = 0; m <= P; ++m) {
-        sts1(base + 8u * m, pack2(cr, ci));
+        sts1(dst, pack2(cr, ci));
+        dst += 8u * kBatch64;
         const float t = cr * cphi - ci * sphi;
         ci = ci * cphi + cr * sphi;
         cr = t;
       }
     }
-    __syncwarp();
   };
 
-  // stage A: gather + fold.  The raw rows of the warp's pairs are copied straight into their tile
-  // columns (cp.async, lane = coefficient: 256 contiguous bytes per instruction, one latency for the whole
-  // batch), then folded in place, lane = unit (n, m >= 0) of one pair:
-  //   a = x_m e^{i m phi},  b = (-1)^m x_{-m} e^{-i m phi}:   s_m = a + b -> row (n, +m),  t_m = a - b -> row (n, -m)
+  // gather: the raw rows of the warp's pairs are copied straight into their tile columns (cp.async,
+  // lane = coefficient: 256 contiguous bytes per instruction; consecutive tile rows are two banks apart)
+  constexpr int kRounds = (kTranslate64MaxDim + 31) / 32;  // 32 coefficients of one pair per warp instruction
   auto issue_gather = [&]() {
 #pragma unroll 1
     for (int pp = 0; pp < kPairsPerWarp; ++pp) {
@@ -331,93 +330,95 @@ __global__ void __launch_bounds__(kTranslate64Warps * 32, 2) translate64_kernel(
       if (!live) continue;  // warp-uniform; the column keeps its (finite) previous contents
       const uint32_t srow = __shfl_sync(0xffffffffu, my_src, pp);
       const float2* src = a.src + size_t(srow) * a.stride + lane;
-      uint32_t dst = tile + 8u * uint32_t(p_first + pp) + kPitchB * uint32_t(lane);
-#pragma unroll 2
-      for (int i = lane; i < sp.dim; i += 32) {
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-        dst += 32u * kPitchB;
-        src += 32;
-      }
+      const uint32_t dst = tile + 8u * uint32_t(p_first + pp) + kPitchB * uint32_t(lane);
+#pragma unroll
+      for (int r = 0; r < kRounds; ++r)
+        if (32 * r + lane < sp.dim)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 32u * r * kPitchB), "l"(src + 32 * r) : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  auto fold = [&]() {
-#pragma unroll 1
-    for (int pp = 0; pp < kPairsPerWarp; ++pp) {
-      const bool live = __shfl_sync(0xffffffffu, my_live, pp);
-      if (!live) continue;
-      const int p = p_first + pp;
-      const uint32_t php = ph_base + 8u * uint32_t(p * sp.phase_pitch), col = tile + 8u * uint32_t(p);
-#pragma unroll
-      for (int u0 = 0; u0 < kTranslate64MaxUnits; u0 += 32) {
-        const int u = u0 + lane;
-        if (u0 < sp.n_units && u < sp.n_units) {
-          const uint32_t un = s_unit[u], rp = un & 0xffffu, m = un >> 16;
-          const uint32_t ap = col + rp * kPitchB, am = col + (rp - 2 * m) * kPitchB;
-          const u64 xp = lds1(ap);
-          const u64 xm = m ? lds1(am) : 0ull;
-          const float2 ph = unpack2(lds1(php + 8u * m));
-          const float sg = (m & 1) ? -1.0f : 1.0f;
-          u64 av = mul2s(xp, ph.x), bv = mul2s(xm, sg * ph.x);
-          fma2s(av, rot90(xp), ph.y);
-          fma2s(bv, rot90(xm), -sg * ph.y);
-          sts1(ap, add2(av, bv));
-          if (m) sts1(am, add2(av, neg2(bv)));
-        }
-      }
-    }
-  };
-
-  // stage E: unfold + scatter, the same lane mapping:
-  //   y_m = (u + v)/2 e^{-i m phi},   y_{-m} = (-1)^m (u - v)/2 e^{+i m phi}
-  auto unfold_scatter = [&]() {
+  // scatter: the same mapping back, tile column -> destination row (RED.64, 256 contiguous bytes each)
+  auto scatter = [&]() {
 #pragma unroll 1
     for (int pp = 0; pp < kPairsPerWarp; ++pp) {
       const bool live = __shfl_sync(0xffffffffu, my_live, pp);
       if (!live) continue;
       const uint32_t drow = __shfl_sync(0xffffffffu, my_dst, pp);
-      const int p = p_first + pp;
-      float2* dst = a.dst + size_t(drow) * a.stride;
-      const uint32_t php = ph_base + 8u * uint32_t(p * sp.phase_pitch), col = tile + 8u * uint32_t(p);
+      float2* dst = a.dst + size_t(drow) * a.stride + lane;
+      const uint32_t src = tile + 8u * uint32_t(p_first + pp) + kPitchB * uint32_t(lane);
 #pragma unroll
-      for (int u0 = 0; u0 < kTranslate64MaxUnits; u0 += 32) {
-        const int u = u0 + lane;
-        if (u0 < sp.n_units && u < sp.n_units) {
-          const uint32_t un = s_unit[u], rp = un & 0xffffu, m = un >> 16, c = rp - m;
-          const u64 uu = lds1(col + rp * kPitchB);
-          const u64 vv = m ? lds1(col + (rp - 2 * m) * kPitchB) : 0ull;
-          const float2 ph = unpack2(lds1(php + 8u * m));
-          const float h = m ? 0.5f : 1.0f, hs = (m & 1) ? -h : h;
-          const u64 sv = add2(uu, vv), dv = add2(uu, neg2(vv));
-          u64 yp = mul2s(sv, h * ph.x), ym = mul2s(dv, hs * ph.x);
-          fma2s(yp, rot90(sv), -h * ph.y);
-          fma2s(ym, rot90(dv), hs * ph.y);
-          const float2 fp = unpack2(yp), fm = unpack2(ym);
-          if (STAGED) {
-            dst[c + m] = fp;
-            if (m) dst[c - m] = fm;
-          } else {
-            atomicAdd(dst + c + m, fp);
-            if (m) atomicAdd(dst + c - m, fm);
-          }
+      for (int r = 0; r < kRounds; ++r)
+        if (32 * r + lane < sp.dim) {
+          const float2 v = unpack2(lds1(src + 32u * r * kPitchB));
+          if (STAGED) dst[32 * r] = v;
+          else atomicAdd(dst + 32 * r, v);
         }
-      }
+    }
+  };
+
+  // fold and unfold, in place, all 64 pairs of a unit (n, m >= 0) per warp step (a lane owns the pairs
+  // l and l + 32 as in the compute stages; the unit — rows, order, sign — is warp-uniform):
+  //   fold    a = x_m e^{i m phi},  b = (-1)^m x_{-m} e^{-i m phi}:   s_m = a + b -> row (n, +m),  t_m = a - b -> row (n, -m)
+  //   unfold  y_m = (u + v)/2 e^{-i m phi},   y_{-m} = (-1)^m (u - v)/2 e^{+i m phi}
+  const uint32_t ph_duo = ph_base + 8u * uint32_t(lane);
+  auto fold = [&]() {
+#pragma unroll 1
+    for (int u = warp; u < sp.n_units; u += kWarps) {
+      const uint32_t un = s_unit[u], rp = un & 0xffffu, m = un >> 16;
+      const uint32_t ap = duo + rp * kPitchB, am = ap - 2u * m * kPitchB;
+      u64 xp0, xp1;
+      ld_duo(ap, xp0, xp1);
+      if (m == 0) continue;  // x_0 is its own folded value (e^{i 0} = 1)
+      u64 xm0, xm1, ph0, ph1;
+      ld_duo(am, xm0, xm1);
+      ld_duo(ph_duo + 8u * kBatch64 * m, ph0, ph1);
+      const float sg = (m & 1) ? -1.0f : 1.0f;
+      const float2 f0 = unpack2(ph0), f1 = unpack2(ph1);
+      u64 a0 = mul2s(xp0, f0.x), a1 = mul2s(xp1, f1.x), b0 = mul2s(xm0, sg * f0.x), b1 = mul2s(xm1, sg * f1.x);
+      fma2s(a0, rot90(xp0), f0.y);
+      fma2s(a1, rot90(xp1), f1.y);
+      fma2s(b0, rot90(xm0), -sg * f0.y);
+      fma2s(b1, rot90(xm1), -sg * f1.y);
+      st_duo(ap, add2(a0, b0), add2(a1, b1));
+      st_duo(am, add2(a0, neg2(b0)), add2(a1, neg2(b1)));
+    }
+  };
+  auto unfold = [&]() {
+#pragma unroll 1
+    for (int u = warp; u < sp.n_units; u += kWarps) {
+      const uint32_t un = s_unit[u], rp = un & 0xffffu, m = un >> 16;
+      if (m == 0) continue;  // y_0 = u_0
+      const uint32_t ap = duo + rp * kPitchB, am = ap - 2u * m * kPitchB;
+      u64 u0, u1, v0, v1, ph0, ph1;
+      ld_duo(ap, u0, u1);
+      ld_duo(am, v0, v1);
+      ld_duo(ph_duo + 8u * kBatch64 * m, ph0, ph1);
+      const float hs = (m & 1) ? -0.5f : 0.5f;
+      const float2 f0 = unpack2(ph0), f1 = unpack2(ph1);
+      const u64 s0 = add2(u0, v0), s1 = add2(u1, v1), d0 = add2(u0, neg2(v0)), d1 = add2(u1, neg2(v1));
+      u64 yp0 = mul2s(s0, 0.5f * f0.x), yp1 = mul2s(s1, 0.5f * f1.x), ym0 = mul2s(d0, hs * f0.x), ym1 = mul2s(d1, hs * f1.x);
+      fma2s(yp0, rot90(s0), -0.5f * f0.y);
+      fma2s(yp1, rot90(s1), -0.5f * f1.y);
+      fma2s(ym0, rot90(d0), hs * f0.y);
+      fma2s(ym1, rot90(d1), hs * f1.y);
+      st_duo(ap, yp0, yp1);
+      st_duo(am, ym0, ym1);
     }
   };
 
   TranslateItem item = a.items[it_begin];
   uint32_t loaded_grp = item.group;
   fetch_tables(a.classes[a.pair_cls[item.pair_begin]]);
-  __syncthreads();  // s_um, the cleared tile
+  __syncthreads();  // s_unit, the cleared tile
   load_pairs(item);
   issue_gather();
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncwarp();
-  fold();
 
   for (uint32_t it = it_begin; it < it_end; ++it) {
-    asm volatile("cp.async.wait_all;" ::: "memory");  // this group's tables
-    __syncthreads();                                  // every warp's columns are folded, tables landed
+    asm volatile("cp.async.wait_all;" ::: "memory");  // this batch's rows, this group's tables
+    __syncthreads();
+    fold();
+    __syncthreads();
     // stage B: forward rotation, in place
     for (int t = sched.rot_begin[warp]; t < sched.rot_begin[warp + 1]; ++t) {
       const Translate64Task d = sched.rot[t];
@@ -436,7 +437,7 @@ __global__ void __launch_bounds__(kTranslate64Warps * 32, 2) translate64_kernel(
       rot_dispatch64<true>(d.w, win + d.tab_off, d.ws_b, duo + d.row0 * kPitchB, d.step * int(kPitchB));
     }
     __syncthreads();
-    // the tables have had their last reader: fetch the next group's behind the scatter
+    // the tables have had their last reader: fetch the next group's behind the unfold and the scatter
     TranslateItem next = item;
     const bool has_next = it + 1 < it_end;
     if (has_next) {
@@ -446,25 +447,14 @@ __global__ void __launch_bounds__(kTranslate64Warps * 32, 2) translate64_kernel(
         loaded_grp = next.group;
       }
     }
-    // stage E, then this warp's columns of the next batch (no CTA barrier in between: a warp reads and
-    // rewrites only its own eight tile columns)
-    unfold_scatter();
-    __syncwarp();
+    unfold();
+    __syncthreads();
+    // scatter, then this warp's columns of the next batch: a warp reads and rewrites only its own eight
+    // tile columns and phase columns, so no CTA barrier separates the two
+    scatter();
     if (has_next) {
-      // the previous phases and (source, destination) rows have had their last reader
-      bool live_next = false;
-      uint32_t src_next = 0;
-      if (lane < kPairsPerWarp && p_first + lane < int(next.count)) {
-        live_next = true;
-        src_next = a.pair_src[next.pair_begin + p_first + lane];
-      }
-      my_live = live_next;
-      my_src = src_next;
-      issue_gather();       // in flight while the azimuth phases are computed
       load_pairs(next);
-      asm volatile("cp.async.wait_all;" ::: "memory");
-      __syncwarp();
-      fold();
+      issue_gather();
     }
     item = next;
   }
@@ -548,11 +538,8 @@ void upload_translate64_schedule(int order) {
 
 // the 64-pair kernel holds one operand tile per CTA: two CTAs per SM up to P = 12
 bool translate64_supported(int order) {
-  static const bool off = [] {
-    const char* e = getenv("HFMM_TRANSLATE");
-    return e && !strcmp(e, "32");
-  }();
-  if (off || order > kTranslate64MaxOrder) return false;
+  const char* e = getenv("HFMM_TRANSLATE");
+  if ((e && !strcmp(e, "32")) || order > kTranslate64MaxOrder) return false;
   return 2 * (plan64(order).bytes + 1024) <= size_t(227) * 1024;
 }
 

@@ -383,6 +383,27 @@ def test_complex_wavenumber(oracle, k):
         assert rel_l2(y, f.matvec(q)) < 1e-5
 
 
+@pytest.mark.parametrize("order", [0, 1, 3, 7, 12])
+def test_64_pair_translation_kernel_against_the_32_pair_kernel(oracle, monkeypatch, order):
+    """orders <= 12 run the 64-pair in-place kernel (kernels_translate64.cu); HFMM_TRANSLATE=32 forces the
+    32-pair ping-pong kernel on the same lists: same operator, two work layouts"""
+    n, k = 12000, 5.0
+    xyz, q = plummer_points(n, 43), charges(n, 43)
+    res = {}
+    for kernel in ("64", "32"):
+        monkeypatch.setenv("HFMM_TRANSLATE", kernel)
+        op = HfmmCuda(k=k, order=order, ncrit=32)
+        op.set_points(xyz)
+        res[kernel] = op.matvec(q)
+        if kernel == "64":
+            pairs, batches = op.stats()["m2l_pairs"], op.stats()["m2l_batches"]
+            assert pairs > 0 and batches * 32 < 2 * pairs + 64 * 2000   # 64-pair batches
+    assert rel_l2(res["64"], res["32"]) < 2e-6
+    if order >= 7:
+        tg = np.arange(0, n, 23)
+        assert rel_l2(res["64"][tg], oracle.direct_sum(xyz, q, k, tg)) < (1e-3 if order == 7 else 2e-6)
+
+
 @pytest.mark.parametrize("order", [6, 13])
 def test_both_batch_layouts_of_the_translation_kernel(oracle, monkeypatch, order):
     """batches cut per table group (per-pair azimuth phases) and per shift class (per-class phases) are two
@@ -391,6 +412,7 @@ def test_both_batch_layouts_of_the_translation_kernel(oracle, monkeypatch, order
     n, k = 9000, 5.0
     xyz, q = plummer_points(n, 41), charges(n, 41)
     res, batches = {}, {}
+    monkeypatch.setenv("HFMM_TRANSLATE", "32")     # the 64-pair kernel always batches per table group
     for layout in ("group", "class"):
         monkeypatch.setenv("HFMM_BATCHING", layout)
         op = HfmmCuda(k=k, order=order, ncrit=32)
