@@ -68,8 +68,12 @@ struct TraversalConfig {
   int c = 128;
   double theta = 0.5;
   double kd_max = 1.0;
-  bool deterministic = true;  // -> HFMM_FLAG_DETERMINISTIC: ordered accumulation, bitwise reproducible
-                              //    (+22 % per matvec); false: floating-point atomics in M2M / M2L
+  // -> HFMM_FLAG_DETERMINISTIC.  The default follows the REFERENCE (traversal.hpp:17: results repeat bit
+  // for bit, test_fmm.cpp:1024-1050) and costs ~+22 % per matvec and up to HFMM_ORDERED_STAGING_MB of device
+  // memory; every throughput number this repository publishes (bench.py) is measured with
+  // deterministic = false (floating-point atomics in M2M / M2L, results equal to ~1e-7), and bench.py
+  // reports the deterministic step beside it (`deterministic_ms_per_step`).  Set it to false for speed.
+  bool deterministic = true;
   int threads = 0;            // accepted for source compatibility (host threads of the table builder)
 };
 
@@ -115,7 +119,13 @@ class DeviceTree {
     if (int rc = hfmm_cuda_create(&h_, &c)) detail::raise(rc, hfmm_cuda_last_error(nullptr));
     n_ = points.size();
     static_assert(sizeof(Vec3) == 3 * sizeof(double), "Vec3 must be three packed doubles");
-    check(hfmm_cuda_set_points(h_, reinterpret_cast<const double*>(points.data()), n_));
+    try {
+      check(hfmm_cuda_set_points(h_, reinterpret_cast<const double*>(points.data()), n_));
+    } catch (...) {  // a throwing constructor runs no destructor: release the handle here
+      hfmm_cuda_destroy(h_);
+      h_ = nullptr;
+      throw;
+    }
   }
   DeviceTree(const DeviceTree&) = delete;
   DeviceTree& operator=(const DeviceTree&) = delete;
@@ -133,6 +143,7 @@ class DeviceTree {
     FmmStats f;
     f.m2l_pairs = s.m2l_pairs;
     f.p2p_pairs = s.p2p_pairs;
+    f.tasks = s.tasks;
     f.starved_cells = s.starved_cells;
     f.upward_seconds = s.upward_seconds;
     f.interaction_seconds = s.interaction_seconds;
@@ -192,6 +203,13 @@ struct SolveReport {
   std::vector<double> matvec_seconds;
 };
 using MatVec = std::function<std::vector<cplx>(const std::vector<cplx>&)>;
+// include/hfmm/solver.hpp:19-24
+struct IncidentWave {
+  Vec3 direction{0, 0, 1};  // must be unit length
+  cplx amplitude{1.0, 0.0};
+  WaveNumber k;             // informational here: the operator's own wavenumber is used
+  double sound_speed = 343.0;
+};
 
 // The tree path of a DiscreteSystem (solver.hpp:44-81) on the device: the FMM operator plus the
 // sparse corrections and block-Jacobi factors of build_system (solver.cpp:80-230): either the
@@ -224,12 +242,26 @@ class DeviceOperator {
     tree_.check(hfmm_cuda_build_corrections(tree_.handle(), &rules, &nnz));
     return nnz;
   }
+  // CurvilinearPatch::diameter() of every patch: enables evaluate_scattered_field's singular_error when an
+  // observation comes within 0.1 x diameter of a sample (solver.cpp:399-413); build_corrections sets them itself
+  void set_patch_diameters(const std::vector<double>& diameter) {
+    tree_.check(hfmm_cuda_set_patch_diameters(tree_.handle(), diameter.data(), diameter.size()));
+  }
   std::size_t size() const { return tree_.size(); }
   fmm::DeviceTree& tree() { return tree_; }
 
  private:
   fmm::DeviceTree tree_;
 };
+
+// assemble_rhs (solver.hpp, solver.cpp:302-312): A exp(i k d.x) at the samples; config_error unless |d| = 1
+inline std::vector<cplx> assemble_rhs(DeviceOperator& sys, const IncidentWave& wave) {
+  const double d[3] = {wave.direction.x, wave.direction.y, wave.direction.z};
+  const double a[2] = {wave.amplitude.real(), wave.amplitude.imag()};
+  std::vector<cplx> rhs(sys.size());
+  sys.tree().check(hfmm_cuda_assemble_rhs(sys.tree().handle(), d, a, reinterpret_cast<double*>(rhs.data())));
+  return rhs;
+}
 
 // apply_operator (solver.hpp:95): length check -> config_error (solver.cpp:315-316)
 inline std::vector<cplx> apply_operator(DeviceOperator& sys, const std::vector<cplx>& x) {
@@ -252,6 +284,10 @@ inline std::pair<std::vector<cplx>, SolveReport> gmres_solve(DeviceOperator& sys
   hfmm_gmres_report r{};
   std::vector<cplx> x(rhs.size());
   std::vector<double> res(std::size_t(cfg.max_iterations > 0 ? cfg.max_iterations : 0) + 1);
+  std::vector<double> sec(res.size()), mv(res.size());
+  r.seconds_history = sec.data();
+  r.matvec_seconds_history = mv.data();
+  r.history_cap = int(res.size());
   sys.tree().check(hfmm_cuda_gmres(sys.tree().handle(), reinterpret_cast<const double*>(rhs.data()),
                                    reinterpret_cast<double*>(x.data()), &c, &r, res.data(), int(res.size())));
   SolveReport rep;
@@ -261,9 +297,11 @@ inline std::pair<std::vector<cplx>, SolveReport> gmres_solve(DeviceOperator& sys
   rep.rhs_norm = r.rhs_norm;
   rep.final_residual = r.final_residual;
   res.resize(std::size_t(r.iterations));
+  sec.resize(std::size_t(r.iterations));
+  mv.resize(std::size_t(r.iterations));
   rep.residuals = std::move(res);
-  rep.matvec_seconds.assign(1, r.matvec_seconds);
-  rep.seconds.assign(1, r.seconds);
+  rep.seconds = std::move(sec);            // per iteration, wall clock since the start of the solve
+  rep.matvec_seconds = std::move(mv);      // per iteration, operator time
   return {std::move(x), std::move(rep)};
 }
 

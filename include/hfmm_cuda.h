@@ -55,7 +55,11 @@ enum {
    * over the staged rows (cfg 2: +22 % per matvec) and up to HFMM_ORDERED_STAGING_MB (environment,
    * default 4096) MiB of device memory.  The near field, the leaf passes and the Krylov reductions
    * are ordered in every mode. */
-  HFMM_FLAG_DETERMINISTIC = 1 << 3
+  HFMM_FLAG_DETERMINISTIC = 1 << 3,
+  /* never switch to the host builder: when the device builder meets one of its limits (see
+   * HFMM_FLAG_HOST_TREE) set_points fails with the builder's status instead.  hfmm_cuda_stats::
+   * host_tree_used tells which builder produced the current tree either way. */
+  HFMM_FLAG_NO_HOST_FALLBACK = 1 << 4
 };
 
 /* POD mirror of WaveNumber (common.hpp:37-40), TraversalConfig (traversal.hpp:11-18) and the
@@ -93,6 +97,8 @@ typedef struct {
   uint64_t p2p_mode;           /* near-field kernel variant: 0 three MUFU per pair (any R'), 1..3 bounded
                                   R' with sin(R')/R' (and cos) as polynomials on the FMA pipe            */
   double near_r2_max;          /* bound on (k_r |x_i - x_j|)^2 over the near lists (selects p2p_mode)  */
+  uint64_t tasks;              /* FmmStats::tasks: walk nodes where the body count first drops to the grain s
+                                  (traversal.cpp:56-59)                                                 */
 } hfmm_cuda_stats;
 
 typedef struct hfmm_cuda hfmm_cuda_t;
@@ -147,6 +153,12 @@ typedef struct {
   double final_residual;
   double seconds;
   double matvec_seconds;
+  /* SolveReport::seconds / matvec_seconds (solver.hpp:106-116): optional caller buffers of history_cap
+   * doubles, one entry per iteration — wall clock since the start of the solve, and the operator time
+   * of that iteration (gmres.cpp:65-71,144).  Inputs; leave null / 0 when not wanted. */
+  double* seconds_history;
+  double* matvec_seconds_history;
+  int history_cap;
 } hfmm_gmres_report;
 
 /* gmres / gmres_solve (gmres.cpp:35-174, solver.cpp:361-391) with device-resident Krylov vectors.
@@ -155,10 +167,23 @@ typedef struct {
 int hfmm_cuda_gmres(hfmm_cuda_t* h, const double* rhs, double* x, const hfmm_gmres_config* cfg,
                     hfmm_gmres_report* report, double* residuals, int residual_cap);
 
+/* assemble_rhs (solver.cpp:302-312): rhs[i] = amplitude * exp(i k d . x_i) over the points of
+ * set_points (caller order), k the handle's (complex) wavenumber; evaluated in FP64 on the device.
+ * direction: 3 doubles, unit length (config_error beyond 1e-9, as the reference); amplitude: (re, im);
+ * out: n interleaved complex doubles (host). */
+int hfmm_cuda_assemble_rhs(hfmm_cuda_t* h, const double* direction, const double* amplitude, double* out);
+
 /* evaluate_scattered_field (solver.cpp:393-419): plain single-layer sum at exterior points.
- * coeff: n complex (caller order, multiplied by far_weight inside); obs: nobs x 3; out: nobs complex */
+ * coeff: n complex (caller order, multiplied by far_weight inside); obs: nobs x 3; out: nobs complex.
+ * Distances are formed in FP64 from the FP64 points.  When the patch diameters are known — after
+ * hfmm_cuda_build_corrections, or hfmm_cuda_set_patch_diameters — an observation within 0.1 x patch
+ * diameter of a sample fails with HFMM_ERR_SINGULAR like the reference (solver.cpp:399-413); without
+ * them only coincident points are skipped (there is no geometry to test against). */
 int hfmm_cuda_evaluate_field(hfmm_cuda_t* h, const double* coeff, const double* obs, size_t nobs,
                              double* out);
+/* CurvilinearPatch::diameter() of every patch (n / ni of them, ni from set_corrections), for the
+ * singular test of hfmm_cuda_evaluate_field when the corrections came through set_corrections */
+int hfmm_cuda_set_patch_diameters(hfmm_cuda_t* h, const double* diameter, size_t n_patches);
 
 /* Fills the statistics of the tree/lists and the per-kernel device times of the LAST matvec (CUDA
  * events recorded on the streams the kernels ran on; this call synchronises the handle). */
@@ -273,9 +298,12 @@ int hfmm_cuda_get_corrections(hfmm_cuda_t* h, double* patch_block, double* block
  * reduced scalars. */
 typedef struct {
   void* user;
-  void (*allreduce_sum)(void* user, double* values, int count);  /* host doubles, in place      */
-  void (*gather_vector)(void* user, void* full_dev);             /* n float2, Morton order       */
-  void (*gather_multipoles)(void* user);                         /* rows of hfmm_cuda_partition  */
+  /* every callback returns 0 on success; any other value aborts the solve at once with
+   * HFMM_ERR_DEVICE (the ranks of a real communicator fail together: a collective that failed on one
+   * rank failed on all of them) */
+  int (*allreduce_sum)(void* user, double* values, int count);  /* host doubles, in place      */
+  int (*gather_vector)(void* user, void* full_dev);             /* n float2, Morton order       */
+  int (*gather_multipoles)(void* user);                         /* rows of hfmm_cuda_partition  */
 } hfmm_dist_callbacks;
 /* rhs_owned / x_owned: body_count interleaved complex doubles, Morton order (host) */
 int hfmm_cuda_dist_gmres(hfmm_cuda_t* h, const double* rhs_owned, double* x_owned,

@@ -181,6 +181,9 @@ void ref_fmm_counts(const RefFmm* h, long long* c) {
   c[8] = mm;
   c[9] = mx;
 }
+// TraversalPlan::tasks (traversal.cpp:56-59) and FmmStats::starved_cells of the last execute_plan
+long long ref_fmm_tasks(const RefFmm* h) { return (long long)h->plan.tasks; }
+long long ref_fmm_starved(const RefFmm* h) { return (long long)h->stats.starved_cells; }
 // per cell: level, ix, iy, iz, body_first, body_count, child_first, child_count (8 x u32)
 void ref_fmm_cells(const RefFmm* h, unsigned* out) {
   for (size_t i = 0; i < h->tree.cells.size(); ++i) {

@@ -15,6 +15,7 @@ HFMM_FLAG_HOST_TREE = 1 << 0
 HFMM_FLAG_PHASE_TIMERS = 1 << 1
 HFMM_FLAG_NEAR_FIRST = 1 << 2
 HFMM_FLAG_DETERMINISTIC = 1 << 3
+HFMM_FLAG_NO_HOST_FALLBACK = 1 << 4
 
 _STATUS = {1: "config_error", 2: "singular_error", 3: "structural_error", 4: "accuracy_error",
            5: "domain_error", 6: "device_error", 9: "internal_error"}
@@ -44,7 +45,8 @@ class Stats(C.Structure):
                  "p2p_seconds", "m2l_seconds", "p2m_seconds", "m2m_seconds", "l2l_seconds",
                  "l2p_seconds", "matvec_seconds")] + \
                [("kernel_launches", C.c_uint64), ("device_bytes", C.c_uint64), ("m2l_batches", C.c_uint64),
-                ("host_tree_used", C.c_uint64), ("p2p_mode", C.c_uint64), ("near_r2_max", C.c_double)]
+                ("host_tree_used", C.c_uint64), ("p2p_mode", C.c_uint64), ("near_r2_max", C.c_double),
+                ("tasks", C.c_uint64)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -68,7 +70,8 @@ class _GmresConfig(C.Structure):
 class _GmresReport(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("breakdown", C.c_int),
                 ("rhs_norm", C.c_double), ("final_residual", C.c_double), ("seconds", C.c_double),
-                ("matvec_seconds", C.c_double)]
+                ("matvec_seconds", C.c_double), ("seconds_history", C.c_void_p),
+                ("matvec_seconds_history", C.c_void_p), ("history_cap", C.c_int)]
 
 
 class CorrectionRules(C.Structure):
@@ -96,9 +99,9 @@ def make_correction_rules(patches, tables, mode=2, near_patch_distance=-1.0):
     return r, keep
 
 
-ALLREDUCE_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_double), C.c_int)
-GATHER_VECTOR_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
-GATHER_MULTIPOLES_FN = C.CFUNCTYPE(None, C.c_void_p)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int)
+GATHER_VECTOR_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p)
+GATHER_MULTIPOLES_FN = C.CFUNCTYPE(C.c_int, C.c_void_p)
 
 
 class _DistCallbacks(C.Structure):
@@ -291,19 +294,42 @@ class HfmmCuda:
             ptr(near_offset, np.uint32), ptr(near_source, np.uint32), ptr(near_delta, np.complex128),
             ptr(block_lu, np.complex128), ptr(block_piv, np.int32)))
 
+    @staticmethod
+    def _report(rep, res, sec, mv):
+        it = rep.iterations
+        return dict(iterations=it, converged=bool(rep.converged), breakdown=bool(rep.breakdown),
+                    rhs_norm=rep.rhs_norm, final_residual=rep.final_residual, seconds=rep.seconds,
+                    matvec_seconds=rep.matvec_seconds, residuals=res[:it].copy(),
+                    seconds_history=sec[:it].copy(), matvec_seconds_history=mv[:it].copy())
+
     def gmres(self, rhs, rtol=1e-4, restart=30, max_iterations=500, precondition=True):
         rhs = _c128(rhs)
+        if rhs.shape != (self.n,):
+            raise ValueError("right-hand side length mismatch")
         x = np.zeros(self.n, dtype=np.complex128)
         cfg = _GmresConfig(rtol, restart, max_iterations, int(precondition))
-        rep = _GmresReport()
-        res = np.zeros(max_iterations + 1)
+        cap = max(int(max_iterations), 0) + 1
+        res, sec, mv = np.zeros(cap), np.zeros(cap), np.zeros(cap)
+        rep = _GmresReport(seconds_history=sec.ctypes.data, matvec_seconds_history=mv.ctypes.data, history_cap=cap)
         self._check(self.lib.hfmm_cuda_gmres(self.h, rhs.ctypes.data_as(_dp), x.ctypes.data_as(_dp),
                                              C.byref(cfg), C.byref(rep), res.ctypes.data_as(_dp),
                                              len(res)))
-        return x, dict(iterations=rep.iterations, converged=bool(rep.converged),
-                       breakdown=bool(rep.breakdown), rhs_norm=rep.rhs_norm,
-                       final_residual=rep.final_residual, seconds=rep.seconds,
-                       matvec_seconds=rep.matvec_seconds, residuals=res[:rep.iterations].copy())
+        return x, self._report(rep, res, sec, mv)
+
+    def assemble_rhs(self, direction=(0.0, 0.0, 1.0), amplitude=1.0):
+        """plane-wave right-hand side A exp(i k d.x) over the points of set_points (reference assemble_rhs)"""
+        d = np.ascontiguousarray(direction, dtype=np.float64)
+        if d.shape != (3,):
+            raise ValueError("direction must have three components")
+        a = np.array([np.real(amplitude), np.imag(amplitude)], dtype=np.float64)
+        out = np.zeros(self.n, dtype=np.complex128)
+        self._check(self.lib.hfmm_cuda_assemble_rhs(self.h, d.ctypes.data_as(_dp), a.ctypes.data_as(_dp),
+                                                    out.ctypes.data_as(_dp)))
+        return out
+
+    def set_patch_diameters(self, diameters):
+        d = np.ascontiguousarray(diameters, dtype=np.float64)
+        self._check(self.lib.hfmm_cuda_set_patch_diameters(self.h, d.ctypes.data_as(_dp), C.c_size_t(d.shape[0])))
 
     def dist_gmres(self, rhs_owned, allreduce_sum, gather_vector, gather_multipoles, rtol=1e-4,
                    restart=30, max_iterations=500, precondition=True):
@@ -312,20 +338,25 @@ class HfmmCuda:
         all-gathers the n-float2 Morton vector at dev_ptr; gather_multipoles() exchanges the owned
         multipole rows.  Exceptions raised inside a callback abort the solve."""
         rhs = _c128(rhs_owned)
+        if rhs.shape != (int(self.partition().body_count),):
+            raise ValueError("rhs_owned must hold exactly the owned Morton slice")
         x = np.zeros(rhs.shape[0], dtype=np.complex128)
         cfg = _GmresConfig(rtol, restart, max_iterations, int(precondition))
-        rep = _GmresReport()
-        res = np.zeros(max_iterations + 1)
+        cap = max(int(max_iterations), 0) + 1
+        res, sec, mv = np.zeros(cap), np.zeros(cap), np.zeros(cap)
+        rep = _GmresReport(seconds_history=sec.ctypes.data, matvec_seconds_history=mv.ctypes.data, history_cap=cap)
         failure = []
 
         def guard(fn):
-            def run(*args):
+            def run(*args):     # status for the library: non-zero aborts the solve at once
                 if failure:
-                    return
+                    return 1
                 try:
                     fn(*args)
+                    return 0
                 except BaseException as e:  # a callback must not unwind through C
                     failure.append(e)
+                    return 1
             return run
 
         cb = _DistCallbacks(
@@ -339,10 +370,7 @@ class HfmmCuda:
         if failure:
             raise failure[0]
         self._check(rc)
-        return x, dict(iterations=rep.iterations, converged=bool(rep.converged),
-                       breakdown=bool(rep.breakdown), rhs_norm=rep.rhs_norm,
-                       final_residual=rep.final_residual, seconds=rep.seconds,
-                       matvec_seconds=rep.matvec_seconds, residuals=res[:rep.iterations].copy())
+        return x, self._report(rep, res, sec, mv)
 
     def build_corrections(self, patches, tables, mode=2, near_patch_distance=-1.0, fetch=True):
         """Correction arrays built on the device from the patches and the reference's rule tables
@@ -368,6 +396,8 @@ class HfmmCuda:
     def evaluate_field(self, coeff, obs):
         coeff = _c128(coeff)
         obs = np.ascontiguousarray(obs, dtype=np.float64)
+        if coeff.shape != (self.n,) or obs.ndim != 2 or obs.shape[1] != 3:
+            raise ValueError("coeff must have one entry per unknown and obs must be (nobs, 3)")
         out = np.zeros(obs.shape[0], dtype=np.complex128)
         self._check(self.lib.hfmm_cuda_evaluate_field(self.h, coeff.ctypes.data_as(_dp),
                                                       obs.ctypes.data_as(_dp),

@@ -17,8 +17,9 @@ struct hfmm_cuda {
 
 namespace {
 thread_local std::string g_create_error;
-
-std::string g_stale_error;
+// leftover CUDA error name of other CUDA users on this host thread (diagnosis only); thread-local like
+// the CUDA error state it mirrors: handles may be driven from different host threads
+thread_local std::string g_stale_error;
 
 template <typename Fn>
 int guarded(hfmm_cuda* h, Fn&& fn) {
@@ -29,7 +30,8 @@ int guarded(hfmm_cuda* h, Fn&& fn) {
     // below report this call's errors only; the leftover stays readable for diagnosis
     if (const char* stale = Engine::take_stale_cuda_error()) g_stale_error = stale;
     // buffers created or dropped inside the call are ordered on the handle's stream (device_utils.cuh)
-    hfmm_b200::AllocStreamScope scope((h && h->engine) ? h->engine->stream() : nullptr);
+    hfmm_b200::AllocStreamScope scope((h && h->engine) ? h->engine->stream() : nullptr,
+                                      (h && h->engine) ? h->engine->device() : -1);
     fn();
     return HFMM_OK;
   } catch (const Error& e) {
@@ -185,6 +187,19 @@ int hfmm_cuda_evaluate_field(hfmm_cuda_t* h, const double* coeff, const double* 
     if (!coeff || (!obs && nobs) || (!out && nobs)) throw Error(HFMM_ERR_CONFIG, "null argument");
     h->engine->evaluate_field(coeff, obs, nobs, out);
   });
+}
+
+int hfmm_cuda_assemble_rhs(hfmm_cuda_t* h, const double* direction, const double* amplitude, double* out) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] {
+    if (!direction || !amplitude || !out) throw Error(HFMM_ERR_CONFIG, "null argument");
+    h->engine->assemble_rhs(direction, amplitude, out);
+  });
+}
+
+int hfmm_cuda_set_patch_diameters(hfmm_cuda_t* h, const double* diameter, size_t n_patches) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] { h->engine->set_patch_diameters(diameter, n_patches); });
 }
 
 int hfmm_cuda_set_partition(hfmm_cuda_t* h, int rank, int nranks) {

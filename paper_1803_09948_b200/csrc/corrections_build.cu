@@ -78,7 +78,8 @@ __device__ __forceinline__ uint64_t cell_key(long long cx, long long cy, long lo
 // K1: geometry.cpp:9-20 (diameter), solver.cpp:40-43 (threshold), solver.cpp:283-294 (samples)
 __global__ void patch_geometry_kernel(const double* __restrict__ nodes, const double* __restrict__ sample_ref,
                                       int ni, uint64_t n_patches, double near_patch_distance,
-                                      double* __restrict__ thr, double* __restrict__ xyz) {
+                                      double* __restrict__ thr, double* __restrict__ touch2,
+                                      double* __restrict__ xyz) {
   const uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (p >= n_patches) return;
   const double* node = nodes + 18 * p;
@@ -97,6 +98,7 @@ __global__ void patch_geometry_kernel(const double* __restrict__ nodes, const do
     r = fmax(r, sqrt(dx * dx + dy * dy + dz * dz));
   }
   thr[p] = near_patch_distance < 0 ? 2.0 * (2.0 * r) : near_patch_distance;
+  touch2[p] = (0.1 * (2.0 * r)) * (0.1 * (2.0 * r));  // evaluate_scattered_field's touch radius (solver.cpp:399-403)
   for (int j = 0; j < ni; ++j) {
     const D3 v = map_to_physical(node, sample_ref[2 * j], sample_ref[2 * j + 1]);
     xyz[3 * (p * ni + j)] = v.x;
@@ -348,9 +350,11 @@ void Engine::build_corrections(const hfmm_correction_rules& r, uint64_t* nnz_out
   // K1
   store->xyz.resize(n * 3);
   store->thr.resize(std::max<uint64_t>(r.n_patches, 1));
+  touch2_.resize(std::max<uint64_t>(r.n_patches, 1));
+  touch_ni_ = uint32_t(ni);
   patch_geometry_kernel<<<blocks_for(r.n_patches, 128), 128, 0, s>>>(d_nodes.get(), d_ref.get(), ni, r.n_patches,
                                                                       r.near_patch_distance, store->thr.get(),
-                                                                      store->xyz.get());
+                                                                      touch2_.get(), store->xyz.get());
   HFMM_CUDA_CHECK(cudaGetLastError());
   {  // the samples must be the points the tree was built on (caller order; body_abs_ holds k x in FP32)
     DeviceBuffer<double> d_diff(1);

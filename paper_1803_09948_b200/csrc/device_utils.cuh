@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstddef>
 #include <string>
 #include <vector>
@@ -19,8 +20,9 @@ namespace hfmm_b200 {
                                                     cudaGetErrorString(err__));            \
   } while (0)
 
-// bytes currently held through DeviceBuffer on this process (reported in hfmm_cuda_stats)
-size_t& device_bytes_counter();
+// bytes currently held through DeviceBuffer by all handles of this process (hfmm_cuda_stats::device_bytes);
+// atomic: handles may be driven from different host threads
+std::atomic<size_t>& device_bytes_counter();
 
 // Stream-ordered allocation.  Inside a library call the calling thread carries the handle's stream
 // (AllocStreamScope, set by the C API wrapper): buffers then come from the device's memory pool with
@@ -30,17 +32,27 @@ size_t& device_bytes_counter();
 // cudaMalloc / cudaFree).  All work that touches a buffer is ordered on the handle's stream (the
 // near-field stream joins it at the end of every matvec), so freeing in that stream's order is
 // safe.  Outside a scope (handle construction and destruction) the synchronous calls are used;
-// cudaFree accepts pool allocations.  The pool keeps freed memory while a handle is alive and is
-// trimmed when the last one goes (configure_memory_pool / trim_memory_pool).
+// cudaFree accepts pool allocations.  The pool is the LIBRARY'S OWN (one cudaMemPool per device, created
+// on first use): the device's default pool belongs to the host application (torch's cudaMallocAsync
+// backend, for one) and is neither reconfigured nor trimmed here.  It keeps freed memory while a handle
+// is alive and is trimmed when the last one goes (library_memory_pool / trim_memory_pool).
 cudaStream_t& alloc_stream();
+cudaMemPool_t& alloc_pool();
+cudaMemPool_t library_memory_pool(int device);
 struct AllocStreamScope {
   cudaStream_t prev;
-  explicit AllocStreamScope(cudaStream_t s) : prev(alloc_stream()) { alloc_stream() = s; }
-  ~AllocStreamScope() { alloc_stream() = prev; }
+  cudaMemPool_t prev_pool;
+  explicit AllocStreamScope(cudaStream_t s, int device = -1) : prev(alloc_stream()), prev_pool(alloc_pool()) {
+    alloc_stream() = s;
+    alloc_pool() = (s && device >= 0) ? library_memory_pool(device) : nullptr;
+  }
+  ~AllocStreamScope() {
+    alloc_stream() = prev;
+    alloc_pool() = prev_pool;
+  }
   AllocStreamScope(const AllocStreamScope&) = delete;
   AllocStreamScope& operator=(const AllocStreamScope&) = delete;
 };
-void configure_memory_pool(int device);
 void trim_memory_pool(int device);
 
 template <typename T>
@@ -67,7 +79,10 @@ class DeviceBuffer {
     if (n == n_) return;
     release();
     if (n) {
-      if (cudaStream_t s = alloc_stream())
+      cudaStream_t s = alloc_stream();
+      if (s && alloc_pool())
+        HFMM_CUDA_CHECK(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&ptr_), n * sizeof(T), alloc_pool(), s));
+      else if (s)
         HFMM_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&ptr_), n * sizeof(T), s));
       else
         HFMM_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&ptr_), n * sizeof(T)));

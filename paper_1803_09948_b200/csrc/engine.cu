@@ -10,6 +10,7 @@
 #include <cmath>
 #include <complex>
 #include <map>
+#include <mutex>
 #include <numeric>
 #include <thread>
 #include <unordered_map>
@@ -28,28 +29,53 @@ namespace {
 std::atomic<int> g_live_engines{0};
 }
 
-void configure_memory_pool(int device) {
+cudaMemPool_t& alloc_pool() {
+  thread_local cudaMemPool_t p = nullptr;
+  return p;
+}
+
+namespace {
+std::mutex g_pool_mutex;
+std::map<int, cudaMemPool_t> g_pools;
+}  // namespace
+
+// the library's private stream-ordered pool of `device` (null if pools are unavailable: the buffers
+// then come from the device's default pool)
+cudaMemPool_t library_memory_pool(int device) {
+  std::lock_guard<std::mutex> lock(g_pool_mutex);
+  auto it = g_pools.find(device);
+  if (it != g_pools.end()) return it->second;
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.handleTypes = cudaMemHandleTypeNone;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = device;
   cudaMemPool_t pool = nullptr;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) {
+  if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
     (void)cudaGetLastError();
-    return;
+    pool = nullptr;
+  } else {
+    uint64_t keep = ~uint64_t(0);  // freed buffers stay in the pool while a handle lives
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
   }
-  uint64_t keep = ~uint64_t(0);  // freed buffers stay in the pool while a handle lives
-  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  g_pools[device] = pool;
+  return pool;
 }
 
 void trim_memory_pool(int device) {
   cudaMemPool_t pool = nullptr;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) {
-    (void)cudaGetLastError();
-    return;
+  {
+    std::lock_guard<std::mutex> lock(g_pool_mutex);
+    auto it = g_pools.find(device);
+    if (it != g_pools.end()) pool = it->second;
   }
+  if (!pool) return;
   cudaDeviceSynchronize();
   cudaMemPoolTrimTo(pool, 0);
 }
 
-size_t& device_bytes_counter() {
-  static size_t bytes = 0;
+std::atomic<size_t>& device_bytes_counter() {
+  static std::atomic<size_t> bytes{0};
   return bytes;
 }
 
@@ -166,27 +192,46 @@ Engine::Engine(const hfmm_cuda_config& cfg) : cfg_(cfg) {
     throw Error(HFMM_ERR_DEVICE, "no CUDA device available (this library has no CPU fallback)");
   if (cfg.device < 0 || cfg.device >= ndev) throw Error(HFMM_ERR_CONFIG, "device ordinal out of range");
   HFMM_CUDA_CHECK(cudaSetDevice(cfg.device));
-  // the far-field stream outranks the near-field stream: when both have blocks waiting, freed SM
-  // resources go to the (few, persistent) M2L CTAs first and the near field fills what is left
-  int prio_lo = 0, prio_hi = 0;
-  HFMM_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-  HFMM_CUDA_CHECK(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, prio_hi));
-  HFMM_CUDA_CHECK(cudaStreamCreateWithPriority(&stream_near_, cudaStreamNonBlocking, prio_lo));
-  configure_memory_pool(cfg_.device);
-  ++g_live_engines;
-  HFMM_CUDA_CHECK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
-  HFMM_CUDA_CHECK(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
-  ev_.resize(14);
-  for (auto& e : ev_) HFMM_CUDA_CHECK(cudaEventCreate(&e));
-  user_ev_.resize(16);
-  for (auto& e : user_ev_) HFMM_CUDA_CHECK(cudaEventCreate(&e));
+  try {
+    // the far-field stream outranks the near-field stream: when both have blocks waiting, freed SM
+    // resources go to the (few, persistent) M2L CTAs first and the near field fills what is left
+    int prio_lo = 0, prio_hi = 0;
+    HFMM_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    HFMM_CUDA_CHECK(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, prio_hi));
+    HFMM_CUDA_CHECK(cudaStreamCreateWithPriority(&stream_near_, cudaStreamNonBlocking, prio_lo));
+    HFMM_CUDA_CHECK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+    HFMM_CUDA_CHECK(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    ev_.assign(14, nullptr);
+    for (auto& e : ev_) HFMM_CUDA_CHECK(cudaEventCreate(&e));
+    user_ev_.assign(16, nullptr);
+    for (auto& e : user_ev_) HFMM_CUDA_CHECK(cudaEventCreate(&e));
 
-  const int P = cfg.order;
-  const size_t tri = size_t(P + 1) * (P + 2) / 2;
-  std::vector<float> diag(P + 1), sub(P + 1), a(tri), b(tri);
-  build_legendre_coefficients(P, diag.data(), sub.data(), a.data(), b.data());
-  upload_legendre_constants(diag.data(), sub.data(), a.data(), b.data(), P);
-  upload_translate_schedule(P);
+    const int P = cfg.order;
+    const size_t tri = size_t(P + 1) * (P + 2) / 2;
+    std::vector<float> diag(P + 1), sub(P + 1), a(tri), b(tri);
+    build_legendre_coefficients(P, diag.data(), sub.data(), a.data(), b.data());
+    upload_legendre_constants(diag.data(), sub.data(), a.data(), b.data(), P);
+    upload_translate_schedule(P);
+  } catch (...) {
+    destroy_streams_and_events();  // a failed constructor runs no destructor: nothing may leak
+    throw;
+  }
+  ++g_live_engines;  // last: counted only when the handle exists
+}
+
+void Engine::destroy_streams_and_events() {
+  for (auto& e : ev_)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : user_ev_)
+    if (e) cudaEventDestroy(e);
+  ev_.clear();
+  user_ev_.clear();
+  if (ev_fork_) cudaEventDestroy(ev_fork_);
+  if (ev_join_) cudaEventDestroy(ev_join_);
+  if (stream_) cudaStreamDestroy(stream_);
+  if (stream_near_) cudaStreamDestroy(stream_near_);
+  ev_fork_ = ev_join_ = nullptr;
+  stream_ = stream_near_ = nullptr;
 }
 
 void Engine::release_device_state() { --g_live_engines; }
@@ -195,12 +240,7 @@ bool Engine::any_engine_alive() { return g_live_engines.load() > 0; }
 Engine::~Engine() {
   cudaSetDevice(cfg_.device);
   release_device_state();
-  for (auto& e : ev_) cudaEventDestroy(e);
-  for (auto& e : user_ev_) cudaEventDestroy(e);
-  if (ev_fork_) cudaEventDestroy(ev_fork_);
-  if (ev_join_) cudaEventDestroy(ev_join_);
-  if (stream_) cudaStreamDestroy(stream_);
-  if (stream_near_) cudaStreamDestroy(stream_near_);
+  destroy_streams_and_events();
 }
 
 const char* Engine::take_stale_cuda_error() {
@@ -210,6 +250,37 @@ const char* Engine::take_stale_cuda_error() {
 
 void Engine::require_points() const {
   if (!have_points_) throw Error(HFMM_ERR_CONFIG, "hfmm_cuda_set_points has not been called");
+}
+
+// compute_multipoles' truncation-waste scan (expansion.cpp:253-262): cells whose top radial factor
+// j_P(|k| radius) vanishes in FP64.  The radius depends on the level only; j_P is evaluated as the reference
+// does for small arguments (ascending series, special.cpp:17-34) — only there can it underflow to zero.
+uint64_t Engine::count_starved_cells() const {
+  const int P = cfg_.order;
+  if (P <= 0) return 0;
+  const double kmag = std::hypot(cfg_.wave_r, cfg_.wave_i);
+  uint64_t starved = 0;
+  for (int L = 0; L <= tree_.max_level; ++L) {
+    const uint64_t cells = tree_.level_offset[L + 1] - tree_.level_offset[L];
+    if (!cells) continue;
+    const double z = kmag * (tree_.side(L) * std::sqrt(3.0) / 2);
+    if (z >= 0.5) continue;  // Miller recurrence normalised by j_0: never exactly zero
+    const double z2h = 0.5 * z * z;
+    double zn = 1.0, dfact = 1.0, top = 0.0;
+    for (int n = 0; n <= P; ++n) {
+      double term = 1.0, sum = 1.0;
+      for (int k = 1; k < 40; ++k) {
+        term *= -z2h / double(k * (2 * n + 2 * k + 1));
+        sum += term;
+        if (std::abs(term) < 1e-18 * std::abs(sum)) break;
+      }
+      top = zn / dfact * sum;
+      zn *= z;
+      dfact *= double(2 * n + 3);
+    }
+    if (top == 0.0) starved += cells;
+  }
+  return starved;
 }
 
 // Classes that share the rotation table (polar angle) and the coaxial table (levels, distance) differ
@@ -638,9 +709,13 @@ void Engine::get_partition(hfmm_cuda_partition* out) {
       }
     out->cell_first[L] = f == 0xffffffffu ? t.level_offset[L] : f;
     out->cell_count[L] = f == 0xffffffffu ? 0 : l - f;
-    // ownership follows contiguous body ranges, so owned cells of a level are contiguous too
-    for (uint32_t c = out->cell_first[L]; c < out->cell_first[L] + out->cell_count[L]; ++c)
-      if (!owned_[c]) throw Error(HFMM_ERR_STRUCTURAL, "owned cells of a level are not contiguous");
+    // ownership follows contiguous body ranges, so the owned cells of a level at or below the
+    // partition cut are contiguous too.  Above the cut a level can interleave owned leaves with
+    // unowned interior cells (cell_rank -1: nobody translates into them); those levels are never
+    // exchanged (level_first is the coarsest translating level), so only the exchanged ones are checked
+    if (have_far_ && L >= lmin_src_)
+      for (uint32_t c = out->cell_first[L]; c < out->cell_first[L] + out->cell_count[L]; ++c)
+        if (!owned_[c]) throw Error(HFMM_ERR_STRUCTURAL, "owned cells of a level are not contiguous");
   }
 }
 
@@ -678,6 +753,7 @@ void Engine::set_points(const double* xyz, size_t n) {
   have_points_ = false;
   have_weight_ = have_block_ = have_near_ = have_lu_ = false;  // corrections belong to a point set
   release_correction_store();
+  touch2_.release();
   identity_.release();
   dev_pairs_ = DevicePairs{};
   pairs_ = PairLists{};
@@ -690,6 +766,7 @@ void Engine::set_points(const double* xyz, size_t n) {
     try {
       set_points_device(xyz, n);
     } catch (const DeviceBuilderLimit& lim) {
+      if (cfg_.flags & HFMM_FLAG_NO_HOST_FALLBACK) throw;  // the caller asked for the device builder or nothing
       // ... and lists beyond the device traversal's capacity (a gate that forbids every coarse
       // translation) are left to it for moderate sizes only: at a million points that configuration
       // is a mistake to report, not hours of host work to start
@@ -716,7 +793,7 @@ void Engine::set_points(const double* xyz, size_t n) {
   stats_.n_cells = tree_.n_cells();
   stats_.n_leaves = tree_.leaves.size();
   stats_.max_level = uint64_t(tree_.max_level);
-  stats_.starved_cells = 0;
+  stats_.starved_cells = count_starved_cells();
   stats_.setup_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   stats_.device_bytes = device_bytes_counter();
@@ -736,15 +813,16 @@ void Engine::set_points_device(const double* xyz, size_t n) {
     fprintf(stderr, "[hfmm setup] %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t_prev).count());
     t_prev = now;
   };
-  DeviceBuffer<double> d_xyz;
+  DeviceBuffer<double>& d_xyz = xyz64_;  // kept: FP64 points in caller order
   DeviceBuffer<uint32_t> d_index;
   build_tree_device(tree_, xyz, n, cfg_.ncrit, leaf_cap_, d_xyz, d_index, stream_);
   mark("tree");
   const TreeArrays& t = tree_;
   DeviceCells cells;
   cells.upload(t, stream_);
-  dual_tree_traversal_device(t, cells, std::hypot(cfg_.wave_r, cfg_.wave_i), cfg_.theta, cfg_.kd_max, dev_pairs_,
-                             stream_);  // the gate uses |k| (traversal.cpp:86)
+  dual_tree_traversal_device(t, cells, std::hypot(cfg_.wave_r, cfg_.wave_i), cfg_.theta, cfg_.kd_max, cfg_.grain,
+                             dev_pairs_, stream_);  // the gate uses |k| (traversal.cpp:86)
+  stats_.tasks = dev_pairs_.tasks;
   far_pair_level_range(dev_pairs_, cells, lmin_dst_, lmin_src_, stream_);
   mark("traversal");
   have_far_ = dev_pairs_.n_far > 0;
@@ -804,7 +882,10 @@ void Engine::set_points_device(const double* xyz, size_t n) {
 // ---- builder on the host (HFMM_FLAG_HOST_TREE): host_tree.cpp ---------------------------------
 void Engine::set_points_host(const double* xyz, size_t n) {
   build_tree_host(tree_, xyz, n, cfg_.ncrit, leaf_cap_, threads_);
-  dual_tree_traversal_host(tree_, std::hypot(cfg_.wave_r, cfg_.wave_i), cfg_.theta, cfg_.kd_max, pairs_, threads_);
+  xyz64_.upload(xyz, 3 * n, stream_);
+  dual_tree_traversal_host(tree_, std::hypot(cfg_.wave_r, cfg_.wave_i), cfg_.theta, cfg_.kd_max, pairs_, threads_,
+                           cfg_.grain);
+  stats_.tasks = pairs_.tasks;
   const TreeArrays& t = tree_;
   const size_t nc = t.n_cells();
   const double k = cfg_.wave_r;

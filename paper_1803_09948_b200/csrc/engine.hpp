@@ -76,6 +76,8 @@ class Engine {
   // clears and returns the name of a non-sticky CUDA error left behind on this host thread (or null)
   static const char* take_stale_cuda_error();
   void evaluate_field(const double* coeff, const double* obs, size_t nobs, double* out);
+  void assemble_rhs(const double* direction, const double* amplitude, double* out);
+  void set_patch_diameters(const double* diameter, size_t n_patches);
   // correction builders on the device (corrections_build.cu; reference solver.cpp:80-230)
   void build_corrections(const hfmm_correction_rules& rules, uint64_t* near_nnz);
   void get_corrections(double* patch_block, double* block_lu, int* block_piv, uint32_t* near_offset,
@@ -91,11 +93,13 @@ class Engine {
  private:
   void require_points() const;
   void release_device_state();
+  void destroy_streams_and_events();
   void run_far_and_near();  // body_q_ -> near_, far_
   void phase_upward();      // near field (own stream) + P2M + M2M
   void phase_downward();    // M2L + L2L + L2P, joins the near field
   void run_stage(const TranslateStage& st, const float2* src, float2* dst);
   void compute_partition();
+  uint64_t count_starved_cells() const;
   void collect_timings();
   void apply_operator_device(const float2* x, float2* y);  // caller order, weights + corrections
   const uint32_t* identity_index();
@@ -177,7 +181,10 @@ class Engine {
   DeviceBuffer<float2> patch_block_, near_delta_, block_lu_;
   DeviceBuffer<uint32_t> near_offset_, near_source_, identity_;
   DeviceBuffer<int> block_piv_;
-  DeviceBuffer<float4> body_abs_;  // k * x, caller order (exterior field evaluation)
+  DeviceBuffer<float4> body_abs_;  // k * x, caller order
+  DeviceBuffer<double> xyz64_;     // the points as given, FP64, caller order (rhs, exterior field)
+  DeviceBuffer<double> touch2_;    // (0.1 patch diameter)^2 per patch: singular test of evaluate_field
+  uint32_t touch_ni_ = 1;
   DeviceBuffer<float2> x32_, y32_;
   // vectors
   DeviceBuffer<float2> body_q_, near_, far_;

@@ -91,7 +91,13 @@ void Engine::gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cf
   const bool precond = cfg.precondition && have_lu_;
   const uint32_t npatch = ni_ ? n / uint32_t(ni_) : 0;
 
+  double* const sec_hist = rep->seconds_history;
+  double* const mv_hist = rep->matvec_seconds_history;
+  const int hist_cap = rep->history_cap;
   *rep = hfmm_gmres_report{};
+  rep->seconds_history = sec_hist;
+  rep->matvec_seconds_history = mv_hist;
+  rep->history_cap = hist_cap;
   double bnorm2 = 0;
   for (size_t i = 0; i < size_t(n) * 2; ++i) bnorm2 += rhs[i] * rhs[i];
   const double bnorm = std::sqrt(bnorm2);
@@ -130,7 +136,7 @@ void Engine::gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cf
 
   int iterations = 0, nres = 0;
   bool done = false, breakdown = false;
-  double last_est = -1, beta = bnorm;
+  double last_est = -1, beta = bnorm, matvec_prev = 0;
   while (!done) {
     if (beta <= target || iterations >= cfg.max_iterations) break;
     launch_scale(n, r32.get(), float(1.0 / beta), V.get(), stream_);
@@ -199,6 +205,11 @@ void Engine::gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cf
       cols = j + 1;
       last_est = std::abs(g[j + 1]);
       if (residuals && nres < residual_cap) residuals[nres] = last_est / bnorm;
+      if (nres < hist_cap) {  // SolveReport::seconds / matvec_seconds (gmres.cpp:65-71,144)
+        if (sec_hist) sec_hist[nres] = std::chrono::duration<double>(clk::now() - t_start).count();
+        if (mv_hist) mv_hist[nres] = matvec_s - matvec_prev;
+      }
+      matvec_prev = matvec_s;
       ++nres;
       if (broke) {
         breakdown = true;
@@ -275,8 +286,17 @@ void Engine::dist_gmres(const double* rhs, double* x_out, const hfmm_gmres_confi
   const uint32_t npatch = ni_ ? n / uint32_t(ni_) : 0;
   const size_t ml = std::max<uint32_t>(mloc, 1);
 
-  auto reduce = [&](double* v, int count) { cb.allreduce_sum(cb.user, v, count); };
+  // a callback that reports failure ends the solve at once: its peers failed in the same collective
+  auto reduce = [&](double* v, int count) {
+    if (cb.allreduce_sum(cb.user, v, count) != 0) throw Error(HFMM_ERR_DEVICE, "all-reduce callback failed");
+  };
+  double* const sec_hist = rep->seconds_history;
+  double* const mv_hist = rep->matvec_seconds_history;
+  const int hist_cap = rep->history_cap;
   *rep = hfmm_gmres_report{};
+  rep->seconds_history = sec_hist;
+  rep->matvec_seconds_history = mv_hist;
+  rep->history_cap = hist_cap;
   double b2[1] = {0};
   for (size_t i = 0; i < size_t(mloc) * 2; ++i) b2[0] += rhs[i] * rhs[i];
   reduce(b2, 1);
@@ -306,7 +326,7 @@ void Engine::dist_gmres(const double* rhs, double* x_out, const hfmm_gmres_confi
     HFMM_CUDA_CHECK(cudaMemcpyAsync(full.get() + first, in, size_t(mloc) * sizeof(float2),
                                     cudaMemcpyDeviceToDevice, stream_));
     HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
-    cb.gather_vector(cb.user, full.get());
+    if (cb.gather_vector(cb.user, full.get()) != 0) throw Error(HFMM_ERR_DEVICE, "vector gather callback failed");
     launch_scatter_potentials(full.get(), nullptr, body_index_.get(), nullptr, vc.get(), n, stream_);
     const float2* xc = vc.get();
     if (precond) {
@@ -318,7 +338,8 @@ void Engine::dist_gmres(const double* rhs, double* x_out, const hfmm_gmres_confi
     phase_upward();
     HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
     HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_near_));
-    if (have_far_) cb.gather_multipoles(cb.user);
+    if (have_far_ && cb.gather_multipoles(cb.user) != 0)
+      throw Error(HFMM_ERR_DEVICE, "multipole exchange callback failed");
     phase_downward();
     if (corr) {
       yc.zero(stream_);
@@ -348,7 +369,7 @@ void Engine::dist_gmres(const double* rhs, double* x_out, const hfmm_gmres_confi
   auto h = [&](int i, int j) -> cd& { return H[size_t(j) * (m + 1) + i]; };
   int iterations = 0, nres = 0;
   bool done = false, breakdown = false;
-  double last_est = -1, beta = bnorm, tmp[2];
+  double last_est = -1, beta = bnorm, tmp[2], matvec_prev = 0;
   while (!done) {
     if (beta <= target || iterations >= cfg.max_iterations) break;
     launch_scale(mloc, r32.get(), float(1.0 / beta), V.get(), stream_);
@@ -395,6 +416,11 @@ void Engine::dist_gmres(const double* rhs, double* x_out, const hfmm_gmres_confi
       cols = j + 1;
       last_est = std::abs(g[j + 1]);
       if (residuals && nres < residual_cap) residuals[nres] = last_est / bnorm;
+      if (nres < hist_cap) {
+        if (sec_hist) sec_hist[nres] = std::chrono::duration<double>(clk::now() - t_start).count();
+        if (mv_hist) mv_hist[nres] = matvec_s - matvec_prev;
+      }
+      matvec_prev = matvec_s;
       ++nres;
       if (broke) {
         breakdown = true;
@@ -443,7 +469,7 @@ void Engine::dist_gmres(const double* rhs, double* x_out, const hfmm_gmres_confi
     HFMM_CUDA_CHECK(cudaMemcpyAsync(full.get() + first, V.get(), size_t(mloc) * sizeof(float2),
                                     cudaMemcpyDeviceToDevice, stream_));
     HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
-    cb.gather_vector(cb.user, full.get());
+    if (cb.gather_vector(cb.user, full.get()) != 0) throw Error(HFMM_ERR_DEVICE, "vector gather callback failed");
     launch_scatter_potentials(full.get(), nullptr, body_index_.get(), nullptr, vc.get(), n, stream_);
     launch_precondition(npatch, ni_, block_lu_.get(), block_piv_.get(), vc.get(), pc.get(), stream_);
     launch_gather_charges(nullptr, pc.get(), body_index_.get(), nullptr, full.get(), n, stream_);
@@ -457,6 +483,33 @@ void Engine::dist_gmres(const double* rhs, double* x_out, const hfmm_gmres_confi
   rep->converged = (final_res <= cfg.rtol || (nres > 0 && last_est / bnorm <= cfg.rtol)) ? 1 : 0;
   rep->seconds = std::chrono::duration<double>(clk::now() - t_start).count();
   rep->matvec_seconds = matvec_s;
+}
+
+void Engine::set_patch_diameters(const double* diameter, size_t n_patches) {
+  require_points();
+  HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  if (!diameter || n_patches == 0 || tree_.n_bodies % n_patches != 0)
+    throw Error(HFMM_ERR_CONFIG, "the patch count must divide the number of unknowns");
+  std::vector<double> t2(n_patches);
+  for (size_t p = 0; p < n_patches; ++p) {
+    const double t = 0.1 * diameter[p];  // solver.cpp:399-403
+    t2[p] = t * t;
+  }
+  touch2_.upload(t2, stream_);
+  touch_ni_ = uint32_t(tree_.n_bodies / n_patches);
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+void Engine::assemble_rhs(const double* direction, const double* amplitude, double* out) {
+  require_points();
+  HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  const double n2 = direction[0] * direction[0] + direction[1] * direction[1] + direction[2] * direction[2];
+  if (!(std::abs(n2 - 1.0) <= 1e-9)) throw Error(HFMM_ERR_CONFIG, "incident direction must be unit length");
+  const uint32_t n = tree_.n_bodies;
+  if (io64_.size() != n) io64_.resize(n);
+  launch_assemble_rhs(n, xyz64_.get(), direction, cfg_.wave_r, cfg_.wave_i, amplitude, io64_.get(), stream_);
+  HFMM_CUDA_CHECK(cudaMemcpyAsync(out, io64_.get(), size_t(n) * sizeof(double2), cudaMemcpyDeviceToHost, stream_));
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
 }
 
 void Engine::evaluate_field(const double* coeff, const double* obs, size_t nobs, double* out) {
@@ -475,16 +528,21 @@ void Engine::evaluate_field(const double* coeff, const double* obs, size_t nobs,
     HFMM_CUDA_CHECK(cudaMemcpyAsync(body_q_.get(), cdev.get(), size_t(n) * sizeof(float2),
                                     cudaMemcpyDeviceToDevice, stream_));
   }
-  std::vector<float4> o(nobs);
-  for (size_t i = 0; i < nobs; ++i)
-    o[i] = make_float4(float(k * obs[3 * i]), float(k * obs[3 * i + 1]), float(k * obs[3 * i + 2]), 0.f);
-  DeviceBuffer<float4> odev;
-  odev.upload(o, stream_);
+  DeviceBuffer<double> odev;
+  odev.upload(obs, 3 * nobs, stream_);
   DeviceBuffer<double2> res(nobs);
-  launch_field(n, body_abs_.get(), body_q_.get(), odev.get(), uint32_t(nobs), float(k / (4.0 * kPi)),
-               float(cfg_.wave_i / cfg_.wave_r), res.get(), stream_);
+  DeviceBuffer<int> flag(1);
+  flag.zero(stream_);
+  const bool test = touch2_.size() != 0;
+  launch_field(n, xyz64_.get(), body_q_.get(), odev.get(), uint32_t(nobs), k, float(k / (4.0 * kPi)),
+               float(cfg_.wave_i / cfg_.wave_r), test ? touch2_.get() : nullptr, touch_ni_, res.get(), flag.get(),
+               stream_);
+  int touched = 0;
+  flag.download(&touched, 1, stream_);
   res.download(reinterpret_cast<double2*>(out), nobs, stream_);
   HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  if (touched)
+    throw Error(HFMM_ERR_SINGULAR, "evaluate_scattered_field: observation point touches the surface");
 }
 
 }  // namespace hfmm_b200

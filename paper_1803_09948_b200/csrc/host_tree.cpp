@@ -163,7 +163,7 @@ void build_tree_host(TreeArrays& t, const double* xyz, size_t n, int ncrit, doub
 // The pair SET equals the reference's; the order inside a target's list is not preserved (only
 // floating-point summation order depends on it).
 void dual_tree_traversal_host(const TreeArrays& t, double kmag, double theta, double kd_max,
-                              PairLists& out, int threads) {
+                              PairLists& out, int threads, int grain) {
   if (!(theta > 0) || theta > 1)
     throw Error(HFMM_ERR_CONFIG, "opening angle must satisfy 0 < theta <= 1");
   out = PairLists{};
@@ -175,7 +175,10 @@ void dual_tree_traversal_host(const TreeArrays& t, double kmag, double theta, do
   const int nthreads = std::max(threads, 1);
   struct Local {
     std::vector<Pair> next, far, near;
+    uint64_t tasks = 0;
   };
+  const uint32_t s_grain = uint32_t(std::max(grain, 0));
+  uint64_t tasks = (t.n_cells() && 2 * uint64_t(t.n_bodies) <= s_grain) ? 1 : 0;  // the root node
   while (!frontier.empty()) {
     std::vector<Local> loc(nthreads);
     parallel_chunks(frontier.size(), nthreads, [&](size_t b, size_t e, int tid) {
@@ -202,15 +205,24 @@ void dual_tree_traversal_host(const TreeArrays& t, double kmag, double theta, do
           L.near.push_back({a, s});
           continue;
         }
+        // a child node opens a task when its bodies first fit the grain (its parent, this node, did not)
+        const bool open = t.body_count[a] + t.body_count[s] > s_grain;
         if (!aleaf && (sleaf || ra > rs)) {
-          for (uint32_t c = 0; c < t.child_count[a]; ++c) L.next.push_back({t.child_first[a] + c, s});
+          for (uint32_t c = 0; c < t.child_count[a]; ++c) {
+            L.next.push_back({t.child_first[a] + c, s});
+            if (open && t.body_count[t.child_first[a] + c] + t.body_count[s] <= s_grain) ++L.tasks;
+          }
         } else {
-          for (uint32_t c = 0; c < t.child_count[s]; ++c) L.next.push_back({a, t.child_first[s] + c});
+          for (uint32_t c = 0; c < t.child_count[s]; ++c) {
+            L.next.push_back({a, t.child_first[s] + c});
+            if (open && t.body_count[a] + t.body_count[t.child_first[s] + c] <= s_grain) ++L.tasks;
+          }
         }
       }
     });
     next.clear();
     for (auto& L : loc) {
+      tasks += L.tasks;
       next.insert(next.end(), L.next.begin(), L.next.end());
       for (auto& p : L.far) {
         out.m2l_t.push_back(p.t);
@@ -223,6 +235,7 @@ void dual_tree_traversal_host(const TreeArrays& t, double kmag, double theta, do
     }
     frontier.swap(next);
   }
+  out.tasks = tasks;
 }
 
 int partition_units(const TreeArrays& t, int lmin_src, int lmin_dst, std::vector<uint32_t>& unit) {

@@ -41,6 +41,7 @@ struct TreeArrays {
 struct PairLists {
   // admissible cell pairs (M2L) and leaf pairs (P2P), as flat (target, source) arrays
   std::vector<uint32_t> m2l_t, m2l_s, p2p_t, p2p_s;
+  uint64_t tasks = 0;  // FmmStats::tasks: walk nodes whose bodies first fit the grain s (traversal.cpp:56-59)
 };
 
 // level-21 key of p inside the cubified box (octree.cpp:25-51); throws Error(HFMM_ERR_DOMAIN)
@@ -54,7 +55,7 @@ void build_tree_host(TreeArrays& tree, const double* xyz, size_t n, int ncrit, d
                      int threads);
 
 void dual_tree_traversal_host(const TreeArrays& tree, double kmag, double theta, double kd_max,
-                              PairLists& out, int threads);
+                              PairLists& out, int threads, int grain = 0);
 
 // Cuts the Morton order into nranks contiguous body ranges.  Cut points sit on the
 // boundaries of PARTITION UNITS = the cells of level `lcut` (the coarsest level that takes part in

@@ -215,10 +215,14 @@ void launch_update_solution(uint32_t n, int cols, const float2* basis, size_t ld
 void launch_residual(uint32_t n, const double2* b, const float2* ax, float2* r32, double* out,
                      double* scratch, cudaStream_t s);
 void launch_narrow(uint32_t n, const double2* in, float2* out, cudaStream_t s);
-// out[o] = scale * sum_i q_i e^{i|o-x_i|} e^{-eps |o-x_i|}/|o-x_i| over k_r-scaled absolute coordinates
-// (eps = k_i / k_r, 0 for a real wavenumber)
-void launch_field(uint32_t n, const float4* src_pos, const float2* q, const float4* obs, uint32_t nobs,
-                  float scale, float eps, double2* out, cudaStream_t s);
+// out[o] = scale * sum_i q_i e^{i k|o-x_i|} e^{-eps k|o-x_i|}/(k|o-x_i|), distances in FP64 from the FP64
+// points (caller order); touch2 (per patch of ni samples, may be null): *flag = 1 when |o-x_i|^2 <= touch2
+void launch_field(uint32_t n, const double* xyz, const float2* q, const double* obs, uint32_t nobs, double k,
+                  float scale, float eps, const double* touch2, uint32_t ni, double2* out, int* flag,
+                  cudaStream_t s);
+// out[i] = amp * exp(i (kr + i ki) dir . x_i), FP64
+void launch_assemble_rhs(uint32_t n, const double* xyz, const double dir[3], double kr, double ki,
+                         const double amp[2], double2* out, cudaStream_t s);
 void launch_widen(uint32_t n, const float2* in, double2* out, cudaStream_t s);
 
 // out[s] = near[s] + far[s] + corr[index[s]], s over the owned Morton slots (corr may be null)

@@ -234,16 +234,23 @@ widen_kernel(uint32_t n, const float2* __restrict__ in, double2* __restrict__ ou
   out[i] = make_double2(double(v.x), double(v.y));
 }
 
-// plain single-layer sum at exterior points (solver.cpp:393-419): one block per observation
+// plain single-layer sum at exterior points (solver.cpp:393-419): one block per observation.
+// x_i - o is formed in FP64 from the FP64 points (absolute FP32 coordinates would cost a phase error of
+// ulp(k |x|)); the kernel value itself is complex FP32 like the rest of the path.  touch2: squared touch
+// radius per patch (0.1 x diameter, solver.cpp:399-403), or null; a sample within it raises *flag.
 __global__ void __launch_bounds__(kBlock)
-field_kernel(uint32_t n, const float4* __restrict__ src_pos, const float2* __restrict__ q,
-             const float4* __restrict__ obs, float scale, float eps, double2* __restrict__ out) {
-  const float4 o = obs[blockIdx.x];
+field_kernel(uint32_t n, const double* __restrict__ xyz, const float2* __restrict__ q, const double* __restrict__ obs,
+             double k, float scale, float eps, const double* __restrict__ touch2, uint32_t ni,
+             double2* __restrict__ out, int* __restrict__ flag) {
+  const double ox = obs[3 * blockIdx.x], oy = obs[3 * blockIdx.x + 1], oz = obs[3 * blockIdx.x + 2];
   double re = 0, im = 0;
+  bool touched = false;
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const float4 p = src_pos[i];
+    const double ddx = ox - xyz[3 * i], ddy = oy - xyz[3 * i + 1], ddz = oz - xyz[3 * i + 2];
+    const double d2 = ddx * ddx + ddy * ddy + ddz * ddz;
+    if (touch2 && d2 <= touch2[i / ni]) touched = true;
     const float2 c = q[i];
-    const float dx = o.x - p.x, dy = o.y - p.y, dz = o.z - p.z;
+    const float dx = float(k * ddx), dy = float(k * ddy), dz = float(k * ddz);
     const float r2 = dx * dx + dy * dy + dz * dz;
     if (r2 > 0.f) {
       const float r0 = rsqrtf(r2), r = r2 * r0;
@@ -255,8 +262,24 @@ field_kernel(uint32_t n, const float4* __restrict__ src_pos, const float2* __res
       im += double(gr * c.y + gi * c.x);
     }
   }
+  if (touched) *flag = 1;
   block_sum(re, im);
   if (threadIdx.x == 0) out[blockIdx.x] = make_double2(re * scale, im * scale);
+}
+
+// assemble_rhs (solver.cpp:302-312): rhs[i] = A exp(i k d.x_i), k = kr + i ki, all in FP64
+__global__ void __launch_bounds__(kBlock)
+assemble_rhs_kernel(uint32_t n, const double* __restrict__ xyz, double dx, double dy, double dz, double kr,
+                    double ki, double ar, double ai, double2* __restrict__ out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double t = dx * xyz[3 * i] + dy * xyz[3 * i + 1] + dz * xyz[3 * i + 2];
+  // exp(i k t) = exp(-ki t) (cos(kr t) + i sin(kr t))
+  double sn, cs;
+  sincos(kr * t, &sn, &cs);
+  const double m = exp(-ki * t);
+  const double er = m * cs, ei = m * sn;
+  out[i] = make_double2(ar * er - ai * ei, ar * ei + ai * er);
 }
 
 inline uint32_t grid_for(uint32_t n) { return (n + kBlock - 1) / kBlock; }
@@ -307,10 +330,17 @@ void launch_residual(uint32_t n, const double2* b, const float2* ax, float2* r32
   residual_kernel<<<reduce_grid(n), kBlock, 0, s>>>(n, b, ax, r32, out, scratch);
   HFMM_CUDA_CHECK(cudaGetLastError());
 }
-void launch_field(uint32_t n, const float4* src_pos, const float2* q, const float4* obs, uint32_t nobs,
-                  float scale, float eps, double2* out, cudaStream_t s) {
+void launch_field(uint32_t n, const double* xyz, const float2* q, const double* obs, uint32_t nobs, double k,
+                  float scale, float eps, const double* touch2, uint32_t ni, double2* out, int* flag,
+                  cudaStream_t s) {
   if (!n || !nobs) return;
-  field_kernel<<<nobs, kBlock, 0, s>>>(n, src_pos, q, obs, scale, eps, out);
+  field_kernel<<<nobs, kBlock, 0, s>>>(n, xyz, q, obs, k, scale, eps, touch2, ni ? ni : 1u, out, flag);
+  HFMM_CUDA_CHECK(cudaGetLastError());
+}
+void launch_assemble_rhs(uint32_t n, const double* xyz, const double dir[3], double kr, double ki,
+                         const double amp[2], double2* out, cudaStream_t s) {
+  if (!n) return;
+  assemble_rhs_kernel<<<grid_for(n), kBlock, 0, s>>>(n, xyz, dir[0], dir[1], dir[2], kr, ki, amp[0], amp[1], out);
   HFMM_CUDA_CHECK(cudaGetLastError());
 }
 void launch_narrow(uint32_t n, const double2* in, float2* out, cudaStream_t s) {

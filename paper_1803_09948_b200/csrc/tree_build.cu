@@ -155,7 +155,8 @@ __global__ void __launch_bounds__(kBlock)
 traversal_kernel(const uint2* __restrict__ frontier, unsigned long long n_front, const uint8_t* __restrict__ lvl,
                  const uint32_t* __restrict__ ix, const uint32_t* __restrict__ iy,
                  const uint32_t* __restrict__ iz, const uint32_t* __restrict__ child_first,
-                 const uint32_t* __restrict__ child_count, const TraversalGeom g, PairSink next,
+                 const uint32_t* __restrict__ child_count, const uint32_t* __restrict__ body_count,
+                 uint32_t grain, unsigned long long* __restrict__ tasks, const TraversalGeom g, PairSink next,
                  PairSink far, PairSink near, int* __restrict__ overflow) {
   const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = i < n_front;
@@ -203,8 +204,16 @@ traversal_kernel(const uint2* __restrict__ frontier, unsigned long long n_front,
   if (n_next) {
     if (s_next + n_next <= next.cap) {
       const uint32_t cf = split_target ? child_first[a] : child_first[b];
-      for (uint32_t c = 0; c < n_next; ++c)
+      // FmmStats::tasks (traversal.cpp:56-59): a walk node opens a task when the bodies of its two cells
+      // first fit the grain s — its parent node (this one) did not fit, body counts only shrink downwards
+      const uint32_t other = split_target ? body_count[b] : body_count[a];
+      const bool parent_open = body_count[a] + body_count[b] > grain;
+      uint32_t opened = 0;
+      for (uint32_t c = 0; c < n_next; ++c) {
         next.data[s_next + c] = split_target ? make_uint2(cf + c, b) : make_uint2(a, cf + c);
+        if (parent_open && body_count[cf + c] + other <= grain) ++opened;
+      }
+      if (opened) atomicAdd(tasks, (unsigned long long)opened);
     } else {
       *overflow = 1;
     }
@@ -524,7 +533,7 @@ void build_tree_device(TreeArrays& t, const double* xyz, size_t n, int ncrit, do
 }
 
 void dual_tree_traversal_device(const TreeArrays& t, const DeviceCells& cells, double kmag, double theta,
-                                double kd_max, DevicePairs& out, cudaStream_t s) {
+                                double kd_max, int grain, DevicePairs& out, cudaStream_t s) {
   if (!(theta > 0) || theta > 1) throw Error(HFMM_ERR_CONFIG, "opening angle must satisfy 0 < theta <= 1");
   const TraversalGeom g = make_geom(t, kmag, theta, kd_max);
   const uint64_t n = t.n_bodies;
@@ -548,15 +557,18 @@ void dual_tree_traversal_device(const TreeArrays& t, const DeviceCells& cells, d
           near{out.near.get(), counters.get() + 1, cap_near};
       traversal_kernel<<<grid_for(n_front), kBlock, 0, s>>>(
           cur, n_front, cells.level.get(), cells.ix.get(), cells.iy.get(), cells.iz.get(),
-          cells.child_first.get(), cells.child_count.get(), g, next, far, near, overflow.get());
+          cells.child_first.get(), cells.child_count.get(), cells.body_count.get(), uint32_t(grain),
+          counters.get() + 3, g, next, far, near, overflow.get());
       HFMM_CUDA_CHECK(cudaGetLastError());
-      unsigned long long h[3];
+      unsigned long long h[4];
       HFMM_CUDA_CHECK(cudaMemcpyAsync(h, counters.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
       HFMM_CUDA_CHECK(cudaMemcpyAsync(&ovf, overflow.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
       HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
       out.n_far = h[0];
       out.n_near = h[1];
       n_front = h[2];
+      // the root node opens a task itself when the whole problem fits the grain
+      out.tasks = h[3] + (2 * uint64_t(t.n_bodies) <= uint64_t(grain) ? 1 : 0);
       std::swap(cur, nxt);
     }
     if (!ovf) return;

@@ -29,6 +29,7 @@ namespace hfmm_b200 {
 struct DevicePairs {
   DeviceBuffer<uint2> far, near;  // (target, source) cell ids, unordered
   uint64_t n_far = 0, n_near = 0;
+  uint64_t tasks = 0;  // FmmStats::tasks (traversal.cpp:56-59)
 };
 
 // K1 + K2.  Fills `tree` (host mirror: cells, leaves, index; `key` is left empty) and leaves the
@@ -45,7 +46,7 @@ struct DeviceCells {
 
 // K3
 void dual_tree_traversal_device(const TreeArrays& tree, const DeviceCells& cells, double kmag,
-                                double theta, double kd_max, DevicePairs& out, cudaStream_t s);
+                                double theta, double kd_max, int grain, DevicePairs& out, cudaStream_t s);
 
 // min level over the M2L targets / sources (kMaxLevel + 1 when there are no pairs)
 void far_pair_level_range(const DevicePairs& p, const DeviceCells& cells, int& lmin_dst, int& lmin_src,

@@ -54,6 +54,16 @@ class _Fmm:
                 "m2l_groups", "p2p_groups", "max_m2l_list", "max_p2p_list"]
         return dict(zip(keys, [int(v) for v in c]))
 
+    def tasks(self):
+        f = self._f("tasks")
+        f.restype = C.c_longlong
+        return int(f(self.h))
+
+    def starved(self):
+        f = self._f("starved")
+        f.restype = C.c_longlong
+        return int(f(self.h))
+
     def cells(self):
         nc = self.counts()["cells"]
         out = np.zeros((nc, 8), dtype=np.uint32)

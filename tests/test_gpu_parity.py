@@ -38,6 +38,33 @@ def test_matvec_vs_oracle_fmm(oracle, n, k, order, ncrit, cap):
     assert rel_l2(y, y_ref) < TOL
 
 
+@pytest.mark.parametrize("n,k,ncrit,grain,cap", [(5000, 2.0, 20, 40, 0.5), (3000, 4.0, 32, 32, -1.0),
+                                                 (40, 1.0, 64, 128, 0.0), (2000, 1.0, 16, 4000, 0.0)])
+def test_task_and_starved_counters_match_the_reference(n, k, ncrit, grain, cap):
+    """FmmStats::tasks (traversal.cpp:56-59) and ::starved_cells (expansion.cpp:253-262), device and host builder"""
+    from checkers import Ref, have_ref
+    if not have_ref():
+        pytest.skip("compiled reference not on this box")
+    from paper_1803_09948_b200.api import HFMM_FLAG_HOST_TREE
+    xyz, q = plummer_points(n, 77), charges(n, 77)
+    cap_res = cap if cap >= 0 else 1.0 / k
+    f = Ref().fmm(xyz, k, 6, ncrit=ncrit, leaf_cap=cap_res, theta=0.4, kd_max=1.0, s=grain)
+    f.matvec(q)
+    for flags in (0, HFMM_FLAG_HOST_TREE):
+        op = HfmmCuda(k=k, order=6, ncrit=ncrit, grain=grain, leaf_cap=cap, flags=flags)
+        op.set_points(xyz)
+        st = op.stats()
+        assert st["host_tree_used"] == (1 if flags else 0)
+        assert st["tasks"] == f.tasks(), (flags, st["tasks"], f.tasks())
+        assert st["starved_cells"] == f.starved()
+    # a wavenumber small enough for j_P(k r) to underflow in FP64: every cell is starved, on both sides
+    f2 = Ref().fmm(xyz, 1e-30, 12, ncrit=ncrit, leaf_cap=0.0, theta=0.4, kd_max=0.0, s=grain)
+    f2.matvec(q)
+    op = HfmmCuda(k=1e-30, order=12, ncrit=ncrit, grain=grain, leaf_cap=0.0, kd_max=0.0)
+    op.set_points(xyz)
+    assert f2.starved() == f2.counts()["cells"] == op.stats()["starved_cells"]
+
+
 def test_near_field_only(oracle):
     # theta tiny-ish and kd gate closed => everything is P2P: checks the near kernel alone
     n, k = 3000, 3.0

@@ -75,6 +75,68 @@ def test_scattered_field_matches_reference_fixture():
     assert rel_l2(f, G["bie_scattered"]) < 1e-5
 
 
+def test_assemble_rhs_matches_reference_fixture():
+    # reference solver.cpp:302-312, evaluated in FP64 on the device from the FP64 points
+    op = _bie_operator(G)
+    rhs = op.assemble_rhs((0.0, 0.0, 1.0))
+    assert np.abs(rhs - G["bie_rhs"]).max() < 1e-13
+    k = float(G["bie_k"])
+    d = np.array([1.0, 2.0, -2.0]) / 3.0
+    amp = 0.5 - 1.5j
+    assert np.abs(op.assemble_rhs(d, amp) - amp * np.exp(1j * k * (G["bie_xyz"] @ d))).max() < 1e-13
+    with pytest.raises(HfmmError) as e:          # "incident direction must be unit length"
+        op.assemble_rhs((0.0, 0.0, 1.0001))
+    assert e.value.kind == "config_error"
+    # complex wavenumber: exp(i (kr + i ki) d.x)
+    opc = HfmmCuda(k=2.0 + 0.3j, order=6, ncrit=16)
+    opc.set_points(G["bie_xyz"])
+    assert np.abs(opc.assemble_rhs(d) - np.exp(1j * (2.0 + 0.3j) * (G["bie_xyz"] @ d))).max() < 1e-13
+
+
+def test_scattered_field_refuses_points_on_the_surface():
+    # reference solver.cpp:399-413: singular_error within 0.1 x patch diameter of a sample
+    op = _bie_operator(G)
+    patches = G["bie_patches"]
+    diam = 2 * np.linalg.norm(patches - patches.mean(axis=1, keepdims=True), axis=2).max(axis=1)
+    far = op.evaluate_field(G["bie_sol"], G["bie_obs"])       # no geometry known: nothing to test against
+    op.set_patch_diameters(diam)
+    assert np.array_equal(op.evaluate_field(G["bie_sol"], G["bie_obs"]), far)
+    x0 = G["bie_xyz"][17]
+    near = x0 * (1.0 + 0.05 * diam[17 // 3] / np.linalg.norm(x0))
+    with pytest.raises(HfmmError) as e:
+        op.evaluate_field(G["bie_sol"], np.vstack([G["bie_obs"], near]))
+    assert e.value.kind == "singular_error"
+    ok = x0 * (1.0 + 0.5 * diam[17 // 3] / np.linalg.norm(x0))
+    assert np.isfinite(op.evaluate_field(G["bie_sol"], ok[None, :])).all()
+    # the device builders know the patches: the test is armed without set_patch_diameters
+    tables = {key: G["bie_rule_" + key] for key in ("sample_ref", "far_weight", "near_pts", "near_basis",
+                                                    "self_npts", "self_pts", "self_basis")}
+    op2 = HfmmCuda(k=float(G["bie_k"]), order=int(G["bie_order"]), ncrit=16)
+    op2.set_points(G["bie_xyz"])
+    op2.build_corrections(patches, tables, mode=2, fetch=False)
+    with pytest.raises(HfmmError) as e:
+        op2.evaluate_field(G["bie_sol"], near[None, :])
+    assert e.value.kind == "singular_error"
+    # far away, FP64 distances: a large offset of the whole geometry leaves the field unchanged to FP32 rounding
+    shift = np.array([300.0, -200.0, 100.0])
+    op3 = HfmmCuda(k=float(G["bie_k"]), order=int(G["bie_order"]), ncrit=16)
+    op3.set_points(G["bie_xyz"] + shift)
+    op3.set_corrections(int(G["bie_ni"]), far_weight=G["bie_far_weight"])
+    assert rel_l2(op3.evaluate_field(G["bie_sol"], G["bie_obs"] + shift), G["bie_scattered"]) < 1e-5
+
+
+def test_solve_report_histories():
+    # SolveReport::seconds / matvec_seconds, one entry per iteration (solver.hpp:106-116)
+    op = _bie_operator(G)
+    x, rep = op.gmres(G["bie_rhs"], rtol=1e-4, restart=30, max_iterations=200, precondition=True)
+    it = rep["iterations"]
+    assert len(rep["seconds_history"]) == it == len(rep["matvec_seconds_history"]) == len(rep["residuals"])
+    assert np.all(np.diff(rep["seconds_history"]) > 0) and rep["seconds_history"][-1] <= rep["seconds"]
+    assert np.all(rep["matvec_seconds_history"] > 0)
+    # restarts add one operator application to the iteration that follows them; the exit residual one more
+    assert rep["matvec_seconds_history"].sum() <= rep["matvec_seconds"] + 1e-12
+
+
 @pytest.mark.skipif(not have_ref(), reason="compiled reference not on this box")
 def test_midsize_system_against_oracle_gmres(oracle):
     """320 curved triangles (960 unknowns): system built by the reference, GMRES run (a) on the
