@@ -214,10 +214,10 @@ int hfmm_cuda_get_expansions(hfmm_cuda_t* h, int which, double* out);
  * Every rank passes the GLOBAL point set to set_points after set_partition(rank, nranks): the
  * tree and lists are identical on all ranks, the Morton order is cut into nranks contiguous body
  * ranges balanced by estimated work, and each rank keeps only the work whose TARGETS it owns.
- * One matvec is two device phases around one exchange that the caller performs with its own
- * communicator (torch.distributed over NCCL in bench.py / paper_1803_09948_b200/distributed.py):
- *   all-gather of the charge slices -> dist_upward -> all-gather of the owned multipole rows
- *   (hfmm_cuda_partition describes them) -> dist_downward.                                    */
+ * hfmm_cuda_dist_matvec / hfmm_cuda_dist_solve below run the whole exchange inside the library.  The two
+ * phase calls that follow are the building blocks for a caller that moves the data itself (and for the
+ * single-device emulation of several ranks in the tests): all the charges in place -> dist_upward ->
+ * the needed multipole rows in place (hfmm_cuda_partition, hfmm_cuda_get_exchange_masks) -> dist_downward. */
 typedef struct {
   int32_t rank, nranks;
   uint64_t n_bodies, body_first, body_count;     /* owned Morton slots                           */
@@ -288,27 +288,42 @@ int hfmm_cuda_build_corrections(hfmm_cuda_t* h, const hfmm_correction_rules* rul
 int hfmm_cuda_get_corrections(hfmm_cuda_t* h, double* patch_block, double* block_lu, int32_t* block_piv,
                               uint32_t* near_offset, uint32_t* near_source, double* near_delta);
 
-/* Restarted GMRES over Morton-sharded vectors: every rank holds the slice
- * [body_first, body_first + body_count) of each Krylov vector; inner products are local FP64
- * reductions followed by `allreduce_sum`; the operator is the two-phase matvec above.  The three
- * exchanges are performed by the caller's communicator through these callbacks (NCCL via
- * torch.distributed in distributed.py); the handle's stream is idle when a callback runs and the
- * callback must have completed its device work when it returns.  The iteration itself is the
- * reference's (gmres.cpp:35-174), so all ranks take identical branches: they see identical
- * reduced scalars. */
+/* ---- the library's own data plane (reference let.cpp:150-362) -----------------
+ * After hfmm_cuda_set_partition(rank, nranks) the handle can own a communicator:
+ *   NCCL   rank 0 calls hfmm_cuda_nccl_unique_id and hands the 128 bytes to its peers by whatever bootstrap
+ *          the application has (torchrun's store, MPI_Bcast, a file); every rank then calls
+ *          hfmm_cuda_comm_init_nccl (ncclCommInitRank; collective).  NCCL is loaded at run time
+ *          (libnccl.so.2), a single-GPU user needs none.
+ *   host   the same packed buffers staged through pinned host memory, the collectives performed by two
+ *          caller callbacks on HOST buffers — the MPI escape hatch, and the way two processes can share
+ *          one GPU in tests (NCCL refuses two ranks on one device).
+ * One matvec = pack kernel -> one grouped ncclSend/ncclRecv over all peers -> unpack kernel, for the halo
+ * charges and for the multipoles of the cells the peers translate from (index lists fixed at set_points,
+ * identical on both sides without a handshake), on a communication stream overlapped with the upward pass
+ * and the near field.  The exchange index lists are rebuilt lazily after every hfmm_cuda_set_points. */
 typedef struct {
   void* user;
-  /* every callback returns 0 on success; any other value aborts the solve at once with
-   * HFMM_ERR_DEVICE (the ranks of a real communicator fail together: a collective that failed on one
-   * rank failed on all of them) */
-  int (*allreduce_sum)(void* user, double* values, int count);  /* host doubles, in place      */
-  int (*gather_vector)(void* user, void* full_dev);             /* n float2, Morton order       */
-  int (*gather_multipoles)(void* user);                         /* rows of hfmm_cuda_partition  */
-} hfmm_dist_callbacks;
-/* rhs_owned / x_owned: body_count interleaved complex doubles, Morton order (host) */
-int hfmm_cuda_dist_gmres(hfmm_cuda_t* h, const double* rhs_owned, double* x_owned,
-                         const hfmm_gmres_config* cfg, hfmm_gmres_report* report, double* residuals,
-                         int residual_cap, const hfmm_dist_callbacks* cb);
+  /* send / recv: host buffers; send_bytes[p] / recv_bytes[p]: bytes for / from rank p (nranks entries,
+   * blocks in rank order, own entry 0).  Return 0 on success. */
+  int (*alltoallv)(void* user, const void* send, const uint64_t* send_bytes, void* recv, const uint64_t* recv_bytes);
+  int (*allreduce_sum)(void* user, double* values, int count);   /* host doubles, in place */
+} hfmm_host_transport;
+int hfmm_cuda_nccl_unique_id(void* out128);
+int hfmm_cuda_comm_init_nccl(hfmm_cuda_t* h, const void* unique_id_128);
+int hfmm_cuda_comm_init_host(hfmm_cuda_t* h, const hfmm_host_transport* transport);
+/* plain FMM product over the ranks: q_owned_dev / out_owned_dev are device float2 arrays holding this rank's
+ * slice [body_first, body_first + body_count) of the Morton-ordered vectors (hfmm_cuda_get_partition,
+ * hfmm_cuda_get_body_order).  Asynchronous on the handle's streams until hfmm_cuda_sync. */
+int hfmm_cuda_dist_matvec(hfmm_cuda_t* h, const void* q_owned_dev, void* out_owned_dev);
+/* gmres / gmres_solve (gmres.cpp:35-174) over Morton-sharded vectors: rhs_owned / x_owned are body_count
+ * interleaved complex doubles (host, Morton order).  Inner products are local FP64 reductions all-reduced
+ * on the device (ncclAllReduce in stream order: no host round trip per coefficient); with corrections /
+ * block-Jacobi set, the operand is all-gathered and the streaming BIE tail evaluated redundantly.  All ranks
+ * see identical scalars and take identical branches. */
+int hfmm_cuda_dist_solve(hfmm_cuda_t* h, const double* rhs_owned, double* x_owned, const hfmm_gmres_config* cfg,
+                         hfmm_gmres_report* report, double* residuals, int residual_cap);
+/* bytes this rank RECEIVES per matvec in the two exchanges (halo charges, remote multipoles) */
+int hfmm_cuda_get_exchange_volume(hfmm_cuda_t* h, uint64_t* charge_bytes, uint64_t* multipole_bytes);
 
 const char* hfmm_cuda_version(void);
 

@@ -99,14 +99,13 @@ def make_correction_rules(patches, tables, mode=2, near_patch_distance=-1.0):
     return r, keep
 
 
+ALLTOALLV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.c_void_p, C.POINTER(C.c_uint64))
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int)
-GATHER_VECTOR_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p)
-GATHER_MULTIPOLES_FN = C.CFUNCTYPE(C.c_int, C.c_void_p)
 
 
-class _DistCallbacks(C.Structure):
-    _fields_ = [("user", C.c_void_p), ("allreduce_sum", ALLREDUCE_FN),
-                ("gather_vector", GATHER_VECTOR_FN), ("gather_multipoles", GATHER_MULTIPOLES_FN)]
+class _HostTransport(C.Structure):
+    """hfmm_host_transport (include/hfmm_cuda.h)"""
+    _fields_ = [("user", C.c_void_p), ("alltoallv", ALLTOALLV_FN), ("allreduce_sum", ALLREDUCE_FN)]
 
 
 def library_path() -> str:
@@ -331,12 +330,79 @@ class HfmmCuda:
         d = np.ascontiguousarray(diameters, dtype=np.float64)
         self._check(self.lib.hfmm_cuda_set_patch_diameters(self.h, d.ctypes.data_as(_dp), C.c_size_t(d.shape[0])))
 
-    def dist_gmres(self, rhs_owned, allreduce_sum, gather_vector, gather_multipoles, rtol=1e-4,
-                   restart=30, max_iterations=500, precondition=True):
-        """GMRES over Morton-sharded vectors.  rhs_owned: the owned Morton slice (complex128).
-        allreduce_sum(np.ndarray[float64]) reduces in place over the ranks; gather_vector(dev_ptr)
-        all-gathers the n-float2 Morton vector at dev_ptr; gather_multipoles() exchanges the owned
-        multipole rows.  Exceptions raised inside a callback abort the solve."""
+    # ---- the library's own data plane (csrc/comm.cu)
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        """128 bytes from ncclGetUniqueId (rank 0 creates, the application's bootstrap distributes)"""
+        buf = C.create_string_buffer(128)
+        lib = load_library()
+        rc = lib.hfmm_cuda_nccl_unique_id(buf)
+        if rc:
+            raise HfmmError(rc, lib.hfmm_cuda_last_error(None).decode())
+        return buf.raw
+
+    def comm_init_nccl(self, unique_id: bytes):
+        """ncclCommInitRank over (rank, nranks) of set_partition; collective"""
+        if len(unique_id) != 128:
+            raise ValueError("an NCCL unique id is 128 bytes")
+        self._check(self.lib.hfmm_cuda_comm_init_nccl(self.h, C.c_char_p(unique_id)))
+
+    def comm_init_host(self, alltoallv, allreduce_sum):
+        """Host-staged transport.  alltoallv(send: np.uint8[...], send_bytes: np.uint64[R], recv: np.uint8[...],
+        recv_bytes: np.uint64[R]) and allreduce_sum(values: np.float64[...]) work in place on host arrays;
+        an exception inside either aborts the running call with a device error."""
+        nranks = int(self.partition().nranks) if self.n else None
+        failure = self._transport_failure = []
+
+        def a2a(_u, send, sbytes, recv, rbytes):
+            if failure:
+                return 1
+            try:
+                R = nranks if nranks is not None else int(self.partition().nranks)
+                sb = np.ctypeslib.as_array(sbytes, shape=(R,)).copy()
+                rb = np.ctypeslib.as_array(rbytes, shape=(R,)).copy()
+                s_arr = np.ctypeslib.as_array(C.cast(send, C.POINTER(C.c_uint8)), shape=(max(int(sb.sum()), 1),))
+                r_arr = np.ctypeslib.as_array(C.cast(recv, C.POINTER(C.c_uint8)), shape=(max(int(rb.sum()), 1),))
+                alltoallv(s_arr[:int(sb.sum())], sb, r_arr[:int(rb.sum())], rb)
+                return 0
+            except BaseException as e:      # a callback must not unwind through C
+                failure.append(e)
+                return 1
+
+        def red(_u, p, c):
+            if failure:
+                return 1
+            try:
+                allreduce_sum(np.ctypeslib.as_array(p, shape=(c,)))
+                return 0
+            except BaseException as e:
+                failure.append(e)
+                return 1
+
+        self._transport = _HostTransport(None, ALLTOALLV_FN(a2a), ALLREDUCE_FN(red))   # kept alive with the handle
+        self._check(self.lib.hfmm_cuda_comm_init_host(self.h, C.byref(self._transport)))
+
+    def _raise_transport_failure(self):
+        f = getattr(self, "_transport_failure", None)
+        if f:
+            e = f[0]
+            f.clear()
+            raise e
+
+    def dist_matvec(self, q_owned_dev_ptr: int, out_owned_dev_ptr: int):
+        rc = self.lib.hfmm_cuda_dist_matvec(self.h, C.c_void_p(q_owned_dev_ptr), C.c_void_p(out_owned_dev_ptr))
+        self._raise_transport_failure()
+        self._check(rc)
+
+    def exchange_volume(self):
+        """(halo charge bytes, remote multipole bytes) this rank receives per matvec"""
+        a, b = C.c_uint64(), C.c_uint64()
+        self._check(self.lib.hfmm_cuda_get_exchange_volume(self.h, C.byref(a), C.byref(b)))
+        return int(a.value), int(b.value)
+
+    def dist_solve(self, rhs_owned, rtol=1e-4, restart=30, max_iterations=500, precondition=True):
+        """GMRES over Morton-sharded vectors through the handle's communicator.  rhs_owned: the owned
+        Morton slice (complex128); returns the same slice of the solution and the report."""
         rhs = _c128(rhs_owned)
         if rhs.shape != (int(self.partition().body_count),):
             raise ValueError("rhs_owned must hold exactly the owned Morton slice")
@@ -345,30 +411,10 @@ class HfmmCuda:
         cap = max(int(max_iterations), 0) + 1
         res, sec, mv = np.zeros(cap), np.zeros(cap), np.zeros(cap)
         rep = _GmresReport(seconds_history=sec.ctypes.data, matvec_seconds_history=mv.ctypes.data, history_cap=cap)
-        failure = []
-
-        def guard(fn):
-            def run(*args):     # status for the library: non-zero aborts the solve at once
-                if failure:
-                    return 1
-                try:
-                    fn(*args)
-                    return 0
-                except BaseException as e:  # a callback must not unwind through C
-                    failure.append(e)
-                    return 1
-            return run
-
-        cb = _DistCallbacks(
-            None,
-            ALLREDUCE_FN(guard(lambda _u, p, c: allreduce_sum(np.ctypeslib.as_array(p, shape=(c,))))),
-            GATHER_VECTOR_FN(guard(lambda _u, ptr: gather_vector(int(ptr)))),
-            GATHER_MULTIPOLES_FN(guard(lambda _u: gather_multipoles())))
-        rc = self.lib.hfmm_cuda_dist_gmres(self.h, rhs.ctypes.data_as(_dp), x.ctypes.data_as(_dp),
-                                           C.byref(cfg), C.byref(rep), res.ctypes.data_as(_dp),
-                                           len(res), C.byref(cb))
-        if failure:
-            raise failure[0]
+        vp = lambda a: a.ctypes.data_as(_dp) if a.size else None
+        rc = self.lib.hfmm_cuda_dist_solve(self.h, vp(rhs), vp(x), C.byref(cfg), C.byref(rep),
+                                           res.ctypes.data_as(_dp), len(res))
+        self._raise_transport_failure()
         self._check(rc)
         return x, self._report(rep, res, sec, mv)
 

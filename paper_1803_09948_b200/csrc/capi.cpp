@@ -275,15 +275,45 @@ int hfmm_cuda_get_corrections(hfmm_cuda_t* h, double* patch_block, double* block
   });
 }
 
-int hfmm_cuda_dist_gmres(hfmm_cuda_t* h, const double* rhs_owned, double* x_owned,
-                         const hfmm_gmres_config* cfg, hfmm_gmres_report* report, double* residuals,
-                         int residual_cap, const hfmm_dist_callbacks* cb) {
+int hfmm_cuda_nccl_unique_id(void* out128) {
+  return guarded(nullptr, [&] {
+    if (!out128) throw Error(HFMM_ERR_CONFIG, "null argument");
+    hfmm_b200::nccl_unique_id(out128);
+  });
+}
+
+int hfmm_cuda_comm_init_nccl(hfmm_cuda_t* h, const void* unique_id_128) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] { h->engine->comm_init_nccl(unique_id_128); });
+}
+
+int hfmm_cuda_comm_init_host(hfmm_cuda_t* h, const hfmm_host_transport* t) {
   if (int rc = need(h)) return rc;
   return guarded(h, [&] {
-    if (!rhs_owned || !x_owned || !cfg || !report || !cb || !cb->allreduce_sum || !cb->gather_vector ||
-        !cb->gather_multipoles)
-      throw Error(HFMM_ERR_CONFIG, "null argument");
-    h->engine->dist_gmres(rhs_owned, x_owned, *cfg, report, residuals, residual_cap, *cb);
+    if (!t) throw Error(HFMM_ERR_CONFIG, "null transport");
+    h->engine->comm_init_host(*t);
+  });
+}
+
+int hfmm_cuda_dist_matvec(hfmm_cuda_t* h, const void* q_owned_dev, void* out_owned_dev) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] { h->engine->dist_matvec(q_owned_dev, out_owned_dev); });
+}
+
+int hfmm_cuda_dist_solve(hfmm_cuda_t* h, const double* rhs_owned, double* x_owned, const hfmm_gmres_config* cfg,
+                         hfmm_gmres_report* report, double* residuals, int residual_cap) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] {
+    if (!cfg || !report) throw Error(HFMM_ERR_CONFIG, "null argument");
+    h->engine->dist_solve(rhs_owned, x_owned, *cfg, report, residuals, residual_cap);
+  });
+}
+
+int hfmm_cuda_get_exchange_volume(hfmm_cuda_t* h, uint64_t* charge_bytes, uint64_t* multipole_bytes) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] {
+    if (!charge_bytes || !multipole_bytes) throw Error(HFMM_ERR_CONFIG, "null argument");
+    h->engine->get_exchange_volume(charge_bytes, multipole_bytes);
   });
 }
 

@@ -662,6 +662,8 @@ void Engine::set_partition_alpha(double alpha) {
 
 void Engine::set_partition(int rank, int nranks) {
   if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(HFMM_ERR_CONFIG, "rank out of range");
+  if (nranks > 64) throw Error(HFMM_ERR_CONFIG, "at most 64 ranks (exchange masks are 64 bits wide)");
+  if (rank != rank_ || nranks != nranks_) release_comm();  // a communicator belongs to one (rank, nranks)
   rank_ = rank;
   nranks_ = nranks;
   have_points_ = false;  // work lists depend on the partition: set_points must follow
@@ -753,6 +755,7 @@ void Engine::set_points(const double* xyz, size_t n) {
   have_points_ = false;
   have_weight_ = have_block_ = have_near_ = have_lu_ = false;  // corrections belong to a point set
   release_correction_store();
+  exchange_.reset();  // the index lists of the exchanges belong to a point set
   touch2_.release();
   identity_.release();
   dev_pairs_ = DevicePairs{};
@@ -1035,6 +1038,7 @@ void Engine::phase_upward() {
   p2p_late_ = !serial && have_far_ && !(cfg_.flags & HFMM_FLAG_NEAR_FIRST);
   if (!p2p_late_) {
     cudaStream_t sn = serial ? stream_ : stream_near_;
+    if (near_gate_) HFMM_CUDA_CHECK(cudaStreamWaitEvent(sn, near_gate_, 0));
     HFMM_CUDA_CHECK(cudaEventRecord(ev_[0], sn));
     launch_p2p(pa, sn);
     ++launches;
@@ -1117,6 +1121,7 @@ void Engine::phase_downward() {
     if (p2p_late_) HFMM_CUDA_CHECK(cudaStreamWaitEvent(stream_near_, ev_[12], 0));
     run_stage(m2l_, multipole_.get(), local_.get());
     if (p2p_late_) {  // enqueued behind the persistent M2L launch: its CTAs fill what M2L leaves free
+      if (near_gate_) HFMM_CUDA_CHECK(cudaStreamWaitEvent(stream_near_, near_gate_, 0));
       HFMM_CUDA_CHECK(cudaEventRecord(ev_[0], stream_near_));
       launch_p2p(p2p_args_, stream_near_);
       ++launches;

@@ -82,9 +82,16 @@ class Engine {
   void build_corrections(const hfmm_correction_rules& rules, uint64_t* near_nnz);
   void get_corrections(double* patch_block, double* block_lu, int* block_piv, uint32_t* near_offset,
                        uint32_t* near_source, double* near_delta);
-  void dist_gmres(const double* rhs_owned, double* x_owned, const hfmm_gmres_config& cfg,
-                  hfmm_gmres_report* rep, double* residuals, int residual_cap,
-                  const hfmm_dist_callbacks& cb);
+  // multi-GPU data plane (comm.cu): communicator, locally-essential-tree exchange, sharded solver
+  struct Transport;
+  struct ExchangePlan;
+  void comm_init_nccl(const void* unique_id_128);
+  void comm_init_host(const hfmm_host_transport& cb);
+  const char* comm_name() const;
+  void get_exchange_volume(uint64_t* charge_bytes, uint64_t* multipole_bytes);
+  void dist_matvec(const void* q_owned_dev, void* out_owned_dev);
+  void dist_solve(const double* rhs_owned, double* x_owned, const hfmm_gmres_config& cfg,
+                  hfmm_gmres_report* rep, double* residuals, int residual_cap);
 
   std::string last_error;
   const hfmm_cuda_config& config() const { return cfg_; }
@@ -99,6 +106,13 @@ class Engine {
   void phase_downward();    // M2L + L2L + L2P, joins the near field
   void run_stage(const TranslateStage& st, const float2* src, float2* dst);
   void compute_partition();
+  void gmres_impl(bool sharded, const double* rhs, double* x_out, const hfmm_gmres_config& cfg,
+                  hfmm_gmres_report* rep, double* residuals, int residual_cap);
+  void build_exchange_plan();
+  void dist_far_and_near();   // body_q_ (owned slots) -> near_, far_ (owned slots), over the two exchanges
+  void comm_allreduce(double* dev, int count);
+  void comm_allgather_morton(float2* full);
+  void release_comm();
   uint64_t count_starved_cells() const;
   void collect_timings();
   void apply_operator_device(const float2* x, float2* y);  // caller order, weights + corrections
@@ -125,6 +139,10 @@ class Engine {
   double partition_alpha_ = -1.0;
   P2PArgs p2p_args_{};
   bool p2p_late_ = false;
+  cudaEvent_t near_gate_ = nullptr;  // sharded matvec: the near field waits for the halo charges
+  std::shared_ptr<Transport> transport_;
+  std::shared_ptr<ExchangePlan> exchange_;
+  uint64_t exchange_bytes_[2] = {0, 0};
   bool host_lists_ = false;  // the pair lists of the current point set live on the host (host builder)
   std::vector<uint8_t> owned_;  // per cell
   std::vector<int32_t> cell_rank_;  // per cell: owning rank of the Morton partition
@@ -194,6 +212,9 @@ class Engine {
 // FP64 composition of the factored operator into a dense (P+1)^2 x (P+1)^2 matrix in the
 // reference's UNSCALED convention — used by the CPU-side table tests against
 // fmm::translation_matrix (expansion.cpp:95-124).  kind: 0 M2L (singular), 1 regular.
+// ncclGetUniqueId through the run-time loaded NCCL (comm.cu)
+void nccl_unique_id(void* out128);
+
 void compose_dense_from_tables(int order, double k, const double t[3], int kind, double s_src,
                                double s_dst, double* out_complex, double k_imag = 0.0);
 

@@ -76,8 +76,44 @@ void Engine::apply_operator_device(const float2* x, float2* y) {
                        near_source_.get(), have_near_ ? near_delta_.get() : nullptr, x, y, stream_);
 }
 
-void Engine::gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cfg,
-                   hfmm_gmres_report* rep, double* residuals, int residual_cap) {
+namespace {
+// body_q[first + i] = in[i] * weight[index[first + i]]: an owned Morton slice becomes the rank's charges
+__global__ void __launch_bounds__(256)
+owned_charges_kernel(const float2* __restrict__ in, const uint32_t* __restrict__ index, const float* __restrict__ weight,
+                     float2* __restrict__ body_q, uint32_t first, uint32_t count) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  float2 v = in[i];
+  if (weight) {
+    const float w = weight[index[first + i]];
+    v.x *= w;
+    v.y *= w;
+  }
+  body_q[first + i] = v;
+}
+}  // namespace
+
+void Engine::gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cfg, hfmm_gmres_report* rep,
+                   double* residuals, int residual_cap) {
+  gmres_impl(false, rhs, x_out, cfg, rep, residuals, residual_cap);
+}
+
+// GMRES over Morton-sharded vectors through the handle's communicator (comm.cu); see hfmm_cuda.h
+void Engine::dist_solve(const double* rhs_owned, double* x_owned, const hfmm_gmres_config& cfg,
+                        hfmm_gmres_report* rep, double* residuals, int residual_cap) {
+  if (!transport_ && nranks_ > 1)
+    throw Error(HFMM_ERR_CONFIG, "no communicator: call hfmm_cuda_comm_init_nccl / _host first");
+  gmres_impl(true, rhs_owned, x_owned, cfg, rep, residuals, residual_cap);
+}
+
+// One iteration loop for both layouts.  sharded = false: vectors of all n unknowns in caller order, the
+// operator is apply_operator.  sharded = true: every rank holds the slice [own_first_, own_first_ + own_count_)
+// of each Krylov vector in Morton order; inner products are local FP64 reductions all-reduced IN PLACE ON THE
+// DEVICE (stream-ordered, no host round trip per coefficient), the operator runs the two exchanges of comm.cu.
+// All ranks see identical reduced scalars and therefore take identical branches (restart, convergence,
+// breakdown).  The iteration itself is the reference's (gmres.cpp:35-174).
+void Engine::gmres_impl(bool sharded, const double* rhs, double* x_out, const hfmm_gmres_config& cfg,
+                        hfmm_gmres_report* rep, double* residuals, int residual_cap) {
   require_points();
   HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
   // validation as gmres.cpp:25-31
@@ -86,10 +122,14 @@ void Engine::gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cf
   if (cfg.max_iterations < 1) throw Error(HFMM_ERR_CONFIG, "gmres: max_iterations must be >= 1");
   using clk = std::chrono::steady_clock;
   const auto t_start = clk::now();
-  const uint32_t n = tree_.n_bodies;
+  const uint32_t n_all = tree_.n_bodies;
+  const uint32_t n = sharded ? own_count_ : n_all, first = sharded ? own_first_ : 0;
+  const size_t ld = std::max<uint32_t>(n, 1);  // leading dimension of the Krylov basis
   const int m = cfg.restart;
   const bool precond = cfg.precondition && have_lu_;
-  const uint32_t npatch = ni_ ? n / uint32_t(ni_) : 0;
+  const bool corr = have_block_ || have_near_;
+  const uint32_t npatch = ni_ ? n_all / uint32_t(ni_) : 0;
+  const bool reduce = sharded && transport_ != nullptr;
 
   double* const sec_hist = rep->seconds_history;
   double* const mv_hist = rep->matvec_seconds_history;
@@ -98,8 +138,24 @@ void Engine::gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cf
   rep->seconds_history = sec_hist;
   rep->matvec_seconds_history = mv_hist;
   rep->history_cap = hist_cap;
+
+  DeviceBuffer<float2> V(size_t(m + 1) * ld), w(ld), u(sharded ? 1 : n_all), r32(ld);
+  DeviceBuffer<float2> full(sharded && (precond || corr) ? n_all : 1), vc(full.size()), pc(full.size()),
+      yc(sharded && corr ? n_all : 1);
+  DeviceBuffer<double2> b64(ld), x64(ld);
+  DeviceBuffer<double> scal(size_t(2) * (2 * (m + 1) + 2)), ydev(size_t(2) * m), red(reduce_scratch_doubles());
+  red.zero(stream_);
+  std::vector<double> hscal(scal.size());
+
   double bnorm2 = 0;
   for (size_t i = 0; i < size_t(n) * 2; ++i) bnorm2 += rhs[i] * rhs[i];
+  if (reduce) {  // ||b||^2 over the ranks
+    scal.zero(stream_);
+    HFMM_CUDA_CHECK(cudaMemcpyAsync(scal.get(), &bnorm2, sizeof(double), cudaMemcpyHostToDevice, stream_));
+    comm_allreduce(scal.get(), 1);
+    scal.download(&bnorm2, 1, stream_);
+    HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  }
   const double bnorm = std::sqrt(bnorm2);
   rep->rhs_norm = bnorm;
   std::fill(x_out, x_out + size_t(n) * 2, 0.0);
@@ -110,26 +166,59 @@ void Engine::gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cf
   }
   const double target = cfg.rtol * bnorm;
 
-  DeviceBuffer<float2> V(size_t(m + 1) * n), w(n), u(n), r32(n);
-  DeviceBuffer<double2> b64(n), x64(n);
-  DeviceBuffer<double> scal(size_t(2) * (2 * (m + 1) + 2)), ydev(size_t(2) * m), red(reduce_scratch_doubles());
-  red.zero(stream_);
-  std::vector<double> hscal(scal.size());
-  HFMM_CUDA_CHECK(cudaMemcpyAsync(b64.get(), rhs, size_t(n) * sizeof(double2), cudaMemcpyHostToDevice, stream_));
+  if (n) HFMM_CUDA_CHECK(cudaMemcpyAsync(b64.get(), rhs, size_t(n) * sizeof(double2), cudaMemcpyHostToDevice, stream_));
   x64.zero(stream_);
   launch_narrow(n, b64.get(), r32.get(), stream_);  // x0 = 0: the first residual is b
 
   std::vector<cd> H(size_t(m + 1) * m), cs(m), sn(m), g(m + 1);
   auto h = [&](int i, int j) -> cd& { return H[size_t(j) * (m + 1) + i]; };
   double matvec_s = 0;
-  auto apply = [&](const float2* in, float2* out) {  // Z = A M^-1  (solver.cpp:383-387)
+  auto allreduce = [&](double* dev, int count) {
+    if (reduce) comm_allreduce(dev, count);
+  };
+  // Z = A M^-1  (solver.cpp:383-387)
+  auto apply = [&](const float2* in, float2* out) {
     const auto t0 = clk::now();
-    const float2* src = in;
-    if (precond) {
-      launch_precondition(npatch, ni_, block_lu_.get(), block_piv_.get(), in, u.get(), stream_);
-      src = u.get();
+    if (!sharded) {
+      const float2* src = in;
+      if (precond) {
+        launch_precondition(npatch, ni_, block_lu_.get(), block_piv_.get(), in, u.get(), stream_);
+        src = u.get();
+      }
+      apply_operator_device(src, out);
+    } else if (!(precond || corr)) {
+      // plain FMM operator: the owned slice becomes the owned charges, the halo arrives through the exchange
+      if (n)
+        owned_charges_kernel<<<(n + 255) / 256, 256, 0, stream_>>>(in, body_index_.get(),
+                                                                   have_weight_ ? far_weight_.get() : nullptr,
+                                                                   body_q_.get(), first, n);
+      HFMM_CUDA_CHECK(cudaGetLastError());
+      dist_far_and_near();
+      launch_combine_owned(near_.get() + first, far_.get() + first, nullptr, body_index_.get() + first, out, n, stream_);
+    } else {
+      // BIE tail: gather the operand, precondition and correct redundantly in caller order (streaming
+      // kernels, < 1 % of a matvec), run the FMM over the exchanges
+      if (n)
+        HFMM_CUDA_CHECK(cudaMemcpyAsync(full.get() + first, in, size_t(n) * sizeof(float2), cudaMemcpyDeviceToDevice,
+                                        stream_));
+      comm_allgather_morton(full.get());
+      launch_scatter_potentials(full.get(), nullptr, body_index_.get(), nullptr, vc.get(), n_all, stream_);
+      const float2* xc = vc.get();
+      if (precond) {
+        launch_precondition(npatch, ni_, block_lu_.get(), block_piv_.get(), vc.get(), pc.get(), stream_);
+        xc = pc.get();
+      }
+      launch_gather_charges(nullptr, xc, body_index_.get(), have_weight_ ? far_weight_.get() : nullptr, body_q_.get(),
+                            n_all, stream_);
+      dist_far_and_near();
+      if (corr) {
+        yc.zero(stream_);
+        launch_corrections(n_all, ni_, have_block_ ? patch_block_.get() : nullptr, near_offset_.get(),
+                           near_source_.get(), have_near_ ? near_delta_.get() : nullptr, xc, yc.get(), stream_);
+      }
+      launch_combine_owned(near_.get() + first, far_.get() + first, corr ? yc.get() : nullptr,
+                           body_index_.get() + first, out, n, stream_);
     }
-    apply_operator_device(src, out);
     HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
     matvec_s += std::chrono::duration<double>(clk::now() - t0).count();
   };
@@ -145,31 +234,35 @@ void Engine::gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cf
     int cols = 0;
     for (int j = 0; j < m; ++j) {
       if (iterations >= cfg.max_iterations) break;
-      apply(V.get() + size_t(j) * n, w.get());
-      // one fused sweep: ||w||^2, two Gram-Schmidt passes, ||w||^2 again; scalars stay on device
+      apply(V.get() + size_t(j) * ld, w.get());
+      // one fused sweep: ||w||^2, two Gram-Schmidt passes, ||w||^2 again; scalars stay on the device (and are
+      // all-reduced there in the sharded layout: the subtraction of a projection reads the reduced coefficient)
       scal.zero(stream_);
       double* s0 = scal.get();                  // [0]: w_scale^2
       double* h1 = s0 + 2;                      // pass 1, j+1 entries
       double* h2 = h1 + 2 * (m + 1);            // pass 2
       double* hn = h2 + 2 * (m + 1);            // ||w||^2 after both passes
       launch_norm2(n, w.get(), s0, red.get(), stream_);
+      allreduce(s0, 2);
       for (int pass = 0; pass < 2; ++pass) {
         double* hp = pass ? h2 : h1;
         for (int i = 0; i <= j; ++i) {
           const float2* vprev = nullptr;
           const double* cprev = nullptr;
           if (i > 0) {
-            vprev = V.get() + size_t(i - 1) * n;
+            vprev = V.get() + size_t(i - 1) * ld;
             cprev = hp + 2 * (i - 1);
           } else if (pass == 1) {
-            vprev = V.get() + size_t(j) * n;
+            vprev = V.get() + size_t(j) * ld;
             cprev = h1 + 2 * j;
           }
-          launch_mgs_step(n, w.get(), vprev, cprev, V.get() + size_t(i) * n, hp + 2 * i, red.get(), stream_);
+          launch_mgs_step(n, w.get(), vprev, cprev, V.get() + size_t(i) * ld, hp + 2 * i, red.get(), stream_);
+          allreduce(hp + 2 * i, 2);
         }
       }
-      launch_mgs_step(n, w.get(), V.get() + size_t(j) * n, h2 + 2 * j, nullptr, nullptr, red.get(), stream_);
+      launch_mgs_step(n, w.get(), V.get() + size_t(j) * ld, h2 + 2 * j, nullptr, nullptr, red.get(), stream_);
       launch_norm2(n, w.get(), hn, red.get(), stream_);
+      allreduce(hn, 2);
       scal.download(hscal.data(), hscal.size(), stream_);
       HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
       const double w_scale = std::sqrt(hscal[0]);
@@ -220,7 +313,7 @@ void Engine::gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cf
         done = true;
         break;
       }
-      launch_scale(n, w.get(), float(1.0 / hnext), V.get() + size_t(j + 1) * n, stream_);
+      launch_scale(n, w.get(), float(1.0 / hnext), V.get() + size_t(j + 1) * ld, stream_);
     }
     // fold the Arnoldi columns into x, skipping trailing dead diagonals (gmres.cpp:75-85)
     while (cols > 0 && std::abs(h(cols - 1, cols - 1)) == 0.0) --cols;
@@ -232,7 +325,7 @@ void Engine::gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cf
     }
     if (cols > 0) {
       HFMM_CUDA_CHECK(cudaMemcpyAsync(ydev.get(), y.data(), sizeof(cd) * cols, cudaMemcpyHostToDevice, stream_));
-      launch_update_solution(n, cols, V.get(), n, ydev.get(), x64.get(), stream_);
+      launch_update_solution(n, cols, V.get(), ld, ydev.get(), x64.get(), stream_);
       HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
     }
     if (!done) {  // restart boundary: true residual, not an Arnoldi step
@@ -240,6 +333,7 @@ void Engine::gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cf
       apply(r32.get(), w.get());
       scal.zero(stream_);
       launch_residual(n, b64.get(), w.get(), r32.get(), scal.get(), red.get(), stream_);
+      allreduce(scal.get(), 2);
       scal.download(hscal.data(), 2, stream_);
       HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
       beta = std::sqrt(hscal[0]);
@@ -250,237 +344,30 @@ void Engine::gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cf
   apply(V.get(), w.get());
   scal.zero(stream_);
   launch_residual(n, b64.get(), w.get(), r32.get(), scal.get(), red.get(), stream_);
+  allreduce(scal.get(), 2);
   scal.download(hscal.data(), 2, stream_);
   // the returned iterate maps back through M^-1 (solver.cpp:388)
   if (precond) {
-    launch_precondition(npatch, ni_, block_lu_.get(), block_piv_.get(), V.get(), u.get(), stream_);
-    launch_widen(n, u.get(), x64.get(), stream_);
+    if (!sharded) {
+      launch_precondition(npatch, ni_, block_lu_.get(), block_piv_.get(), V.get(), u.get(), stream_);
+      launch_widen(n, u.get(), x64.get(), stream_);
+    } else {  // gather the iterate, solve redundantly, keep the owned slots
+      if (n)
+        HFMM_CUDA_CHECK(cudaMemcpyAsync(full.get() + first, V.get(), size_t(n) * sizeof(float2), cudaMemcpyDeviceToDevice,
+                                        stream_));
+      comm_allgather_morton(full.get());
+      launch_scatter_potentials(full.get(), nullptr, body_index_.get(), nullptr, vc.get(), n_all, stream_);
+      launch_precondition(npatch, ni_, block_lu_.get(), block_piv_.get(), vc.get(), pc.get(), stream_);
+      launch_gather_charges(nullptr, pc.get(), body_index_.get(), nullptr, full.get(), n_all, stream_);
+      launch_widen(n, full.get() + first, x64.get(), stream_);
+    }
   }
-  HFMM_CUDA_CHECK(cudaMemcpyAsync(x_out, x64.get(), size_t(n) * sizeof(double2), cudaMemcpyDeviceToHost, stream_));
+  if (n) HFMM_CUDA_CHECK(cudaMemcpyAsync(x_out, x64.get(), size_t(n) * sizeof(double2), cudaMemcpyDeviceToHost, stream_));
   HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
   rep->iterations = iterations;
   rep->breakdown = breakdown ? 1 : 0;
   rep->final_residual = std::sqrt(hscal[0]) / bnorm;
   rep->converged = (rep->final_residual <= cfg.rtol || (nres > 0 && last_est / bnorm <= cfg.rtol)) ? 1 : 0;
-  rep->seconds = std::chrono::duration<double>(clk::now() - t_start).count();
-  rep->matvec_seconds = matvec_s;
-}
-
-// GMRES over Morton-sharded vectors; see hfmm_cuda.h.  Same iteration as Engine::gmres; every
-// inner product is followed by the caller's allreduce, so the modified-Gram-Schmidt sweep is not
-// fused here (one host round trip per coefficient, ~2(j+1)+2 small allreduces per iteration).
-void Engine::dist_gmres(const double* rhs, double* x_out, const hfmm_gmres_config& cfg,
-                        hfmm_gmres_report* rep, double* residuals, int residual_cap,
-                        const hfmm_dist_callbacks& cb) {
-  require_points();
-  HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
-  if (!(cfg.rtol > 0.0 && cfg.rtol < 1.0)) throw Error(HFMM_ERR_CONFIG, "gmres: rtol must lie in (0, 1)");
-  if (cfg.restart < 1) throw Error(HFMM_ERR_CONFIG, "gmres: restart must be >= 1");
-  if (cfg.max_iterations < 1) throw Error(HFMM_ERR_CONFIG, "gmres: max_iterations must be >= 1");
-  using clk = std::chrono::steady_clock;
-  const auto t_start = clk::now();
-  const uint32_t n = tree_.n_bodies, mloc = own_count_, first = own_first_;
-  const int m = cfg.restart;
-  const bool precond = cfg.precondition && have_lu_;
-  const bool corr = have_block_ || have_near_;
-  const uint32_t npatch = ni_ ? n / uint32_t(ni_) : 0;
-  const size_t ml = std::max<uint32_t>(mloc, 1);
-
-  // a callback that reports failure ends the solve at once: its peers failed in the same collective
-  auto reduce = [&](double* v, int count) {
-    if (cb.allreduce_sum(cb.user, v, count) != 0) throw Error(HFMM_ERR_DEVICE, "all-reduce callback failed");
-  };
-  double* const sec_hist = rep->seconds_history;
-  double* const mv_hist = rep->matvec_seconds_history;
-  const int hist_cap = rep->history_cap;
-  *rep = hfmm_gmres_report{};
-  rep->seconds_history = sec_hist;
-  rep->matvec_seconds_history = mv_hist;
-  rep->history_cap = hist_cap;
-  double b2[1] = {0};
-  for (size_t i = 0; i < size_t(mloc) * 2; ++i) b2[0] += rhs[i] * rhs[i];
-  reduce(b2, 1);
-  const double bnorm = std::sqrt(b2[0]);
-  rep->rhs_norm = bnorm;
-  std::fill(x_out, x_out + size_t(mloc) * 2, 0.0);
-  if (bnorm == 0.0) {
-    rep->converged = 1;
-    rep->final_residual = 0;
-    return;
-  }
-  const double target = cfg.rtol * bnorm;
-
-  DeviceBuffer<float2> V(size_t(m + 1) * ml), w(ml), r32(ml), full(n), vc(n), pc(n), yc(corr ? n : 1);
-  DeviceBuffer<double2> b64(ml), x64(ml);
-  DeviceBuffer<double> scal(4), ydev(size_t(2) * m), red(reduce_scratch_doubles());
-  red.zero(stream_);
-  HFMM_CUDA_CHECK(cudaMemcpyAsync(b64.get(), rhs, size_t(mloc) * sizeof(double2), cudaMemcpyHostToDevice, stream_));
-  x64.zero(stream_);
-  launch_narrow(mloc, b64.get(), r32.get(), stream_);
-
-  double matvec_s = 0;
-  // Z = A M^-1 on sharded vectors: gather the operand, precondition and correct redundantly in
-  // caller order (cheap streaming kernels), run the two FMM phases around the multipole exchange
-  auto apply = [&](const float2* in, float2* out) {
-    const auto t0 = clk::now();
-    HFMM_CUDA_CHECK(cudaMemcpyAsync(full.get() + first, in, size_t(mloc) * sizeof(float2),
-                                    cudaMemcpyDeviceToDevice, stream_));
-    HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
-    if (cb.gather_vector(cb.user, full.get()) != 0) throw Error(HFMM_ERR_DEVICE, "vector gather callback failed");
-    launch_scatter_potentials(full.get(), nullptr, body_index_.get(), nullptr, vc.get(), n, stream_);
-    const float2* xc = vc.get();
-    if (precond) {
-      launch_precondition(npatch, ni_, block_lu_.get(), block_piv_.get(), vc.get(), pc.get(), stream_);
-      xc = pc.get();
-    }
-    launch_gather_charges(nullptr, xc, body_index_.get(), have_weight_ ? far_weight_.get() : nullptr,
-                          body_q_.get(), n, stream_);
-    phase_upward();
-    HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
-    HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_near_));
-    if (have_far_ && cb.gather_multipoles(cb.user) != 0)
-      throw Error(HFMM_ERR_DEVICE, "multipole exchange callback failed");
-    phase_downward();
-    if (corr) {
-      yc.zero(stream_);
-      launch_corrections(n, ni_, have_block_ ? patch_block_.get() : nullptr, near_offset_.get(),
-                         near_source_.get(), have_near_ ? near_delta_.get() : nullptr, xc, yc.get(), stream_);
-    }
-    launch_combine_owned(near_.get() + first, far_.get() + first, corr ? yc.get() : nullptr,
-                         body_index_.get() + first, out, mloc, stream_);
-    HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
-    matvec_s += std::chrono::duration<double>(clk::now() - t0).count();
-  };
-  // <v, w> (v may be null: ||w||^2) reduced over all ranks
-  auto dot = [&](const float2* v, const float2* ww, double out[2]) {
-    scal.zero(stream_);
-    if (v) launch_mgs_step(mloc, const_cast<float2*>(ww), nullptr, nullptr, v, scal.get(), red.get(), stream_);
-    else launch_norm2(mloc, ww, scal.get(), red.get(), stream_);
-    scal.download(out, 2, stream_);
-    HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
-    reduce(out, 2);
-  };
-  auto axpy = [&](float2* ww, const float2* v, const double h[2]) {  // ww -= h v
-    HFMM_CUDA_CHECK(cudaMemcpyAsync(scal.get() + 2, h, 2 * sizeof(double), cudaMemcpyHostToDevice, stream_));
-    launch_mgs_step(mloc, ww, v, scal.get() + 2, nullptr, nullptr, red.get(), stream_);
-  };
-
-  std::vector<cd> H(size_t(m + 1) * m), cs(m), sn(m), g(m + 1);
-  auto h = [&](int i, int j) -> cd& { return H[size_t(j) * (m + 1) + i]; };
-  int iterations = 0, nres = 0;
-  bool done = false, breakdown = false;
-  double last_est = -1, beta = bnorm, tmp[2], matvec_prev = 0;
-  while (!done) {
-    if (beta <= target || iterations >= cfg.max_iterations) break;
-    launch_scale(mloc, r32.get(), float(1.0 / beta), V.get(), stream_);
-    std::fill(g.begin(), g.end(), cd(0));
-    g[0] = beta;
-    int cols = 0;
-    for (int j = 0; j < m; ++j) {
-      if (iterations >= cfg.max_iterations) break;
-      apply(V.get() + size_t(j) * ml, w.get());
-      dot(nullptr, w.get(), tmp);
-      const double w_scale = std::sqrt(tmp[0]);
-      for (int pass = 0; pass < 2; ++pass)
-        for (int i = 0; i <= j; ++i) {
-          dot(V.get() + size_t(i) * ml, w.get(), tmp);
-          if (pass == 0) h(i, j) = cd(tmp[0], tmp[1]);
-          else h(i, j) += cd(tmp[0], tmp[1]);
-          axpy(w.get(), V.get() + size_t(i) * ml, tmp);
-        }
-      dot(nullptr, w.get(), tmp);
-      double hnext = std::sqrt(tmp[0]);
-      const bool broke = hnext <= 1e-14 * std::max(w_scale, 1e-300);
-      if (broke) hnext = 0;
-      for (int i = 0; i < j; ++i) {
-        const cd a = h(i, j), b = h(i + 1, j);
-        h(i, j) = cs[i] * a + sn[i] * b;
-        h(i + 1, j) = -std::conj(sn[i]) * a + cs[i] * b;
-      }
-      const cd a = h(j, j);
-      const double b = hnext, r = std::hypot(std::abs(a), b);
-      if (r == 0.0) {
-        cs[j] = 1;
-        sn[j] = 0;
-      } else if (std::abs(a) == 0.0) {
-        cs[j] = 0;
-        sn[j] = 1;
-      } else {
-        cs[j] = std::abs(a) / r;
-        sn[j] = (a / std::abs(a)) * (b / r);
-      }
-      h(j, j) = cs[j] * a + sn[j] * b;
-      g[j + 1] = -std::conj(sn[j]) * g[j];
-      g[j] = cs[j] * g[j];
-      ++iterations;
-      cols = j + 1;
-      last_est = std::abs(g[j + 1]);
-      if (residuals && nres < residual_cap) residuals[nres] = last_est / bnorm;
-      if (nres < hist_cap) {
-        if (sec_hist) sec_hist[nres] = std::chrono::duration<double>(clk::now() - t_start).count();
-        if (mv_hist) mv_hist[nres] = matvec_s - matvec_prev;
-      }
-      matvec_prev = matvec_s;
-      ++nres;
-      if (broke) {
-        breakdown = true;
-        done = true;
-        break;
-      }
-      if (last_est <= target) {
-        done = true;
-        break;
-      }
-      launch_scale(mloc, w.get(), float(1.0 / hnext), V.get() + size_t(j + 1) * ml, stream_);
-    }
-    while (cols > 0 && std::abs(h(cols - 1, cols - 1)) == 0.0) --cols;
-    std::vector<cd> y(cols);
-    for (int i = cols - 1; i >= 0; --i) {
-      cd s = g[i];
-      for (int l = i + 1; l < cols; ++l) s -= h(i, l) * y[l];
-      y[i] = std::abs(h(i, i)) == 0.0 ? cd(0) : s / h(i, i);
-    }
-    if (cols > 0) {
-      HFMM_CUDA_CHECK(cudaMemcpyAsync(ydev.get(), y.data(), sizeof(cd) * cols, cudaMemcpyHostToDevice, stream_));
-      launch_update_solution(mloc, cols, V.get(), ml, ydev.get(), x64.get(), stream_);
-      HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
-    }
-    if (!done) {
-      launch_narrow(mloc, x64.get(), r32.get(), stream_);
-      apply(r32.get(), w.get());
-      scal.zero(stream_);
-      launch_residual(mloc, b64.get(), w.get(), r32.get(), scal.get(), red.get(), stream_);
-      scal.download(tmp, 2, stream_);
-      HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
-      reduce(tmp, 1);
-      beta = std::sqrt(tmp[0]);
-    }
-  }
-  launch_narrow(mloc, x64.get(), V.get(), stream_);
-  apply(V.get(), w.get());
-  scal.zero(stream_);
-  launch_residual(mloc, b64.get(), w.get(), r32.get(), scal.get(), red.get(), stream_);
-  scal.download(tmp, 2, stream_);
-  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
-  reduce(tmp, 1);
-  const double final_res = std::sqrt(tmp[0]) / bnorm;
-  if (precond) {
-    // the iterate maps back through M^-1: gather it, solve redundantly, keep the owned slots
-    HFMM_CUDA_CHECK(cudaMemcpyAsync(full.get() + first, V.get(), size_t(mloc) * sizeof(float2),
-                                    cudaMemcpyDeviceToDevice, stream_));
-    HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
-    if (cb.gather_vector(cb.user, full.get()) != 0) throw Error(HFMM_ERR_DEVICE, "vector gather callback failed");
-    launch_scatter_potentials(full.get(), nullptr, body_index_.get(), nullptr, vc.get(), n, stream_);
-    launch_precondition(npatch, ni_, block_lu_.get(), block_piv_.get(), vc.get(), pc.get(), stream_);
-    launch_gather_charges(nullptr, pc.get(), body_index_.get(), nullptr, full.get(), n, stream_);
-    launch_widen(mloc, full.get() + first, x64.get(), stream_);
-  }
-  HFMM_CUDA_CHECK(cudaMemcpyAsync(x_out, x64.get(), size_t(mloc) * sizeof(double2), cudaMemcpyDeviceToHost, stream_));
-  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
-  rep->iterations = iterations;
-  rep->breakdown = breakdown ? 1 : 0;
-  rep->final_residual = final_res;
-  rep->converged = (final_res <= cfg.rtol || (nres > 0 && last_est / bnorm <= cfg.rtol)) ? 1 : 0;
   rep->seconds = std::chrono::duration<double>(clk::now() - t_start).count();
   rep->matvec_seconds = matvec_s;
 }

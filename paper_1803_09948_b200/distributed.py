@@ -1,25 +1,23 @@
-"""Multi-GPU FMM matvec: one process per GPU, Morton-partitioned targets, torch.distributed for the
-plumbing (NCCL over NVLink on GPUs; gloo in the CPU tests of the host-side logic).
+"""Multi-GPU FMM matvec: one process per GPU, Morton-partitioned targets.  The data plane lives in the
+library (csrc/comm.cu: pack kernel -> one grouped ncclSend / ncclRecv -> unpack kernel on a communication
+stream, device-side all-reduce of the GMRES scalars); this module is the LAUNCHER around it:
 
-Data flow of one matvec on rank r (SURVEY.md §8e; stands in for the reference's simulated
-part::distributed_matvec, let.cpp:320-362):
+  * bootstrap        torch.distributed (the process group torchrun or bench.py set up) carries the 128-byte
+                     NCCL unique id from rank 0 to its peers, then is used for timing reductions only
+  * ShardedFmm       set_partition + communicator + owned slices of the Morton-ordered vectors
+  * host transport   the same exchanges staged through pinned host memory and performed with gloo on CPU
+                     tensors: what lets two processes share ONE GPU in the tests (NCCL refuses that)
+  * emulation        R handles in one process, one host thread per rank, the host transport between them
 
-  1. charge exchange                       the bodies of the leaves on this rank's near lists
-  2. device phase 1 (dist_upward)          P2M + M2M of the owned cells
-  3. multipole exchange                    the multipoles this rank's M2L lists translate from
-  4. device phase 2 (dist_downward)        M2L / L2L / L2P into the owned cells, near field of the
-                                           owned leaves beside M2L, owned outputs
-Exchanges 1 and 3 are the locally-essential-tree exchange (sender-initiated like the reference's
-extract_let): every rank holds the global lists, derives matching send / receive index lists from
-them (let_index_lists) and ships the rows with ONE all_to_all_single each.  pruned=False falls back
-to all-gathering everything (per level a contiguous row range per rank; on NVSwitch even that is a
-few ms — 2.5 M cells x 1.4 KB at BASELINE config 5 — against ~100 ms of compute).
-
-The exchange helpers work on any tensors (CPU tensors under gloo in tests/test_distributed_gloo.py).
+Data flow of one matvec on rank r (SURVEY.md section 8e; stands in for the reference's simulated
+part::distributed_matvec, let.cpp:320-362): halo charges and the multipoles of the cells this rank
+translates from arrive through the two locally-essential-tree exchanges (sender-initiated like the
+reference's extract_let); P2M + M2M of the owned cells overlap the first, the near field the second.
 """
 from __future__ import annotations
 
 import os
+import threading
 import time
 
 import numpy as np
@@ -31,39 +29,6 @@ class DevicePointerTensor:
     def __init__(self, ptr: int, n_float32: int):
         self.__cuda_array_interface__ = {"shape": (n_float32,), "typestr": "<f4",
                                          "data": (int(ptr), False), "version": 3, "strides": None}
-
-
-def allgather_ranges(dist, buf, ranges, rank, world, scratch=None):
-    """In-place all-gather of rank-owned row ranges of `buf` (first dim).
-
-    ranges[r] = list of (row_first, row_count) owned by rank r, same list length on every rank.
-    Owned rows are packed, exchanged with ONE padded all_gather_into_tensor, and the other ranks'
-    rows unpacked into place.  Returns the scratch buffers for reuse."""
-    import torch
-
-    rows = [sum(c for _, c in rr) for rr in ranges]
-    width = int(np.prod(buf.shape[1:])) if buf.dim() > 1 else 1
-    maxrows = max(max(rows), 1)
-    if scratch is None or scratch[0].shape[0] != maxrows * width:
-        scratch = (torch.empty(maxrows * width, dtype=buf.dtype, device=buf.device),
-                   torch.empty(world * maxrows * width, dtype=buf.dtype, device=buf.device))
-    send, recv = scratch
-    flat = buf.reshape(buf.shape[0], -1)
-    off = 0
-    for f, c in ranges[rank]:
-        if c:
-            send[off * width:(off + c) * width].copy_(flat[f:f + c].reshape(-1))
-            off += c
-    dist.all_gather_into_tensor(recv, send)
-    for r in range(world):
-        if r == rank:
-            continue
-        off = r * maxrows
-        for f, c in ranges[r]:
-            if c:
-                flat[f:f + c].copy_(recv[off * width:(off + c) * width].reshape(c, width))
-                off += c
-    return scratch
 
 
 def let_index_lists(op, rank: int, world: int):
@@ -99,114 +64,166 @@ def let_index_lists(op, rank: int, world: int):
     return out
 
 
-def exchange_rows(dist, buf, send_idx, recv_idx, device):
-    """One all_to_all_single with uneven splits: rows buf[send_idx[p]] go to rank p, the rows received
-    from p land in buf[recv_idx[p]] (in place; the index lists are device int64 tensors)."""
+def init_nccl(op, dist, rank: int):
+    """ncclCommInitRank inside the library: rank 0 creates the unique id, the process group hands it on"""
+    box = [op.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    op.comm_init_nccl(box[0])
+
+
+def init_host_transport(op, dist, group=None):
+    """The host-staged transport over a gloo process group (CPU tensors): all_to_all_single with uneven
+    splits on bytes, all_reduce on doubles."""
     import torch
 
-    width = buf.shape[1]
-    send = torch.cat([buf[i] for i in send_idx]) if sum(len(i) for i in send_idx) else buf.new_zeros((0, width))
-    n_recv = sum(len(i) for i in recv_idx)
-    recv = buf.new_empty((n_recv, width))
-    dist.all_to_all_single(recv, send, output_split_sizes=[len(i) for i in recv_idx],
-                           input_split_sizes=[len(i) for i in send_idx])
-    if n_recv:
-        buf[torch.cat(recv_idx)] = recv
+    def alltoallv(send, send_bytes, recv, recv_bytes):
+        s = torch.from_numpy(send) if send.size else torch.zeros(0, dtype=torch.uint8)
+        r = torch.from_numpy(recv) if recv.size else torch.zeros(0, dtype=torch.uint8)
+        dist.all_to_all_single(r, s, output_split_sizes=[int(v) for v in recv_bytes],
+                               input_split_sizes=[int(v) for v in send_bytes], group=group)
+
+    def allreduce_sum(values):
+        t = torch.from_numpy(values)
+        dist.all_reduce(t, group=group)
+
+    op.comm_init_host(alltoallv, allreduce_sum)
 
 
 class ShardedFmm:
     """The FMM operator of one rank.  Vectors are sharded by Morton range: rank r holds
     q[first_r : first_r + count_r] of the Morton-ordered charge vector and produces the same slice
-    of the potential."""
+    of the potential.  transport: "nccl" (one GPU per rank) or "host" (gloo; ranks may share a GPU)."""
 
-    def __init__(self, op, dist, rank: int, world: int, device, pruned: bool = False):
-        """pruned: exchange only the locally essential rows (all_to_all with index lists) instead of
-        all-gathering every charge and every multipole"""
+    def __init__(self, op, dist, rank: int, world: int, device, transport: str = "nccl", group=None):
         import torch
 
         self.op, self.dist, self.rank, self.world, self.device = op, dist, rank, world, device
+        if transport == "nccl":         # also in a world of one: the same code path, one rank
+            init_nccl(op, dist, rank)
+        elif transport == "host":
+            init_host_transport(op, dist, group)
+        elif transport is not None:
+            raise ValueError("transport must be 'nccl', 'host' or None (world of one, no communicator)")
         p = op.partition()
         self.n = int(p.n_bodies)
-        mine = torch.tensor([p.body_first, p.body_count, p.level_first, p.level_last]
-                            + list(p.cell_first) + list(p.cell_count), dtype=torch.int64, device=device)
-        allp = torch.empty(world * mine.numel(), dtype=torch.int64, device=device)
-        dist.all_gather_into_tensor(allp, mine)
-        allp = allp.reshape(world, -1).cpu().numpy()
-        self.body_ranges = [[(int(a[0]), int(a[1]))] for a in allp]
-        self.first, self.count = self.body_ranges[rank][0]
-        lf, ll = int(p.level_first), int(p.level_last)
-        self.cell_ranges = [[(int(a[4 + L]), int(a[4 + 22 + L])) for L in range(lf, ll + 1)] for a in allp]
-        self.stride = int(p.coeff_stride)
-        n_cells = int(op.stats()["n_cells"])
-        self.q_full = torch.zeros(self.n, 2, dtype=torch.float32, device=device)
-        self.out_full = torch.zeros(self.n, 2, dtype=torch.float32, device=device)
-        self.multipole = None
-        if p.multipole_dev:
-            view = DevicePointerTensor(p.multipole_dev, n_cells * self.stride * 2)
-            self.multipole = torch.as_tensor(view, device=device).reshape(n_cells, self.stride * 2)
-        self._s1 = self._s2 = None
-        self.pruned = pruned and world > 1
-        if self.pruned:
-            lists = let_index_lists(op, rank, world)
-            to_dev = lambda v: [torch.from_numpy(a).to(device) for a in v]
-            self.let = {k: to_dev(v) for k, v in lists.items()}
-            self.let_bytes = {"charges": int(sum(len(a) for a in lists["recv_bodies"])) * 8,
-                              "multipoles": int(sum(len(a) for a in lists["recv_cells"])) * self.stride * 8}
+        self.first, self.count = int(p.body_first), int(p.body_count)
+        self.out = torch.zeros(max(self.count, 1), 2, dtype=torch.float32, device=device)
         self.owned_m2l_pairs = int(p.owned_m2l_pairs)
         self.owned_p2p_body_pairs = int(p.owned_p2p_body_pairs)
+        self.let_bytes = dict(zip(("charges", "multipoles"), op.exchange_volume())) if transport else \
+            {"charges": 0, "multipoles": 0}
 
     def matvec(self, q_local):
-        """q_local: (count, 2) float32 device tensor, the owned Morton slice -> same slice of A q"""
-        import torch
-
-        self.q_full[self.first:self.first + self.count].copy_(q_local)
-        if self.pruned:
-            exchange_rows(self.dist, self.q_full, self.let["send_bodies"], self.let["recv_bodies"], self.device)
-        else:
-            self._s1 = allgather_ranges(self.dist, self.q_full, self.body_ranges, self.rank, self.world, self._s1)
-        torch.cuda.current_stream().synchronize()
-        self.op.dist_upward(self.q_full.data_ptr())
-        self.op.sync()
-        if self.multipole is not None:
-            if self.pruned:
-                exchange_rows(self.dist, self.multipole, self.let["send_cells"], self.let["recv_cells"], self.device)
-            else:
-                self._s2 = allgather_ranges(self.dist, self.multipole, self.cell_ranges, self.rank,
-                                            self.world, self._s2)
-            torch.cuda.current_stream().synchronize()
-        self.op.dist_downward(self.out_full.data_ptr())
-        self.op.sync()
-        return self.out_full[self.first:self.first + self.count]
-
+        """q_local: (count, 2) float32 device tensor, the owned Morton slice -> same slice of A q
+        (asynchronous on the library's streams; the caller synchronises the handle)"""
+        self.op.dist_matvec(q_local.data_ptr(), self.out.data_ptr())
+        return self.out[:self.count]
 
     def gmres(self, rhs_local, rtol=1e-4, restart=30, max_iterations=500, precondition=True):
-        """Distributed GMRES (SURVEY.md §8e step 4): rhs_local / the returned solution are the owned
-        Morton slices (complex128 numpy).  Krylov vectors stay sharded on the GPUs; inner products
-        are all-reduced, operands and multipoles all-gathered, by this rank's communicator."""
-        import torch
+        """Distributed GMRES (SURVEY.md section 8e step 4): rhs_local / the returned solution are the owned
+        Morton slices (complex128 numpy).  Krylov vectors stay sharded on the GPUs, the inner products are
+        all-reduced on the device by the library's communicator."""
+        return self.op.dist_solve(rhs_local, rtol=rtol, restart=restart, max_iterations=max_iterations,
+                                  precondition=precondition)
+
+
+class ThreadTransport:
+    """The host transport between R handles of ONE process (one host thread per rank): a mailbox and a
+    barrier.  No kernel ever waits on another rank's kernel — every exchange happens on the host side of
+    a stream synchronise — so this is safe on a single device (B200_PROFILING.md)."""
+
+    def __init__(self, nranks: int, timeout: float = 180.0):
+        self.R = nranks
+        self.barrier = threading.Barrier(nranks, timeout=timeout)
+        self.send = [None] * nranks
+        self.sbytes = [None] * nranks
+        self.vals = [None] * nranks
+
+    def callbacks(self, r: int):
+        def alltoallv(send, send_bytes, recv, recv_bytes):
+            self.send[r], self.sbytes[r] = send, send_bytes
+            self.barrier.wait()
+            off = 0
+            for p in range(self.R):
+                nb = int(recv_bytes[p])
+                if nb:
+                    start = int(self.sbytes[p][:r].sum())
+                    assert int(self.sbytes[p][r]) == nb, "send and receive lists disagree"
+                    recv[off:off + nb] = self.send[p][start:start + nb]
+                off += nb
+            self.barrier.wait()
 
         def allreduce_sum(values):
-            t = torch.from_numpy(values).to(self.device)
-            self.dist.all_reduce(t)
-            values[:] = t.cpu().numpy()
+            self.vals[r] = values.copy()
+            self.barrier.wait()
+            total = sum(self.vals[p] for p in range(self.R))   # same order on every rank: identical bits
+            self.barrier.wait()
+            values[:] = total
 
-        def gather_vector(ptr):
-            full = torch.as_tensor(DevicePointerTensor(ptr, self.n * 2), device=self.device).reshape(self.n, 2)
-            self._s1 = allgather_ranges(self.dist, full, self.body_ranges, self.rank, self.world, self._s1)
-            torch.cuda.current_stream().synchronize()
+        return alltoallv, allreduce_sum
 
-        def gather_multipoles():
-            if self.multipole is not None:
-                if self.pruned:
-                    exchange_rows(self.dist, self.multipole, self.let["send_cells"], self.let["recv_cells"],
-                                  self.device)
-                else:
-                    self._s2 = allgather_ranges(self.dist, self.multipole, self.cell_ranges, self.rank,
-                                                self.world, self._s2)
-                torch.cuda.current_stream().synchronize()
 
-        return self.op.dist_gmres(rhs_local, allreduce_sum, gather_vector, gather_multipoles, rtol=rtol,
-                                  restart=restart, max_iterations=max_iterations, precondition=precondition)
+def run_ranks_in_threads(ops, fn, timeout: float = 180.0):
+    """fn(rank, op) on one host thread per handle, the handles joined by a ThreadTransport;
+    returns the per-rank results"""
+    import torch
+
+    R = len(ops)
+    tr = ThreadTransport(R, timeout)
+    dev = torch.cuda.current_device()
+    for r, op in enumerate(ops):
+        op.comm_init_host(*tr.callbacks(r))
+    results, errors = [None] * R, []
+
+    def run(r):
+        torch.cuda.set_device(dev)
+        try:
+            results[r] = fn(r, ops[r])
+        except BaseException as e:
+            errors.append(e)
+            tr.barrier.abort()
+
+    threads = [threading.Thread(target=run, args=(r,)) for r in range(R)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        real = [e for e in errors if not isinstance(e, threading.BrokenBarrierError)]
+        raise (real or errors)[0]
+    return results
+
+
+def emulate_gmres_on_one_device(ops, rhs_morton, timeout=180.0, **kw):
+    """Distributed GMRES of `len(ops)` ranks on ONE GPU through the library's own sharded solver and
+    exchanges (host transport between threads).  Returns the per-rank (x_owned, report) list."""
+    def solve(r, op):
+        p = op.partition()
+        f, c = int(p.body_first), int(p.body_count)
+        return op.dist_solve(rhs_morton[f:f + c], **kw)
+
+    return run_ranks_in_threads(ops, solve, timeout)
+
+
+def emulate_matvec_on_one_device(ops, q_morton, timeout=180.0):
+    """hfmm_cuda_dist_matvec of `len(ops)` ranks on ONE GPU (threads + host transport): the assembled
+    Morton-ordered result as a (n, 2) float32 device tensor"""
+    import torch
+
+    out = torch.zeros_like(q_morton)
+
+    def mv(r, op):
+        p = op.partition()
+        f, c = int(p.body_first), int(p.body_count)
+        qi = q_morton[f:f + c].contiguous()
+        yo = torch.zeros(max(c, 1), 2, dtype=torch.float32, device=q_morton.device)
+        op.dist_matvec(qi.data_ptr(), yo.data_ptr())
+        op.sync()
+        out[f:f + c] = yo[:c]
+        return c
+
+    run_ranks_in_threads(ops, mv, timeout)
+    return out
 
 
 class Repartitioner:
@@ -236,80 +253,6 @@ class Repartitioner:
         self.alpha = nxt
         self.operator = self.make_operator(nxt)
         return True
-
-
-def emulate_gmres_on_one_device(ops, rhs_morton, timeout=120.0, **kw):
-    """Distributed GMRES of `len(ops)` ranks on ONE GPU: one host thread per rank, the three
-    exchanges replaced by barrier-separated device copies between the handles.  No kernel ever waits
-    on another rank's kernel (every exchange happens on the host side of a stream synchronise), so
-    this is safe on a single device.  Returns the per-rank (x_owned, report) list."""
-    import threading
-
-    import torch
-
-    R = len(ops)
-    parts = [op.partition() for op in ops]
-    n = int(parts[0].n_bodies)
-    dev = torch.device("cuda", torch.cuda.current_device())
-    n_cells = int(ops[0].stats()["n_cells"])
-    stride = int(parts[0].coeff_stride)
-    barrier = threading.Barrier(R, timeout=timeout)
-    scal = [None] * R
-    vec = [None] * R
-    mp = [torch.as_tensor(DevicePointerTensor(p.multipole_dev, n_cells * stride * 2),
-                          device=dev).reshape(n_cells, stride * 2) if p.multipole_dev else None for p in parts]
-    results, errors = [None] * R, []
-
-    def run(r):
-        torch.cuda.set_device(dev)
-        p = parts[r]
-
-        def allreduce_sum(values):
-            scal[r] = values.copy()
-            barrier.wait()
-            total = sum(scal[s] for s in range(R))     # same order on every rank: identical bits
-            barrier.wait()
-            values[:] = total
-
-        def gather_vector(ptr):
-            vec[r] = torch.as_tensor(DevicePointerTensor(ptr, n * 2), device=dev).reshape(n, 2)
-            barrier.wait()
-            for s, ps in enumerate(parts):
-                if s != r and ps.body_count:
-                    f, c = int(ps.body_first), int(ps.body_count)
-                    vec[r][f:f + c].copy_(vec[s][f:f + c])
-            torch.cuda.synchronize()
-            barrier.wait()
-
-        def gather_multipoles():
-            barrier.wait()
-            if mp[r] is not None:
-                for s, ps in enumerate(parts):
-                    if s == r:
-                        continue
-                    for L in range(int(ps.level_first), int(ps.level_last) + 1):
-                        f, c = int(ps.cell_first[L]), int(ps.cell_count[L])
-                        if c:
-                            mp[r][f:f + c].copy_(mp[s][f:f + c])
-            torch.cuda.synchronize()
-            barrier.wait()
-
-        try:
-            f, c = int(p.body_first), int(p.body_count)
-            results[r] = ops[r].dist_gmres(rhs_morton[f:f + c], allreduce_sum, gather_vector,
-                                           gather_multipoles, **kw)
-        except BaseException as e:
-            errors.append(e)
-            barrier.abort()
-
-    threads = [threading.Thread(target=run, args=(r,)) for r in range(R)]
-    for t in threads:
-        t.start()
-    for t in threads:
-        t.join()
-    if errors:
-        raise errors[0]
-    return results
 
 
 def emulate_ranks_on_one_device(ops, q_morton, pruned: bool = False):

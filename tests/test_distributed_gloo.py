@@ -1,5 +1,6 @@
 """Host-side logic of the multi-GPU mode on CPU: the Morton partition (no device needed) and the
-range all-gather under a 2-rank gloo group."""
+host transport of the library's data plane (all-to-all-v on bytes, all-reduce on doubles) under a 2-rank
+gloo group."""
 import os
 import socket
 
@@ -11,8 +12,8 @@ from paper_1803_09948_b200.workloads import plummer_points, sphere_points
 
 
 @pytest.mark.parametrize("xyz,k,ncrit,cap,theta", [
-    (sphere_points(20000, 1), 4.0, 64, 0.25, 0.4),
-    (plummer_points(15000, 2, 0.05), 8.0, 64, 0.125, 0.35),
+    (sphere_points(200000, 1), 4.0, 64, 0.25, 0.4),          # BASELINE cfg 2 / cfg 5 parameters
+    (plummer_points(150000, 2, 0.05), 8.0, 64, 0.125, 0.35),  # BASELINE cfg 4 parameters
 ])
 @pytest.mark.parametrize("nranks", [2, 4, 8])
 def test_morton_partition_tiles_and_balances(xyz, k, ncrit, cap, theta, nranks):
@@ -40,7 +41,8 @@ def test_morton_partition_tiles_and_balances(xyz, k, ncrit, cap, theta, nranks):
     np.add.at(w, cell_rank[m2l_t], 1600.0)
     np.add.at(w, cell_rank[p2p[:, 0]], cells[p2p[:, 0], 5].astype(float) * cells[p2p[:, 1], 5])
     assert w.min() > 0
-    assert w.max() / w.mean() < (1.6 if nranks <= 4 else 2.2)
+    # the slowest rank sets the matvec time: 5 % imbalance is the most the >= 80 % scaling target leaves room for
+    assert w.max() / w.mean() < 1.05
 
 
 def _free_port():
@@ -51,52 +53,48 @@ def _free_port():
     return p
 
 
+class _FakeHandle:
+    """stands in for HfmmCuda.comm_init_host: keeps the two callbacks the launcher installs"""
+
+    def comm_init_host(self, alltoallv, allreduce_sum):
+        self.alltoallv, self.allreduce_sum = alltoallv, allreduce_sum
+
+
 def _worker(rank, world, port, q):
-    import torch
     import torch.distributed as dist
 
-    from paper_1803_09948_b200.distributed import allgather_ranges
+    from paper_1803_09948_b200.distributed import init_host_transport
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        # rows owned per rank: two ranges each (as two tree levels), uneven sizes
-        ranges = [[(0, 3), (10, 2)], [(3, 7), (12, 5)]]
-        truth = torch.arange(17 * 4, dtype=torch.float32).reshape(17, 4)
-        buf = torch.full((17, 4), -1.0)
-        for f, c in ranges[rank]:
-            buf[f:f + c] = truth[f:f + c]
-        scratch = allgather_ranges(dist, buf, ranges, rank, world)
-        ok1 = bool((buf == truth).all())
-        # reuse of the scratch buffers, 1-D payload, body-range style
-        br = [[(0, 9)], [(9, 4)]]
-        v = torch.zeros(13, 2)
-        v[br[rank][0][0]:br[rank][0][0] + br[rank][0][1]] = float(rank + 1)
-        allgather_ranges(dist, v, br, rank, world)
-        ok2 = bool((v[:9] == 1).all() and (v[9:] == 2).all())
-        # locally-essential-tree exchange: uneven all_to_all with index lists (rows sent to the peer /
-        # rows received from it), in place
-        from paper_1803_09948_b200.distributed import exchange_rows
-        truth = torch.arange(12 * 3, dtype=torch.float32).reshape(12, 3)
-        own = [torch.tensor([0, 1, 2, 3, 4, 5]), torch.tensor([6, 7, 8, 9, 10, 11])]
-        need = [torch.tensor([7, 10, 11]), torch.tensor([1, 4])]      # rows rank r needs from the other rank
-        buf = torch.full((12, 3), -1.0)
-        buf[own[rank]] = truth[own[rank]]
-        empty = torch.zeros(0, dtype=torch.int64)
-        send = [empty, empty]
-        recv = [empty, empty]
-        send[1 - rank] = need[1 - rank]
-        recv[1 - rank] = need[rank]
-        exchange_rows(dist, buf, send, recv, "cpu")
-        have = torch.cat([own[rank], need[rank]])
-        rest = torch.tensor([i for i in range(12) if i not in set(have.tolist())])
-        ok3 = bool((buf[have] == truth[have]).all() and (buf[rest] == -1).all())
-        q.put((rank, ok1 and ok2 and ok3 and scratch is not None))
+        h = _FakeHandle()
+        init_host_transport(h, dist)
+        # uneven blocks, as the locally-essential-tree exchange produces them: rank 0 sends 24 bytes to rank 1
+        # and expects 40 back; the own block is empty
+        sizes = {0: [0, 24], 1: [40, 0]}
+        send_bytes = np.array(sizes[rank], dtype=np.uint64)
+        recv_bytes = np.array([sizes[p][rank] for p in range(world)], dtype=np.uint64)
+        send = (np.arange(int(send_bytes.sum()), dtype=np.uint8) + 100 * rank).astype(np.uint8)
+        recv = np.full(int(recv_bytes.sum()), 255, dtype=np.uint8)
+        h.alltoallv(send, send_bytes, recv, recv_bytes)
+        other = 1 - rank
+        ok1 = np.array_equal(recv, (np.arange(sizes[other][rank], dtype=np.uint8) + 100 * other).astype(np.uint8))
+        # an exchange in which one side sends nothing
+        sb = np.array([0, 8] if rank == 0 else [0, 0], dtype=np.uint64)
+        rb = np.array([0, 0] if rank == 0 else [8, 0], dtype=np.uint64)
+        r2 = np.zeros(int(rb.sum()), dtype=np.uint8)
+        h.alltoallv(np.full(int(sb.sum()), 7, dtype=np.uint8), sb, r2, rb)
+        ok2 = rank == 0 or bool((r2 == 7).all())
+        v = np.array([1.5 + rank, -2.0 * rank, 1e-300], dtype=np.float64)
+        h.allreduce_sum(v)
+        ok3 = np.array_equal(v, np.array([1.5 + 2.5, -2.0, 2e-300]))
+        q.put((rank, bool(ok1 and ok2 and ok3)))
     finally:
         dist.destroy_process_group()
 
 
-def test_range_allgather_two_ranks_gloo():
+def test_host_transport_two_ranks_gloo():
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
@@ -109,3 +107,35 @@ def test_range_allgather_two_ranks_gloo():
     for p in procs:
         p.join(timeout=60)
     assert sorted(res) == [(0, True), (1, True)]
+
+
+def test_thread_transport_moves_uneven_blocks():
+    """the in-process transport of the emulated ranks: same contract as the gloo one"""
+    import threading
+
+    from paper_1803_09948_b200.distributed import ThreadTransport
+
+    R = 3
+    tr = ThreadTransport(R, timeout=30)
+    sizes = [[0, 3, 5], [2, 0, 1], [4, 6, 0]]       # sizes[s][d]: bytes rank s sends to rank d
+    out = [None] * R
+
+    def run(r):
+        a2a, red = tr.callbacks(r)
+        sb = np.array(sizes[r], dtype=np.uint64)
+        rb = np.array([sizes[p][r] for p in range(R)], dtype=np.uint64)
+        send = np.concatenate([np.full(sizes[r][d], 10 * r + d, dtype=np.uint8) for d in range(R)])
+        recv = np.zeros(int(rb.sum()), dtype=np.uint8)
+        a2a(send, sb, recv, rb)
+        v = np.array([float(r + 1)])
+        red(v)
+        out[r] = (recv, v[0])
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(R)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for r in range(R):
+        want = np.concatenate([np.full(sizes[p][r], 10 * p + r, dtype=np.uint8) for p in range(R)])
+        assert np.array_equal(out[r][0], want) and out[r][1] == 6.0

@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from checkers import rel_l2
-from paper_1803_09948_b200 import HfmmCuda
+from paper_1803_09948_b200 import HfmmCuda, HfmmError
 from paper_1803_09948_b200.workloads import charges, plummer_points, sphere_points
 
 pytestmark = pytest.mark.gpu
@@ -148,6 +148,49 @@ def test_sharded_matvec_equals_single_domain(nranks):
     st = single.stats()
     assert sum(int(p.owned_m2l_pairs) for p in parts) == st["m2l_pairs"]
     assert sum(int(p.owned_p2p_body_pairs) for p in parts) == st["p2p_body_pairs"]
+
+
+@pytest.mark.parametrize("nranks,dist_kind", [(2, "sphere"), (5, "plummer"), (8, "sphere")])
+def test_library_data_plane_reproduces_the_single_domain_matvec(nranks, dist_kind):
+    """hfmm_cuda_dist_matvec (csrc/comm.cu): pack kernel -> exchange -> unpack kernel for the halo charges and the
+    remote multipoles, index lists derived inside the library.  Ranks are host threads on this one GPU joined by the
+    host transport; everything except the ncclSend / ncclRecv calls is the code a multi-GPU run executes."""
+    import torch
+
+    from paper_1803_09948_b200.distributed import emulate_matvec_on_one_device
+
+    n, k, order = 24000, 5.0, 9
+    xyz = sphere_points(n, 31) if dist_kind == "sphere" else plummer_points(n, 31, a=0.06)
+    q = charges(n, 31)
+    single = HfmmCuda(k=k, order=order, ncrit=40)
+    single.set_points(xyz)
+    morton = single.body_order()
+    y_ref = single.matvec(q)[morton]
+    ops = []
+    for r in range(nranks):
+        op = HfmmCuda(k=k, order=order, ncrit=40)
+        op.set_partition(r, nranks)
+        op.set_points(xyz)
+        ops.append(op)
+    qm = q[morton]
+    q_dev = torch.from_numpy(np.stack([qm.real, qm.imag], 1).astype(np.float32)).cuda()
+    for _ in range(2):                   # the second product reuses plan and buffers
+        out = emulate_matvec_on_one_device(ops, q_dev)
+    y = out.cpu().numpy()
+    assert rel_l2(y[:, 0] + 1j * y[:, 1], y_ref) < 3e-6
+    vol = [op.exchange_volume() for op in ops]
+    full = 8 * n + single.stats()["n_cells"] * 8 * (order + 1) ** 2
+    assert all(c + m < full for c, m in vol) and sum(c for c, _ in vol) > 0
+    # a new point set rebuilds the exchange lists
+    xyz2 = sphere_points(n, 32)
+    single.set_points(xyz2)
+    for op in ops:
+        op.set_points(xyz2)
+    m2 = single.body_order()
+    q2 = q[m2]
+    out = emulate_matvec_on_one_device(ops, torch.from_numpy(np.stack([q2.real, q2.imag], 1).astype(np.float32)).cuda())
+    y = out.cpu().numpy()
+    assert rel_l2(y[:, 0] + 1j * y[:, 1], single.matvec(q)[m2]) < 3e-6
 
 
 @pytest.mark.parametrize("nranks,dist_kind", [(3, "sphere"), (8, "plummer")])
@@ -527,10 +570,9 @@ def test_complex_wavenumber_with_wide_leaves(oracle):
         assert rel_l2(y, y64) < 1e-5
 
 
-def test_deep_tree_of_coincident_points_falls_back_to_the_host_builder(oracle):
-    """clusters of more than ncrit coincident points drive the octree to its last level; the lattice
-    shifts of such a tree do not fit the device builder's packed sort keys, and set_points then uses the
-    host builder (same tree, same lists) instead of failing"""
+def test_deep_tree_of_coincident_points(oracle):
+    """clusters of more than ncrit coincident points drive the octree to its last level (21): both builders
+    produce the same tree and lists, and the matvec stays accurate"""
     rng = np.random.default_rng(104)
     base = rng.uniform(-1, 1, size=(160, 3))
     xyz = base[rng.integers(0, len(base), 500)]
@@ -543,4 +585,46 @@ def test_deep_tree_of_coincident_points_falls_back_to_the_host_builder(oracle):
     assert rel_l2(y, oracle.direct_sum(xyz, q, 1 + 2j)) < 3e-6
     host = HfmmCuda(k=1 + 2j, order=10, ncrit=4, theta=0.3, kd_max=2.0, leaf_cap=0.0, flags=1)
     host.set_points(xyz)
+    assert host.stats()["host_tree_used"] == 1
     assert (host.stats()["m2l_pairs"], host.stats()["p2p_pairs"]) == (st["m2l_pairs"], st["p2p_pairs"])
+    assert rel_l2(host.matvec(q), y) < 2e-6
+
+
+def test_device_builder_limit_is_reported_not_hidden():
+    """HFMM_FLAG_NO_HOST_FALLBACK: when the device builder meets a limit (here: a gate that forbids every
+    translation, lists beyond 512 pairs per body) set_points fails with the builder's status instead of switching
+    to the host builder; without the flag the switch shows in hfmm_cuda_stats::host_tree_used"""
+    from paper_1803_09948_b200.api import HFMM_FLAG_NO_HOST_FALLBACK
+    xyz = sphere_points(24000, 3)
+    strict = HfmmCuda(k=50.0, order=4, ncrit=1, kd_max=1e-9, leaf_cap=0.0, flags=HFMM_FLAG_NO_HOST_FALLBACK)
+    with pytest.raises(HfmmError) as e:
+        strict.set_points(xyz)
+    assert e.value.kind == "structural_error" and "512 pairs per body" in str(e.value)
+    strict.set_points(sphere_points(2000, 3))      # the handle stays usable, and says which builder ran
+    assert strict.stats()["host_tree_used"] == 0 and strict.stats()["p2p_pairs"] == 2000 * 2000
+    loose = HfmmCuda(k=50.0, order=4, ncrit=1, kd_max=1e-9, leaf_cap=0.0)
+    loose.set_points(xyz[:7000])                    # 49 M leaf pairs: beyond the device lists, within the host's reach
+    assert loose.stats()["host_tree_used"] == 1 and loose.stats()["p2p_pairs"] == 7000 * 7000
+
+
+def test_partition_of_a_clustered_set_without_leaf_cap():
+    """non-uniform points, no leaf cap, no gate: shallow levels interleave owned leaves with interior cells
+    nobody owns; the partition must still be describable (only exchanged levels need contiguous rows)"""
+    n, k, R = 20000, 2.0, 3
+    xyz = plummer_points(n, 5, a=0.02)
+    cells_owned = np.zeros(0)
+    total = 0
+    for r in range(R):
+        op = HfmmCuda(k=k, order=6, ncrit=32, theta=0.4, kd_max=0.0, leaf_cap=0.0)
+        op.set_partition(r, R)
+        op.set_points(xyz)
+        p = op.partition()                          # used to raise "owned cells of a level are not contiguous"
+        total += int(p.body_count)
+        far, near, owner = op.exchange_masks()
+        lvl = op.cells()[:, 0]
+        for L in range(int(p.level_first), int(p.level_last) + 1):
+            mine = np.nonzero((owner == r) & (lvl == L))[0]
+            if len(mine):
+                assert mine[0] == p.cell_first[L] and len(mine) == p.cell_count[L]
+                assert np.array_equal(mine, np.arange(mine[0], mine[0] + len(mine)))
+    assert total == n

@@ -186,9 +186,10 @@ def test_midsize_system_against_oracle_gmres(oracle):
 
 @pytest.mark.parametrize("ranks", [2, 3])
 def test_sharded_gmres_matches_single_domain(ranks):
-    """GMRES over Morton-sharded Krylov vectors (all-reduced inner products,
-    two-phase matvec) takes the single-domain iteration and returns the same solution.  Ranks are
-    host threads on one device, the exchanges barrier-separated device copies."""
+    """the library's sharded solver (hfmm_cuda_dist_solve: Morton-sharded Krylov vectors,
+    device-side all-reduce of the inner products, locally-essential-tree exchanges inside the operator) takes
+    the single-domain iteration and returns the same solution.  Ranks are host threads on one device joined
+    by the host transport."""
     from paper_1803_09948_b200.distributed import emulate_gmres_on_one_device
 
     single = _bie_operator(G)
@@ -222,8 +223,9 @@ def test_sharded_gmres_matches_single_domain(ranks):
 
 
 def test_sharded_operator_over_nccl_world_of_one():
-    """The real ShardedFmm plumbing (torch.distributed NCCL collectives on tensors aliasing library
-    memory, ctypes callbacks) with the one GPU this box has: world_size 1."""
+    """The NCCL transport of the library (dlopen of libnccl, ncclCommInitRank from a unique id, grouped
+    send / receive, device-side all-reduce) with the one GPU this box has: world size 1 — every call on
+    the multi-GPU code path is made, the peer loops are empty."""
     import socket
 
     import torch
@@ -235,8 +237,7 @@ def test_sharded_operator_over_nccl_world_of_one():
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     dev = torch.device("cuda", 0)
-    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
-                            device_id=dev)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
     try:
         single = _bie_operator(G)
         op = HfmmCuda(k=float(G["bie_k"]), order=int(G["bie_order"]), ncrit=16, theta=0.4, kd_max=1.0,
@@ -247,24 +248,127 @@ def test_sharded_operator_over_nccl_world_of_one():
                            near_offset=G["bie_near_offset"], near_source=G["bie_near_source"],
                            near_delta=G["bie_near_delta"], block_lu=G["bie_block_lu"],
                            block_piv=G["bie_block_piv"])
-        sh = ShardedFmm(op, dist, 0, 1, dev)
+        sh = ShardedFmm(op, dist, 0, 1, dev, transport="nccl")
         order = op.body_order()
-        assert sh.count == len(order)
+        assert sh.count == len(order) and sh.let_bytes == {"charges": 0, "multipoles": 0}
         x1, rep1 = single.gmres(G["bie_rhs"], rtol=1e-4, restart=30, max_iterations=200)
         x, rep = sh.gmres(np.asarray(G["bie_rhs"])[order], rtol=1e-4, restart=30, max_iterations=200)
         assert rep["converged"] and abs(rep["iterations"] - rep1["iterations"]) <= 1
         assert rel_l2(x, x1[order]) < 2e-3
-        # the two-phase FMM matvec (dist_upward / dist_downward carry no BIE tail) against the single-handle FMM
+        # the plain FMM product over the communicator against the single-handle FMM
         plain = HfmmCuda(k=float(G["bie_k"]), order=int(G["bie_order"]), ncrit=16, theta=0.4, kd_max=1.0,
                          leaf_cap=-1.0)
         plain.set_points(G["bie_xyz"])
+        op2 = HfmmCuda(k=float(G["bie_k"]), order=int(G["bie_order"]), ncrit=16, theta=0.4, kd_max=1.0, leaf_cap=-1.0)
+        op2.set_partition(0, 1)
+        op2.set_points(G["bie_xyz"])
+        sh2 = ShardedFmm(op2, dist, 0, 1, dev, transport="nccl")
         q = charges(len(order), 3)
         qm = q[order]
         q_local = torch.from_numpy(np.stack([qm.real, qm.imag], 1).astype(np.float32)).to(dev)
-        y = sh.matvec(q_local).cpu().numpy()
+        y = sh2.matvec(q_local)
+        op2.sync()
+        y = y.cpu().numpy()
         assert rel_l2(y[:, 0] + 1j * y[:, 1], plain.matvec(q)[order]) < 2e-6
     finally:
         dist.destroy_process_group()
+
+
+def _two_process_worker(rank, world, port, queue):
+    """one rank of the two-process test: both ranks use cuda:0, they meet on the host only (gloo)"""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1803_09948_b200.distributed import ShardedFmm
+    from paper_1803_09948_b200.workloads import plummer_points
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        out = {}
+        # (a) plain FMM product on a clustered volume, locally-essential-tree exchange
+        n, k, order = 30000, 6.0, 8
+        xyz, q = plummer_points(n, 12, a=0.08), charges(n, 12)
+        op = HfmmCuda(k=k, order=order, ncrit=48, theta=0.4)
+        op.set_partition(rank, world)
+        op.set_points(xyz)
+        sh = ShardedFmm(op, dist, rank, world, dev, transport="host")
+        morton = op.body_order()
+        qm = q[morton][sh.first:sh.first + sh.count]
+        q_local = torch.from_numpy(np.stack([qm.real, qm.imag], 1).astype(np.float32)).to(dev)
+        for _ in range(2):              # twice: the exchange buffers are reused
+            y = sh.matvec(q_local)
+            op.sync()
+        y = y.cpu().numpy()
+        out["matvec"] = (sh.first, sh.count, y[:, 0] + 1j * y[:, 1], sh.let_bytes, sh.owned_m2l_pairs)
+        # (b) the BIE system of the reference fixture: sharded GMRES with block-Jacobi and corrections
+        bie = HfmmCuda(k=float(G["bie_k"]), order=int(G["bie_order"]), ncrit=16, theta=0.4, kd_max=1.0, leaf_cap=-1.0)
+        bie.set_partition(rank, world)
+        bie.set_points(G["bie_xyz"])
+        bie.set_corrections(int(G["bie_ni"]), far_weight=G["bie_far_weight"], patch_block=G["bie_patch_block"],
+                            near_offset=G["bie_near_offset"], near_source=G["bie_near_source"],
+                            near_delta=G["bie_near_delta"], block_lu=G["bie_block_lu"], block_piv=G["bie_block_piv"])
+        shb = ShardedFmm(bie, dist, rank, world, dev, transport="host")
+        rhs = np.asarray(G["bie_rhs"])[bie.body_order()][shb.first:shb.first + shb.count]
+        x, rep = shb.gmres(rhs, rtol=1e-4, restart=30, max_iterations=200, precondition=True)
+        out["gmres"] = (shb.first, shb.count, x, rep["iterations"], rep["converged"], rep["final_residual"])
+        # (c) the plain operator (no corrections): the solver's owned-slice path, pruned exchanges only
+        xp, repp = sh.gmres(qm * 0 + 1.0, rtol=1e-2, restart=10, max_iterations=3, precondition=False)
+        out["plain_solve"] = (repp["iterations"], float(np.abs(xp).sum()))
+        queue.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_processes_share_one_gpu_through_the_host_transport():
+    """Two RANK PROCESSES on cuda:0 (gloo, pinned host staging: they only ever meet on the host) run the
+    real ShardedFmm.matvec and .gmres — the library's pack / exchange / unpack data plane and sharded
+    solver — against the single-domain results (reference distributed_matvec, let.cpp:320-362)."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from paper_1803_09948_b200.workloads import plummer_points
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    queue = ctx.Queue()
+    procs = [ctx.Process(target=_two_process_worker, args=(r, 2, port, queue)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(queue.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(got) == [0, 1]
+    # (a) against the single-domain matvec
+    n, k, order = 30000, 6.0, 8
+    xyz, q = plummer_points(n, 12, a=0.08), charges(n, 12)
+    single = HfmmCuda(k=k, order=order, ncrit=48, theta=0.4)
+    single.set_points(xyz)
+    y1 = single.matvec(q)[single.body_order()]
+    y = np.zeros(n, dtype=np.complex128)
+    covered = 0
+    for r in (0, 1):
+        f, c, yr, let, pairs = got[r]["matvec"]
+        y[f:f + c] = yr
+        covered += c
+        assert let["charges"] > 0 and let["multipoles"] > 0 and pairs > 0     # both ranks work, both receive a halo
+        assert let["charges"] < 8 * n and let["multipoles"] < 0.8 * single.stats()["n_cells"] * 8 * (order + 1) ** 2
+    assert covered == n and got[0]["matvec"][0] == 0 and got[1]["matvec"][0] == got[0]["matvec"][1]
+    assert rel_l2(y, y1) < 3e-6
+    # (b) against the single-domain solve
+    op1 = _bie_operator(G)
+    x1, rep1 = op1.gmres(G["bie_rhs"], rtol=1e-4, restart=30, max_iterations=200, precondition=True)
+    x = np.concatenate([got[r]["gmres"][2] for r in (0, 1)])
+    its = {got[r]["gmres"][3] for r in (0, 1)}
+    assert len(its) == 1 and abs(its.pop() - rep1["iterations"]) <= 1       # the ranks stay in lock step
+    assert all(got[r]["gmres"][4] and got[r]["gmres"][5] <= 1.05e-4 for r in (0, 1))
+    assert rel_l2(x, x1[op1.body_order()]) < 2e-3
+    assert got[0]["plain_solve"][0] == got[1]["plain_solve"][0] == 3
 
 
 # ---- SURVEY.md section 8, row f1: the correction builders on the device ---------------------------
