@@ -3,7 +3,8 @@
 
     python bench.py --gpus 1 --steps K --warmup W              # this repo's CUDA path
     python bench.py --impl reference --gpus 1 --steps K ...     # the reference's CPU path, same metric
-    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...   # N > 1
+    python bench.py --gpus N ...                                # N > 1: spawns its own N ranks (one per GPU)
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...   # N > 1 under torchrun
 
 A "step" is one FMM matvec (P2M, M2M, M2L, L2L, L2P, P2P) over one synthetic charge vector.
 N = 1 runs BASELINE.json configs[1] (1,048,576 points on the unit sphere, k = 4, P = 12,
@@ -123,22 +124,23 @@ def cpu_reference_arm(cfg, n_sample: int, steps: int, warmup: int, budget_s: flo
 def run_reference(args, cfg, rank: int):
     if rank != 0:
         return
-    # The sample is a quarter of the points (262,144 of cfg 2's 1,048,576): the reference rebuilds one
-    # dense translation matrix per distinct shift on every call (traversal.cpp:252-256), a cost that
-    # does not shrink with the sample (6 s per matvec on 16 cores), so a small sample would understate
-    # its throughput: measured 0.0026 / 0.0052 / 0.0059 Mpoints/s at 16 k / 131 k / 262 k points.
-    # One matvec takes ~45 s on 16 cores; the arm is budgeted to ~170 s: at most one warm-up and as
-    # many of the requested timed matvecs as fit.
-    warmup = min(args.warmup, 1)
-    base = cpu_reference_arm(cfg, args.ref_arm_points, max(1, min(args.steps, 7)), warmup, budget_s=170.0)
-    steps = base["steps"]
+    # The arm runs the configuration it prints: by default ALL of cfg 2 (1,048,576 points), one matvec and no
+    # warm-up — about three to four minutes on this box's host cores (the reference rebuilds ~10^4 dense
+    # translation matrices on every call and streams a 457 KB matrix per cell pair).  --ref-arm-points N
+    # shrinks it; the config printed is then that of the N-point run, so the line never claims a size it did
+    # not run.
+    n_run = min(args.ref_arm_points or cfg.n, cfg.n)
+    full = n_run == cfg.n
+    warmup = 0 if full else min(args.warmup, 1)
+    steps = 1 if full else max(1, min(args.steps, 7))
+    base = cpu_reference_arm(cfg, n_run, steps, warmup, budget_s=0.0 if full else 170.0)
     line = {
         "impl": "reference", "metric": METRIC, "value": base["value"], "unit": UNIT,
-        "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
+        "n_gpus": args.gpus, "steps": base["steps"], "warmup": warmup,
         "steps_requested": args.steps, "warmup_requested": args.warmup,
         "ms_per_step": base["seconds_per_matvec"] * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(cfg, cfg.n, args.gpus), "cpu_baseline": base,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(cfg, n_run, 1), "cpu_baseline": base,
         "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -152,6 +154,55 @@ def workload_config(cfg, n_total: int, gpus: int) -> dict:
             "theta": cfg.theta, "kd_max": cfg.kd_max, "leaf_cap": cfg.resolved_leaf_cap(),
             "parallelism": f"morton{gpus}" if gpus > 1 else "single",
             "l2": "working set (expansions + lists + bodies) > 126 MB L2; no explicit flush"}
+
+
+def committed_traffic(cfg, n: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the dominant launch from the committed `ncu --set full`
+    capture of this configuration (profiles/m2l_dram_traffic.json names the report it was read from and the
+    commit it was taken at); None when no capture of this configuration is on record"""
+    try:
+        rec = json.load(open(os.path.join(ROOT, "profiles", "m2l_dram_traffic.json")))
+    except (OSError, ValueError):
+        return None, None
+    for e in rec.get("entries", []):
+        if e.get("config") == cfg.name and e.get("n_points") == n and e.get("order") == cfg.order:
+            return float(e["dram_bytes_read"]) + float(e["dram_bytes_write"]), e.get("source")
+    return None, None
+
+
+def kernel_roofline(cfg, n: int, steps: int, fp32_peak: float):
+    """P2P and M2L of one configuration timed alone (near field serialised behind the far field)"""
+    import torch
+
+    from paper_1803_09948_b200 import HfmmCuda
+    from paper_1803_09948_b200.api import HFMM_FLAG_PHASE_TIMERS
+
+    xyz, q = make_points(cfg, n), charges(n, cfg.seed)
+    op = HfmmCuda(k=cfg.k, order=cfg.order, ncrit=cfg.ncrit, theta=cfg.theta, kd_max=cfg.kd_max,
+                  leaf_cap=cfg.leaf_cap, device=0, flags=HFMM_FLAG_PHASE_TIMERS)
+    t0 = time.perf_counter()
+    op.set_points(xyz)
+    setup = time.perf_counter() - t0
+    q_dev = torch.from_numpy(np.stack([q.real, q.imag], 1).astype(np.float32)).cuda()
+    out_dev = torch.empty_like(q_dev)
+    acc = {k: 0.0 for k in ("p2p", "m2l", "matvec")}
+    for it in range(steps + 1):
+        op.matvec_device(q_dev.data_ptr(), out_dev.data_ptr())
+        st = op.stats()
+        if it:
+            for k in acc:
+                acc[k] += st[f"{k}_seconds"] / steps
+    ex, dense = m2l_flops_per_pair(cfg.order)
+    m2l_tf = st["m2l_pairs"] * ex / acc["m2l"] * 1e-12 if acc["m2l"] else 0.0
+    p2p_tf = st["p2p_body_pairs"] * 24 / acc["p2p"] * 1e-12 if acc["p2p"] else 0.0
+    op.close()
+    return {"workload": workload_config(cfg, n, 1)["workload"], "n_points": n, "order": cfg.order,
+            "setup_seconds": setup, "matvec_ms_serialised": acc["matvec"] * 1e3,
+            "m2l": {"ms": acc["m2l"] * 1e3, "pairs": st["m2l_pairs"], "flops_per_pair": ex,
+                    "tflops_executed": m2l_tf, "frac_of_fp32_peak": m2l_tf / fp32_peak if fp32_peak else None,
+                    "dense_equivalent_tflops": st["m2l_pairs"] * dense / acc["m2l"] * 1e-12 if acc["m2l"] else None},
+            "p2p": {"ms": acc["p2p"] * 1e3, "body_pairs": st["p2p_body_pairs"], "tflops_24flop_per_pair": p2p_tf,
+                    "frac_of_fp32_peak": p2p_tf / fp32_peak if fp32_peak else None, "kernel_variant": st["p2p_mode"]}}
 
 
 def run_single(args, cfg):
@@ -246,11 +297,30 @@ def run_single(args, cfg):
         "l2p": n * 20 + st0["n_leaves"] * 8 * stride,
         "m2m": st0["n_cells"] * 2 * 8 * stride, "l2l": st0["n_cells"] * 2 * 8 * stride}
 
+    # the reference interface's default, TraversalConfig::deterministic = true (ordered accumulation), beside it
+    from paper_1803_09948_b200.api import HFMM_FLAG_DETERMINISTIC
+    det_ms = None
+    if not args.no_deterministic:
+        opd = HfmmCuda(k=cfg.k, order=cfg.order, ncrit=cfg.ncrit, theta=cfg.theta, kd_max=cfg.kd_max,
+                       leaf_cap=cfg.leaf_cap, device=0, flags=HFMM_FLAG_DETERMINISTIC)
+        opd.set_points(xyz)
+        for _ in range(2):
+            opd.matvec_device(q_dev.data_ptr(), out_dev.data_ptr())
+        opd.sync()
+        ks = max(1, min(args.steps, 5))
+        opd.timer_record(0)
+        for _ in range(ks):
+            opd.matvec_device(q_dev.data_ptr(), out_dev.data_ptr())
+        opd.timer_record(1)
+        det_ms = opd.timer_elapsed_ms(0, 1) / ks
+        opd.close()
+    traffic, traffic_source = committed_traffic(cfg, n)
+
     cpu = cpu_reference_arm(cfg, args.ref_points, 1, 0) if not args.no_cpu_baseline else None
     line = {
         "metric": METRIC, "value": n / ms_step * 1e-3, "unit": UNIT, "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": workload_config(cfg, n, 1),
         "e2e": {"value": n / e2e_s * 1e-6, "unit": UNIT, "ms_per_step": e2e_s * 1e3,
                 "h2d_bytes_per_step": n * 16, "d2h_bytes_per_step": n * 16, "checksum": checksum},
@@ -273,18 +343,19 @@ def run_single(args, cfg):
             # near-field CTA shares every SM with the two M2L CTAs
             "ms_per_launch_alone": alone["m2l"] * 1e3, "achieved_alone": m2l_tf_alone,
             "frac_alone": m2l_tf_alone / fp32_peak if fp32_peak else None,
-            # dram__bytes_read + dram__bytes_write of this launch from the committed ncu --set full
-            # capture of the same configuration (profiles/r01_ncu_final_cfg2_full.txt:
-            # 11.12 GB read + 5.57 GB written); algorithmic bytes
-            # are pairs x 2 x 8 (P+1)^2 (one source row read, one destination row reduced)
-            "traffic": 16.69e9 if (cfg.name == "cfg2" and n == cfg.n) else None,
+            # dram__bytes_read + dram__bytes_write of this launch, read from the committed ncu --set full
+            # capture of the same configuration (profiles/m2l_dram_traffic.json; null when none is on
+            # record); algorithmic bytes are pairs x 2 x 8 (P+1)^2 (one source row read, one destination
+            # row reduced)
+            "traffic": traffic, "traffic_source": traffic_source,
             "algorithmic_bytes": st0["m2l_pairs"] * 2 * 8 * (cfg.order + 1) ** 2},
         # kernel-alone durations (near field serialised behind the far field); "ms_in_step" is the event
         # interval inside the timed region, where P2P is co-resident with M2L
         "kernels": {
             "p2p": {"ms": alone["p2p"] * 1e3, "ms_in_step": kern["p2p"] * 1e3, "tflops_24flop_per_pair": p2p_tf,
                     "frac_of_fp32_peak": p2p_tf / fp32_peak if fp32_peak else None,
-                    "body_pairs": st0["p2p_body_pairs"]},
+                    "body_pairs": st0["p2p_body_pairs"], "kernel_variant": st0["p2p_mode"],
+                    "near_r2_max": st0["near_r2_max"]},
             "m2l": {"ms": alone["m2l"] * 1e3, "ms_in_step": kern["m2l"] * 1e3, "tflops_executed": m2l_tf_alone,
                     "pairs": st0["m2l_pairs"]},
             **{k: {"ms": alone[k] * 1e3, "gbs": tree_bytes[k] / alone[k] * 1e-9 if alone[k] else None,
@@ -295,11 +366,21 @@ def run_single(args, cfg):
                                      "p2p_body_pairs", "m2l_shift_classes")},
         "setup_seconds": statistics.median(setup_warm), "setup_seconds_first_call": setup_cold,
         "setup_seconds_calls": setup_warm, "clocks": clocks,
+        "host_tree_used": st0["host_tree_used"],
+        # the same step with the reference interface's default TraversalConfig::deterministic = true
+        "deterministic_ms_per_step": det_ms,
     }
     if cpu:
         line["cpu_baseline"] = cpu
-    if not args.no_bie and cfg.name == "cfg2" and n == cfg.n:
+    if not args.no_cfg4 and cfg.name == "cfg2" and n == cfg.n:
+        # BASELINE configs[3] (Plummer, P = 14, theta = 0.35): the order-14 kernels, otherwise unbenchmarked
         del op
+        torch.cuda.empty_cache()
+        line["cfg4_kernels"] = kernel_roofline(CONFIGS["cfg4"], CONFIGS["cfg4"].n, 2, fp32_peak)
+        op = None
+    if not args.no_bie and cfg.name == "cfg2" and n == cfg.n:
+        op = None
+        torch.cuda.empty_cache()
         line["bie_solve"] = run_bie_solve()
     print(json.dumps(line), flush=True)
 
@@ -316,9 +397,8 @@ def run_bie_solve(subdivisions: int = 7, k: float = 4.0, order: int = 12):
     from paper_1803_09948_b200 import HfmmCuda
     from paper_1803_09948_b200.workloads import icosphere_patches, patch_samples
 
-    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "tests", "golden", "solver.npz"))
-    tables = {key: g["bie_rule_" + key] for key in ("sample_ref", "far_weight", "near_pts", "near_basis",
-                                                    "self_npts", "self_pts", "self_basis")}
+    from paper_1803_09948_b200.workloads import quadrature_tables
+    tables = quadrature_tables(basis_order=1)
     patches = icosphere_patches(subdivisions)
     xyz = patch_samples(patches, tables["sample_ref"])
     op = HfmmCuda(k=k, order=order, ncrit=64, theta=0.4, kd_max=1.0, leaf_cap=-1.0, device=0)
@@ -328,7 +408,7 @@ def run_bie_solve(subdivisions: int = 7, k: float = 4.0, order: int = 12):
     t0 = time.perf_counter()
     nnz = op.build_corrections(patches, tables, mode=2, fetch=False)
     t_corr = time.perf_counter() - t0
-    rhs = np.exp(1j * k * xyz[:, 2])
+    rhs = op.assemble_rhs((0.0, 0.0, 1.0))      # reference assemble_rhs: e^{ikz} at the samples
     t0 = time.perf_counter()
     x, rep = op.gmres(rhs, rtol=1e-4, restart=30, max_iterations=1000, precondition=False)
     t_solve = time.perf_counter() - t0
@@ -350,13 +430,39 @@ def run_bie_solve(subdivisions: int = 7, k: float = 4.0, order: int = 12):
 def run_multi(args, cfg, rank: int, world: int):
     from paper_1803_09948_b200.distributed import bench_distributed
 
-    if "RANK" not in os.environ:   # single process: stand up a 1-rank group
-        os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
-                          MASTER_PORT="29517")
-
     line = bench_distributed(args, cfg, rank, world, METRIC, UNIT, workload_config, ClockSampler)
     if rank == 0 and line is not None:
         print(json.dumps(line), flush=True)
+
+
+def spawn_ranks(args) -> int:
+    """`python bench.py --gpus N` without torchrun: start N ranks of this script (one per GPU), pass rank 0's
+    JSON line through.  Fails loudly when the node has fewer than N GPUs — never a silent world of one."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if args.share_gpu and args.transport != "host":
+        sys.stderr.write("bench.py: --share-gpu needs --transport host (NCCL refuses two ranks on one device)\n")
+        return 2
+    if have < args.gpus and not (args.share_gpu and have >= 1):
+        print(json.dumps({"error": f"--gpus {args.gpus} requested, this node has {have} GPU(s)", "n_gpus": args.gpus}),
+              flush=True)
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} requested, this node has {have} GPU(s)\n")
+        return 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    procs = []
+    for r in range(args.gpus):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK="0" if args.share_gpu else str(r), WORLD_SIZE=str(args.gpus),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env))
+    rc = 0
+    for p in procs:
+        rc = rc or p.wait()
+    return rc
 
 
 def main():
@@ -365,28 +471,46 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default=None, help="cfg1|cfg2|cfg4|cfg5 (default: cfg2 at N=1, cfg5 weak at N>1)")
+    ap.add_argument("--config", default=None,
+                    help="cfg1|cfg2|cfg4|cfg5 (default: cfg2 at N=1; at N>1 cfg5 strong, cfg5_per_gpu weak)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N>1: strong = the configuration's points shared out over the ranks (BASELINE configs[4]: "
+                         "33,554,432), weak = that many per GPU")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "host"],
+                    help="N>1: the library's NCCL data plane, or its host-staged transport over gloo")
     ap.add_argument("--n", type=int, default=None, help="override the point count (debug)")
     ap.add_argument("--ref-points", type=int, default=131072,
                     help="sample size of the cpu_baseline leg of the default arm (one matvec, ~25 s on 16 cores)")
-    ap.add_argument("--ref-arm-points", type=int, default=262144, help="sample size of --impl reference")
+    ap.add_argument("--ref-arm-points", type=int, default=None,
+                    help="--impl reference: run this many points instead of the whole configuration")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-bie", action="store_true", help="skip the configs[2] BIE solve reported next to the headline")
+    ap.add_argument("--no-cfg4", action="store_true", help="skip the configs[3] kernel rooflines (P = 14)")
+    ap.add_argument("--no-deterministic", action="store_true", help="skip the ordered-accumulation step time")
+    ap.add_argument("--no-single-domain", action="store_true", help="N>1: skip the one-domain baseline on rank 0")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="debug: all ranks on cuda:0 (with --transport host) — exercises the N>1 path on a one-GPU "
+                         "box; its numbers are NOT scaling measurements")
     ap.add_argument("--force-distributed", action="store_true",
                     help="run the N > 1 code path even with one rank (exercises the exchange plumbing)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
+    if args.impl == "reference":
+        run_reference(args, CONFIGS[args.config or "cfg2"], int(os.environ.get("RANK", "0")))
+        return
+    if args.gpus > 1 and "RANK" not in os.environ:
+        sys.exit(spawn_ranks(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    name = args.config or ("cfg2" if args.gpus == 1 else "cfg5_per_gpu")
-    cfg = CONFIGS[name]
-    if args.impl == "reference":
-        run_reference(args, CONFIGS[args.config or "cfg2"], rank)
-        return
+    if args.gpus > 1 and world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.gpus == 1 and world == 1 and not args.force_distributed:
-        run_single(args, cfg)
-    else:
-        run_multi(args, cfg, rank, world)
+        run_single(args, CONFIGS[args.config or "cfg2"])
+        return
+    if args.force_distributed and "RANK" not in os.environ:
+        os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1", MASTER_PORT="29517")
+    name = args.config or ("cfg5" if args.scaling == "strong" else "cfg5_per_gpu")
+    run_multi(args, CONFIGS[name], rank, world)
 
 
 if __name__ == "__main__":

@@ -6,9 +6,9 @@
   python -m paper_1803_09948_b200 matvec  --config cfg2 [--n N]        one BASELINE FMM configuration
   python -m paper_1803_09948_b200 info                                 library version, device probes
 
-The quadrature tables of the correction builders are the reference's (geometry.cpp), read from a
-.npz with the keys sample_ref, far_weight, near_pts, near_basis, self_npts, self_pts, self_basis
-(--rules; tests/golden/solver.npz carries them for the order-1 basis under the prefix bie_rule_)."""
+The quadrature tables of the correction builders are the reference's (geometry.cpp); the package ships
+them for basis orders 1 and 2 (data/quadrature_rules.npz, --basis-order), --rules reads other ones from a
+.npz with the keys sample_ref, far_weight, near_pts, near_basis, self_npts, self_pts, self_basis."""
 from __future__ import annotations
 
 import argparse
@@ -33,7 +33,8 @@ def cmd_solve(a):
     from .api import HFMM_FLAG_DETERMINISTIC
     from .workloads import icosphere_patches, mie_soft_sphere, patch_samples
 
-    tables = _load_rules(a.rules)
+    from .workloads import quadrature_tables
+    tables = _load_rules(a.rules) if a.rules else quadrature_tables(a.basis_order)
     if a.mesh:       # GMSH MSH 2.2 ASCII or the reference's binary block format (meshio.py)
         from .meshio import read_mesh
         patches = read_mesh(a.mesh)
@@ -45,7 +46,7 @@ def cmd_solve(a):
                   flags=HFMM_FLAG_DETERMINISTIC if a.deterministic else 0)
     t0 = time.perf_counter(); op.set_points(xyz); t_tree = time.perf_counter() - t0
     t0 = time.perf_counter(); nnz = op.build_corrections(patches, tables, mode=2, fetch=False); t_corr = time.perf_counter() - t0
-    rhs = np.exp(1j * a.k * xyz[:, 2])
+    rhs = op.assemble_rhs((0.0, 0.0, 1.0))          # plane wave e^{ikz} (reference assemble_rhs)
     t0 = time.perf_counter()
     x, rep = op.gmres(rhs, rtol=a.rtol, restart=a.restart, max_iterations=a.max_iterations,
                       precondition=a.block_jacobi)
@@ -131,8 +132,8 @@ def main(argv=None):
     s.add_argument("--deterministic", action="store_true", help="ordered accumulation: bitwise reproducible runs")
     s.add_argument("--observations", type=int, default=37)
     s.add_argument("--obs-radius", type=float, default=4.0, help="in sphere radii")
-    s.add_argument("--rules", default=os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                                                   "tests", "golden", "solver.npz"))
+    s.add_argument("--basis-order", type=int, default=1, choices=[1, 2], help="Lagrange basis of the shipped tables")
+    s.add_argument("--rules", default=None, help=".npz with other quadrature tables (default: the shipped ones)")
     s.set_defaults(fn=cmd_solve)
     m = sub.add_parser("matvec", help="one BASELINE FMM configuration, checked against an FP64 direct sum")
     m.add_argument("--config", default="cfg2")

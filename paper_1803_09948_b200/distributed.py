@@ -311,7 +311,10 @@ def emulate_ranks_on_one_device(ops, q_morton, pruned: bool = False):
 
 
 def bench_distributed(args, cfg, rank, world, metric, unit, workload_config, ClockSampler):
-    """bench.py --gpus N (N > 1): weak scaling, cfg.n points PER GPU, Morton-partitioned"""
+    """bench.py --gpus N (N > 1), one rank per GPU.  --scaling strong (default): the configuration's points
+    (BASELINE cfg 5: 33,554,432) are shared out over the ranks; weak: cfg.n points per GPU.  Rank 0 also times
+    the same total problem as ONE domain on its own GPU (when it fits) so that every line carries its own
+    single-GPU baseline."""
     import torch
     import torch.distributed as dist
 
@@ -319,10 +322,15 @@ def bench_distributed(args, cfg, rank, world, metric, unit, workload_config, Clo
     from .workloads import charges, make_points
 
     local = int(os.environ.get("LOCAL_RANK", rank))
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"bench.py --gpus {world}: rank {rank} needs cuda:{local}, "
+                         f"this node has {torch.cuda.device_count()} GPU(s)")
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = torch.device("cuda", local)
-    n_total = (args.n or cfg.n) * world
+    # the process group is bootstrap and timing plumbing only (gloo); the data plane is the library's NCCL
+    dist.init_process_group("gloo")
+    strong = args.scaling == "strong"
+    n_total = (args.n or cfg.n) if strong else (args.n or cfg.n) * world
     xyz = make_points(cfg, n_total)              # every rank builds the same global tree
     op = HfmmCuda(k=cfg.k, order=cfg.order, ncrit=cfg.ncrit, theta=cfg.theta, kd_max=cfg.kd_max,
                   leaf_cap=cfg.leaf_cap, device=local)
@@ -330,68 +338,105 @@ def bench_distributed(args, cfg, rank, world, metric, unit, workload_config, Clo
     t0 = time.perf_counter()
     op.set_points(xyz)
     setup = time.perf_counter() - t0
-    sh = ShardedFmm(op, dist, rank, world, device, pruned=True)
+    sh = ShardedFmm(op, dist, rank, world, device, transport=args.transport)
     order = op.body_order()
-    q = charges(n_total, cfg.seed)[order[sh.first:sh.first + sh.count]]
+    q_all = charges(n_total, cfg.seed)
+    q = q_all[order[sh.first:sh.first + sh.count]]
     q_local = torch.from_numpy(np.stack([q.real, q.imag], 1).astype(np.float32)).to(device)
+
+    def barrier():
+        op.sync()
+        torch.cuda.synchronize()
+        dist.barrier()
 
     sampler = ClockSampler(local)
     if rank == 0:
         sampler.start()
     for _ in range(args.warmup):
         sh.matvec(q_local)
-    dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
     t0 = time.perf_counter()
-    e0.record()
+    op.timer_record(0)
     for _ in range(args.steps):
-        y = sh.matvec(q_local)
-    e1.record()
-    torch.cuda.synchronize()
-    dist.barrier()
+        sh.matvec(q_local)
+    op.timer_record(1)
+    dev_ms = op.timer_elapsed_ms(0, 1) / args.steps
+    barrier()
     wall_ms = (time.perf_counter() - t0) * 1e3 / args.steps
-    ms = torch.tensor([max(e0.elapsed_time(e1) / args.steps, 0.0), wall_ms], device=device)
+    ms = torch.tensor([dev_ms, wall_ms], dtype=torch.float64)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     # end to end: owned charges come from / results go to pinned host memory every step
     qh = torch.from_numpy(np.stack([q.real, q.imag], 1).astype(np.float32)).pin_memory()
     oh = torch.empty_like(qh).pin_memory()
-    dist.barrier()
-    torch.cuda.synchronize()
+    barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         q_local.copy_(qh, non_blocking=True)
-        oh.copy_(sh.matvec(q_local), non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        y = sh.matvec(q_local)
+        op.sync()
+        oh.copy_(y, non_blocking=True)
         torch.cuda.synchronize()
-    e2e = torch.tensor([(time.perf_counter() - t0) / args.steps], device=device)
+    e2e = torch.tensor([(time.perf_counter() - t0) / args.steps], dtype=torch.float64)
     dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
     st = op.stats()
-    work = torch.tensor([float(sh.owned_m2l_pairs), float(sh.owned_p2p_body_pairs), float(sh.count)],
-                        device=device)
-    allw = torch.empty(world * 3, device=device)
-    dist.all_gather_into_tensor(allw, work)
+    work = torch.tensor([float(sh.owned_m2l_pairs), float(sh.owned_p2p_body_pairs), float(sh.count),
+                         float(sh.let_bytes["charges"]), float(sh.let_bytes["multipoles"])], dtype=torch.float64)
+    allw = [torch.zeros_like(work) for _ in range(world)]
+    dist.all_gather(allw, work)
     clocks = sampler.stop() if rank == 0 else None
+    # the same total problem as one domain on rank 0's GPU: the baseline of this line
+    single = None
+    if rank == 0 and not args.no_single_domain:
+        del sh
+        op.close()
+        torch.cuda.empty_cache()
+        try:
+            one = HfmmCuda(k=cfg.k, order=cfg.order, ncrit=cfg.ncrit, theta=cfg.theta, kd_max=cfg.kd_max,
+                           leaf_cap=cfg.leaf_cap, device=local)
+            one.set_points(xyz)
+            qd = torch.from_numpy(np.stack([q_all.real, q_all.imag], 1).astype(np.float32)).to(device)
+            od = torch.empty_like(qd)
+            for _ in range(min(args.warmup, 2)):
+                one.matvec_device(qd.data_ptr(), od.data_ptr())
+            one.sync()
+            ks = max(1, min(args.steps, 5))
+            one.timer_record(0)
+            for _ in range(ks):
+                one.matvec_device(qd.data_ptr(), od.data_ptr())
+            one.timer_record(1)
+            t1 = one.timer_elapsed_ms(0, 1) / ks
+            single = {"n_points": n_total, "ms_per_step": t1, "value": n_total / t1 * 1e-3, "unit": unit, "steps": ks}
+            one.close()
+        except Exception as e:        # e.g. out of memory for a problem sized for N GPUs
+            single = {"unavailable": str(e)[:200]}
+    dist.barrier()
     dist.destroy_process_group()
     if rank != 0:
         return None
     ms_step = float(ms[1])     # wall clock between barriers bounds the max over ranks
-    allw = allw.reshape(world, 3).cpu().numpy()
-    return {
+    allw = torch.stack(allw).numpy()
+    line = {
         "metric": metric, "value": n_total / ms_step * 1e-3, "unit": unit, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": workload_config(cfg, n_total, world),
         "e2e": {"value": n_total / float(e2e[0]) * 1e-6, "unit": unit,
                 "ms_per_step": float(e2e[0]) * 1e3,
-                "h2d_bytes_per_step": int(sh.count) * 8, "d2h_bytes_per_step": int(sh.count) * 8},
-        "gpu_launches": int(st["kernel_launches"]) * args.steps,
-        # rank 0's receive volume per matvec: locally essential rows only (full gather in brackets)
-        "exchange": {"kind": "locally essential tree, all_to_all" if sh.pruned else "all-gather",
-                     "charges_bytes_per_rank": sh.let_bytes["charges"] if sh.pruned else n_total * 8,
-                     "multipole_bytes_per_rank": sh.let_bytes["multipoles"] if sh.pruned else
-                     int(sum(c for rr in sh.cell_ranges for _, c in rr)) * sh.stride * 8,
-                     "full_gather_bytes_per_rank": n_total * 8 + int(sum(c for rr in sh.cell_ranges for _, c in rr)) * sh.stride * 8},
+                "h2d_bytes_per_step": int(allw[0, 2]) * 8, "d2h_bytes_per_step": int(allw[0, 2]) * 8},
+        "gpu_launches": (int(st["kernel_launches"]) + 4) * args.steps,
+        # per rank receive volume per matvec: locally essential rows only
+        "exchange": {"kind": f"locally essential tree: pack kernel, grouped send/recv ({args.transport}), unpack kernel",
+                     "charges_bytes_per_rank": allw[:, 3].astype(int).tolist(),
+                     "multipole_bytes_per_rank": allw[:, 4].astype(int).tolist()},
         "balance": {"m2l_pairs": allw[:, 0].tolist(), "p2p_body_pairs": allw[:, 1].tolist(),
                     "bodies": allw[:, 2].tolist()},
         "device_ms_rank_max": float(ms[0]), "setup_seconds": setup, "clocks": clocks,
     }
+    if getattr(args, "share_gpu", False):
+        line["invalid_as_scaling"] = "all ranks shared cuda:0 (--share-gpu): plumbing check, not a measurement"
+    if single is not None:
+        line["single_domain_same_problem"] = single
+        if "ms_per_step" in single:
+            line["speedup_vs_single_domain"] = single["ms_per_step"] / ms_step
+    return line

@@ -159,3 +159,19 @@ def mie_soft_sphere(radius: float, k: float, r, theta) -> np.ndarray:
         out[idx] = -np.sum((2 * n + 1) * (1j ** n) * ratio * h(k * r[idx]) * eval_legendre(n, np.cos(theta[idx])))
     return out
 
+
+
+def quadrature_tables(basis_order: int = 1) -> dict:
+    """The interpolation / quadrature tables of hfmm_correction_rules for basis order 1 or 2 (near rule 25,
+    Duffy rule 8 — the reference's KernelConfig defaults, kernel.hpp:48-50), shipped with the package
+    (data/quadrature_rules.npz, tabulated from the reference's geometry.cpp by
+    scripts/make_quadrature_tables.py)."""
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "quadrature_rules.npz")
+    g = np.load(path)
+    prefix = f"order{int(basis_order)}_"
+    keys = ("sample_ref", "far_weight", "near_pts", "near_basis", "self_npts", "self_pts", "self_basis")
+    if prefix + keys[0] not in g.files:
+        raise ValueError("tables are shipped for basis orders 1 and 2")
+    return {k: g[prefix + k] for k in keys}
