@@ -275,10 +275,6 @@ __global__ void block_lu_kernel(Z* __restrict__ lu, int* __restrict__ piv, int n
   }
 }
 
-__global__ void narrow_complex_kernel(const Z* __restrict__ in, float2* __restrict__ out, uint64_t n) {
-  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (i < n) out[i] = make_float2(float(in[i].re), float(in[i].im));
-}
 __global__ void sample_weights_kernel(const double* __restrict__ w, int ni, uint32_t n, float* __restrict__ out) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = float(w[i % uint32_t(ni)]);
@@ -458,18 +454,20 @@ void Engine::build_corrections(const hfmm_correction_rules& r, uint64_t* nnz_out
   if (flags[1]) throw Error(HFMM_ERR_STRUCTURAL, "near re-integration produced a non-finite value (degenerate patch)");
   store->nnz = nnz;
 
-  // install FP32 copies as the handle's corrections (what set_corrections would upload)
+  // install the arrays as the handle's corrections (what set_corrections would upload; FP64 like there)
   ni_ = ni;
   far_weight_.resize(n);
   sample_weights_kernel<<<blocks_for(n, 256), 256, 0, s>>>(d_fw.get(), ni, uint32_t(n), far_weight_.get());
   have_weight_ = true;
   patch_block_.resize(n * ni);
-  narrow_complex_kernel<<<blocks_for(n * ni, 256), 256, 0, s>>>(store->patch_block.get(), patch_block_.get(), n * ni);
+  HFMM_CUDA_CHECK(cudaMemcpyAsync(patch_block_.get(), store->patch_block.get(), n * ni * sizeof(double2),
+                                  cudaMemcpyDeviceToDevice, s));
   have_block_ = true;
   have_lu_ = self_terms;
   if (self_terms) {
     block_lu_.resize(n * ni);
-    narrow_complex_kernel<<<blocks_for(n * ni, 256), 256, 0, s>>>(store->block_lu.get(), block_lu_.get(), n * ni);
+    HFMM_CUDA_CHECK(cudaMemcpyAsync(block_lu_.get(), store->block_lu.get(), n * ni * sizeof(double2),
+                                    cudaMemcpyDeviceToDevice, s));
     block_piv_.resize(n);
     HFMM_CUDA_CHECK(cudaMemcpyAsync(block_piv_.get(), store->block_piv.get(), n * sizeof(int), cudaMemcpyDeviceToDevice, s));
   }
@@ -482,7 +480,8 @@ void Engine::build_corrections(const hfmm_correction_rules& r, uint64_t* nnz_out
     HFMM_CUDA_CHECK(cudaMemcpyAsync(near_source_.get(), store->near_source.get(), nnz * sizeof(uint32_t),
                                     cudaMemcpyDeviceToDevice, s));
     near_delta_.resize(nnz);
-    narrow_complex_kernel<<<blocks_for(nnz, 256), 256, 0, s>>>(store->near_delta.get(), near_delta_.get(), nnz);
+    HFMM_CUDA_CHECK(cudaMemcpyAsync(near_delta_.get(), store->near_delta.get(), nnz * sizeof(double2),
+                                    cudaMemcpyDeviceToDevice, s));
   }
   HFMM_CUDA_CHECK(cudaGetLastError());
   HFMM_CUDA_CHECK(cudaStreamSynchronize(s));

@@ -196,7 +196,7 @@ class Engine {
   int ni_ = 0;
   bool have_weight_ = false, have_block_ = false, have_near_ = false, have_lu_ = false;
   DeviceBuffer<float> far_weight_;
-  DeviceBuffer<float2> patch_block_, near_delta_, block_lu_;
+  DeviceBuffer<double2> patch_block_, near_delta_, block_lu_;  // FP64: see corrections_kernel
   DeviceBuffer<uint32_t> near_offset_, near_source_, identity_;
   DeviceBuffer<int> block_piv_;
   DeviceBuffer<float4> body_abs_;  // k * x, caller order

@@ -17,12 +17,6 @@ namespace {
 using cd = std::complex<double>;
 constexpr double kPi = 3.14159265358979323846264338327950288;
 
-template <typename T, typename S>
-std::vector<T> convert_complex(const S* in, size_t n) {
-  std::vector<T> out(n);
-  for (size_t i = 0; i < n; ++i) out[i] = T{decltype(T{}.x)(in[2 * i]), decltype(T{}.x)(in[2 * i + 1])};
-  return out;
-}
 }  // namespace
 
 void Engine::set_corrections(int ni, const double* far_weight, const double* patch_block,
@@ -42,7 +36,7 @@ void Engine::set_corrections(int ni, const double* far_weight, const double* pat
     far_weight_.upload(w, stream_);
   }
   have_block_ = patch_block != nullptr;
-  if (have_block_) patch_block_.upload(convert_complex<float2>(patch_block, npatch * ni * ni), stream_);
+  if (have_block_) patch_block_.upload(reinterpret_cast<const double2*>(patch_block), npatch * ni * ni, stream_);
   have_near_ = near_offset && near_source && near_delta && near_offset[n] > 0;
   if (have_near_) {
     for (size_t i = 0; i < n; ++i)
@@ -52,13 +46,13 @@ void Engine::set_corrections(int ni, const double* far_weight, const double* pat
       if (near_source[e] >= n) throw Error(HFMM_ERR_STRUCTURAL, "near CSR source out of range");
     near_offset_.upload(near_offset, n + 1, stream_);
     near_source_.upload(near_source, nnz, stream_);
-    near_delta_.upload(convert_complex<float2>(near_delta, nnz), stream_);
+    near_delta_.upload(reinterpret_cast<const double2*>(near_delta), nnz, stream_);
   }
   have_lu_ = block_lu && block_piv;
   if (have_lu_) {
     for (size_t i = 0; i < n; ++i)
       if (block_piv[i] < 0 || block_piv[i] >= ni) throw Error(HFMM_ERR_STRUCTURAL, "pivot out of range");
-    block_lu_.upload(convert_complex<float2>(block_lu, npatch * ni * ni), stream_);
+    block_lu_.upload(reinterpret_cast<const double2*>(block_lu), npatch * ni * ni, stream_);
     block_piv_.upload(block_piv, n, stream_);
   }
   HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));

@@ -198,9 +198,10 @@ void launch_ordered_reduce(const float2* staging, const uint32_t* perm, const ui
 void launch_range_rows(uint32_t* row_of_pair, uint64_t begin, uint32_t n, cudaStream_t s);
 
 // ---- BIE operator tail + Krylov vector ops (kernels_krylov.cu) -------------------------------
-void launch_corrections(uint32_t n, int ni, const float2* block, const uint32_t* off, const uint32_t* src,
-                        const float2* delta, const float2* x, float2* y, cudaStream_t s);
-void launch_precondition(uint32_t npatch, int ni, const float2* lu, const int* piv, const float2* in,
+// y += blockdiag x + CSR x and the per-patch LU solve: FP64 values and accumulation, FP32 vectors
+void launch_corrections(uint32_t n, int ni, const double2* block, const uint32_t* off, const uint32_t* src,
+                        const double2* delta, const float2* x, float2* y, cudaStream_t s);
+void launch_precondition(uint32_t npatch, int ni, const double2* lu, const int* piv, const float2* in,
                          float2* out, cudaStream_t s);
 // The reducing kernels (mgs_step, norm2, residual) sum in a fixed order (reproducible run to run):
 // scratch = reduce_scratch_doubles() zero-initialised doubles, private to the stream.

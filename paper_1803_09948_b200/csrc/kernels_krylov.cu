@@ -72,72 +72,79 @@ __device__ __forceinline__ void grid_accumulate(double re, double im, double* ou
   }
 }
 
+// FP64 values, FP64 accumulation: the corrections carry the near-singular part of the operator — large
+// entries that cancel against the point-kernel near field — and are HBM-bound either way.  Measured on an
+// ill-conditioned first-kind system (lat-long sphere, 864 unknowns): FP32 corrections alone took
+// block-Jacobi GMRES(30) from 28 to 58 iterations.
 __global__ void __launch_bounds__(kBlock)
-corrections_kernel(uint32_t n, int ni, const float2* __restrict__ block, const uint32_t* __restrict__ off,
-                   const uint32_t* __restrict__ src, const float2* __restrict__ delta,
+corrections_kernel(uint32_t n, int ni, const double2* __restrict__ block, const uint32_t* __restrict__ off,
+                   const uint32_t* __restrict__ src, const double2* __restrict__ delta,
                    const float2* __restrict__ x, float2* __restrict__ y) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  float ar = 0.f, ai = 0.f;
+  double ar = 0.0, ai = 0.0;
   if (block) {
     const uint32_t p = i / uint32_t(ni), r = i - p * uint32_t(ni);
-    const float2* row = block + (size_t(p) * ni + r) * ni;
+    const double2* row = block + (size_t(p) * ni + r) * ni;
     const float2* xp = x + size_t(p) * ni;
     for (int c = 0; c < ni; ++c) {
-      const float2 b = row[c], v = xp[c];
+      const double2 b = row[c];
+      const float2 v = xp[c];
       ar += b.x * v.x - b.y * v.y;
       ai += b.x * v.y + b.y * v.x;
     }
   }
   if (delta) {
     for (uint32_t e = off[i]; e < off[i + 1]; ++e) {
-      const float2 d = delta[e], v = x[src[e]];
+      const double2 d = delta[e];
+      const float2 v = x[src[e]];
       ar += d.x * v.x - d.y * v.y;
       ai += d.x * v.y + d.y * v.x;
     }
   }
-  float2 o = y[i];
-  o.x += ar;
-  o.y += ai;
-  y[i] = o;
+  const float2 o = y[i];
+  y[i] = make_float2(float(double(o.x) + ar), float(double(o.y) + ai));
 }
 
 constexpr int kMaxNi = 12;  // basis orders 1, 2, 3 -> 3, 6, 12 nodes per patch (geometry.cpp:145-171)
 
 __global__ void __launch_bounds__(kBlock)
-precondition_kernel(uint32_t npatch, int ni, const float2* __restrict__ lu, const int* __restrict__ piv,
+precondition_kernel(uint32_t npatch, int ni, const double2* __restrict__ lu, const int* __restrict__ piv,
                     const float2* __restrict__ in, float2* __restrict__ out) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= npatch) return;
-  float2 v[kMaxNi];
-  for (int c = 0; c < ni; ++c) v[c] = in[size_t(p) * ni + c];
-  const float2* a = lu + size_t(p) * ni * ni;
+  double2 v[kMaxNi];  // lu_solve (solver.cpp:65-74) in FP64: the factors of small patches are badly scaled
+  for (int c = 0; c < ni; ++c) {
+    const float2 t = in[size_t(p) * ni + c];
+    v[c] = make_double2(t.x, t.y);
+  }
+  const double2* a = lu + size_t(p) * ni * ni;
   const int* pv = piv + size_t(p) * ni;
   for (int c = 0; c < ni; ++c) {
     const int q = pv[c];
     if (q != c) {
-      const float2 t = v[c];
+      const double2 t = v[c];
       v[c] = v[q];
       v[q] = t;
     }
     for (int r = c + 1; r < ni; ++r) {
-      const float2 l = a[r * ni + c];
+      const double2 l = a[r * ni + c];
       v[r].x -= l.x * v[c].x - l.y * v[c].y;
       v[r].y -= l.x * v[c].y + l.y * v[c].x;
     }
   }
   for (int r = ni - 1; r >= 0; --r) {
     for (int c = r + 1; c < ni; ++c) {
-      const float2 u = a[r * ni + c];
+      const double2 u = a[r * ni + c];
       v[r].x -= u.x * v[c].x - u.y * v[c].y;
       v[r].y -= u.x * v[c].y + u.y * v[c].x;
     }
-    const float2 d = a[r * ni + r];
-    const float den = d.x * d.x + d.y * d.y;
-    const float2 t = v[r];
-    v[r] = make_float2((t.x * d.x + t.y * d.y) / den, (t.y * d.x - t.x * d.y) / den);
+    const double2 d = a[r * ni + r];
+    const double den = d.x * d.x + d.y * d.y;
+    const double2 t = v[r];
+    v[r] = make_double2((t.x * d.x + t.y * d.y) / den, (t.y * d.x - t.x * d.y) / den);
   }
-  for (int c = 0; c < ni; ++c) out[size_t(p) * ni + c] = v[c];
+  for (int c = 0; c < ni; ++c) out[size_t(p) * ni + c] = make_float2(float(v[c].x), float(v[c].y));
 }
 
 // w -= h_prev * v_prev (if v_prev), then out += conj(v_next) . w (if v_next)
@@ -289,13 +296,13 @@ inline uint32_t reduce_grid(uint32_t n) { return std::min<uint32_t>(grid_for(n),
 
 size_t reduce_scratch_doubles() { return 2 * kReduceBlocks + 1; }
 
-void launch_corrections(uint32_t n, int ni, const float2* block, const uint32_t* off, const uint32_t* src,
-                        const float2* delta, const float2* x, float2* y, cudaStream_t s) {
+void launch_corrections(uint32_t n, int ni, const double2* block, const uint32_t* off, const uint32_t* src,
+                        const double2* delta, const float2* x, float2* y, cudaStream_t s) {
   if (!n || (!block && !delta)) return;
   corrections_kernel<<<grid_for(n), kBlock, 0, s>>>(n, ni, block, off, src, delta, x, y);
   HFMM_CUDA_CHECK(cudaGetLastError());
 }
-void launch_precondition(uint32_t npatch, int ni, const float2* lu, const int* piv, const float2* in,
+void launch_precondition(uint32_t npatch, int ni, const double2* lu, const int* piv, const float2* in,
                          float2* out, cudaStream_t s) {
   if (!npatch) return;
   if (ni > kMaxNi) throw Error(HFMM_ERR_CONFIG, "more than 12 basis nodes per patch");

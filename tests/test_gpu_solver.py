@@ -138,20 +138,32 @@ def test_solve_report_histories():
 
 
 @pytest.mark.skipif(not have_ref(), reason="compiled reference not on this box")
-def test_midsize_system_against_oracle_gmres(oracle):
-    """320 curved triangles (960 unknowns): system built by the reference, GMRES run (a) on the
-    device and (b) by the oracle's restatement of gmres.cpp over the oracle's FMM matvec."""
+@pytest.mark.parametrize("direction", [(0.36, 0.48, 0.8), (0.0, 0.0, 1.0)], ids=["generic-wave", "wave-along-a-symmetry-axis"])
+def test_midsize_system_against_oracle_gmres(oracle, direction):
+    """320 curved triangles (960 unknowns): system built by the reference, GMRES run (a) on the device and
+    (b) by the oracle's restatement of gmres.cpp over the oracle's FP64 FMM matvec.
+
+    North star: the same iteration count +-1.  That holds — restarted or not — for a GENERIC right-hand
+    side.  With the wave along a symmetry axis of the mesh (the icosphere's five-fold axis here, the polar
+    axis of the reference's lat-long sphere in tests/test_gpu_dropin.py) the all-FP64 iteration never leaves
+    the invariant subspace of that symmetry and converges early; ANY rounding at FP32 level breaks the
+    symmetry, the Krylov vectors leak into the other sectors and have to be resolved there too.  The
+    reference's own FP32 near-field mode (kernel::Precision::f32) does exactly the same
+    (tests/test_oracle_vs_reference.py::test_symmetric_problem_iteration_count_is_not_robust_in_fp32), so
+    for that degenerate case the device count is pinned against the same operator under the FP64 Krylov
+    loop, and only loosely against the all-FP64 run."""
     from checkers import Ref
 
     k, order = 3.0, 10
     sysr = Ref().bie(icosphere_patches(2), 1, k, mode=2, use_tree=False)
     xyz, fw = sysr.samples()
     corr = sysr.corrections()
-    rhs = sysr.rhs((0, 0, 1))
+    rhs = sysr.rhs(direction)
     # ordered accumulation: "the same operator" below must be a function, not a run-to-run variable
     op = HfmmCuda(k=k, order=order, ncrit=16, flags=HFMM_FLAG_DETERMINISTIC)
     op.set_points(xyz)
     op.set_corrections(sysr.ni, far_weight=fw, **corr)
+    assert np.abs(op.assemble_rhs(direction) - rhs).max() < 1e-13
     f = oracle.fmm(xyz, k, order, ncrit=16, leaf_cap=1.0 / k, theta=0.4, kd_max=1.0)
 
     def minv(u):
@@ -165,22 +177,21 @@ def test_midsize_system_against_oracle_gmres(oracle):
     def z_gpu(u):       # the device operator (FP32 arithmetic) under the oracle's FP64 Krylov loop
         return op.matvec(minv(u))
 
-    # (1) without restarts the count matches the all-FP64 CPU solve within +-1
+    generic = direction[2] != 1.0
+    # (1) without restarts
     x_gpu, rep = op.gmres(rhs, rtol=1e-4, restart=300, max_iterations=300)
     u, rep_o = oracle.gmres(z_cpu, rhs, rtol=1e-4, restart=300, max_iterations=300)
     assert rep["converged"] and rep_o["converged"]
     assert abs(rep["iterations"] - rep_o["iterations"]) <= 1, (rep["iterations"], rep_o["iterations"])
     assert rel_l2(x_gpu, minv(u)) < 2e-3
-    # (2) restart 30: the device solver reproduces, within +-1, what the reference's algorithm does
-    # on the SAME (FP32) operator.  Against the all-FP64 operator this first-kind system (condition
-    # number ~1e5) shifts by a few iterations under ANY 3e-7 operator perturbation — measured:
-    # 56 (FP64) vs 59-60 (FP32 operator, or FP64 operator + 3e-7 noise); see DESIGN.md §7.
+    # (2) restart 30
     x30, rep30 = op.gmres(rhs, rtol=1e-4, restart=30, max_iterations=300)
     _, rep30_same_op = oracle.gmres(z_gpu, rhs, rtol=1e-4, restart=30, max_iterations=300)
     _, rep30_cpu = oracle.gmres(z_cpu, rhs, rtol=1e-4, restart=30, max_iterations=300)
     assert rep30["converged"]
     assert abs(rep30["iterations"] - rep30_same_op["iterations"]) <= 1
-    assert abs(rep30["iterations"] - rep30_cpu["iterations"]) <= 5
+    assert abs(rep30["iterations"] - rep30_cpu["iterations"]) <= (1 if generic else 5), \
+        (rep30["iterations"], rep30_cpu["iterations"])
     assert rel_l2(x30, x_gpu) < 2e-3
 
 
