@@ -190,7 +190,27 @@ def test_midsize_system_against_oracle_gmres(oracle, direction):
     _, rep30_cpu = oracle.gmres(z_cpu, rhs, rtol=1e-4, restart=30, max_iterations=300)
     assert rep30["converged"]
     assert abs(rep30["iterations"] - rep30_same_op["iterations"]) <= 1
-    assert abs(rep30["iterations"] - rep30_cpu["iterations"]) <= (1 if generic else 5), \
+    if generic:
+        # the comparison the north star asks for ("in FP32 complex"): the REFERENCE in its own single-precision
+        # near-field mode (kernel::Precision::f32, kernel.hpp:43-55; everything else FP64) under the same
+        # FP64 Krylov loop.  Measured for five generic directions (scripts/diag_midsize.py and the reference
+        # against itself): all-FP64 57 every time; reference f32 near field 58-59; FP64 operator applied to
+        # the FP32-rounded operand 58-59; FP64 operator + 1e-7 noise 58-59; device 58-59.  The 57 is the
+        # outlier of exact arithmetic — the residual of iteration 57 sits 6 % under the threshold — so the
+        # device is pinned to +-1 of the reference's FP32 mode and to +2 of the all-FP64 run.
+        fr = Ref().fmm(xyz, k, order, ncrit=16, leaf_cap=1.0 / k, theta=0.4, kd_max=1.0)
+
+        def z_ref32(u):
+            v = minv(u)
+            return oracle.apply_corrections(sysr.ni, corr["patch_block"], corr["near_offset"],
+                                            corr["near_source"], corr["near_delta"], v,
+                                            fr.matvec(v * fw, f32_p2p=True))
+
+        _, rep30_ref32 = oracle.gmres(z_ref32, rhs, rtol=1e-4, restart=30, max_iterations=300)
+        assert abs(rep30["iterations"] - rep30_ref32["iterations"]) <= 1, \
+            (rep30["iterations"], rep30_ref32["iterations"])
+        assert rep30_ref32["iterations"] >= rep30_cpu["iterations"]
+    assert abs(rep30["iterations"] - rep30_cpu["iterations"]) <= (2 if generic else 5), \
         (rep30["iterations"], rep30_cpu["iterations"])
     assert rel_l2(x30, x_gpu) < 2e-3
 
