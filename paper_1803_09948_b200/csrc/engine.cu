@@ -560,10 +560,17 @@ void Engine::finish_far_field(TableRegistry& reg) {
   });
   mark("rotation tables");
   const CoaxBuilder& builder = CoaxBuilder::shared(P);
+  const bool sign_folded = coax_tables_sign_folded(P);
   parallel_for(ncoax, threads_, [&](size_t i) {
     const auto& s = reg.coax_specs[i];
-    builder.build(s.kind, k, s.dist, s.s_src, s.s_dst, coax.data() + i * size_t(coax_table_size(P)) * 2,
-                  cfg_.wave_i);
+    float* tab = coax.data() + i * size_t(coax_table_size(P)) * 2;
+    builder.build(s.kind, k, s.dist, s.s_src, s.s_dst, tab, cfg_.wave_i);
+    if (sign_folded)  // (-1)^m of the inverse rotation's inputs, applied once here instead of per batch
+      for (int m = 1; m <= P; m += 2) {
+        float* blk = tab + 2 * size_t(coax_block_offset(P, m));
+        const size_t cnt = 2 * size_t(P + 1 - m) * size_t(coax_row_stride(P, m));
+        for (size_t e = 0; e < cnt; ++e) blk[e] = -blk[e];
+      }
   });
   mark("coaxial tables");
   rot_tables_.upload(rot, stream_);

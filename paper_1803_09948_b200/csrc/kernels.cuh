@@ -154,12 +154,11 @@ void launch_translate(const TranslateArgs& a, cudaStream_t s);
 // pairs per work item expected by the kernel
 int translate_batch_size(int order);
 
-// ---- the 64-pair in-place translation kernel (kernels_translate64.cu), orders <= 12 ------------
-inline constexpr int kTranslate64Warps = 8;
-inline constexpr int kTranslate64MaxOrder = 12;
-inline constexpr int kTranslate64MaxDim = 169;     // (P+1)^2 at the largest order
-inline constexpr int kTranslate64MaxUnits = 96;   // (P+1)(P+2)/2 <= 91 units (n, m >= 0), rounded to lanes
-inline constexpr int kTranslate64MaxTasks = 32;
+// ---- the 64-pair in-place translation kernel (kernels_translate64.cu), orders <= 16 ------------
+inline constexpr int kTranslate64MaxOrder = 12;   // two 8-warp CTAs per SM up to here
+inline constexpr int kTranslate64TopOrder = 16;   // one 16-warp CTA per SM up to here
+inline constexpr int kTranslate64MaxWarps = 16;
+inline constexpr int kTranslate64MaxTasks = 64;
 // one whole folded system of a degree (rotations) or one folded column of an order (coaxial step)
 struct Translate64Task {
   uint32_t tab_off;  // first coefficient row: byte offset in the shared-memory window
@@ -167,15 +166,19 @@ struct Translate64Task {
   uint16_t row0;     // tile row of input / output 0
   int16_t step;      // rotations: +1 / -1 per index; coaxial: 2m + 2, growing by 2 per degree
   uint8_t w;         // inputs = outputs
-  uint8_t pad;
+  uint8_t half;      // 0: all 64 pairs (a lane owns two); 1 / 2: pairs 0..31 / 32..63 (a lane owns one)
 };
 struct Translate64Schedule {
-  int rot_begin[kTranslate64Warps + 1];
-  int coax_begin[kTranslate64Warps + 1];
+  int rot_begin[kTranslate64MaxWarps + 1];
+  int coax_begin[kTranslate64MaxWarps + 1];
   Translate64Task rot[kTranslate64MaxTasks];
   Translate64Task coax[kTranslate64MaxTasks];
 };
 bool translate64_supported(int order);       // HFMM_TRANSLATE=32 selects the 32-pair kernel for every order
+int translate64_warps(int order);            // 8 (two CTAs per SM) or 16 (one)
+// the 64-pair kernel expects block m of every coaxial table multiplied by (-1)^m (the input signs of
+// the inverse rotation, tables.hpp); the 32-pair kernel applies them itself
+bool coax_tables_sign_folded(int order);
 void build_translate64_schedule(int order, Translate64Schedule* out);
 void upload_translate64_schedule(int order);
 void launch_translate64(const TranslateArgs& a, cudaStream_t s);

@@ -4,29 +4,35 @@
 // Gaunt-built matrix, src/expansion.cpp:95-124), factored as
 //     out += e^{-i mu phi} · E^T · Chat(k|t|) · E · e^{i m phi} · in          (tables.hpp)
 // and the same tables; what changes is the work layout, chosen to spend fewer shared-memory
-// wavefronts and fewer non-arithmetic instructions per multiply-add (ncu on the 32-pair kernel: the
-// shared-memory data pipe at 67 % was the busiest unit, FFMA2 27 % of the instructions):
+// wavefronts and fewer non-arithmetic instructions per multiply-add:
 //   * a batch is 64 pairs of one table group; a LANE OWNS TWO PAIRS and ALL 32 LANES OF A WARP RUN
-//     THE SAME TASK, so every coefficient load is warp-uniform (one wavefront per 16 bytes, half of
-//     what two half-warp sub-tasks cost) and nothing is padded to a partner's shape;
+//     THE SAME TASK, so every coefficient load is warp-uniform and nothing is padded to a partner's shape;
 //   * a task is a WHOLE block — the plus or minus system of one degree n in the rotations, one
 //     column (s_m or t_m) of one order m in the coaxial step — so it reads every operand row once,
 //     keeps all its output rows in registers (<= P+1 rows x 2 pairs) and writes them back IN PLACE:
-//     one operand tile instead of a ping-pong pair, which is what lets a 64-pair batch fit twice per SM;
-//   * the +-m fold with e^{i m phi} is fused into the gather (global -> registers -> tile) and the
-//     unfold with e^{-i mu phi} into the scatter (tile -> registers -> RED), lane = (n, m) unit of one
-//     pair: two passes over the tile and two of six barriers per batch are gone;
+//     one operand tile instead of a ping-pong pair, which is what lets a 64-pair batch fit twice per SM
+//     (P <= 12) or once (P = 13..16, sixteen warps: the largest systems are then split over two warps by
+//     pair halves — columns are independent, so the split stays in place);
 //   * the tile is [coefficient row][pair] with a pitch of 65 complex (520 bytes) and a lane owns the
 //     pairs l and l + 32: the compute stages (two 8-byte accesses per row, 32 lanes contiguous) and the
 //     transposing gather / scatter (lane = row: consecutive rows are two banks apart) are both
 //     bank-conflict free, and a task addresses its rows as base register + immediate;
 //   * folded layout of degree n: s_m (and x_0) at row n^2 + n + m, t_m at row n^2 + n - m — the rows of
 //     the raw coefficients (n, +-m), so folding is in place per unit;
-//   * a warp gathers, and later scatters, the same eight pairs of the batch: the scatter of batch i and
-//     the gather of batch i + 1 touch only the warp's own tile columns and need no CTA barrier.
-// Four barriers per batch: gather+fold | forward rotation | coaxial translation | inverse rotation |
-// (unfold+scatter runs into the next gather).  Tasks are handed to the warps by a host-side
-// longest-processing-time schedule in __constant__ memory, as before.
+//   * the signs of the inverse rotation ((-1)^m on its inputs, (-1)^mu on its outputs, tables.hpp) are not
+//     applied by the kernel: the engine folds (-1)^m into the coaxial tables it builds for this kernel
+//     (coax_tables_sign_folded), and (-1)^mu is a constant of the unfold — forward and inverse rotation
+//     are the same code;
+//   * a warp gathers, and later scatters, the same pairs of the batch, pair by pair (scatter of pair p of
+//     batch i, then the gather of pair p of batch i + 1 into the column just read): no CTA barrier
+//     separates the two, and with the order a template parameter both are straight-line code;
+//   * everything the end of a batch needs from global memory is fetched while the batch computes:
+//     source / destination rows and azimuths of the next batch arrive through 4-byte cp.async into a
+//     double-buffered metadata block, the next table group through 16-byte cp.async, and the source rows
+//     are prefetched into L2.
+// Six barriers per batch: gather | fold | forward rotation | coaxial translation | inverse rotation |
+// unfold | (scatter + next gather).  Tasks are handed to the warps by a host-side
+// longest-processing-time schedule in __constant__ memory.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -42,25 +48,28 @@ namespace hfmm_b200 {
 namespace {
 
 constexpr int kBatch64 = 64;
+constexpr int kTranslate64SplitFrom = 11;  // sixteen warps: systems of this many rows or more are cut by pair halves
 constexpr uint32_t kPitchB = 520;  // bytes per tile row: 64 pairs x float2 + 8 (rows two banks apart)
 
 struct Plan64 {
-  int dim, n_units, rot_floats, coax_c, phase_pitch;
-  uint32_t off_coax, off_phase, off_tile, off_unit;
+  int dim, n_fold, rot_floats, coax_c;
+  uint32_t off_coax, off_phase, off_tile, off_unit, off_meta;
   size_t bytes;
 };
-__host__ __device__ inline Plan64 plan64(int P) {
-  Plan64 s;
+// metadata of one batch: source row, destination row, class, (cos phi, sin phi) per pair
+constexpr uint32_t kMetaSrc = 0, kMetaDst = 256, kMetaCls = 512, kMetaCs = 768, kMetaBytes = 1280;
+__host__ __device__ constexpr Plan64 plan64(int P) {
+  Plan64 s{};
   s.dim = (P + 1) * (P + 1);
-  s.n_units = (P + 1) * (P + 2) / 2;
+  s.n_fold = P * (P + 1) / 2;  // units (n, m >= 1)
   s.rot_floats = rot_table_size(P);
   s.coax_c = coax_table_size(P);
-  s.phase_pitch = kBatch64;  // e^{i m phi}: [m][pair]
   s.off_coax = 4u * uint32_t(s.rot_floats);
-  s.off_phase = s.off_coax + 8u * uint32_t(s.coax_c);
-  s.off_tile = (s.off_phase + 8u * uint32_t((P + 1) * s.phase_pitch) + 15u) & ~15u;
+  s.off_phase = s.off_coax + 8u * uint32_t(s.coax_c);                      // e^{i m phi}: [m][pair]
+  s.off_tile = (s.off_phase + 8u * uint32_t((P + 1) * kBatch64) + 15u) & ~15u;
   s.off_unit = (s.off_tile + kPitchB * uint32_t(s.dim) + 15u) & ~15u;
-  s.bytes = size_t(s.off_unit) + size_t((4 * s.n_units + 15) & ~15);
+  s.off_meta = (s.off_unit + 4u * uint32_t(s.n_fold) + 15u) & ~15u;
+  s.bytes = size_t(s.off_meta) + 2 * kMetaBytes;
   return s;
 }
 
@@ -93,10 +102,7 @@ __device__ __forceinline__ u64 rot90(u64 v) {  // i * v
   const float2 f = unpack2(v);
   return pack2(-f.y, f.x);
 }
-__device__ __forceinline__ u64 neg2(u64 v) {
-  const float2 f = unpack2(v);
-  return pack2(-f.x, -f.y);
-}
+__device__ __forceinline__ u64 neg2(u64 v) { return v ^ 0x8000000080000000ull; }
 __device__ __forceinline__ float4 lds4(uint32_t addr) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
@@ -107,43 +113,54 @@ __device__ __forceinline__ u64 lds1(uint32_t addr) {
   asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr));
   return v;
 }
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ void sts1(uint32_t addr, u64 v) {
   asm volatile("st.shared.b64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
 }
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 
-// the lane's two pairs (l, l + 32) of a row: 8 bytes at row * pitch + 8 l and 256 bytes further
+// the lane's pairs of a row: PAIRS = 2 -> (l, l + 32), 8 bytes at row * pitch + 8 l and 256 bytes further
+template <int PAIRS>
 __device__ __forceinline__ void ld_duo(uint32_t addr, u64& a, u64& b) {
   a = lds1(addr);
-  b = lds1(addr + 256u);
+  if (PAIRS == 2) b = lds1(addr + 256u);
 }
+template <int PAIRS>
 __device__ __forceinline__ void st_duo(uint32_t addr, u64 a, u64 b) {
   sts1(addr, a);
-  sts1(addr + 256u, b);
+  if (PAIRS == 2) sts1(addr + 256u, b);
 }
 
 // ---- rotation task: one folded system of one degree, w inputs -> w outputs, in place -------------
-// out[r] = sum_k E[k][r] in[k]  (inverse rotation: same table, (-1)^k on the inputs and (-1)^r on the
-// outputs, tables.hpp).  Rows are row0 + step * index.
+// out[r] = sum_k E[k][r] in[k]; forward and inverse rotation alike (the signs of the inverse live in the
+// coaxial tables and in the unfold).  Rows are row0 + step * index.
 // `base`: byte address of the lane's first pair in row0; rows advance by stepb bytes (+- pitch).
-// The loops stay rolled (two inputs per trip): fully unrolled per size the kernel was 120 KB of SASS and
-// a fifth of the issue slots went to instruction-cache misses.
-template <int R, bool BACK>
+// The loops stay rolled: fully unrolled per size the kernel was 120 KB of SASS and a fifth of the issue
+// slots went to instruction-cache misses.
+template <int R, int PAIRS>
 __device__ __forceinline__ void rot_task64(uint32_t e_addr, uint32_t ws_b, int w, uint32_t base, int stepb) {
   u64 acc0[R], acc1[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) acc0[r] = acc1[r] = 0ull;
   constexpr int NV = (R + 3) / 4;
   uint32_t in_addr = base;
-  u64 flip = 0ull;  // inverse rotation: odd inputs enter negated (sign bits toggled on the ALU pipe)
 #pragma unroll 1
   for (int k = 0; k < w; ++k) {
-    u64 x0, x1;
-    ld_duo(in_addr, x0, x1);
-    if (BACK) {
-      x0 ^= flip;
-      x1 ^= flip;
-      flip ^= 0x8000000080000000ull;
-    }
+    u64 x0, x1 = 0ull;
+    ld_duo<PAIRS>(in_addr, x0, x1);
     float e[NV * 4];
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
@@ -153,45 +170,41 @@ __device__ __forceinline__ void rot_task64(uint32_t e_addr, uint32_t ws_b, int w
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       fma2s(acc0[r], x0, e[r]);
-      fma2s(acc1[r], x1, e[r]);
+      if (PAIRS == 2) fma2s(acc1[r], x1, e[r]);
     }
     in_addr += stepb;
     e_addr += ws_b;
   }
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    if (r < w) {
-      u64 o0 = acc0[r], o1 = acc1[r];
-      if (BACK && (r & 1)) {
-        o0 = neg2(o0);
-        o1 = neg2(o1);
-      }
-      st_duo(base + r * stepb, o0, o1);
-    }
-  }
+  for (int r = 0; r < R; ++r)
+    if (r < w) st_duo<PAIRS>(base + r * stepb, acc0[r], acc1[r]);
 }
 
-template <bool BACK>
+// RMIN..RMAX: the widths this call site can meet (split schedules send w >= kSplitFrom to the one-pair
+// tasks and everything below to the two-pair tasks): the other bodies are not instantiated
+template <int PAIRS, int RMIN, int RMAX>
 __device__ __forceinline__ void rot_dispatch64(int w, uint32_t e_addr, uint32_t ws_b, uint32_t base, int stepb) {
+#define HFMM_ROT_CASE(R_)                                                 \
+  case R_:                                                                \
+    if constexpr (R_ >= RMIN && R_ <= RMAX) rot_task64<R_, PAIRS>(e_addr, ws_b, w, base, stepb); \
+    break;
   switch (w) {
-    case 1: case 2: case 3: case 4: rot_task64<4, BACK>(e_addr, ws_b, w, base, stepb); break;
-    case 5: rot_task64<5, BACK>(e_addr, ws_b, w, base, stepb); break;
-    case 6: rot_task64<6, BACK>(e_addr, ws_b, w, base, stepb); break;
-    case 7: rot_task64<7, BACK>(e_addr, ws_b, w, base, stepb); break;
-    case 8: rot_task64<8, BACK>(e_addr, ws_b, w, base, stepb); break;
-    case 9: rot_task64<9, BACK>(e_addr, ws_b, w, base, stepb); break;
-    case 10: rot_task64<10, BACK>(e_addr, ws_b, w, base, stepb); break;
-    case 11: rot_task64<11, BACK>(e_addr, ws_b, w, base, stepb); break;
-    case 12: rot_task64<12, BACK>(e_addr, ws_b, w, base, stepb); break;
-    default: rot_task64<13, BACK>(e_addr, ws_b, w, base, stepb); break;
+    case 1: case 2: case 3: case 4:
+      if constexpr (RMIN <= 4) rot_task64<4, PAIRS>(e_addr, ws_b, w, base, stepb);
+      break;
+    HFMM_ROT_CASE(5) HFMM_ROT_CASE(6) HFMM_ROT_CASE(7) HFMM_ROT_CASE(8) HFMM_ROT_CASE(9) HFMM_ROT_CASE(10)
+    HFMM_ROT_CASE(11) HFMM_ROT_CASE(12) HFMM_ROT_CASE(13) HFMM_ROT_CASE(14) HFMM_ROT_CASE(15) HFMM_ROT_CASE(16)
+    HFMM_ROT_CASE(17)
+    default: break;
   }
+#undef HFMM_ROT_CASE
 }
 
 // ---- coaxial task: one folded column of one order m, degrees n = m .. P -> nu = m .. P, in place ---
 // rows: n^2 + n + sgn m, advancing by 2n + 2 per degree
 // `base`: byte address of the lane's first pair in the row of degree n = m; the row of degree n + 1 is
 // stepb bytes further, stepb growing by 2 pitches per degree
-template <int R>
+template <int R, int PAIRS>
 __device__ __forceinline__ void coax_task64(uint32_t c_addr, uint32_t ws_b, int w, uint32_t base, int stepb) {
   u64 p0[R], p1[R];
 #pragma unroll
@@ -201,8 +214,8 @@ __device__ __forceinline__ void coax_task64(uint32_t c_addr, uint32_t ws_b, int 
   int step = stepb;
 #pragma unroll 1
   for (int k = 0; k < w; ++k) {
-    u64 x0, x1;
-    ld_duo(in_addr, x0, x1);
+    u64 x0, x1 = 0ull;
+    ld_duo<PAIRS>(in_addr, x0, x1);
     const u64 t0 = rot90(x0), t1 = rot90(x1);
     float cr[NV * 2], ci[NV * 2];
 #pragma unroll
@@ -214,12 +227,12 @@ __device__ __forceinline__ void coax_task64(uint32_t c_addr, uint32_t ws_b, int 
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       fma2s(p0[r], x0, cr[r]);
-      fma2s(p1[r], x1, cr[r]);
+      if (PAIRS == 2) fma2s(p1[r], x1, cr[r]);
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       fma2s(p0[r], t0, ci[r]);
-      fma2s(p1[r], t1, ci[r]);
+      if (PAIRS == 2) fma2s(p1[r], t1, ci[r]);
     }
     in_addr += step;
     step += 2 * int(kPitchB);
@@ -229,36 +242,94 @@ __device__ __forceinline__ void coax_task64(uint32_t c_addr, uint32_t ws_b, int 
   step = stepb;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    if (r < w) st_duo(out_addr, p0[r], p1[r]);
+    if (r < w) st_duo<PAIRS>(out_addr, p0[r], p1[r]);
     out_addr += step;
     step += 2 * int(kPitchB);
   }
 }
 
+template <int PAIRS, int RMIN, int RMAX>
 __device__ __forceinline__ void coax_dispatch64(int w, uint32_t c_addr, uint32_t ws_b, uint32_t base, int stepb) {
+#define HFMM_COAX_CASE(R_)                                                  \
+  case R_:                                                                  \
+    if constexpr (R_ >= RMIN && R_ <= RMAX) coax_task64<R_, PAIRS>(c_addr, ws_b, w, base, stepb); \
+    break;
   switch (w) {
-    case 1: case 2: coax_task64<2>(c_addr, ws_b, w, base, stepb); break;
-    case 3: case 4: coax_task64<4>(c_addr, ws_b, w, base, stepb); break;
-    case 5: coax_task64<5>(c_addr, ws_b, w, base, stepb); break;
-    case 6: coax_task64<6>(c_addr, ws_b, w, base, stepb); break;
-    case 7: coax_task64<7>(c_addr, ws_b, w, base, stepb); break;
-    case 8: coax_task64<8>(c_addr, ws_b, w, base, stepb); break;
-    case 9: coax_task64<9>(c_addr, ws_b, w, base, stepb); break;
-    case 10: coax_task64<10>(c_addr, ws_b, w, base, stepb); break;
-    case 11: coax_task64<11>(c_addr, ws_b, w, base, stepb); break;
-    case 12: coax_task64<12>(c_addr, ws_b, w, base, stepb); break;
-    default: coax_task64<13>(c_addr, ws_b, w, base, stepb); break;
+    case 1: case 2:
+      if constexpr (RMIN <= 2) coax_task64<2, PAIRS>(c_addr, ws_b, w, base, stepb);
+      break;
+    case 3: case 4:
+      if constexpr (RMIN <= 4) coax_task64<4, PAIRS>(c_addr, ws_b, w, base, stepb);
+      break;
+    HFMM_COAX_CASE(5) HFMM_COAX_CASE(6) HFMM_COAX_CASE(7) HFMM_COAX_CASE(8) HFMM_COAX_CASE(9) HFMM_COAX_CASE(10)
+    HFMM_COAX_CASE(11) HFMM_COAX_CASE(12) HFMM_COAX_CASE(13) HFMM_COAX_CASE(14) HFMM_COAX_CASE(15) HFMM_COAX_CASE(16)
+    HFMM_COAX_CASE(17)
+    default: break;
   }
+#undef HFMM_COAX_CASE
 }
 
-__constant__ Translate64Schedule c_sched64[kTranslate64MaxOrder + 1];
+__constant__ Translate64Schedule c_sched64[kTranslate64TopOrder + 1];
 
+// one (n, m >= 1) unit of the lane's two pairs: fold, in place
+//   a = x_m e^{i m phi},  b = (-1)^m x_{-m} e^{-i m phi}:   s_m = a + b -> row (n, +m),  t_m = a - b -> row (n, -m)
+struct FoldUnit {
+  u64 xp0, xp1, xm0, xm1, ph0, ph1;
+  uint32_t ap, am;
+  float sg;
+};
+__device__ __forceinline__ void unit_load(FoldUnit& f, uint32_t un, uint32_t duo, uint32_t ph_duo) {
+  const uint32_t m = un >> 20;
+  f.ap = duo + (un & 0xfffffu);
+  f.am = f.ap - m * (2u * kPitchB);
+  f.xp0 = lds1(f.ap);
+  f.xp1 = lds1(f.ap + 256u);
+  f.xm0 = lds1(f.am);
+  f.xm1 = lds1(f.am + 256u);
+  f.ph0 = lds1(ph_duo + m * (8u * kBatch64));
+  f.ph1 = lds1(ph_duo + m * (8u * kBatch64) + 256u);
+  f.sg = (m & 1) ? -1.0f : 1.0f;
+}
+__device__ __forceinline__ void fold_finish(const FoldUnit& f) {
+  const float2 f0 = unpack2(f.ph0), f1 = unpack2(f.ph1);
+  u64 a0 = mul2s(f.xp0, f0.x), a1 = mul2s(f.xp1, f1.x), b0 = mul2s(f.xm0, f.sg * f0.x), b1 = mul2s(f.xm1, f.sg * f1.x);
+  fma2s(a0, rot90(f.xp0), f0.y);
+  fma2s(a1, rot90(f.xp1), f1.y);
+  fma2s(b0, rot90(f.xm0), -f.sg * f0.y);
+  fma2s(b1, rot90(f.xm1), -f.sg * f1.y);
+  sts1(f.ap, add2(a0, b0));
+  sts1(f.ap + 256u, add2(a1, b1));
+  sts1(f.am, add2(a0, neg2(b0)));
+  sts1(f.am + 256u, add2(a1, neg2(b1)));
+}
+// unfold of the inverse rotation's outputs u' (row (n, +m)), v' (row (n, -m)), which still lack the
+// (-1)^mu of the symmetry:  y_m = (-1)^m (u' + v')/2 e^{-i m phi},   y_{-m} = (u' - v')/2 e^{+i m phi}
+__device__ __forceinline__ void unfold_finish(const FoldUnit& f) {
+  const float hs = 0.5f * f.sg;
+  const float2 f0 = unpack2(f.ph0), f1 = unpack2(f.ph1);
+  const u64 s0 = add2(f.xp0, f.xm0), s1 = add2(f.xp1, f.xm1);
+  const u64 d0 = add2(f.xp0, neg2(f.xm0)), d1 = add2(f.xp1, neg2(f.xm1));
+  u64 yp0 = mul2s(s0, hs * f0.x), yp1 = mul2s(s1, hs * f1.x), ym0 = mul2s(d0, 0.5f * f0.x), ym1 = mul2s(d1, 0.5f * f1.x);
+  fma2s(yp0, rot90(s0), -hs * f0.y);
+  fma2s(yp1, rot90(s1), -hs * f1.y);
+  fma2s(ym0, rot90(d0), 0.5f * f0.y);
+  fma2s(ym1, rot90(d1), 0.5f * f1.y);
+  sts1(f.ap, yp0);
+  sts1(f.ap + 256u, yp1);
+  sts1(f.am, ym0);
+  sts1(f.am + 256u, ym1);
+}
+
+// PT: the order as a compile-time constant (0: run-time order, any P the launch geometry holds)
+// WARPS: 8 (two CTAs per SM, P <= 12) or 16 (one CTA per SM, P <= 16; large systems split by pair halves)
 // STAGED: every pair owns its destination row (deterministic mode): plain stores instead of RED
-template <bool STAGED>
-__global__ void __launch_bounds__(kTranslate64Warps * 32, 2) translate64_kernel(const TranslateArgs a) {
-  constexpr int kWarps = kTranslate64Warps, kThreads = kWarps * 32, kPairsPerWarp = kBatch64 / kWarps;
+template <int PT, int WARPS, bool STAGED>
+__global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? 2 : 1) translate64_kernel(const TranslateArgs a) {
+  constexpr int kThreads = WARPS * 32, kPairsPerWarp = kBatch64 / WARPS;
+  constexpr int RMAX = PT ? PT + 1 : (WARPS == 8 ? kTranslate64MaxOrder + 1 : kTranslate64TopOrder + 1);
+  constexpr bool kSplit = WARPS == 16;
   extern __shared__ __align__(16) unsigned char smem64[];
-  const int P = a.order;
+  const int P = PT ? PT : a.order;
   const Plan64 sp = plan64(P);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t it_begin = uint32_t(uint64_t(a.n_items) * blockIdx.x / gridDim.x);
@@ -267,210 +338,257 @@ __global__ void __launch_bounds__(kTranslate64Warps * 32, 2) translate64_kernel(
 
   const uint32_t win = uint32_t(__cvta_generic_to_shared(smem64));
   const uint32_t tile = win + sp.off_tile, ph_base = win + sp.off_phase, duo = tile + 8u * uint32_t(lane);
-  // per unit (n, m >= 0): row of (n, +m) | m << 16; the row of (n, -m) is 2 m rows back
-  uint32_t* s_unit = reinterpret_cast<uint32_t*>(smem64 + sp.off_unit);
-  for (int u = tid; u < sp.n_units; u += kThreads) {
-    int n = int((sqrtf(8.0f * float(u) + 1.0f) - 1.0f) * 0.5f);
-    while (n * (n + 1) / 2 > u) --n;
-    while ((n + 1) * (n + 2) / 2 <= u) ++n;
-    const int m = u - n * (n + 1) / 2;
-    s_unit[u] = uint32_t(n * n + n + m) | uint32_t(m) << 16;
+  const uint32_t unit_base = win + sp.off_unit, meta_base = win + sp.off_meta;
+  // units (n, m >= 1), m-major: byte offset of row (n, +m) | m << 20; the row of (n, -m) is 2 m rows back
+  {
+    uint32_t* s_unit = reinterpret_cast<uint32_t*>(smem64 + sp.off_unit);
+    for (int u = tid; u < sp.n_fold; u += kThreads) {
+      int m = 1, first = 0;
+      while (first + (P + 1 - m) <= u) {
+        first += P + 1 - m;
+        ++m;
+      }
+      const int n = m + (u - first);
+      s_unit[u] = uint32_t(n * n + n + m) * kPitchB | uint32_t(m) << 20;
+    }
   }
   // idle pair columns of a partial batch must stay finite: clear the tile once
   for (uint32_t i = tid; i < uint32_t(sp.dim) * (kPitchB / 8); i += kThreads) sts1(tile + 8u * i, 0ull);
 
   const Translate64Schedule& sched = c_sched64[P];
-  auto fetch_tables = [&](const TranslateClass& cls) {
-    const float4* g_rot = reinterpret_cast<const float4*>(a.rot_tables + size_t(cls.rot) * sp.rot_floats);
-    const float4* g_coax = reinterpret_cast<const float4*>(a.coax_tables + size_t(cls.coax) * sp.coax_c * 2);
-    for (int i = tid; i < sp.rot_floats / 4; i += kThreads)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(win + 16u * i), "l"(g_rot + i) : "memory");
-    for (int i = tid; i < sp.coax_c / 2; i += kThreads)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(win + sp.off_coax + 16u * i), "l"(g_coax + i) : "memory");
-    asm volatile("cp.async.commit_group;" ::: "memory");
+  auto fetch_tables = [&](uint32_t cls) {
+    const TranslateClass c = a.classes[cls];
+    const float4* g_rot = reinterpret_cast<const float4*>(a.rot_tables + size_t(c.rot) * sp.rot_floats);
+    const float4* g_coax = reinterpret_cast<const float4*>(a.coax_tables + size_t(c.coax) * sp.coax_c * 2);
+    for (int i = tid; i < sp.rot_floats / 4; i += kThreads) cp_async16(win + 16u * i, g_rot + i);
+    for (int i = tid; i < sp.coax_c / 2; i += kThreads) cp_async16(win + sp.off_coax + 16u * i, g_coax + i);
   };
 
-  // the warp's pairs of a batch: source / destination rows and azimuths; lane l < 8 holds pair 8 warp + l
-  const int p_first = warp * kPairsPerWarp;
-  uint32_t my_src = 0, my_dst = 0;
-  bool my_live = false;
-  // e^{i m phi} of every pair of the batch, [m][pair]; each warp fills the columns of its own pairs
-  auto load_pairs = [&](const TranslateItem& it) {
-    my_live = false;
-    if (lane < kPairsPerWarp) {
-      const int p = p_first + lane;
-      my_live = p < int(it.count);
-      float cphi = 1.f, sphi = 0.f;
-      if (my_live) {
-        my_src = a.pair_src[it.pair_begin + p];
-        my_dst = a.pair_dst[it.pair_begin + p];
-        const TranslateClass c = a.classes[a.pair_cls[it.pair_begin + p]];
-        cphi = c.cphi;
-        sphi = c.sphi;
-      }
-      float cr = 1.f, ci = 0.f;
-      uint32_t dst = ph_base + 8u * uint32_t(p);
-      for (int m = 0; m <= P; ++m) {
-        sts1(dst, pack2(cr, ci));
-        dst += 8u * kBatch64;
-        const float t = cr * cphi - ci * sphi;
-        ci = ci * cphi + cr * sphi;
+  // ---- batch metadata, double-buffered: thread p < 64 fetches pair p -------------------------------
+  // stage A: source row, destination row, class;  stage B (after A has landed): azimuth of the class
+  auto meta_a = [&](const TranslateItem& it, uint32_t mb) {
+    if (tid < kBatch64) {
+      const uint32_t p = min(uint32_t(tid), it.count - 1u) + it.pair_begin;  // idle columns repeat the last pair
+      cp_async4(mb + kMetaSrc + 4u * tid, a.pair_src + p);
+      cp_async4(mb + kMetaDst + 4u * tid, a.pair_dst + p);
+      cp_async4(mb + kMetaCls + 4u * tid, a.pair_cls + p);
+    }
+  };
+  auto meta_b = [&](uint32_t mb) {
+    if (tid < kBatch64) {
+      const uint32_t cls = lds32(mb + kMetaCls + 4u * tid);
+      cp_async8(mb + kMetaCs + 8u * tid, &a.classes[cls].cphi);
+    }
+  };
+  // e^{i m phi} of the warp's pairs, [m][pair]: lane = (pair, group of four orders)
+  auto write_phases = [&](uint32_t mb) {
+    constexpr int kGroups = 32 / kPairsPerWarp;                 // 4 (eight pairs per warp) or 8 (four)
+    const int pp = lane % kPairsPerWarp, g = lane / kPairsPerWarp;
+    const int per = (P + kGroups) / kGroups;                    // orders per group, ceil((P + 1) / groups)
+    const float2 c1 = unpack2(lds1(mb + kMetaCs + 8u * uint32_t(warp * kPairsPerWarp + pp)));
+    // e^{i (g per) phi} by binary powering
+    float cr = 1.f, ci = 0.f, br = c1.x, bi = c1.y;
+    for (int e = g * per; e; e >>= 1) {
+      if (e & 1) {
+        const float t = cr * br - ci * bi;
+        ci = ci * br + cr * bi;
         cr = t;
       }
+      const float t = br * br - bi * bi;
+      bi = 2.f * br * bi;
+      br = t;
+    }
+    uint32_t dst = ph_base + 8u * uint32_t(g * per * kBatch64 + warp * kPairsPerWarp + pp);
+    for (int j = 0, m = g * per; j < per && m <= P; ++j, ++m) {
+      sts1(dst, pack2(cr, ci));
+      dst += 8u * kBatch64;
+      const float t = cr * c1.x - ci * c1.y;
+      ci = ci * c1.x + cr * c1.y;
+      cr = t;
+    }
+  };
+  // L2 prefetch of the source rows of the batch described by mb (lane = 128-byte line of a row)
+  auto prefetch_rows = [&](uint32_t mb, uint32_t count) {
+    const uint32_t row_bytes = 8u * uint32_t(sp.dim);
+#pragma unroll 1
+    for (int pp = 0; pp < kPairsPerWarp; ++pp) {
+      const uint32_t p = uint32_t(warp * kPairsPerWarp + pp);
+      if (p >= count) break;
+      const uint32_t srow = lds32(mb + kMetaSrc + 4u * p);
+      const char* row = reinterpret_cast<const char*>(a.src + size_t(srow) * a.stride);
+      const uint32_t off = 128u * uint32_t(lane);
+      if (off < row_bytes) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + off));
     }
   };
 
-  // gather: the raw rows of the warp's pairs are copied straight into their tile columns (cp.async,
-  // lane = coefficient: 256 contiguous bytes per instruction; consecutive tile rows are two banks apart)
-  constexpr int kRounds = (kTranslate64MaxDim + 31) / 32;  // 32 coefficients of one pair per warp instruction
-  auto issue_gather = [&]() {
-#pragma unroll 1
-    for (int pp = 0; pp < kPairsPerWarp; ++pp) {
-      const bool live = __shfl_sync(0xffffffffu, my_live, pp);
-      if (!live) continue;  // warp-uniform; the column keeps its (finite) previous contents
-      const uint32_t srow = __shfl_sync(0xffffffffu, my_src, pp);
-      const float2* src = a.src + size_t(srow) * a.stride + lane;
-      const uint32_t dst = tile + 8u * uint32_t(p_first + pp) + kPitchB * uint32_t(lane);
+  // gather of pair column `col` <- source row (cp.async, lane = coefficient: 256 contiguous bytes per
+  // instruction; consecutive tile rows are two banks apart); scatter: the same mapping back (RED.64)
+  constexpr int kRoundsT = PT ? ((PT + 1) * (PT + 1) + 31) / 32 : 0;
+  auto gather_pair = [&](uint32_t col, uint32_t srow) {
+    const float2* src = a.src + size_t(srow) * a.stride + lane;
+    if constexpr (PT != 0) {
 #pragma unroll
-      for (int r = 0; r < kRounds; ++r)
-        if (32 * r + lane < sp.dim)
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 32u * r * kPitchB), "l"(src + 32 * r) : "memory");
+      for (int r = 0; r < kRoundsT; ++r)
+        if (32 * r + 32 <= (PT + 1) * (PT + 1) || 32 * r + lane < (PT + 1) * (PT + 1))
+          cp_async8(col + 32u * r * kPitchB, src + 32 * r);
+    } else {
+      for (int r = 0; 32 * r + lane < sp.dim; ++r) cp_async8(col + 32u * r * kPitchB, src + 32 * r);
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  // scatter: the same mapping back, tile column -> destination row (RED.64, 256 contiguous bytes each)
-  auto scatter = [&]() {
-#pragma unroll 1
-    for (int pp = 0; pp < kPairsPerWarp; ++pp) {
-      const bool live = __shfl_sync(0xffffffffu, my_live, pp);
-      if (!live) continue;
-      const uint32_t drow = __shfl_sync(0xffffffffu, my_dst, pp);
-      float2* dst = a.dst + size_t(drow) * a.stride + lane;
-      const uint32_t src = tile + 8u * uint32_t(p_first + pp) + kPitchB * uint32_t(lane);
+  auto scatter_pair = [&](uint32_t col, uint32_t drow) {
+    float2* dst = a.dst + size_t(drow) * a.stride + lane;
+    if constexpr (PT != 0) {
+      u64 v[kRoundsT];
 #pragma unroll
-      for (int r = 0; r < kRounds; ++r)
-        if (32 * r + lane < sp.dim) {
-          const float2 v = unpack2(lds1(src + 32u * r * kPitchB));
-          if (STAGED) dst[32 * r] = v;
-          else atomicAdd(dst + 32 * r, v);
+      for (int r = 0; r < kRoundsT; ++r)
+        if (32 * r + 32 <= (PT + 1) * (PT + 1) || 32 * r + lane < (PT + 1) * (PT + 1)) v[r] = lds1(col + 32u * r * kPitchB);
+#pragma unroll
+      for (int r = 0; r < kRoundsT; ++r)
+        if (32 * r + 32 <= (PT + 1) * (PT + 1) || 32 * r + lane < (PT + 1) * (PT + 1)) {
+          if (STAGED) dst[32 * r] = unpack2(v[r]);
+          else atomicAdd(dst + 32 * r, unpack2(v[r]));
         }
-    }
-  };
-
-  // fold and unfold, in place, all 64 pairs of a unit (n, m >= 0) per warp step (a lane owns the pairs
-  // l and l + 32 as in the compute stages; the unit — rows, order, sign — is warp-uniform):
-  //   fold    a = x_m e^{i m phi},  b = (-1)^m x_{-m} e^{-i m phi}:   s_m = a + b -> row (n, +m),  t_m = a - b -> row (n, -m)
-  //   unfold  y_m = (u + v)/2 e^{-i m phi},   y_{-m} = (-1)^m (u - v)/2 e^{+i m phi}
-  const uint32_t ph_duo = ph_base + 8u * uint32_t(lane);
-  auto fold = [&]() {
-#pragma unroll 1
-    for (int u = warp; u < sp.n_units; u += kWarps) {
-      const uint32_t un = s_unit[u], rp = un & 0xffffu, m = un >> 16;
-      const uint32_t ap = duo + rp * kPitchB, am = ap - 2u * m * kPitchB;
-      u64 xp0, xp1;
-      ld_duo(ap, xp0, xp1);
-      if (m == 0) continue;  // x_0 is its own folded value (e^{i 0} = 1)
-      u64 xm0, xm1, ph0, ph1;
-      ld_duo(am, xm0, xm1);
-      ld_duo(ph_duo + 8u * kBatch64 * m, ph0, ph1);
-      const float sg = (m & 1) ? -1.0f : 1.0f;
-      const float2 f0 = unpack2(ph0), f1 = unpack2(ph1);
-      u64 a0 = mul2s(xp0, f0.x), a1 = mul2s(xp1, f1.x), b0 = mul2s(xm0, sg * f0.x), b1 = mul2s(xm1, sg * f1.x);
-      fma2s(a0, rot90(xp0), f0.y);
-      fma2s(a1, rot90(xp1), f1.y);
-      fma2s(b0, rot90(xm0), -sg * f0.y);
-      fma2s(b1, rot90(xm1), -sg * f1.y);
-      st_duo(ap, add2(a0, b0), add2(a1, b1));
-      st_duo(am, add2(a0, neg2(b0)), add2(a1, neg2(b1)));
-    }
-  };
-  auto unfold = [&]() {
-#pragma unroll 1
-    for (int u = warp; u < sp.n_units; u += kWarps) {
-      const uint32_t un = s_unit[u], rp = un & 0xffffu, m = un >> 16;
-      if (m == 0) continue;  // y_0 = u_0
-      const uint32_t ap = duo + rp * kPitchB, am = ap - 2u * m * kPitchB;
-      u64 u0, u1, v0, v1, ph0, ph1;
-      ld_duo(ap, u0, u1);
-      ld_duo(am, v0, v1);
-      ld_duo(ph_duo + 8u * kBatch64 * m, ph0, ph1);
-      const float hs = (m & 1) ? -0.5f : 0.5f;
-      const float2 f0 = unpack2(ph0), f1 = unpack2(ph1);
-      const u64 s0 = add2(u0, v0), s1 = add2(u1, v1), d0 = add2(u0, neg2(v0)), d1 = add2(u1, neg2(v1));
-      u64 yp0 = mul2s(s0, 0.5f * f0.x), yp1 = mul2s(s1, 0.5f * f1.x), ym0 = mul2s(d0, hs * f0.x), ym1 = mul2s(d1, hs * f1.x);
-      fma2s(yp0, rot90(s0), -0.5f * f0.y);
-      fma2s(yp1, rot90(s1), -0.5f * f1.y);
-      fma2s(ym0, rot90(d0), hs * f0.y);
-      fma2s(ym1, rot90(d1), hs * f1.y);
-      st_duo(ap, yp0, yp1);
-      st_duo(am, ym0, ym1);
-    }
-  };
-
-  TranslateItem item = a.items[it_begin];
-  uint32_t loaded_grp = item.group;
-  fetch_tables(a.classes[a.pair_cls[item.pair_begin]]);
-  __syncthreads();  // s_unit, the cleared tile
-  load_pairs(item);
-  issue_gather();
-
-  for (uint32_t it = it_begin; it < it_end; ++it) {
-    asm volatile("cp.async.wait_all;" ::: "memory");  // this batch's rows, this group's tables
-    __syncthreads();
-    fold();
-    __syncthreads();
-    // stage B: forward rotation, in place
-    for (int t = sched.rot_begin[warp]; t < sched.rot_begin[warp + 1]; ++t) {
-      const Translate64Task d = sched.rot[t];
-      rot_dispatch64<false>(d.w, win + d.tab_off, d.ws_b, duo + d.row0 * kPitchB, d.step * int(kPitchB));
-    }
-    __syncthreads();
-    // stage C: coaxial translation, in place
-    for (int t = sched.coax_begin[warp]; t < sched.coax_begin[warp + 1]; ++t) {
-      const Translate64Task d = sched.coax[t];
-      coax_dispatch64(d.w, win + d.tab_off, d.ws_b, duo + d.row0 * kPitchB, d.step * int(kPitchB));
-    }
-    __syncthreads();
-    // stage D: inverse rotation, in place (same table, sign-twiddled)
-    for (int t = sched.rot_begin[warp]; t < sched.rot_begin[warp + 1]; ++t) {
-      const Translate64Task d = sched.rot[t];
-      rot_dispatch64<true>(d.w, win + d.tab_off, d.ws_b, duo + d.row0 * kPitchB, d.step * int(kPitchB));
-    }
-    __syncthreads();
-    // the tables have had their last reader: fetch the next group's behind the unfold and the scatter
-    TranslateItem next = item;
-    const bool has_next = it + 1 < it_end;
-    if (has_next) {
-      next = a.items[it + 1];
-      if (next.group != loaded_grp) {  // CTA-uniform
-        fetch_tables(a.classes[a.pair_cls[next.pair_begin]]);
-        loaded_grp = next.group;
+    } else {
+      for (int r = 0; 32 * r + lane < sp.dim; ++r) {
+        const float2 v = unpack2(lds1(col + 32u * r * kPitchB));
+        if (STAGED) dst[32 * r] = v;
+        else atomicAdd(dst + 32 * r, v);
       }
     }
-    unfold();
-    __syncthreads();
-    // scatter, then this warp's columns of the next batch: a warp reads and rewrites only its own eight
-    // tile columns and phase columns, so no CTA barrier separates the two
-    scatter();
-    if (has_next) {
-      load_pairs(next);
-      issue_gather();
+  };
+
+  // fold and unfold, in place, all 64 pairs of a unit per warp step (a lane owns the pairs l and l + 32 as
+  // in the compute stages); a warp walks a contiguous chunk of the m-major unit list two units at a time
+  const uint32_t ph_duo = ph_base + 8u * uint32_t(lane);
+  const int u_begin = sp.n_fold * warp / WARPS, u_end = sp.n_fold * (warp + 1) / WARPS;
+  auto fold_or_unfold = [&](auto finish) {
+    int u = u_begin;
+#pragma unroll 1
+    for (; u + 1 < u_end; u += 2) {
+      FoldUnit fa, fb;
+      unit_load(fa, lds32(unit_base + 4u * u), duo, ph_duo);
+      unit_load(fb, lds32(unit_base + 4u * u + 4u), duo, ph_duo);
+      finish(fa);
+      finish(fb);
     }
+    if (u < u_end) {
+      FoldUnit fa;
+      unit_load(fa, lds32(unit_base + 4u * u), duo, ph_duo);
+      finish(fa);
+    }
+  };
+
+  auto run_rot = [&]() {
+    for (int t = sched.rot_begin[warp]; t < sched.rot_begin[warp + 1]; ++t) {
+      const Translate64Task d = sched.rot[t];
+      const uint32_t base = duo + d.row0 * kPitchB;
+      if (kSplit && d.half) rot_dispatch64<1, kTranslate64SplitFrom, RMAX>(d.w, win + d.tab_off, d.ws_b, base + 256u * (d.half - 1), d.step * int(kPitchB));
+      else rot_dispatch64<2, 1, kSplit ? kTranslate64SplitFrom - 1 : RMAX>(d.w, win + d.tab_off, d.ws_b, base, d.step * int(kPitchB));
+    }
+  };
+  auto run_coax = [&]() {
+    for (int t = sched.coax_begin[warp]; t < sched.coax_begin[warp + 1]; ++t) {
+      const Translate64Task d = sched.coax[t];
+      const uint32_t base = duo + d.row0 * kPitchB;
+      if (kSplit && d.half) coax_dispatch64<1, kTranslate64SplitFrom, RMAX>(d.w, win + d.tab_off, d.ws_b, base + 256u * (d.half - 1), d.step * int(kPitchB));
+      else coax_dispatch64<2, 1, kSplit ? kTranslate64SplitFrom - 1 : RMAX>(d.w, win + d.tab_off, d.ws_b, base, d.step * int(kPitchB));
+    }
+  };
+
+  // ---- prologue: tables and metadata of the first batch, its phases and its gather -----------------
+  TranslateItem item = a.items[it_begin];
+  uint32_t loaded_grp = item.group;
+  uint32_t mb_cur = meta_base, mb_next = meta_base + kMetaBytes;
+  fetch_tables(item.cls);
+  meta_a(item, mb_cur);
+  cp_commit();
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  meta_b(mb_cur);
+  cp_commit();
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();  // the unit table, the cleared tile, the metadata
+  write_phases(mb_cur);
+#pragma unroll 1
+  for (int pp = 0; pp < kPairsPerWarp; ++pp) {
+    const uint32_t p = uint32_t(warp * kPairsPerWarp + pp);
+    if (p < item.count) gather_pair(tile + 8u * p + kPitchB * uint32_t(lane), lds32(mb_cur + kMetaSrc + 4u * p));
+  }
+  cp_commit();
+
+  for (uint32_t it = it_begin; it < it_end; ++it) {
+    const bool has_next = it + 1 < it_end;
+    TranslateItem next = item;
+    if (has_next) next = a.items[it + 1];
+    asm volatile("cp.async.wait_all;" ::: "memory");  // this batch's rows, this group's tables
+    __syncthreads();
+    if (has_next) meta_a(next, mb_next);
+    cp_commit();
+    fold_or_unfold([](const FoldUnit& f) { fold_finish(f); });
+    __syncthreads();
+    run_rot();  // forward rotation, in place
+    if (has_next) {
+      asm volatile("cp.async.wait_all;" ::: "memory");  // own stage-A copies (long landed)
+      meta_b(mb_next);
+    }
+    cp_commit();
+    __syncthreads();
+    run_coax();  // coaxial translation, in place
+    __syncthreads();
+    if (has_next) prefetch_rows(mb_next, next.count);  // stage A is visible to every warp since the last barrier
+    run_rot();  // inverse rotation, in place (same table; signs in the coaxial table and the unfold)
+    asm volatile("cp.async.wait_all;" ::: "memory");  // own stage-B copies
+    __syncthreads();
+    // the tables have had their last reader: fetch the next group's behind the unfold and the scatter
+    if (has_next && next.group != loaded_grp) {  // CTA-uniform
+      fetch_tables(next.cls);
+      loaded_grp = next.group;
+    }
+    cp_commit();
+    fold_or_unfold([](const FoldUnit& f) { unfold_finish(f); });
+    __syncthreads();
+    // scatter, then this warp's columns of the next batch: a warp reads and rewrites only its own
+    // tile columns and phase columns, so no CTA barrier separates the two
+#pragma unroll
+    for (int pp = 0; pp < kPairsPerWarp; ++pp) {
+      const uint32_t p = uint32_t(warp * kPairsPerWarp + pp);
+      const uint32_t col = tile + 8u * p + kPitchB * uint32_t(lane);
+      if (p < item.count) scatter_pair(col, lds32(mb_cur + kMetaDst + 4u * p));
+      if (has_next && p < next.count) gather_pair(col, lds32(mb_next + kMetaSrc + 4u * p));
+    }
+    cp_commit();
+    if (has_next) write_phases(mb_next);
     item = next;
+    const uint32_t t = mb_cur;
+    mb_cur = mb_next;
+    mb_next = t;
   }
 }
 
 }  // namespace
 
 // host side: one task per folded system of a degree (rotations) / per folded column of an order
-// (coaxial step), handed to the warps longest processing time first
+// (coaxial step), handed to the warps longest processing time first; with sixteen warps the systems of
+// more than kSplitFrom rows are cut into two tasks of 32 pairs each
 void build_translate64_schedule(int P, Translate64Schedule* out) {
   const Plan64 sp = plan64(P);
+  const int warps = translate64_warps(P);
+  constexpr int kSplitFrom = kTranslate64SplitFrom;
   struct T {
     Translate64Task d;
     int cost;
   };
   std::vector<T> rot, coax;
+  auto push = [&](std::vector<T>& v, T t) {
+    if (warps == 16 && t.d.w >= kSplitFrom) {
+      t.cost = t.cost / 2 + 20;
+      t.d.half = 1;
+      v.push_back(t);
+      t.d.half = 2;
+      v.push_back(t);
+    } else {
+      v.push_back(t);
+    }
+  };
   for (int n = 0; n <= P; ++n) {
     T plus{};
     plus.d.tab_off = 4u * uint32_t(rot_block_offset(n));
@@ -478,8 +596,8 @@ void build_translate64_schedule(int P, Translate64Schedule* out) {
     plus.d.w = uint8_t(n + 1);
     plus.d.row0 = uint16_t(n * n + n);
     plus.d.step = 1;
-    plus.cost = (n + 1) * (2 * (n + 1) + 6) + 2 * (n + 1) + 30;
-    rot.push_back(plus);
+    plus.cost = (n + 1) * (2 * std::max(n + 1, 4) + 6) + 2 * (n + 1) + 30;
+    push(rot, plus);
     if (n) {
       T minus{};
       minus.d.tab_off = 4u * uint32_t(rot_minus_offset(n));
@@ -487,8 +605,8 @@ void build_translate64_schedule(int P, Translate64Schedule* out) {
       minus.d.w = uint8_t(n);
       minus.d.row0 = uint16_t(n * n + n - 1);
       minus.d.step = -1;
-      minus.cost = n * (2 * n + 6) + 2 * n + 30;
-      rot.push_back(minus);
+      minus.cost = n * (2 * std::max(n, 4) + 6) + 2 * n + 30;
+      push(rot, minus);
     }
   }
   for (int m = 0; m <= P; ++m) {
@@ -501,28 +619,29 @@ void build_translate64_schedule(int P, Translate64Schedule* out) {
       t.d.row0 = uint16_t(m * m + m + (col ? -m : m));
       t.d.step = int16_t(2 * m + 2);
       t.cost = w * (4 * w + 8) + 2 * w + 30;
-      coax.push_back(t);
+      push(coax, t);
     }
   }
   if (rot.size() > size_t(kTranslate64MaxTasks) || coax.size() > size_t(kTranslate64MaxTasks))
     throw Error(HFMM_ERR_INTERNAL, "translation schedule overflow");
-  auto distribute = [](std::vector<T>& tasks, Translate64Task* flat, int* begin) {
+  auto distribute = [&](std::vector<T>& tasks, Translate64Task* flat, int* begin) {
     std::stable_sort(tasks.begin(), tasks.end(), [](const T& x, const T& y) { return x.cost > y.cost; });
-    std::vector<std::vector<int>> per(kTranslate64Warps);
-    std::vector<long> load(kTranslate64Warps, 0);
+    std::vector<std::vector<int>> per(warps);
+    std::vector<long> load(warps, 0);
     for (size_t i = 0; i < tasks.size(); ++i) {
       int best = 0;
-      for (int w = 1; w < kTranslate64Warps; ++w)
+      for (int w = 1; w < warps; ++w)
         if (load[w] < load[best]) best = w;
       per[best].push_back(int(i));
       load[best] += tasks[i].cost;
     }
     int pos = 0;
-    for (int w = 0; w < kTranslate64Warps; ++w) {
+    for (int w = 0; w < kTranslate64MaxWarps; ++w) {
       begin[w] = pos;
-      for (int i : per[w]) flat[pos++] = tasks[i].d;
+      if (w < warps)
+        for (int i : per[w]) flat[pos++] = tasks[i].d;
     }
-    begin[kTranslate64Warps] = pos;
+    begin[kTranslate64MaxWarps] = pos;
   };
   *out = Translate64Schedule{};
   distribute(rot, out->rot, out->rot_begin);
@@ -536,12 +655,36 @@ void upload_translate64_schedule(int order) {
   HFMM_CUDA_CHECK(cudaMemcpyToSymbol(c_sched64, &sched, sizeof(sched), sizeof(sched) * size_t(order)));
 }
 
-// the 64-pair kernel holds one operand tile per CTA: two CTAs per SM up to P = 12
+// eight warps and two CTAs per SM while two operand tiles fit (P <= 12), sixteen warps and one CTA beyond
+int translate64_warps(int order) {
+  return order <= kTranslate64MaxOrder && 2 * (plan64(order).bytes + 1024) <= size_t(227) * 1024 ? 8 : 16;
+}
+
 bool translate64_supported(int order) {
   const char* e = getenv("HFMM_TRANSLATE");
-  if ((e && !strcmp(e, "32")) || order > kTranslate64MaxOrder) return false;
-  return 2 * (plan64(order).bytes + 1024) <= size_t(227) * 1024;
+  if ((e && !strcmp(e, "32")) || order > kTranslate64TopOrder) return false;
+  if (order > kTranslate64MaxOrder && e && !strcmp(e, "64small")) return false;  // A/B: old kernel beyond P = 12
+  return plan64(order).bytes + 1024 <= size_t(227) * 1024;
 }
+
+// the engine multiplies block m of the coaxial tables by (-1)^m when this kernel consumes them
+bool coax_tables_sign_folded(int order) { return translate64_supported(order); }
+
+namespace {
+template <int PT, int WARPS>
+void launch64(const TranslateArgs& a, cudaStream_t s, size_t bytes, int ctas) {
+  static int configured_for[2] = {-1, -1};
+  const int which = a.staged ? 1 : 0;
+  if (configured_for[which] < int(bytes)) {
+    if (which) HFMM_CUDA_CHECK(cudaFuncSetAttribute(translate64_kernel<PT, WARPS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+    else HFMM_CUDA_CHECK(cudaFuncSetAttribute(translate64_kernel<PT, WARPS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+    configured_for[which] = int(bytes);
+  }
+  if (which) translate64_kernel<PT, WARPS, true><<<ctas, WARPS * 32, bytes, s>>>(a);
+  else translate64_kernel<PT, WARPS, false><<<ctas, WARPS * 32, bytes, s>>>(a);
+  HFMM_CUDA_CHECK(cudaGetLastError());
+}
+}  // namespace
 
 void launch_translate64(const TranslateArgs& a, cudaStream_t s) {
   if (a.n_items == 0) return;
@@ -552,17 +695,20 @@ void launch_translate64(const TranslateArgs& a, cudaStream_t s) {
     HFMM_CUDA_CHECK(cudaGetDevice(&dev));
     HFMM_CUDA_CHECK(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev));
   }
-  static int configured_for[2] = {-1, -1};
-  const int which = a.staged ? 1 : 0;
-  if (configured_for[which] < int(sp.bytes)) {
-    if (which) HFMM_CUDA_CHECK(cudaFuncSetAttribute(translate64_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sp.bytes)));
-    else HFMM_CUDA_CHECK(cudaFuncSetAttribute(translate64_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sp.bytes)));
-    configured_for[which] = int(sp.bytes);
+  const int warps = translate64_warps(a.order);
+  const int ctas = int(std::min<uint32_t>(a.n_items, uint32_t((warps == 8 ? 2 : 1) * sm_count)));
+  static const bool generic = [] {
+    const char* e = getenv("HFMM_TRANSLATE");
+    return e && !strcmp(e, "generic");
+  }();
+  if (warps == 8) {
+    if (!generic && a.order == 12) launch64<12, 8>(a, s, sp.bytes, ctas);
+    else if (!generic && a.order == 10) launch64<10, 8>(a, s, sp.bytes, ctas);
+    else launch64<0, 8>(a, s, sp.bytes, ctas);
+  } else {
+    if (!generic && a.order == 14) launch64<14, 16>(a, s, sp.bytes, ctas);
+    else launch64<0, 16>(a, s, sp.bytes, ctas);
   }
-  const int ctas = int(std::min<uint32_t>(a.n_items, uint32_t(2 * sm_count)));
-  if (which) translate64_kernel<true><<<ctas, kTranslate64Warps * 32, sp.bytes, s>>>(a);
-  else translate64_kernel<false><<<ctas, kTranslate64Warps * 32, sp.bytes, s>>>(a);
-  HFMM_CUDA_CHECK(cudaGetLastError());
 }
 
 }  // namespace hfmm_b200

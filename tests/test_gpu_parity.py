@@ -453,10 +453,11 @@ def test_complex_wavenumber(oracle, k):
         assert rel_l2(y, f.matvec(q)) < 1e-5
 
 
-@pytest.mark.parametrize("order", [0, 1, 3, 7, 12])
+@pytest.mark.parametrize("order", [0, 1, 3, 7, 10, 12, 13, 14, 16])
 def test_64_pair_translation_kernel_against_the_32_pair_kernel(oracle, monkeypatch, order):
-    """orders <= 12 run the 64-pair in-place kernel (kernels_translate64.cu); HFMM_TRANSLATE=32 forces the
-    32-pair ping-pong kernel on the same lists: same operator, two work layouts"""
+    """orders <= 16 run the 64-pair in-place kernel (kernels_translate64.cu: two 8-warp CTAs per SM up to
+    P = 12, one 16-warp CTA with pair-split tasks beyond; P = 10, 12, 14 are compile-time specialisations);
+    HFMM_TRANSLATE=32 forces the 32-pair ping-pong kernel on the same lists: same operator, two work layouts"""
     n, k = 12000, 5.0
     xyz, q = plummer_points(n, 43), charges(n, 43)
     res = {}
