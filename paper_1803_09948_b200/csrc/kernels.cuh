@@ -149,6 +149,7 @@ struct TranslateArgs {
   int stride;
   int mixed;                 // batches mix classes of a table group (per-pair phases) / one class per batch
   int staged;                // every pair owns its dst row (deterministic mode): plain stores instead of atomics
+  int prefetch = 0;          // 64-pair kernel: prefetch the next batch's source rows into L2
 };
 void launch_translate(const TranslateArgs& a, cudaStream_t s);
 // pairs per work item expected by the kernel

@@ -324,7 +324,7 @@ __device__ __forceinline__ void unfold_finish(const FoldUnit& f) {
 // WARPS: 8 (two CTAs per SM, P <= 12) or 16 (one CTA per SM, P <= 16; large systems split by pair halves)
 // STAGED: every pair owns its destination row (deterministic mode): plain stores instead of RED
 template <int PT, int WARPS, bool STAGED>
-__global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? 2 : 1) translate64_kernel(const TranslateArgs a) {
+__global__ void __launch_bounds__(WARPS * 32) __maxnreg__(WARPS == 8 ? 112 : 128) translate64_kernel(const TranslateArgs a) {
   constexpr int kThreads = WARPS * 32, kPairsPerWarp = kBatch64 / WARPS;
   constexpr int RMAX = PT ? PT + 1 : (WARPS == 8 ? kTranslate64MaxOrder + 1 : kTranslate64TopOrder + 1);
   constexpr bool kSplit = WARPS == 16;
@@ -457,6 +457,35 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? 2 : 1) translate64_ke
     }
   };
 
+  // two adjacent columns at once: twice the loads in flight before the first reduction leaves
+  auto scatter_two = [&](uint32_t col, uint32_t drow_a, uint32_t drow_b) {
+    if constexpr (PT != 0) {
+      float2* da = a.dst + size_t(drow_a) * a.stride + lane;
+      float2* db = a.dst + size_t(drow_b) * a.stride + lane;
+      u64 va[kRoundsT], vb[kRoundsT];
+#pragma unroll
+      for (int r = 0; r < kRoundsT; ++r)
+        if (32 * r + 32 <= (PT + 1) * (PT + 1) || 32 * r + lane < (PT + 1) * (PT + 1)) {
+          va[r] = lds1(col + 32u * r * kPitchB);
+          vb[r] = lds1(col + 32u * r * kPitchB + 8u);
+        }
+#pragma unroll
+      for (int r = 0; r < kRoundsT; ++r)
+        if (32 * r + 32 <= (PT + 1) * (PT + 1) || 32 * r + lane < (PT + 1) * (PT + 1)) {
+          if (STAGED) {
+            da[32 * r] = unpack2(va[r]);
+            db[32 * r] = unpack2(vb[r]);
+          } else {
+            atomicAdd(da + 32 * r, unpack2(va[r]));
+            atomicAdd(db + 32 * r, unpack2(vb[r]));
+          }
+        }
+    } else {
+      scatter_pair(col, drow_a);
+      scatter_pair(col + 8u, drow_b);
+    }
+  };
+
   // fold and unfold, in place, all 64 pairs of a unit per warp step (a lane owns the pairs l and l + 32 as
   // in the compute stages); a warp walks a contiguous chunk of the m-major unit list two units at a time
   const uint32_t ph_duo = ph_base + 8u * uint32_t(lane);
@@ -534,7 +563,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? 2 : 1) translate64_ke
     __syncthreads();
     run_coax();  // coaxial translation, in place
     __syncthreads();
-    if (has_next) prefetch_rows(mb_next, next.count);  // stage A is visible to every warp since the last barrier
+    if (has_next && a.prefetch) prefetch_rows(mb_next, next.count);  // stage A is visible to every warp since the last barrier
     run_rot();  // inverse rotation, in place (same table; signs in the coaxial table and the unfold)
     asm volatile("cp.async.wait_all;" ::: "memory");  // own stage-B copies
     __syncthreads();
@@ -547,13 +576,30 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? 2 : 1) translate64_ke
     fold_or_unfold([](const FoldUnit& f) { unfold_finish(f); });
     __syncthreads();
     // scatter, then this warp's columns of the next batch: a warp reads and rewrites only its own
-    // tile columns and phase columns, so no CTA barrier separates the two
+    // tile columns and phase columns, so no CTA barrier separates the two.  The rows of all the warp's
+    // pairs are read first (16-byte loads), then two pairs move at a time.
+    {
+      uint32_t drow[kPairsPerWarp], srow[kPairsPerWarp];
 #pragma unroll
-    for (int pp = 0; pp < kPairsPerWarp; ++pp) {
-      const uint32_t p = uint32_t(warp * kPairsPerWarp + pp);
-      const uint32_t col = tile + 8u * p + kPitchB * uint32_t(lane);
-      if (p < item.count) scatter_pair(col, lds32(mb_cur + kMetaDst + 4u * p));
-      if (has_next && p < next.count) gather_pair(col, lds32(mb_next + kMetaSrc + 4u * p));
+      for (int v = 0; v < kPairsPerWarp / 4; ++v) {
+        const float4 d4 = lds4(mb_cur + kMetaDst + 4u * uint32_t(warp * kPairsPerWarp + 4 * v));
+        const float4 s4 = lds4(mb_next + kMetaSrc + 4u * uint32_t(warp * kPairsPerWarp + 4 * v));
+        drow[4 * v] = __float_as_uint(d4.x); drow[4 * v + 1] = __float_as_uint(d4.y);
+        drow[4 * v + 2] = __float_as_uint(d4.z); drow[4 * v + 3] = __float_as_uint(d4.w);
+        srow[4 * v] = __float_as_uint(s4.x); srow[4 * v + 1] = __float_as_uint(s4.y);
+        srow[4 * v + 2] = __float_as_uint(s4.z); srow[4 * v + 3] = __float_as_uint(s4.w);
+      }
+      const uint32_t col0 = tile + 8u * uint32_t(warp * kPairsPerWarp) + kPitchB * uint32_t(lane);
+      const uint32_t live = item.count - min(item.count, uint32_t(warp * kPairsPerWarp));  // pairs of this warp in the batch
+#pragma unroll
+      for (int pp = 0; pp < kPairsPerWarp; pp += 2) {
+        if (uint32_t(pp + 1) < live) scatter_two(col0 + 8u * pp, drow[pp], drow[pp + 1]);
+        else if (uint32_t(pp) < live) scatter_pair(col0 + 8u * pp, drow[pp]);
+        if (has_next) {  // idle columns of a partial batch re-read the batch's last pair: finite, never scattered
+          gather_pair(col0 + 8u * pp, srow[pp]);
+          gather_pair(col0 + 8u * pp + 8u, srow[pp + 1]);
+        }
+      }
     }
     cp_commit();
     if (has_next) write_phases(mb_next);
@@ -686,9 +732,15 @@ void launch64(const TranslateArgs& a, cudaStream_t s, size_t bytes, int ctas) {
 }
 }  // namespace
 
-void launch_translate64(const TranslateArgs& a, cudaStream_t s) {
-  if (a.n_items == 0) return;
-  const Plan64 sp = plan64(a.order);
+void launch_translate64(const TranslateArgs& a_in, cudaStream_t s) {
+  if (a_in.n_items == 0) return;
+  const Plan64 sp = plan64(a_in.order);
+  static const int prefetch = [] {
+    const char* e = getenv("HFMM_T64_PREFETCH");
+    return e ? atoi(e) : 1;
+  }();
+  TranslateArgs a = a_in;
+  a.prefetch = prefetch;
   static int sm_count = 0;
   if (!sm_count) {
     int dev = 0;
@@ -697,6 +749,7 @@ void launch_translate64(const TranslateArgs& a, cudaStream_t s) {
   }
   const int warps = translate64_warps(a.order);
   const int ctas = int(std::min<uint32_t>(a.n_items, uint32_t((warps == 8 ? 2 : 1) * sm_count)));
+
   static const bool generic = [] {
     const char* e = getenv("HFMM_TRANSLATE");
     return e && !strcmp(e, "generic");
