@@ -618,6 +618,8 @@ void Engine::upload_cell_geometry(std::vector<int4>& geom) {
   double max_leaf_side = 0;
   for (uint32_t c : t.leaves) max_leaf_side = std::max(max_leaf_side, t.side(t.level[c]));
   grid_ = std::ldexp(1.0, int(std::ceil(std::log2(4.0 * k * max_leaf_side))) - 23);
+  // k rho <= sqrt(3)/2 k side for every body of every leaf: inside the 7-term range of the scaled series?
+  leaf_small_args_ = 0.8661 * k * max_leaf_side <= 0.999;
   cell_geom_.upload(geom, stream_);
   cell_body_.upload(cbody, stream_);
   level_scale_.upload(level_scale_host_, stream_);
@@ -1064,6 +1066,7 @@ void Engine::phase_upward() {
     la.stride = stride_;
     la.k = float(cfg_.wave_r);
     la.k_imag = float(cfg_.wave_i);
+    la.small_arguments = leaf_small_args_;
     la.leaves = p2m_leaves_.get();
     la.n_leaves = n_p2m_leaves_;
     HFMM_CUDA_CHECK(cudaEventRecord(ev_[2], stream_));
@@ -1124,6 +1127,7 @@ void Engine::phase_downward() {
     la.stride = stride_;
     la.k = float(cfg_.wave_r);
     la.k_imag = float(cfg_.wave_i);
+    la.small_arguments = leaf_small_args_;
     HFMM_CUDA_CHECK(cudaEventRecord(ev_[12], stream_));
     if (p2p_late_) HFMM_CUDA_CHECK(cudaStreamWaitEvent(stream_near_, ev_[12], 0));
     run_stage(m2l_, multipole_.get(), local_.get());

@@ -185,6 +185,7 @@ class Engine {
   DeviceBuffer<float2> ordered_staging_;  // HFMM_FLAG_DETERMINISTIC: one row per pair of the largest range
   DeviceBuffer<uint32_t> p2m_leaves_, l2p_leaves_;
   uint32_t n_p2m_leaves_ = 0, n_l2p_leaves_ = 0;
+  bool leaf_small_args_ = false;  // every leaf body has k rho <= 1: the unrolled P2M / L2P kernels apply
   DeviceBuffer<float> rot_tables_, coax_tables_;
   TranslateStage m2l_;
   std::vector<TranslateStage> m2m_;  // deepest level first

@@ -80,6 +80,7 @@ struct LeafExpansionArgs {
   int stride;                // coefficient row stride (complex elements)
   float k;                   // Re k
   float k_imag;              // Im k (attenuation); 0 selects the real-argument kernels
+  bool small_arguments = false;  // every body of every listed leaf has k rho <= 1 (7-term series): unrolled kernels
 };
 void launch_p2m(const LeafExpansionArgs& a, const float2* body_q, float2* multipole, cudaStream_t s);
 // out[slot] = sum over the leaf's local expansion (overwrites; bodies of unlisted leaves untouched)
