@@ -323,6 +323,12 @@ int hfmm_cuda_dist_matvec(hfmm_cuda_t* h, const void* q_owned_dev, void* out_own
 int hfmm_cuda_dist_solve(hfmm_cuda_t* h, const double* rhs_owned, double* x_owned, const hfmm_gmres_config* cfg,
                          hfmm_gmres_report* report, double* residuals, int residual_cap);
 /* bytes this rank RECEIVES per matvec in the two exchanges (halo charges, remote multipoles) */
+/* The residual vector b - Z u behind `final_residual` of the last hfmm_cuda_gmres / hfmm_cuda_dist_solve
+ * (all unknowns in caller order, or the owned Morton slice): `capacity` interleaved complex doubles, FP32
+ * values widened.  With max_iterations = restart a caller drives the restart cycles itself — solve
+ * Z d = r, x += d, r <- this vector — and may re-cut the Morton partition between two cycles, which is
+ * where the reference's repartitioning loop acts (partition.cpp:143-227; distributed.repartitioned_gmres). */
+int hfmm_cuda_get_solve_residual(hfmm_cuda_t* h, double* out, size_t capacity);
 int hfmm_cuda_get_exchange_volume(hfmm_cuda_t* h, uint64_t* charge_bytes, uint64_t* multipole_bytes);
 
 const char* hfmm_cuda_version(void);

@@ -162,6 +162,7 @@ class HfmmCuda:
             raise HfmmError(rc, self.lib.hfmm_cuda_last_error(None).decode())
         self.order = order
         self.n = 0
+        self.partitioned = False
 
     def _check(self, rc):
         if rc:
@@ -197,6 +198,7 @@ class HfmmCuda:
     # ---- multi-GPU (Morton partition; see paper_1803_09948_b200/distributed.py)
     def set_partition(self, rank: int, nranks: int):
         self._check(self.lib.hfmm_cuda_set_partition(self.h, int(rank), int(nranks)))
+        self.partitioned = True
 
     def set_partition_alpha(self, alpha: float):
         """Morton cuts balanced by the reference's w = l + alpha r (alpha < 0: default cost model)"""
@@ -417,6 +419,14 @@ class HfmmCuda:
         self._raise_transport_failure()
         self._check(rc)
         return x, self._report(rep, res, sec, mv)
+
+    def solve_residual(self):
+        """b - Z u of the last gmres / dist_solve (complex128; all unknowns or the owned Morton slice)"""
+        n = int(self.partition().body_count) if self.partitioned else self.n
+        out = np.zeros(n, dtype=np.complex128)
+        self.lib.hfmm_cuda_get_solve_residual.argtypes = [C.c_void_p, _dp, C.c_size_t]
+        self._check(self.lib.hfmm_cuda_get_solve_residual(self.h, out.ctypes.data_as(_dp) if n else None, n))
+        return out
 
     def build_corrections(self, patches, tables, mode=2, near_patch_distance=-1.0, fetch=True):
         """Correction arrays built on the device from the patches and the reference's rule tables

@@ -309,6 +309,14 @@ int hfmm_cuda_dist_solve(hfmm_cuda_t* h, const double* rhs_owned, double* x_owne
   });
 }
 
+int hfmm_cuda_get_solve_residual(hfmm_cuda_t* h, double* out, size_t capacity) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] {
+    if (!out && capacity) throw Error(HFMM_ERR_CONFIG, "null argument");
+    h->engine->get_solve_residual(out, capacity);
+  });
+}
+
 int hfmm_cuda_get_exchange_volume(hfmm_cuda_t* h, uint64_t* charge_bytes, uint64_t* multipole_bytes) {
   if (int rc = need(h)) return rc;
   return guarded(h, [&] {

@@ -89,6 +89,8 @@ class Engine {
   void comm_init_host(const hfmm_host_transport& cb);
   const char* comm_name() const;
   void get_exchange_volume(uint64_t* charge_bytes, uint64_t* multipole_bytes);
+  // b - Z u of the last gmres / dist_solve (the vector behind final_residual), owned slice, FP32 widened
+  void get_solve_residual(double* out, size_t capacity);
   void dist_matvec(const void* q_owned_dev, void* out_owned_dev);
   void dist_solve(const double* rhs_owned, double* x_owned, const hfmm_gmres_config& cfg,
                   hfmm_gmres_report* rep, double* residuals, int residual_cap);
@@ -208,6 +210,8 @@ class Engine {
   // vectors
   DeviceBuffer<float2> body_q_, near_, far_;
   DeviceBuffer<double2> io64_;
+  DeviceBuffer<float2> solve_residual_;  // residual vector of the last solve (restart cycles driven by the caller)
+  uint32_t solve_residual_n_ = 0;
 };
 
 // FP64 composition of the factored operator into a dense (P+1)^2 x (P+1)^2 matrix in the

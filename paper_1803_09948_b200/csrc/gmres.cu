@@ -340,6 +340,10 @@ void Engine::gmres_impl(bool sharded, const double* rhs, double* x_out, const hf
   launch_residual(n, b64.get(), w.get(), r32.get(), scal.get(), red.get(), stream_);
   allreduce(scal.get(), 2);
   scal.download(hscal.data(), 2, stream_);
+  // kept for callers that drive the restart cycles themselves (repartitioning between cycles, partition.cpp:143-227)
+  if (solve_residual_.size() < ld) solve_residual_.resize(ld);
+  if (n) HFMM_CUDA_CHECK(cudaMemcpyAsync(solve_residual_.get(), r32.get(), size_t(n) * sizeof(float2), cudaMemcpyDeviceToDevice, stream_));
+  solve_residual_n_ = n;
   // the returned iterate maps back through M^-1 (solver.cpp:388)
   if (precond) {
     if (!sharded) {
@@ -364,6 +368,17 @@ void Engine::gmres_impl(bool sharded, const double* rhs, double* x_out, const hf
   rep->converged = (rep->final_residual <= cfg.rtol || (nres > 0 && last_est / bnorm <= cfg.rtol)) ? 1 : 0;
   rep->seconds = std::chrono::duration<double>(clk::now() - t_start).count();
   rep->matvec_seconds = matvec_s;
+}
+
+void Engine::get_solve_residual(double* out, size_t capacity) {
+  HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  if (capacity < solve_residual_n_) throw Error(HFMM_ERR_CONFIG, "residual buffer too small");
+  const uint32_t n = solve_residual_n_;
+  if (!n) return;
+  if (io64_.size() < n) io64_.resize(n);
+  launch_widen(n, solve_residual_.get(), io64_.get(), stream_);
+  HFMM_CUDA_CHECK(cudaMemcpyAsync(out, io64_.get(), size_t(n) * sizeof(double2), cudaMemcpyDeviceToHost, stream_));
+  HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
 }
 
 void Engine::set_patch_diameters(const double* diameter, size_t n_patches) {

@@ -255,6 +255,50 @@ class Repartitioner:
         return True
 
 
+def repartitioned_gmres_emulated(make_ops, rhs_morton, rtol=1e-4, restart=30, max_iterations=500,
+                                 precondition=True, alpha_max: float = 2.0, timeout=180.0):
+    """GMRES(restart) over Morton-sharded vectors with the reference's repartitioning loop acting at the restart
+    boundaries (partition.cpp:143-227), ranks emulated on ONE GPU.
+
+    make_ops(alpha) -> the handles of all ranks, partitioned with w = l + alpha r (set_partition +
+    set_partition_alpha before set_points).  Every restart cycle is one hfmm_cuda_dist_solve of the residual
+    equation Z d = r with max_iterations = restart (x += d, r <- hfmm_cuda_get_solve_residual): the same
+    iteration as the monolithic restarted solver — the absolute target rtol ||b|| is kept by rescaling rtol —
+    but the handles may change between two cycles.  A cycle's matvec time per iteration (max over ranks) is
+    what update_alpha sees; when it moves alpha the Morton cuts are redrawn (make_ops) and iterate and residual,
+    held in global Morton order here, are simply sliced again.  Returns (x_morton, report)."""
+    rp = Repartitioner(make_ops, alpha_max)
+    rhs = np.asarray(rhs_morton, dtype=np.complex128)
+    bnorm = float(np.linalg.norm(rhs))
+    x, r = np.zeros_like(rhs), rhs.copy()
+    rep = {"iterations": 0, "converged": bnorm == 0.0, "residuals": [], "alphas": [], "cuts": [], "recuts": 0,
+           "final_residual": 0.0 if bnorm == 0.0 else 1.0}
+    target = rtol * bnorm
+    while not rep["converged"] and rep["iterations"] < max_iterations:
+        ops = rp.operator
+        parts = [op.partition() for op in ops]
+        rep["alphas"].append(rp.alpha)
+        rep["cuts"].append([int(p.body_first) for p in parts])
+        rnorm = float(np.linalg.norm(r))
+        res = emulate_gmres_on_one_device(ops, r, timeout, rtol=min(target / rnorm, 0.999999), restart=restart,
+                                          max_iterations=min(restart, max_iterations - rep["iterations"]),
+                                          precondition=precondition)
+        x += np.concatenate([d for d, _ in res])
+        r = np.concatenate([op.solve_residual() for op in ops])
+        r0 = res[0][1]
+        assert len({q["iterations"] for _, q in res}) == 1, "ranks left lock step"
+        rep["iterations"] += int(r0["iterations"])
+        rep["residuals"] += [float(v) * rnorm / bnorm for v in r0["residuals"]]
+        rep["final_residual"] = float(np.linalg.norm(r)) / bnorm
+        if rep["final_residual"] <= rtol or (rep["residuals"] and rep["residuals"][-1] <= rtol) or r0["breakdown"]:
+            rep["converged"] = rep["final_residual"] <= rtol or rep["residuals"][-1] <= rtol
+            break
+        per_it = max(float(q["matvec_seconds"]) for _, q in res) / max(int(r0["iterations"]), 1)
+        if rp.record(per_it):
+            rep["recuts"] += 1
+    return x, rep
+
+
 def emulate_ranks_on_one_device(ops, q_morton, pruned: bool = False):
     """Runs the sharded matvec of `len(ops)` ranks sequentially on ONE GPU (each op was created with
     set_partition(r, R) on the same global point set), replacing the two all-gathers by device

@@ -532,3 +532,90 @@ def test_deterministic_gmres_history_is_bitwise_reproducible():
     assert runs[0][2] == runs[1][2]
     assert np.array_equal(runs[0][1], runs[1][1])
     assert np.array_equal(runs[0][0], runs[1][0])
+
+
+def test_repartitioning_loop_converges_on_a_clustered_set():
+    """SURVEY.md section 8 row f3 end to end (partition.cpp:143-227): the loop measure -> update_alpha ->
+    re-cut (distributed.Repartitioner) on a Plummer set with four emulated ranks.  The "runtime" fed to
+    update_alpha is the slowest rank's modelled work (owned near body pairs + 1600 x owned M2L pairs, the
+    measured kernel-time ratio), which makes the run deterministic.  The golden-section search must stay in
+    [0, alpha_max] and settle, every partition it visits must reproduce the single-domain matvec, and the
+    partition it settles on must not be worse than the one it started from."""
+    import torch
+
+    from paper_1803_09948_b200.distributed import Repartitioner, emulate_matvec_on_one_device
+    from paper_1803_09948_b200.workloads import plummer_points
+
+    n, k, order, ranks = 40000, 6.0, 6, 4
+    xyz, q = plummer_points(n, 21), charges(n, 21)
+    single = HfmmCuda(k=k, order=order, ncrit=32, theta=0.4)
+    single.set_points(xyz)
+    y1, order_m = single.matvec(q), single.body_order()
+    qm = q[order_m]
+    qd = torch.from_numpy(np.stack([qm.real, qm.imag], 1).astype(np.float32)).cuda()
+
+    def make_ops(alpha):
+        ops = []
+        for rank in range(ranks):
+            op = HfmmCuda(k=k, order=order, ncrit=32, theta=0.4)
+            op.set_partition(rank, ranks)
+            op.set_partition_alpha(alpha)
+            op.set_points(xyz)
+            ops.append(op)
+        return ops
+
+    def slowest(ops):
+        return max(int(op.partition().owned_p2p_body_pairs) + 1600 * int(op.partition().owned_m2l_pairs) for op in ops)
+
+    rp = Repartitioner(make_ops, alpha_max=2.0)
+    visited, work = [], []
+    for _ in range(12):
+        ops = rp.operator
+        y = emulate_matvec_on_one_device(ops, qd).cpu().numpy()
+        assert rel_l2(y[:, 0] + 1j * y[:, 1], y1[order_m]) < 3e-6
+        visited.append(rp.alpha)
+        work.append(slowest(ops))
+        if not rp.record(work[-1]):
+            break
+    assert all(0.0 <= a <= 2.0 for a in visited)
+    assert len(visited) >= 4                                   # it searched
+    assert abs(visited[-1] - visited[-2]) < abs(visited[1] - visited[0])   # and the bracket shrank
+    assert work[-1] <= 1.02 * min(work)                       # it sits at (or next to) the best partition it saw
+
+
+def test_gmres_with_repartitioning_between_restart_cycles():
+    """f3 inside the solver: restart cycles driven by the caller (hfmm_cuda_dist_solve with max_iterations =
+    restart on the residual equation, hfmm_cuda_get_solve_residual), the Morton partition re-cut by the
+    repartitioning loop at every restart boundary.  Same iteration as the monolithic restarted solver: same
+    count +-1, same solution."""
+    from paper_1803_09948_b200.distributed import repartitioned_gmres_emulated
+
+    single = _bie_operator(G)
+    order = single.body_order()
+    rhs = np.asarray(G["bie_rhs"])
+
+    def make_ops(alpha):
+        ops = []
+        for r in range(2):
+            op = HfmmCuda(k=float(G["bie_k"]), order=int(G["bie_order"]), ncrit=16, theta=0.4, kd_max=1.0, leaf_cap=-1.0)
+            op.set_partition(r, 2)
+            op.set_partition_alpha(alpha)
+            op.set_points(G["bie_xyz"])
+            op.set_corrections(int(G["bie_ni"]), far_weight=G["bie_far_weight"], patch_block=G["bie_patch_block"],
+                               near_offset=G["bie_near_offset"], near_source=G["bie_near_source"],
+                               near_delta=G["bie_near_delta"], block_lu=G["bie_block_lu"], block_piv=G["bie_block_piv"])
+            ops.append(op)
+        return ops
+
+    for precondition in (True, False):
+        x1, rep1 = single.gmres(rhs, rtol=1e-4, restart=6, max_iterations=300, precondition=precondition)
+        assert rep1["converged"] and rep1["iterations"] > 12          # several restart cycles
+        x, rep = repartitioned_gmres_emulated(make_ops, rhs[order], rtol=1e-4, restart=6, max_iterations=300,
+                                              precondition=precondition)
+        assert rep["converged"] and rep["final_residual"] <= 1.05e-4
+        assert abs(rep["iterations"] - rep1["iterations"]) <= 1, (rep["iterations"], rep1["iterations"])
+        assert rep["recuts"] >= 2 and len(set(rep["alphas"])) >= 3   # the loop moved alpha between cycles
+        assert rel_l2(x, x1[order]) < 2e-3
+        # the single-domain solver exposes the same vector: b - Z u of the last solve
+        r1 = single.solve_residual()
+        assert abs(np.linalg.norm(r1) / np.linalg.norm(rhs) - rep1["final_residual"]) < 1e-6
