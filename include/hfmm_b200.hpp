@@ -165,6 +165,18 @@ inline FmmStats execute_plan(DeviceTree& tree, const std::vector<cplx>& src, std
   return tree.stats();
 }
 
+// execute_plan with distinct target and source trees (traversal.hpp:59-62): potentials of the tree's points,
+// carrying src, at `targets`
+inline std::vector<cplx> execute_plan(DeviceTree& source_tree, const std::vector<cplx>& src,
+                                      const std::vector<Vec3>& targets) {
+  if (src.size() != source_tree.size()) throw config_error("execute_plan: source vector length mismatch");
+  std::vector<cplx> trg(targets.size());
+  source_tree.check(hfmm_cuda_evaluate_targets(source_tree.handle(), reinterpret_cast<const double*>(targets.data()),
+                                               targets.size(), reinterpret_cast<const double*>(src.data()),
+                                               reinterpret_cast<double*>(trg.data())));
+  return trg;
+}
+
 // fmm_evaluate (traversal.hpp:65-67): traversal + execution in one call over Body records
 inline FmmStats fmm_evaluate(std::vector<Body>& bodies, WaveNumber k, int order,
                              const TraversalConfig& cfg, double max_leaf_diameter = 0) {

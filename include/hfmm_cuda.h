@@ -323,6 +323,13 @@ int hfmm_cuda_dist_matvec(hfmm_cuda_t* h, const void* q_owned_dev, void* out_own
 int hfmm_cuda_dist_solve(hfmm_cuda_t* h, const double* rhs_owned, double* x_owned, const hfmm_gmres_config* cfg,
                          hfmm_gmres_report* report, double* residuals, int residual_cap);
 /* bytes this rank RECEIVES per matvec in the two exchanges (halo charges, remote multipoles) */
+/* fmm_evaluate / execute_plan with DISTINCT target and source trees (traversal.hpp:59-67): out[t] = sum_j q_j
+ * G(targets[t], x_j) over the handle's points x_j (strengths q, caller order, interleaved complex doubles) at
+ * n_targets other points (3 doubles each); out: n_targets interleaved complex doubles.  A target that coincides
+ * with a source skips that pair, as green_t does (kernel.hpp:22).  Runs the ordinary pipeline on one tree over
+ * sources + targets held by a second engine inside the handle, rebuilt only when the targets change; single-domain
+ * handles only.  Corrections and far weights of the handle are NOT applied (plain layer potential). */
+int hfmm_cuda_evaluate_targets(hfmm_cuda_t* h, const double* targets, size_t n_targets, const double* q, double* out);
 /* The residual vector b - Z u behind `final_residual` of the last hfmm_cuda_gmres / hfmm_cuda_dist_solve
  * (all unknowns in caller order, or the owned Morton slice): `capacity` interleaved complex doubles, FP32
  * values widened.  With max_iterations = restart a caller drives the restart cycles itself — solve

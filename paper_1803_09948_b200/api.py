@@ -420,6 +420,19 @@ class HfmmCuda:
         self._check(rc)
         return x, self._report(rep, res, sec, mv)
 
+    def evaluate_targets(self, targets, q):
+        """potentials of the operator's points (strengths q) at other points: fmm_evaluate with distinct
+        target and source trees (traversal.hpp:59-67)"""
+        t = np.ascontiguousarray(targets, dtype=np.float64)
+        q = _c128(q)
+        if t.ndim != 2 or t.shape[1] != 3 or q.shape != (self.n,):
+            raise ValueError("targets must be (m, 3), q must hold one strength per source")
+        out = np.zeros(t.shape[0], dtype=np.complex128)
+        self.lib.hfmm_cuda_evaluate_targets.argtypes = [C.c_void_p, _dp, C.c_size_t, _dp, _dp]
+        self._check(self.lib.hfmm_cuda_evaluate_targets(self.h, t.ctypes.data_as(_dp), t.shape[0],
+                                                        q.ctypes.data_as(_dp), out.ctypes.data_as(_dp)))
+        return out
+
     def solve_residual(self):
         """b - Z u of the last gmres / dist_solve (complex128; all unknowns or the owned Morton slice)"""
         n = int(self.partition().body_count) if self.partitioned else self.n

@@ -309,6 +309,11 @@ int hfmm_cuda_dist_solve(hfmm_cuda_t* h, const double* rhs_owned, double* x_owne
   });
 }
 
+int hfmm_cuda_evaluate_targets(hfmm_cuda_t* h, const double* targets, size_t n_targets, const double* q, double* out) {
+  if (int rc = need(h)) return rc;
+  return guarded(h, [&] { h->engine->evaluate_targets(targets, n_targets, q, out); });
+}
+
 int hfmm_cuda_get_solve_residual(hfmm_cuda_t* h, double* out, size_t capacity) {
   if (int rc = need(h)) return rc;
   return guarded(h, [&] {

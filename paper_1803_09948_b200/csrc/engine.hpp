@@ -89,6 +89,9 @@ class Engine {
   void comm_init_host(const hfmm_host_transport& cb);
   const char* comm_name() const;
   void get_exchange_volume(uint64_t* charge_bytes, uint64_t* multipole_bytes);
+  // potentials at `nt` points that are not sources (fmm_evaluate with distinct target and source trees,
+  // traversal.hpp:59-67): one tree over sources + targets, targets carry zero charge
+  void evaluate_targets(const double* targets, size_t nt, const double* q, double* out);
   // b - Z u of the last gmres / dist_solve (the vector behind final_residual), owned slice, FP32 widened
   void get_solve_residual(double* out, size_t capacity);
   void dist_matvec(const void* q_owned_dev, void* out_owned_dev);
@@ -210,6 +213,9 @@ class Engine {
   // vectors
   DeviceBuffer<float2> body_q_, near_, far_;
   DeviceBuffer<double2> io64_;
+  std::unique_ptr<Engine> target_engine_;  // sources + targets of the last evaluate_targets (rebuilt when they change)
+  uint64_t target_hash_ = 0;
+  size_t target_count_ = 0;
   DeviceBuffer<float2> solve_residual_;  // residual vector of the last solve (restart cycles driven by the caller)
   uint32_t solve_residual_n_ = 0;
 };

@@ -370,6 +370,43 @@ void Engine::gmres_impl(bool sharded, const double* rhs, double* x_out, const hf
   rep->matvec_seconds = matvec_s;
 }
 
+// fmm_evaluate(target_tree, source_tree) with targets != sources (traversal.hpp:59-67, traversal.cpp:281-287):
+// the potentials of the handle's points, carrying the strengths q, at `nt` other points.  One tree over the
+// union (the targets carry zero charge) runs the ordinary pipeline on a second engine; the interaction lists are
+// those of the union set, not of the reference's two-tree descent, the potentials agree to the FMM's tolerance.
+// The union tree is kept until the targets change (FNV-1a of their coordinates).
+void Engine::evaluate_targets(const double* targets, size_t nt, const double* q, double* out) {
+  require_points();
+  HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
+  if (nranks_ > 1) throw Error(HFMM_ERR_CONFIG, "evaluate_targets needs a single-domain handle");
+  if (!nt) return;
+  if (!targets || !q || !out) throw Error(HFMM_ERR_CONFIG, "null argument");
+  const size_t n = tree_.n_bodies;
+  uint64_t hash = 1469598103934665603ull;
+  const unsigned char* bytes = reinterpret_cast<const unsigned char*>(targets);
+  for (size_t i = 0; i < nt * 3 * sizeof(double); ++i) hash = (hash ^ bytes[i]) * 1099511628211ull;
+  if (!target_engine_ || target_hash_ != hash || target_count_ != nt) {
+    std::vector<double> all(3 * (n + nt));
+    xyz64_.download(all.data(), 3 * n, stream_);
+    HFMM_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    std::copy(targets, targets + 3 * nt, all.begin() + 3 * n);
+    hfmm_cuda_config c = cfg_;
+    target_engine_.reset();
+    target_engine_ = std::make_unique<Engine>(c);
+    AllocStreamScope scope(target_engine_->stream(), cfg_.device);
+    target_engine_->set_points(all.data(), n + nt);
+    target_hash_ = hash;
+    target_count_ = nt;
+  }
+  std::vector<double> qq(2 * (n + nt), 0.0), res(2 * (n + nt));
+  std::copy(q, q + 2 * n, qq.begin());
+  {
+    AllocStreamScope scope(target_engine_->stream(), cfg_.device);
+    target_engine_->matvec_host(qq.data(), res.data());
+  }
+  std::copy(res.begin() + 2 * n, res.end(), out);
+}
+
 void Engine::get_solve_residual(double* out, size_t capacity) {
   HFMM_CUDA_CHECK(cudaSetDevice(cfg_.device));
   if (capacity < solve_residual_n_) throw Error(HFMM_ERR_CONFIG, "residual buffer too small");

@@ -629,3 +629,27 @@ def test_partition_of_a_clustered_set_without_leaf_cap():
                 assert mine[0] == p.cell_first[L] and len(mine) == p.cell_count[L]
                 assert np.array_equal(mine, np.arange(mine[0], mine[0] + len(mine)))
     assert total == n
+
+
+def test_distinct_targets_and_sources(oracle):
+    """execute_plan / fmm_evaluate with a target tree that is not the source tree (traversal.hpp:59-67):
+    potentials of the sources at other points — outside the surface, inside it, one ON a source (that pair is
+    skipped, kernel.hpp:22) — against the FP64 direct sum; the union tree is reused until the targets change"""
+    n, m, k, order = 30000, 5000, 5.0, 10
+    xyz, q = sphere_points(n, 31), charges(n, 31)
+    rng = np.random.default_rng(32)
+    tg = rng.uniform(-1.6, 1.6, size=(m, 3))
+    tg[7] = xyz[123]
+    op = HfmmCuda(k=k, order=order, ncrit=64)
+    op.set_points(xyz)
+    y_self = op.matvec(q)
+    y = op.evaluate_targets(tg, q)
+    exact = oracle.direct_sum(np.vstack([xyz, tg]), np.concatenate([q, np.zeros(m)]), k, targets=np.arange(n, n + m))
+    assert rel_l2(y, exact) < 1e-5
+    assert abs(y[7] - y_self[123]) < 1e-5 * abs(y_self[123])          # the coincident pair contributes nothing
+    t_first = op.evaluate_targets(tg, 2 * q)                          # same targets: the tree is kept, linear in q
+    assert rel_l2(t_first, 2 * y) < 1e-6
+    assert rel_l2(op.evaluate_targets(tg[:100] + 0.01, q),
+                  oracle.direct_sum(np.vstack([xyz, tg[:100] + 0.01]), np.concatenate([q, np.zeros(100)]), k,
+                                    targets=np.arange(n, n + 100))) < 1e-5
+    assert rel_l2(op.matvec(q), y_self) < 1e-6                         # the handle's own operator is untouched
