@@ -3,8 +3,14 @@
 
   python -m paper_1803_09948_b200 solve   --subdivisions 5 --k 4      sphere scattering, Mie check
   python -m paper_1803_09948_b200 solve   --mesh sphere.msh --k 2      the same on a mesh file (meshio.py)
+  python -m paper_1803_09948_b200 solve   ... --out-prefix run1        + run1.report.json, run1.residuals.csv, run1.field.csv
+  python -m paper_1803_09948_b200 verify  --orders 1 2 --k 2           Mie error per basis order (SPEC cmd_verify)
+  python -m paper_1803_09948_b200 scaling --n 20000 40000 80000        CSV of (N, FMM seconds) + fitted slope (cmd_scaling)
+  python -m paper_1803_09948_b200 convert in.msh out.bin               ASCII mesh -> binary blocks (cmd_convert; no GPU)
+  python -m paper_1803_09948_b200 partition --ranks 8 --config cfg4    Morton partition statistics (host; no GPU)
   python -m paper_1803_09948_b200 matvec  --config cfg2 [--n N]        one BASELINE FMM configuration
   python -m paper_1803_09948_b200 info                                 library version, device probes
+Exit codes follow the SPEC: 0 converged / done, 2 not converged, 64 usage error.
 
 The quadrature tables of the correction builders are the reference's (geometry.cpp); the package ships
 them for basis orders 1 and 2 (data/quadrature_rules.npz, --basis-order), --rules reads other ones from a
@@ -62,7 +68,100 @@ def cmd_solve(a):
            "final_residual": float(rep["final_residual"]), "solve_seconds": t_solve,
            "mie_mismatch_rel_l2": float(np.linalg.norm(scat - mie) / np.linalg.norm(mie))}
     print(json.dumps(out))
+    if a.out_prefix:   # SPEC cmd_solve: report JSON, residual CSV, field CSV
+        out["residuals"] = [float(v) for v in rep["residuals"]]
+        with open(a.out_prefix + ".report.json", "w") as f:
+            json.dump(out, f, indent=1)
+        with open(a.out_prefix + ".residuals.csv", "w") as f:
+            f.write("iteration,relative_residual,seconds,matvec_seconds\n")
+            for i, (r, t, m) in enumerate(zip(rep["residuals"], rep["seconds_history"], rep["matvec_seconds_history"])):
+                f.write(f"{i + 1},{r:.9e},{t:.6e},{m:.6e}\n")
+        with open(a.out_prefix + ".field.csv", "w") as f:
+            f.write("theta,re_scattered,im_scattered,re_mie,im_mie\n")
+            for t, u, v in zip(th, scat, mie):
+                f.write(f"{t:.9f},{u.real:.9e},{u.imag:.9e},{v.real:.9e},{v.imag:.9e}\n")
     return 0 if rep["converged"] else 2
+
+
+def cmd_verify(a):
+    """SPEC cmd_verify: sound-soft sphere against the Mie series, one row per basis order (p-refinement)"""
+    import argparse as _ap
+    if not a.k > 0:
+        print("verify: k must be positive", file=sys.stderr)
+        return 64
+    rows = []
+    for bo in a.orders:
+        sub = _ap.Namespace(**{**vars(a), "basis_order": bo, "rules": None, "mesh": None, "out_prefix": None})
+        import io, contextlib
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            rc = cmd_solve(sub)
+        row = json.loads(buf.getvalue().strip().splitlines()[-1])
+        row["basis_order"], row["exit_code"] = bo, rc
+        rows.append(row)
+    print(json.dumps({"k": a.k, "subdivisions": a.subdivisions, "rows": rows,
+                      "errors_decrease": all(x["mie_mismatch_rel_l2"] > y["mie_mismatch_rel_l2"]
+                                             for x, y in zip(rows, rows[1:]))}))
+    return 0 if all(r["converged"] for r in rows) else 2
+
+
+def cmd_scaling(a):
+    """SPEC cmd_scaling: FMM matvec seconds over a list of N (uniform sphere surface), CSV on stdout; duplicate N
+    are averaged (count column); the log-log slope of the fit goes to stderr as JSON"""
+    from . import HfmmCuda
+    from .workloads import charges, sphere_points
+
+    acc = {}
+    for n in a.n:
+        xyz, q = sphere_points(n, a.seed), charges(n, a.seed)
+        op = HfmmCuda(k=a.k, order=a.order, ncrit=a.ncrit, theta=a.theta, kd_max=1.0, leaf_cap=0.0 if a.no_leaf_cap else -1.0)
+        op.set_points(xyz)
+        op.matvec(q)
+        ts = []
+        for _ in range(a.repeat):
+            op.matvec(q)
+            ts.append(op.stats()["matvec_seconds"])
+        acc.setdefault(n, []).append(float(np.median(ts)))
+        op.close()
+    print("n,fmm_seconds,count")
+    for n in sorted(acc):
+        print(f"{n},{np.mean(acc[n]):.6e},{len(acc[n])}")
+    if len(acc) > 1:
+        ns = np.array(sorted(acc), dtype=float)
+        t = np.array([np.mean(acc[int(v)]) for v in ns])
+        print(json.dumps({"loglog_slope": float(np.polyfit(np.log(ns), np.log(t), 1)[0])}), file=sys.stderr)
+    return 0
+
+
+def cmd_convert(a):
+    """SPEC cmd_convert: ASCII mesh -> the reference's binary block format (mesh-io); no GPU"""
+    from .meshio import MeshError, read_mesh, write_binary
+    try:
+        write_binary(read_mesh(a.mesh), a.out)
+    except (OSError, ValueError, MeshError) as e:
+        print(f"convert: {e}", file=sys.stderr)
+        return 1
+    return 0
+
+
+def cmd_partition(a):
+    """Morton partition of a BASELINE point set over R ranks (host tree, no GPU): bodies, modelled work and
+    the work-balanced cuts (near body pairs + 1600 x M2L pairs) and the bodies each rank then owns — the partition
+    the reference's cmd_partition_sim starts its network simulation from (the simulator itself is out of scope)"""
+    from .api import debug_partition
+    from .workloads import CONFIGS, make_points
+
+    cfg = CONFIGS[a.config]
+    n = a.n or min(cfg.n, 262144)
+    if a.ranks < 1:
+        print("partition: --ranks must be >= 1", file=sys.stderr)
+        return 64
+    first, count, _, lcut = debug_partition(make_points(cfg, n), cfg.ncrit, cfg.resolved_leaf_cap(), cfg.k, cfg.theta,
+                                            cfg.kd_max, a.ranks)
+    print(json.dumps({"config": a.config, "points": n, "ranks": a.ranks, "cut_level": int(lcut),
+                      "body_first": [int(v) for v in first], "bodies": [int(v) for v in count],
+                      "bodies_max_over_mean": float(count.max() / count.mean())}))
+    return 0
 
 
 def cmd_matvec(a):
@@ -142,9 +241,42 @@ def main(argv=None):
     m.add_argument("--deterministic", action="store_true", help="ordered accumulation: bitwise reproducible runs")
     m.add_argument("--check", type=int, default=64)
     m.set_defaults(fn=cmd_matvec)
+    s.add_argument("--out-prefix", default=None, help="also write <prefix>.report.json, .residuals.csv, .field.csv")
+    v = sub.add_parser("verify", help="Mie error of the sphere solve per basis order")
+    for flag, typ, dflt in (("--subdivisions", int, 3), ("--radius", float, 1.0), ("--k", float, 2.0), ("--order", int, 10),
+                            ("--ncrit", int, 64), ("--theta", float, 0.4), ("--kd-max", float, 1.0), ("--rtol", float, 1e-4),
+                            ("--restart", int, 30), ("--max-iterations", int, 1000), ("--observations", int, 37),
+                            ("--obs-radius", float, 4.0)):
+        v.add_argument(flag, type=typ, default=dflt)
+    v.add_argument("--orders", type=int, nargs="+", default=[1, 2], choices=[1, 2])
+    v.add_argument("--block-jacobi", action="store_true")
+    v.add_argument("--deterministic", action="store_true")
+    v.set_defaults(fn=cmd_verify)
+    c = sub.add_parser("scaling", help="FMM seconds over a list of N")
+    c.add_argument("--n", type=int, nargs="+", required=True)
+    c.add_argument("--seed", type=int, default=1)
+    c.add_argument("--k", type=float, default=4.0)
+    c.add_argument("--order", type=int, default=10)
+    c.add_argument("--ncrit", type=int, default=64)
+    c.add_argument("--theta", type=float, default=0.4)
+    c.add_argument("--repeat", type=int, default=5)
+    c.add_argument("--no-leaf-cap", action="store_true", help="leaves bounded by ncrit only (fixed k: the leaf cap fixes the leaf SIZE)")
+    c.set_defaults(fn=cmd_scaling)
+    cv = sub.add_parser("convert", help="ASCII mesh -> binary mesh")
+    cv.add_argument("mesh")
+    cv.add_argument("out")
+    cv.set_defaults(fn=cmd_convert)
+    pt = sub.add_parser("partition", help="Morton partition statistics of a BASELINE point set (host)")
+    pt.add_argument("--config", default="cfg2")
+    pt.add_argument("--n", type=int, default=None)
+    pt.add_argument("--ranks", type=int, default=8)
+    pt.set_defaults(fn=cmd_partition)
     i = sub.add_parser("info", help="library version and device probes")
     i.set_defaults(fn=cmd_info)
-    a = ap.parse_args(argv)
+    try:
+        a = ap.parse_args(argv)
+    except SystemExit as e:      # argparse exits with 2 on a usage error: the SPEC says 64
+        return 64 if e.code not in (0, None) else 0
     return a.fn(a)
 
 

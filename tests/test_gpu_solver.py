@@ -619,3 +619,28 @@ def test_gmres_with_repartitioning_between_restart_cycles():
         # the single-domain solver exposes the same vector: b - Z u of the last solve
         r1 = single.solve_residual()
         assert abs(np.linalg.norm(r1) / np.linalg.norm(rhs) - rep1["final_residual"]) < 1e-6
+
+
+def test_cli_solve_verify_scaling(tmp_path, capsys):
+    """SPEC cmd_solve (report JSON, residual CSV, field CSV; exit 0 on convergence), cmd_verify (Mie error per basis
+    order, decreasing with the order) and cmd_scaling (one CSV row per N, duplicates averaged) through the package's
+    command line"""
+    import json
+
+    from paper_1803_09948_b200.__main__ import main
+
+    prefix = str(tmp_path / "run")
+    assert main(["solve", "--subdivisions", "2", "--k", "2", "--order", "8", "--out-prefix", prefix]) == 0
+    rep = json.load(open(prefix + ".report.json"))
+    assert rep["converged"] and rep["final_residual"] <= 1e-4 and len(rep["residuals"]) == rep["iterations"]
+    assert len(open(prefix + ".residuals.csv").read().splitlines()) == rep["iterations"] + 1
+    assert len(open(prefix + ".field.csv").read().splitlines()) == 37 + 1
+    capsys.readouterr()
+    assert main(["verify", "--subdivisions", "2", "--k", "2", "--order", "8", "--orders", "1", "2"]) == 0
+    out = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    errs = [r["mie_mismatch_rel_l2"] for r in out["rows"]]
+    assert out["errors_decrease"] and errs[1] < errs[0] < 0.3
+    assert main(["verify", "--k", "0"]) == 64                                  # zero frequency is rejected
+    assert main(["scaling", "--n", "20000", "40000", "20000", "--order", "6"]) == 0
+    rows = capsys.readouterr().out.strip().splitlines()
+    assert rows[0] == "n,fmm_seconds,count" and len(rows) == 3 and rows[1].endswith(",2") and rows[2].endswith(",1")

@@ -186,3 +186,22 @@ def test_mesh_ingestion_reads_the_reference_s_files(tmp_path):
         meshio.read_binary(b, 3, 3)
     assert e.value.kind == "config_error"
 
+
+
+def test_cli_host_verbs(tmp_path):
+    """SPEC cmd_convert (idempotent, missing file -> nonzero exit), usage error -> 64, partition statistics: the
+    verbs of python -m paper_1803_09948_b200 that need no GPU"""
+    from paper_1803_09948_b200.__main__ import main
+    from paper_1803_09948_b200.meshio import read_mesh, write_gmsh
+    from paper_1803_09948_b200.workloads import icosphere_patches
+
+    patches = icosphere_patches(1)
+    msh, b1, b2 = (str(tmp_path / f) for f in ("s.msh", "a.bin", "b.bin"))
+    write_gmsh(patches, msh)
+    assert main(["convert", msh, b1]) == 0 and main(["convert", b1, b2]) == 0
+    assert open(b1, "rb").read() == open(b2, "rb").read()                      # convert twice -> identical bytes
+    assert len(open(b1, "rb").read()) == 32 + 144 * len(patches)               # SPEC: 32 + 144 E bytes
+    assert np.allclose(read_mesh(b1), patches, rtol=0, atol=1e-15)
+    assert main(["convert", str(tmp_path / "missing.msh"), b2]) != 0
+    assert main(["solve", "--no-such-flag"]) == 64
+    assert main(["partition", "--config", "cfg4", "--n", "20000", "--ranks", "4"]) == 0
