@@ -278,7 +278,12 @@ struct FoldUnit {
   uint32_t ap, am;
   float sg;
 };
-__device__ __forceinline__ void unit_load(FoldUnit& f, uint32_t un, uint32_t duo, uint32_t ph_duo) {
+// e^{i m phi} of the lane's two pairs, kept across the units of one order (the unit list is m-major)
+struct UnitPhase {
+  u64 ph0 = 0ull, ph1 = 0ull;
+  uint32_t m = 0;
+};
+__device__ __forceinline__ void unit_load(FoldUnit& f, uint32_t un, uint32_t duo, uint32_t ph_duo, UnitPhase& ph) {
   const uint32_t m = un >> 20;
   f.ap = duo + (un & 0xfffffu);
   f.am = f.ap - m * (2u * kPitchB);
@@ -286,8 +291,13 @@ __device__ __forceinline__ void unit_load(FoldUnit& f, uint32_t un, uint32_t duo
   f.xp1 = lds1(f.ap + 256u);
   f.xm0 = lds1(f.am);
   f.xm1 = lds1(f.am + 256u);
-  f.ph0 = lds1(ph_duo + m * (8u * kBatch64));
-  f.ph1 = lds1(ph_duo + m * (8u * kBatch64) + 256u);
+  if (m != ph.m) {  // warp-uniform
+    ph.ph0 = lds1(ph_duo + m * (8u * kBatch64));
+    ph.ph1 = lds1(ph_duo + m * (8u * kBatch64) + 256u);
+    ph.m = m;
+  }
+  f.ph0 = ph.ph0;
+  f.ph1 = ph.ph1;
   f.sg = (m & 1) ? -1.0f : 1.0f;
 }
 __device__ __forceinline__ void fold_finish(const FoldUnit& f) {
@@ -492,17 +502,18 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(WARPS == 8 ? 112 : 128
   const int u_begin = sp.n_fold * warp / WARPS, u_end = sp.n_fold * (warp + 1) / WARPS;
   auto fold_or_unfold = [&](auto finish) {
     int u = u_begin;
+    UnitPhase ph;
 #pragma unroll 1
     for (; u + 1 < u_end; u += 2) {
       FoldUnit fa, fb;
-      unit_load(fa, lds32(unit_base + 4u * u), duo, ph_duo);
-      unit_load(fb, lds32(unit_base + 4u * u + 4u), duo, ph_duo);
+      unit_load(fa, lds32(unit_base + 4u * u), duo, ph_duo, ph);
+      unit_load(fb, lds32(unit_base + 4u * u + 4u), duo, ph_duo, ph);
       finish(fa);
       finish(fb);
     }
     if (u < u_end) {
       FoldUnit fa;
-      unit_load(fa, lds32(unit_base + 4u * u), duo, ph_duo);
+      unit_load(fa, lds32(unit_base + 4u * u), duo, ph_duo, ph);
       finish(fa);
     }
   };
