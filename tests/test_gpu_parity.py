@@ -653,3 +653,33 @@ def test_distinct_targets_and_sources(oracle):
                   oracle.direct_sum(np.vstack([xyz, tg[:100] + 0.01]), np.concatenate([q, np.zeros(100)]), k,
                                     targets=np.arange(n, n + 100))) < 1e-5
     assert rel_l2(op.matvec(q), y_self) < 1e-6                         # the handle's own operator is untouched
+
+
+def test_partition_of_a_clustered_set_without_leaf_cap():
+    """Advisor finding (round 1): with leaf_cap = 0 a clustered set puts owned leaves beside unowned interior
+    cells on the levels ABOVE the partition cut; those levels are never exchanged and must not trip the
+    contiguity check of hfmm_cuda_get_partition.  Three emulated ranks still reproduce the single-domain matvec."""
+    import torch
+
+    from paper_1803_09948_b200.distributed import emulate_matvec_on_one_device
+
+    n, k, order = 30000, 3.0, 6
+    xyz, q = plummer_points(n, 77, a=0.02), charges(n, 77)
+    kw = dict(k=k, order=order, ncrit=48, theta=0.4, kd_max=1.0, leaf_cap=0.0)
+    single = HfmmCuda(**kw)
+    single.set_points(xyz)
+    y1, order_m = single.matvec(q), single.body_order()
+    ops = []
+    for rank in range(3):
+        op = HfmmCuda(**kw)
+        op.set_partition(rank, 3)
+        op.set_points(xyz)
+        p = op.partition()                      # raised HFMM_ERR_STRUCTURAL before the fix
+        assert int(p.body_count) > 0
+        ops.append(op)
+    levels = single.cells()[:, 0]
+    assert levels.max() - levels[single.cells()[:, 7] == 0].min() >= 3      # leaves spread over several levels
+    qm = q[order_m]
+    qd = torch.from_numpy(np.stack([qm.real, qm.imag], 1).astype(np.float32)).cuda()
+    y = emulate_matvec_on_one_device(ops, qd).cpu().numpy()
+    assert rel_l2(y[:, 0] + 1j * y[:, 1], y1[order_m]) < 3e-6
