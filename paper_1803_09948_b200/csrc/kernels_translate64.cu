@@ -52,8 +52,8 @@ constexpr int kTranslate64SplitFrom = 11;  // sixteen warps: systems of this man
 constexpr uint32_t kPitchB = 520;  // bytes per tile row: 64 pairs x float2 + 8 (rows two banks apart)
 
 struct Plan64 {
-  int dim, n_fold, rot_floats, coax_c;
-  uint32_t off_coax, off_phase, off_tile, off_unit, off_meta;
+  int dim, n_fold, n_units, rot_floats, coax_c;
+  uint32_t off_coax, off_phase, off_tile, off_unit, off_unit_s, off_meta;
   size_t bytes;
 };
 // metadata of one batch: source row, destination row, class, (cos phi, sin phi) per pair
@@ -62,13 +62,15 @@ __host__ __device__ constexpr Plan64 plan64(int P) {
   Plan64 s{};
   s.dim = (P + 1) * (P + 1);
   s.n_fold = P * (P + 1) / 2;  // units (n, m >= 1)
+  s.n_units = (P + 1) * (P + 2) / 2;  // units (n, m >= 0)
   s.rot_floats = rot_table_size(P);
   s.coax_c = coax_table_size(P);
   s.off_coax = 4u * uint32_t(s.rot_floats);
-  s.off_phase = s.off_coax + 8u * uint32_t(s.coax_c);                      // e^{i m phi}: [m][pair]
-  s.off_tile = (s.off_phase + 8u * uint32_t((P + 1) * kBatch64) + 15u) & ~15u;
+  s.off_phase = s.off_coax + 8u * uint32_t(s.coax_c);                      // e^{i m phi}: [m][pair], tile pitch
+  s.off_tile = (s.off_phase + kPitchB * uint32_t(P + 1) + 15u) & ~15u;
   s.off_unit = (s.off_tile + kPitchB * uint32_t(s.dim) + 15u) & ~15u;
-  s.off_meta = (s.off_unit + 4u * uint32_t(s.n_fold) + 15u) & ~15u;
+  s.off_unit_s = (s.off_unit + 4u * uint32_t(s.n_fold) + 15u) & ~15u;
+  s.off_meta = (s.off_unit_s + 4u * uint32_t(s.n_units) + 15u) & ~15u;
   s.bytes = size_t(s.off_meta) + 2 * kMetaBytes;
   return s;
 }
@@ -292,8 +294,8 @@ __device__ __forceinline__ void unit_load(FoldUnit& f, uint32_t un, uint32_t duo
   f.xm0 = lds1(f.am);
   f.xm1 = lds1(f.am + 256u);
   if (m != ph.m) {  // warp-uniform
-    ph.ph0 = lds1(ph_duo + m * (8u * kBatch64));
-    ph.ph1 = lds1(ph_duo + m * (8u * kBatch64) + 256u);
+    ph.ph0 = lds1(ph_duo + m * kPitchB);
+    ph.ph1 = lds1(ph_duo + m * kPitchB + 256u);
     ph.m = m;
   }
   f.ph0 = ph.ph0;
@@ -348,7 +350,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(WARPS == 8 ? 112 : 128
 
   const uint32_t win = uint32_t(__cvta_generic_to_shared(smem64));
   const uint32_t tile = win + sp.off_tile, ph_base = win + sp.off_phase, duo = tile + 8u * uint32_t(lane);
-  const uint32_t unit_base = win + sp.off_unit, meta_base = win + sp.off_meta;
+  const uint32_t unit_base = win + sp.off_unit, unit_s_base = win + sp.off_unit_s, meta_base = win + sp.off_meta;
   // units (n, m >= 1), m-major: byte offset of row (n, +m) | m << 20; the row of (n, -m) is 2 m rows back
   {
     uint32_t* s_unit = reinterpret_cast<uint32_t*>(smem64 + sp.off_unit);
@@ -360,6 +362,17 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(WARPS == 8 ? 112 : 128
       }
       const int n = m + (u - first);
       s_unit[u] = uint32_t(n * n + n + m) * kPitchB | uint32_t(m) << 20;
+    }
+  }
+  // all units (n, m >= 0) in coefficient order, for the unfold + scatter: row of (n, +m) | m << 16
+  {
+    uint32_t* s_unit_s = reinterpret_cast<uint32_t*>(smem64 + sp.off_unit_s);
+    for (int u = tid; u < sp.n_units; u += kThreads) {
+      int n = int((sqrtf(8.0f * float(u) + 1.0f) - 1.0f) * 0.5f);
+      while (n * (n + 1) / 2 > u) --n;
+      while ((n + 1) * (n + 2) / 2 <= u) ++n;
+      const int m = u - n * (n + 1) / 2;
+      s_unit_s[u] = uint32_t(n * n + n + m) | uint32_t(m) << 16;
     }
   }
   // idle pair columns of a partial batch must stay finite: clear the tile once
@@ -408,10 +421,10 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(WARPS == 8 ? 112 : 128
       bi = 2.f * br * bi;
       br = t;
     }
-    uint32_t dst = ph_base + 8u * uint32_t(g * per * kBatch64 + warp * kPairsPerWarp + pp);
+    uint32_t dst = ph_base + kPitchB * uint32_t(g * per) + 8u * uint32_t(warp * kPairsPerWarp + pp);
     for (int j = 0, m = g * per; j < per && m <= P; ++j, ++m) {
       sts1(dst, pack2(cr, ci));
-      dst += 8u * kBatch64;
+      dst += kPitchB;
       const float t = cr * c1.x - ci * c1.y;
       ci = ci * c1.x + cr * c1.y;
       cr = t;
@@ -496,7 +509,42 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(WARPS == 8 ? 112 : 128
     }
   };
 
-  // fold and unfold, in place, all 64 pairs of a unit per warp step (a lane owns the pairs l and l + 32 as
+  // unfold + scatter of one pair column, lane = unit (n, m >= 0): the inverse rotation left u' in row (n, +m) and
+  // v' in row (n, -m), still without the (-1)^mu of the symmetry;
+  //   y_m = (-1)^m (u' + v')/2 e^{-i m phi} -> element n^2 + n + m,   y_{-m} = (u' - v')/2 e^{+i m phi} -> n^2 + n - m
+  // go straight from registers to the destination row (RED.64; plain stores in deterministic mode).  Lanes read
+  // different rows of one column (two banks apart: conflict free) and the phase column at the tile pitch.
+  constexpr int kURoundsT = PT ? ((PT + 1) * (PT + 2) / 2 + 31) / 32 : 0;
+  auto unfold_scatter_round = [&](uint32_t col, uint32_t phc, float2* dst, int u) {
+    const uint32_t un = lds32(unit_s_base + 4u * uint32_t(u)), rp = un & 0xffffu, m = un >> 16;
+    const u64 up = lds1(col + rp * kPitchB), vm = lds1(col + (rp - 2u * m) * kPitchB), ph = lds1(phc + m * kPitchB);
+    const float2 f = unpack2(ph);
+    const float hs = (m & 1) ? -0.5f : 0.5f;
+    const u64 sm = m ? add2(up, vm) : add2(up, up), df = add2(up, neg2(vm));   // m = 0: y_0 = u'
+    u64 yp = mul2s(sm, hs * f.x), ym = mul2s(df, 0.5f * f.x);
+    fma2s(yp, rot90(sm), -hs * f.y);
+    fma2s(ym, rot90(df), 0.5f * f.y);
+    if (STAGED) {
+      dst[rp] = unpack2(yp);
+      if (m) dst[rp - 2u * m] = unpack2(ym);
+    } else {
+      atomicAdd(dst + rp, unpack2(yp));
+      if (m) atomicAdd(dst + (rp - 2u * m), unpack2(ym));
+    }
+  };
+  auto unfold_scatter = [&](uint32_t col, uint32_t phc, uint32_t drow) {
+    float2* dst = a.dst + size_t(drow) * a.stride;
+    if constexpr (PT != 0) {
+#pragma unroll
+      for (int r = 0; r < kURoundsT; ++r)
+        if (32 * r + 32 <= (PT + 1) * (PT + 2) / 2 || 32 * r + lane < (PT + 1) * (PT + 2) / 2)
+          unfold_scatter_round(col, phc, dst, 32 * r + lane);
+    } else {
+      for (int u = lane; u < sp.n_units; u += 32) unfold_scatter_round(col, phc, dst, u);
+    }
+  };
+
+  // fold, in place, all 64 pairs of a unit per warp step (a lane owns the pairs l and l + 32 as
   // in the compute stages); a warp walks a contiguous chunk of the m-major unit list two units at a time
   const uint32_t ph_duo = ph_base + 8u * uint32_t(lane);
   const int u_begin = sp.n_fold * warp / WARPS, u_end = sp.n_fold * (warp + 1) / WARPS;
@@ -584,11 +632,8 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(WARPS == 8 ? 112 : 128
       loaded_grp = next.group;
     }
     cp_commit();
-    fold_or_unfold([](const FoldUnit& f) { unfold_finish(f); });
-    __syncthreads();
-    // scatter, then this warp's columns of the next batch: a warp reads and rewrites only its own
-    // tile columns and phase columns, so no CTA barrier separates the two.  The rows of all the warp's
-    // pairs are read first (16-byte loads), then two pairs move at a time.
+    // unfold + scatter, then this warp's columns of the next batch: a warp reads and rewrites only its own
+    // tile columns and phase columns, so no CTA barrier separates the inverse rotation's barrier from the gather
     {
       uint32_t drow[kPairsPerWarp], srow[kPairsPerWarp];
 #pragma unroll
@@ -600,16 +645,13 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(WARPS == 8 ? 112 : 128
         srow[4 * v] = __float_as_uint(s4.x); srow[4 * v + 1] = __float_as_uint(s4.y);
         srow[4 * v + 2] = __float_as_uint(s4.z); srow[4 * v + 3] = __float_as_uint(s4.w);
       }
-      const uint32_t col0 = tile + 8u * uint32_t(warp * kPairsPerWarp) + kPitchB * uint32_t(lane);
-      const uint32_t live = item.count - min(item.count, uint32_t(warp * kPairsPerWarp));  // pairs of this warp in the batch
+      const uint32_t p0 = uint32_t(warp * kPairsPerWarp);
+      const uint32_t live = item.count - min(item.count, p0);  // pairs of this warp in the batch
 #pragma unroll
-      for (int pp = 0; pp < kPairsPerWarp; pp += 2) {
-        if (uint32_t(pp + 1) < live) scatter_two(col0 + 8u * pp, drow[pp], drow[pp + 1]);
-        else if (uint32_t(pp) < live) scatter_pair(col0 + 8u * pp, drow[pp]);
-        if (has_next) {  // idle columns of a partial batch re-read the batch's last pair: finite, never scattered
-          gather_pair(col0 + 8u * pp, srow[pp]);
-          gather_pair(col0 + 8u * pp + 8u, srow[pp + 1]);
-        }
+      for (int pp = 0; pp < kPairsPerWarp; ++pp) {
+        if (uint32_t(pp) < live) unfold_scatter(tile + 8u * (p0 + pp), ph_base + 8u * (p0 + pp), drow[pp]);
+        // idle columns of a partial batch re-read the batch's last pair: finite, never scattered
+        if (has_next) gather_pair(tile + 8u * (p0 + pp) + kPitchB * uint32_t(lane), srow[pp]);
       }
     }
     cp_commit();
