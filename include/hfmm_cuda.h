@@ -203,7 +203,9 @@ int hfmm_cuda_get_cells(hfmm_cuda_t* h, uint32_t* out, size_t capacity_cells);
 /* Morton order: out[slot] = caller index (Body::index) */
 int hfmm_cuda_get_body_order(hfmm_cuda_t* h, uint32_t* out);
 /* which: 0 M2L cell pairs, 1 P2P leaf pairs; (target, source) u32 pairs, unspecified order.
- * Pass out == NULL to query the count only. */
+ * Pass out == NULL to query the count only.  With nranks > 1 (device builder) the lists are built per rank:
+ * exactly the pairs of the global walk whose target OR source cell this rank owns; hfmm_cuda_stats keeps the
+ * counts of the global lists. */
 int hfmm_cuda_get_pairs(hfmm_cuda_t* h, int which, uint32_t* out, uint64_t* count);
 /* which: 0 multipole, 1 local, of the last matvec, UNSCALED back to the reference's convention
  * (M_n^m / L_n^m at index n(n+1)+m); out: n_cells x (P+1)^2 interleaved complex doubles */
@@ -212,8 +214,10 @@ int hfmm_cuda_get_expansions(hfmm_cuda_t* h, int which, double* out);
 /* ---- multi-GPU: one process per GPU, Morton-partitioned ---------------------
  * Stands in for the reference's simulated-rank layer (part::distributed_matvec, let.cpp:320-362).
  * Every rank passes the GLOBAL point set to set_points after set_partition(rank, nranks): the
- * tree and lists are identical on all ranks, the Morton order is cut into nranks contiguous body
- * ranges balanced by estimated work, and each rank keeps only the work whose TARGETS it owns.
+ * tree is identical on all ranks, the Morton order is cut into nranks contiguous body ranges balanced by
+ * estimated work (a census pass of the dual tree walk that stores no pair: same cuts on every rank, no
+ * handshake), and each rank then walks, stores and sorts only the pairs that touch a cell it owns — its
+ * work (target owned) and what it must send (source owned).
  * hfmm_cuda_dist_matvec / hfmm_cuda_dist_solve below run the whole exchange inside the library.  The two
  * phase calls that follow are the building blocks for a caller that moves the data itself (and for the
  * single-device emulation of several ranks in the tests): all the charges in place -> dist_upward ->
@@ -238,9 +242,10 @@ int hfmm_cuda_dist_downward(hfmm_cuda_t* h, void* out_morton_dev);
 /* Locally essential trees (reference extract_let, let.cpp:150-253): per cell (n_cells entries, the
  * order of hfmm_cuda_get_cells), bit p of far_mask says rank p needs the cell's multipole (it is the
  * source of an M2L pair whose target p owns), bit p of near_mask says rank p needs the bodies of the
- * leaf; cell_rank is the owner.  All ranks compute identical masks from the global lists, so the
- * send list "my cells with bit p" and the receive list "p's cells with my bit" match without any
- * handshake.  At most 64 ranks. */
+ * leaf; cell_rank is the owner (identical on all ranks).  A rank's lists hold every pair out of its own
+ * cells and every pair into them, so the bits it reads — bit p of ITS OWN cells (send list) and ITS OWN bit
+ * of p's cells (receive list) — are those of the global lists and the two sides match element for element
+ * without any handshake; the other bits of foreign cells are not filled in.  At most 64 ranks. */
 int hfmm_cuda_get_exchange_masks(hfmm_cuda_t* h, uint64_t* far_mask, uint64_t* near_mask, int32_t* cell_rank);
 
 /* ---- repartitioning loop (reference partition.cpp:137-227) -------
@@ -248,7 +253,8 @@ int hfmm_cuda_get_exchange_masks(hfmm_cuda_t* h, uint64_t* far_mask, uint64_t* n
  * estimates come from the interaction lists of the current point set; alpha is searched by the
  * caller's driver from measured matvec times (max over ranks). */
 /* per body, caller order: local[i] = bodies of the P2P partner leaves of i's leaf, remote[i] = number
- * of M2L pairs of all cells holding i (measure_weights, partition.cpp:143-163) */
+ * of M2L pairs of all cells holding i (measure_weights, partition.cpp:143-163).  With nranks > 1 the
+ * entries of the bodies this rank owns are exact; the others only count the pairs out of this rank's cells. */
 int hfmm_cuda_measure_weights(hfmm_cuda_t* h, double* local, double* remote);
 /* balance the Morton cuts of hfmm_cuda_set_partition by sum(l + alpha r) (apply_weights,
  * partition.cpp:165-173); alpha < 0 (default) balances by measured kernel cost per list entry instead.

@@ -288,8 +288,8 @@ void Engine::comm_init_host(const hfmm_host_transport& cb) {
 const char* Engine::comm_name() const { return transport_ ? transport_->name() : "none"; }
 
 // Index lists of the locally-essential-tree exchange (let.cpp:150-253, sender-initiated): every rank holds
-// the global lists, so "my cells peer p translates from" here equals "the cells of mine that p expects" there,
-// element for element (ascending cell order) — no handshake.
+// all pairs of the global walk into and out of its own cells, so "my cells peer p translates from" here equals
+// "the cells of mine that p expects" there, element for element (ascending cell order) — no handshake.
 void Engine::build_exchange_plan() {
   require_points();
   if (!transport_) throw Error(HFMM_ERR_CONFIG, "no communicator: call hfmm_cuda_comm_init_nccl / _host first");

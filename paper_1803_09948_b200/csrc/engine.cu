@@ -832,37 +832,59 @@ void Engine::set_points_device(const double* xyz, size_t n) {
   const TreeArrays& t = tree_;
   DeviceCells cells;
   cells.upload(t, stream_);
-  dual_tree_traversal_device(t, cells, std::hypot(cfg_.wave_r, cfg_.wave_i), cfg_.theta, cfg_.kd_max, cfg_.grain,
-                             dev_pairs_, stream_);  // the gate uses |k| (traversal.cpp:86)
-  stats_.tasks = dev_pairs_.tasks;
-  far_pair_level_range(dev_pairs_, cells, lmin_dst_, lmin_src_, stream_);
-  mark("traversal");
-  have_far_ = dev_pairs_.n_far > 0;
-  stats_.m2l_pairs = dev_pairs_.n_far;
-  stats_.p2p_pairs = dev_pairs_.n_near;
-
-  // Morton partition: units on the host, their work weights from the device pair lists
+  const double kmag = std::hypot(cfg_.wave_r, cfg_.wave_i);  // the gate uses |k| (traversal.cpp:86)
   const size_t nc = t.n_cells();
   owned_.assign(nc, 1);
   own_first_ = 0;
   own_count_ = t.n_bodies;
-  {
+  uint64_t global_body_pairs = 0;
+  if (nranks_ == 1) {
+    dual_tree_traversal_device(t, cells, kmag, cfg_.theta, cfg_.kd_max, cfg_.grain, dev_pairs_, stream_);
+    stats_.tasks = dev_pairs_.tasks;
+    far_pair_level_range(dev_pairs_, cells, lmin_dst_, lmin_src_, stream_);
+    mark("traversal");
+    stats_.m2l_pairs = dev_pairs_.n_far;
+    stats_.p2p_pairs = dev_pairs_.n_near;
     std::vector<uint32_t> unit;
     lcut_ = partition_units(t, lmin_src_, lmin_dst_, unit);
-    if (nranks_ > 1) {
-      std::vector<double> weight;
-      partition_weights_device(dev_pairs_, cells, unit, partition_alpha_, weight, stream_);
-      std::vector<int> cell_rank;
-      std::vector<uint32_t> first, count;
-      partition_cuts(t, unit, weight, nranks_, cell_rank, first, count);
-      own_first_ = first[rank_];
-      own_count_ = count[rank_];
-      for (size_t c = 0; c < nc; ++c) owned_[c] = cell_rank[c] == rank_;
-      cell_rank_.assign(cell_rank.begin(), cell_rank.end());
-    } else {
-      cell_rank_.assign(nc, 0);
-    }
+    cell_rank_.assign(nc, 0);
+  } else {
+    // Several ranks: the pair lists are built PER RANK.  Pass 1 walks the global descent without storing a pair
+    // and leaves the work of every target cell (the weights that place the Morton cuts, identical on all ranks:
+    // no handshake); pass 2 repeats the descent pruned to the nodes that touch a subtree this rank owns, so the
+    // stored lists, their sorts and everything derived from them are O(N / ranks + boundary).
+    TraversalCensus census;
+    dual_tree_census_device(t, cells, kmag, cfg_.theta, cfg_.kd_max, cfg_.grain, partition_alpha_, census, stream_);
+    mark("traversal (census)");
+    stats_.tasks = census.tasks;
+    stats_.m2l_pairs = census.n_far;
+    stats_.p2p_pairs = census.n_near;
+    global_body_pairs = census.body_pairs;
+    lmin_dst_ = census.lmin_dst;
+    lmin_src_ = census.lmin_src;
+    std::vector<uint32_t> unit;
+    lcut_ = partition_units(t, lmin_src_, lmin_dst_, unit);
+    std::vector<double> weight(nc, 0.0);
+    for (size_t c = 0; c < nc; ++c)
+      if (census.cell_weight[c] != 0.0) {
+        if (unit[c] == 0xffffffffu) throw Error(HFMM_ERR_INTERNAL, "a target cell above the partition cut carries work");
+        weight[unit[c]] += census.cell_weight[c];
+      }
+    std::vector<int> cell_rank;
+    std::vector<uint32_t> first, count;
+    partition_cuts(t, unit, weight, nranks_, cell_rank, first, count);
+    own_first_ = first[rank_];
+    own_count_ = count[rank_];
+    for (size_t c = 0; c < nc; ++c) owned_[c] = cell_rank[c] == rank_;
+    cell_rank_.assign(cell_rank.begin(), cell_rank.end());
+    // subtrees that hold an owned cell (cells are stored level by level, parents first)
+    std::vector<uint8_t> interest(owned_.begin(), owned_.end());
+    for (size_t c = nc; c-- > 1;)
+      if (interest[c]) interest[t.parent[c]] = 1;
+    dual_tree_traversal_pruned_device(t, cells, kmag, cfg_.theta, cfg_.kd_max, interest, dev_pairs_, stream_);
+    mark("traversal (pruned to the rank)");
   }
+  have_far_ = stats_.m2l_pairs > 0;
 
   std::vector<int4> geom;
   upload_cell_geometry(geom);
@@ -871,7 +893,7 @@ void Engine::set_points_device(const double* xyz, size_t n) {
 
   NearLists nl;
   build_near_lists_device(dev_pairs_, t, cells, owned_, p2p_offset_, p2p_split_, p2p_src_, nl, stream_);
-  stats_.p2p_body_pairs = nl.body_pairs;
+  stats_.p2p_body_pairs = nranks_ == 1 ? nl.body_pairs : global_body_pairs;  // of the global lists
   owned_body_pairs_ = nl.owned_body_pairs;
   select_near_kernel(nl.max_r2_lattice);
   build_tiles(nl.work);

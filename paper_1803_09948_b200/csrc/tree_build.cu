@@ -134,6 +134,12 @@ struct PairSink {
   unsigned long long* count;
   unsigned long long cap;
 };
+// census pass of the multi-rank setup (tree_build.cuh): per-target-cell work instead of stored pairs
+struct CensusSink {
+  unsigned long long* cell_work = nullptr;  // [2 c] far pairs, [2 c + 1] near body pairs of target cell c: integers,
+                                            // so the totals do not depend on the order of the atomics
+  int* level_min = nullptr;                 // coarsest level among the SOURCES of the far pairs
+};
 
 // reserves `cnt` slots for this lane; one atomic per warp
 __device__ __forceinline__ unsigned long long warp_reserve(unsigned long long* counter, uint32_t cnt) {
@@ -157,9 +163,11 @@ traversal_kernel(const uint2* __restrict__ frontier, unsigned long long n_front,
                  const uint32_t* __restrict__ iz, const uint32_t* __restrict__ child_first,
                  const uint32_t* __restrict__ child_count, const uint32_t* __restrict__ body_count,
                  uint32_t grain, unsigned long long* __restrict__ tasks, const TraversalGeom g, PairSink next,
-                 PairSink far, PairSink near, int* __restrict__ overflow) {
+                 PairSink far, PairSink near, int* __restrict__ overflow, const uint8_t* __restrict__ interest,
+                 const CensusSink census) {
   const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = i < n_front;
+  // pruned descent (multi-rank setup): a node none of whose two subtrees holds an owned cell is dropped
+  const bool live = i < n_front && (!interest || (interest[frontier[i].x] | interest[frontier[i].y]));
   uint32_t a = 0, b = 0, n_far = 0, n_near = 0, n_next = 0;
   bool split_target = false;
   if (live) {
@@ -193,13 +201,25 @@ traversal_kernel(const uint2* __restrict__ frontier, unsigned long long n_front,
   const unsigned long long s_far = warp_reserve(far.count, n_far);
   const unsigned long long s_near = warp_reserve(near.count, n_near);
   const unsigned long long s_next = warp_reserve(next.count, n_next);
-  if (n_far) {
-    if (s_far < far.cap) far.data[s_far] = make_uint2(a, b);
-    else *overflow = 1;
-  }
-  if (n_near) {
-    if (s_near < near.cap) near.data[s_near] = make_uint2(a, b);
-    else *overflow = 1;
+  if (census.cell_work) {
+    // census: nothing is stored; the pair's work goes to its target cell
+    const unsigned long long bp = n_near ? (unsigned long long)body_count[a] * body_count[b] : 0ull;
+    if (n_far) atomicAdd(census.cell_work + 2ull * a, 1ull);
+    if (n_near) atomicAdd(census.cell_work + 2ull * a + 1, bp);
+    // coarsest source level of the far pairs: the running minimum settles within the first levels of the walk,
+    // after which no warp issues the atomic any more (the target side and the body-pair total are read off
+    // cell_work on the host)
+    const int ls = __reduce_min_sync(0xffffffffu, n_far ? int(lvl[b]) : kMaxLevel + 1);
+    if ((threadIdx.x & 31) == 0 && ls < *reinterpret_cast<volatile int*>(census.level_min)) atomicMin(census.level_min, ls);
+  } else {
+    if (n_far) {
+      if (s_far < far.cap) far.data[s_far] = make_uint2(a, b);
+      else *overflow = 1;
+    }
+    if (n_near) {
+      if (s_near < near.cap) near.data[s_near] = make_uint2(a, b);
+      else *overflow = 1;
+    }
   }
   if (n_next) {
     if (s_next + n_next <= next.cap) {
@@ -532,33 +552,54 @@ void build_tree_device(TreeArrays& t, const double* xyz, size_t n, int ncrit, do
     }
 }
 
-void dual_tree_traversal_device(const TreeArrays& t, const DeviceCells& cells, double kmag, double theta,
-                                double kd_max, int grain, DevicePairs& out, cudaStream_t s) {
+namespace {
+// the level-synchronous descent behind the three entry points below
+//   census != nullptr : nothing stored, work per target cell and totals (global lists)
+//   interest != nullptr: pruned to the nodes that touch an owned subtree
+void run_traversal(const TreeArrays& t, const DeviceCells& cells, double kmag, double theta, double kd_max, int grain,
+                   const uint8_t* d_interest, TraversalCensus* census, double alpha, DevicePairs& out, cudaStream_t s) {
   if (!(theta > 0) || theta > 1) throw Error(HFMM_ERR_CONFIG, "opening angle must satisfy 0 < theta <= 1");
   const TraversalGeom g = make_geom(t, kmag, theta, kd_max);
   const uint64_t n = t.n_bodies;
   uint64_t cap_far = 16 * n + (1 << 20), cap_near = 8 * n + (1 << 20), cap_front = 16 * n + (1 << 20);
   DeviceBuffer<unsigned long long> counters(4);
-  DeviceBuffer<int> overflow(1);
+  DeviceBuffer<int> overflow(1), level_min;
+  DeviceBuffer<unsigned long long> cell_work;
+  if (census) {
+    cell_work.resize(2 * t.n_cells());
+    level_min.resize(1);
+  }
   for (int attempt = 0; attempt < 6; ++attempt) {
-    out.far.resize(cap_far);
-    out.near.resize(cap_near);
+    if (!census) {
+      out.far.resize(cap_far);
+      out.near.resize(cap_near);
+    }
     DeviceBuffer<uint2> fa(cap_front), fb(cap_front);
     counters.zero(s);
     overflow.zero(s);
+    CensusSink cs;
+    if (census) {
+      cell_work.zero(s);
+      const int init = kMaxLevel + 1;
+      HFMM_CUDA_CHECK(cudaMemcpyAsync(level_min.get(), &init, sizeof(init), cudaMemcpyHostToDevice, s));
+      cs.cell_work = cell_work.get();
+      cs.level_min = level_min.get();
+    }
     const uint2 root = make_uint2(0, 0);
     HFMM_CUDA_CHECK(cudaMemcpyAsync(fa.get(), &root, sizeof(uint2), cudaMemcpyHostToDevice, s));
     unsigned long long n_front = 1;
     uint2 *cur = fa.get(), *nxt = fb.get();
     int ovf = 0;
+    const unsigned long long unbounded = ~0ull;
     while (n_front > 0 && !ovf) {
       HFMM_CUDA_CHECK(cudaMemsetAsync(counters.get() + 2, 0, sizeof(unsigned long long), s));
-      PairSink next{nxt, counters.get() + 2, cap_front}, far{out.far.get(), counters.get(), cap_far},
-          near{out.near.get(), counters.get() + 1, cap_near};
+      PairSink next{nxt, counters.get() + 2, cap_front},
+          far{census ? nullptr : out.far.get(), counters.get(), census ? unbounded : cap_far},
+          near{census ? nullptr : out.near.get(), counters.get() + 1, census ? unbounded : cap_near};
       traversal_kernel<<<grid_for(n_front), kBlock, 0, s>>>(
           cur, n_front, cells.level.get(), cells.ix.get(), cells.iy.get(), cells.iz.get(),
           cells.child_first.get(), cells.child_count.get(), cells.body_count.get(), uint32_t(grain),
-          counters.get() + 3, g, next, far, near, overflow.get());
+          counters.get() + 3, g, next, far, near, overflow.get(), d_interest, cs);
       HFMM_CUDA_CHECK(cudaGetLastError());
       unsigned long long h[4];
       HFMM_CUDA_CHECK(cudaMemcpyAsync(h, counters.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -571,7 +612,31 @@ void dual_tree_traversal_device(const TreeArrays& t, const DeviceCells& cells, d
       out.tasks = h[3] + (2 * uint64_t(t.n_bodies) <= uint64_t(grain) ? 1 : 0);
       std::swap(cur, nxt);
     }
-    if (!ovf) return;
+    if (!ovf) {
+      if (census) {
+        census->n_far = out.n_far;
+        census->n_near = out.n_near;
+        census->tasks = out.tasks;
+        int lm = kMaxLevel + 1;
+        level_min.download(&lm, 1, s);
+        std::vector<unsigned long long> work(2 * t.n_cells());
+        cell_work.download(work.data(), work.size(), s);
+        HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
+        census->lmin_src = lm;
+        census->lmin_dst = kMaxLevel + 1;
+        census->body_pairs = 0;
+        for (size_t c = 0; c < t.n_cells(); ++c) {
+          if (work[2 * c]) census->lmin_dst = std::min(census->lmin_dst, int(t.level[c]));
+          census->body_pairs += work[2 * c + 1];
+        }
+        // partition_weights_device's model, evaluated in a fixed order: identical on every rank
+        census->cell_weight.resize(t.n_cells());
+        for (size_t c = 0; c < t.n_cells(); ++c)
+          census->cell_weight[c] = double(work[2 * c]) * (alpha < 0 ? kPartitionM2lWeight : alpha * double(t.body_count[c])) +
+                                   double(work[2 * c + 1]);
+      }
+      return;
+    }
     cap_far *= 2;
     cap_near *= 2;
     cap_front *= 2;
@@ -582,6 +647,27 @@ void dual_tree_traversal_device(const TreeArrays& t, const DeviceCells& cells, d
                            "dual tree traversal: interaction lists exceed 512 pairs per body (kd_max too small for "
                            "this wavenumber and domain?)",
                            false);
+}
+}  // namespace
+
+void dual_tree_traversal_device(const TreeArrays& t, const DeviceCells& cells, double kmag, double theta,
+                                double kd_max, int grain, DevicePairs& out, cudaStream_t s) {
+  run_traversal(t, cells, kmag, theta, kd_max, grain, nullptr, nullptr, -1.0, out, s);
+}
+
+void dual_tree_census_device(const TreeArrays& t, const DeviceCells& cells, double kmag, double theta,
+                             double kd_max, int grain, double alpha, TraversalCensus& out, cudaStream_t s) {
+  DevicePairs none;
+  run_traversal(t, cells, kmag, theta, kd_max, grain, nullptr, &out, alpha, none, s);
+}
+
+void dual_tree_traversal_pruned_device(const TreeArrays& t, const DeviceCells& cells, double kmag, double theta,
+                                       double kd_max, const std::vector<uint8_t>& interest, DevicePairs& out,
+                                       cudaStream_t s) {
+  DeviceBuffer<uint8_t> d_interest;
+  d_interest.upload(interest, s);
+  // the grain only feeds the task counter, which the census already holds for the global lists
+  run_traversal(t, cells, kmag, theta, kd_max, 0, d_interest.get(), nullptr, -1.0, out, s);
 }
 
 void far_pair_level_range(const DevicePairs& p, const DeviceCells& cells, int& lmin_dst, int& lmin_src,

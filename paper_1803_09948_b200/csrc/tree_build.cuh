@@ -48,6 +48,22 @@ struct DeviceCells {
 void dual_tree_traversal_device(const TreeArrays& tree, const DeviceCells& cells, double kmag,
                                 double theta, double kd_max, int grain, DevicePairs& out, cudaStream_t s);
 
+// Multi-rank setup, pass 1: the SAME global descent, but nothing is stored — every accepted pair only adds its
+// work to its target cell (partition_weights_device's model) and to the totals; memory is the frontier alone.
+struct TraversalCensus {
+  uint64_t n_far = 0, n_near = 0, tasks = 0, body_pairs = 0;  // of the whole (global) lists
+  int lmin_dst = 0, lmin_src = 0;                              // far_pair_level_range of the global lists
+  std::vector<double> cell_weight;                             // per TARGET cell
+};
+void dual_tree_census_device(const TreeArrays& tree, const DeviceCells& cells, double kmag, double theta,
+                             double kd_max, int grain, double alpha, TraversalCensus& out, cudaStream_t s);
+// Multi-rank setup, pass 2: the descent pruned to one rank.  `interest[c]` != 0 iff the subtree of cell c holds a
+// cell the rank owns; a node (t, s) of the walk survives iff interest[t] | interest[s], so the lists hold exactly
+// the pairs whose target the rank owns (its work) or whose source it owns (what it sends: the exchange masks).
+void dual_tree_traversal_pruned_device(const TreeArrays& tree, const DeviceCells& cells, double kmag, double theta,
+                                       double kd_max, const std::vector<uint8_t>& interest, DevicePairs& out,
+                                       cudaStream_t s);
+
 // min level over the M2L targets / sources (kMaxLevel + 1 when there are no pairs)
 void far_pair_level_range(const DevicePairs& p, const DeviceCells& cells, int& lmin_dst, int& lmin_src,
                           cudaStream_t s);

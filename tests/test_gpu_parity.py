@@ -150,6 +150,51 @@ def test_sharded_matvec_equals_single_domain(nranks):
     assert sum(int(p.owned_p2p_body_pairs) for p in parts) == st["p2p_body_pairs"]
 
 
+@pytest.mark.parametrize("nranks,dist_kind", [(2, "sphere"), (4, "plummer"), (8, "sphere")])
+def test_pair_lists_are_built_per_rank(nranks, dist_kind):
+    """Multi-rank setup: a rank stores only the walk's pairs whose target it owns (its work) or whose source
+    it owns (what it must send) — reference: one tree per rank + grafted LETs, let.cpp:98-123, 150-318.  The
+    union over the ranks of the target-owned pairs is the single-domain list, every pair exactly once; the
+    statistics stay those of the global lists; the cuts are the ones every rank derives on its own."""
+    n, k, order = 30000, 4.0, 8
+    xyz = sphere_points(n, 21) if dist_kind == "sphere" else plummer_points(n, 21, a=0.05)
+    single = HfmmCuda(k=k, order=order)
+    single.set_points(xyz)
+    st = single.stats()
+    glob = [set(map(tuple, single.pairs(w).tolist())) for w in (0, 1)]
+    assert len(glob[0]) == st["m2l_pairs"] and len(glob[1]) == st["p2p_pairs"]
+    seen = [set(), set()]
+    stored = 0
+    cuts = None
+    for r in range(nranks):
+        op = HfmmCuda(k=k, order=order)
+        op.set_partition(r, nranks)
+        op.set_points(xyz)
+        sr = op.stats()
+        for key in ("m2l_pairs", "p2p_pairs", "p2p_body_pairs", "tasks", "n_cells"):
+            assert sr[key] == st[key], key
+        _, _, owner = op.exchange_masks()
+        cuts = owner if cuts is None else cuts
+        assert np.array_equal(owner, cuts)  # same partition on every rank, no handshake
+        for w in (0, 1):
+            pr = op.pairs(w)
+            stored += len(pr)
+            t_mine, s_mine = owner[pr[:, 0]] == r, owner[pr[:, 1]] == r
+            assert np.all(t_mine | s_mine)  # nothing the rank neither computes nor sends
+            mine = set(map(tuple, pr[t_mine].tolist()))
+            assert len(mine) == int(t_mine.sum()) and not (mine & seen[w])
+            seen[w] |= mine
+            # complete on the sending side too: every global pair out of one of its cells is there
+            need = {p for p in glob[w] if owner[p[1]] == r}
+            assert need <= set(map(tuple, pr.tolist()))
+        del op
+    assert seen[0] == glob[0] and seen[1] == glob[1]
+    total = len(glob[0]) + len(glob[1])
+    # each pair is stored by the owner of its target and the owner of its source: at most twice over all ranks,
+    # against `nranks` copies of the global lists before
+    assert stored <= 2 * total
+
+
 @pytest.mark.parametrize("nranks,dist_kind", [(2, "sphere"), (5, "plummer"), (8, "sphere")])
 def test_library_data_plane_reproduces_the_single_domain_matvec(nranks, dist_kind):
     """hfmm_cuda_dist_matvec (csrc/comm.cu): pack kernel -> exchange -> unpack kernel for the halo charges and the
