@@ -48,6 +48,12 @@ namespace hfmm_b200 {
 namespace {
 
 constexpr int kBatch64 = 64;
+// Register caps (measured, profiles/r02_notes.md).  Eight warps, two CTAs per SM: ptxas takes 120 registers when
+// left alone; 96 (no spills) is the fastest cap tried between 80 and 128 (11.34 ms against 11.53 at 112, cfg 2).
+// Sixteen warps, one CTA per SM (P = 13..16): the kernel alone is fastest at 128 (567.7 ms at cfg 4), but at 80
+// (no spills, 573.8 ms) three near-field CTAs find registers and shared memory beside it and the STEP drops from
+// 619 to 595 ms.
+constexpr int kMaxReg8 = 96, kMaxReg16 = 80;
 constexpr int kTranslate64SplitFrom = 11;  // sixteen warps: systems of this many rows or more are cut by pair halves
 constexpr uint32_t kPitchB = 520;  // bytes per tile row: 64 pairs x float2 + 8 (rows two banks apart)
 
@@ -336,7 +342,7 @@ __device__ __forceinline__ void unfold_finish(const FoldUnit& f) {
 // WARPS: 8 (two CTAs per SM, P <= 12) or 16 (one CTA per SM, P <= 16; large systems split by pair halves)
 // STAGED: every pair owns its destination row (deterministic mode): plain stores instead of RED
 template <int PT, int WARPS, bool STAGED>
-__global__ void __launch_bounds__(WARPS * 32) __maxnreg__(WARPS == 8 ? 112 : 128) translate64_kernel(const TranslateArgs a) {
+__global__ void __launch_bounds__(WARPS * 32) __maxnreg__(WARPS == 8 ? kMaxReg8 : kMaxReg16) translate64_kernel(const TranslateArgs a) {
   constexpr int kThreads = WARPS * 32, kPairsPerWarp = kBatch64 / WARPS;
   constexpr int RMAX = PT ? PT + 1 : (WARPS == 8 ? kTranslate64MaxOrder + 1 : kTranslate64TopOrder + 1);
   constexpr bool kSplit = WARPS == 16;
