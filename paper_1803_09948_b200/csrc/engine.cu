@@ -1062,10 +1062,11 @@ void Engine::phase_upward() {
   std::copy(p2p_sinc_, p2p_sinc_ + 8, pa.sinc_c);
   std::copy(p2p_cos_, p2p_cos_ + 8, pa.cos_c);
   p2p_args_ = pa;
-  // The near field (MUFU-bound, no shared-memory traffic) and M2L (shared-memory-bound) complement
-  // each other, but only if they are co-resident: enqueued first, the 14 k P2P CTAs fill every SM
-  // and the persistent M2L CTAs wait for them; enqueued BEHIND the M2L launch, one 2-warp P2P CTA
-  // fits next to the two M2L CTAs of an SM and the near field hides under M2L (19.7 -> 18.5 ms at cfg 2)
+  // The near field is enqueued BEHIND the persistent M2L launch (enqueued first, its 30 k CTAs fill every SM
+  // and the M2L CTAs wait for them).  Beside the one sixteen-warp M2L CTA of P >= 13 (80 registers, one tile)
+  // three 2-warp near-field CTAs fit and the near field really hides under M2L (cfg 4: 619 -> 595 ms); the two
+  // eight-warp CTAs of P <= 12 leave 8 KB of shared memory, less than one near-field CTA needs, and the near
+  // field then runs in the gaps and behind M2L (0.4 ms gained over the serialised order at cfg 2)
   p2p_late_ = !serial && have_far_ && !(cfg_.flags & HFMM_FLAG_NEAR_FIRST);
   if (!p2p_late_) {
     cudaStream_t sn = serial ? stream_ : stream_near_;
