@@ -39,10 +39,11 @@ typedef enum {
 
 enum {
   /* build tree + interaction lists with the host C++ builder instead of the device builder (same
-   * tree, same lists; cross-check and fallback).  Without the flag set_points still switches to the
-   * host builder by itself when the device builder's packed sort keys cannot hold a lattice shift
-   * (trees that reach the last levels) or, up to 262,144 points, when the lists exceed its 512 pairs
-   * per body */
+   * tree, same lists; cross-check).  The device builder has no list-size limit of its own: its pair lists grow
+   * until they fit (60 % of the free device memory, 31 / 32-bit pair indexing) and lattice shifts beyond its
+   * packed sort keys are classified on the host.  Only when the lists themselves exceed the device — a gate
+   * that forbids every coarse translation — does set_points switch to the host builder by itself, and only up
+   * to 262,144 points (hfmm_cuda_stats::host_tree_used says so; HFMM_FLAG_NO_HOST_FALLBACK forbids it) */
   HFMM_FLAG_HOST_TREE = 1 << 0,
   /* time each phase with CUDA events (fills hfmm_cuda_stats seconds); costs a few syncs */
   HFMM_FLAG_PHASE_TIMERS = 1 << 1,

@@ -20,8 +20,8 @@ struct Error : std::runtime_error {
   Error(int s, const std::string& msg) : std::runtime_error(msg), status(s) {}
 };
 
-// a size limit of the DEVICE tree / list builder (packed 64-bit sort keys): Engine::set_points falls
-// back to the host builder, which has none
+// the pair lists of the DEVICE builder exceed the device memory / 32-bit pair indexing: Engine::set_points falls
+// back to the host builder for moderate sizes (or reports it: HFMM_FLAG_NO_HOST_FALLBACK)
 struct DeviceBuilderLimit : Error {
   // any_size: the host builder handles the input at the usual cost (O(N)); otherwise the lists
   // themselves are huge and the fallback is taken for moderate point counts only

@@ -779,14 +779,11 @@ void Engine::set_points(const double* xyz, size_t n) {
       set_points_device(xyz, n);
     } catch (const DeviceBuilderLimit& lim) {
       if (cfg_.flags & HFMM_FLAG_NO_HOST_FALLBACK) throw;  // the caller asked for the device builder or nothing
-      // ... and lists beyond the device traversal's capacity (a gate that forbids every coarse
-      // translation) are left to it for moderate sizes only: at a million points that configuration
-      // is a mistake to report, not hours of host work to start
+      // lists beyond the device memory / 32-bit pair indexing (a gate that forbids every coarse translation)
+      // are left to the host builder for moderate sizes only: at a million points that configuration is a
+      // mistake to report, not hours of host work to start
       if (!lim.any_size && n > kHostFallbackBodies) throw;
       host_lists_ = true;
-      // very deep trees (clusters of coincident points driving the octree to its last levels) have
-      // shifts the device builder's packed sort keys cannot hold: the host builder produces the same
-      // tree and lists without that limit (setup only; the matvec is unaffected)
       dev_pairs_ = DevicePairs{};
       pairs_ = PairLists{};
       m2l_ = TranslateStage{};
@@ -904,7 +901,7 @@ void Engine::set_points_device(const double* xyz, size_t n) {
   owned_m2l_pairs_ = 0;
   if (have_far_) {
     FarClasses fc;
-    build_far_classes_device(dev_pairs_, cells, owned_, t.max_level, m2l_.pair_src, m2l_.pair_dst, fc, stream_);
+    build_far_classes_device(dev_pairs_, t, cells, owned_, m2l_.pair_src, m2l_.pair_dst, fc, stream_);
     mark("far classes (sort)");
     build_m2l_stage_device(reg, fc);
     mark("M2L stage (classes, batches)");

@@ -4,6 +4,10 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <climits>
+#include <cstdlib>
+#include <tuple>
 #include <cmath>
 
 #include "common.hpp"
@@ -214,11 +218,11 @@ traversal_kernel(const uint2* __restrict__ frontier, unsigned long long n_front,
   } else {
     if (n_far) {
       if (s_far < far.cap) far.data[s_far] = make_uint2(a, b);
-      else *overflow = 1;
+      else atomicOr(overflow, 1);
     }
     if (n_near) {
       if (s_near < near.cap) near.data[s_near] = make_uint2(a, b);
-      else *overflow = 1;
+      else atomicOr(overflow, 2);
     }
   }
   if (n_next) {
@@ -235,7 +239,7 @@ traversal_kernel(const uint2* __restrict__ frontier, unsigned long long n_front,
       }
       if (opened) atomicAdd(tasks, (unsigned long long)opened);
     } else {
-      *overflow = 1;
+      atomicOr(overflow, 4);
     }
   }
 }
@@ -360,7 +364,7 @@ __global__ void __launch_bounds__(kBlock)
 far_keys_kernel(const uint2* __restrict__ far, unsigned long long n, const uint8_t* __restrict__ lvl,
                 const uint32_t* __restrict__ ix, const uint32_t* __restrict__ iy,
                 const uint32_t* __restrict__ iz, const uint8_t* __restrict__ owned,
-                uint64_t* __restrict__ keys, uint64_t* __restrict__ vals, int* __restrict__ flags) {
+                uint64_t* __restrict__ keys, uint64_t* __restrict__ vals, long long limit) {
   const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint2 p = far[i];
@@ -370,9 +374,14 @@ far_keys_kernel(const uint2* __restrict__ far, unsigned long long n, const uint8
     auto c = [lmax](uint32_t v, int l) { return (long long)(2ull * v + 1) << (lmax - l); };
     const long long dx = c(ix[p.x], la) - c(ix[p.y], lb), dy = c(iy[p.x], la) - c(iy[p.y], lb),
                     dz = c(iz[p.x], la) - c(iz[p.y], lb);
-    if (llabs(dx) >= kShiftBias || llabs(dy) >= kShiftBias || llabs(dz) >= kShiftBias) *flags = 1;
-    key = uint64_t(la) << 59 | uint64_t(lb) << 54 | uint64_t(dx + kShiftBias) << 36 |
-          uint64_t(dy + kShiftBias) << 18 | uint64_t(dz + kShiftBias);
+    // a shift beyond the packed range (a deep leaf translated straight from / to a coarse cell: level gaps of
+    // fifteen and more) keeps its pair index instead: such pairs sort behind the packed keys, ahead of the
+    // unowned ones, and the host groups the few of them into classes (build_far_classes_device)
+    if (llabs(dx) >= limit || llabs(dy) >= limit || llabs(dz) >= limit)
+      key = uint64_t(1) << 63 | uint64_t(i);
+    else
+      key = uint64_t(la) << 59 | uint64_t(lb) << 54 | uint64_t(dx + kShiftBias) << 36 |
+            uint64_t(dy + kShiftBias) << 18 | uint64_t(dz + kShiftBias);
   }
   keys[i] = key;
   vals[i] = uint64_t(p.x) << 32 | p.y;
@@ -569,7 +578,16 @@ void run_traversal(const TreeArrays& t, const DeviceCells& cells, double kmag, d
     cell_work.resize(2 * t.n_cells());
     level_min.resize(1);
   }
-  for (int attempt = 0; attempt < 6; ++attempt) {
+  // A list that does not fit is doubled and the walk repeated, as long as the lists (8 bytes per pair, two
+  // frontiers) stay within 60 % of the device memory that is free now and within the 31 / 32-bit indexing of the
+  // list builders; only then is the configuration given up (a gate that forbids every coarse translation at a
+  // size whose all-pairs lists no memory holds — the reference would walk them for hours).
+  size_t free_b = 0, total_b = 0;
+  HFMM_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+  uint64_t budget = uint64_t(0.6 * double(free_b)) + 8 * (out.far.size() + out.near.size());
+  if (const char* e = getenv("HFMM_DEBUG_LIST_BUDGET_MB"))  // tests: reach the limit without filling the device
+    if (atoll(e) > 0) budget = std::min<uint64_t>(budget, uint64_t(atoll(e)) << 20);
+  for (;;) {
     if (!census) {
       out.far.resize(cap_far);
       out.near.resize(cap_near);
@@ -637,16 +655,22 @@ void run_traversal(const TreeArrays& t, const DeviceCells& cells, double kmag, d
       }
       return;
     }
-    cap_far *= 2;
-    cap_near *= 2;
-    cap_front *= 2;
+    if (ovf & 1) cap_far *= 2;
+    if (ovf & 2) cap_near *= 2;
+    if (ovf & 4) cap_front *= 2;
+    const uint64_t need = 8 * ((census ? 0 : cap_far + cap_near) + 2 * cap_front);
+    if (getenv("HFMM_SETUP_TRACE"))
+      fprintf(stderr, "[hfmm setup] traversal lists grown: far %llu near %llu front %llu (need %llu MB, budget %llu MB)\n",
+              (unsigned long long)cap_far, (unsigned long long)cap_near, (unsigned long long)cap_front,
+              (unsigned long long)(need >> 20), (unsigned long long)(budget >> 20));
+    if (need > budget || cap_far > (uint64_t(1) << 31) || cap_near > (uint64_t(1) << 32))
+      // the kd_max gate forbids every coarse translation (k x box >> kd_max) and the lists degenerate towards all
+      // pairs of finest-level cells, as they do in the reference
+      throw DeviceBuilderLimit(HFMM_ERR_STRUCTURAL,
+                               "dual tree traversal: the interaction lists exceed the device memory / 32-bit indexing "
+                               "(kd_max too small for this wavenumber and domain?)",
+                               false);
   }
-  // more than ~500 pairs per body: the kd_max gate forbids every coarse translation (k x box >> kd_max)
-  // and the lists degenerate towards all pairs of finest-level cells, as they do in the reference
-  throw DeviceBuilderLimit(HFMM_ERR_STRUCTURAL,
-                           "dual tree traversal: interaction lists exceed 512 pairs per body (kd_max too small for "
-                           "this wavenumber and domain?)",
-                           false);
 }
 }  // namespace
 
@@ -749,11 +773,10 @@ void build_near_lists_device(const DevicePairs& p, const TreeArrays& t, const De
   out.work.assign(hw.begin(), hw.end());
 }
 
-void build_far_classes_device(const DevicePairs& p, const DeviceCells& cells,
-                              const std::vector<uint8_t>& owned, int max_level,
+void build_far_classes_device(const DevicePairs& p, const TreeArrays& t, const DeviceCells& cells,
+                              const std::vector<uint8_t>& owned,
                               DeviceBuffer<uint32_t>& pair_src, DeviceBuffer<uint32_t>& pair_dst,
                               FarClasses& out, cudaStream_t s) {
-  (void)max_level;
   out = FarClasses{};
   if (p.n_far == 0) return;
   if (p.n_far >= (uint64_t(1) << 31)) throw Error(HFMM_ERR_CONFIG, "M2L pair count exceeds 31-bit indexing");
@@ -761,11 +784,13 @@ void build_far_classes_device(const DevicePairs& p, const DeviceCells& cells,
   DeviceBuffer<uint8_t> d_owned;
   d_owned.upload(owned, s);
   DeviceBuffer<uint64_t> k_in(n), k_out(n), v_in(n), v_out(n);
-  DeviceBuffer<int> flag(1);
-  flag.zero(s);
+  // HFMM_DEBUG_SHIFT_LIMIT (tests): shifts from this size on take the unpacked path although they would fit
+  const char* dbg = getenv("HFMM_DEBUG_SHIFT_LIMIT");
+  const long long dbg_limit = dbg ? atoll(dbg) : 0;
+  const long long limit = dbg_limit > 0 && dbg_limit < kShiftBias ? dbg_limit : (long long)kShiftBias;
   far_keys_kernel<<<grid_for(n), kBlock, 0, s>>>(p.far.get(), p.n_far, cells.level.get(), cells.ix.get(),
                                                  cells.iy.get(), cells.iz.get(), d_owned.get(), k_in.get(),
-                                                 v_in.get(), flag.get());
+                                                 v_in.get(), limit);
   HFMM_CUDA_CHECK(cudaGetLastError());
   TempStorage tmp;
   size_t bytes = 0;
@@ -779,21 +804,21 @@ void build_far_classes_device(const DevicePairs& p, const DeviceCells& cells,
   cub::DeviceRunLengthEncode::Encode(nullptr, bytes, k_out.get(), uniq.get(), counts.get(), nruns.get(), n, s);
   HFMM_CUDA_CHECK(cub::DeviceRunLengthEncode::Encode(tmp.get(bytes), bytes, k_out.get(), uniq.get(),
                                                      counts.get(), nruns.get(), n, s));
-  int h_flag = 0, h_runs = 0;
-  flag.download(&h_flag, 1, s);
+  int h_runs = 0;
   nruns.download(&h_runs, 1, s);
   HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
-  if (h_flag)
-    throw DeviceBuilderLimit(HFMM_ERR_INTERNAL,
-                             "an M2L lattice shift exceeds the packed key range; rebuild with HFMM_FLAG_HOST_TREE",
-                             true);
   std::vector<uint64_t> hk(h_runs);
   std::vector<int> hc(h_runs);
   uniq.download(hk.data(), h_runs, s);
   counts.download(hc.data(), h_runs, s);
   HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
+  uint64_t n_unpacked = 0;
   for (int r = 0; r < h_runs; ++r) {
     if (hk[r] == ~uint64_t(0)) continue;  // pairs of targets other ranks own
+    if (hk[r] >> 63) {                    // shift beyond the packed range: one run per pair, grouped below
+      n_unpacked += uint64_t(hc[r]);
+      continue;
+    }
     out.lt.push_back(int16_t(hk[r] >> 59));
     out.ls.push_back(int16_t((hk[r] >> 54) & 31));
     out.dx.push_back(int32_t((hk[r] >> 36) & 0x3ffff) - kShiftBias);
@@ -801,6 +826,49 @@ void build_far_classes_device(const DevicePairs& p, const DeviceCells& cells,
     out.dz.push_back(int32_t(hk[r] & 0x3ffff) - kShiftBias);
     out.count.push_back(uint32_t(hc[r]));
     out.n_owned_pairs += uint64_t(hc[r]);
+  }
+  if (n_unpacked) {
+    // the unpacked pairs sit at positions [n_owned_pairs, n_owned_pairs + n_unpacked) of the sorted payloads, in
+    // pair-index order: classify them on the host with the kernel's own arithmetic, sort them by class and put
+    // them back, so that every class is again one contiguous range of the pair arrays
+    std::vector<uint64_t> pay(n_unpacked);
+    HFMM_CUDA_CHECK(cudaMemcpyAsync(pay.data(), v_out.get() + out.n_owned_pairs, n_unpacked * sizeof(uint64_t),
+                                    cudaMemcpyDeviceToHost, s));
+    HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
+    struct Unpacked {
+      int16_t lt, ls;
+      int64_t dx, dy, dz;
+      uint64_t pay;
+    };
+    std::vector<Unpacked> u(n_unpacked);
+    for (uint64_t i = 0; i < n_unpacked; ++i) {
+      const uint32_t a = uint32_t(pay[i] >> 32), b = uint32_t(pay[i]);
+      const int la = t.level[a], lb = t.level[b], lmax = std::max(la, lb);
+      auto c = [lmax](uint32_t v, int l) { return int64_t(2ull * v + 1) << (lmax - l); };
+      u[i] = {int16_t(la), int16_t(lb), c(t.ix[a], la) - c(t.ix[b], lb), c(t.iy[a], la) - c(t.iy[b], lb),
+              c(t.iz[a], la) - c(t.iz[b], lb), pay[i]};
+      if (std::llabs(u[i].dx) > INT32_MAX || std::llabs(u[i].dy) > INT32_MAX || std::llabs(u[i].dz) > INT32_MAX)
+        throw Error(HFMM_ERR_INTERNAL, "M2L lattice shift beyond 32 bits");  // needs a level gap of 30: kMaxLevel is 21
+    }
+    auto cls = [](const Unpacked& x) { return std::make_tuple(x.lt, x.ls, x.dx, x.dy, x.dz); };
+    std::stable_sort(u.begin(), u.end(), [&](const Unpacked& x, const Unpacked& y) { return cls(x) < cls(y); });
+    for (uint64_t i = 0; i < n_unpacked; ++i) {
+      pay[i] = u[i].pay;
+      if (i && cls(u[i]) == cls(u[i - 1])) {
+        ++out.count.back();
+      } else {
+        out.lt.push_back(u[i].lt);
+        out.ls.push_back(u[i].ls);
+        out.dx.push_back(int32_t(u[i].dx));
+        out.dy.push_back(int32_t(u[i].dy));
+        out.dz.push_back(int32_t(u[i].dz));
+        out.count.push_back(1);
+      }
+    }
+    HFMM_CUDA_CHECK(cudaMemcpyAsync(v_out.get() + out.n_owned_pairs, pay.data(), n_unpacked * sizeof(uint64_t),
+                                    cudaMemcpyHostToDevice, s));
+    HFMM_CUDA_CHECK(cudaStreamSynchronize(s));
+    out.n_owned_pairs += n_unpacked;
   }
   const uint32_t no = uint32_t(out.n_owned_pairs);
   pair_src.resize(std::max<uint32_t>(no, 1));

@@ -96,8 +96,8 @@ struct FarClasses {
   uint64_t n_owned_pairs = 0;
 };
 // pairs sorted by shift class: pair_src / pair_dst hold the owned pairs class by class
-void build_far_classes_device(const DevicePairs& p, const DeviceCells& cells,
-                              const std::vector<uint8_t>& owned, int max_level,
+void build_far_classes_device(const DevicePairs& p, const TreeArrays& tree, const DeviceCells& cells,
+                              const std::vector<uint8_t>& owned,
                               DeviceBuffer<uint32_t>& pair_src, DeviceBuffer<uint32_t>& pair_dst,
                               FarClasses& out, cudaStream_t s);
 

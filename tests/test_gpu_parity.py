@@ -636,21 +636,65 @@ def test_deep_tree_of_coincident_points(oracle):
     assert rel_l2(host.matvec(q), y) < 2e-6
 
 
-def test_device_builder_limit_is_reported_not_hidden():
-    """HFMM_FLAG_NO_HOST_FALLBACK: when the device builder meets a limit (here: a gate that forbids every
-    translation, lists beyond 512 pairs per body) set_points fails with the builder's status instead of switching
-    to the host builder; without the flag the switch shows in hfmm_cuda_stats::host_tree_used"""
+def test_device_builder_limit_is_reported_not_hidden(oracle):
+    """The device builder's lists grow until they fit (60 % of the free device memory, 32-bit indexing).  A gate that
+    forbids every translation turns the near lists into all pairs of leaves: the device builder takes them as long as
+    they fit.  Beyond that (here: a 256 MB budget set for the test), HFMM_FLAG_NO_HOST_FALLBACK makes set_points fail
+    with the builder's status instead of switching to the host builder; without the flag the switch shows in
+    hfmm_cuda_stats::host_tree_used"""
+    import os
+
     from paper_1803_09948_b200.api import HFMM_FLAG_NO_HOST_FALLBACK
     xyz = sphere_points(24000, 3)
-    strict = HfmmCuda(k=50.0, order=4, ncrit=1, kd_max=1e-9, leaf_cap=0.0, flags=HFMM_FLAG_NO_HOST_FALLBACK)
-    with pytest.raises(HfmmError) as e:
-        strict.set_points(xyz)
-    assert e.value.kind == "structural_error" and "512 pairs per body" in str(e.value)
-    strict.set_points(sphere_points(2000, 3))      # the handle stays usable, and says which builder ran
-    assert strict.stats()["host_tree_used"] == 0 and strict.stats()["p2p_pairs"] == 2000 * 2000
-    loose = HfmmCuda(k=50.0, order=4, ncrit=1, kd_max=1e-9, leaf_cap=0.0)
-    loose.set_points(xyz[:7000])                    # 49 M leaf pairs: beyond the device lists, within the host's reach
-    assert loose.stats()["host_tree_used"] == 1 and loose.stats()["p2p_pairs"] == 7000 * 7000
+    kw = dict(k=50.0, order=4, ncrit=1, kd_max=1e-9, leaf_cap=0.0)
+    dev = HfmmCuda(flags=HFMM_FLAG_NO_HOST_FALLBACK, **kw)
+    dev.set_points(xyz[:7000])                      # 49 M leaf pairs, 96 x the initial list capacity: still the device builder
+    st = dev.stats()
+    assert st["host_tree_used"] == 0 and st["p2p_pairs"] == 7000 * 7000 and st["m2l_pairs"] == 0
+    q = charges(7000, 3)
+    sample = np.arange(0, 7000, 7)
+    assert rel_l2(dev.matvec(q)[sample], oracle.direct_sum(xyz[:7000], q, 50.0, targets=sample)) < 5e-6
+    del dev
+    os.environ["HFMM_DEBUG_LIST_BUDGET_MB"] = "256"
+    try:
+        strict = HfmmCuda(flags=HFMM_FLAG_NO_HOST_FALLBACK, **kw)
+        with pytest.raises(HfmmError) as e:
+            strict.set_points(xyz)
+        assert e.value.kind == "structural_error" and "interaction lists exceed" in str(e.value)
+        strict.set_points(sphere_points(2000, 3))      # the handle stays usable, and says which builder ran
+        assert strict.stats()["host_tree_used"] == 0 and strict.stats()["p2p_pairs"] == 2000 * 2000
+        loose = HfmmCuda(**kw)
+        loose.set_points(xyz[:7000])                    # beyond the (test) budget of the device lists, within the host's reach
+        assert loose.stats()["host_tree_used"] == 1 and loose.stats()["p2p_pairs"] == 7000 * 7000
+    finally:
+        del os.environ["HFMM_DEBUG_LIST_BUDGET_MB"]
+
+
+def test_m2l_shifts_beyond_the_packed_key_range(oracle):
+    """A lattice shift that does not fit the 18-bit fields of the device builder's sort key (a deep leaf translated
+    straight from a coarse cell) keeps its pair index as key and is grouped into classes on the host.  The path is
+    forced on an ordinary input by lowering the limit: same classes, same pairs, same potentials."""
+    import os
+
+    n, k = 12000, 3.0
+    xyz, q = plummer_points(n, 31, a=0.05), charges(n, 31)
+    ref = HfmmCuda(k=k, order=8, theta=0.4)
+    ref.set_points(xyz)
+    y_ref, st_ref = ref.matvec(q), ref.stats()
+    os.environ["HFMM_DEBUG_SHIFT_LIMIT"] = "6"         # most shifts now take the unpacked path
+    try:
+        op = HfmmCuda(k=k, order=8, theta=0.4)
+        op.set_points(xyz)
+    finally:
+        del os.environ["HFMM_DEBUG_SHIFT_LIMIT"]
+    st = op.stats()
+    assert st["host_tree_used"] == 0
+    for key in ("m2l_pairs", "p2p_pairs", "m2l_shift_classes", "rotation_tables", "coaxial_tables"):
+        assert st[key] == st_ref[key], key
+    y = op.matvec(q)
+    assert rel_l2(y, y_ref) < 2e-6
+    sample = np.arange(0, n, 6)
+    assert rel_l2(y[sample], oracle.direct_sum(xyz, q, k, targets=sample)) < 1e-5
 
 
 def test_partition_of_a_clustered_set_without_leaf_cap():
