@@ -47,8 +47,9 @@ enum {
   HFMM_FLAG_HOST_TREE = 1 << 0,
   /* time each phase with CUDA events (fills hfmm_cuda_stats seconds); costs a few syncs */
   HFMM_FLAG_PHASE_TIMERS = 1 << 1,
-  /* enqueue the near field before the far field.  Default: behind the persistent M2L launch, so one
-   * near-field CTA runs beside the two M2L CTAs of every SM (MUFU-bound next to shared-memory-bound) */
+  /* enqueue the near field before the far field.  Default: behind the persistent M2L launch, so that the M2L
+   * CTAs own their SMs first and the near field takes what they leave (three near-field CTAs beside the one
+   * sixteen-warp M2L CTA of orders 13..16; at orders <= 12 the gaps and the tail) */
   HFMM_FLAG_NEAR_FIRST = 1 << 2,
   /* run-to-run reproducible results (TraversalConfig::deterministic, traversal.hpp:11-22: per-target
    * ordered accumulation).  M2M and M2L stage one row per cell pair and add the rows of every
