@@ -202,7 +202,8 @@ def kernel_roofline(cfg, n: int, steps: int, fp32_peak: float):
                     "tflops_executed": m2l_tf, "frac_of_fp32_peak": m2l_tf / fp32_peak if fp32_peak else None,
                     "dense_equivalent_tflops": st["m2l_pairs"] * dense / acc["m2l"] * 1e-12 if acc["m2l"] else None},
             "p2p": {"ms": acc["p2p"] * 1e3, "body_pairs": st["p2p_body_pairs"], "tflops_24flop_per_pair": p2p_tf,
-                    "frac_of_fp32_peak": p2p_tf / fp32_peak if fp32_peak else None, "kernel_variant": st["p2p_mode"]}}
+                    "frac_of_fp32_peak": p2p_tf / fp32_peak if fp32_peak else None, "kernel_variant": st["p2p_mode"],
+                    "kernel_variant_in_step": st["p2p_mode_in_step"]}}
 
 
 def run_single(args, cfg):
@@ -355,6 +356,7 @@ def run_single(args, cfg):
             "p2p": {"ms": alone["p2p"] * 1e3, "ms_in_step": kern["p2p"] * 1e3, "tflops_24flop_per_pair": p2p_tf,
                     "frac_of_fp32_peak": p2p_tf / fp32_peak if fp32_peak else None,
                     "body_pairs": st0["p2p_body_pairs"], "kernel_variant": st0["p2p_mode"],
+                    "kernel_variant_in_step": st0["p2p_mode_in_step"],
                     "near_r2_max": st0["near_r2_max"]},
             "m2l": {"ms": alone["m2l"] * 1e3, "ms_in_step": kern["m2l"] * 1e3, "tflops_executed": m2l_tf_alone,
                     "pairs": st0["m2l_pairs"]},

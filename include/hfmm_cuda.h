@@ -101,6 +101,9 @@ typedef struct {
   double near_r2_max;          /* bound on (k_r |x_i - x_j|)^2 over the near lists (selects p2p_mode)  */
   uint64_t tasks;              /* FmmStats::tasks: walk nodes where the body count first drops to the grain s
                                   (traversal.cpp:56-59)                                                 */
+  uint64_t p2p_mode_in_step;   /* the variant the near field runs with INSIDE a matvec, beside the far field:
+                                  0 when the far field outweighs it (the three-MUFU variant leaves the FMA pipe
+                                  to M2L), else p2p_mode                                                    */
 } hfmm_cuda_stats;
 
 typedef struct hfmm_cuda hfmm_cuda_t;

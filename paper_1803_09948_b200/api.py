@@ -46,7 +46,7 @@ class Stats(C.Structure):
                  "l2p_seconds", "matvec_seconds")] + \
                [("kernel_launches", C.c_uint64), ("device_bytes", C.c_uint64), ("m2l_batches", C.c_uint64),
                 ("host_tree_used", C.c_uint64), ("p2p_mode", C.c_uint64), ("near_r2_max", C.c_double),
-                ("tasks", C.c_uint64)]
+                ("tasks", C.c_uint64), ("p2p_mode_in_step", C.c_uint64)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

@@ -640,6 +640,24 @@ void Engine::select_near_kernel(uint64_t max_r2_lattice) {
   fit_p2p_polynomials(std::max(near_r2_max_, 1e-3), p2p_sinc_, p2p_cos_);
 }
 
+// The variant of the near-field launch that shares the machine with M2L.  On its own the bounded-range variant
+// (sinc as a polynomial: 18 packed FMA-pipe instructions and two MUFU per pair of pairs) is the faster one; beside
+// M2L, which lives on the FMA pipe and leaves the MUFU pipe idle, the general variant (12 + three MUFU) costs the
+// step less: cfg 2 13.95 -> 13.68 ms, cfg 5's per-GPU share 73.1 -> 71.9 ms, nothing at cfg 4, +3 % at cfg 1 where
+// the far field is as short as the near field — hence only when the far field clearly outweighs the near field
+// (estimated kernel times: executed flops at 21 TFLOP/s against 1.0e12 body pairs per second).
+int Engine::near_mode_in_step() const {
+  if (getenv("HFMM_P2P_MODE") || p2p_mode_ != P2P_MODE_SINC_POLY || !have_far_) return p2p_mode_;
+  const int P = cfg_.order;
+  double rot = 0, coax = 0;
+  for (int j = 0; j <= P; ++j) rot += double(j + 1) * (j + 1) + double(j) * j;
+  for (int m = -P; m <= P; ++m) coax += double(P + 1 - std::abs(m)) * (P + 1 - std::abs(m));
+  const double t_far = double(owned_m2l_pairs_) * 2.0 * (4.0 * rot + 4.0 * coax) / 21e12;
+  const double t_near = double(owned_body_pairs_) / 1.0e12;
+  // below half a millisecond of near field the estimates mean nothing (launch latency and tails: cfg 1)
+  return t_near > 0.5e-3 && t_far > 2.0 * t_near ? int(P2P_MODE_MUFU) : p2p_mode_;
+}
+
 // tiles of <= 32 targets per owned leaf, longest first (the tail of the launch fills with short ones)
 void Engine::build_tiles(const std::vector<uint64_t>& work) {
   const TreeArrays& t = tree_;
@@ -806,6 +824,7 @@ void Engine::set_points(const double* xyz, size_t n) {
   stats_.setup_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   stats_.device_bytes = device_bytes_counter();
+  p2p_mode_late_ = near_mode_in_step();
   have_points_ = true;
 }
 
@@ -1154,7 +1173,9 @@ void Engine::phase_downward() {
     if (p2p_late_) {  // enqueued behind the persistent M2L launch: its CTAs fill what M2L leaves free
       if (near_gate_) HFMM_CUDA_CHECK(cudaStreamWaitEvent(stream_near_, near_gate_, 0));
       HFMM_CUDA_CHECK(cudaEventRecord(ev_[0], stream_near_));
-      launch_p2p(p2p_args_, stream_near_);
+      P2PArgs late = p2p_args_;
+      late.mode = p2p_mode_late_;  // beside M2L: the variant that leaves it the FMA pipe (near_mode_in_step)
+      launch_p2p(late, stream_near_);
       ++launches;
       HFMM_CUDA_CHECK(cudaEventRecord(ev_[1], stream_near_));
     }
@@ -1294,6 +1315,7 @@ void Engine::get_stats(hfmm_cuda_stats* out) {
   stats_.m2l_batches = m2l_.n_items;
   stats_.host_tree_used = host_lists_ ? 1 : 0;
   stats_.p2p_mode = uint64_t(p2p_mode_);
+  stats_.p2p_mode_in_step = uint64_t(p2p_mode_late_);
   stats_.near_r2_max = near_r2_max_;
   *out = stats_;
 }

@@ -177,7 +177,9 @@ class Engine {
   DeviceBuffer<P2PTile> p2p_tiles_;
   DeviceBuffer<uint32_t> p2p_offset_, p2p_split_, p2p_src_;
   uint32_t n_tiles_ = 0;
-  int p2p_mode_ = 0;           // P2P_MODE_*
+  int p2p_mode_ = 0;           // P2P_MODE_*: the fastest variant for the near field on its own
+  int p2p_mode_late_ = 0;      // the variant of the launch that runs beside M2L (near_mode_in_step)
+  int near_mode_in_step() const;
   double near_r2_max_ = 0;     // bound on R'^2 over the owned near lists
   float p2p_sinc_[8] = {}, p2p_cos_[8] = {};
   float kunit_ = 0;

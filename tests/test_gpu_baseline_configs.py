@@ -59,6 +59,7 @@ def test_config_2_full_size(oracle):
     # points; ours are seeded differently, the structure is the same): depth 7, ~70 k cells, ~10 M M2L pairs
     assert st["max_level"] == 7 and 6e4 < st["n_cells"] < 8e4 and 9e6 < st["m2l_pairs"] < 1.2e7
     assert st["host_tree_used"] == 0 and st["p2p_mode"] == 1     # device builder, bounded near-field kernel
+    assert st["p2p_mode_in_step"] == 0    # beside a far field five times as long: the variant that leaves M2L the FMA pipe
     y = op.matvec(q)
     assert _sampled_error(oracle, xyz, q, cfg.k, y) < TOL       # measured 3.8e-7
     # linearity (reference tests/test_fmm.cpp:985-1022) at full size: A(a q1 + b q2) = a A q1 + b A q2
