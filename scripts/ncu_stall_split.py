@@ -28,9 +28,8 @@ if len(sys.argv) > 2:
 best = max(secs, key=lambda s: sum(int(x[s["hdr"].index("Instructions Executed")]) for x in s["rows"]))
 h = best["hdr"]
 ie, so, ss = h.index("Instructions Executed"), h.index("Source"), h.index("# Samples")
-stall_cols = [(i, c) for i, c in enumerate(h) if c.lower().startswith("stall_") or c.lower().startswith("warp stall")]
-if not stall_cols:
-    stall_cols = [(i, c) for i, c in enumerate(h) if "stall" in c.lower()]
+# one column per stall reason ("stall_wait", ...); the "(Not Issued)" twins and the two totals are left out
+stall_cols = [(i, c) for i, c in enumerate(h) if c.startswith("stall_") and "Not" not in c]
 print(best["name"][:100])
 print("columns:", [c for _, c in stall_cols][:40])
 
